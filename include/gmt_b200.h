@@ -1,0 +1,263 @@
+/*
+ * gmt_b200.h -- C ABI of the B200-native Group Marching Tree (GMT*) planner.
+ *
+ * This is the drop-in boundary for the reference library `gmtplan`
+ * (/root/reference/proj).  The reference exposes no FFI of its own: its
+ * boundary is the set of free functions in `namespace gmt` that the CLI,
+ * the simulator and the tests call.  Every entry point
+ * below names the reference function it replaces (file:line, paths relative
+ * to /root/reference/proj).  The header-only C++ shim `gmt_b200.hpp`
+ * re-creates those exact `gmt::` signatures on top of this ABI.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Host pointers unless a name says `dev`.
+ *   - Every function returns an int error code (gmt_error); 0 is success.
+ *     The reference throws exceptions; the ABI maps each exception type to a
+ *     code and stores the message in a thread-local string (gmt_last_error).
+ *   - Planning outcomes are values (gmt_plan_status), never errors, exactly
+ *     like the reference (planner.hpp:14).
+ *   - Nothing is retained between calls except explicit handles.
+ *   - There is no CPU fallback: every compute call runs CUDA kernels on the
+ *     context's device and fails with GMT_E_NO_DEVICE when there is none.
+ */
+#ifndef GMT_B200_H
+#define GMT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GMT_B200_ABI_VERSION 1
+
+/* Error codes.  Reference exception types: errors.hpp:9-21. */
+typedef enum gmt_error {
+  GMT_OK = 0,
+  GMT_E_INVALID_INPUT = 1,        /* gmt::InvalidInputError        (errors.hpp:9-11)  */
+  GMT_E_INFEASIBLE_SAMPLING = 2,  /* gmt::InfeasibleSamplingError  (errors.hpp:14-16) */
+  GMT_E_GOAL_BLOCKED = 3,         /* gmt::GoalBlockedError         (errors.hpp:19-21) */
+  GMT_E_CUDA = 4,                 /* CUDA runtime failure (no reference analogue)     */
+  GMT_E_NO_DEVICE = 5,            /* no usable sm_100 device: the ABI never falls back */
+  GMT_E_INTERNAL = 6
+} gmt_error;
+
+/* PlanStatus, same order as planner.hpp:14. */
+typedef enum gmt_plan_status {
+  GMT_PLAN_SUCCESS = 0,
+  GMT_PLAN_FAILURE_OPEN_EMPTY = 1,
+  GMT_PLAN_INFEASIBLE_INPUT = 2
+} gmt_plan_status;
+
+/* NodeLabel, same values as planner.hpp:16. */
+typedef enum gmt_label {
+  GMT_LABEL_UNEXPLORED = 0,
+  GMT_LABEL_OPEN = 1,
+  GMT_LABEL_CLOSED = 2
+} gmt_label;
+
+/* SampleSource::Kind (sampling.hpp:21). */
+typedef enum gmt_sample_kind { GMT_SAMPLE_HALTON = 0, GMT_SAMPLE_UNIFORM = 1 } gmt_sample_kind;
+
+/* ObstacleSet + GoalRegion (space.hpp:19-41), structure-of-arrays.
+ *   box_lo[b*dim + k], box_hi[b*dim + k]   closed boxes, lo <= hi
+ *   goal_lo[k], goal_hi[k]                  closed goal box            */
+typedef struct gmt_scene {
+  int32_t dim;
+  int32_t num_boxes;
+  const double* box_lo;
+  const double* box_hi;
+  const double* goal_lo;
+  const double* goal_hi;
+} gmt_scene;
+
+/* SampleSource (sampling.hpp:20-29). */
+typedef struct gmt_sample_source {
+  int32_t kind;          /* gmt_sample_kind */
+  int32_t with_heading;  /* Dubins headings (halton prime d+1 / extra uniform draw) */
+  uint64_t start_index;  /* halton: first 1-based index */
+  uint64_t seed;         /* uniform: Pcg32 seed */
+} gmt_sample_source;
+
+/* NeighborGraph (graph.hpp:31-54) as compressed rows.
+ *   out row u: out_col[out_ptr[u] .. out_ptr[u+1]) targets, sorted ascending
+ *   in  row x: in_col[in_ptr[x] .. in_ptr[x+1])   sources (list order is the
+ *              reference's in-list order; ties in connect_candidate go to
+ *              the earliest entry, planner.cpp:70-82)
+ *   *_path: path id of the edge (graph.hpp:35) or -1 for exact straight
+ *           edges; the whole array may be NULL (all exact).  in_path[e] must
+ *           be the id that NeighborGraph::edge_path(source, x) returns
+ *           (graph.cpp:34-40), i.e. the out-list's id.
+ *   paths:  path p = path_pts[path_ptr[p]*dim .. path_ptr[p+1]*dim)
+ * directed == 0 declares in == out (Euclidean graphs, graph.cpp:184-186);
+ * the in_* pointers are then ignored.                                      */
+typedef struct gmt_graph_view {
+  int32_t n;
+  int32_t dim;
+  double radius;
+  int32_t directed;
+  int32_t reserved;
+  const int64_t* out_ptr;
+  const int32_t* out_col;
+  const double* out_cost;
+  const int32_t* out_path;
+  const int64_t* in_ptr;
+  const int32_t* in_col;
+  const double* in_cost;
+  const int32_t* in_path;
+  int64_t num_paths;
+  const int64_t* path_ptr;
+  const double* path_pts;
+} gmt_graph_view;
+
+/* PlanResult (planner.hpp:43-51).  Scalars are always written.  Array
+ * outputs are caller-owned and optional (NULL skips them):
+ *   path            capacity n        (path_len entries, root..goal)
+ *   label/tree_cost/parent/iteration_added   capacity n (tree_size entries;
+ *                   tree_size is 0 for infeasible input, planner.cpp:108)
+ *   group_sizes/nodes_added/collision_checks capacity stats_cap >= n + 1
+ *                   (num_stats entries, IterationStats planner.hpp:36-40)  */
+typedef struct gmt_plan_out {
+  int32_t status; /* gmt_plan_status */
+  int32_t goal_node;
+  double cost;
+  int64_t iterations;
+  int64_t total_collision_checks;
+  int32_t path_len;
+  int32_t num_stats;
+  int32_t tree_size;
+  int32_t stats_cap;
+  int32_t* path;
+  uint8_t* label;
+  double* tree_cost;
+  int32_t* parent;
+  int64_t* iteration_added;
+  int32_t* group_sizes;
+  int32_t* nodes_added;
+  int64_t* collision_checks;
+} gmt_plan_out;
+
+/* Per-query summary record gathered after a batched solve. */
+typedef struct gmt_plan_summary {
+  int32_t status;
+  int32_t goal_node;
+  double cost;
+  int64_t iterations;
+  int64_t total_collision_checks;
+  int32_t path_len;
+  int32_t num_stats;
+} gmt_plan_summary;
+
+/* ProblemFile (problem.hpp:17-29) minus the Dubins steering fields. */
+typedef struct gmt_problem {
+  gmt_scene scene;
+  const double* init;     /* dim coords */
+  int32_t init_has_heading;
+  double init_heading;
+  int32_t n;
+  double lambda;
+  double eta;
+  double radius_override; /* <= 0: use connection_radius (problem.cpp:342-351) */
+  gmt_sample_source sampling;
+} gmt_problem;
+
+typedef struct gmt_ctx gmt_ctx;
+typedef struct gmt_instance gmt_instance;
+typedef struct gmt_batch gmt_batch;
+
+/* ---- context ---------------------------------------------------------- */
+const char* gmt_last_error(void);
+int gmt_abi_version(void);
+int gmt_ctx_create(int device, gmt_ctx** out);
+void gmt_ctx_destroy(gmt_ctx* ctx);
+void* gmt_ctx_stream(gmt_ctx* ctx); /* cudaStream_t every kernel of ctx runs on */
+int gmt_ctx_synchronize(gmt_ctx* ctx);
+int64_t gmt_launch_count(const gmt_ctx* ctx); /* kernels launched so far */
+/* GMT_OPT_CLUSTER: CTAs cooperating on one single-query solve (1,2,4,8,16; 0 = auto)
+ * GMT_OPT_THREADS: threads per CTA for single-query solves (0 = auto)
+ * GMT_OPT_BATCH_THREADS: threads per CTA for batched solves (0 = auto)   */
+enum { GMT_OPT_CLUSTER = 1, GMT_OPT_THREADS = 2, GMT_OPT_BATCH_THREADS = 3 };
+int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value);
+
+/* ---- offline phase ---------------------------------------------------- */
+/* unit_ball_volume, connection_radius (graph.cpp:14-32); host scalars. */
+int gmt_unit_ball_volume(int32_t dim, double* out);
+int gmt_connection_radius(int32_t dim, int64_t n, double eta, double mu_free, double* out);
+
+/* sample_free (sampling.cpp:81-142): n free samples, goal tags, goal
+ * substitution.  coords_out[n*dim], heading_out[n] (may be NULL unless
+ * with_heading), goal_idx_out[n]; *goal_count_out entries are written.   */
+int gmt_sample_free(gmt_ctx* ctx, int32_t n, const gmt_scene* scene, const gmt_sample_source* src,
+                    double* coords_out, double* heading_out, int32_t* goal_idx_out,
+                    int32_t* goal_count_out);
+
+/* append_init (sampling.cpp:144-154) over host sample arrays of capacity
+ * n+1: appends init at index n unless an exact duplicate (coords and
+ * heading) exists.  Updates *n and the goal index list.                  */
+int gmt_append_init(gmt_ctx* ctx, int32_t dim, double* coords, double* heading, int32_t* n,
+                    const double* init, int32_t init_has_heading, double init_heading,
+                    const double* goal_lo, const double* goal_hi, int32_t* goal_idx,
+                    int32_t* goal_count, int32_t* index_out);
+
+/* build_neighbor_graph (graph.cpp:117-188), Euclidean model: r-disk CSR
+ * built on the device.  The out rows are the in rows (symmetric).
+ * Two-call pattern: pass NULL arrays to get *num_edges, then call again
+ * with out_ptr[n+1], out_col[E], out_cost[E].                            */
+int gmt_build_neighbor_graph(gmt_ctx* ctx, const double* coords, int32_t n, int32_t dim,
+                             double radius, int64_t* num_edges, int64_t* out_ptr,
+                             int32_t* out_col, double* out_cost);
+
+/* ---- device-resident instances (ProblemInstance, problem.hpp:52-57) --- */
+/* Upload host samples + graph + scene.  goal_count is samples.goal_indices
+ * .size() (only its emptiness matters, planner.cpp:39-41).               */
+int gmt_instance_upload(gmt_ctx* ctx, const gmt_scene* scene, const double* coords, int32_t n,
+                        int32_t goal_count, const gmt_graph_view* graph, gmt_instance** out);
+/* build_instance (problem.cpp:336-363) entirely on the device. */
+int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* problem, gmt_instance** out);
+int gmt_instance_info(const gmt_instance* inst, int32_t* n, int32_t* dim, int32_t* init_index,
+                      double* radius, int64_t* num_edges, int32_t* goal_count);
+/* Copy samples / goal indices / graph of an instance back to the host
+ * (any pointer may be NULL).                                             */
+int gmt_instance_download(gmt_ctx* ctx, const gmt_instance* inst, double* coords,
+                          int32_t* goal_idx, int64_t* out_ptr, int32_t* out_col,
+                          double* out_cost);
+void gmt_instance_destroy(gmt_instance* inst);
+
+/* ---- online phase ------------------------------------------------------ */
+/* gmt_plan (planner.cpp:94-198) on a device-resident instance. */
+int gmt_plan(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, double lambda,
+             double radius, gmt_plan_out* out);
+
+/* gmt_plan with every input in host memory (the drop-in call the C++ shim
+ * makes): upload, solve, download inside one call.                        */
+int gmt_plan_host(gmt_ctx* ctx, const gmt_scene* scene, const double* coords, int32_t n,
+                  int32_t goal_count, const gmt_graph_view* graph, int32_t init_index,
+                  double lambda, double radius, gmt_plan_out* out);
+
+/* fmt_plan (planner.cpp:200-262): the lambda -> 0 baseline, one node per
+ * iteration, on the device.                                              */
+int gmt_fmt_plan(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, gmt_plan_out* out);
+
+/* Batched independent queries: one CTA (or cluster) per query, one launch.
+ * init_index may be NULL (use each instance's built init index).          */
+int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const* insts,
+                     const int32_t* init_index, double lambda, gmt_batch** out);
+int gmt_batch_launch(gmt_ctx* ctx, gmt_batch* batch); /* async on gmt_ctx_stream */
+int gmt_batch_summaries(gmt_ctx* ctx, gmt_batch* batch, gmt_plan_summary* out);
+int gmt_batch_result(gmt_ctx* ctx, gmt_batch* batch, int32_t query, gmt_plan_out* out);
+void gmt_batch_destroy(gmt_batch* batch);
+
+/* Batched drop-in with host inputs: upload `count` host instances into the
+ * batch's device buffers, solve, and return summaries (+ optionally the
+ * per-query path).  The instances must have the shapes the batch was
+ * created with (same n, dim, edge counts, box counts).                    */
+int gmt_batch_plan_host(gmt_ctx* ctx, gmt_batch* batch, const gmt_scene* scenes,
+                        const double* const* coords, const gmt_graph_view* graphs,
+                        gmt_plan_summary* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GMT_B200_H */

@@ -1,0 +1,547 @@
+// ref_capi.cpp -- TEST INFRASTRUCTURE ONLY (oracle).  Never linked into or
+// called by the product library.
+//
+// A flat C wrapper over the *unmodified* reference library gmtplan, compiled
+// from its own sources under /root/reference/proj/src by oracle/Makefile into
+// oracle/_ref/libgmtref.so.  It lets the Python tests and bench.py's CPU
+// baseline call the real reference with the same flat structs the product ABI
+// uses (include/gmt_b200.h).  Nothing here re-implements the algorithm: every
+// function converts flat arrays to the reference's gmt:: types, calls the
+// reference function named in its comment, and converts the result back.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "gmt_b200.h"
+#include "gmtplan/errors.hpp"
+#include "gmtplan/graph.hpp"
+#include "gmtplan/parallel.hpp"
+#include "gmtplan/planner.hpp"
+#include "gmtplan/problem.hpp"
+#include "gmtplan/sampling.hpp"
+#include "gmtplan/space.hpp"
+
+using namespace gmt;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename Fn>
+int guard(Fn&& fn) {
+  try {
+    fn();
+    return GMT_OK;
+  } catch (const InvalidInputError& e) {
+    g_err = e.what();
+    return GMT_E_INVALID_INPUT;
+  } catch (const InfeasibleSamplingError& e) {
+    g_err = e.what();
+    return GMT_E_INFEASIBLE_SAMPLING;
+  } catch (const GoalBlockedError& e) {
+    g_err = e.what();
+    return GMT_E_GOAL_BLOCKED;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GMT_E_INTERNAL;
+  }
+}
+
+ObstacleSet to_obs(const gmt_scene* s) {
+  ObstacleSet o;
+  o.dim = s->dim;
+  for (int b = 0; b < s->num_boxes; ++b) {
+    Aabb box;
+    box.lo.assign(s->box_lo + (size_t)b * s->dim, s->box_lo + (size_t)(b + 1) * s->dim);
+    box.hi.assign(s->box_hi + (size_t)b * s->dim, s->box_hi + (size_t)(b + 1) * s->dim);
+    o.boxes.push_back(std::move(box));
+  }
+  return o;
+}
+
+GoalRegion to_goal(const gmt_scene* s) {
+  GoalRegion g;
+  g.box.lo.assign(s->goal_lo, s->goal_lo + s->dim);
+  g.box.hi.assign(s->goal_hi, s->goal_hi + s->dim);
+  return g;
+}
+
+SampleSource to_src(const gmt_sample_source* s) {
+  SampleSource src;
+  src.kind = s->kind == GMT_SAMPLE_UNIFORM ? SampleSource::Kind::uniform : SampleSource::Kind::halton;
+  src.start_index = s->start_index;
+  src.seed = s->seed;
+  src.with_heading = s->with_heading != 0;
+  return src;
+}
+
+SampleSet to_samples(const double* coords, const double* heading, int n, int dim,
+                     int goal_count) {
+  SampleSet s;
+  s.states.resize(n);
+  for (int i = 0; i < n; ++i) {
+    s.states[i].coords.assign(coords + (size_t)i * dim, coords + (size_t)(i + 1) * dim);
+    if (heading) s.states[i].heading = heading[i];
+  }
+  // Only the emptiness of goal_indices is read by the planners (planner.cpp:39-41).
+  for (int k = 0; k < goal_count; ++k) s.goal_indices.push_back(0);
+  return s;
+}
+
+NeighborGraph to_graph(const gmt_graph_view* v) {
+  NeighborGraph g;
+  g.n = v->n;
+  g.radius = v->radius;
+  // A directed graph only changes dijkstra_oracle's mirroring (planner.cpp:278).
+  g.model.kind = v->directed ? SteeringModel::Kind::dubins_airplane : SteeringModel::Kind::euclidean;
+  g.out.resize(v->n);
+  g.in.resize(v->n);
+  for (int u = 0; u < v->n; ++u) {
+    for (int64_t e = v->out_ptr[u]; e < v->out_ptr[u + 1]; ++e) {
+      g.out[u].push_back({v->out_col[e], v->out_cost[e], v->out_path ? v->out_path[e] : -1});
+    }
+  }
+  if (v->directed) {
+    for (int x = 0; x < v->n; ++x) {
+      for (int64_t e = v->in_ptr[x]; e < v->in_ptr[x + 1]; ++e) {
+        g.in[x].push_back({v->in_col[e], v->in_cost[e], v->in_path ? v->in_path[e] : -1});
+      }
+    }
+  } else {
+    g.in = g.out;
+  }
+  if (v->num_paths > 0) {
+    g.paths.resize(v->num_paths);
+    for (int64_t p = 0; p < v->num_paths; ++p) {
+      for (int64_t q = v->path_ptr[p]; q < v->path_ptr[p + 1]; ++q) {
+        State st;
+        st.coords.assign(v->path_pts + q * v->dim, v->path_pts + (q + 1) * v->dim);
+        g.paths[p].push_back(std::move(st));
+      }
+    }
+  }
+  return g;
+}
+
+void write_out(const PlanResult& r, gmt_plan_out* out) {
+  out->status = static_cast<int32_t>(r.status);
+  out->goal_node = r.path_indices.empty() ? -1 : r.path_indices.back();
+  out->cost = r.cost;
+  out->iterations = r.iterations;
+  out->total_collision_checks = r.total_collision_checks;
+  out->path_len = static_cast<int32_t>(r.path_indices.size());
+  out->num_stats = static_cast<int32_t>(r.stats.group_sizes.size());
+  out->tree_size = static_cast<int32_t>(r.tree.cost.size());
+  if (out->path) std::copy(r.path_indices.begin(), r.path_indices.end(), out->path);
+  for (int32_t v = 0; v < out->tree_size; ++v) {
+    if (out->label) out->label[v] = static_cast<uint8_t>(r.tree.label[v]);
+    if (out->tree_cost) out->tree_cost[v] = r.tree.cost[v];
+    if (out->parent) out->parent[v] = r.tree.parent[v];
+    if (out->iteration_added) out->iteration_added[v] = r.tree.iteration_added[v];
+  }
+  int32_t ns = std::min(out->num_stats, out->stats_cap);
+  for (int32_t k = 0; k < ns; ++k) {
+    if (out->group_sizes) out->group_sizes[k] = r.stats.group_sizes[k];
+    if (out->nodes_added) out->nodes_added[k] = r.stats.nodes_added[k];
+    if (out->collision_checks) out->collision_checks[k] = r.stats.collision_checks[k];
+  }
+}
+
+void write_summary(const PlanResult& r, gmt_plan_summary* s) {
+  s->status = static_cast<int32_t>(r.status);
+  s->goal_node = r.path_indices.empty() ? -1 : r.path_indices.back();
+  s->cost = r.cost;
+  s->iterations = r.iterations;
+  s->total_collision_checks = r.total_collision_checks;
+  s->path_len = static_cast<int32_t>(r.path_indices.size());
+  s->num_stats = static_cast<int32_t>(r.stats.group_sizes.size());
+}
+
+ProblemFile to_problem(const gmt_problem* p) {
+  ProblemFile f;
+  f.dimension = p->scene.dim;
+  f.obstacles = to_obs(&p->scene);
+  f.goal = to_goal(&p->scene);
+  f.init.coords.assign(p->init, p->init + p->scene.dim);
+  if (p->init_has_heading) f.init.heading = p->init_heading;
+  f.n = p->n;
+  f.lambda = p->lambda;
+  f.eta = p->eta;
+  if (p->radius_override > 0.0) f.radius_override = p->radius_override;
+  f.sampling = to_src(&p->sampling);
+  return f;
+}
+
+struct RefInstance {
+  ProblemFile problem;
+  ProblemInstance inst;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// halton / nth_prime / halton_point (sampling.cpp:21-51)
+int ref_halton(uint64_t index, uint32_t base, double* out) {
+  return guard([&] { *out = halton(index, base); });
+}
+int ref_nth_prime(int k, uint32_t* out) {
+  return guard([&] { *out = nth_prime(k); });
+}
+
+// point_free / segment_free (space.cpp:47-90)
+int ref_point_free(const gmt_scene* s, const double* p, int32_t* out) {
+  return guard([&] {
+    std::vector<double> v(p, p + s->dim);
+    *out = point_free(v, to_obs(s)) ? 1 : 0;
+  });
+}
+int ref_segment_free(const gmt_scene* s, const double* a, const double* b, int32_t* out) {
+  return guard([&] {
+    State sa{std::vector<double>(a, a + s->dim), std::nullopt};
+    State sb{std::vector<double>(b, b + s->dim), std::nullopt};
+    *out = segment_free(sa, sb, to_obs(s)) ? 1 : 0;
+  });
+}
+
+// sample_free (sampling.cpp:81-142)
+int ref_sample_free(int32_t n, const gmt_scene* scene, const gmt_sample_source* src,
+                    double* coords, double* heading, int32_t* goal_idx, int32_t* goal_count) {
+  return guard([&] {
+    SampleSet s = sample_free(n, to_obs(scene), to_goal(scene), to_src(src));
+    const int d = scene->dim;
+    for (int i = 0; i < n; ++i) {
+      std::copy(s.states[i].coords.begin(), s.states[i].coords.end(), coords + (size_t)i * d);
+      if (heading) heading[i] = s.states[i].heading ? *s.states[i].heading : 0.0;
+    }
+    *goal_count = static_cast<int32_t>(s.goal_indices.size());
+    std::copy(s.goal_indices.begin(), s.goal_indices.end(), goal_idx);
+  });
+}
+
+// append_init (sampling.cpp:144-154)
+int ref_append_init(int32_t dim, double* coords, double* heading, int32_t* n, const double* init,
+                    int32_t init_has_heading, double init_heading, const double* goal_lo,
+                    const double* goal_hi, int32_t* goal_idx, int32_t* goal_count,
+                    int32_t* index_out) {
+  return guard([&] {
+    SampleSet s;
+    s.states.resize(*n);
+    for (int i = 0; i < *n; ++i) {
+      s.states[i].coords.assign(coords + (size_t)i * dim, coords + (size_t)(i + 1) * dim);
+      if (heading) s.states[i].heading = heading[i];
+    }
+    s.goal_indices.assign(goal_idx, goal_idx + *goal_count);
+    State init_state{std::vector<double>(init, init + dim), std::nullopt};
+    if (init_has_heading) init_state.heading = init_heading;
+    GoalRegion g;
+    g.box.lo.assign(goal_lo, goal_lo + dim);
+    g.box.hi.assign(goal_hi, goal_hi + dim);
+    int idx = append_init(s, init_state, g);
+    if (static_cast<int>(s.states.size()) > *n) {
+      std::copy(init, init + dim, coords + (size_t)(*n) * dim);
+      if (heading) heading[*n] = init_has_heading ? init_heading : 0.0;
+      *n = static_cast<int32_t>(s.states.size());
+    }
+    *goal_count = static_cast<int32_t>(s.goal_indices.size());
+    std::copy(s.goal_indices.begin(), s.goal_indices.end(), goal_idx);
+    *index_out = idx;
+  });
+}
+
+// unit_ball_volume / connection_radius (graph.cpp:14-32)
+int ref_unit_ball_volume(int32_t d, double* out) {
+  return guard([&] { *out = unit_ball_volume(d); });
+}
+int ref_connection_radius(int32_t dim, int64_t n, double eta, double mu, double* out) {
+  return guard([&] {
+    RadiusParams p;
+    p.dimension = dim;
+    p.n = n;
+    p.eta = eta;
+    p.mu_free = mu;
+    *out = connection_radius(p);
+  });
+}
+
+// build_neighbor_graph (graph.cpp:117-188), Euclidean model.  Two-call
+// pattern like the product ABI: NULL arrays return only the edge count.
+int ref_build_neighbor_graph(const double* coords, int32_t n, int32_t dim, double radius,
+                             int32_t workers, int64_t* num_edges, int64_t* out_ptr,
+                             int32_t* out_col, double* out_cost) {
+  return guard([&] {
+    std::vector<State> st(n);
+    for (int i = 0; i < n; ++i) st[i].coords.assign(coords + (size_t)i * dim, coords + (size_t)(i + 1) * dim);
+    NeighborGraph g = build_neighbor_graph(st, SteeringModel{}, radius, workers);
+    *num_edges = static_cast<int64_t>(g.edge_count());
+    if (!out_ptr) return;
+    int64_t e = 0;
+    for (int u = 0; u < n; ++u) {
+      out_ptr[u] = e;
+      for (const auto& ed : g.out[u]) {
+        out_col[e] = ed.other;
+        out_cost[e] = ed.cost;
+        ++e;
+      }
+    }
+    out_ptr[n] = e;
+  });
+}
+
+// gmt_plan (planner.cpp:94-198)
+int ref_gmt_plan(const gmt_scene* scene, const double* coords, int32_t n, int32_t goal_count,
+                 const gmt_graph_view* graph, int32_t init_index, double lambda, double radius,
+                 int32_t workers, gmt_plan_out* out) {
+  return guard([&] {
+    SampleSet s = to_samples(coords, nullptr, n, scene->dim, goal_count);
+    NeighborGraph g = to_graph(graph);
+    GmtParams params;
+    params.lambda = lambda;
+    params.radius = radius;
+    params.workers = workers;
+    PlanResult r = gmt_plan(s, g, to_obs(scene), to_goal(scene), init_index, params);
+    write_out(r, out);
+  });
+}
+
+// fmt_plan (planner.cpp:200-262)
+int ref_fmt_plan(const gmt_scene* scene, const double* coords, int32_t n, int32_t goal_count,
+                 const gmt_graph_view* graph, int32_t init_index, gmt_plan_out* out) {
+  return guard([&] {
+    SampleSet s = to_samples(coords, nullptr, n, scene->dim, goal_count);
+    NeighborGraph g = to_graph(graph);
+    PlanResult r = fmt_plan(s, g, to_obs(scene), to_goal(scene), init_index);
+    write_out(r, out);
+  });
+}
+
+// dijkstra_oracle (planner.cpp:264-334)
+int ref_dijkstra_oracle(const gmt_scene* scene, const double* coords, int32_t n,
+                        int32_t goal_count, const gmt_graph_view* graph, int32_t init_index,
+                        gmt_plan_out* out) {
+  return guard([&] {
+    SampleSet s = to_samples(coords, nullptr, n, scene->dim, goal_count);
+    NeighborGraph g = to_graph(graph);
+    PlanResult r = dijkstra_oracle(s, g, to_obs(scene), to_goal(scene), init_index);
+    write_out(r, out);
+  });
+}
+
+// ---- ProblemInstance handles: build_instance (problem.cpp:336-363) -------
+int ref_instance_build(const gmt_problem* p, int32_t workers, void** out) {
+  return guard([&] {
+    auto* ri = new RefInstance;
+    try {
+      ri->problem = to_problem(p);
+      ri->inst = build_instance(ri->problem, workers);
+    } catch (...) {
+      delete ri;
+      throw;
+    }
+    *out = ri;
+  });
+}
+
+void ref_instance_destroy(void* h) { delete static_cast<RefInstance*>(h); }
+
+int ref_instance_info(void* h, int32_t* n, int32_t* init_index, double* radius,
+                      int64_t* num_edges, int32_t* goal_count) {
+  return guard([&] {
+    auto* ri = static_cast<RefInstance*>(h);
+    *n = static_cast<int32_t>(ri->inst.samples.states.size());
+    *init_index = ri->inst.init_index;
+    *radius = ri->inst.radius;
+    *num_edges = static_cast<int64_t>(ri->inst.graph.edge_count());
+    *goal_count = static_cast<int32_t>(ri->inst.samples.goal_indices.size());
+  });
+}
+
+int ref_instance_download(void* h, double* coords, int32_t* goal_idx, int64_t* out_ptr,
+                          int32_t* out_col, double* out_cost) {
+  return guard([&] {
+    auto* ri = static_cast<RefInstance*>(h);
+    const auto& st = ri->inst.samples.states;
+    const int d = ri->problem.dimension;
+    if (coords) {
+      for (size_t i = 0; i < st.size(); ++i) std::copy(st[i].coords.begin(), st[i].coords.end(), coords + i * d);
+    }
+    if (goal_idx) std::copy(ri->inst.samples.goal_indices.begin(), ri->inst.samples.goal_indices.end(), goal_idx);
+    if (out_ptr) {
+      const auto& g = ri->inst.graph;
+      int64_t e = 0;
+      for (int u = 0; u < g.n; ++u) {
+        out_ptr[u] = e;
+        for (const auto& ed : g.out[u]) {
+          if (out_col) out_col[e] = ed.other;
+          if (out_cost) out_cost[e] = ed.cost;
+          ++e;
+        }
+      }
+      out_ptr[g.n] = e;
+    }
+  });
+}
+
+int ref_instance_plan(void* h, double lambda, int32_t workers, gmt_plan_out* out) {
+  return guard([&] {
+    auto* ri = static_cast<RefInstance*>(h);
+    GmtParams params;
+    params.lambda = lambda;
+    params.radius = ri->inst.radius;
+    params.workers = workers;
+    PlanResult r = gmt_plan(ri->inst.samples, ri->inst.graph, ri->problem.obstacles,
+                            ri->problem.goal, ri->inst.init_index, params);
+    write_out(r, out);
+  });
+}
+
+// Batched CPU baseline: one gmt_plan(workers=1) per query under
+// parallel_chunks, the pattern of simulator.cpp:212.  Returns wall seconds
+// of the whole batch in *seconds.
+int ref_plan_many(void** handles, int32_t count, double lambda, int32_t threads,
+                  gmt_plan_summary* out, double* seconds) {
+  return guard([&] {
+    std::vector<PlanResult> results(count);
+    auto t0 = std::chrono::steady_clock::now();
+    parallel_chunks(threads, static_cast<std::size_t>(count), [&](std::size_t b, std::size_t e) {
+      for (std::size_t q = b; q < e; ++q) {
+        auto* ri = static_cast<RefInstance*>(handles[q]);
+        GmtParams params;
+        params.lambda = lambda;
+        params.radius = ri->inst.radius;
+        params.workers = 1;
+        results[q] = gmt_plan(ri->inst.samples, ri->inst.graph, ri->problem.obstacles,
+                              ri->problem.goal, ri->inst.init_index, params);
+      }
+    });
+    auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (out) {
+      for (int32_t q = 0; q < count; ++q) write_summary(results[q], &out[q]);
+    }
+  });
+}
+
+// Parallel build of many instances (setup for the baseline, not timed).
+int ref_instance_build_many(const gmt_problem* problems, int32_t count, int32_t threads,
+                            void** out) {
+  return guard([&] {
+    std::vector<std::string> errs(count);
+    parallel_chunks(threads, static_cast<std::size_t>(count), [&](std::size_t b, std::size_t e) {
+      for (std::size_t q = b; q < e; ++q) {
+        auto* ri = new RefInstance;
+        try {
+          ri->problem = to_problem(&problems[q]);
+          ri->inst = build_instance(ri->problem, 1);
+          out[q] = ri;
+        } catch (const std::exception& ex) {
+          delete ri;
+          out[q] = nullptr;
+          errs[q] = ex.what();
+        }
+      }
+    });
+    for (int32_t q = 0; q < count; ++q) {
+      if (!out[q]) throw std::runtime_error("query " + std::to_string(q) + ": " + errs[q]);
+    }
+  });
+}
+
+// ---- problem files: parse_problem / problem_key (problem.cpp:102-303) -----
+// Parses JSON text and reports the flat fields.  Arrays are caller-owned with
+// capacity given by the first call (dim, num_boxes are always written).
+int ref_parse_problem(const char* json_text, int32_t* dim, int32_t* num_boxes, double* box_lo,
+                      double* box_hi, double* goal_lo, double* goal_hi, double* init,
+                      int32_t* n, double* lambda, double* eta, double* radius_override,
+                      int32_t* sampling_kind, uint64_t* start_index, uint64_t* seed,
+                      uint64_t* key, int32_t* steering_kind) {
+  return guard([&] {
+    ProblemFile p = parse_problem(json_text);
+    *dim = p.dimension;
+    *num_boxes = static_cast<int32_t>(p.obstacles.boxes.size());
+    if (!box_lo) return;
+    for (int b = 0; b < *num_boxes; ++b) {
+      std::copy(p.obstacles.boxes[b].lo.begin(), p.obstacles.boxes[b].lo.end(), box_lo + b * p.dimension);
+      std::copy(p.obstacles.boxes[b].hi.begin(), p.obstacles.boxes[b].hi.end(), box_hi + b * p.dimension);
+    }
+    std::copy(p.goal.box.lo.begin(), p.goal.box.lo.end(), goal_lo);
+    std::copy(p.goal.box.hi.begin(), p.goal.box.hi.end(), goal_hi);
+    std::copy(p.init.coords.begin(), p.init.coords.end(), init);
+    *n = p.n;
+    *lambda = p.lambda;
+    *eta = p.eta;
+    *radius_override = p.radius_override ? *p.radius_override : 0.0;
+    *sampling_kind = p.sampling.kind == SampleSource::Kind::uniform ? 1 : 0;
+    *start_index = p.sampling.start_index;
+    *seed = p.sampling.seed;
+    *key = problem_key(p);
+    *steering_kind = p.steering.kind == SteeringModel::Kind::euclidean ? 0 : 1;
+  });
+}
+
+}  // extern "C"
+
+// ---- the reference's own seeded problem generator -------------------------
+// make_random_problem (tests/support/oracles.cpp:258-327) and its Pcg32
+// stream, exposed so the Python tests draw the very problems the reference's
+// property tests draw.
+#include "support/oracles.hpp"
+
+extern "C" {
+
+void* ref_rng_create(uint64_t seed) { return new Pcg32(seed); }
+void ref_rng_destroy(void* h) { delete static_cast<Pcg32*>(h); }
+uint32_t ref_rng_next_u32(void* h) { return static_cast<Pcg32*>(h)->next_u32(); }
+
+int ref_random_problem_new(void* rng, int32_t dim, int32_t with_obstacles, int32_t n_min,
+                           int32_t n_max, void** out) {
+  return guard([&] {
+    test::RandomProblemOptions opt;
+    opt.dim = dim;
+    opt.with_obstacles = with_obstacles != 0;
+    opt.n_min = n_min;
+    opt.n_max = n_max;
+    *out = new test::RandomProblem(test::make_random_problem(*static_cast<Pcg32*>(rng), opt));
+  });
+}
+
+void ref_random_problem_free(void* h) { delete static_cast<test::RandomProblem*>(h); }
+
+int ref_random_problem_info(void* h, int32_t* num_boxes, int32_t* n_samples, int32_t* init_index,
+                            double* radius, int32_t* goal_count, uint64_t* seed) {
+  return guard([&] {
+    auto* p = static_cast<test::RandomProblem*>(h);
+    *num_boxes = static_cast<int32_t>(p->obs.boxes.size());
+    *n_samples = static_cast<int32_t>(p->samples.states.size());
+    *init_index = p->init_index;
+    *radius = p->radius;
+    *goal_count = static_cast<int32_t>(p->samples.goal_indices.size());
+    *seed = 0;
+  });
+}
+
+int ref_random_problem_get(void* h, double* box_lo, double* box_hi, double* goal_lo,
+                           double* goal_hi, double* init, double* coords, int32_t* goal_idx) {
+  return guard([&] {
+    auto* p = static_cast<test::RandomProblem*>(h);
+    const int d = p->obs.dim;
+    for (size_t b = 0; b < p->obs.boxes.size(); ++b) {
+      std::copy(p->obs.boxes[b].lo.begin(), p->obs.boxes[b].lo.end(), box_lo + b * d);
+      std::copy(p->obs.boxes[b].hi.begin(), p->obs.boxes[b].hi.end(), box_hi + b * d);
+    }
+    std::copy(p->goal.box.lo.begin(), p->goal.box.lo.end(), goal_lo);
+    std::copy(p->goal.box.hi.begin(), p->goal.box.hi.end(), goal_hi);
+    std::copy(p->init.coords.begin(), p->init.coords.end(), init);
+    for (size_t i = 0; i < p->samples.states.size(); ++i) {
+      std::copy(p->samples.states[i].coords.begin(), p->samples.states[i].coords.end(), coords + i * d);
+    }
+    std::copy(p->samples.goal_indices.begin(), p->samples.goal_indices.end(), goal_idx);
+  });
+}
+
+}  // extern "C"

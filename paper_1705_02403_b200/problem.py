@@ -1,0 +1,452 @@
+"""Problem description (gmt-problem/1) on the host side.
+
+`ProblemSpec` mirrors `gmt::ProblemFile` (problem.hpp:17-29) for the
+Euclidean model, `load_problem`/`parse_problem` mirror the reference's strict
+JSON loader (problem.cpp:102-231: unknown keys rejected at every level,
+errors name the offending field path, init must be free), and the synthetic
+scene generators define the BASELINE workloads that have no reference scene
+file: the 3D forest (C2) and the batched query sets.
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import abi
+from .errors import InvalidInputError
+
+SCHEMA = "gmt-problem/1"
+MASK64 = (1 << 64) - 1
+
+
+# ---- PCG32 / splitmix64 (rng.hpp:11-75), host-side scene generation only ----
+class Pcg32:
+    """PCG-XSH-RR 32 exactly as rng.hpp:11-33 (used to draw synthetic scenes)."""
+
+    def __init__(self, seed: int, seq: int = 0):
+        self.state = 0
+        self.inc = ((seq << 1) | 1) & MASK64
+        self.next_u32()
+        self.state = (self.state + seed) & MASK64
+        self.next_u32()
+
+    def next_u32(self) -> int:
+        old = self.state
+        self.state = (old * 6364136223846793005 + self.inc) & MASK64
+        xorshifted = (((old >> 18) ^ old) >> 27) & 0xFFFFFFFF
+        rot = old >> 59
+        return ((xorshifted >> rot) | (xorshifted << ((32 - rot) & 31))) & 0xFFFFFFFF
+
+    def next_double(self) -> float:
+        return self.next_u32() * 2.0 ** -32
+
+
+def mix64(x: int, b: int | None = None) -> int:
+    """splitmix64 (rng.hpp:68-75); mix64(a, b) = mix64(mix64(a) ^ b)."""
+    if b is not None:
+        return mix64(mix64(x) ^ b)
+    x = (x + 0x9E3779B97F4A7C15) & MASK64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & MASK64
+    return x ^ (x >> 31)
+
+
+@dataclass
+class ProblemSpec:
+    dim: int
+    box_lo: np.ndarray  # [B, dim]
+    box_hi: np.ndarray  # [B, dim]
+    goal_lo: np.ndarray  # [dim]
+    goal_hi: np.ndarray  # [dim]
+    init: np.ndarray  # [dim]
+    n: int
+    lam: float = 1.0
+    eta: float = 0.0
+    radius_override: float | None = None
+    sampling_kind: int = abi.SAMPLE_HALTON
+    start_index: int = 1
+    seed: int = 0
+    notes: str = ""
+    _keep: list = field(default_factory=list, repr=False)
+
+    @property
+    def num_boxes(self) -> int:
+        return int(self.box_lo.shape[0])
+
+    def scene(self) -> abi.Scene:
+        """Flat gmt_scene view (keeps the arrays alive on self)."""
+        lo = abi.f64(self.box_lo.reshape(-1)) if self.num_boxes else np.zeros(1)
+        hi = abi.f64(self.box_hi.reshape(-1)) if self.num_boxes else np.zeros(1)
+        gl, gh = abi.f64(self.goal_lo), abi.f64(self.goal_hi)
+        self._keep = [lo, hi, gl, gh]
+        s = abi.Scene()
+        s.dim = self.dim
+        s.num_boxes = self.num_boxes
+        s.box_lo = abi.ptr(lo, abi.C.c_double)
+        s.box_hi = abi.ptr(hi, abi.C.c_double)
+        s.goal_lo = abi.ptr(gl, abi.C.c_double)
+        s.goal_hi = abi.ptr(gh, abi.C.c_double)
+        return s
+
+    def source(self) -> abi.SampleSource:
+        s = abi.SampleSource()
+        s.kind = self.sampling_kind
+        s.with_heading = 0
+        s.start_index = self.start_index
+        s.seed = self.seed
+        return s
+
+    def flat(self) -> abi.Problem:
+        p = abi.Problem()
+        p.scene = self.scene()
+        init = abi.f64(self.init)
+        self._keep.append(init)
+        p.init = abi.ptr(init, abi.C.c_double)
+        p.init_has_heading = 0
+        p.init_heading = 0.0
+        p.n = self.n
+        p.lambda_ = self.lam
+        p.eta = self.eta
+        p.radius_override = self.radius_override if self.radius_override else 0.0
+        p.sampling = self.source()
+        return p
+
+    def with_n(self, n: int) -> "ProblemSpec":
+        q = ProblemSpec(**{k: getattr(self, k) for k in self.__dataclass_fields__ if k != "_keep"})
+        q.n = n
+        return q
+
+    def point_free(self, p) -> bool:
+        """point_free (space.cpp:47-54)."""
+        p = np.asarray(p, np.float64)
+        if np.any(p < 0.0) or np.any(p > 1.0):
+            return False
+        for b in range(self.num_boxes):
+            if np.all(p >= self.box_lo[b]) and np.all(p <= self.box_hi[b]):
+                return False
+        return True
+
+    def to_json(self) -> str:
+        """problem_json (problem.cpp:233-272), Euclidean model."""
+        doc = {
+            "schema": SCHEMA,
+            "dimension": self.dim,
+            "steering": {"model": "euclidean"},
+            "obstacles": [{"lo": self.box_lo[b].tolist(), "hi": self.box_hi[b].tolist()}
+                          for b in range(self.num_boxes)],
+            "init": {"coords": self.init.tolist()},
+            "goal": {"lo": self.goal_lo.tolist(), "hi": self.goal_hi.tolist()},
+            "n": self.n,
+            "lambda": self.lam,
+            "eta": self.eta,
+        }
+        if self.radius_override:
+            doc["radius_override"] = self.radius_override
+        if self.sampling_kind == abi.SAMPLE_HALTON:
+            doc["sampling"] = {"kind": "halton", "start_index": self.start_index}
+        else:
+            doc["sampling"] = {"kind": "uniform", "seed": self.seed}
+        if self.notes:
+            doc["notes"] = self.notes
+        return json.dumps(doc, indent=2) + "\n"
+
+
+# ---- strict loader (problem.cpp:102-231) ----------------------------------
+def _fail(path: str, what: str):
+    raise InvalidInputError(f"{path}: {what}")
+
+
+def _reject_unknown(obj: dict, path: str, allowed):
+    for k in obj:
+        if k not in allowed:
+            _fail(k if not path else f"{path}.{k}", "unknown field")
+
+
+def _member(obj: dict, path: str, key: str):
+    if key not in obj:
+        _fail(key if not path else f"{path}.{key}", "required field is missing")
+    return obj[key]
+
+
+def _is_num(v) -> bool:
+    return isinstance(v, (int, float)) and not isinstance(v, bool)
+
+
+def _as_double(v, path):
+    if not _is_num(v):
+        _fail(path, "expected a number")
+    return float(v)
+
+
+def _as_int(v, path):
+    if not isinstance(v, int) or isinstance(v, bool):
+        _fail(path, "expected an integer")
+    return v
+
+
+def _as_vector(v, path, dim):
+    if not isinstance(v, list):
+        _fail(path, "expected an array of numbers")
+    if len(v) != dim:
+        _fail(path, f"expected {dim} coordinates, got {len(v)}")
+    return np.array([_as_double(x, f"{path}[{k}]") for k, x in enumerate(v)], np.float64)
+
+
+def _parse_box(v, path, dim):
+    if not isinstance(v, dict):
+        _fail(path, "expected an object with lo and hi")
+    _reject_unknown(v, path, ("lo", "hi"))
+    lo = _as_vector(_member(v, path, "lo"), path + ".lo", dim)
+    hi = _as_vector(_member(v, path, "hi"), path + ".hi", dim)
+    for k in range(dim):
+        if lo[k] > hi[k]:
+            _fail(path, f"lo exceeds hi on axis {k}")
+    return lo, hi
+
+
+def parse_problem(text: str) -> ProblemSpec:
+    """parse_problem (problem.cpp:102-223) for the euclidean model.  The
+    dubins_airplane model parses but is rejected: it is a §8(f) "next" row."""
+    try:
+        doc = json.loads(text)
+    except json.JSONDecodeError as e:
+        raise InvalidInputError(f"invalid JSON: {e}") from None
+    if not isinstance(doc, dict):
+        raise InvalidInputError("top level: expected a JSON object")
+    _reject_unknown(doc, "", ("schema", "dimension", "steering", "obstacles", "init", "goal", "n",
+                              "lambda", "eta", "radius_override", "sampling", "notes"))
+    schema = _member(doc, "", "schema")
+    if not isinstance(schema, str):
+        _fail("schema", "expected a string")
+    if schema != SCHEMA:
+        _fail("schema", f'expected "{SCHEMA}"')
+    dim = _as_int(_member(doc, "", "dimension"), "dimension")
+    if dim < 1:
+        _fail("dimension", "must be at least 1")
+    steering = _member(doc, "", "steering")
+    if not isinstance(steering, dict):
+        _fail("steering", "expected an object")
+    _reject_unknown(steering, "steering", ("model", "rho", "discretization_step", "planar_cost_only"))
+    model = _member(steering, "steering", "model")
+    if not isinstance(model, str):
+        _fail("steering.model", "expected a string")
+    if model == "euclidean":
+        for key in ("rho", "discretization_step", "planar_cost_only"):
+            if key in steering:
+                _fail(f"steering.{key}", "only the dubins_airplane model uses this field")
+    elif model == "dubins_airplane":
+        raise InvalidInputError("steering.model: dubins_airplane is not supported by the B200 "
+                                "build yet (SURVEY.md §8(f) row 1)")
+    else:
+        _fail("steering.model", 'expected "euclidean" or "dubins_airplane"')
+    obstacles = _member(doc, "", "obstacles")
+    if not isinstance(obstacles, list):
+        _fail("obstacles", "expected an array of boxes")
+    los, his = [], []
+    for k, b in enumerate(obstacles):
+        lo, hi = _parse_box(b, f"obstacles[{k}]", dim)
+        los.append(lo)
+        his.append(hi)
+    box_lo = np.array(los, np.float64).reshape(-1, dim)
+    box_hi = np.array(his, np.float64).reshape(-1, dim)
+    init = _member(doc, "", "init")
+    if not isinstance(init, dict):
+        _fail("init", "expected an object with coords")
+    _reject_unknown(init, "init", ("coords", "heading"))
+    init_c = _as_vector(_member(init, "init", "coords"), "init.coords", dim)
+    if "heading" in init:
+        _fail("init.heading", "only the dubins_airplane model uses a heading")
+    goal_lo, goal_hi = _parse_box(_member(doc, "", "goal"), "goal", dim)
+    n = _as_int(_member(doc, "", "n"), "n")
+    if n < 1:
+        _fail("n", "must be at least 1")
+    spec = ProblemSpec(dim=dim, box_lo=box_lo, box_hi=box_hi, goal_lo=goal_lo, goal_hi=goal_hi,
+                       init=init_c, n=n)
+    if not spec.point_free(init_c):
+        _fail("init", "start state is not in free space")
+    if "lambda" in doc:
+        lam = _as_double(doc["lambda"], "lambda")
+        if not lam > 0.0 or lam > 1.0:
+            _fail("lambda", "must be in (0, 1]")
+        spec.lam = lam
+    if "eta" in doc:
+        eta = _as_double(doc["eta"], "eta")
+        if eta < 0.0:
+            _fail("eta", "must be non-negative")
+        spec.eta = eta
+    if "radius_override" in doc:
+        r = _as_double(doc["radius_override"], "radius_override")
+        if not r > 0.0:
+            _fail("radius_override", "must be positive")
+        spec.radius_override = r
+    if "sampling" in doc:
+        s = doc["sampling"]
+        if not isinstance(s, dict):
+            _fail("sampling", "expected an object")
+        _reject_unknown(s, "sampling", ("kind", "start_index", "seed"))
+        kind = _member(s, "sampling", "kind")
+        if not isinstance(kind, str):
+            _fail("sampling.kind", "expected a string")
+        if kind == "halton":
+            spec.sampling_kind = abi.SAMPLE_HALTON
+            if "seed" in s:
+                _fail("sampling.seed", "only uniform sampling takes a seed")
+            if "start_index" in s:
+                v = s["start_index"]
+                if not isinstance(v, int) or isinstance(v, bool) or v < 0:
+                    _fail("sampling.start_index", "expected a non-negative integer")
+                if v == 0:
+                    _fail("sampling.start_index", "must be at least 1")
+                spec.start_index = v
+        elif kind == "uniform":
+            spec.sampling_kind = abi.SAMPLE_UNIFORM
+            if "start_index" in s:
+                _fail("sampling.start_index", "only halton sampling takes a start index")
+            if "seed" in s:
+                v = s["seed"]
+                if not isinstance(v, int) or isinstance(v, bool) or v < 0:
+                    _fail("sampling.seed", "expected a non-negative integer")
+                spec.seed = v
+        else:
+            _fail("sampling.kind", 'expected "halton" or "uniform"')
+    if "notes" in doc:
+        if not isinstance(doc["notes"], str):
+            _fail("notes", "expected a string")
+        spec.notes = doc["notes"]
+    return spec
+
+
+def load_problem(path: str) -> ProblemSpec:
+    """load_problem (problem.cpp:225-231)."""
+    try:
+        with open(path, "rb") as f:
+            text = f.read().decode()
+    except OSError:
+        raise InvalidInputError(f"{path}: cannot open file") from None
+    return parse_problem(text)
+
+
+# ---- synthetic BASELINE scenes ---------------------------
+def forest_3d(seed: int = 3, n: int = 4000, pillars: int = 60) -> ProblemSpec:
+    """C2 "3D forest": `pillars` vertical boxes drawn from Pcg32(seed):
+    centre U[0.1,0.9]^2, square footprint half-width U[0.02,0.05], z from 0 to
+    a height U[0.5,1].  Init (0.03,0.03,0.5); goal [0.92,0.98]^2 x [0.4,0.6];
+    Halton samples; formula radius."""
+    rng = Pcg32(seed)
+    lo, hi = [], []
+    for _ in range(pillars):
+        cx = 0.1 + 0.8 * rng.next_double()
+        cy = 0.1 + 0.8 * rng.next_double()
+        hw = 0.02 + 0.03 * rng.next_double()
+        h = 0.5 + 0.5 * rng.next_double()
+        lo.append([cx - hw, cy - hw, 0.0])
+        hi.append([cx + hw, cy + hw, h])
+    spec = ProblemSpec(dim=3, box_lo=np.array(lo), box_hi=np.array(hi),
+                       goal_lo=np.array([0.92, 0.92, 0.4]), goal_hi=np.array([0.98, 0.98, 0.6]),
+                       init=np.array([0.03, 0.03, 0.5]), n=n,
+                       notes=f"Synthetic 3D forest: {pillars} pillars from Pcg32({seed}).")
+    if not spec.point_free(spec.init):
+        raise InvalidInputError("forest init collides")
+    return spec
+
+
+def random_forest_query(master: int, q: int, n: int = 4000, pillars: int = 60) -> ProblemSpec:
+    """Batched query q (SURVEY.md §8(d) C5 construction, Euclidean 3D): its own
+    forest, start and goal drawn from Pcg32(mix64(master, q)).  Start in the
+    low corner region, goal box in the opposite corner region."""
+    rng = Pcg32(mix64(master, q))
+    lo, hi = [], []
+    for _ in range(pillars):
+        cx = 0.1 + 0.8 * rng.next_double()
+        cy = 0.1 + 0.8 * rng.next_double()
+        hw = 0.02 + 0.03 * rng.next_double()
+        h = 0.5 + 0.5 * rng.next_double()
+        lo.append([cx - hw, cy - hw, 0.0])
+        hi.append([cx + hw, cy + hw, h])
+    box_lo, box_hi = np.array(lo), np.array(hi)
+    spec = None
+    for _ in range(100):
+        init = np.array([0.02 + 0.06 * rng.next_double(), 0.02 + 0.06 * rng.next_double(),
+                         0.2 + 0.6 * rng.next_double()])
+        gc = np.array([0.90 + 0.05 * rng.next_double(), 0.90 + 0.05 * rng.next_double(),
+                       0.3 + 0.4 * rng.next_double()])
+        spec = ProblemSpec(dim=3, box_lo=box_lo, box_hi=box_hi, goal_lo=gc - 0.04,
+                           goal_hi=np.minimum(gc + 0.04, 1.0), init=init, n=n)
+        if spec.point_free(init):
+            return spec
+    raise InvalidInputError("could not draw a free start")
+
+
+def extrude(spec: ProblemSpec, dim: int, n: int | None = None) -> ProblemSpec:
+    """Lift a scene to `dim` dimensions by extruding every box through the
+    extra axes (the construction of rectangles_6d.json and the SURVEY's 12D
+    stand-in, §6 C4).  Init/goal take 0.5 / [0.2,0.8] on new axes."""
+    extra = dim - spec.dim
+    box_lo = np.concatenate([spec.box_lo, np.zeros((spec.num_boxes, extra))], axis=1)
+    box_hi = np.concatenate([spec.box_hi, np.ones((spec.num_boxes, extra))], axis=1)
+    return ProblemSpec(dim=dim, box_lo=box_lo, box_hi=box_hi,
+                       goal_lo=np.concatenate([spec.goal_lo, np.full(extra, 0.2)]),
+                       goal_hi=np.concatenate([spec.goal_hi, np.full(extra, 0.8)]),
+                       init=np.concatenate([spec.init, np.full(extra, 0.5)]),
+                       n=spec.n if n is None else n, lam=spec.lam, eta=spec.eta,
+                       radius_override=spec.radius_override)
+
+
+def random_problem_2d(rng: Pcg32, dim: int = 2, with_obstacles: bool = True, n_min: int = 120,
+                      n_max: int = 350):
+    """make_random_problem (tests/support/oracles.cpp:258-327), Euclidean
+    branch, draw for draw: 2-6 boxes, goal box, free init not in goal,
+    uniform samples seeded mix64(u32, u32), n in [n_min, n_max].  Returns
+    the spec; sampling failures are retried by the caller's loop like the
+    reference (which catches runtime_error and redraws)."""
+    for _ in range(200):
+        lo, hi = [], []
+        if with_obstacles:
+            count = 2 + rng.next_u32() % 5
+            for _b in range(count):
+                l, h = [], []
+                for _k in range(dim):
+                    a = rng.next_double() * 0.85
+                    size = 0.05 + 0.20 * rng.next_double()
+                    l.append(a)
+                    h.append(min(a + size, 1.0))
+                lo.append(l)
+                hi.append(h)
+        gl, gh = [], []
+        for _k in range(dim):
+            c = 0.15 + 0.7 * rng.next_double()
+            half = 0.04 + 0.04 * rng.next_double()
+            gl.append(max(c - half, 0.0))
+            gh.append(min(c + half, 1.0))
+        spec = ProblemSpec(dim=dim, box_lo=np.array(lo, np.float64).reshape(-1, dim),
+                           box_hi=np.array(hi, np.float64).reshape(-1, dim),
+                           goal_lo=np.array(gl), goal_hi=np.array(gh), init=np.zeros(dim), n=1)
+        found = False
+        for _t in range(400):
+            p = np.array([rng.next_double() for _k in range(dim)])
+            in_goal = bool(np.all(p >= spec.goal_lo) and np.all(p <= spec.goal_hi))
+            if spec.point_free(p) and not in_goal:
+                spec.init = p
+                found = True
+                break
+        if not found:
+            continue
+        spec.sampling_kind = abi.SAMPLE_UNIFORM
+        a = rng.next_u32()
+        b = rng.next_u32()
+        spec.seed = mix64(a, b)
+        spec.n = n_min + rng.next_u32() % (n_max - n_min + 1)
+        return spec
+    raise RuntimeError("random problem generation kept hitting infeasible draws")
+
+
+def connection_radius_py(dim: int, n: int, eta: float = 0.0, mu: float = 1.0) -> float:
+    """Python float restatement of graph.cpp:19-32 (for quick checks only;
+    the product computes it in C++ with the same libm calls)."""
+    inv_d = 1.0 / dim
+    zeta = math.pi ** (0.5 * dim) / math.gamma(0.5 * dim + 1.0)
+    return (4.0 * (1.0 + eta) ** inv_d * inv_d ** inv_d * (mu / zeta) ** inv_d
+            * (math.log(n) / n) ** inv_d)
