@@ -176,8 +176,14 @@ int gmt_ctx_synchronize(gmt_ctx* ctx);
 int64_t gmt_launch_count(const gmt_ctx* ctx); /* kernels launched so far */
 /* GMT_OPT_CLUSTER: CTAs cooperating on one single-query solve (1,2,4,8,16; 0 = auto)
  * GMT_OPT_THREADS: threads per CTA for single-query solves (0 = auto)
- * GMT_OPT_BATCH_THREADS: threads per CTA for batched solves (0 = auto)   */
-enum { GMT_OPT_CLUSTER = 1, GMT_OPT_THREADS = 2, GMT_OPT_BATCH_THREADS = 3 };
+ * GMT_OPT_BATCH_THREADS: threads per CTA for batched solves (0 = auto)
+ * GMT_OPT_BATCH_CLUSTER: CTAs per query in batched solves (default 1)    */
+enum {
+  GMT_OPT_CLUSTER = 1,
+  GMT_OPT_THREADS = 2,
+  GMT_OPT_BATCH_THREADS = 3,
+  GMT_OPT_BATCH_CLUSTER = 4
+};
 int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value);
 
 /* ---- offline phase ---------------------------------------------------- */
@@ -248,13 +254,41 @@ int gmt_batch_summaries(gmt_ctx* ctx, gmt_batch* batch, gmt_plan_summary* out);
 int gmt_batch_result(gmt_ctx* ctx, gmt_batch* batch, int32_t query, gmt_plan_out* out);
 void gmt_batch_destroy(gmt_batch* batch);
 
-/* Batched drop-in with host inputs: upload `count` host instances into the
- * batch's device buffers, solve, and return summaries (+ optionally the
- * per-query path).  The instances must have the shapes the batch was
- * created with (same n, dim, edge counts, box counts).                    */
-int gmt_batch_plan_host(gmt_ctx* ctx, gmt_batch* batch, const gmt_scene* scenes,
-                        const double* const* coords, const gmt_graph_view* graphs,
-                        gmt_plan_summary* out);
+/* Batched drop-in with host inputs (Euclidean graphs): `count` independent
+ * queries packed back to back in host arrays (pinned memory recommended).
+ * Query q owns nodes [node_off[q], node_off[q+1]), edges [edge_off[q],
+ * edge_off[q+1]) and boxes [box_off[q], box_off[q+1]); its row_ptr block
+ * holds n_q+1 entries starting at row_ptr[node_off[q] + q], relative to
+ * edge_off[q].  One H2D copy per array, one solve launch, D2H of the
+ * summaries and (optionally) paths [total_nodes] and full trees.         */
+typedef struct gmt_batch_host {
+  int32_t count;
+  int32_t dim;
+  const int64_t* node_off;   /* [count+1] */
+  const int64_t* edge_off;   /* [count+1] */
+  const int32_t* box_off;    /* [count+1] */
+  const double* coords;      /* [total_nodes*dim] */
+  const double* box_lo;      /* [total_boxes*dim] */
+  const double* box_hi;
+  const double* goal_lo;     /* [count*dim] */
+  const double* goal_hi;
+  const int64_t* row_ptr;    /* [total_nodes+count] */
+  const int32_t* col;        /* [total_edges] */
+  const double* cost;        /* [total_edges] */
+  const int32_t* goal_count; /* [count] */
+  const int32_t* init_index; /* [count] */
+  const double* radius;      /* [count] graph radius == params.radius */
+} gmt_batch_host;
+
+/* paths / label / tree_cost / parent / iteration_added are [total_nodes]
+ * arrays indexed like coords (any may be NULL); summaries [count].        */
+int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* batch, double lambda,
+                        gmt_plan_summary* summaries, int32_t* paths, uint8_t* label,
+                        double* tree_cost, int32_t* parent, int64_t* iteration_added);
+
+/* Host buffers the library pins for faster H2D/D2H (cudaHostAlloc). */
+int gmt_host_alloc(size_t bytes, void** out);
+void gmt_host_free(void* p);
 
 #ifdef __cplusplus
 }

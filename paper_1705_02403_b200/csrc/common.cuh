@@ -1,0 +1,153 @@
+// common.cuh -- shared device code of the B200 GMT* library.
+//
+// Bitwise parity with the reference (x86-64 SSE2 doubles, no FMA; SURVEY.md
+// §7 H1) is obtained by (1) compiling the whole library with --fmad=false and
+// (2) spelling every parity-critical operation with the correctly rounded
+// intrinsics (__dadd_rn, __dsub_rn, __dmul_rn, __ddiv_rn, __dsqrt_rn) in the
+// reference's operation order.  Comparisons mirror the reference's exact
+// predicates (closed boxes, inclusive cube, std::max/std::min as ternaries).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gmtb {
+
+constexpr int kWarp = 32;
+constexpr double kInf = __builtin_huge_val();
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+
+// Device-resident problem instance (ProblemInstance + ObstacleSet +
+// GoalRegion, problem.hpp:52-57 / space.hpp:28-41).  A POD descriptor that
+// lives in device memory; batched solves read one per query.
+struct DevInstance {
+  int32_t n;          // samples incl. appended init (V)
+  int32_t dim;
+  int32_t num_boxes;
+  int32_t directed;   // 0: in-lists == out-lists
+  int32_t goal_count; // samples.goal_indices.size()
+  int32_t init_index; // built init index (instance_build) or -1
+  double radius;      // graph radius (NeighborGraph::radius)
+  int64_t num_edges;
+  const double* coords;   // [n*dim] row-major
+  const double* box_lo;   // [num_boxes*dim]
+  const double* box_hi;
+  const double* goal_lo;  // [dim]
+  const double* goal_hi;
+  const int64_t* out_ptr;
+  const int32_t* out_col;
+  const double* out_cost;
+  const int64_t* in_ptr;  // == out_* when !directed
+  const int32_t* in_col;
+  const double* in_cost;
+  const int32_t* in_path; // may be null (all exact edges)
+  const int64_t* path_ptr;
+  const double* path_pts;
+};
+
+// Scalars of one PlanResult (planner.hpp:43-51).
+struct ResultScalars {
+  int32_t status;
+  int32_t goal_node;
+  double cost;
+  int64_t iterations;
+  int64_t total_checks;
+  int32_t path_len;
+  int32_t num_stats;
+  int32_t tree_size;
+  int32_t reserved;
+};
+
+// Device outputs of one query; arrays sized n (stats n+1).  Any array
+// pointer may be null: that output is skipped.
+struct DevResult {
+  ResultScalars* scalars;
+  int32_t* path;
+  uint8_t* label;
+  double* tree_cost;
+  int32_t* parent;
+  int64_t* iter_added;
+  int32_t* group_sizes;
+  int32_t* nodes_added;
+  int64_t* checks;
+};
+
+constexpr int32_t kModeGmt = 0;  // gmt_plan (planner.cpp:94-198)
+constexpr int32_t kModeFmt = 1;  // fmt_plan (planner.cpp:200-262)
+
+struct SolveJob {
+  const DevInstance* inst;
+  DevResult res;
+  int32_t init_index;
+  int32_t mode;
+  double lambda;
+  double radius;  // params.radius (validated == graph radius on the host)
+};
+
+// ---- exact geometry (space.cpp) ------------------------------------------
+
+// point_in_cube (space.cpp:40-45)
+__device__ __forceinline__ bool point_in_cube(const double* p, int d) {
+  for (int k = 0; k < d; ++k)
+    if (p[k] < 0.0 || p[k] > 1.0) return false;
+  return true;
+}
+
+// Aabb::contains (space.cpp:11-16) for box b of an AoS box array.
+__device__ __forceinline__ bool box_contains(const double* lo, const double* hi, int d,
+                                             const double* p) {
+  for (int k = 0; k < d; ++k)
+    if (p[k] < lo[k] || p[k] > hi[k]) return false;
+  return true;
+}
+
+// segment_hits_box (space.cpp:60-78): closed slab clipping.  lo/hi are the
+// box's per-axis bounds with stride `st` (SoA in shared memory: st = B).
+__device__ __forceinline__ bool segment_hits_box(const double* a, const double* b, int d,
+                                                 const double* lo, const double* hi, int st) {
+  double tmin = 0.0, tmax = 1.0;
+  for (int k = 0; k < d; ++k) {
+    const double dk = __dsub_rn(b[k], a[k]);
+    const double l = lo[k * st], h = hi[k * st];
+    if (dk == 0.0) {
+      if (a[k] < l || a[k] > h) return false;
+    } else {
+      double t0 = __ddiv_rn(__dsub_rn(l, a[k]), dk);
+      double t1 = __ddiv_rn(__dsub_rn(h, a[k]), dk);
+      if (t0 > t1) {
+        const double t = t0;
+        t0 = t1;
+        t1 = t;
+      }
+      tmin = (tmin < t0) ? t0 : tmin;  // std::max(tmin, t0)
+      tmax = (t1 < tmax) ? t1 : tmax;  // std::min(tmax, t1)
+      if (tmin > tmax) return false;
+    }
+  }
+  return true;
+}
+
+// euclidean_distance (space.cpp:126-133): sequential sum of squares, sqrt.
+__device__ __forceinline__ double euclid_sq_seq(const double* a, const double* b, int d) {
+  double sq = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double t = __dsub_rn(a[k], b[k]);
+    sq = __dadd_rn(sq, __dmul_rn(t, t));
+  }
+  return sq;
+}
+
+// radical inverse (sampling.cpp:21-34): f /= base; r += f * (index % base).
+__device__ __forceinline__ double halton_dev(uint64_t index, uint32_t base) {
+  double f = 1.0, r = 0.0;
+  const double fb = static_cast<double>(base);
+  while (index > 0) {
+    f = __ddiv_rn(f, fb);
+    r = __dadd_rn(r, __dmul_rn(f, static_cast<double>(index % base)));
+    index /= base;
+  }
+  return r;
+}
+
+}  // namespace gmtb

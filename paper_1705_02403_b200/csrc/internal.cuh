@@ -1,0 +1,75 @@
+// internal.cuh -- host-side internals shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "common.cuh"
+#include "gmt_b200.h"
+
+namespace gmtb {
+
+extern thread_local std::string g_last_error;
+int set_error(int code, const std::string& msg);
+int cuda_error(cudaError_t e, const char* what);
+
+// Growable device allocation (never shrinks).
+struct Arena {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  int reserve(size_t bytes);
+  void release();
+};
+
+// Growable pinned host allocation.
+struct HostPinned {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  int reserve(size_t bytes);
+  void release();
+};
+
+}  // namespace gmtb
+
+struct gmt_instance;
+struct gmt_ctx;
+
+namespace gmtb {
+int validate_scene(const gmt_scene* s);
+int push_desc(gmt_ctx* ctx, gmt_instance* inst);
+}  // namespace gmtb
+
+struct gmt_instance {
+  gmtb::Arena mem;       // samples, boxes, goal, graph rows, paths
+  gmtb::Arena desc_mem;  // the device copy of `desc`
+  gmtb::Arena aux;       // device-built instances: goal index list etc.
+  gmtb::DevInstance desc{};
+  int32_t graph_n = 0;
+  const int32_t* goal_idx_dev = nullptr;
+  ~gmt_instance() {
+    mem.release();
+    desc_mem.release();
+    aux.release();
+  }
+};
+
+struct gmt_ctx {
+  int device = 0;
+  int sm_count = 0;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  int cluster = 0;        // single-query cluster size (0 = auto)
+  int threads = 0;        // single-query CTA threads (0 = auto)
+  int batch_threads = 0;  // batched CTA threads (0 = auto)
+  int batch_cluster = 1;  // batched cluster size
+  gmtb::Arena res;        // single-query / host-batch results
+  gmtb::Arena scratch;    // host-batch inputs, offline build scratch
+  gmtb::Arena jobs;       // SolveJob table
+  gmtb::HostPinned pinned;
+  gmtb::HostPinned pinned2;
+  gmtb::HostPinned pinned_jobs;
+  gmt_instance plan_inst; // staging instance of gmt_plan_host
+};

@@ -1,0 +1,31 @@
+// offline.cuh -- internal entry points of the offline phase (sample.cu, graph.cu).
+#pragma once
+
+#include <cstdint>
+
+#include "internal.cuh"
+
+namespace gmtb {
+
+// build_neighbor_graph on device coordinates; the CSR lands in `out`.
+int build_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, int d, double radius, Arena& out,
+                    int64_t* num_edges, int64_t** row_ptr, int32_t** col, double** cost);
+
+// sample_free on the device.  `out` receives coords [(n+1)*dim] (room for
+// append_init), heading [n+1] when with_heading, and the goal index list
+// [n+1]; *goal_count is set.
+struct DevSamples {
+  double* coords = nullptr;
+  double* heading = nullptr;
+  int32_t* goal_idx = nullptr;
+  int32_t goal_count = 0;
+  int32_t n = 0;
+};
+int sample_free_dev(gmt_ctx* ctx, int32_t n, const gmt_scene* scene, const gmt_sample_source* src,
+                    Arena& out, DevSamples* s);
+
+// append_init on device samples (sampling.cpp:144-154).
+int append_init_dev(gmt_ctx* ctx, int dim, DevSamples* s, const double* init, int has_heading,
+                    double heading, const double* goal_lo, const double* goal_hi, int32_t* index);
+
+}  // namespace gmtb

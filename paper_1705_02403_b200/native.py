@@ -1,0 +1,304 @@
+"""ctypes binding of libgmt_b200.so (the C ABI in include/gmt_b200.h).
+
+There is deliberately no fallback: if the shared library is missing this
+module raises at import, and every compute call fails with NoDeviceError
+when no B200 is present.  Build with ``python -m paper_1705_02403_b200.build``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+from .errors import raise_for
+from .graph import Graph
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgmt_b200.so")
+
+_dp = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_u8p = C.POINTER(C.c_uint8)
+_P = C.POINTER
+_vp = C.c_void_p
+
+# (name, restype, argtypes) for every symbol the header declares.
+SIGNATURES = [
+    ("gmt_last_error", C.c_char_p, []),
+    ("gmt_abi_version", C.c_int, []),
+    ("gmt_ctx_create", C.c_int, [C.c_int, _P(_vp)]),
+    ("gmt_ctx_destroy", None, [_vp]),
+    ("gmt_ctx_stream", _vp, [_vp]),
+    ("gmt_ctx_synchronize", C.c_int, [_vp]),
+    ("gmt_launch_count", C.c_int64, [_vp]),
+    ("gmt_ctx_set_option", C.c_int, [_vp, C.c_int, C.c_int64]),
+    ("gmt_unit_ball_volume", C.c_int, [C.c_int32, _dp]),
+    ("gmt_connection_radius", C.c_int, [C.c_int32, C.c_int64, C.c_double, C.c_double, _dp]),
+    ("gmt_sample_free", C.c_int, [_vp, C.c_int32, _P(abi.Scene), _P(abi.SampleSource), _dp, _dp,
+                                  _i32p, _i32p]),
+    ("gmt_append_init", C.c_int, [_vp, C.c_int32, _dp, _dp, _i32p, _dp, C.c_int32, C.c_double,
+                                  _dp, _dp, _i32p, _i32p, _i32p]),
+    ("gmt_build_neighbor_graph", C.c_int, [_vp, _dp, C.c_int32, C.c_int32, C.c_double, _i64p,
+                                           _i64p, _i32p, _dp]),
+    ("gmt_instance_upload", C.c_int, [_vp, _P(abi.Scene), _dp, C.c_int32, C.c_int32,
+                                      _P(abi.GraphView), _P(_vp)]),
+    ("gmt_instance_build", C.c_int, [_vp, _P(abi.Problem), _P(_vp)]),
+    ("gmt_instance_info", C.c_int, [_vp, _i32p, _i32p, _i32p, _dp, _i64p, _i32p]),
+    ("gmt_instance_download", C.c_int, [_vp, _vp, _dp, _i32p, _i64p, _i32p, _dp]),
+    ("gmt_instance_destroy", None, [_vp]),
+    ("gmt_plan", C.c_int, [_vp, _vp, C.c_int32, C.c_double, C.c_double, _P(abi.PlanOut)]),
+    ("gmt_plan_host", C.c_int, [_vp, _P(abi.Scene), _dp, C.c_int32, C.c_int32, _P(abi.GraphView),
+                                C.c_int32, C.c_double, C.c_double, _P(abi.PlanOut)]),
+    ("gmt_fmt_plan", C.c_int, [_vp, _vp, C.c_int32, _P(abi.PlanOut)]),
+    ("gmt_batch_create", C.c_int, [_vp, C.c_int32, _P(_vp), _i32p, C.c_double, _P(_vp)]),
+    ("gmt_batch_launch", C.c_int, [_vp, _vp]),
+    ("gmt_batch_summaries", C.c_int, [_vp, _vp, _P(abi.PlanSummary)]),
+    ("gmt_batch_result", C.c_int, [_vp, _vp, C.c_int32, _P(abi.PlanOut)]),
+    ("gmt_batch_destroy", None, [_vp]),
+    ("gmt_plan_batch_host", C.c_int, [_vp, _vp, C.c_double, _P(abi.PlanSummary), _i32p, _u8p, _dp,
+                                      _i32p, _i64p]),
+    ("gmt_host_alloc", C.c_int, [C.c_size_t, _P(_vp)]),
+    ("gmt_host_free", None, [_vp]),
+]
+
+OPT_CLUSTER = 1
+OPT_THREADS = 2
+OPT_BATCH_THREADS = 3
+OPT_BATCH_CLUSTER = 4
+
+
+def load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_1705_02403_b200.build` "
+                          "(the B200 library has no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib: C.CDLL | None = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        _lib = load()
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise_for(rc, lib().gmt_last_error().decode())
+
+
+class Instance:
+    """A device-resident ProblemInstance (problem.hpp:52-57)."""
+
+    def __init__(self, ctx: "Context", handle: C.c_void_p, spec=None):
+        self.ctx = ctx
+        self.h = handle
+        self.spec = spec
+        n, d, ii, gc = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        r = C.c_double()
+        ne = C.c_int64()
+        check(lib().gmt_instance_info(self.h, C.byref(n), C.byref(d), C.byref(ii), C.byref(r),
+                                      C.byref(ne), C.byref(gc)))
+        self.n, self.dim, self.init_index = n.value, d.value, ii.value
+        self.radius, self.num_edges, self.goal_count = r.value, ne.value, gc.value
+
+    def download(self, goal: bool = True):
+        """-> (coords [n, dim], goal_idx, Graph)"""
+        coords = np.zeros(self.n * self.dim)
+        gidx = np.zeros(max(self.goal_count, 1), np.int32)
+        ptr = np.zeros(self.n + 1, np.int64)
+        col = np.zeros(max(self.num_edges, 1), np.int32)
+        cost = np.zeros(max(self.num_edges, 1))
+        check(lib().gmt_instance_download(
+            self.ctx.h, self.h, abi.ptr(coords, C.c_double),
+            abi.ptr(gidx if goal else None, C.c_int32), abi.ptr(ptr, C.c_int64),
+            abi.ptr(col, C.c_int32), abi.ptr(cost, C.c_double)))
+        g = Graph(self.n, self.radius, ptr, col[: self.num_edges], cost[: self.num_edges],
+                  dim=self.dim)
+        return coords.reshape(self.n, self.dim), gidx[: self.goal_count], g
+
+    def close(self):
+        if self.h:
+            lib().gmt_instance_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Batch:
+    def __init__(self, ctx: "Context", handle, count: int, sizes):
+        self.ctx, self.h, self.count, self.sizes = ctx, handle, count, sizes
+
+    def launch(self):
+        check(lib().gmt_batch_launch(self.ctx.h, self.h))
+
+    def summaries(self):
+        out = (abi.PlanSummary * self.count)()
+        check(lib().gmt_batch_summaries(self.ctx.h, self.h, out))
+        return list(out)
+
+    def result(self, q: int) -> abi.PlanResultPy:
+        buf = abi.PlanBuffers(self.sizes[q])
+        check(lib().gmt_batch_result(self.ctx.h, self.h, q, C.byref(buf.out)))
+        return buf.result()
+
+    def close(self):
+        if self.h:
+            lib().gmt_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Context:
+    """gmt_ctx: one device, one stream."""
+
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        check(lib().gmt_ctx_create(device, C.byref(self.h)))
+        self.device = device
+
+    @property
+    def stream(self) -> int:
+        return lib().gmt_ctx_stream(self.h) or 0
+
+    @property
+    def launch_count(self) -> int:
+        return lib().gmt_launch_count(self.h)
+
+    def set_option(self, opt: int, value: int):
+        check(lib().gmt_ctx_set_option(self.h, opt, value))
+
+    def synchronize(self):
+        check(lib().gmt_ctx_synchronize(self.h))
+
+    def close(self):
+        if self.h:
+            lib().gmt_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- offline phase ---------------------------------------------------
+    @staticmethod
+    def connection_radius(dim: int, n: int, eta: float = 0.0, mu: float = 1.0) -> float:
+        out = C.c_double()
+        check(lib().gmt_connection_radius(dim, n, eta, mu, C.byref(out)))
+        return out.value
+
+    @staticmethod
+    def unit_ball_volume(d: int) -> float:
+        out = C.c_double()
+        check(lib().gmt_unit_ball_volume(d, C.byref(out)))
+        return out.value
+
+    def sample_free(self, spec, n: int | None = None):
+        n = spec.n if n is None else n
+        coords = np.zeros(n * spec.dim)
+        gidx = np.zeros(n + 1, np.int32)
+        gc = C.c_int32()
+        sc, src = spec.scene(), spec.source()
+        check(lib().gmt_sample_free(self.h, n, C.byref(sc), C.byref(src), abi.ptr(coords, C.c_double),
+                                    abi.ptr(None, C.c_double), abi.ptr(gidx, C.c_int32),
+                                    C.byref(gc)))
+        return coords.reshape(n, spec.dim), gidx[: gc.value].copy()
+
+    def append_init(self, coords, goal_idx, init, goal_lo, goal_hi):
+        n0, dim = coords.shape
+        buf = np.zeros((n0 + 1) * dim)
+        buf[: n0 * dim] = coords.reshape(-1)
+        g = np.zeros(n0 + 2, np.int32)
+        g[: len(goal_idx)] = goal_idx
+        n = C.c_int32(n0)
+        gc = C.c_int32(len(goal_idx))
+        idx = C.c_int32()
+        init, gl, gh = abi.f64(init), abi.f64(goal_lo), abi.f64(goal_hi)
+        check(lib().gmt_append_init(self.h, dim, abi.ptr(buf, C.c_double), abi.ptr(None, C.c_double),
+                                    C.byref(n), abi.ptr(init, C.c_double), 0, 0.0,
+                                    abi.ptr(gl, C.c_double), abi.ptr(gh, C.c_double),
+                                    abi.ptr(g, C.c_int32), C.byref(gc), C.byref(idx)))
+        return buf[: n.value * dim].reshape(n.value, dim), g[: gc.value].copy(), idx.value
+
+    def build_neighbor_graph(self, coords, radius: float) -> Graph:
+        coords = abi.f64(coords)
+        n, dim = coords.shape
+        ne = C.c_int64()
+        check(lib().gmt_build_neighbor_graph(self.h, abi.ptr(coords, C.c_double), n, dim, radius,
+                                             C.byref(ne), abi.ptr(None, C.c_int64),
+                                             abi.ptr(None, C.c_int32), abi.ptr(None, C.c_double)))
+        ptr = np.zeros(n + 1, np.int64)
+        col = np.zeros(max(ne.value, 1), np.int32)
+        cost = np.zeros(max(ne.value, 1))
+        check(lib().gmt_build_neighbor_graph(self.h, abi.ptr(coords, C.c_double), n, dim, radius,
+                                             C.byref(ne), abi.ptr(ptr, C.c_int64),
+                                             abi.ptr(col, C.c_int32), abi.ptr(cost, C.c_double)))
+        return Graph(n, radius, ptr, col[: ne.value], cost[: ne.value], dim=dim)
+
+    def build_instance(self, spec) -> Instance:
+        h = C.c_void_p()
+        p = spec.flat()
+        check(lib().gmt_instance_build(self.h, C.byref(p), C.byref(h)))
+        return Instance(self, h, spec)
+
+    def upload(self, spec, coords, goal_count: int, graph: Graph) -> Instance:
+        coords = abi.f64(coords)
+        h = C.c_void_p()
+        sc = spec.scene()
+        gv = graph.view()
+        check(lib().gmt_instance_upload(self.h, C.byref(sc), abi.ptr(coords, C.c_double),
+                                        coords.shape[0], goal_count, C.byref(gv), C.byref(h)))
+        return Instance(self, h, spec)
+
+    # ---- online phase ----------------------------------------------------
+    def plan(self, inst: Instance, init_index: int | None = None, lam: float = 1.0,
+             radius: float | None = None) -> abi.PlanResultPy:
+        buf = abi.PlanBuffers(inst.n)
+        ii = inst.init_index if init_index is None else init_index
+        r = inst.radius if radius is None else radius
+        check(lib().gmt_plan(self.h, inst.h, ii, lam, r, C.byref(buf.out)))
+        return buf.result()
+
+    def fmt_plan(self, inst: Instance, init_index: int | None = None) -> abi.PlanResultPy:
+        buf = abi.PlanBuffers(inst.n)
+        ii = inst.init_index if init_index is None else init_index
+        check(lib().gmt_fmt_plan(self.h, inst.h, ii, C.byref(buf.out)))
+        return buf.result()
+
+    def plan_host(self, spec, coords, goal_count, graph: Graph, init_index, lam, radius):
+        coords = abi.f64(coords)
+        buf = abi.PlanBuffers(coords.shape[0])
+        sc = spec.scene()
+        gv = graph.view()
+        check(lib().gmt_plan_host(self.h, C.byref(sc), abi.ptr(coords, C.c_double), coords.shape[0],
+                                  goal_count, C.byref(gv), init_index, lam, radius,
+                                  C.byref(buf.out)))
+        return buf.result()
+
+    def batch(self, instances, lam: float = 1.0, init_index=None) -> Batch:
+        arr = (C.c_void_p * len(instances))(*[i.h.value for i in instances])
+        ii = None if init_index is None else abi.i32(init_index)
+        h = C.c_void_p()
+        check(lib().gmt_batch_create(self.h, len(instances), arr, abi.ptr(ii, C.c_int32), lam,
+                                     C.byref(h)))
+        return Batch(self, h, len(instances), [i.n for i in instances])

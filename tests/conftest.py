@@ -1,0 +1,36 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+SCENES = os.path.join(ROOT, "scenes")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA library)")
+
+
+@pytest.fixture(scope="session")
+def port():
+    import oracle
+    return oracle.port()
+
+
+@pytest.fixture(scope="session")
+def ref():
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref (compiled reference) not built")
+    return oracle.ref()
+
+
+@pytest.fixture(scope="session")
+def ctx():
+    from paper_1705_02403_b200 import native
+    c = native.Context(0)
+    yield c
+    c.close()
