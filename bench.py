@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""GMT* benchmark (BASELINE.json metric: p50 ms per GMT* solve at n samples;
+batched plans/sec at 1/2/4/8 B200).
+
+One JSON line on rank 0.
+
+Workload (BASELINE.json configs[1]): 3D forest of 60 AABB pillars, n=4000
+Halton samples, Euclidean cost, formula radius, lambda=1.  A step is one
+launch that solves a batch of `--queries` independent queries per GPU (each
+query its own forest/start/goal drawn from Pcg32(mix64(master, q)); scenes,
+samples and graphs are built on the GPU before timing and stay resident in
+HBM: 512 queries x ~6.5 MB of CSR = 3.3 GB per GPU, far above the 126 MB L2,
+so no step reads a graph another step left in L2).
+
+  value      plans/s over all ranks, device-resident inputs (CUDA events on
+             the library stream, max over ranks)
+  e2e        the same metric through the C ABI drop-in gmt_plan_batch_host:
+             host-resident (pinned) samples + CSR graphs copied H2D, solved,
+             summaries + paths + full trees copied D2H inside the timed region
+  p50        single-query latency of the canonical C2 instance (Pcg32(3)
+             forest) on a cluster of CTAs, p50 over --single-reps launches
+  roofline   HBM roofline of the solve kernel with SURVEY.md §8(d)'s
+             algorithmic bytes 12*InScan + 4*OutScan + 8*OpenParentReads +
+             9*V*Passes counted on the device
+  cpu_baseline  the unmodified reference gmt_plan (oracle/_ref) on the
+             host cores over a bounded sample of the same queries
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GMT* plans/sec (batched queries); p50 ms per single solve"
+UNIT = "plans/s"
+MASTER_SEED = 20171005
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--queries", type=int, default=512, help="queries per GPU per step")
+    ap.add_argument("--n", type=int, default=4000)
+    ap.add_argument("--single-reps", type=int, default=101)
+    ap.add_argument("--cpu-sample", type=int, default=64, help="queries in the CPU baseline sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def query_specs(rank: int, per_gpu: int, n: int):
+    from paper_1705_02403_b200 import problem as P
+    return [P.random_forest_query(MASTER_SEED, rank * per_gpu + j, n=n) for j in range(per_gpu)]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------
+def cpu_reference_leg(specs, lam: float, threads: int, reps: int):
+    """The unmodified reference gmt_plan (oracle/_ref) over a sample of the
+    same queries, one query per worker (simulator.cpp:212 pattern)."""
+    import oracle
+    R = oracle.ref()
+    insts = R.instance_build_many(specs, threads)
+    R.plan_many(insts, lam, threads)  # warm caches
+    best = None
+    secs = []
+    for _ in range(reps):
+        _, s = R.plan_many(insts, lam, threads)
+        secs.append(s)
+    sec = statistics.median(secs)
+    best = len(insts) / sec
+    # single-thread p50 of the first query (the CLI's plan_ms, gmtplan.cpp:144-152)
+    t1 = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        insts[0].plan(lam)
+        t1.append(time.perf_counter() - t0)
+    return best, statistics.median(t1) * 1e3, len(insts)
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libgmtref.so not built"}))
+        return
+    threads = os.cpu_count() or 1
+    sample = min(args.cpu_sample, args.queries)
+    specs = query_specs(0, sample, args.n)
+    R = oracle.ref()
+    insts = R.instance_build_many(specs, threads)
+    for _ in range(args.warmup):
+        R.plan_many(insts, 1.0, threads)
+    secs = []
+    for _ in range(args.steps):
+        _, s = R.plan_many(insts, 1.0, threads)
+        secs.append(s)
+    total = sum(secs)
+    value = len(insts) * args.steps / total
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "forest3d_n4000_batched", "n": args.n, "dim": 3, "boxes": 60,
+                   "lambda": 1.0, "queries_per_step": len(insts)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{len(insts)} queries of the workload per step, "
+                                   f"gmt_plan(workers=1) per query under parallel_chunks({threads})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+def run_b200(args):
+    import numpy as np
+    import torch
+
+    from paper_1705_02403_b200 import abi, problem as P
+    from paper_1705_02403_b200 import native
+    from paper_1705_02403_b200.native import (OPT_BATCH_CLUSTER, OPT_BATCH_THREADS, OPT_COUNTERS,
+                                              Context, PackedBatch, plan_batch_host)
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- setup: build every query's instance on the GPU -------------------
+    Q = args.queries
+    specs = query_specs(rank, Q, args.n)
+    insts = [ctx.build_instance(s) for s in specs]
+    batch = ctx.batch(insts, 1.0)
+
+    # instrumented launch (untimed): algorithmic traffic of one step
+    ctx.set_option(OPT_COUNTERS, 1)
+    ctx.counters(reset=True)
+    cbatch = ctx.batch(insts, 1.0)
+    cbatch.launch()
+    cnt = ctx.counters(reset=True)
+    ctx.set_option(OPT_COUNTERS, 0)
+    sums = cbatch.summaries()
+    cbatch.close()
+    passes = sum(s.num_stats for s in sums)
+    Vpasses = sum(s.num_stats * i.n for s, i in zip(sums, insts))
+    b_alg = 12 * cnt["in_scan"] + 4 * cnt["out_scan"] + 8 * cnt["open_parent_reads"] + 9 * Vpasses
+    ok = sum(1 for s in sums if s.status == abi.PLAN_SUCCESS)
+
+    # ---- device-resident timed loop ---------------------------------------
+    for _ in range(args.warmup):
+        batch.launch()
+    barrier_sync()
+    launches0 = ctx.launch_count
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for k in range(args.steps):
+                batch.launch()
+                ev[k + 1].record(stream)
+        barrier_sync()
+    launches = ctx.launch_count - launches0
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    total_ms = max_over_ranks(sum(step_ms))
+    value = world * Q * args.steps / (total_ms / 1e3)
+    kernel_ms = statistics.mean(step_ms)  # one solve launch per step
+    peak, peak_kind = measured_peak_hbm()
+    achieved = b_alg / (kernel_ms / 1e3) / 1e9
+    clocks = clk.summary()
+
+    # ---- e2e through the C-ABI drop-in with host buffers ------------------
+    entries = []
+    for s, inst in zip(specs, insts):
+        coords, gidx, g = inst.download()
+        entries.append((s, coords, len(gidx), g, inst.init_index))
+    pb = PackedBatch(entries, want_tree=True)
+    for _ in range(max(1, args.warmup)):
+        plan_batch_host(ctx, pb, 1.0)
+    e2e_steps = max(3, min(args.steps, 10))
+    barrier_sync()
+    t = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        plan_batch_host(ctx, pb, 1.0)  # synchronous: returns with results on the host
+        t.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(sum(t))
+    e2e_value = world * Q * e2e_steps / e2e_s
+    # parity spot check of the e2e results against the device-resident ones
+    dev0 = batch.summaries()
+    mism = sum(1 for a, b in zip(dev0, pb.summaries) if (a.status, a.cost, a.iterations) !=
+               (b.status, b.cost, b.iterations))
+    if mism:
+        raise SystemExit(f"e2e results differ from device-resident results in {mism} queries")
+
+    # ---- single-query latency (configs[1] canonical instance) -------------
+    c2 = ctx.build_instance(P.forest_3d(3, args.n))
+    single = {}
+    for cs in (8, 16):
+        ctx.set_option(OPT_BATCH_CLUSTER, cs)
+        ctx.set_option(OPT_BATCH_THREADS, 0)
+        b1 = ctx.batch([c2], 1.0)
+        ctx.set_option(OPT_BATCH_CLUSTER, 1)
+        for _ in range(5):
+            b1.launch()
+        ctx.synchronize()
+        times = []
+        with torch.cuda.stream(stream):
+            for _ in range(args.single_reps):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                b1.launch()
+                e1.record(stream)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+        single[f"cluster{cs}"] = statistics.median(times)
+        b1.close()
+    p50 = min(single.values())
+
+    # ---- gather: one record per query to rank 0 (the only collective) -----
+    recs = np.array([[s.status, s.cost, s.iterations, s.total_collision_checks] for s in dev0],
+                    np.float64)
+    if world > 1:
+        t_local = torch.from_numpy(recs).cuda()
+        gathered = [torch.empty_like(t_local) for _ in range(world)]
+        torch.distributed.all_gather(gathered, t_local)
+        recs = torch.cat(gathered).cpu().numpy()
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            try:
+                import oracle
+                if oracle.ref_available():
+                    threads = os.cpu_count() or 1
+                    sample = min(args.cpu_sample, Q)
+                    val, st_ms, nq = cpu_reference_leg(specs[:sample], 1.0, threads, 3)
+                    cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
+                           "sample": f"{nq} of the step's queries, median of 3 passes, "
+                                     f"gmt_plan(workers=1) per query on {threads} threads; "
+                                     f"single-thread p50 of query 0 = {st_ms:.2f} ms"}
+            except Exception as e:  # the baseline must never break the bench line
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                       "sample": f"failed: {e}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "forest3d_n4000_batched", "n": args.n, "dim": 3, "boxes": 60,
+                       "lambda": 1.0, "queries_per_gpu_per_step": Q, "parallelism": f"dp{world}",
+                       "l2": "inputs larger than L2 (per-GPU resident graphs ~%.1f GB)" %
+                             (sum(i.num_edges for i in insts) * 12 / 1e9),
+                       "solved": f"{int((recs[:, 0] == 0).sum())}/{len(recs)} success"},
+            "p50_ms_single_solve": p50,
+            "single_solve_ms": single,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": pb.h2d_bytes,
+                    "d2h_bytes_per_step": pb.d2h_bytes},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "gmt_solve_kernel<1>",
+                         "bytes_per_launch": b_alg, "kernel_ms": kernel_ms,
+                         "counts": {**cnt, "passes": passes, "V_passes": Vpasses}},
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return line
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -177,14 +177,21 @@ int64_t gmt_launch_count(const gmt_ctx* ctx); /* kernels launched so far */
 /* GMT_OPT_CLUSTER: CTAs cooperating on one single-query solve (1,2,4,8,16; 0 = auto)
  * GMT_OPT_THREADS: threads per CTA for single-query solves (0 = auto)
  * GMT_OPT_BATCH_THREADS: threads per CTA for batched solves (0 = auto)
- * GMT_OPT_BATCH_CLUSTER: CTAs per query in batched solves (default 1)    */
+ * GMT_OPT_BATCH_CLUSTER: CTAs per query in batched solves (default 1)
+ * GMT_OPT_COUNTERS: 1 = solves launched from now on add their traffic
+ *                   counts to the context counters (gmt_ctx_counters)      */
 enum {
   GMT_OPT_CLUSTER = 1,
   GMT_OPT_THREADS = 2,
   GMT_OPT_BATCH_THREADS = 3,
-  GMT_OPT_BATCH_CLUSTER = 4
+  GMT_OPT_BATCH_CLUSTER = 4,
+  GMT_OPT_COUNTERS = 5
 };
 int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value);
+/* Traffic counters summed over counted solves: out[0] in-row edges read
+ * (P5), out[1] out-row edges read (P4), out[2] in-edges whose source was
+ * open (cost[y] gathers).  Synchronizes; reset != 0 zeroes them.          */
+int gmt_ctx_counters(gmt_ctx* ctx, int64_t* out, int32_t reset);
 
 /* ---- offline phase ---------------------------------------------------- */
 /* unit_ball_volume, connection_radius (graph.cpp:14-32); host scalars. */

@@ -125,6 +125,27 @@ class Problem(C.Structure):
     ]
 
 
+class BatchHost(C.Structure):
+    _fields_ = [
+        ("count", C.c_int32),
+        ("dim", C.c_int32),
+        ("node_off", _i64p),
+        ("edge_off", _i64p),
+        ("box_off", _i32p),
+        ("coords", _dp),
+        ("box_lo", _dp),
+        ("box_hi", _dp),
+        ("goal_lo", _dp),
+        ("goal_hi", _dp),
+        ("row_ptr", _i64p),
+        ("col", _i32p),
+        ("cost", _dp),
+        ("goal_count", _i32p),
+        ("init_index", _i32p),
+        ("radius", _dp),
+    ]
+
+
 def ptr(a: np.ndarray | None, ctype):
     """Pointer to a contiguous numpy array (or NULL)."""
     if a is None:

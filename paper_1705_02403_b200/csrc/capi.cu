@@ -126,6 +126,12 @@ extern "C" int gmt_ctx_create(int device, gmt_ctx** out) {
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
   ctx->smem_optin = prop.sharedMemPerBlockOptin;
+  e = cudaMalloc(&ctx->counters, sizeof(int64_t) * 4);
+  if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, sizeof(int64_t) * 4);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return cuda_error(e, "counters");
+  }
   e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete ctx;
@@ -145,6 +151,7 @@ extern "C" void gmt_ctx_destroy(gmt_ctx* ctx) {
   ctx->pinned.release();
   ctx->pinned2.release();
   ctx->pinned_jobs.release();
+  cudaFree(ctx->counters);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -174,6 +181,9 @@ extern "C" int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value) {
       (option == GMT_OPT_THREADS ? ctx->threads : ctx->batch_threads) = static_cast<int>(value);
       return GMT_OK;
     }
+    case GMT_OPT_COUNTERS:
+      ctx->counting = value ? 1 : 0;
+      return GMT_OK;
     case GMT_OPT_BATCH_CLUSTER:
       if (value != 1 && value != 2 && value != 4 && value != 8 && value != 16)
         return set_error(GMT_E_INVALID_INPUT, "batch cluster size must be 1, 2, 4, 8 or 16");
@@ -182,6 +192,13 @@ extern "C" int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value) {
     default:
       return set_error(GMT_E_INVALID_INPUT, "unknown option");
   }
+}
+
+extern "C" int gmt_ctx_counters(gmt_ctx* ctx, int64_t* out, int32_t reset) {
+  GMT_CUDA(cudaStreamSynchronize(ctx->stream));
+  GMT_CUDA(cudaMemcpy(out, ctx->counters, sizeof(int64_t) * 3, cudaMemcpyDeviceToHost));
+  if (reset) GMT_CUDA(cudaMemset(ctx->counters, 0, sizeof(int64_t) * 4));
+  return GMT_OK;
 }
 
 extern "C" int gmt_host_alloc(size_t bytes, void** out) {
@@ -428,7 +445,7 @@ int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, size_t* smem, int*
 
 // Result buffers for `count` queries of up to `n` nodes each.
 int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, bool stats,
-                  std::vector<DevResult>& out, ResultScalars** scalars_base) {
+                  std::vector<DevResult>& out, ResultScalars** scalars_base, int64_t* counters) {
   const int64_t total = node_off[count];
   Carver c;
   const size_t o_sc = c.take<ResultScalars>(count);
@@ -460,6 +477,7 @@ int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, b
     r.group_sizes = stats ? at<int32_t>(b, o_gs) + o + q : nullptr;
     r.nodes_added = stats ? at<int32_t>(b, o_na) + o + q : nullptr;
     r.checks = stats ? at<int64_t>(b, o_ck) + o + q : nullptr;
+    r.counters = counters;
   }
   *scalars_base = at<ResultScalars>(b, o_sc);
   return GMT_OK;
@@ -525,7 +543,8 @@ int plan_on(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, double l
   int64_t node_off[2] = {0, D.n};
   std::vector<DevResult> res;
   ResultScalars* sc;
-  GMT_TRY(carve_results(ctx->res, 1, node_off, true, true, res, &sc));
+  GMT_TRY(carve_results(ctx->res, 1, node_off, true, true, res, &sc,
+                        ctx->counting ? ctx->counters : nullptr));
   SolveJob job{};
   job.inst = static_cast<const DevInstance*>(inst->desc_mem.ptr);
   job.res = res[0];
@@ -534,7 +553,8 @@ int plan_on(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, double l
   job.lambda = lambda;
   job.radius = radius;
   const int cluster = ctx->cluster ? ctx->cluster : 8;
-  const int threads = ctx->threads ? ctx->threads : 512;
+  int threads = ctx->threads ? ctx->threads : 512;
+  if (cluster == 1 && threads > 256) threads = 256;  // batched-shape kernel bound
   GMT_TRY(launch_jobs(ctx, {job}, cluster, threads, smem, obs));
   return download_result(ctx, res[0], D.n, out);
 }
@@ -611,7 +631,9 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
     max_nb = std::max(max_nb, inst->desc.num_boxes);
   }
   int rc = plan_smem(ctx, max_n, max_d, max_nb, &b->smem, &b->obs);
-  if (rc == GMT_OK) rc = carve_results(b->res, count, b->node_off.data(), true, true, b->results, &b->scalars);
+  if (rc == GMT_OK)
+    rc = carve_results(b->res, count, b->node_off.data(), true, true, b->results, &b->scalars,
+                       ctx->counting ? ctx->counters : nullptr);
   if (rc != GMT_OK) {
     delete b;
     return rc;
@@ -734,7 +756,8 @@ extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double
   const bool tree = label || tree_cost || parent || iteration_added;
   std::vector<DevResult> res;
   ResultScalars* sc_dev;
-  GMT_TRY(carve_results(ctx->res, count, B->node_off, tree, false, res, &sc_dev));
+  GMT_TRY(carve_results(ctx->res, count, B->node_off, tree, false, res, &sc_dev,
+                        ctx->counting ? ctx->counters : nullptr));
 
   std::vector<DevInstance> descs(count);
   std::vector<SolveJob> jobs(count);

@@ -71,6 +71,7 @@ struct DevResult {
   int32_t* group_sizes;
   int32_t* nodes_added;
   int64_t* checks;
+  int64_t* counters;  // optional [3]: in-row edges, out-row edges, open in-edges
 };
 
 constexpr int32_t kModeGmt = 0;  // gmt_plan (planner.cpp:94-198)

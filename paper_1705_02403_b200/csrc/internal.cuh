@@ -65,6 +65,8 @@ struct gmt_ctx {
   int threads = 0;        // single-query CTA threads (0 = auto)
   int batch_threads = 0;  // batched CTA threads (0 = auto)
   int batch_cluster = 1;  // batched cluster size
+  int counting = 0;       // GMT_OPT_COUNTERS
+  int64_t* counters = nullptr;  // device [3]
   gmtb::Arena res;        // single-query / host-batch results
   gmtb::Arena scratch;    // host-batch inputs, offline build scratch
   gmtb::Arena jobs;       // SolveJob table

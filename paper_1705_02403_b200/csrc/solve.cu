@@ -44,6 +44,7 @@ struct CtaShared {
   double red_goal_c[32];
   int32_t red_goal_v[32];
   int32_t group_count;
+  int32_t own_count;  // group members this CTA expands in P4
   int32_t cand_count;
   unsigned long long checks_acc;  // rank 0: cluster-wide checks of this pass
   int32_t added_acc;              // rank 0: cluster-wide additions of this pass
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
   }
   if (tid == 0) {
     sh.group_count = 0;
+    sh.own_count = 0;
     sh.cand_count = 0;
     sh.checks_acc = 0ull;
     sh.added_acc = 0;
@@ -280,6 +282,10 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
   int goal = -1;
   int gsize = 0;
   long long total_checks = 0;
+  // Traffic counters for the roofline's algorithmic bytes:
+  // per-lane counts of out-row edges (P4), in-row edges (P5) and in-edges
+  // whose source was open (the cost[y] gathers).
+  int cnt_out = 0, cnt_in = 0, cnt_open = 0;
 
   for (;;) {
     if (job.mode == kModeFmt) {
@@ -303,7 +309,10 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
       }
       if (tid == 0) {
         group_w[z >> 5] = 1u << (z & 31);
-        list[0] = z;
+        if (((z >> 5) & (CS - 1)) == rank) {
+          list[0] = z;
+          sh.own_count = 1;
+        }
       }
       __syncthreads();
     } else {
@@ -337,14 +346,19 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
       const bool g = ((ow >> lane) & 1u) && cost_s[v] <= thr;
       const uint32_t gb = __ballot_sync(kFull, g);
       if (gb) {
+        // Every CTA sees the whole group; the members of words w = rank
+        // (mod CS) go to this CTA's P4 work list (list order is arbitrary,
+        // ownership is not).
         int base = 0;
+        const bool own = (w & (CS - 1)) == rank;
         if (lane == 0) {
           group_w[w] = gb;
-          base = atomicAdd(&sh.group_count, __popc(gb));
+          atomicAdd(&sh.group_count, __popc(gb));
+          if (own) base = atomicAdd(&sh.own_count, __popc(gb));
         }
         base = __shfl_sync(kFull, base, 0);
         if (g) {
-          list[base + __popc(gb & ((1u << lane) - 1u))] = v;
+          if (own) list[base + __popc(gb & ((1u << lane) - 1u))] = v;
           if ((goal_w[w] >> lane) & 1u) argmin_step(gc, gv, cost_s[v], v);
         }
       }
@@ -359,7 +373,8 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
     }  // GMT group selection
 
     // P4: mark unexplored out-neighbours of the group (planner.cpp:159-166).
-    for (int k = rank * nw + warp; k < gsize; k += CS * nw) {
+    const int own = sh.own_count;
+    for (int k = warp; k < own; k += nw) {
       const int g = list[k];
       const int64_t e0 = I.out_ptr[g], e1 = I.out_ptr[g + 1];
       for (int64_t base = e0; base < e1; base += kWarp) {
@@ -367,6 +382,7 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
         bool un = false;
         int x = 0;
         if (e < e1) {
+          ++cnt_out;
           x = __ldg(I.out_col + e);
           un = !(((open_w[x >> 5] | closed_w[x >> 5]) >> (x & 31)) & 1u);
         }
@@ -409,7 +425,9 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
       int by = -1;
       for (int64_t e = e0 + lane; e < e1; e += kWarp) {
         const int y = __ldg(I.in_col + e);
+        ++cnt_in;
         if ((open_w[y >> 5] >> (y & 31)) & 1u) {
+          ++cnt_open;
           const double c = __dadd_rn(cost_s[y], __ldg(I.in_cost + e));
           if (c < bv) {
             bv = c;
@@ -469,6 +487,7 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
     }
     if (tid == 0) {
       sh.group_count = 0;
+      sh.own_count = 0;
       sh.cand_count = 0;
     }
     __syncthreads();
@@ -476,6 +495,19 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
     ++pass;
   }
 
+  if (R.counters) {
+    long long a = cnt_in, b = cnt_out, c = cnt_open;
+    for (int o = 16; o; o >>= 1) {
+      a += __shfl_xor_sync(kFull, a, o);
+      b += __shfl_xor_sync(kFull, b, o);
+      c += __shfl_xor_sync(kFull, c, o);
+    }
+    if (lane == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(R.counters + 0), static_cast<unsigned long long>(a));
+      atomicAdd(reinterpret_cast<unsigned long long*>(R.counters + 1), static_cast<unsigned long long>(b));
+      atomicAdd(reinterpret_cast<unsigned long long*>(R.counters + 2), static_cast<unsigned long long>(c));
+    }
+  }
   if (rank != 0) return;
   // Outputs (rank 0 holds the parent replica).
   if (R.label) {

@@ -34,6 +34,7 @@ SIGNATURES = [
     ("gmt_ctx_synchronize", C.c_int, [_vp]),
     ("gmt_launch_count", C.c_int64, [_vp]),
     ("gmt_ctx_set_option", C.c_int, [_vp, C.c_int, C.c_int64]),
+    ("gmt_ctx_counters", C.c_int, [_vp, _i64p, C.c_int32]),
     ("gmt_unit_ball_volume", C.c_int, [C.c_int32, _dp]),
     ("gmt_connection_radius", C.c_int, [C.c_int32, C.c_int64, C.c_double, C.c_double, _dp]),
     ("gmt_sample_free", C.c_int, [_vp, C.c_int32, _P(abi.Scene), _P(abi.SampleSource), _dp, _dp,
@@ -57,8 +58,8 @@ SIGNATURES = [
     ("gmt_batch_summaries", C.c_int, [_vp, _vp, _P(abi.PlanSummary)]),
     ("gmt_batch_result", C.c_int, [_vp, _vp, C.c_int32, _P(abi.PlanOut)]),
     ("gmt_batch_destroy", None, [_vp]),
-    ("gmt_plan_batch_host", C.c_int, [_vp, _vp, C.c_double, _P(abi.PlanSummary), _i32p, _u8p, _dp,
-                                      _i32p, _i64p]),
+    ("gmt_plan_batch_host", C.c_int, [_vp, _P(abi.BatchHost), C.c_double, _P(abi.PlanSummary),
+                                      _i32p, _u8p, _dp, _i32p, _i64p]),
     ("gmt_host_alloc", C.c_int, [C.c_size_t, _P(_vp)]),
     ("gmt_host_free", None, [_vp]),
 ]
@@ -67,6 +68,7 @@ OPT_CLUSTER = 1
 OPT_THREADS = 2
 OPT_BATCH_THREADS = 3
 OPT_BATCH_CLUSTER = 4
+OPT_COUNTERS = 5
 
 
 def load() -> C.CDLL:
@@ -189,6 +191,12 @@ class Context:
     def synchronize(self):
         check(lib().gmt_ctx_synchronize(self.h))
 
+    def counters(self, reset: bool = False) -> dict:
+        """Traffic counts of the solves launched while OPT_COUNTERS was on."""
+        out = np.zeros(3, np.int64)
+        check(lib().gmt_ctx_counters(self.h, abi.ptr(out, C.c_int64), 1 if reset else 0))
+        return {"in_scan": int(out[0]), "out_scan": int(out[1]), "open_parent_reads": int(out[2])}
+
     def close(self):
         if self.h:
             lib().gmt_ctx_destroy(self.h)
@@ -302,3 +310,121 @@ class Context:
         check(lib().gmt_batch_create(self.h, len(instances), arr, abi.ptr(ii, C.c_int32), lam,
                                      C.byref(h)))
         return Batch(self, h, len(instances), [i.n for i in instances])
+
+
+class PinnedArray:
+    """A numpy view of page-locked host memory from gmt_host_alloc."""
+
+    def __init__(self, count: int, dtype):
+        self.dtype = np.dtype(dtype)
+        nbytes = max(int(count), 1) * self.dtype.itemsize
+        self.p = C.c_void_p()
+        check(lib().gmt_host_alloc(nbytes, C.byref(self.p)))
+        buf = (C.c_char * nbytes).from_address(self.p.value)
+        self.a = np.frombuffer(buf, dtype=self.dtype, count=max(int(count), 1))[: int(count)]
+
+    def __del__(self):
+        try:
+            if self.p:
+                lib().gmt_host_free(self.p)
+                self.p = None
+        except Exception:
+            pass
+
+
+class PackedBatch:
+    """Independent Euclidean queries packed back to back in pinned host
+    memory: the gmt_batch_host layout of include/gmt_b200.h.  `entries` are
+    (spec, coords [n,d], goal_count, Graph, init_index) tuples."""
+
+    def __init__(self, entries, want_tree: bool = True):
+        self.count = len(entries)
+        d = entries[0][0].dim
+        ns = [e[1].shape[0] for e in entries]
+        es = [e[3].num_edges for e in entries]
+        bs = [e[0].num_boxes for e in entries]
+        tn, te, tb = sum(ns), sum(es), sum(bs)
+        A = PinnedArray
+        self.node_off = A(self.count + 1, np.int64)
+        self.edge_off = A(self.count + 1, np.int64)
+        self.box_off = A(self.count + 1, np.int32)
+        self.coords = A(tn * d, np.float64)
+        self.box_lo = A(tb * d, np.float64)
+        self.box_hi = A(tb * d, np.float64)
+        self.goal_lo = A(self.count * d, np.float64)
+        self.goal_hi = A(self.count * d, np.float64)
+        self.row_ptr = A(tn + self.count, np.int64)
+        self.col = A(te, np.int32)
+        self.cost = A(te, np.float64)
+        self.goal_count = A(self.count, np.int32)
+        self.init_index = A(self.count, np.int32)
+        self.radius = A(self.count, np.float64)
+        self.node_off.a[:] = np.concatenate([[0], np.cumsum(ns)])
+        self.edge_off.a[:] = np.concatenate([[0], np.cumsum(es)])
+        self.box_off.a[:] = np.concatenate([[0], np.cumsum(bs)])
+        for q, (spec, coords, gc, g, ii) in enumerate(entries):
+            no, eo, bo = self.node_off.a[q], self.edge_off.a[q], self.box_off.a[q]
+            n, nb = coords.shape[0], spec.num_boxes
+            self.coords.a[no * d:(no + n) * d] = coords.reshape(-1)
+            self.box_lo.a[bo * d:(bo + nb) * d] = spec.box_lo.reshape(-1)
+            self.box_hi.a[bo * d:(bo + nb) * d] = spec.box_hi.reshape(-1)
+            self.goal_lo.a[q * d:(q + 1) * d] = spec.goal_lo
+            self.goal_hi.a[q * d:(q + 1) * d] = spec.goal_hi
+            self.row_ptr.a[no + q:no + q + n + 1] = g.out_ptr
+            self.col.a[eo:eo + g.num_edges] = g.out_col
+            self.cost.a[eo:eo + g.num_edges] = g.out_cost
+            self.goal_count.a[q] = gc
+            self.init_index.a[q] = ii
+            self.radius.a[q] = g.radius
+        self.total_nodes, self.total_edges = tn, te
+        self.paths = A(tn, np.int32)
+        self.label = A(tn, np.uint8) if want_tree else None
+        self.tree_cost = A(tn, np.float64) if want_tree else None
+        self.parent = A(tn, np.int32) if want_tree else None
+        self.iteration_added = A(tn, np.int64) if want_tree else None
+        s = abi.BatchHost()
+        s.count, s.dim = self.count, d
+        for name, ct in (("node_off", C.c_int64), ("edge_off", C.c_int64), ("box_off", C.c_int32),
+                         ("coords", C.c_double), ("box_lo", C.c_double), ("box_hi", C.c_double),
+                         ("goal_lo", C.c_double), ("goal_hi", C.c_double),
+                         ("row_ptr", C.c_int64), ("col", C.c_int32), ("cost", C.c_double),
+                         ("goal_count", C.c_int32), ("init_index", C.c_int32),
+                         ("radius", C.c_double)):
+            setattr(s, name, abi.ptr(getattr(self, name).a, ct))
+        self.struct = s
+        self.summaries = (abi.PlanSummary * self.count)()
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(getattr(self, k).a.nbytes for k in (
+            "coords", "box_lo", "box_hi", "goal_lo", "goal_hi", "row_ptr", "col", "cost"))
+
+    @property
+    def d2h_bytes(self) -> int:
+        b = C.sizeof(abi.PlanSummary) * self.count + self.paths.a.nbytes
+        for k in ("label", "tree_cost", "parent", "iteration_added"):
+            if getattr(self, k) is not None:
+                b += getattr(self, k).a.nbytes
+        return b
+
+    def query_result(self, q: int) -> abi.PlanResultPy:
+        """PlanResult-shaped view of query q after a plan_batch_host call."""
+        s = self.summaries[q]
+        no, n1 = self.node_off.a[q], self.node_off.a[q + 1]
+        t = (lambda x: None if x is None else x.a[no:n1].copy())
+        return abi.PlanResultPy(status=s.status, cost=s.cost, iterations=s.iterations,
+                                total_collision_checks=s.total_collision_checks,
+                                path_indices=self.paths.a[no:no + s.path_len].copy(),
+                                label=t(self.label), tree_cost=t(self.tree_cost),
+                                parent=t(self.parent), iteration_added=t(self.iteration_added))
+
+
+def plan_batch_host(ctx: Context, pb: PackedBatch, lam: float = 1.0):
+    """gmt_plan_batch_host: H2D of the packed queries, one solve launch,
+    D2H of summaries, paths and (if allocated) the trees."""
+    opt = lambda x, ct: abi.ptr(None if x is None else x.a, ct)  # noqa: E731
+    check(lib().gmt_plan_batch_host(ctx.h, C.byref(pb.struct), lam, pb.summaries,
+                                    abi.ptr(pb.paths.a, C.c_int32), opt(pb.label, C.c_uint8),
+                                    opt(pb.tree_cost, C.c_double), opt(pb.parent, C.c_int32),
+                                    opt(pb.iteration_added, C.c_int64)))
+    return pb.summaries

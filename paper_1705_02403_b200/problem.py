@@ -435,9 +435,12 @@ def random_problem_2d(rng: Pcg32, dim: int = 2, with_obstacles: bool = True, n_m
         if not found:
             continue
         spec.sampling_kind = abi.SAMPLE_UNIFORM
-        a = rng.next_u32()
-        b = rng.next_u32()
-        spec.seed = mix64(a, b)
+        # mix64(rng.next_u32(), rng.next_u32()) (oracles.cpp:303): GCC on
+        # x86-64 evaluates the arguments right to left, so the FIRST draw is
+        # the second argument.  Pinned by tests/test_oracle.py.
+        first = rng.next_u32()
+        second = rng.next_u32()
+        spec.seed = mix64(second, first)
         spec.n = n_min + rng.next_u32() % (n_max - n_min + 1)
         return spec
     raise RuntimeError("random problem generation kept hitting infeasible draws")
