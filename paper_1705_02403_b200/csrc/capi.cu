@@ -425,13 +425,21 @@ int validate_plan(const gmt_instance* inst, int32_t init_index, double lambda, d
 
 // Shared-memory plan for a set of queries; errors when a query's wavefront
 // cannot live on chip.
-int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, size_t* smem, int* obs_in_smem) {
+int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, int cluster, size_t* smem,
+              int* obs_in_smem) {
+  if (max_n > kMaxSolveNodes)
+    return set_error(GMT_E_INVALID_INPUT, "n = " + std::to_string(max_n) + " exceeds the " +
+                                              std::to_string(kMaxSolveNodes) +
+                                              "-node limit of the on-chip wavefront");
+  if (max_d > kMaxSolveDim)
+    return set_error(GMT_E_INVALID_INPUT, "dimension above 16 is not supported");
+  const bool parent_smem = cluster > 1;
   const size_t obs_bytes = sizeof(double) * 2 * static_cast<size_t>(max_nb) * max_d;
   *obs_in_smem = obs_bytes <= 48 * 1024 ? 1 : 0;
-  SolveLayout L = solve_layout(max_n, max_d, max_nb, *obs_in_smem != 0);
+  SolveLayout L = solve_layout(max_n, max_d, max_nb, *obs_in_smem != 0, parent_smem);
   if (L.total > ctx->smem_optin && *obs_in_smem) {
     *obs_in_smem = 0;
-    L = solve_layout(max_n, max_d, max_nb, false);
+    L = solve_layout(max_n, max_d, max_nb, false, parent_smem);
   }
   if (L.total > ctx->smem_optin) {
     return set_error(GMT_E_INVALID_INPUT,
@@ -450,11 +458,11 @@ int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, b
   Carver c;
   const size_t o_sc = c.take<ResultScalars>(count);
   const size_t o_path = c.take<int32_t>(total);
-  size_t o_label = 0, o_cost = 0, o_parent = 0, o_iter = 0, o_gs = 0, o_na = 0, o_ck = 0;
+  size_t o_label = 0, o_cost = 0, o_iter = 0, o_gs = 0, o_na = 0, o_ck = 0;
+  const size_t o_parent = c.take<int32_t>(total);  // always: batched solves walk it
   if (tree) {
     o_label = c.take<uint8_t>(total);
     o_cost = c.take<double>(total);
-    o_parent = c.take<int32_t>(total);
     o_iter = c.take<int64_t>(total);
   }
   if (stats) {
@@ -472,7 +480,7 @@ int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, b
     r.path = at<int32_t>(b, o_path) + o;
     r.label = tree ? at<uint8_t>(b, o_label) + o : nullptr;
     r.tree_cost = tree ? at<double>(b, o_cost) + o : nullptr;
-    r.parent = tree ? at<int32_t>(b, o_parent) + o : nullptr;
+    r.parent = at<int32_t>(b, o_parent) + o;
     r.iter_added = tree ? at<int64_t>(b, o_iter) + o : nullptr;
     r.group_sizes = stats ? at<int32_t>(b, o_gs) + o + q : nullptr;
     r.nodes_added = stats ? at<int32_t>(b, o_na) + o + q : nullptr;
@@ -539,7 +547,7 @@ int plan_on(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, double l
   const DevInstance& D = inst->desc;
   size_t smem;
   int obs;
-  GMT_TRY(plan_smem(ctx, D.n, D.dim, D.num_boxes, &smem, &obs));
+  GMT_TRY(plan_smem(ctx, D.n, D.dim, D.num_boxes, ctx->cluster ? ctx->cluster : 8, &smem, &obs));
   int64_t node_off[2] = {0, D.n};
   std::vector<DevResult> res;
   ResultScalars* sc;
@@ -630,7 +638,7 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
     max_d = std::max(max_d, inst->desc.dim);
     max_nb = std::max(max_nb, inst->desc.num_boxes);
   }
-  int rc = plan_smem(ctx, max_n, max_d, max_nb, &b->smem, &b->obs);
+  int rc = plan_smem(ctx, max_n, max_d, max_nb, ctx->batch_cluster, &b->smem, &b->obs);
   if (rc == GMT_OK)
     rc = carve_results(b->res, count, b->node_off.data(), true, true, b->results, &b->scalars,
                        ctx->counting ? ctx->counters : nullptr);
@@ -723,7 +731,7 @@ extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double
   }
   size_t smem;
   int obs;
-  GMT_TRY(plan_smem(ctx, max_n, d, max_nb, &smem, &obs));
+  GMT_TRY(plan_smem(ctx, max_n, d, max_nb, ctx->batch_cluster, &smem, &obs));
 
   // Inputs: one H2D copy per array.
   Carver c;

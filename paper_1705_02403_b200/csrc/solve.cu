@@ -1,5 +1,6 @@
-// solve.cu -- the GMT* online phase (gmt_plan, planner.cpp:94-198) as ONE
-// persistent kernel launch per query (or per batch of queries).
+// solve.cu -- the GMT* online phase (gmt_plan, planner.cpp:94-198; fmt_plan,
+// planner.cpp:200-262) as ONE persistent kernel launch per query (or per
+// batch of queries).
 //
 // Execution model:
 //   * A query is solved by a thread-block cluster of CS CTAs (CS = 1 for
@@ -8,16 +9,19 @@
 //     cost f64[V] plus open/closed/group bitmasks.  Phases P0-P3 of the
 //     reference pass (min-open, fast-forward, group, goal test) therefore run
 //     redundantly and locally in every CTA with no communication.
-//   * P4 (candidate gather) partitions the group over all warps of the
-//     cluster; each unexplored out-neighbour is marked in the candidate
-//     bitmask of its owner CTA (word-interleaved) with DSMEM atomics,
-//     lane-aggregated with __match_any_sync/__reduce_or_sync.
+//   * Ownership is word-interleaved: node v belongs to CTA (v/32) mod CS.
+//   * P4 (candidate gather): each CTA expands the group members it owns; the
+//     lanes stream an out-row (sorted targets), OR the unexplored targets of
+//     each 32-node word together with a segmented shuffle scan over the
+//     sorted run, and one lane per word sets the bits in the owner's
+//     candidate bitmask (a DSMEM atomic when the owner is another CTA).
 //   * P5 (connect_candidate) runs warp-per-candidate on the owner CTA: the
-//     lanes stream the candidate's in-row (col/cost, coalesced) from HBM/L2,
-//     gather cost[y]/open(y) from the local replica, reduce (cost, position)
-//     lexicographically (== the reference's strict-< first-in-list rule),
-//     then slab-test the single best edge against the smem-staged boxes with
-//     the boxes spread over the lanes.
+//     lanes stream the candidate's in-row (col/cost, coalesced, 4 chunks in
+//     flight per lane, next row's offsets prefetched), gather cost[y]/open(y)
+//     from the local replica, reduce (cost, position) lexicographically (==
+//     the reference's strict-< first-in-list rule), then slab-test the single
+//     best edge with its endpoints staged in shared memory and the
+//     smem-staged boxes spread over the lanes.
 //   * P6 (commit) writes the new cost into every replica (DSMEM stores) and
 //     sets a `newopen` bit; labels only change at the next pass start, so
 //     every candidate sees iteration-start labels exactly as in the
@@ -38,6 +42,7 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int32_t kNone = 0x7fffffff;
+constexpr int kUnroll = 4;  // row chunks in flight per lane
 
 struct CtaShared {
   double red_min[32];
@@ -78,10 +83,9 @@ __device__ __forceinline__ T* remote(T* p, int rank) {
   }
 }
 
-__device__ __forceinline__ bool point_free_warp(const double* p, int d, const Boxes& bx,
-                                                int lane) {
-  // point_free (space.cpp:47-54); boxes spread over the lanes.
-  if (!point_in_cube(p, d)) return false;
+// Closed boxes contain p (the loop of point_free, space.cpp:50-52), boxes
+// spread over the lanes.  p is warp-uniform (shared memory).
+__device__ __forceinline__ bool any_box_contains(const double* p, int d, const Boxes& bx, int lane) {
   bool in = false;
   for (int b = lane; b < bx.count && !in; b += kWarp) {
     bool c = true;
@@ -94,16 +98,32 @@ __device__ __forceinline__ bool point_free_warp(const double* p, int d, const Bo
     }
     in = c;
   }
-  return !__any_sync(kFull, in);
+  return __any_sync(kFull, in);
 }
 
-__device__ __forceinline__ bool segment_free_warp(const double* a, const double* b, int d,
-                                                  const Boxes& bx, int lane) {
-  // segment_free (space.cpp:80-90)
-  bool same = true;
-  for (int k = 0; k < d; ++k) same = same && (a[k] == b[k]);
-  if (same) return point_free_warp(a, d, bx, lane);
-  if (!point_in_cube(a, d) || !point_in_cube(b, d)) return false;
+// segment_free (space.cpp:80-90) of the closed segment [A, B] (global
+// memory).  The endpoints are staged in the warp's `seg` scratch
+// (a = seg[0..15], b = seg[16..31]); the coordinate predicates are
+// evaluated lane-per-axis, the boxes lane-per-box.
+__device__ bool segment_free_warp(const double* A, const double* B, int d, const Boxes& bx,
+                                  int lane, double* seg) {
+  __syncwarp();
+  if (lane < d) seg[lane] = A[lane];
+  if (lane >= 16 && lane - 16 < d) seg[lane] = B[lane - 16];
+  __syncwarp();
+  const double* a = seg;
+  const double* b = seg + 16;
+  bool eq = true, cube_a = true, cube_b = true;
+  if (lane < d) {
+    const double x = a[lane], y = b[lane];
+    eq = x == y;
+    cube_a = !(x < 0.0 || x > 1.0);
+    cube_b = !(y < 0.0 || y > 1.0);
+  }
+  const bool same = __all_sync(kFull, eq);
+  const bool in_a = __all_sync(kFull, cube_a);
+  if (same) return in_a && !any_box_contains(a, d, bx, lane);  // point_free(a)
+  if (!in_a || !__all_sync(kFull, cube_b)) return false;
   bool hit = false;
   for (int i = lane; i < bx.count && !hit; i += kWarp) {
     hit = segment_hits_box(a, b, d, bx.lo + i * bx.bs, bx.hi + i * bx.bs, bx.as);
@@ -111,21 +131,32 @@ __device__ __forceinline__ bool segment_free_warp(const double* a, const double*
   return !__any_sync(kFull, hit);
 }
 
+__device__ bool point_free_warp(const double* P, int d, const Boxes& bx, int lane, double* seg) {
+  __syncwarp();
+  if (lane < d) seg[lane] = P[lane];
+  __syncwarp();
+  bool cube = true;
+  if (lane < d) cube = !(seg[lane] < 0.0 || seg[lane] > 1.0);
+  if (!__all_sync(kFull, cube)) return false;
+  return !any_box_contains(seg, d, bx, lane);
+}
+
 // motion_free (planner.cpp:54-60): cached polyline for path edges, exact
 // clipping for straight edges.
 __device__ bool motion_free_warp(const DevInstance& I, const Boxes& bx, int from, int to,
-                                 int32_t pid, int lane) {
+                                 int32_t pid, int lane, double* seg) {
   const int d = I.dim;
   if (pid >= 0) {
     const int64_t a = I.path_ptr[pid], b = I.path_ptr[pid + 1];
     const double* pts = I.path_pts + a * d;
-    if (b - a == 1) return point_free_warp(pts, d, bx, lane);
+    if (b - a == 1) return point_free_warp(pts, d, bx, lane, seg);
     for (int64_t s = 0; s + 1 < b - a; ++s) {
-      if (!segment_free_warp(pts + s * d, pts + (s + 1) * d, d, bx, lane)) return false;
+      if (!segment_free_warp(pts + s * d, pts + (s + 1) * d, d, bx, lane, seg)) return false;
     }
     return true;
   }
-  return segment_free_warp(I.coords + (int64_t)from * d, I.coords + (int64_t)to * d, d, bx, lane);
+  return segment_free_warp(I.coords + static_cast<int64_t>(from) * d,
+                           I.coords + static_cast<int64_t>(to) * d, d, bx, lane, seg);
 }
 
 __device__ __forceinline__ double block_min(double v, double* red, int lane, int warp, int nw) {
@@ -173,39 +204,43 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 // Batched solves (CS == 1) want several small CTAs per SM; single-query
 // clusters want one wide CTA per SM.
 template <int CS>
-__global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solve_kernel(const SolveJob* __restrict__ jobs,
-                                                         int obs_in_smem) {
+__global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
+    gmt_solve_kernel(const SolveJob* __restrict__ jobs, int obs_in_smem) {
+  constexpr bool kParentSmem = CS > 1;  // batched solves keep parents in HBM
+  constexpr int kMaxWarps = CS == 1 ? 8 : 16;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
+  __shared__ double seg_s[kMaxWarps * 32];
 
   const int q = blockIdx.x / CS;
   int rank = 0;
   if constexpr (CS > 1) rank = static_cast<int>(cg::this_cluster().block_rank());
   const SolveJob job = jobs[q];
-  const DevInstance& I = *job.inst;
+  const DevInstance I = *job.inst;
   const DevResult R = job.res;
   const int n = I.n, d = I.dim, nb = I.num_boxes;
-  const SolveLayout L = solve_layout(n, d, nb, obs_in_smem != 0);
+  const SolveLayout L = solve_layout(n, d, nb, obs_in_smem != 0, kParentSmem);
   const int W = L.words;
 
   double* cost_s = reinterpret_cast<double*>(smem + L.off_cost);
-  int32_t* parent_s = reinterpret_cast<int32_t*>(smem + L.off_parent);
+  uint16_t* parent_s = reinterpret_cast<uint16_t*>(smem + L.off_parent);
   uint32_t* open_w = reinterpret_cast<uint32_t*>(smem + L.off_bits);
   uint32_t* closed_w = open_w + L.words_pad;
   uint32_t* group_w = closed_w + L.words_pad;
   uint32_t* newopen_w = group_w + L.words_pad;
   uint32_t* cand_w = newopen_w + L.words_pad;
   uint32_t* goal_w = cand_w + L.words_pad;
-  int32_t* list = reinterpret_cast<int32_t*>(smem + L.off_list);
+  uint16_t* list = reinterpret_cast<uint16_t*>(smem + L.off_list);
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  double* seg = seg_s + warp * 32;
 
   Boxes bx;
   bx.count = nb;
   if (obs_in_smem) {
     double* lo = reinterpret_cast<double*>(smem + L.off_obs);
-    double* hi = lo + (size_t)nb * d;
+    double* hi = lo + static_cast<size_t>(nb) * d;
     for (int idx = tid; idx < nb * d; idx += nt) {
       const int b = idx / d, k = idx - b * d;
       lo[k * nb + b] = I.box_lo[idx];
@@ -220,7 +255,7 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
   const int init = job.init_index;
   for (int v = tid; v < n; v += nt) {
     cost_s[v] = kInf;
-    parent_s[v] = -1;
+    if constexpr (kParentSmem) parent_s[v] = 0xffffu;
   }
   for (int w = tid; w < W; w += nt) {
     open_w[w] = closed_w[w] = group_w[w] = newopen_w[w] = cand_w[w] = 0u;
@@ -230,12 +265,13 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
   for (int w = warp; w < W; w += nw) {
     const int v = w * 32 + lane;
     bool g = v < n;
-    if (g) g = box_contains(I.goal_lo, I.goal_hi, d, I.coords + (int64_t)v * d);
+    if (g) g = box_contains(I.goal_lo, I.goal_hi, d, I.coords + static_cast<int64_t>(v) * d);
     const uint32_t gb = __ballot_sync(kFull, g);
     if (lane == 0) goal_w[w] = gb;
   }
-  if (R.iter_added) {
-    for (int v = rank * nt + tid; v < n; v += CS * nt) R.iter_added[v] = (v == init) ? 0 : -1;
+  for (int v = rank * nt + tid; v < n; v += CS * nt) {
+    if (R.iter_added) R.iter_added[v] = (v == init) ? 0 : -1;
+    if (!kParentSmem) R.parent[v] = -1;
   }
   if (tid == 0) {
     sh.group_count = 0;
@@ -249,7 +285,7 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
   // infeasible_input (planner.cpp:39-41, 108): empty tree.
   if (warp == 0) {
     const bool ok = I.goal_count > 0 &&
-                    point_free_warp(I.coords + (int64_t)init * d, d, bx, lane);
+                    point_free_warp(I.coords + static_cast<int64_t>(init) * d, d, bx, lane, seg);
     if (lane == 0) sh.feasible = ok ? 1 : 0;
   }
   __syncthreads();
@@ -310,91 +346,119 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
       if (tid == 0) {
         group_w[z >> 5] = 1u << (z & 31);
         if (((z >> 5) & (CS - 1)) == rank) {
-          list[0] = z;
+          list[0] = static_cast<uint16_t>(z);
           sh.own_count = 1;
         }
       }
       __syncthreads();
     } else {
-    // P0: min cost over open nodes (planner.cpp:119-122).
-    double m = kInf;
-    for (int w = warp; w < W; w += nw) {
-      if ((open_w[w] >> lane) & 1u) {
-        const double c = cost_s[w * 32 + lane];
-        m = c < m ? c : m;
-      }
-    }
-    m = block_min(m, sh.red_min, lane, warp, nw);
-    if (m == kInf) {  // planner.cpp:123-127
-      status = 1;
-      break;
-    }
-    // P1: fast-forward (planner.cpp:132-136); i*delta is (double)i * delta.
-    if (m > __dmul_rn(static_cast<double>(i), delta)) {
-      const long long jump = static_cast<long long>(ceil(__ddiv_rn(m, delta)));
-      i = jump > i + 1 ? jump : i + 1;
-      while (m > __dmul_rn(static_cast<double>(i), delta)) ++i;
-    }
-    const double thr = __dmul_rn(static_cast<double>(i), delta);
-
-    // P2 + P3: group bitmask/list and min-cost goal member (planner.cpp:137-149).
-    double gc = kInf;
-    int32_t gv = kNone;
-    for (int w = warp; w < W; w += nw) {
-      const uint32_t ow = open_w[w];
-      const int v = w * 32 + lane;
-      const bool g = ((ow >> lane) & 1u) && cost_s[v] <= thr;
-      const uint32_t gb = __ballot_sync(kFull, g);
-      if (gb) {
-        // Every CTA sees the whole group; the members of words w = rank
-        // (mod CS) go to this CTA's P4 work list (list order is arbitrary,
-        // ownership is not).
-        int base = 0;
-        const bool own = (w & (CS - 1)) == rank;
-        if (lane == 0) {
-          group_w[w] = gb;
-          atomicAdd(&sh.group_count, __popc(gb));
-          if (own) base = atomicAdd(&sh.own_count, __popc(gb));
-        }
-        base = __shfl_sync(kFull, base, 0);
-        if (g) {
-          if (own) list[base + __popc(gb & ((1u << lane) - 1u))] = v;
-          if ((goal_w[w] >> lane) & 1u) argmin_step(gc, gv, cost_s[v], v);
+      // P0: min cost over open nodes (planner.cpp:119-122).
+      double m = kInf;
+      for (int w = warp; w < W; w += nw) {
+        if ((open_w[w] >> lane) & 1u) {
+          const double c = cost_s[w * 32 + lane];
+          m = c < m ? c : m;
         }
       }
-    }
-    block_argmin(gc, gv, sh, lane, warp, nw);
-    gsize = sh.group_count;
-    if (gv != kNone) {  // planner.cpp:150-156
-      status = 0;
-      goal = gv;
-      break;
-    }
-    }  // GMT group selection
+      m = block_min(m, sh.red_min, lane, warp, nw);
+      if (m == kInf) {  // planner.cpp:123-127
+        status = 1;
+        break;
+      }
+      // P1: fast-forward (planner.cpp:132-136); i*delta is (double)i * delta.
+      if (m > __dmul_rn(static_cast<double>(i), delta)) {
+        const long long jump = static_cast<long long>(ceil(__ddiv_rn(m, delta)));
+        i = jump > i + 1 ? jump : i + 1;
+        while (m > __dmul_rn(static_cast<double>(i), delta)) ++i;
+      }
+      const double thr = __dmul_rn(static_cast<double>(i), delta);
 
-    // P4: mark unexplored out-neighbours of the group (planner.cpp:159-166).
-    const int own = sh.own_count;
-    for (int k = warp; k < own; k += nw) {
-      const int g = list[k];
-      const int64_t e0 = I.out_ptr[g], e1 = I.out_ptr[g + 1];
-      for (int64_t base = e0; base < e1; base += kWarp) {
-        const int64_t e = base + lane;
-        bool un = false;
-        int x = 0;
-        if (e < e1) {
-          ++cnt_out;
-          x = __ldg(I.out_col + e);
-          un = !(((open_w[x >> 5] | closed_w[x >> 5]) >> (x & 31)) & 1u);
-        }
-        const uint32_t act = __ballot_sync(kFull, un);
-        if (un) {
-          const int word = x >> 5;
-          const uint32_t peers = __match_any_sync(act, word);
-          const uint32_t bits = __reduce_or_sync(peers, 1u << (x & 31));
-          if (lane == __ffs(peers) - 1) {
-            atomicOr(remote<CS>(cand_w, word & (CS - 1)) + word, bits);
+      // P2 + P3: group bitmask/list and min-cost goal member (planner.cpp:137-149).
+      double gc = kInf;
+      int32_t gv = kNone;
+      for (int w = warp; w < W; w += nw) {
+        const uint32_t ow = open_w[w];
+        const int v = w * 32 + lane;
+        const bool g = ((ow >> lane) & 1u) && cost_s[v] <= thr;
+        const uint32_t gb = __ballot_sync(kFull, g);
+        if (gb) {
+          // Every CTA sees the whole group; the members of words it owns go
+          // to its P4 work list (list order is arbitrary, ownership is not).
+          int base = 0;
+          const bool own = (w & (CS - 1)) == rank;
+          if (lane == 0) {
+            group_w[w] = gb;
+            atomicAdd(&sh.group_count, __popc(gb));
+            if (own) base = atomicAdd(&sh.own_count, __popc(gb));
+          }
+          base = __shfl_sync(kFull, base, 0);
+          if (g) {
+            if (own) list[base + __popc(gb & ((1u << lane) - 1u))] = static_cast<uint16_t>(v);
+            if ((goal_w[w] >> lane) & 1u) argmin_step(gc, gv, cost_s[v], v);
           }
         }
+      }
+      block_argmin(gc, gv, sh, lane, warp, nw);
+      gsize = sh.group_count;
+      if (gv != kNone) {  // planner.cpp:150-156
+        status = 0;
+        goal = gv;
+        break;
+      }
+    }
+
+    // P4: mark unexplored out-neighbours of the owned group members
+    // (planner.cpp:159-166).
+    {
+      const int own = sh.own_count;
+      int k = warp;
+      int64_t e0 = 0, e1 = 0;
+      if (k < own) {
+        const int g = list[k];
+        e0 = __ldg(I.out_ptr + g);
+        e1 = __ldg(I.out_ptr + g + 1);
+      }
+      while (k < own) {
+        const int kn = k + nw;
+        int64_t n0 = 0, n1 = 0;
+        if (kn < own) {  // next row's offsets in flight during this row
+          const int gn = list[kn];
+          n0 = __ldg(I.out_ptr + gn);
+          n1 = __ldg(I.out_ptr + gn + 1);
+        }
+        for (int64_t base = e0; base < e1; base += kWarp * kUnroll) {
+          int xs[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int64_t e = base + u * kWarp + lane;
+            xs[u] = e < e1 ? __ldg(I.out_col + e) : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            if (base + u * kWarp >= e1) break;  // warp-uniform
+            const int x = xs[u];
+            const bool valid = x >= 0;
+            cnt_out += valid ? 1 : 0;
+            const int w = valid ? (x >> 5) : (-1 - lane);
+            uint32_t bit = 0u;
+            if (valid && !(((open_w[w] | closed_w[w]) >> (x & 31)) & 1u)) bit = 1u << (x & 31);
+            // Rows are sorted, so equal words form runs: suffix-OR each run
+            // into its first lane, which sets the word once.
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t ob = __shfl_down_sync(kFull, bit, o);
+              const int ow = __shfl_down_sync(kFull, w, o);
+              if (lane + o < 32 && ow == w) bit |= ob;
+            }
+            const int pw = __shfl_up_sync(kFull, w, 1);
+            if ((lane == 0 || pw != w) && bit) {
+              atomicOr(remote<CS>(cand_w, w & (CS - 1)) + w, bit);
+            }
+          }
+        }
+        k = kn;
+        e0 = n0;
+        e1 = n1;
       }
     }
     cluster_barrier<CS>();  // [1] candidate marks complete
@@ -408,7 +472,7 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
         while (bits) {
           const int b = __ffs(bits) - 1;
           bits &= bits - 1u;
-          list[base++] = w * 32 + b;
+          list[base++] = static_cast<uint16_t>(w * 32 + b);
         }
       }
     }
@@ -417,48 +481,90 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
 
     // P5 + P6: connect_candidate (planner.cpp:62-90) and commit (178-189).
     int my_checks = 0, my_added = 0;
-    for (int k = warp; k < ccount; k += nw) {
-      const int x = list[k];
-      const int64_t e0 = I.in_ptr[x], e1 = I.in_ptr[x + 1];
-      double bv = kInf;
-      long long be = -1;
-      int by = -1;
-      for (int64_t e = e0 + lane; e < e1; e += kWarp) {
-        const int y = __ldg(I.in_col + e);
-        ++cnt_in;
-        if ((open_w[y >> 5] >> (y & 31)) & 1u) {
-          ++cnt_open;
-          const double c = __dadd_rn(cost_s[y], __ldg(I.in_cost + e));
-          if (c < bv) {
-            bv = c;
-            be = e;
-            by = y;
+    {
+      int k = warp;
+      int x = 0;
+      int64_t e0 = 0, e1 = 0;
+      if (k < ccount) {
+        x = list[k];
+        e0 = __ldg(I.in_ptr + x);
+        e1 = __ldg(I.in_ptr + x + 1);
+      }
+      while (k < ccount) {
+        const int kn = k + nw;
+        int xn = 0;
+        int64_t n0 = 0, n1 = 0;
+        if (kn < ccount) {
+          xn = list[kn];
+          n0 = __ldg(I.in_ptr + xn);
+          n1 = __ldg(I.in_ptr + xn + 1);
+        }
+        double bv = kInf;
+        long long be = -1;
+        int by = -1;
+        for (int64_t base = e0; base < e1; base += kWarp * kUnroll) {
+          int ys[kUnroll];
+          double cs[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int64_t e = base + u * kWarp + lane;
+            ys[u] = -1;
+            cs[u] = 0.0;
+            if (e < e1) {
+              ys[u] = __ldg(I.in_col + e);
+              cs[u] = __ldg(I.in_cost + e);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int y = ys[u];
+            if (y >= 0) {
+              ++cnt_in;
+              if ((open_w[y >> 5] >> (y & 31)) & 1u) {
+                ++cnt_open;
+                const double c = __dadd_rn(cost_s[y], cs[u]);
+                if (c < bv) {
+                  bv = c;
+                  be = base + u * kWarp + lane;
+                  by = y;
+                }
+              }
+            }
           }
         }
-      }
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(kFull, bv, o);
-        const long long oe = __shfl_xor_sync(kFull, be, o);
-        const int oy = __shfl_xor_sync(kFull, by, o);
-        if (ov < bv || (ov == bv && oe >= 0 && (be < 0 || oe < be))) {
-          bv = ov;
-          be = oe;
-          by = oy;
+        for (int o = 16; o; o >>= 1) {
+          const double ov = __shfl_xor_sync(kFull, bv, o);
+          const long long oe = __shfl_xor_sync(kFull, be, o);
+          const int oy = __shfl_xor_sync(kFull, by, o);
+          if (ov < bv || (ov == bv && oe >= 0 && (be < 0 || oe < be))) {
+            bv = ov;
+            be = oe;
+            by = oy;
+          }
         }
-      }
-      if (be < 0) continue;  // no open in-neighbour: not checked
-      ++my_checks;
-      const int32_t pid = I.in_path ? __ldg(I.in_path + be) : -1;
-      if (motion_free_warp(I, bx, by, x, pid, lane)) {
-        ++my_added;
-        if (lane < CS) {
-          remote<CS>(cost_s, lane)[x] = bv;
-          atomicOr(remote<CS>(newopen_w, lane) + (x >> 5), 1u << (x & 31));
+        if (be >= 0) {  // no open in-neighbour: not checked
+          ++my_checks;
+          const int32_t pid = I.in_path ? __ldg(I.in_path + be) : -1;
+          if (motion_free_warp(I, bx, by, x, pid, lane, seg)) {
+            ++my_added;
+            if (lane < CS) {
+              remote<CS>(cost_s, lane)[x] = bv;
+              atomicOr(remote<CS>(newopen_w, lane) + (x >> 5), 1u << (x & 31));
+            }
+            if (lane == 0) {
+              if constexpr (kParentSmem) {
+                remote<CS>(parent_s, 0)[x] = static_cast<uint16_t>(by);
+              } else {
+                R.parent[x] = by;
+              }
+              if (R.iter_added) R.iter_added[x] = i;
+            }
+          }
         }
-        if (lane == 0) {
-          remote<CS>(parent_s, 0)[x] = by;
-          if (R.iter_added) R.iter_added[x] = i;
-        }
+        k = kn;
+        x = xn;
+        e0 = n0;
+        e1 = n1;
       }
     }
     if (lane == 0 && (my_checks | my_added)) {
@@ -509,13 +615,13 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
     }
   }
   if (rank != 0) return;
-  // Outputs (rank 0 holds the parent replica).
+  // Outputs (rank 0 holds the parent replica, or the parents are in HBM).
   if (R.label) {
     for (int v = tid; v < n; v += nt) {
       const uint32_t bit = 1u << (v & 31);
       R.label[v] = (open_w[v >> 5] & bit) ? 1 : ((closed_w[v >> 5] & bit) ? 2 : 0);
       R.tree_cost[v] = cost_s[v];
-      R.parent[v] = parent_s[v];
+      if constexpr (kParentSmem) R.parent[v] = parent_s[v] == 0xffffu ? -1 : parent_s[v];
     }
   }
   if (tid == 0) {
@@ -535,11 +641,19 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1) gmt_solv
       }
       s.num_stats = pass + 1;
       s.cost = cost_s[goal];
+      // finalize_success (planner.cpp:43-50): walk the parents.
+      auto par = [&](int v) -> int {
+        if constexpr (kParentSmem) {
+          return parent_s[v] == 0xffffu ? -1 : parent_s[v];
+        } else {
+          return R.parent[v];
+        }
+      };
       int len = 0;
-      for (int v = goal; v >= 0; v = parent_s[v]) ++len;
+      for (int v = goal; v >= 0; v = par(v)) ++len;
       int k = len;
       if (R.path) {
-        for (int v = goal; v >= 0; v = parent_s[v]) R.path[--k] = v;
+        for (int v = goal; v >= 0; v = par(v)) R.path[--k] = v;
       }
       s.path_len = len;
     } else {

@@ -10,31 +10,40 @@
 
 namespace gmtb {
 
-// Per-CTA shared memory of one query (V = n samples, W = ceil(V/32)):
-//   cost   f64[V]    replicated cost-to-arrive
-//   parent i32[V]    parent replica (read by rank 0 for the path walk)
-//   bits   6 x u32[Wp]  open, closed, group, newopen, cand, goal
-//   list   i32[V]    group list (P4) / owned candidate list (P5)
-//   obs    f64[2*B*d] boxes, axis-major (SoA) when they fit
+// Largest node count the on-chip wavefront supports (u16 node ids in the
+// work lists and the parent replica).
+constexpr int kMaxSolveNodes = 65535;
+constexpr int kMaxSolveDim = 16;
+
+// Per-CTA dynamic shared memory of one query (V = n samples,
+// W = ceil(V/32), Wp = W rounded up to 4):
+//   cost   f64[32W]    replicated cost-to-arrive
+//   parent u16[32W]    parent replica (clusters only; batched solves keep
+//                      parents in HBM and walk them once at the end)
+//   bits   6 x u32[Wp] open, closed, group, newopen, cand, goal
+//   list   u16[32W]    owned group members (P4) / owned candidates (P5)
+//   obs    f64[2*B*d]  boxes, axis-major (SoA) when they fit
 struct SolveLayout {
   int words;
   int words_pad;
   size_t off_cost, off_parent, off_bits, off_list, off_obs, total;
 };
 
-__host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool obs_smem) {
+__host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool obs_smem,
+                                                    bool parent_smem) {
   SolveLayout L;
   L.words = (n + 31) >> 5;
   L.words_pad = (L.words + 3) & ~3;
+  const size_t nodes = static_cast<size_t>(L.words) * 32;
   size_t off = 0;
   L.off_cost = off;
-  off = align16(off + sizeof(double) * static_cast<size_t>(L.words) * 32);
+  off = align16(off + sizeof(double) * nodes);
   L.off_parent = off;
-  off = align16(off + sizeof(int32_t) * static_cast<size_t>(L.words) * 32);
+  if (parent_smem) off = align16(off + sizeof(uint16_t) * nodes);
   L.off_bits = off;
   off = align16(off + sizeof(uint32_t) * 6 * static_cast<size_t>(L.words_pad));
   L.off_list = off;
-  off = align16(off + sizeof(int32_t) * static_cast<size_t>(L.words) * 32);
+  off = align16(off + sizeof(uint16_t) * nodes);
   L.off_obs = off;
   if (obs_smem) off = align16(off + sizeof(double) * 2 * static_cast<size_t>(nb) * d);
   L.total = off;
