@@ -67,7 +67,8 @@ def dist_env():
 
 def query_specs(rank: int, per_gpu: int, n: int):
     from paper_1705_02403_b200 import problem as P
-    return [P.random_forest_query(MASTER_SEED, rank * per_gpu + j, n=n) for j in range(per_gpu)]
+    from paper_1705_02403_b200.shard import weak_range
+    return [P.random_forest_query(MASTER_SEED, q, n=n) for q in weak_range(per_gpu, rank)]
 
 
 class ClockSampler:
@@ -307,13 +308,8 @@ def run_b200(args):
     p50 = min(single.values())
 
     # ---- gather: one record per query to rank 0 (the only collective) -----
-    recs = np.array([[s.status, s.cost, s.iterations, s.total_collision_checks] for s in dev0],
-                    np.float64)
-    if world > 1:
-        t_local = torch.from_numpy(recs).cuda()
-        gathered = [torch.empty_like(t_local) for _ in range(world)]
-        torch.distributed.all_gather(gathered, t_local)
-        recs = torch.cat(gathered).cpu().numpy()
+    from paper_1705_02403_b200.shard import gather_records, records
+    recs = gather_records(records(dev0), device=f"cuda:{local}")
 
     line = None
     if rank == 0:
