@@ -49,7 +49,7 @@ MASTER_SEED = 20171005
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--queries", type=int, default=512, help="queries per GPU per step")
@@ -94,7 +94,7 @@ class ClockSampler:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self.stop.wait(0.2)
+            self.stop.wait(0.05)
 
     def __enter__(self):
         self.t.start()
@@ -115,6 +115,21 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.rows)}
+
+
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu --set full summary (profiles/<round>/ncu_summary.json)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_summary.json")), reverse=True):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            k = d["kernels"][kernel]
+            return k["dram_bytes_read"] + k["dram_bytes_write"], os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
 
 
 def measured_peak_hbm():
@@ -257,6 +272,7 @@ def run_b200(args):
     peak, peak_kind = measured_peak_hbm()
     achieved = b_alg / (kernel_ms / 1e3) / 1e9
     clocks = clk.summary()
+    traffic, traffic_src = ncu_traffic("gmt_solve_kernel<1>:forest3d_n4000_q512")
 
     # ---- e2e through the C-ABI drop-in with host buffers ------------------
     entries = []
@@ -342,7 +358,8 @@ def run_b200(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": pb.h2d_bytes,
                     "d2h_bytes_per_step": pb.d2h_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_kind": peak_kind,
                          "kernel": "gmt_solve_kernel<1>",
                          "bytes_per_launch": b_alg, "kernel_ms": kernel_ms,
                          "counts": {**cnt, "passes": passes, "V_passes": Vpasses}},
