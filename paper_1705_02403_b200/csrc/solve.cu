@@ -105,12 +105,7 @@ __device__ __forceinline__ bool any_box_contains(const double* p, int d, const B
 // memory).  The endpoints are staged in the warp's `seg` scratch
 // (a = seg[0..15], b = seg[16..31]); the coordinate predicates are
 // evaluated lane-per-axis, the boxes lane-per-box.
-__device__ bool segment_free_warp(const double* A, const double* B, int d, const Boxes& bx,
-                                  int lane, double* seg) {
-  __syncwarp();
-  if (lane < d) seg[lane] = A[lane];
-  if (lane >= 16 && lane - 16 < d) seg[lane] = B[lane - 16];
-  __syncwarp();
+__device__ bool segment_free_staged(int d, const Boxes& bx, int lane, const double* seg) {
   const double* a = seg;
   const double* b = seg + 16;
   bool eq = true, cube_a = true, cube_b = true;
@@ -126,9 +121,36 @@ __device__ bool segment_free_warp(const double* A, const double* B, int d, const
   if (!in_a || !__all_sync(kFull, cube_b)) return false;
   bool hit = false;
   for (int i = lane; i < bx.count && !hit; i += kWarp) {
-    hit = segment_hits_box(a, b, d, bx.lo + i * bx.bs, bx.hi + i * bx.bs, bx.as);
+    const double* lo = bx.lo + i * bx.bs;
+    const double* hi = bx.hi + i * bx.bs;
+    // Exact-safe separation pre-test (no division): if on some axis both
+    // endpoints lie below lo - m or above hi + m (m = 1e-9), the reference's
+    // floating-point slab clip (space.cpp:60-78) reports a miss.  Proof
+    // sketch: a, b are in the unit cube here, so |dk| <= 1; for b < a < lo - m
+    // or b > a > hi + m (and dk > 0 mirrored) both rounded slab parameters
+    // are strictly negative, and for a < b < lo - m (or a > b > hi + m) both
+    // exceed (1 + m)(1 - 2^-53)/(1 + 2^-53) > 1, so tmin > tmax on that axis;
+    // the clip's outcome does not depend on the axis order (max/min of the
+    // slab ends are order-free and emptiness is monotone).  dk == 0 is the
+    // clip's own early miss.  Boxes that pass go through the exact clip.
+    bool sep = false;
+    for (int k = 0; k < d && !sep; ++k) {
+      const double x = a[k], y = b[k];
+      const double l = lo[k * bx.as], h = hi[k * bx.as];
+      sep = (x < l - 1e-9 && y < l - 1e-9) || (x > h + 1e-9 && y > h + 1e-9);
+    }
+    if (!sep) hit = segment_hits_box(a, b, d, lo, hi, bx.as);
   }
   return !__any_sync(kFull, hit);
+}
+
+__device__ bool segment_free_warp(const double* A, const double* B, int d, const Boxes& bx,
+                                  int lane, double* seg) {
+  __syncwarp();
+  if (lane < d) seg[lane] = A[lane];
+  if (lane >= 16 && lane - 16 < d) seg[lane] = B[lane - 16];
+  __syncwarp();
+  return segment_free_staged(d, bx, lane, seg);
 }
 
 __device__ bool point_free_warp(const double* P, int d, const Boxes& bx, int lane, double* seg) {
@@ -499,8 +521,13 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
           n0 = __ldg(I.in_ptr + xn);
           n1 = __ldg(I.in_ptr + xn + 1);
         }
+        // The segment's B endpoint (the candidate) is staged while the row
+        // streams in; the A endpoint (the chosen parent) after the argmin.
+        __syncwarp();
+        if (lane >= 16 && lane - 16 < d)
+          seg[lane] = __ldg(I.coords + static_cast<int64_t>(x) * d + (lane - 16));
         double bv = kInf;
-        long long be = -1;
+        int bo = -1;  // position of the lane's best edge within the row
         int by = -1;
         for (int64_t base = e0; base < e1; base += kWarp * kUnroll) {
           int ys[kUnroll];
@@ -525,27 +552,39 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
                 const double c = __dadd_rn(cost_s[y], cs[u]);
                 if (c < bv) {
                   bv = c;
-                  be = base + u * kWarp + lane;
+                  bo = static_cast<int>(base - e0) + u * kWarp + lane;
                   by = y;
                 }
               }
             }
           }
         }
-        for (int o = 16; o; o >>= 1) {
-          const double ov = __shfl_xor_sync(kFull, bv, o);
-          const long long oe = __shfl_xor_sync(kFull, be, o);
-          const int oy = __shfl_xor_sync(kFull, by, o);
-          if (ov < bv || (ov == bv && oe >= 0 && (be < 0 || oe < be))) {
-            bv = ov;
-            be = oe;
-            by = oy;
-          }
-        }
-        if (be >= 0) {  // no open in-neighbour: not checked
+        // Warp argmin of (cost, position): costs are >= 0, so their IEEE bit
+        // patterns order like the values; three REDUX.MIN steps pick the
+        // smallest cost, then the earliest position among exact ties.
+        const unsigned long long key =
+            bo >= 0 ? static_cast<unsigned long long>(__double_as_longlong(bv)) : ~0ull;
+        const uint32_t khi = static_cast<uint32_t>(key >> 32), klo = static_cast<uint32_t>(key);
+        const uint32_t mhi = __reduce_min_sync(kFull, khi);
+        const uint32_t mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xffffffffu);
+        const bool tie = khi == mhi && klo == mlo;
+        const uint32_t mbo = __reduce_min_sync(kFull, tie ? static_cast<uint32_t>(bo) : 0xffffffffu);
+        if (mhi != 0xffffffffu || mlo != 0xffffffffu) {  // else: no open in-neighbour, not checked
+          const int src = __ffs(__ballot_sync(kFull, tie && static_cast<uint32_t>(bo) == mbo)) - 1;
+          bv = __shfl_sync(kFull, bv, src);
+          by = __shfl_sync(kFull, by, src);
+          const int64_t be = e0 + mbo;
           ++my_checks;
           const int32_t pid = I.in_path ? __ldg(I.in_path + be) : -1;
-          if (motion_free_warp(I, bx, by, x, pid, lane, seg)) {
+          bool ok;
+          if (pid < 0) {
+            if (lane < d) seg[lane] = __ldg(I.coords + static_cast<int64_t>(by) * d + lane);
+            __syncwarp();
+            ok = segment_free_staged(d, bx, lane, seg);
+          } else {
+            ok = motion_free_warp(I, bx, by, x, pid, lane, seg);
+          }
+          if (ok) {
             ++my_added;
             if (lane < CS) {
               remote<CS>(cost_s, lane)[x] = bv;
