@@ -434,7 +434,7 @@ int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, int cluster, size_
   if (max_d > kMaxSolveDim)
     return set_error(GMT_E_INVALID_INPUT, "dimension above 16 is not supported");
   const bool parent_smem = cluster > 1;
-  const size_t obs_bytes = sizeof(double) * 2 * static_cast<size_t>(max_nb) * max_d;
+  const size_t obs_bytes = sizeof(double) * 4 * static_cast<size_t>(max_nb) * max_d;
   *obs_in_smem = obs_bytes <= 48 * 1024 ? 1 : 0;
   SolveLayout L = solve_layout(max_n, max_d, max_nb, *obs_in_smem != 0, parent_smem);
   if (L.total > ctx->smem_optin && *obs_in_smem) {
@@ -492,7 +492,7 @@ int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, b
 }
 
 int launch_jobs(gmt_ctx* ctx, const std::vector<SolveJob>& jobs, int cluster, int threads,
-                size_t smem, int obs_in_smem) {
+                size_t smem, int obs_in_smem, int dim) {
   const size_t bytes = sizeof(SolveJob) * jobs.size();
   GMT_TRY(ctx->jobs.reserve(bytes));
   GMT_TRY(ctx->pinned_jobs.reserve(bytes));
@@ -500,7 +500,7 @@ int launch_jobs(gmt_ctx* ctx, const std::vector<SolveJob>& jobs, int cluster, in
   GMT_CUDA(cudaMemcpyAsync(ctx->jobs.ptr, ctx->pinned_jobs.ptr, bytes, cudaMemcpyHostToDevice,
                            ctx->stream));
   GMT_CUDA(launch_solve(static_cast<const SolveJob*>(ctx->jobs.ptr), static_cast<int>(jobs.size()),
-                        cluster, threads, smem, obs_in_smem, ctx->stream));
+                        cluster, threads, smem, obs_in_smem, dim, ctx->stream));
   ++ctx->launches;
   return GMT_OK;
 }
@@ -563,7 +563,7 @@ int plan_on(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, double l
   const int cluster = ctx->cluster ? ctx->cluster : 8;
   int threads = ctx->threads ? ctx->threads : 512;
   if (cluster == 1 && threads > 256) threads = 256;  // batched-shape kernel bound
-  GMT_TRY(launch_jobs(ctx, {job}, cluster, threads, smem, obs));
+  GMT_TRY(launch_jobs(ctx, {job}, cluster, threads, smem, obs, D.dim));
   return download_result(ctx, res[0], D.n, out);
 }
 
@@ -611,6 +611,7 @@ struct gmt_batch {
   int obs = 0;
   int cluster = 1;
   int threads = 256;
+  int dim = 0;  // common dimension of the queries (0: mixed)
   ~gmt_batch() {
     res.release();
     jobs_mem.release();
@@ -638,6 +639,9 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
     max_d = std::max(max_d, inst->desc.dim);
     max_nb = std::max(max_nb, inst->desc.num_boxes);
   }
+  b->dim = insts[0]->desc.dim;
+  for (int q = 1; q < count; ++q)
+    if (insts[q]->desc.dim != b->dim) b->dim = 0;
   int rc = plan_smem(ctx, max_n, max_d, max_nb, ctx->batch_cluster, &b->smem, &b->obs);
   if (rc == GMT_OK)
     rc = carve_results(b->res, count, b->node_off.data(), true, true, b->results, &b->scalars,
@@ -674,7 +678,7 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
 
 extern "C" int gmt_batch_launch(gmt_ctx* ctx, gmt_batch* b) {
   GMT_CUDA(launch_solve(static_cast<const SolveJob*>(b->jobs_mem.ptr), static_cast<int>(b->jobs.size()),
-                        b->cluster, b->threads, b->smem, b->obs, ctx->stream));
+                        b->cluster, b->threads, b->smem, b->obs, b->dim, ctx->stream));
   ++ctx->launches;
   return GMT_OK;
 }
@@ -806,7 +810,7 @@ extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double
   std::memcpy(ctx->pinned.ptr, descs.data(), sizeof(DevInstance) * count);
   GMT_TRY(put(o_desc, ctx->pinned.ptr, sizeof(DevInstance) * count));
   GMT_TRY(launch_jobs(ctx, jobs, ctx->batch_cluster, ctx->batch_threads ? ctx->batch_threads : 256,
-                      smem, obs));
+                      smem, obs, d));
 
   // Outputs.
   GMT_TRY(ctx->pinned2.reserve(sizeof(ResultScalars) * count));

@@ -2,7 +2,7 @@
 // planner.cpp:200-262) as ONE persistent kernel launch per query (or per
 // batch of queries).
 //
-// Execution model (DESIGN.md §3):
+// Execution model (DESIGN.md §4):
 //   * A query is solved by a thread-block cluster of CS CTAs (CS = 1 for
 //     batched solves, up to 16 for a single latency-critical query).
 //   * Every CTA keeps a full replica of the wavefront in shared memory:
@@ -18,15 +18,18 @@
 //   * P5 (connect_candidate) runs warp-per-candidate on the owner CTA: the
 //     lanes stream the candidate's in-row (col/cost, coalesced, 4 chunks in
 //     flight per lane, next row's offsets prefetched), gather cost[y]/open(y)
-//     from the local replica, reduce (cost, position) lexicographically (==
-//     the reference's strict-< first-in-list rule), then slab-test the single
-//     best edge with its endpoints staged in shared memory and the
-//     smem-staged boxes spread over the lanes.
+//     from the local replica, reduce (cost, position) lexicographically with
+//     three REDUX.MIN steps (== the reference's strict-< first-in-list rule),
+//     then slab-test the single best edge: endpoints staged in shared memory,
+//     boxes spread over the lanes, an exact-safe bounding-box separation test
+//     in registers before the division-based clip.
 //   * P6 (commit) writes the new cost into every replica (DSMEM stores) and
 //     sets a `newopen` bit; labels only change at the next pass start, so
 //     every candidate sees iteration-start labels exactly as in the
 //     reference's parallel map + serial commit.
 //   * Two cluster barriers per pass; no host round trip until the answer.
+// The kernel is specialised on the dimension D (0 = any d <= 16) so the
+// per-axis loops of the geometry unroll into registers.
 #include <cooperative_groups.h>
 
 #include <cstdint>
@@ -42,7 +45,8 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int32_t kNone = 0x7fffffff;
-constexpr int kUnroll = 4;  // row chunks in flight per lane
+constexpr int kUnroll = 4;        // row chunks in flight per lane
+constexpr double kSepMargin = 1e-9;  // see segment_free_staged
 
 struct CtaShared {
   double red_min[32];
@@ -56,12 +60,15 @@ struct CtaShared {
   int32_t feasible;
 };
 
-// Box access: box b, axis k at base[b*bs + k*as].
+// Boxes: box b, axis k at base[b*bs + k*as].  lom/him hold lo - m and
+// hi + m (the separation bounds) when the boxes are staged in shared memory.
 struct Boxes {
   const double* lo;
   const double* hi;
-  int bs;  // box stride
-  int as;  // axis stride
+  const double* lom;
+  const double* him;
+  int bs;
+  int as;
   int count;
 };
 
@@ -83,29 +90,111 @@ __device__ __forceinline__ T* remote(T* p, int rank) {
   }
 }
 
-// Closed boxes contain p (the loop of point_free, space.cpp:50-52), boxes
-// spread over the lanes.  p is warp-uniform (shared memory).
+template <int D>
+__device__ __forceinline__ int dims(int rt) {
+  return D > 0 ? D : rt;
+}
+
+// Bulk prefetch of a byte range into L2 by the TMA engine
+// (cp.async.bulk.prefetch.L2, sm_90+): one instruction per range, no
+// registers, no completion to wait for.  The range is widened to 16-byte
+// alignment as the instruction requires.
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  if (bytes == 0) return;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~static_cast<uintptr_t>(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~static_cast<uintptr_t>(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a),
+               "r"(static_cast<uint32_t>(e - a))
+               : "memory");
+}
+
+// Row prefetch for a work list: lane j of the warp takes entry k0 + j*step
+// (the entries this warp will process) and prefetches its CSR row span.
+__device__ __forceinline__ void prefetch_rows(const uint16_t* list, int k0, int step, int count,
+                                              const int64_t* ptr, const int32_t* col,
+                                              const double* cost, int lane) {
+  for (int k = k0 + lane * step; k < count; k += 32 * step) {
+    const int v = list[k];
+    const int64_t e0 = __ldg(ptr + v), e1 = __ldg(ptr + v + 1);
+    prefetch_l2(col + e0, sizeof(int32_t) * static_cast<size_t>(e1 - e0));
+    if (cost) prefetch_l2(cost + e0, sizeof(double) * static_cast<size_t>(e1 - e0));
+  }
+}
+
+// Closed box b contains p (Aabb::contains, space.cpp:11-16).
+template <int D>
+__device__ __forceinline__ bool box_has(const double* p, int d_rt, const Boxes& bx, int b) {
+  const int d = dims<D>(d_rt);
+  bool in = true;
+#pragma unroll
+  for (int k = 0; k < (D > 0 ? D : kMaxSolveDim); ++k) {
+    if (D > 0 || k < d) {
+      const double x = p[k];
+      in = in && !(x < bx.lo[b * bx.bs + k * bx.as] || x > bx.hi[b * bx.bs + k * bx.as]);
+    }
+  }
+  return in;
+}
+
+// Any box contains p (the loop of point_free, space.cpp:50-52), boxes spread
+// over the lanes.  p is warp-uniform (shared memory).
+template <int D>
 __device__ __forceinline__ bool any_box_contains(const double* p, int d, const Boxes& bx, int lane) {
   bool in = false;
-  for (int b = lane; b < bx.count && !in; b += kWarp) {
-    bool c = true;
-    for (int k = 0; k < d; ++k) {
-      const double x = p[k];
-      if (x < bx.lo[b * bx.bs + k * bx.as] || x > bx.hi[b * bx.bs + k * bx.as]) {
-        c = false;
-        break;
-      }
-    }
-    in = c;
-  }
+  for (int b = lane; b < bx.count && !in; b += kWarp) in = box_has<D>(p, d, bx, b);
   return __any_sync(kFull, in);
 }
 
-// segment_free (space.cpp:80-90) of the closed segment [A, B] (global
-// memory).  The endpoints are staged in the warp's `seg` scratch
-// (a = seg[0..15], b = seg[16..31]); the coordinate predicates are
-// evaluated lane-per-axis, the boxes lane-per-box.
-__device__ bool segment_free_staged(int d, const Boxes& bx, int lane, const double* seg) {
+// segment_hits_box (space.cpp:60-78), closed slab clipping, axis loop
+// unrolled for a fixed dimension.
+template <int D>
+__device__ __forceinline__ bool clip_hits(const double* a, const double* b, int d_rt,
+                                          const double* lo, const double* hi, int st) {
+  const int d = dims<D>(d_rt);
+  double tmin = 0.0, tmax = 1.0;
+  // Not unrolled: the clip only runs for boxes that survive the separation
+  // pre-test, and its divisions are register-hungry.
+#pragma unroll 1
+  for (int k = 0; k < d; ++k) {
+    const double dk = __dsub_rn(b[k], a[k]);
+    const double l = lo[k * st], h = hi[k * st];
+    if (dk == 0.0) {
+      if (a[k] < l || a[k] > h) return false;
+    } else {
+      double t0 = __ddiv_rn(__dsub_rn(l, a[k]), dk);
+      double t1 = __ddiv_rn(__dsub_rn(h, a[k]), dk);
+      if (t0 > t1) {
+        const double t = t0;
+        t0 = t1;
+        t1 = t;
+      }
+      tmin = (tmin < t0) ? t0 : tmin;  // std::max(tmin, t0)
+      tmax = (t1 < tmax) ? t1 : tmax;  // std::min(tmax, t1)
+      if (tmin > tmax) return false;
+    }
+  }
+  return true;
+}
+
+// segment_free (space.cpp:80-90) of the segment staged in the warp's `seg`
+// scratch (a = seg[0..15], b = seg[16..31]).  Coordinate predicates run
+// lane-per-axis, boxes lane-per-box.
+//
+// Exact-safe separation pre-test (no division): if on some axis both
+// endpoints lie below lo - m or above hi + m (m = 1e-9), the reference's
+// floating-point slab clip (space.cpp:60-78) reports a miss.  Proof sketch:
+// a, b are in the unit cube here, so |dk| <= 1.  For b < a < lo - m or
+// b > a > hi + m both rounded slab parameters are strictly negative; for
+// a < b < lo - m or a > b > hi + m both exceed
+// (1 + m)(1 - 2^-53)/(1 + 2^-53) > 1; either way tmin > tmax on that axis.
+// The clip's outcome does not depend on the axis order (the running max/min
+// of the slab ends are order-free and emptiness is monotone), and dk == 0
+// is the clip's own early miss.  (fl(lo - m) differs from lo - m by at most
+// 2^-53 |lo|, which only matters for |lo| > 1 where lo - b > 1 anyway.)
+// Boxes that pass the pre-test go through the exact clip.
+template <int D>
+__device__ bool segment_free_staged(int d_rt, const Boxes& bx, int lane, const double* seg) {
+  const int d = dims<D>(d_rt);
   const double* a = seg;
   const double* b = seg + 16;
   bool eq = true, cube_a = true, cube_b = true;
@@ -117,42 +206,61 @@ __device__ bool segment_free_staged(int d, const Boxes& bx, int lane, const doub
   }
   const bool same = __all_sync(kFull, eq);
   const bool in_a = __all_sync(kFull, cube_a);
-  if (same) return in_a && !any_box_contains(a, d, bx, lane);  // point_free(a)
+  if (same) return in_a && !any_box_contains<D>(a, d, bx, lane);  // point_free(a)
   if (!in_a || !__all_sync(kFull, cube_b)) return false;
+  // Segment bounding box: registers for a fixed small dimension, the staged
+  // endpoints otherwise.
+  constexpr int kReg = (D > 0 && D <= 6) ? D : 1;
+  double mn[kReg], mx[kReg];
+  if constexpr (D > 0 && D <= 6) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double x = a[k], y = b[k];
+      mn[k] = x < y ? x : y;
+      mx[k] = x < y ? y : x;
+    }
+  }
   bool hit = false;
   for (int i = lane; i < bx.count && !hit; i += kWarp) {
-    const double* lo = bx.lo + i * bx.bs;
-    const double* hi = bx.hi + i * bx.bs;
-    // Exact-safe separation pre-test (no division): if on some axis both
-    // endpoints lie below lo - m or above hi + m (m = 1e-9), the reference's
-    // floating-point slab clip (space.cpp:60-78) reports a miss.  Proof
-    // sketch: a, b are in the unit cube here, so |dk| <= 1; for b < a < lo - m
-    // or b > a > hi + m (and dk > 0 mirrored) both rounded slab parameters
-    // are strictly negative, and for a < b < lo - m (or a > b > hi + m) both
-    // exceed (1 + m)(1 - 2^-53)/(1 + 2^-53) > 1, so tmin > tmax on that axis;
-    // the clip's outcome does not depend on the axis order (max/min of the
-    // slab ends are order-free and emptiness is monotone).  dk == 0 is the
-    // clip's own early miss.  Boxes that pass go through the exact clip.
     bool sep = false;
-    for (int k = 0; k < d && !sep; ++k) {
-      const double x = a[k], y = b[k];
-      const double l = lo[k * bx.as], h = hi[k * bx.as];
-      sep = (x < l - 1e-9 && y < l - 1e-9) || (x > h + 1e-9 && y > h + 1e-9);
+#pragma unroll
+    for (int k = 0; k < (D > 0 ? D : kMaxSolveDim); ++k) {
+      if (D == 0 && k >= d) break;
+      double lo_k, hi_k;
+      if (bx.lom) {
+        lo_k = bx.lom[i * bx.bs + k * bx.as];
+        hi_k = bx.him[i * bx.bs + k * bx.as];
+      } else {
+        lo_k = bx.lo[i * bx.bs + k * bx.as] - kSepMargin;
+        hi_k = bx.hi[i * bx.bs + k * bx.as] + kSepMargin;
+      }
+      double smin, smax;
+      if constexpr (D > 0 && D <= 6) {
+        smin = mn[k];
+        smax = mx[k];
+      } else {
+        const double x = a[k], y = b[k];
+        smin = x < y ? x : y;
+        smax = x < y ? y : x;
+      }
+      sep = sep || smax < lo_k || smin > hi_k;
     }
-    if (!sep) hit = segment_hits_box(a, b, d, lo, hi, bx.as);
+    if (!sep) hit = clip_hits<D>(a, b, d, bx.lo + i * bx.bs, bx.hi + i * bx.bs, bx.as);
   }
   return !__any_sync(kFull, hit);
 }
 
+template <int D>
 __device__ bool segment_free_warp(const double* A, const double* B, int d, const Boxes& bx,
                                   int lane, double* seg) {
   __syncwarp();
   if (lane < d) seg[lane] = A[lane];
   if (lane >= 16 && lane - 16 < d) seg[lane] = B[lane - 16];
   __syncwarp();
-  return segment_free_staged(d, bx, lane, seg);
+  return segment_free_staged<D>(d, bx, lane, seg);
 }
 
+template <int D>
 __device__ bool point_free_warp(const double* P, int d, const Boxes& bx, int lane, double* seg) {
   __syncwarp();
   if (lane < d) seg[lane] = P[lane];
@@ -160,25 +268,21 @@ __device__ bool point_free_warp(const double* P, int d, const Boxes& bx, int lan
   bool cube = true;
   if (lane < d) cube = !(seg[lane] < 0.0 || seg[lane] > 1.0);
   if (!__all_sync(kFull, cube)) return false;
-  return !any_box_contains(seg, d, bx, lane);
+  return !any_box_contains<D>(seg, d, bx, lane);
 }
 
-// motion_free (planner.cpp:54-60): cached polyline for path edges, exact
-// clipping for straight edges.
-__device__ bool motion_free_warp(const DevInstance& I, const Boxes& bx, int from, int to,
-                                 int32_t pid, int lane, double* seg) {
-  const int d = I.dim;
-  if (pid >= 0) {
-    const int64_t a = I.path_ptr[pid], b = I.path_ptr[pid + 1];
-    const double* pts = I.path_pts + a * d;
-    if (b - a == 1) return point_free_warp(pts, d, bx, lane, seg);
-    for (int64_t s = 0; s + 1 < b - a; ++s) {
-      if (!segment_free_warp(pts + s * d, pts + (s + 1) * d, d, bx, lane, seg)) return false;
-    }
-    return true;
+// motion_free (planner.cpp:54-60) for a path edge: the cached polyline,
+// every sub-segment through the exact test (polyline_free, space.cpp:92-99).
+template <int D>
+__device__ bool polyline_free_warp(const DevInstance& I, int d, const Boxes& bx, int32_t pid,
+                                   int lane, double* seg) {
+  const int64_t a = I.path_ptr[pid], b = I.path_ptr[pid + 1];
+  const double* pts = I.path_pts + a * d;
+  if (b - a == 1) return point_free_warp<D>(pts, d, bx, lane, seg);
+  for (int64_t s = 0; s + 1 < b - a; ++s) {
+    if (!segment_free_warp<D>(pts + s * d, pts + (s + 1) * d, d, bx, lane, seg)) return false;
   }
-  return segment_free_warp(I.coords + static_cast<int64_t>(from) * d,
-                           I.coords + static_cast<int64_t>(to) * d, d, bx, lane, seg);
+  return true;
 }
 
 __device__ __forceinline__ double block_min(double v, double* red, int lane, int warp, int nw) {
@@ -225,8 +329,11 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 
 // Batched solves (CS == 1) want several small CTAs per SM; single-query
 // clusters want one wide CTA per SM.
-template <int CS>
-__global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
+template <int CS, int D>
+#ifndef GMT_BATCH_MIN_BLOCKS
+#define GMT_BATCH_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? GMT_BATCH_MIN_BLOCKS : 1)
     gmt_solve_kernel(const SolveJob* __restrict__ jobs, int obs_in_smem) {
   constexpr bool kParentSmem = CS > 1;  // batched solves keep parents in HBM
   constexpr int kMaxWarps = CS == 1 ? 8 : 16;
@@ -237,10 +344,20 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
   const int q = blockIdx.x / CS;
   int rank = 0;
   if constexpr (CS > 1) rank = static_cast<int>(cg::this_cluster().block_rank());
-  const SolveJob job = jobs[q];
-  const DevInstance I = *job.inst;
-  const DevResult R = job.res;
-  const int n = I.n, d = I.dim, nb = I.num_boxes;
+  // The job, instance and result descriptors live in shared memory: their
+  // ~30 pointers are reloaded (LDS, broadcast) where used instead of pinning
+  // registers for the whole solve.
+  __shared__ SolveJob job_s;
+  __shared__ DevInstance inst_s;
+  if (threadIdx.x == 0) {
+    job_s = jobs[q];
+    inst_s = *job_s.inst;
+  }
+  __syncthreads();
+  const SolveJob& job = job_s;
+  const DevInstance& I = inst_s;
+  const DevResult& R = job_s.res;
+  const int n = I.n, d = dims<D>(I.dim), nb = I.num_boxes;
   const SolveLayout L = solve_layout(n, d, nb, obs_in_smem != 0, kParentSmem);
   const int W = L.words;
 
@@ -261,16 +378,22 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
   Boxes bx;
   bx.count = nb;
   if (obs_in_smem) {
+    // Stage the boxes axis-major, with the separation bounds lo - m, hi + m.
     double* lo = reinterpret_cast<double*>(smem + L.off_obs);
     double* hi = lo + static_cast<size_t>(nb) * d;
+    double* lom = hi + static_cast<size_t>(nb) * d;
+    double* him = lom + static_cast<size_t>(nb) * d;
     for (int idx = tid; idx < nb * d; idx += nt) {
       const int b = idx / d, k = idx - b * d;
-      lo[k * nb + b] = I.box_lo[idx];
-      hi[k * nb + b] = I.box_hi[idx];
+      const double l = I.box_lo[idx], h = I.box_hi[idx];
+      lo[k * nb + b] = l;
+      hi[k * nb + b] = h;
+      lom[k * nb + b] = l - kSepMargin;
+      him[k * nb + b] = h + kSepMargin;
     }
-    bx.lo = lo, bx.hi = hi, bx.bs = 1, bx.as = nb;
+    bx.lo = lo, bx.hi = hi, bx.lom = lom, bx.him = him, bx.bs = 1, bx.as = nb;
   } else {
-    bx.lo = I.box_lo, bx.hi = I.box_hi, bx.bs = d, bx.as = 1;
+    bx.lo = I.box_lo, bx.hi = I.box_hi, bx.lom = nullptr, bx.him = nullptr, bx.bs = d, bx.as = 1;
   }
 
   // make_wavefront (planner.cpp:25-35) on every replica.
@@ -307,7 +430,7 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
   // infeasible_input (planner.cpp:39-41, 108): empty tree.
   if (warp == 0) {
     const bool ok = I.goal_count > 0 &&
-                    point_free_warp(I.coords + static_cast<int64_t>(init) * d, d, bx, lane, seg);
+                    point_free_warp<D>(I.coords + static_cast<int64_t>(init) * d, d, bx, lane, seg);
     if (lane == 0) sh.feasible = ok ? 1 : 0;
   }
   __syncthreads();
@@ -330,6 +453,17 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
   if (tid == 0) {
     cost_s[init] = 0.0;
     open_w[init >> 5] |= 1u << (init & 31);
+  }
+  // The coordinates are read once per lazy check (both endpoints): make the
+  // whole array L2-resident up front (each CTA of a cluster takes a slice).
+  if (tid == 0) {
+    const size_t bytes = sizeof(double) * static_cast<size_t>(n) * d;
+    const size_t slice = (bytes / CS + 15) & ~static_cast<size_t>(15);
+    const size_t off = slice * rank;
+    if (off < bytes) {
+      prefetch_l2(reinterpret_cast<const char*>(I.coords) + off,
+                  off + slice < bytes ? slice : bytes - off);
+    }
   }
   cluster_barrier<CS>();  // every replica initialised before any remote access
 
@@ -433,6 +567,7 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
     // (planner.cpp:159-166).
     {
       const int own = sh.own_count;
+      prefetch_rows(list, warp, nw, own, I.out_ptr, I.out_col, nullptr, lane);
       int k = warp;
       int64_t e0 = 0, e1 = 0;
       if (k < own) {
@@ -500,6 +635,7 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
     }
     __syncthreads();
     const int ccount = sh.cand_count;
+    prefetch_rows(list, warp, nw, ccount, I.in_ptr, I.in_col, I.in_cost, lane);
 
     // P5 + P6: connect_candidate (planner.cpp:62-90) and commit (178-189).
     int my_checks = 0, my_added = 0;
@@ -577,12 +713,12 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
           ++my_checks;
           const int32_t pid = I.in_path ? __ldg(I.in_path + be) : -1;
           bool ok;
-          if (pid < 0) {
+          if (pid < 0) {  // straight edge: segment_free (planner.cpp:59)
             if (lane < d) seg[lane] = __ldg(I.coords + static_cast<int64_t>(by) * d + lane);
             __syncwarp();
-            ok = segment_free_staged(d, bx, lane, seg);
-          } else {
-            ok = motion_free_warp(I, bx, by, x, pid, lane, seg);
+            ok = segment_free_staged<D>(d, bx, lane, seg);
+          } else {  // cached path: polyline_free (planner.cpp:56-58)
+            ok = polyline_free_warp<D>(I, d, bx, pid, lane, seg);
           }
           if (ok) {
             ++my_added;
@@ -703,10 +839,10 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? 4 : 1)
   }
 }
 
-template <int CS>
+template <int CS, int D>
 static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_t smem,
                              int obs_in_smem, cudaStream_t stream) {
-  auto kern = gmt_solve_kernel<CS>;
+  auto kern = gmt_solve_kernel<CS, D>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;
@@ -731,14 +867,25 @@ static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_
   return cudaLaunchKernelEx(&cfg, kern, jobs, obs_in_smem);
 }
 
+template <int CS>
+static cudaError_t launch_dim(const SolveJob* jobs, int count, int threads, size_t smem,
+                              int obs_in_smem, int dim, cudaStream_t stream) {
+  switch (dim) {
+    case 2: return launch_cs<CS, 2>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 3: return launch_cs<CS, 3>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 6: return launch_cs<CS, 6>(jobs, count, threads, smem, obs_in_smem, stream);
+    default: return launch_cs<CS, 0>(jobs, count, threads, smem, obs_in_smem, stream);
+  }
+}
+
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
-                         int obs_in_smem, cudaStream_t stream) {
+                         int obs_in_smem, int dim, cudaStream_t stream) {
   switch (cluster) {
-    case 1: return launch_cs<1>(jobs, count, threads, smem, obs_in_smem, stream);
-    case 2: return launch_cs<2>(jobs, count, threads, smem, obs_in_smem, stream);
-    case 4: return launch_cs<4>(jobs, count, threads, smem, obs_in_smem, stream);
-    case 8: return launch_cs<8>(jobs, count, threads, smem, obs_in_smem, stream);
-    case 16: return launch_cs<16>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 1: return launch_dim<1>(jobs, count, threads, smem, obs_in_smem, dim, stream);
+    case 2: return launch_dim<2>(jobs, count, threads, smem, obs_in_smem, dim, stream);
+    case 4: return launch_dim<4>(jobs, count, threads, smem, obs_in_smem, dim, stream);
+    case 8: return launch_dim<8>(jobs, count, threads, smem, obs_in_smem, dim, stream);
+    case 16: return launch_dim<16>(jobs, count, threads, smem, obs_in_smem, dim, stream);
     default: return cudaErrorInvalidValue;
   }
 }

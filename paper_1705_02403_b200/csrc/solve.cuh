@@ -22,7 +22,7 @@ constexpr int kMaxSolveDim = 16;
 //                      parents in HBM and walk them once at the end)
 //   bits   6 x u32[Wp] open, closed, group, newopen, cand, goal
 //   list   u16[32W]    owned group members (P4) / owned candidates (P5)
-//   obs    f64[2*B*d]  boxes, axis-major (SoA) when they fit
+//   obs    f64[4*B*d]  boxes lo, hi, lo - m, hi + m, axis-major (SoA), when they fit
 struct SolveLayout {
   int words;
   int words_pad;
@@ -45,12 +45,14 @@ __host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool o
   L.off_list = off;
   off = align16(off + sizeof(uint16_t) * nodes);
   L.off_obs = off;
-  if (obs_smem) off = align16(off + sizeof(double) * 2 * static_cast<size_t>(nb) * d);
+  if (obs_smem) off = align16(off + sizeof(double) * 4 * static_cast<size_t>(nb) * d);
   L.total = off;
   return L;
 }
 
+// dim: the common dimension of every job (selects the specialised kernel;
+// 0 = generic).
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
-                         int obs_in_smem, cudaStream_t stream);
+                         int obs_in_smem, int dim, cudaStream_t stream);
 
 }  // namespace gmtb

@@ -15,7 +15,8 @@ from . import abi
 from .errors import raise_for
 from .graph import Graph
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgmt_b200.so")
+LIB_PATH = os.environ.get("GMT_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libgmt_b200.so")
 
 _dp = C.POINTER(C.c_double)
 _i32p = C.POINTER(C.c_int32)
