@@ -149,7 +149,23 @@ typedef struct gmt_plan_summary {
   int32_t num_stats;
 } gmt_plan_summary;
 
-/* ProblemFile (problem.hpp:17-29) minus the Dubins steering fields. */
+/* Steering models.  GMT_STEER_EUCLIDEAN is the reference's euclidean model
+ * (steering.hpp:10); GMT_STEER_DOUBLE_INTEGRATOR is the NEW 6D double
+ * integrator of SURVEY.md §8 row a22 (no reference):
+ * state [p(3), s(3)] in [0,1]^6 with velocity v = vmax (2s - 1), cost
+ * tau + weight * integral |u|^2, directed edges, `segments`-segment
+ * trajectory polylines for the lazy check.                                 */
+typedef enum gmt_steering { GMT_STEER_EUCLIDEAN = 0, GMT_STEER_DOUBLE_INTEGRATOR = 2 } gmt_steering;
+
+typedef struct gmt_di_params {
+  double vmax;
+  double weight;
+  int32_t segments;
+  int32_t reserved;
+} gmt_di_params;
+
+/* ProblemFile (problem.hpp:17-29) minus the Dubins steering fields, plus the
+ * double-integrator model (radius_override is required for it).          */
 typedef struct gmt_problem {
   gmt_scene scene;
   const double* init;     /* dim coords */
@@ -160,6 +176,9 @@ typedef struct gmt_problem {
   double eta;
   double radius_override; /* <= 0: use connection_radius (problem.cpp:342-351) */
   gmt_sample_source sampling;
+  int32_t steering;       /* gmt_steering */
+  int32_t reserved;
+  gmt_di_params di;
 } gmt_problem;
 
 typedef struct gmt_ctx gmt_ctx;
@@ -220,6 +239,22 @@ int gmt_append_init(gmt_ctx* ctx, int32_t dim, double* coords, double* heading, 
 int gmt_build_neighbor_graph(gmt_ctx* ctx, const double* coords, int32_t n, int32_t dim,
                              double radius, int64_t* num_edges, int64_t* out_ptr,
                              int32_t* out_col, double* out_cost);
+
+/* Double-integrator steering (NEW, row a22): cost and duration of `count`
+ * state pairs x0s[i*6..], x1s[i*6..], evaluated on the device.           */
+int gmt_di_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count,
+                 const gmt_di_params* params, double* cost_out, double* tau_out);
+
+/* Directed double-integrator r-disk graph over 6D samples, built on the
+ * device in NeighborGraph conventions (graph.cpp:117-188): out-rows sorted
+ * by target, in-rows by source, path ids = out-edge indices
+ * (graph.cpp:172-183).  Two-call pattern (NULL out_ptr: count only).
+ * out_tau / in_path / path_pts (E*(segments+1)*6 waypoints, the degenerate
+ * zero-duration edge repeating its state) may be NULL.                   */
+int gmt_build_di_graph(gmt_ctx* ctx, const double* coords, int32_t n, const gmt_di_params* params,
+                       double radius, int64_t* num_edges, int64_t* out_ptr, int32_t* out_col,
+                       double* out_cost, double* out_tau, int64_t* in_ptr, int32_t* in_col,
+                       double* in_cost, int32_t* in_path, double* path_pts);
 
 /* ---- device-resident instances (ProblemInstance, problem.hpp:52-57) --- */
 /* Upload host samples + graph + scene.  goal_count is samples.goal_indices

@@ -184,6 +184,79 @@ class _Lib:
         return buf.result()
 
 
+class PortLib(_Lib):
+    """The C restatement, plus its statement of the NEW double-integrator
+    model (no reference exists for it)."""
+
+    def __init__(self):
+        super().__init__(PORT_SO, "oracle_")
+        L = self.lib
+        L.oracle_di_cost.restype = C.c_double
+        L.oracle_di_cost.argtypes = [_dp, _dp, C.c_double, C.c_double, _dp]
+        L.oracle_di_coord.restype = C.c_double
+        L.oracle_di_coord.argtypes = [_dp, _dp, C.c_double, C.c_int, C.c_int, C.c_int, C.c_double]
+        L.oracle_di_paths.restype = None
+        L.oracle_di_paths.argtypes = [_dp, C.c_int32, _i64p, _i32p, _dp, C.c_int, C.c_double, _dp]
+        L.oracle_build_di_graph.restype = C.c_int
+        L.oracle_build_di_graph.argtypes = [_dp, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                            _i64p, _i64p, _i32p, _dp, _dp]
+
+    def di_cost(self, x0, x1, vmax=0.5, weight=1.0):
+        x0, x1 = abi.f64(x0), abi.f64(x1)
+        t = C.c_double()
+        c = self.lib.oracle_di_cost(abi.ptr(x0, C.c_double), abi.ptr(x1, C.c_double), vmax, weight,
+                                    C.byref(t))
+        return c, t.value
+
+    def di_waypoints(self, x0, x1, tau, segments=8, vmax=0.5):
+        x0, x1 = abi.f64(x0), abi.f64(x1)
+        return np.array([[self.lib.oracle_di_coord(abi.ptr(x0, C.c_double), abi.ptr(x1, C.c_double),
+                                                   tau, k, i, segments, vmax) for i in range(6)]
+                         for k in range(segments + 1)])
+
+    def build_di_graph(self, coords, radius, vmax=0.5, weight=1.0):
+        """-> (out_ptr, out_col, out_cost, out_tau)"""
+        coords = abi.f64(coords)
+        n = coords.shape[0]
+        ne = C.c_int64()
+        self._check(self.lib.oracle_build_di_graph(abi.ptr(coords, C.c_double), n, vmax, weight,
+                                                   radius, C.byref(ne), abi.ptr(None, C.c_int64),
+                                                   abi.ptr(None, C.c_int32),
+                                                   abi.ptr(None, C.c_double),
+                                                   abi.ptr(None, C.c_double)))
+        E = ne.value
+        ptr = np.zeros(n + 1, np.int64)
+        col = np.zeros(max(E, 1), np.int32)
+        cost, tau = np.zeros(max(E, 1)), np.zeros(max(E, 1))
+        self._check(self.lib.oracle_build_di_graph(abi.ptr(coords, C.c_double), n, vmax, weight,
+                                                   radius, C.byref(ne), abi.ptr(ptr, C.c_int64),
+                                                   abi.ptr(col, C.c_int32),
+                                                   abi.ptr(cost, C.c_double),
+                                                   abi.ptr(tau, C.c_double)))
+        return ptr, col[:E], cost[:E], tau[:E]
+
+    def di_graph(self, coords, radius, segments=8, vmax=0.5, weight=1.0):
+        """Reference-shaped directed Graph with cached waypoint paths (path
+        ids = out-edge indices, in-lists by ascending source)."""
+        from paper_1705_02403_b200.graph import Graph
+        ptr, col, cost, tau = self.build_di_graph(coords, radius, vmax, weight)
+        n, E, M1 = coords.shape[0], len(col), segments + 1
+        pts = np.zeros((max(E, 1), M1, 6))
+        coords = abi.f64(coords)
+        self.lib.oracle_di_paths(abi.ptr(coords, C.c_double), n, abi.ptr(ptr, C.c_int64),
+                                 abi.ptr(abi.i32(col), C.c_int32), abi.ptr(abi.f64(tau), C.c_double),
+                                 segments, vmax, abi.ptr(pts, C.c_double))
+        g = Graph(n, radius, ptr, col, cost, dim=6, directed=True,
+                  out_path=np.arange(E, dtype=np.int32),
+                  path_ptr=np.arange(E + 1, dtype=np.int64) * M1,
+                  path_pts=pts[:E].reshape(-1))
+        in_ptr, in_col, in_cost, in_path = g.transpose()
+        g.in_ptr, g.in_col, g.in_cost, g.in_path = (abi.i64(in_ptr), abi.i32(in_col),
+                                                     abi.f64(in_cost), abi.i32(in_path))
+        g.out_tau = tau
+        return g
+
+
 class RefLib(_Lib):
     """The unmodified reference (plus its test-support oracles)."""
 
@@ -379,10 +452,10 @@ _port = None
 _ref = None
 
 
-def port() -> _Lib:
+def port() -> PortLib:
     global _port
     if _port is None:
-        _port = _Lib(PORT_SO, "oracle_")
+        _port = PortLib()
     return _port
 
 

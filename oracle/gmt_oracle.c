@@ -698,3 +698,127 @@ int oracle_fmt_plan(const gmt_scene* s, const double* coords, int32_t n, int32_t
   free(label), free(cost), free(parent), free(iter_added), free(results);
   return GMT_OK;
 }
+
+/* ---- 6D double integrator (NEW model; no reference exists) ----
+ * Independent C statement of the model the B200 library defines in
+ * paper_1705_02403_b200/csrc/di.cuh: parity of this model
+ * against the reference is UNPINNED; it is pinned by properties
+ * (tests/test_di.py: Gramian-form cost, stationarity, brute-force duration
+ * scan) and the planner on top of it is pinned against the reference's
+ * gmt_plan on the injected directed graph with cached paths. */
+static double di_vel(double s, double vmax) { return vmax * (2.0 * s - 1.0); }
+
+typedef struct {
+  double a, b, c0;
+} di_coef_t;
+
+static di_coef_t di_coef(const double* x0, const double* x1, double vmax, double w) {
+  double sa = 0.0, sb = 0.0, sc = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    double D = x1[k] - x0[k];
+    double v0 = di_vel(x0[3 + k], vmax), v1 = di_vel(x1[3 + k], vmax);
+    sa = sa + ((v0 * v0 + v0 * v1) + v1 * v1);
+    sb = sb + D * (v0 + v1);
+    sc = sc + D * D;
+  }
+  di_coef_t c;
+  c.a = (4.0 * w) * sa;
+  c.b = (-12.0 * w) * sb;
+  c.c0 = (12.0 * w) * sc;
+  return c;
+}
+
+static double di_g(di_coef_t c, double t) { return (((t * t - c.a) * t) - 2.0 * c.b) * t - 3.0 * c.c0; }
+static double di_c(di_coef_t c, double t) { return t + ((c.c0 / t + c.b) / t + c.a) / t; }
+
+double oracle_di_cost(const double* x0, const double* x1, double vmax, double w, double* tau) {
+  di_coef_t c = di_coef(x0, x1, vmax, w);
+  if (c.a == 0.0 && c.b == 0.0 && c.c0 == 0.0) {
+    *tau = 0.0;
+    return 0.0;
+  }
+  double T = c.a, b2 = 2.0 * (c.b < 0.0 ? -c.b : c.b), c3 = 3.0 * c.c0;
+  if (b2 > T) T = b2;
+  if (c3 > T) T = c3;
+  T = 1.0 + T;
+  double best_c = 0.0, best_t = 0.0;
+  int have = 0;
+  double t_hi = T, g_hi = di_g(c, t_hi);
+  for (int j = 1; j <= 96; ++j) {
+    double t_lo = t_hi * 0.75, g_lo = di_g(c, t_lo);
+    if (g_lo <= 0.0 && g_hi > 0.0) {
+      double lo = t_lo, hi = t_hi;
+      for (int it = 0; it < 64; ++it) {
+        double mid = 0.5 * (lo + hi);
+        if (di_g(c, mid) > 0.0) hi = mid; else lo = mid;
+      }
+      double ct = di_c(c, hi);
+      if (!have || ct <= best_c) {
+        best_c = ct;
+        best_t = hi;
+        have = 1;
+      }
+    }
+    t_hi = t_lo;
+    g_hi = g_lo;
+  }
+  if (!have) {
+    best_t = t_hi;
+    best_c = di_c(c, best_t);
+  }
+  *tau = best_t;
+  return best_c;
+}
+
+double oracle_di_coord(const double* x0, const double* x1, double tau, int k, int i, int M,
+                       double vmax) {
+  if (k <= 0 || tau == 0.0) return x0[i];
+  if (k >= M) return x1[i];
+  double t = (tau * (double)k) / (double)M;
+  int a = i < 3 ? i : i - 3;
+  double D = x1[a] - x0[a];
+  double v0 = di_vel(x0[3 + a], vmax), v1 = di_vel(x1[3 + a], vmax);
+  double tt = tau * tau;
+  double c2 = (3.0 * D) / tt - (2.0 * v0 + v1) / tau;
+  double c3 = (v0 + v1) / tt - (2.0 * D) / (tt * tau);
+  if (i < 3) return x0[a] + t * (v0 + t * (c2 + t * c3));
+  double v = v0 + t * (2.0 * c2 + t * (3.0 * c3));
+  return 0.5 * (v / vmax + 1.0);
+}
+
+/* Brute-force directed r-disk graph of the double integrator (out-rows:
+ * targets v != u with cost(u -> v) <= r, ascending) + per-edge durations. */
+int oracle_build_di_graph(const double* coords, int32_t n, double vmax, double w, double radius,
+                          int64_t* num_edges, int64_t* out_ptr, int32_t* out_col, double* out_cost,
+                          double* out_tau) {
+  int64_t e = 0;
+  for (int32_t u = 0; u < n; ++u) {
+    if (out_ptr) out_ptr[u] = e;
+    for (int32_t v = 0; v < n; ++v) {
+      if (v == u) continue;
+      double t;
+      double c = oracle_di_cost(coords + (int64_t)u * 6, coords + (int64_t)v * 6, vmax, w, &t);
+      if (!(c <= radius)) continue;
+      if (out_col) {
+        out_col[e] = v;
+        out_cost[e] = c;
+        out_tau[e] = t;
+      }
+      ++e;
+    }
+  }
+  if (out_ptr) out_ptr[n] = e;
+  *num_edges = e;
+  return GMT_OK;
+}
+
+/* Waypoints of every out-edge (pts[e][k][i], k = 0..M). */
+void oracle_di_paths(const double* coords, int32_t n, const int64_t* ptr, const int32_t* col,
+                     const double* tau, int M, double vmax, double* pts) {
+  for (int32_t u = 0; u < n; ++u)
+    for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e)
+      for (int k = 0; k <= M; ++k)
+        for (int i = 0; i < 6; ++i)
+          pts[(e * (M + 1) + k) * 6 + i] =
+              oracle_di_coord(coords + (int64_t)u * 6, coords + (int64_t)col[e] * 6, tau[e], k, i, M, vmax);
+}

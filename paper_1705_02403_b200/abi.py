@@ -111,6 +111,20 @@ class PlanSummary(C.Structure):
     ]
 
 
+STEER_EUCLIDEAN = 0
+STEER_DOUBLE_INTEGRATOR = 2
+
+
+class DiParams(C.Structure):
+    """gmt_di_params: 6D double integrator (NEW model)."""
+    _fields_ = [
+        ("vmax", C.c_double),
+        ("weight", C.c_double),
+        ("segments", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
 class Problem(C.Structure):
     _fields_ = [
         ("scene", Scene),
@@ -122,6 +136,9 @@ class Problem(C.Structure):
         ("eta", C.c_double),
         ("radius_override", C.c_double),
         ("sampling", SampleSource),
+        ("steering", C.c_int32),
+        ("reserved", C.c_int32),
+        ("di", DiParams),
     ]
 
 

@@ -19,8 +19,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgmt_b200.so")
 OBJ = os.path.join(ROOT, "build", "obj")
-SOURCES = ["solve.cu", "graph.cu", "sample.cu", "capi.cu"]
-HEADERS = ["common.cuh", "solve.cuh", "internal.cuh", "offline.cuh"]
+SOURCES = ["solve.cu", "graph.cu", "di_graph.cu", "sample.cu", "capi.cu"]
+HEADERS = ["common.cuh", "solve.cuh", "internal.cuh", "offline.cuh", "di.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
          "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),

@@ -44,6 +44,14 @@ struct DevInstance {
   const int32_t* in_path; // may be null (all exact edges)
   const int64_t* path_ptr;
   const double* path_pts;
+  // Double-integrator instances built on the device (steering == 2) keep
+  // each in-edge's duration instead of a cached polyline; the solve kernel
+  // regenerates the trajectory waypoints of the one edge it checks (di.cuh).
+  const double* in_tau;
+  int32_t steering;
+  int32_t di_segments;
+  double di_vmax;
+  double di_weight;
 };
 
 // Scalars of one PlanResult (planner.hpp:43-51).

@@ -1,0 +1,210 @@
+// di.cuh -- 6D double-integrator steering (NEW: the
+// reference has no double integrator, so this model is defined
+// here).
+//
+// State x = [p_0, p_1, p_2, s_0, s_1, s_2] in [0,1]^6: positions p and
+// normalised velocities s, v_k = vmax (2 s_k - 1).  Dynamics p'' = u, cost
+// J = tau + w * integral |u|^2 dt (the paper's "mixed time/quadratic control
+// effort").  For a fixed duration tau the minimum-effort
+// cost is, with D = p1 - p0 per axis,
+//   c(tau) = tau + a/tau + b/tau^2 + c0/tau^3,
+//   a = 4w sum(v0^2 + v0 v1 + v1^2), b = -12w sum D (v0 + v1), c0 = 12w sum D^2
+// and c'(tau) = 0  <=>  g(tau) = tau^4 - a tau^2 - 2 b tau - 3 c0 = 0.
+//
+// tau* (deterministic, +-*/ only, so host and device agree bit for bit):
+// every positive root lies below T = 1 + max(a, 2|b|, 3c0) (Cauchy); g is
+// sampled on the geometric grid T q^j (q = 3/4, j = 96 .. 0, ascending tau);
+// every sign change g <= 0 -> g > 0 (a local minimum of c) is refined by 64
+// bisection steps; tau* is the refined root with the smallest c (ties to the
+// smaller tau).  The optimal state trajectory is the cubic
+//   p(t) = p0 + v0 t + c2 t^2 + c3 t^3,  v(t) = v0 + 2 c2 t + 3 c3 t^2,
+//   c2 = 3D/tau^2 - (2 v0 + v1)/tau,  c3 = (v0 + v1)/tau^2 - 2D/tau^3,
+// discretised at t = tau k / M (k = 1..M-1) between the exact endpoint
+// states; the lazy check tests the polyline (the reference's
+// polyline_free, space.cpp:92-99), so velocities leaving [-vmax, vmax]
+// (normalised coordinates outside [0,1]) block the edge.
+#pragma once
+
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define GMT_HD __host__ __device__ __forceinline__
+#else
+#define GMT_HD inline
+#endif
+
+namespace gmtb {
+
+struct DiParams {
+  double vmax;     // velocity bound of the normalised velocity coordinates
+  double weight;   // control-effort weight w
+  int32_t segments;  // M: polyline segments per trajectory
+  int32_t reserved;
+};
+
+constexpr int kDiDim = 6;
+constexpr int kDiGrid = 96;
+constexpr int kDiBisect = 64;
+
+// Correctly rounded arithmetic without contraction on both sides.
+#if defined(__CUDA_ARCH__)
+GMT_HD double di_add(double a, double b) { return __dadd_rn(a, b); }
+GMT_HD double di_sub(double a, double b) { return __dsub_rn(a, b); }
+GMT_HD double di_mul(double a, double b) { return __dmul_rn(a, b); }
+GMT_HD double di_div(double a, double b) { return __ddiv_rn(a, b); }
+#else
+GMT_HD double di_add(double a, double b) {
+  volatile double r = a + b;
+  return r;
+}
+GMT_HD double di_sub(double a, double b) {
+  volatile double r = a - b;
+  return r;
+}
+GMT_HD double di_mul(double a, double b) {
+  volatile double r = a * b;
+  return r;
+}
+GMT_HD double di_div(double a, double b) {
+  volatile double r = a / b;
+  return r;
+}
+#endif
+
+GMT_HD double di_vel(double s, const DiParams& P) {  // v = vmax (2s - 1)
+  return di_mul(P.vmax, di_sub(di_mul(2.0, s), 1.0));
+}
+
+struct DiCoef {
+  double a, b, c0;
+};
+
+GMT_HD DiCoef di_coef(const double* x0, const double* x1, const DiParams& P) {
+  double sa = 0.0, sb = 0.0, sc = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    const double D = di_sub(x1[k], x0[k]);
+    const double v0 = di_vel(x0[3 + k], P), v1 = di_vel(x1[3 + k], P);
+    sa = di_add(sa, di_add(di_add(di_mul(v0, v0), di_mul(v0, v1)), di_mul(v1, v1)));
+    sb = di_add(sb, di_mul(D, di_add(v0, v1)));
+    sc = di_add(sc, di_mul(D, D));
+  }
+  DiCoef c;
+  c.a = di_mul(di_mul(4.0, P.weight), sa);
+  c.b = di_mul(di_mul(-12.0, P.weight), sb);
+  c.c0 = di_mul(di_mul(12.0, P.weight), sc);
+  return c;
+}
+
+// g(tau) = ((tau^2 - a) tau - 2b) tau - 3 c0
+GMT_HD double di_g(const DiCoef& c, double t) {
+  return di_sub(di_mul(di_sub(di_mul(di_sub(di_mul(t, t), c.a), t), di_mul(2.0, c.b)), t),
+                di_mul(3.0, c.c0));
+}
+
+// c(tau) = tau + ((c0/tau + b)/tau + a)/tau
+GMT_HD double di_c(const DiCoef& c, double t) {
+  return di_add(t, di_div(di_add(di_div(di_add(di_div(c.c0, t), c.b), t), c.a), t));
+}
+
+// Minimum cost and its duration; cost 0 / tau 0 for identical states at rest.
+GMT_HD double di_cost_tau(const double* x0, const double* x1, const DiParams& P, double* tau_out) {
+  const DiCoef c = di_coef(x0, x1, P);
+  if (c.a == 0.0 && c.b == 0.0 && c.c0 == 0.0) {
+    *tau_out = 0.0;
+    return 0.0;
+  }
+  double T = c.a;
+  const double b2 = di_mul(2.0, c.b < 0.0 ? -c.b : c.b);
+  const double c3 = di_mul(3.0, c.c0);
+  if (b2 > T) T = b2;
+  if (c3 > T) T = c3;
+  T = di_add(1.0, T);
+  // Geometric grid tau_j = T q^j (j = 0..kDiGrid, each point the rounded
+  // product of the previous one), walked from large to small tau; brackets
+  // [tau_{j+1}, tau_j] with g(tau_{j+1}) <= 0 < g(tau_j).  The choice (min c,
+  // ties to the smaller tau) does not depend on the walk direction.
+  double best_c = 0.0, best_t = 0.0;
+  bool have = false;
+  double t_hi = T;
+  double g_hi = di_g(c, t_hi);
+  for (int j = 1; j <= kDiGrid; ++j) {
+    const double t_lo = di_mul(t_hi, 0.75);
+    const double g_lo = di_g(c, t_lo);
+    if (g_lo <= 0.0 && g_hi > 0.0) {
+      double lo = t_lo, hi = t_hi;
+      for (int it = 0; it < kDiBisect; ++it) {
+        const double mid = di_mul(0.5, di_add(lo, hi));
+        if (di_g(c, mid) > 0.0) {
+          hi = mid;
+        } else {
+          lo = mid;
+        }
+      }
+      const double ct = di_c(c, hi);
+      if (!have || ct <= best_c) {  // later brackets have smaller tau
+        best_c = ct;
+        best_t = hi;
+        have = true;
+      }
+    }
+    t_hi = t_lo;
+    g_hi = g_lo;
+  }
+  if (!have) {  // g > 0 on the whole grid cannot happen for c0 > 0; be total
+    best_t = t_hi;
+    best_c = di_c(c, best_t);
+  }
+  *tau_out = best_t;
+  return best_c;
+}
+
+// State at time t on the optimal trajectory x0 -> x1 of duration tau
+// (normalised coordinates).  Callers pass the exact endpoints for t = 0, tau.
+GMT_HD void di_state_at(const double* x0, const double* x1, double tau, double t,
+                        const DiParams& P, double* out) {
+  for (int k = 0; k < 3; ++k) {
+    const double D = di_sub(x1[k], x0[k]);
+    const double v0 = di_vel(x0[3 + k], P), v1 = di_vel(x1[3 + k], P);
+    const double tt = di_mul(tau, tau);
+    const double c2 = di_sub(di_div(di_mul(3.0, D), tt), di_div(di_add(di_mul(2.0, v0), v1), tau));
+    const double c3 = di_sub(di_div(di_add(v0, v1), tt), di_div(di_mul(2.0, D), di_mul(tt, tau)));
+    // p(t) = p0 + t (v0 + t (c2 + t c3)),  v(t) = v0 + t (2 c2 + t 3 c3)
+    const double p = di_add(x0[k], di_mul(t, di_add(v0, di_mul(t, di_add(c2, di_mul(t, c3))))));
+    const double v = di_add(v0, di_mul(t, di_add(di_mul(2.0, c2), di_mul(t, di_mul(3.0, c3)))));
+    out[k] = p;
+    // s = (v / vmax + 1) / 2
+    out[3 + k] = di_mul(0.5, di_add(di_div(v, P.vmax), 1.0));
+  }
+}
+
+// Coordinate i (0..5) of waypoint k (0..M) of the edge trajectory; k = 0 / M
+// return the endpoint coordinates exactly.  The same operations as
+// di_state_at, one coordinate at a time (lane-parallel on the device).
+GMT_HD double di_coord(const double* x0, const double* x1, double tau, int k, int i,
+                       const DiParams& P) {
+  const int M = P.segments;
+  if (k <= 0 || tau == 0.0) return x0[i];
+  if (k >= M) return x1[i];
+  const double t = di_div(di_mul(tau, static_cast<double>(k)), static_cast<double>(M));
+  const int a = i < 3 ? i : i - 3;
+  const double D = di_sub(x1[a], x0[a]);
+  const double v0 = di_vel(x0[3 + a], P), v1 = di_vel(x1[3 + a], P);
+  const double tt = di_mul(tau, tau);
+  const double c2 = di_sub(di_div(di_mul(3.0, D), tt), di_div(di_add(di_mul(2.0, v0), v1), tau));
+  const double c3 = di_sub(di_div(di_add(v0, v1), tt), di_div(di_mul(2.0, D), di_mul(tt, tau)));
+  if (i < 3) return di_add(x0[a], di_mul(t, di_add(v0, di_mul(t, di_add(c2, di_mul(t, c3))))));
+  const double v = di_add(v0, di_mul(t, di_add(di_mul(2.0, c2), di_mul(t, di_mul(3.0, c3)))));
+  return di_mul(0.5, di_add(di_div(v, P.vmax), 1.0));
+}
+
+GMT_HD void di_waypoint(const double* x0, const double* x1, double tau, int k, const DiParams& P,
+                        double* out) {
+  for (int i = 0; i < kDiDim; ++i) out[i] = di_coord(x0, x1, tau, k, i, P);
+}
+
+// Number of states of an edge's polyline: a single state for the
+// degenerate zero-duration edge (the reference's convention for degenerate
+// steering, steering.cpp:78-81), else M + 1.
+GMT_HD int di_path_len(double tau, const DiParams& P) { return tau == 0.0 ? 1 : P.segments + 1; }
+
+}  // namespace gmtb

@@ -1,0 +1,361 @@
+// di_graph.cu -- the directed r-disk graph of the 6D double integrator
+// built on the device, in the reference's
+// NeighborGraph conventions (graph.cpp:117-188): out-row u = targets v != u
+// with cost(u -> v) <= r ascending, in-row x = sources u with
+// cost(u -> x) <= r ascending (the sequential merge order), path ids in
+// (source, target) order (graph.cpp:172-183).
+//
+// Kernels: warp per row, lanes over 32 consecutive columns, the steering
+// solve per pair (di.cuh), ballot + popc ordered compaction; a count pass,
+// an exclusive scan, a fill pass, for the out-rows and (roles swapped) the
+// in-rows; optionally every out-edge's waypoint polyline.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "common.cuh"
+#include "di.cuh"
+#include "internal.cuh"
+#include "offline.cuh"
+
+namespace gmtb {
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+#define GMT_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_error(_e, #call); \
+  } while (0)
+
+// Necessary condition for cost(x0 -> x1) <= r (no false rejections): the
+// effort term is >= 3w (2D - (v0+v1) tau)^2 / tau^3 per axis and tau <= r, so
+// |D| > vmax r + r^2 / (2 sqrt(3w)) on any axis rules the pair out.
+__device__ __forceinline__ bool di_may_connect(const double* x0, const double* x1, double bound) {
+  for (int k = 0; k < 3; ++k) {
+    const double D = x1[k] - x0[k];
+    if (D > bound || -D > bound) return false;
+  }
+  return true;
+}
+
+// SWAP = false: row r lists targets c with cost(r -> c) <= radius.
+// SWAP = true:  row r lists sources c with cost(c -> r) <= radius.
+template <bool SWAP, bool FILL>
+__global__ void __launch_bounds__(256) di_rows_kernel(const double* __restrict__ coords, int n,
+                                                      DiParams P, double radius, double bound,
+                                                      int64_t* __restrict__ counts,
+                                                      const int64_t* __restrict__ row_ptr,
+                                                      int32_t* __restrict__ col,
+                                                      double* __restrict__ cost,
+                                                      double* __restrict__ tau) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (blockDim.x >> 5) * gridDim.x;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    double xr[kDiDim];
+    for (int k = 0; k < kDiDim; ++k) xr[k] = __ldg(coords + static_cast<int64_t>(r) * kDiDim + k);
+    int64_t out = FILL ? row_ptr[r] : 0;
+    for (int base = 0; base < n; base += 32) {
+      const int c = base + lane;
+      bool keep = false;
+      double cc = 0.0, tc = 0.0;
+      if (c < n && c != r) {
+        double xc[kDiDim];
+        for (int k = 0; k < kDiDim; ++k) xc[k] = __ldg(coords + static_cast<int64_t>(c) * kDiDim + k);
+        const double* from = SWAP ? xc : xr;
+        const double* to = SWAP ? xr : xc;
+        if (di_may_connect(from, to, bound)) {
+          cc = di_cost_tau(from, to, P, &tc);
+          keep = cc <= radius;
+        }
+      }
+      const uint32_t m = __ballot_sync(kFull, keep);
+      if (FILL && keep) {
+        const int64_t slot = out + __popc(m & ((1u << lane) - 1u));
+        col[slot] = c;
+        cost[slot] = cc;
+        if (tau) tau[slot] = tc;
+      }
+      out += __popc(m);
+    }
+    if (!FILL && lane == 0) counts[r] = out;
+  }
+}
+
+// in_path[e] for in-edge (u -> x): the out-edge index of (u -> x), found by
+// binary search in u's sorted out-row (NeighborGraph::edge_path, graph.cpp:34-40).
+__global__ void in_path_kernel(const int64_t* __restrict__ in_ptr, const int32_t* __restrict__ in_col,
+                               const int64_t* __restrict__ out_ptr,
+                               const int32_t* __restrict__ out_col, int n,
+                               int32_t* __restrict__ in_path) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    for (int64_t e = in_ptr[x]; e < in_ptr[x + 1]; ++e) {
+      const int u = in_col[e];
+      int64_t lo = out_ptr[u], hi = out_ptr[u + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (out_col[mid] < x) lo = mid + 1; else hi = mid;
+      }
+      in_path[e] = static_cast<int32_t>(lo);
+    }
+  }
+}
+
+// Waypoints of every out-edge: path e = pts[e*(M+1)*6 ...] (M+1 states,
+// the degenerate zero-duration edge repeats its single state).
+__global__ void di_paths_kernel(const double* __restrict__ coords, const int64_t* __restrict__ out_ptr,
+                                const int32_t* __restrict__ out_col, const double* __restrict__ out_tau,
+                                int n, DiParams P, double* __restrict__ pts) {
+  const int M = P.segments;
+  for (int u = blockIdx.x; u < n; u += gridDim.x) {
+    const double* x0 = coords + static_cast<int64_t>(u) * kDiDim;
+    for (int64_t e = out_ptr[u] + threadIdx.x; e < out_ptr[u + 1]; e += blockDim.x) {
+      const double* x1 = coords + static_cast<int64_t>(out_col[e]) * kDiDim;
+      double* p = pts + e * (M + 1) * kDiDim;
+      for (int k = 0; k <= M; ++k) di_waypoint(x0, x1, out_tau[e], k, P, p + k * kDiDim);
+    }
+  }
+}
+
+__global__ void di_pairs_kernel(const double* __restrict__ x0s, const double* __restrict__ x1s,
+                                int64_t count, DiParams P, double* __restrict__ cost,
+                                double* __restrict__ tau) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double t;
+    cost[i] = di_cost_tau(x0s + i * kDiDim, x1s + i * kDiDim, P, &t);
+    tau[i] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) scan_rows_kernel(const int64_t* __restrict__ counts, int n,
+                                                         int64_t* __restrict__ row_ptr) {
+  __shared__ int64_t warp_sum[32];
+  __shared__ int64_t carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + tid;
+    const int64_t x = i < n ? counts[i] : 0;
+    int64_t incl = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = lane < (blockDim.x >> 5) ? warp_sum[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(kFull, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sum[lane] = w;
+    }
+    __syncthreads();
+    const int64_t before = carry + (warp > 0 ? warp_sum[warp - 1] : 0) + incl - x;
+    if (i < n) row_ptr[i] = before;
+    __syncthreads();
+    if (tid == blockDim.x - 1) carry = before + x;
+    __syncthreads();
+  }
+  if (tid == 0) row_ptr[n] = carry;
+}
+
+int rows_pass(gmt_ctx* ctx, bool swap, const double* coords, int n, const DiParams& P, double radius,
+              double bound, Arena& mem, DiRows* rows, bool with_tau) {
+  cudaStream_t s = ctx->stream;
+  const int blocks = std::max(1, std::min((n + 7) / 8, ctx->sm_count * 8));
+  Arena cnt;
+  int rc = cnt.reserve(sizeof(int64_t) * (n + 1));
+  if (rc) return rc;
+  int64_t* counts = static_cast<int64_t*>(cnt.ptr);
+  if (swap)
+    di_rows_kernel<true, false><<<blocks, 256, 0, s>>>(coords, n, P, radius, bound, counts, nullptr,
+                                                       nullptr, nullptr, nullptr);
+  else
+    di_rows_kernel<false, false><<<blocks, 256, 0, s>>>(coords, n, P, radius, bound, counts, nullptr,
+                                                        nullptr, nullptr, nullptr);
+  GMT_CUDA(cudaGetLastError());
+  Arena rp;
+  rc = rp.reserve(sizeof(int64_t) * (n + 1));
+  if (rc) {
+    cnt.release();
+    return rc;
+  }
+  scan_rows_kernel<<<1, 1024, 0, s>>>(counts, n, static_cast<int64_t*>(rp.ptr));
+  GMT_CUDA(cudaGetLastError());
+  ctx->launches += 2;
+  int64_t E = 0;
+  GMT_CUDA(cudaMemcpyAsync(&E, static_cast<int64_t*>(rp.ptr) + n, sizeof(E), cudaMemcpyDeviceToHost, s));
+  GMT_CUDA(cudaStreamSynchronize(s));
+  const size_t o_ptr = 0;
+  const size_t o_col = align16(sizeof(int64_t) * (n + 1));
+  const size_t o_cost = o_col + align16(sizeof(int32_t) * E);
+  const size_t o_tau = o_cost + align16(sizeof(double) * E);
+  const size_t total = o_tau + (with_tau ? align16(sizeof(double) * E) : 0);
+  rc = mem.reserve(total);
+  if (rc) {
+    cnt.release();
+    rp.release();
+    return rc;
+  }
+  char* b = static_cast<char*>(mem.ptr);
+  rows->ptr = reinterpret_cast<int64_t*>(b + o_ptr);
+  rows->col = reinterpret_cast<int32_t*>(b + o_col);
+  rows->cost = reinterpret_cast<double*>(b + o_cost);
+  rows->tau = with_tau ? reinterpret_cast<double*>(b + o_tau) : nullptr;
+  rows->edges = E;
+  GMT_CUDA(cudaMemcpyAsync(rows->ptr, rp.ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+  if (swap)
+    di_rows_kernel<true, true><<<blocks, 256, 0, s>>>(coords, n, P, radius, bound, nullptr, rows->ptr,
+                                                      rows->col, rows->cost, rows->tau);
+  else
+    di_rows_kernel<false, true><<<blocks, 256, 0, s>>>(coords, n, P, radius, bound, nullptr, rows->ptr,
+                                                       rows->col, rows->cost, rows->tau);
+  GMT_CUDA(cudaGetLastError());
+  ++ctx->launches;
+  GMT_CUDA(cudaStreamSynchronize(s));
+  cnt.release();
+  rp.release();
+  return GMT_OK;
+}
+
+}  // namespace
+
+DiParams to_di(const gmt_di_params* p) {
+  DiParams P;
+  P.vmax = p->vmax;
+  P.weight = p->weight;
+  P.segments = p->segments;
+  P.reserved = 0;
+  return P;
+}
+
+int validate_di(const gmt_di_params* p) {
+  if (!p) return set_error(GMT_E_INVALID_INPUT, "double-integrator parameters are null");
+  if (!(p->vmax > 0.0)) return set_error(GMT_E_INVALID_INPUT, "di.vmax must be positive");
+  if (!(p->weight > 0.0)) return set_error(GMT_E_INVALID_INPUT, "di.weight must be positive");
+  if (p->segments < 1 || p->segments > 64)
+    return set_error(GMT_E_INVALID_INPUT, "di.segments must be in [1, 64]");
+  return GMT_OK;
+}
+
+double di_prefilter_bound(const DiParams& P, double radius) {
+  // vmax r + r^2 / (2 sqrt(3 w)), widened by 1e-9 relative against rounding.
+  return (P.vmax * radius + radius * radius / (2.0 * std::sqrt(3.0 * P.weight))) * (1.0 + 1e-9) + 1e-12;
+}
+
+int build_di_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const DiParams& P, double radius,
+                       Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in) {
+  if (!(radius > 0.0)) return set_error(GMT_E_INVALID_INPUT, "connection radius must be positive");
+  if (n < 1) return set_error(GMT_E_INVALID_INPUT, "cannot build a graph over zero samples");
+  const double bound = di_prefilter_bound(P, radius);
+  int rc = rows_pass(ctx, false, d_coords, n, P, radius, bound, out_mem, out, true);
+  if (rc) return rc;
+  return rows_pass(ctx, true, d_coords, n, P, radius, bound, in_mem, in, true);
+}
+
+}  // namespace gmtb
+
+using namespace gmtb;
+
+extern "C" int gmt_di_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count,
+                            const gmt_di_params* params, double* cost_out, double* tau_out) {
+  int rc = validate_di(params);
+  if (rc) return rc;
+  if (count <= 0) return GMT_OK;
+  const DiParams P = to_di(params);
+  Arena buf;
+  const size_t xs = sizeof(double) * kDiDim * static_cast<size_t>(count);
+  rc = buf.reserve(2 * xs + 2 * sizeof(double) * count);
+  if (rc) return rc;
+  double* d0 = static_cast<double*>(buf.ptr);
+  double* d1 = d0 + kDiDim * count;
+  double* dc = d1 + kDiDim * count;
+  double* dt = dc + count;
+  cudaStream_t s = ctx->stream;
+  GMT_CUDA(cudaMemcpyAsync(d0, x0s, xs, cudaMemcpyHostToDevice, s));
+  GMT_CUDA(cudaMemcpyAsync(d1, x1s, xs, cudaMemcpyHostToDevice, s));
+  const int blocks = static_cast<int>(std::min<int64_t>((count + 255) / 256, 4096));
+  di_pairs_kernel<<<blocks, 256, 0, s>>>(d0, d1, count, P, dc, dt);
+  GMT_CUDA(cudaGetLastError());
+  ++ctx->launches;
+  GMT_CUDA(cudaMemcpyAsync(cost_out, dc, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+  GMT_CUDA(cudaMemcpyAsync(tau_out, dt, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+  GMT_CUDA(cudaStreamSynchronize(s));
+  buf.release();
+  return GMT_OK;
+}
+
+extern "C" int gmt_build_di_graph(gmt_ctx* ctx, const double* coords, int32_t n,
+                                  const gmt_di_params* params, double radius, int64_t* num_edges,
+                                  int64_t* out_ptr, int32_t* out_col, double* out_cost,
+                                  double* out_tau, int64_t* in_ptr, int32_t* in_col,
+                                  double* in_cost, int32_t* in_path, double* path_pts) {
+  int rc = validate_di(params);
+  if (rc) return rc;
+  if (n < 1) return set_error(GMT_E_INVALID_INPUT, "cannot build a graph over zero samples");
+  const DiParams P = to_di(params);
+  cudaStream_t s = ctx->stream;
+  Arena cbuf;
+  rc = cbuf.reserve(sizeof(double) * kDiDim * static_cast<size_t>(n));
+  if (rc) return rc;
+  GMT_CUDA(cudaMemcpyAsync(cbuf.ptr, coords, sizeof(double) * kDiDim * n, cudaMemcpyHostToDevice, s));
+  const double* dc = static_cast<const double*>(cbuf.ptr);
+  Arena om, im;
+  DiRows o, in;
+  rc = build_di_graph_dev(ctx, dc, n, P, radius, om, &o, im, &in);
+  if (rc) {
+    cbuf.release();
+    return rc;
+  }
+  *num_edges = o.edges;
+  if (out_ptr) {
+    auto get = [&](void* dst, const void* src, size_t bytes) -> int {
+      if (dst && bytes) GMT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+      return GMT_OK;
+    };
+    const size_t E = static_cast<size_t>(o.edges);
+    get(out_ptr, o.ptr, sizeof(int64_t) * (n + 1));
+    get(out_col, o.col, sizeof(int32_t) * E);
+    get(out_cost, o.cost, sizeof(double) * E);
+    get(out_tau, o.tau, sizeof(double) * E);
+    get(in_ptr, in.ptr, sizeof(int64_t) * (n + 1));
+    get(in_col, in.col, sizeof(int32_t) * E);
+    get(in_cost, in.cost, sizeof(double) * E);
+    Arena extra;
+    if (in_path || path_pts) {
+      const size_t pts_bytes = path_pts ? sizeof(double) * E * (P.segments + 1) * kDiDim : 0;
+      rc = extra.reserve(sizeof(int32_t) * E + pts_bytes + 16);
+      if (rc) return rc;
+      int32_t* ip = static_cast<int32_t*>(extra.ptr);
+      double* pp = reinterpret_cast<double*>(static_cast<char*>(extra.ptr) + align16(sizeof(int32_t) * E));
+      if (in_path) {
+        in_path_kernel<<<std::max(1, std::min((n + 255) / 256, 1024)), 256, 0, s>>>(in.ptr, in.col, o.ptr,
+                                                                               o.col, n, ip);
+        GMT_CUDA(cudaGetLastError());
+        ++ctx->launches;
+        get(in_path, ip, sizeof(int32_t) * E);
+      }
+      if (path_pts) {
+        di_paths_kernel<<<std::max(1, std::min(n, 4096)), 128, 0, s>>>(dc, o.ptr, o.col, o.tau, n, P, pp);
+        GMT_CUDA(cudaGetLastError());
+        ++ctx->launches;
+        get(path_pts, pp, pts_bytes);
+      }
+      GMT_CUDA(cudaStreamSynchronize(s));
+      extra.release();
+    }
+    GMT_CUDA(cudaStreamSynchronize(s));
+  }
+  om.release();
+  im.release();
+  cbuf.release();
+  return GMT_OK;
+}

@@ -45,6 +45,7 @@ struct gmt_instance {
   gmtb::Arena mem;       // samples, boxes, goal, graph rows, paths
   gmtb::Arena desc_mem;  // the device copy of `desc`
   gmtb::Arena aux;       // device-built instances: goal index list etc.
+  gmtb::Arena mem2;      // device-built directed graphs: the in-rows
   gmtb::DevInstance desc{};
   int32_t graph_n = 0;
   const int32_t* goal_idx_dev = nullptr;
@@ -52,6 +53,7 @@ struct gmt_instance {
     mem.release();
     desc_mem.release();
     aux.release();
+    mem2.release();
   }
 };
 

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "internal.cuh"
+#include "di.cuh"
 #include "offline.cuh"
 
 namespace gmtb {
@@ -618,8 +619,18 @@ extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instan
     samples.release();
     return rc;
   }
+  const bool di = p->steering == GMT_STEER_DOUBLE_INTEGRATOR;
+  if (p->steering != GMT_STEER_EUCLIDEAN && !di) {
+    samples.release();
+    return set_error(GMT_E_INVALID_INPUT, "unsupported steering model");
+  }
   double radius = p->radius_override;
   if (!(radius > 0.0)) {
+    if (di) {  // the Theorem 1 radius assumes straight-line costs
+      samples.release();
+      return set_error(GMT_E_INVALID_INPUT,
+                       "the double integrator needs radius_override (a cost threshold)");
+    }
     rc = gmt_connection_radius(d, p->n, p->eta, 1.0 /* free_measure_upper_bound, space.cpp:101-104 */,
                                &radius);
     if (rc) {
@@ -627,13 +638,29 @@ extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instan
       return rc;
     }
   }
-  Arena g;
+  Arena g, g2;
   int64_t E = 0, *rp = nullptr;
   int32_t* col = nullptr;
   double* cost = nullptr;
-  rc = build_graph_dev(ctx, S.coords, S.n, d, radius, g, &E, &rp, &col, &cost);
+  DiRows dout, din;
+  if (di) {
+    if (d != kDiDim) {
+      samples.release();
+      return set_error(GMT_E_INVALID_INPUT, "the double integrator needs dimension 6");
+    }
+    rc = validate_di(&p->di);
+    if (rc == GMT_OK) rc = build_di_graph_dev(ctx, S.coords, S.n, to_di(&p->di), radius, g, &dout, g2, &din);
+    E = dout.edges;
+    rp = dout.ptr;
+    col = dout.col;
+    cost = dout.cost;
+  } else {
+    rc = build_graph_dev(ctx, S.coords, S.n, d, radius, g, &E, &rp, &col, &cost);
+  }
   if (rc) {
     samples.release();
+    g.release();
+    g2.release();
     return rc;
   }
   auto* inst = new gmt_instance;
@@ -683,13 +710,26 @@ extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instan
     D.in_ptr = rp;
     D.in_col = col;
     D.in_cost = cost;
+    if (di) {
+      D.directed = 1;
+      D.in_ptr = din.ptr;
+      D.in_col = din.col;
+      D.in_cost = din.cost;
+      D.in_tau = din.tau;
+      D.steering = GMT_STEER_DOUBLE_INTEGRATOR;
+      D.di_segments = p->di.segments;
+      D.di_vmax = p->di.vmax;
+      D.di_weight = p->di.weight;
+    }
     inst->goal_idx_dev = reinterpret_cast<const int32_t*>(b + o_gidx);
     inst->graph_n = n;
   }
   samples.release();
   if (rc == GMT_OK) {
-    inst->mem = g;  // the graph arena now belongs to the instance
+    inst->mem = g;  // the graph arenas now belong to the instance
     g.ptr = nullptr;
+    inst->mem2 = g2;
+    g2.ptr = nullptr;
     rc = push_desc(ctx, inst);
     if (rc == GMT_OK) {
       cudaError_t e = cudaStreamSynchronize(s);
@@ -698,6 +738,7 @@ extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instan
   }
   if (rc != GMT_OK) {
     g.release();
+    g2.release();
     delete inst;
     return rc;
   }

@@ -35,6 +35,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "di.cuh"
 #include "solve.cuh"
 
 namespace cg = cooperative_groups;
@@ -281,6 +282,31 @@ __device__ bool polyline_free_warp(const DevInstance& I, int d, const Boxes& bx,
   if (b - a == 1) return point_free_warp<D>(pts, d, bx, lane, seg);
   for (int64_t s = 0; s + 1 < b - a; ++s) {
     if (!segment_free_warp<D>(pts + s * d, pts + (s + 1) * d, d, bx, lane, seg)) return false;
+  }
+  return true;
+}
+
+// The same test for a double-integrator edge whose polyline is not stored:
+// lanes 0..5 and 16..21 evaluate the coordinates of waypoints s and s+1
+// (di_coord, the very function that materialises stored paths), then the
+// segment goes through segment_free_staged.
+template <int D>
+__device__ bool di_edge_free_warp(const DevInstance& I, const Boxes& bx, int from, int to,
+                                  double tau, int lane, double* seg) {
+  DiParams P;
+  P.vmax = I.di_vmax;
+  P.weight = I.di_weight;
+  P.segments = I.di_segments;
+  P.reserved = 0;
+  const double* x0 = I.coords + static_cast<int64_t>(from) * kDiDim;
+  const double* x1 = I.coords + static_cast<int64_t>(to) * kDiDim;
+  if (tau == 0.0) return point_free_warp<D>(x0, kDiDim, bx, lane, seg);
+  for (int s = 0; s < P.segments; ++s) {
+    __syncwarp();
+    if (lane < kDiDim) seg[lane] = di_coord(x0, x1, tau, s, lane, P);
+    if (lane >= 16 && lane < 16 + kDiDim) seg[lane] = di_coord(x0, x1, tau, s + 1, lane - 16, P);
+    __syncwarp();
+    if (!segment_free_staged<D>(kDiDim, bx, lane, seg)) return false;
   }
   return true;
 }
@@ -713,7 +739,9 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? GMT_BATCH_MIN_B
           ++my_checks;
           const int32_t pid = I.in_path ? __ldg(I.in_path + be) : -1;
           bool ok;
-          if (pid < 0) {  // straight edge: segment_free (planner.cpp:59)
+          if (I.in_tau) {  // double integrator: regenerated polyline (di.cuh)
+            ok = di_edge_free_warp<D>(I, bx, by, x, __ldg(I.in_tau + be), lane, seg);
+          } else if (pid < 0) {  // straight edge: segment_free (planner.cpp:59)
             if (lane < d) seg[lane] = __ldg(I.coords + static_cast<int64_t>(by) * d + lane);
             __syncwarp();
             ok = segment_free_staged<D>(d, bx, lane, seg);

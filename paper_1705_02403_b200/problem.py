@@ -70,7 +70,16 @@ class ProblemSpec:
     start_index: int = 1
     seed: int = 0
     notes: str = ""
+    steering: int = abi.STEER_EUCLIDEAN
+    di_vmax: float = 0.5
+    di_weight: float = 1.0
+    di_segments: int = 8
     _keep: list = field(default_factory=list, repr=False)
+
+    def di_params(self) -> abi.DiParams:
+        p = abi.DiParams()
+        p.vmax, p.weight, p.segments, p.reserved = self.di_vmax, self.di_weight, self.di_segments, 0
+        return p
 
     @property
     def num_boxes(self) -> int:
@@ -112,6 +121,9 @@ class ProblemSpec:
         p.eta = self.eta
         p.radius_override = self.radius_override if self.radius_override else 0.0
         p.sampling = self.source()
+        p.steering = self.steering
+        p.reserved = 0
+        p.di = self.di_params()
         return p
 
     def with_n(self, n: int) -> "ProblemSpec":
@@ -444,6 +456,39 @@ def random_problem_2d(rng: Pcg32, dim: int = 2, with_obstacles: bool = True, n_m
         spec.n = n_min + rng.next_u32() % (n_max - n_min + 1)
         return spec
     raise RuntimeError("random problem generation kept hitting infeasible draws")
+
+
+def di_forest(seed: int = 3, n: int = 4000, pillars: int = 60, radius: float = 1.6,
+              vmax: float = 0.5) -> ProblemSpec:
+    """C3 "6D double integrator in a 3D obstacle field":
+    the C2 forest's pillars extruded over the full normalised velocity range,
+    state [p, s] with v = vmax (2s - 1); start at rest in the low corner,
+    goal = a position box with speeds below vmax/2 on every axis; Halton
+    samples; the connection radius is a cost threshold (radius_override)."""
+    base = forest_3d(seed, n, pillars)
+    box_lo = np.concatenate([base.box_lo, np.zeros((base.num_boxes, 3))], axis=1)
+    box_hi = np.concatenate([base.box_hi, np.ones((base.num_boxes, 3))], axis=1)
+    spec = ProblemSpec(dim=6, box_lo=box_lo, box_hi=box_hi,
+                       goal_lo=np.array([0.90, 0.90, 0.35, 0.25, 0.25, 0.25]),
+                       goal_hi=np.array([0.98, 0.98, 0.65, 0.75, 0.75, 0.75]),
+                       init=np.array([0.03, 0.03, 0.5, 0.5, 0.5, 0.5]), n=n,
+                       radius_override=radius, steering=abi.STEER_DOUBLE_INTEGRATOR,
+                       di_vmax=vmax, notes=f"6D double integrator, forest Pcg32({seed}).")
+    return spec
+
+
+def random_di_query(master: int, q: int, n: int = 4000, pillars: int = 60,
+                    radius: float = 1.6) -> ProblemSpec:
+    """C5 batched 6D double-integrator query q: its own forest, start and
+    goal from Pcg32(mix64(master, q)) (random_forest_query extruded)."""
+    base = random_forest_query(master, q, n=n, pillars=pillars)
+    box_lo = np.concatenate([base.box_lo, np.zeros((base.num_boxes, 3))], axis=1)
+    box_hi = np.concatenate([base.box_hi, np.ones((base.num_boxes, 3))], axis=1)
+    return ProblemSpec(dim=6, box_lo=box_lo, box_hi=box_hi,
+                       goal_lo=np.concatenate([base.goal_lo, np.full(3, 0.25)]),
+                       goal_hi=np.concatenate([base.goal_hi, np.full(3, 0.75)]),
+                       init=np.concatenate([base.init, np.full(3, 0.5)]), n=n,
+                       radius_override=radius, steering=abi.STEER_DOUBLE_INTEGRATOR)
 
 
 def connection_radius_py(dim: int, n: int, eta: float = 0.0, mu: float = 1.0) -> float:
