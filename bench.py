@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--single-reps", type=int, default=101)
     ap.add_argument("--cpu-sample", type=int, default=64, help="queries in the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--di-queries", type=int, default=148,
+                    help="batched 6D double-integrator queries per GPU (0: skip the DI legs)")
     return ap.parse_args()
 
 
@@ -206,6 +208,7 @@ def run_b200(args):
     import torch
 
     from paper_1705_02403_b200 import abi, problem as P
+    from paper_1705_02403_b200.shard import weak_range
     from paper_1705_02403_b200 import native
     from paper_1705_02403_b200.native import (OPT_BATCH_CLUSTER, OPT_BATCH_THREADS, OPT_COUNTERS,
                                               Context, PackedBatch, plan_batch_host)
@@ -299,29 +302,63 @@ def run_b200(args):
         raise SystemExit(f"e2e results differ from device-resident results in {mism} queries")
 
     # ---- single-query latency (configs[1] canonical instance) -------------
-    c2 = ctx.build_instance(P.forest_3d(3, args.n))
-    single = {}
-    for cs in (8, 16):
-        ctx.set_option(OPT_BATCH_CLUSTER, cs)
-        ctx.set_option(OPT_BATCH_THREADS, 0)
-        b1 = ctx.batch([c2], 1.0)
-        ctx.set_option(OPT_BATCH_CLUSTER, 1)
-        for _ in range(5):
-            b1.launch()
-        ctx.synchronize()
-        times = []
-        with torch.cuda.stream(stream):
-            for _ in range(args.single_reps):
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
+    def single_p50(inst):
+        out = {}
+        for cs in (8, 16):
+            ctx.set_option(OPT_BATCH_CLUSTER, cs)
+            ctx.set_option(OPT_BATCH_THREADS, 0)
+            b1 = ctx.batch([inst], 1.0)
+            ctx.set_option(OPT_BATCH_CLUSTER, 0)
+            for _ in range(5):
                 b1.launch()
-                e1.record(stream)
-                e1.synchronize()
-                times.append(e0.elapsed_time(e1))
-        single[f"cluster{cs}"] = statistics.median(times)
-        b1.close()
+            ctx.synchronize()
+            times = []
+            with torch.cuda.stream(stream):
+                for _ in range(args.single_reps):
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    b1.launch()
+                    e1.record(stream)
+                    e1.synchronize()
+                    times.append(e0.elapsed_time(e1))
+            out[f"cluster{cs}"] = statistics.median(times)
+            b1.close()
+        return out
+
+    c2 = ctx.build_instance(P.forest_3d(3, args.n))
+    single = single_p50(c2)
     p50 = min(single.values())
+
+    # ---- configs[2] / configs[4]: the 6D double integrator -----------------
+    di = None
+    if args.di_queries > 0:
+        t0 = time.perf_counter()
+        c3 = ctx.build_instance(P.di_forest(3, args.n))
+        ctx.synchronize()
+        build_ms = (time.perf_counter() - t0) * 1e3
+        s3 = single_p50(c3)
+        di_insts = [ctx.build_instance(P.random_di_query(MASTER_SEED, q, n=args.n))
+                    for q in weak_range(args.di_queries, rank)]
+        bdi = ctx.batch(di_insts, 1.0)
+        for _ in range(args.warmup):
+            bdi.launch()
+        barrier_sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(5):
+                bdi.launch()
+            e1.record(stream)
+        barrier_sync()
+        di_ms = max_over_ranks(e0.elapsed_time(e1) / 5)
+        di = {"workload": "di6d_forest_n4000 (configs[2]) / batched random DI queries (configs[4])",
+              "radius": c3.radius, "mean_out_degree": c3.num_edges / c3.n,
+              "device_build_ms": build_ms, "p50_ms_single_solve": min(s3.values()),
+              "single_solve_ms": s3, "batched_plans_per_s": world * len(di_insts) / (di_ms / 1e3),
+              "batched_queries_per_gpu": len(di_insts),
+              "solved": sum(1 for s in bdi.summaries() if s.status == abi.PLAN_SUCCESS)}
+        bdi.close()
 
     # ---- gather: one record per query to rank 0 (the only collective) -----
     from paper_1705_02403_b200.shard import gather_records, records
@@ -354,6 +391,7 @@ def run_b200(args):
                              (sum(i.num_edges for i in insts) * 12 / 1e9),
                        "solved": f"{int((recs[:, 0] == 0).sum())}/{len(recs)} success"},
             "p50_ms_single_solve": p50,
+            "double_integrator_6d": di,
             "single_solve_ms": single,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": pb.h2d_bytes,
                     "d2h_bytes_per_step": pb.d2h_bytes},

@@ -174,7 +174,7 @@ extern "C" int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value) {
       return GMT_OK;
     case GMT_OPT_THREADS:
     case GMT_OPT_BATCH_THREADS: {
-      const int cap = option == GMT_OPT_THREADS ? 512 : 256;
+      const int cap = 512;  // <= 256: narrow CTA shape, above: wide (solve.cu)
       if (value != 0 && (value < 32 || value > cap || value % 32 != 0))
         return set_error(GMT_E_INVALID_INPUT, "threads must be 0 or a multiple of 32 up to " +
                                                   std::to_string(cap));
@@ -185,8 +185,8 @@ extern "C" int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value) {
       ctx->counting = value ? 1 : 0;
       return GMT_OK;
     case GMT_OPT_BATCH_CLUSTER:
-      if (value != 1 && value != 2 && value != 4 && value != 8 && value != 16)
-        return set_error(GMT_E_INVALID_INPUT, "batch cluster size must be 1, 2, 4, 8 or 16");
+      if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8 && value != 16)
+        return set_error(GMT_E_INVALID_INPUT, "batch cluster size must be 0 (auto), 1, 2, 4, 8 or 16");
       ctx->batch_cluster = static_cast<int>(value);
       return GMT_OK;
     default:
@@ -562,7 +562,6 @@ int plan_on(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, double l
   job.radius = radius;
   const int cluster = ctx->cluster ? ctx->cluster : 8;
   int threads = ctx->threads ? ctx->threads : 512;
-  if (cluster == 1 && threads > 256) threads = 256;  // batched-shape kernel bound
   GMT_TRY(launch_jobs(ctx, {job}, cluster, threads, smem, obs, D.dim));
   return download_result(ctx, res[0], D.n, out);
 }
@@ -642,7 +641,16 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
   b->dim = insts[0]->desc.dim;
   for (int q = 1; q < count; ++q)
     if (insts[q]->desc.dim != b->dim) b->dim = 0;
-  int rc = plan_smem(ctx, max_n, max_d, max_nb, ctx->batch_cluster, &b->smem, &b->obs);
+  // Auto shape (batch cluster 0): double-integrator queries (eight polyline
+  // segments per lazy check) run on 2-CTA clusters of wide CTAs, the rest on
+  // single narrow CTAs -- the measured optimum (profiles/r01/sweep_*.txt).
+  b->cluster = ctx->batch_cluster;
+  if (b->cluster == 0) {
+    b->cluster = 1;
+    for (int q = 0; q < count; ++q)
+      if (insts[q]->desc.steering == GMT_STEER_DOUBLE_INTEGRATOR) b->cluster = 2;
+  }
+  int rc = plan_smem(ctx, max_n, max_d, max_nb, b->cluster, &b->smem, &b->obs);
   if (rc == GMT_OK)
     rc = carve_results(b->res, count, b->node_off.data(), true, true, b->results, &b->scalars,
                        ctx->counting ? ctx->counters : nullptr);
@@ -660,7 +668,6 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
     j.lambda = lambda;
     j.radius = insts[q]->desc.radius;
   }
-  b->cluster = ctx->batch_cluster;
   b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
   rc = b->jobs_mem.reserve(sizeof(SolveJob) * count);
   if (rc == GMT_OK) {
@@ -735,7 +742,8 @@ extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double
   }
   size_t smem;
   int obs;
-  GMT_TRY(plan_smem(ctx, max_n, d, max_nb, ctx->batch_cluster, &smem, &obs));
+  const int cluster = ctx->batch_cluster ? ctx->batch_cluster : 1;
+  GMT_TRY(plan_smem(ctx, max_n, d, max_nb, cluster, &smem, &obs));
 
   // Inputs: one H2D copy per array.
   Carver c;
@@ -809,7 +817,7 @@ extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double
   GMT_TRY(ctx->pinned.reserve(sizeof(DevInstance) * count));
   std::memcpy(ctx->pinned.ptr, descs.data(), sizeof(DevInstance) * count);
   GMT_TRY(put(o_desc, ctx->pinned.ptr, sizeof(DevInstance) * count));
-  GMT_TRY(launch_jobs(ctx, jobs, ctx->batch_cluster, ctx->batch_threads ? ctx->batch_threads : 256,
+  GMT_TRY(launch_jobs(ctx, jobs, cluster, ctx->batch_threads ? ctx->batch_threads : (cluster > 1 ? 512 : 256),
                       smem, obs, d));
 
   // Outputs.

@@ -66,7 +66,7 @@ struct gmt_ctx {
   int cluster = 0;        // single-query cluster size (0 = auto)
   int threads = 0;        // single-query CTA threads (0 = auto)
   int batch_threads = 0;  // batched CTA threads (0 = auto)
-  int batch_cluster = 1;  // batched cluster size
+  int batch_cluster = 0;  // batched cluster size (0 = auto by steering model)
   int counting = 0;       // GMT_OPT_COUNTERS
   int64_t* counters = nullptr;  // device [3]
   gmtb::Arena res;        // single-query / host-batch results

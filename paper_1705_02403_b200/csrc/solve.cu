@@ -353,16 +353,17 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 
 }  // namespace
 
-// Batched solves (CS == 1) want several small CTAs per SM; single-query
-// clusters want one wide CTA per SM.
-template <int CS, int D>
+// Two CTA shapes: WIDE = 512 threads with up to 128 registers (clusters,
+// and single-CTA queries that want the registers), narrow = 256 threads,
+// 64 registers, four CTAs per SM.
 #ifndef GMT_BATCH_MIN_BLOCKS
 #define GMT_BATCH_MIN_BLOCKS 4
 #endif
-__global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? GMT_BATCH_MIN_BLOCKS : 1)
+template <int CS, int D, bool WIDE>
+__global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLOCKS)
     gmt_solve_kernel(const SolveJob* __restrict__ jobs, int obs_in_smem) {
-  constexpr bool kParentSmem = CS > 1;  // batched solves keep parents in HBM
-  constexpr int kMaxWarps = CS == 1 ? 8 : 16;
+  constexpr bool kParentSmem = CS > 1;  // single-CTA solves keep parents in HBM
+  constexpr int kMaxWarps = WIDE ? 16 : 8;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ double seg_s[kMaxWarps * 32];
@@ -867,10 +868,10 @@ __global__ void __launch_bounds__(CS == 1 ? 256 : 512, CS == 1 ? GMT_BATCH_MIN_B
   }
 }
 
-template <int CS, int D>
+template <int CS, int D, bool WIDE>
 static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_t smem,
                              int obs_in_smem, cudaStream_t stream) {
-  auto kern = gmt_solve_kernel<CS, D>;
+  auto kern = gmt_solve_kernel<CS, D, WIDE>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;
@@ -895,25 +896,27 @@ static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_
   return cudaLaunchKernelEx(&cfg, kern, jobs, obs_in_smem);
 }
 
-template <int CS>
+template <int CS, bool WIDE>
 static cudaError_t launch_dim(const SolveJob* jobs, int count, int threads, size_t smem,
                               int obs_in_smem, int dim, cudaStream_t stream) {
   switch (dim) {
-    case 2: return launch_cs<CS, 2>(jobs, count, threads, smem, obs_in_smem, stream);
-    case 3: return launch_cs<CS, 3>(jobs, count, threads, smem, obs_in_smem, stream);
-    case 6: return launch_cs<CS, 6>(jobs, count, threads, smem, obs_in_smem, stream);
-    default: return launch_cs<CS, 0>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 2: return launch_cs<CS, 2, WIDE>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 3: return launch_cs<CS, 3, WIDE>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 6: return launch_cs<CS, 6, WIDE>(jobs, count, threads, smem, obs_in_smem, stream);
+    default: return launch_cs<CS, 0, WIDE>(jobs, count, threads, smem, obs_in_smem, stream);
   }
 }
 
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
                          int obs_in_smem, int dim, cudaStream_t stream) {
   switch (cluster) {
-    case 1: return launch_dim<1>(jobs, count, threads, smem, obs_in_smem, dim, stream);
-    case 2: return launch_dim<2>(jobs, count, threads, smem, obs_in_smem, dim, stream);
-    case 4: return launch_dim<4>(jobs, count, threads, smem, obs_in_smem, dim, stream);
-    case 8: return launch_dim<8>(jobs, count, threads, smem, obs_in_smem, dim, stream);
-    case 16: return launch_dim<16>(jobs, count, threads, smem, obs_in_smem, dim, stream);
+    case 1:
+      return threads > 256 ? launch_dim<1, true>(jobs, count, threads, smem, obs_in_smem, dim, stream)
+                           : launch_dim<1, false>(jobs, count, threads, smem, obs_in_smem, dim, stream);
+    case 2: return launch_dim<2, true>(jobs, count, threads, smem, obs_in_smem, dim, stream);
+    case 4: return launch_dim<4, true>(jobs, count, threads, smem, obs_in_smem, dim, stream);
+    case 8: return launch_dim<8, true>(jobs, count, threads, smem, obs_in_smem, dim, stream);
+    case 16: return launch_dim<16, true>(jobs, count, threads, smem, obs_in_smem, dim, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -13,7 +13,8 @@ from paper_1705_02403_b200.native import (Context, OPT_BATCH_CLUSTER,  # noqa: E
 ctx = Context(0)
 stream = torch.cuda.ExternalStream(ctx.stream)
 qmax = int(sys.argv[1]) if len(sys.argv) > 1 else 512
-insts = [ctx.build_instance(P.random_forest_query(20171005, q, n=4000)) for q in range(qmax)]
+mk = P.random_di_query if os.environ.get("DI") else P.random_forest_query
+insts = [ctx.build_instance(mk(20171005, q, n=4000)) for q in range(qmax)]
 
 
 def timeit(b, reps=10):
@@ -29,10 +30,10 @@ def timeit(b, reps=10):
     return e0.elapsed_time(e1) / reps
 
 
-for cs, thr in ((1, 256), (1, 128), (2, 256), (4, 256)):
+for cs, thr in ((1, 256), (1, 512), (1, 384), (2, 512), (2, 256)):
     ctx.set_option(OPT_BATCH_CLUSTER, cs)
-    ctx.set_option(OPT_BATCH_THREADS, thr if cs == 1 else 0)
-    for q in (1, 8, 64, 148, 296, 444, 512):
+    ctx.set_option(OPT_BATCH_THREADS, thr)
+    for q in (1, 148, 296, 512):
         if q > qmax:
             continue
         try:
