@@ -188,6 +188,10 @@ typedef struct gmt_batch gmt_batch;
 /* ---- context ---------------------------------------------------------- */
 const char* gmt_last_error(void);
 int gmt_abi_version(void);
+/* sizeof of the ABI structs, in the order gmt_scene, gmt_sample_source,
+ * gmt_graph_view, gmt_plan_out, gmt_plan_summary, gmt_problem,
+ * gmt_di_params, gmt_batch_host (bindings check their layouts with it).   */
+int gmt_struct_sizes(int64_t* out, int32_t count);
 int gmt_ctx_create(int device, gmt_ctx** out);
 void gmt_ctx_destroy(gmt_ctx* ctx);
 void* gmt_ctx_stream(gmt_ctx* ctx); /* cudaStream_t every kernel of ctx runs on */

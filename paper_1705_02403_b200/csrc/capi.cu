@@ -105,6 +105,15 @@ static T* at(void* base, size_t off) {
 extern "C" const char* gmt_last_error(void) { return g_last_error.c_str(); }
 extern "C" int gmt_abi_version(void) { return GMT_B200_ABI_VERSION; }
 
+extern "C" int gmt_struct_sizes(int64_t* out, int32_t count) {
+  const int64_t sizes[] = {sizeof(gmt_scene),        sizeof(gmt_sample_source), sizeof(gmt_graph_view),
+                           sizeof(gmt_plan_out),     sizeof(gmt_plan_summary),  sizeof(gmt_problem),
+                           sizeof(gmt_di_params),    sizeof(gmt_batch_host)};
+  const int32_t n = static_cast<int32_t>(sizeof(sizes) / sizeof(sizes[0]));
+  for (int32_t i = 0; i < count && i < n; ++i) out[i] = sizes[i];
+  return n;
+}
+
 extern "C" int gmt_ctx_create(int device, gmt_ctx** out) {
   *out = nullptr;
   int count = 0;

@@ -29,6 +29,7 @@ _vp = C.c_void_p
 SIGNATURES = [
     ("gmt_last_error", C.c_char_p, []),
     ("gmt_abi_version", C.c_int, []),
+    ("gmt_struct_sizes", C.c_int, [_i64p, C.c_int32]),
     ("gmt_ctx_create", C.c_int, [C.c_int, _P(_vp)]),
     ("gmt_ctx_destroy", None, [_vp]),
     ("gmt_ctx_stream", _vp, [_vp]),

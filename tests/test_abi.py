@@ -68,3 +68,45 @@ def test_missing_library_raises(monkeypatch, tmp_path):
     monkeypatch.setattr(native, "LIB_PATH", str(tmp_path / "nope.so"))
     with pytest.raises(ImportError):
         native.load()
+
+
+ABI_STRUCTS = ("Scene", "SampleSource", "GraphView", "PlanOut", "PlanSummary", "Problem",
+               "DiParams", "BatchHost")
+
+
+def _sizes(fn):
+    out = (C.c_int64 * 16)()
+    n = fn(out, 16)
+    return list(out)[:n]
+
+
+def test_struct_layouts_match_bindings():
+    """ctypes mirrors of the ABI structs have the C sizes (product library
+    and the compiled-reference wrapper, which must be rebuilt when the header
+    changes)."""
+    from paper_1705_02403_b200 import abi
+    want = [C.sizeof(getattr(abi, s)) for s in ABI_STRUCTS]
+    assert _sizes(native.lib().gmt_struct_sizes) == want
+    import oracle
+    if oracle.ref_available():
+        f = oracle.ref().lib.ref_struct_sizes
+        f.restype, f.argtypes = C.c_int, [C.POINTER(C.c_int64), C.c_int32]
+        assert _sizes(f) == want
+
+
+def test_reference_batch_api():
+    """The bench's reference leg: build_instance for many queries and the
+    parallel plan loop agree with one-at-a-time planning."""
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("no compiled reference")
+    from paper_1705_02403_b200 import problem as P
+    R = oracle.ref()
+    specs = [P.random_forest_query(5, q, n=600) for q in range(5)]
+    insts = R.instance_build_many(specs, 3)
+    sums, sec = R.plan_many(insts, 1.0, 3)
+    assert sec > 0
+    for s, inst in zip(sums, insts):
+        r = inst.plan(1.0)
+        assert (s.status, s.cost, s.iterations, s.total_collision_checks) == (
+            r.status, r.cost, r.iterations, r.total_collision_checks)
