@@ -109,18 +109,6 @@ __device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
                : "memory");
 }
 
-// Row prefetch for a work list: lane j of the warp takes entry k0 + j*step
-// (the entries this warp will process) and prefetches its CSR row span.
-__device__ __forceinline__ void prefetch_rows(const uint16_t* list, int k0, int step, int count,
-                                              const int64_t* ptr, const int32_t* col,
-                                              const double* cost, int lane) {
-  for (int k = k0 + lane * step; k < count; k += 32 * step) {
-    const int v = list[k];
-    const int64_t e0 = __ldg(ptr + v), e1 = __ldg(ptr + v + 1);
-    prefetch_l2(col + e0, sizeof(int32_t) * static_cast<size_t>(e1 - e0));
-    if (cost) prefetch_l2(cost + e0, sizeof(double) * static_cast<size_t>(e1 - e0));
-  }
-}
 
 // Closed box b contains p (Aabb::contains, space.cpp:11-16).
 template <int D>
@@ -594,7 +582,6 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
     // (planner.cpp:159-166).
     {
       const int own = sh.own_count;
-      prefetch_rows(list, warp, nw, own, I.out_ptr, I.out_col, nullptr, lane);
       int k = warp;
       int64_t e0 = 0, e1 = 0;
       if (k < own) {
@@ -662,7 +649,6 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
     }
     __syncthreads();
     const int ccount = sh.cand_count;
-    prefetch_rows(list, warp, nw, ccount, I.in_ptr, I.in_col, I.in_cost, lane);
 
     // P5 + P6: connect_candidate (planner.cpp:62-90) and commit (178-189).
     int my_checks = 0, my_added = 0;
