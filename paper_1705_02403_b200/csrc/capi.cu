@@ -142,6 +142,9 @@ extern "C" int gmt_ctx_create(int device, gmt_ctx** out) {
     return cuda_error(e, "counters");
   }
   e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+  for (int k = 0; k < kMaxCopyChunks && e == cudaSuccess; ++k)
+    e = cudaEventCreateWithFlags(&ctx->copy_done[k], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete ctx;
     return cuda_error(e, "cudaStreamCreate");
@@ -161,6 +164,9 @@ extern "C" void gmt_ctx_destroy(gmt_ctx* ctx) {
   ctx->pinned2.release();
   ctx->pinned_jobs.release();
   cudaFree(ctx->counters);
+  for (int k = 0; k < kMaxCopyChunks; ++k)
+    if (ctx->copy_done[k]) cudaEventDestroy(ctx->copy_done[k]);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -754,7 +760,8 @@ extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double
   const int cluster = ctx->batch_cluster ? ctx->batch_cluster : 1;
   GMT_TRY(plan_smem(ctx, max_n, d, max_nb, cluster, &smem, &obs));
 
-  // Inputs: one H2D copy per array.
+  // Device layout: every array of the batch back to back, one descriptor
+  // per query; the host side only computes offsets.
   Carver c;
   const size_t o_coords = c.take<double>(total_nodes * d);
   const size_t o_lo = c.take<double>(total_boxes * d);
@@ -767,20 +774,7 @@ extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double
   const size_t o_desc = c.take<DevInstance>(count);
   GMT_TRY(ctx->scratch.reserve(c.off));
   void* base = ctx->scratch.ptr;
-  cudaStream_t s = ctx->stream;
-  auto put = [&](size_t off, const void* src, size_t bytes) -> int {
-    if (bytes == 0) return GMT_OK;
-    GMT_CUDA(cudaMemcpyAsync(at<char>(base, off), src, bytes, cudaMemcpyHostToDevice, s));
-    return GMT_OK;
-  };
-  GMT_TRY(put(o_coords, B->coords, sizeof(double) * total_nodes * d));
-  GMT_TRY(put(o_lo, B->box_lo, sizeof(double) * total_boxes * d));
-  GMT_TRY(put(o_hi, B->box_hi, sizeof(double) * total_boxes * d));
-  GMT_TRY(put(o_glo, B->goal_lo, sizeof(double) * count * d));
-  GMT_TRY(put(o_ghi, B->goal_hi, sizeof(double) * count * d));
-  GMT_TRY(put(o_rp, B->row_ptr, sizeof(int64_t) * (total_nodes + count)));
-  GMT_TRY(put(o_col, B->col, sizeof(int32_t) * total_edges));
-  GMT_TRY(put(o_cost, B->cost, sizeof(double) * total_edges));
+  cudaStream_t s = ctx->stream, cs = ctx->copy_stream;
 
   const bool tree = label || tree_cost || parent || iteration_added;
   std::vector<DevResult> res;
@@ -825,23 +819,61 @@ extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double
   }
   GMT_TRY(ctx->pinned.reserve(sizeof(DevInstance) * count));
   std::memcpy(ctx->pinned.ptr, descs.data(), sizeof(DevInstance) * count);
-  GMT_TRY(put(o_desc, ctx->pinned.ptr, sizeof(DevInstance) * count));
-  GMT_TRY(launch_jobs(ctx, jobs, cluster, ctx->batch_threads ? ctx->batch_threads : (cluster > 1 ? 512 : 256),
-                      smem, obs, d));
-
-  // Outputs.
+  GMT_CUDA(cudaMemcpyAsync(at<char>(base, o_desc), ctx->pinned.ptr, sizeof(DevInstance) * count,
+                           cudaMemcpyHostToDevice, s));
+  const size_t job_bytes = sizeof(SolveJob) * count;
+  GMT_TRY(ctx->jobs.reserve(job_bytes));
+  GMT_TRY(ctx->pinned_jobs.reserve(job_bytes));
+  std::memcpy(ctx->pinned_jobs.ptr, jobs.data(), job_bytes);
+  GMT_CUDA(cudaMemcpyAsync(ctx->jobs.ptr, ctx->pinned_jobs.ptr, job_bytes, cudaMemcpyHostToDevice, s));
   GMT_TRY(ctx->pinned2.reserve(sizeof(ResultScalars) * count));
   auto* sc_host = static_cast<ResultScalars*>(ctx->pinned2.ptr);
-  GMT_CUDA(cudaMemcpyAsync(sc_host, sc_dev, sizeof(ResultScalars) * count, cudaMemcpyDeviceToHost, s));
-  if (paths) GMT_CUDA(cudaMemcpyAsync(paths, res[0].path, sizeof(int32_t) * total_nodes, cudaMemcpyDeviceToHost, s));
-  if (label) GMT_CUDA(cudaMemcpyAsync(label, res[0].label, total_nodes, cudaMemcpyDeviceToHost, s));
-  if (tree_cost)
-    GMT_CUDA(cudaMemcpyAsync(tree_cost, res[0].tree_cost, sizeof(double) * total_nodes, cudaMemcpyDeviceToHost, s));
-  if (parent)
-    GMT_CUDA(cudaMemcpyAsync(parent, res[0].parent, sizeof(int32_t) * total_nodes, cudaMemcpyDeviceToHost, s));
-  if (iteration_added)
-    GMT_CUDA(cudaMemcpyAsync(iteration_added, res[0].iter_added, sizeof(int64_t) * total_nodes,
-                             cudaMemcpyDeviceToHost, s));
+  const int threads = ctx->batch_threads ? ctx->batch_threads : (cluster > 1 ? 512 : 256);
+
+  // Pipeline: the queries go in chunks; chunk k's host->device copies run
+  // on the copy stream while chunk k-1 solves on the compute stream, and
+  // each chunk's results come back right after its solve.
+  const int nchunks = std::max(1, std::min(kMaxCopyChunks, count / 64));
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int q0 = static_cast<int>(static_cast<int64_t>(count) * ch / nchunks);
+    const int q1 = static_cast<int>(static_cast<int64_t>(count) * (ch + 1) / nchunks);
+    const int64_t n0 = B->node_off[q0], n1 = B->node_off[q1];
+    const int64_t e0 = B->edge_off[q0], e1 = B->edge_off[q1];
+    const int64_t b0 = B->box_off[q0], b1 = B->box_off[q1];
+    auto put = [&](size_t off, size_t elem, int64_t first, int64_t last, const void* src) -> int {
+      if (last <= first) return GMT_OK;
+      GMT_CUDA(cudaMemcpyAsync(at<char>(base, off) + elem * first,
+                               static_cast<const char*>(src) + elem * first, elem * (last - first),
+                               cudaMemcpyHostToDevice, cs));
+      return GMT_OK;
+    };
+    GMT_TRY(put(o_coords, sizeof(double), n0 * d, n1 * d, B->coords));
+    GMT_TRY(put(o_lo, sizeof(double), b0 * d, b1 * d, B->box_lo));
+    GMT_TRY(put(o_hi, sizeof(double), b0 * d, b1 * d, B->box_hi));
+    GMT_TRY(put(o_glo, sizeof(double), static_cast<int64_t>(q0) * d, static_cast<int64_t>(q1) * d, B->goal_lo));
+    GMT_TRY(put(o_ghi, sizeof(double), static_cast<int64_t>(q0) * d, static_cast<int64_t>(q1) * d, B->goal_hi));
+    GMT_TRY(put(o_rp, sizeof(int64_t), n0 + q0, n1 + q1, B->row_ptr));
+    GMT_TRY(put(o_col, sizeof(int32_t), e0, e1, B->col));
+    GMT_TRY(put(o_cost, sizeof(double), e0, e1, B->cost));
+    GMT_CUDA(cudaEventRecord(ctx->copy_done[ch], cs));
+    GMT_CUDA(cudaStreamWaitEvent(s, ctx->copy_done[ch], 0));
+    GMT_CUDA(launch_solve(static_cast<const SolveJob*>(ctx->jobs.ptr) + q0, q1 - q0, cluster, threads,
+                          smem, obs, d, s));
+    ++ctx->launches;
+    auto get = [&](void* dst, const void* src, size_t elem, int64_t first, int64_t last) -> int {
+      if (!dst || last <= first) return GMT_OK;
+      GMT_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + elem * first,
+                               static_cast<const char*>(src) + elem * first, elem * (last - first),
+                               cudaMemcpyDeviceToHost, s));
+      return GMT_OK;
+    };
+    GMT_TRY(get(sc_host, sc_dev, sizeof(ResultScalars), q0, q1));
+    GMT_TRY(get(paths, res[0].path, sizeof(int32_t), n0, n1));
+    GMT_TRY(get(label, res[0].label, sizeof(uint8_t), n0, n1));
+    GMT_TRY(get(tree_cost, res[0].tree_cost, sizeof(double), n0, n1));
+    GMT_TRY(get(parent, res[0].parent, sizeof(int32_t), n0, n1));
+    GMT_TRY(get(iteration_added, res[0].iter_added, sizeof(int64_t), n0, n1));
+  }
   GMT_CUDA(cudaStreamSynchronize(s));
   for (int q = 0; q < count; ++q) to_summary(sc_host[q], &summaries[q]);
   return GMT_OK;

@@ -11,6 +11,8 @@
 
 namespace gmtb {
 
+constexpr int kMaxCopyChunks = 8;  // pipeline depth of gmt_plan_batch_host
+
 extern thread_local std::string g_last_error;
 int set_error(int code, const std::string& msg);
 int cuda_error(cudaError_t e, const char* what);
@@ -62,6 +64,8 @@ struct gmt_ctx {
   int sm_count = 0;
   size_t smem_optin = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;            // host->device copies of batches
+  cudaEvent_t copy_done[gmtb::kMaxCopyChunks] = {};
   int64_t launches = 0;
   int cluster = 0;        // single-query cluster size (0 = auto)
   int threads = 0;        // single-query CTA threads (0 = auto)

@@ -203,3 +203,24 @@ def test_batch_equals_single(ctx, port):
         got = b.result(q)
         _assert_parity(got, wants[q], f"batch q={q}")
         assert sums[q].status == wants[q].status and sums[q].iterations == wants[q].iterations
+
+
+def test_plan_batch_host_pipelined_matches_reference(ctx, port):
+    """The batched drop-in with host buffers (gmt_plan_batch_host): 130
+    queries go through the chunked copy/solve pipeline; every summary, path
+    and tree equals the oracle's plan of the same query."""
+    from paper_1705_02403_b200.native import PackedBatch, plan_batch_host
+    entries, wants = [], []
+    for q in range(130):
+        s = P.random_forest_query(77, q, n=300)
+        o = oracle_instance(port, s)
+        entries.append((s, o["coords"], len(o["goal_idx"]), o["graph"], o["init"]))
+        wants.append(port.gmt_plan(s, o["coords"], len(o["goal_idx"]), o["graph"], o["init"], 1.0,
+                                   o["radius"]))
+    pb = PackedBatch(entries, want_tree=True)
+    plan_batch_host(ctx, pb, 1.0)
+    for q, w in enumerate(wants):
+        got = pb.query_result(q)
+        assert abi.same_tree(got, w), q
+        assert got.iterations == w.iterations and got.total_collision_checks == w.total_collision_checks
+        assert np.array_equal(got.iteration_added, w.iteration_added)
