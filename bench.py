@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--di-queries", type=int, default=148,
                     help="batched 6D double-integrator queries per GPU (0: skip the DI legs)")
+    ap.add_argument("--no-quad", action="store_true", help="skip the 12D quadrotor leg (configs[3])")
     return ap.parse_args()
 
 
@@ -360,6 +361,23 @@ def run_b200(args):
               "solved": sum(1 for s in bdi.summaries() if s.status == abi.PLAN_SUCCESS)}
         bdi.close()
 
+    # ---- configs[3]: the 12D linearised quadrotor, n = 8000 ---------------
+    quad = None
+    if not args.no_quad:
+        spec4 = P.quad_scene()
+        t0 = time.perf_counter()
+        c4 = ctx.build_instance(spec4)
+        ctx.synchronize()
+        build_ms = (time.perf_counter() - t0) * 1e3
+        s4 = single_p50(c4)
+        r4 = ctx.plan(c4)
+        quad = {"workload": "quad12d_scene_n8000 (configs[3]): 90 pillars + 40 beams",
+                "radius": c4.radius, "weight": spec4.quad_weight, "n": c4.n,
+                "mean_out_degree": c4.num_edges / c4.n, "goal_samples": c4.goal_count,
+                "device_build_ms": build_ms, "p50_ms_single_solve": min(s4.values()),
+                "single_solve_ms": s4, "status": r4.status, "cost": r4.cost,
+                "iterations": r4.iterations, "collision_checks": r4.total_collision_checks}
+
     # ---- gather: one record per query to rank 0 (the only collective) -----
     from paper_1705_02403_b200.shard import gather_records, records
     recs = gather_records(records(dev0), device=f"cuda:{local}")
@@ -392,6 +410,7 @@ def run_b200(args):
                        "solved": f"{int((recs[:, 0] == 0).sum())}/{len(recs)} success"},
             "p50_ms_single_solve": p50,
             "double_integrator_6d": di,
+            "quadrotor_12d": quad,
             "single_solve_ms": single,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": pb.h2d_bytes,
                     "d2h_bytes_per_step": pb.d2h_bytes},

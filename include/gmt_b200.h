@@ -155,7 +155,11 @@ typedef struct gmt_plan_summary {
  * state [p(3), s(3)] in [0,1]^6 with velocity v = vmax (2s - 1), cost
  * tau + weight * integral |u|^2, directed edges, `segments`-segment
  * trajectory polylines for the lazy check.                                 */
-typedef enum gmt_steering { GMT_STEER_EUCLIDEAN = 0, GMT_STEER_DOUBLE_INTEGRATOR = 2 } gmt_steering;
+typedef enum gmt_steering {
+  GMT_STEER_EUCLIDEAN = 0,
+  GMT_STEER_DOUBLE_INTEGRATOR = 2,
+  GMT_STEER_QUADROTOR = 3
+} gmt_steering;
 
 typedef struct gmt_di_params {
   double vmax;
@@ -163,6 +167,23 @@ typedef struct gmt_di_params {
   int32_t segments;
   int32_t reserved;
 } gmt_di_params;
+
+/* GMT_STEER_QUADROTOR: the NEW 12D linearised quadrotor of SURVEY.md §8 row
+ * a22.  State [p(3), v(3), roll/pitch/yaw(3), rates(3)] in
+ * [0,1]^12: v = vmax (2s - 1), roll/pitch = amax (2s - 1), yaw = ymax (2s - 1),
+ * rates = wmax (2s - 1); hover linearisation with gravity g (workspace
+ * units / s^2); cost tau + weight * integral of the squared torques and
+ * thrust.                                                                  */
+typedef struct gmt_quad_params {
+  double g;
+  double vmax;
+  double amax;
+  double ymax;
+  double wmax;
+  double weight;
+  int32_t segments;
+  int32_t reserved;
+} gmt_quad_params;
 
 /* ProblemFile (problem.hpp:17-29) minus the Dubins steering fields, plus the
  * double-integrator model (radius_override is required for it).          */
@@ -179,6 +200,7 @@ typedef struct gmt_problem {
   int32_t steering;       /* gmt_steering */
   int32_t reserved;
   gmt_di_params di;
+  gmt_quad_params quad;
 } gmt_problem;
 
 typedef struct gmt_ctx gmt_ctx;
@@ -190,7 +212,8 @@ const char* gmt_last_error(void);
 int gmt_abi_version(void);
 /* sizeof of the ABI structs, in the order gmt_scene, gmt_sample_source,
  * gmt_graph_view, gmt_plan_out, gmt_plan_summary, gmt_problem,
- * gmt_di_params, gmt_batch_host (bindings check their layouts with it).   */
+ * gmt_di_params, gmt_batch_host, gmt_quad_params (bindings check their
+ * layouts with it).                                                        */
 int gmt_struct_sizes(int64_t* out, int32_t count);
 int gmt_ctx_create(int device, gmt_ctx** out);
 void gmt_ctx_destroy(gmt_ctx* ctx);
@@ -259,6 +282,16 @@ int gmt_build_di_graph(gmt_ctx* ctx, const double* coords, int32_t n, const gmt_
                        double radius, int64_t* num_edges, int64_t* out_ptr, int32_t* out_col,
                        double* out_cost, double* out_tau, int64_t* in_ptr, int32_t* in_col,
                        double* in_cost, int32_t* in_path, double* path_pts);
+
+/* 12D quadrotor steering (NEW, row a22): the same pair of entry points for
+ * the quadrotor model (states of 12 coordinates; path_pts E*(segments+1)*12). */
+int gmt_quad_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count,
+                   const gmt_quad_params* params, double* cost_out, double* tau_out);
+int gmt_build_quad_graph(gmt_ctx* ctx, const double* coords, int32_t n,
+                         const gmt_quad_params* params, double radius, int64_t* num_edges,
+                         int64_t* out_ptr, int32_t* out_col, double* out_cost, double* out_tau,
+                         int64_t* in_ptr, int32_t* in_col, double* in_cost, int32_t* in_path,
+                         double* path_pts);
 
 /* ---- device-resident instances (ProblemInstance, problem.hpp:52-57) --- */
 /* Upload host samples + graph + scene.  goal_count is samples.goal_indices

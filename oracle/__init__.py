@@ -185,8 +185,8 @@ class _Lib:
 
 
 class PortLib(_Lib):
-    """The C restatement, plus its statement of the NEW double-integrator
-    model (no reference exists for it)."""
+    """The C restatement, plus its statements of the NEW double-integrator
+    and quadrotor models (no reference exists for them)."""
 
     def __init__(self):
         super().__init__(PORT_SO, "oracle_")
@@ -200,6 +200,16 @@ class PortLib(_Lib):
         L.oracle_build_di_graph.restype = C.c_int
         L.oracle_build_di_graph.argtypes = [_dp, C.c_int32, C.c_double, C.c_double, C.c_double,
                                             _i64p, _i64p, _i32p, _dp, _dp]
+        _qp = C.POINTER(abi.QuadParams)
+        L.oracle_quad_cost.restype = C.c_double
+        L.oracle_quad_cost.argtypes = [_dp, _dp, _qp, _dp]
+        L.oracle_quad_coord.restype = C.c_double
+        L.oracle_quad_coord.argtypes = [_dp, _dp, C.c_double, C.c_int, C.c_int, _qp]
+        L.oracle_quad_paths.restype = None
+        L.oracle_quad_paths.argtypes = [_dp, C.c_int32, _i64p, _i32p, _dp, _qp, _dp]
+        L.oracle_build_quad_graph.restype = C.c_int
+        L.oracle_build_quad_graph.argtypes = [_dp, C.c_int32, _qp, C.c_double, _i64p, _i64p, _i32p,
+                                              _dp, _dp]
 
     def di_cost(self, x0, x1, vmax=0.5, weight=1.0):
         x0, x1 = abi.f64(x0), abi.f64(x1)
@@ -247,6 +257,62 @@ class PortLib(_Lib):
                                  abi.ptr(abi.i32(col), C.c_int32), abi.ptr(abi.f64(tau), C.c_double),
                                  segments, vmax, abi.ptr(pts, C.c_double))
         g = Graph(n, radius, ptr, col, cost, dim=6, directed=True,
+                  out_path=np.arange(E, dtype=np.int32),
+                  path_ptr=np.arange(E + 1, dtype=np.int64) * M1,
+                  path_pts=pts[:E].reshape(-1))
+        in_ptr, in_col, in_cost, in_path = g.transpose()
+        g.in_ptr, g.in_col, g.in_cost, g.in_path = (abi.i64(in_ptr), abi.i32(in_col),
+                                                     abi.f64(in_cost), abi.i32(in_path))
+        g.out_tau = tau
+        return g
+
+    # ---- 12D quadrotor (NEW model) ----
+    def quad_cost(self, x0, x1, params):
+        x0, x1 = abi.f64(x0), abi.f64(x1)
+        t = C.c_double()
+        c = self.lib.oracle_quad_cost(abi.ptr(x0, C.c_double), abi.ptr(x1, C.c_double),
+                                      C.byref(params), C.byref(t))
+        return c, t.value
+
+    def quad_waypoints(self, x0, x1, tau, params):
+        x0, x1 = abi.f64(x0), abi.f64(x1)
+        return np.array([[self.lib.oracle_quad_coord(abi.ptr(x0, C.c_double),
+                                                     abi.ptr(x1, C.c_double), tau, k, i,
+                                                     C.byref(params)) for i in range(12)]
+                         for k in range(params.segments + 1)])
+
+    def build_quad_graph(self, coords, radius, params):
+        """-> (out_ptr, out_col, out_cost, out_tau)"""
+        coords = abi.f64(coords)
+        n = coords.shape[0]
+        ne = C.c_int64()
+        self._check(self.lib.oracle_build_quad_graph(abi.ptr(coords, C.c_double), n, C.byref(params),
+                                                     radius, C.byref(ne), abi.ptr(None, C.c_int64),
+                                                     abi.ptr(None, C.c_int32),
+                                                     abi.ptr(None, C.c_double),
+                                                     abi.ptr(None, C.c_double)))
+        E = ne.value
+        ptr = np.zeros(n + 1, np.int64)
+        col = np.zeros(max(E, 1), np.int32)
+        cost, tau = np.zeros(max(E, 1)), np.zeros(max(E, 1))
+        self._check(self.lib.oracle_build_quad_graph(abi.ptr(coords, C.c_double), n, C.byref(params),
+                                                     radius, C.byref(ne), abi.ptr(ptr, C.c_int64),
+                                                     abi.ptr(col, C.c_int32),
+                                                     abi.ptr(cost, C.c_double),
+                                                     abi.ptr(tau, C.c_double)))
+        return ptr, col[:E], cost[:E], tau[:E]
+
+    def quad_graph(self, coords, radius, params):
+        """As di_graph, for the quadrotor."""
+        from paper_1705_02403_b200.graph import Graph
+        ptr, col, cost, tau = self.build_quad_graph(coords, radius, params)
+        n, E, M1 = coords.shape[0], len(col), params.segments + 1
+        pts = np.zeros((max(E, 1), M1, 12))
+        coords = abi.f64(coords)
+        self.lib.oracle_quad_paths(abi.ptr(coords, C.c_double), n, abi.ptr(ptr, C.c_int64),
+                                   abi.ptr(abi.i32(col), C.c_int32), abi.ptr(abi.f64(tau), C.c_double),
+                                   C.byref(params), abi.ptr(pts, C.c_double))
+        g = Graph(n, radius, ptr, col, cost, dim=12, directed=True,
                   out_path=np.arange(E, dtype=np.int32),
                   path_ptr=np.arange(E + 1, dtype=np.int64) * M1,
                   path_pts=pts[:E].reshape(-1))

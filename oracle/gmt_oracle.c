@@ -822,3 +822,207 @@ void oracle_di_paths(const double* coords, int32_t n, const int64_t* ptr, const 
           pts[(e * (M + 1) + k) * 6 + i] =
               oracle_di_coord(coords + (int64_t)u * 6, coords + (int64_t)col[e] * 6, tau[e], k, i, M, vmax);
 }
+
+/* ---- 12D linearised quadrotor (NEW model; no reference exists) -----------
+ * Independent C statement of paper_1705_02403_b200/csrc/quad.cuh (DESIGN.md
+ * §3.3), same operation order, -ffp-contract=off: parity against the
+ * reference is UNPINNED; pinned by properties in tests/test_quad.py
+ * (Gramian-form cost with numpy matrices, stationarity, duration scan,
+ * trajectory endpoints and dynamics). */
+static const double q_h2[2][2] = {{12.0, -6.0}, {-6.0, 4.0}};
+static const double q_h4[4][4] = {{100800.0, -50400.0, 10080.0, -840.0},
+                                  {-50400.0, 25920.0, -5400.0, 480.0},
+                                  {10080.0, -5400.0, 1200.0, -120.0},
+                                  {-840.0, 480.0, -120.0, 16.0}};
+static const int q_map[4][4] = {{0, 3, 7, 10}, {1, 4, 6, 9}, {2, 5, -1, -1}, {8, 11, -1, -1}};
+
+static double q_hinv(int m, int i, int j) { return m == 2 ? q_h2[i][j] : q_h4[i][j]; }
+static double q_fact(int k) {
+  double f = 1.0;
+  for (int i = 2; i <= k; ++i) f = f * (double)i;
+  return f;
+}
+static double q_pow(double t, int e) {
+  double r = 1.0;
+  for (int i = 0; i < e; ++i) r = r * t;
+  return r;
+}
+static int q_order(int c) { return c < 2 ? 4 : 2; }
+static double q_range(int idx, const gmt_quad_params* P) {
+  if (idx == 6 || idx == 7) return P->amax;
+  if (idx == 8) return P->ymax;
+  if (idx >= 9) return P->wmax;
+  return P->vmax;
+}
+static void q_chain(const double* x, int c, const gmt_quad_params* P, double* z) {
+  for (int i = 0; i < q_order(c); ++i) {
+    int idx = q_map[c][i];
+    double v = idx < 3 ? x[idx] : q_range(idx, P) * (2.0 * x[idx] - 1.0);
+    if (c == 0 && i >= 2) v = P->g * v;
+    if (c == 1 && i >= 2) v = -(P->g * v);
+    z[i] = v;
+  }
+}
+static void q_delta(const double* z0, const double* z1, int m, double delta[4][4]) {
+  for (int i = 0; i < m; ++i) {
+    delta[i][0] = z1[i] - z0[i];
+    for (int p = 1; p < m - i; ++p) delta[i][p] = -(z0[i + p] / q_fact(p));
+  }
+}
+static void q_coef(const double* x0, const double* x1, const gmt_quad_params* P, double* C) {
+  for (int k = 0; k <= 7; ++k) C[k] = 0.0;
+  for (int c = 0; c < 4; ++c) {
+    int m = q_order(c);
+    double wc = c < 2 ? P->weight / (P->g * P->g) : P->weight;
+    double z0[4], z1[4], delta[4][4];
+    q_chain(x0, c, P, z0);
+    q_chain(x1, c, P, z1);
+    q_delta(z0, z1, m, delta);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) {
+        double h = wc * q_hinv(m, i, j);
+        for (int p = 0; p < m - i; ++p)
+          for (int q = 0; q < m - j; ++q) {
+            int k = 2 * m - i - j - 1 - p - q;
+            C[k] = C[k] + (h * delta[i][p]) * delta[j][q];
+          }
+      }
+  }
+}
+static double q_g(const double* C, double t) {
+  double r = 1.0 * t;
+  for (int k = 1; k <= 7; ++k) r = r * t - (double)k * C[k];
+  return r;
+}
+static double q_c(const double* C, double t) {
+  double r = C[7] / t;
+  for (int k = 6; k >= 1; --k) r = (r + C[k]) / t;
+  return t + r;
+}
+
+double oracle_quad_cost(const double* x0, const double* x1, const gmt_quad_params* P, double* tau) {
+  double C[8];
+  q_coef(x0, x1, P, C);
+  int zero = 1;
+  for (int k = 1; k <= 7; ++k) zero = zero && C[k] == 0.0;
+  if (zero) {
+    *tau = 0.0;
+    return 0.0;
+  }
+  double T = 0.0;
+  for (int k = 1; k <= 7; ++k) {
+    double a = (double)k * C[k];
+    a = a < 0.0 ? -a : a;
+    if (a > T) T = a;
+  }
+  T = 1.0 + T;
+  double best_c = 0.0, best_t = 0.0;
+  int have = 0;
+  double t_hi = T, g_hi = q_g(C, t_hi);
+  for (int j = 1; j <= 96; ++j) {
+    double t_lo = t_hi * 0.75, g_lo = q_g(C, t_lo);
+    if (g_lo <= 0.0 && g_hi > 0.0) {
+      double lo = t_lo, hi = t_hi;
+      for (int it = 0; it < 64; ++it) {
+        double mid = 0.5 * (lo + hi);
+        if (q_g(C, mid) > 0.0) hi = mid; else lo = mid;
+      }
+      double ct = q_c(C, hi);
+      if (!have || ct <= best_c) {
+        best_c = ct;
+        best_t = hi;
+        have = 1;
+      }
+    }
+    t_hi = t_lo;
+    g_hi = g_lo;
+  }
+  if (!have) {
+    best_t = t_hi;
+    best_c = q_c(C, best_t);
+  }
+  *tau = best_t;
+  return best_c;
+}
+
+double oracle_quad_coord(const double* x0, const double* x1, double tau, int k, int idx,
+                         const gmt_quad_params* P) {
+  int M = P->segments;
+  if (k <= 0 || tau == 0.0) return x0[idx];
+  if (k >= M) return x1[idx];
+  int c = 0, i = 0;
+  for (int cc = 0; cc < 4; ++cc)
+    for (int ii = 0; ii < q_order(cc); ++ii)
+      if (q_map[cc][ii] == idx) c = cc, i = ii;
+  int m = q_order(c);
+  double t = (tau * (double)k) / (double)M;
+  double z0[4], z1[4], delta[4][4], d[4], lam[4];
+  q_chain(x0, c, P, z0);
+  q_chain(x1, c, P, z1);
+  q_delta(z0, z1, m, delta);
+  for (int j = 0; j < m; ++j) {
+    double v = 0.0;
+    for (int p = m - j - 1; p >= 0; --p) v = v * tau + delta[j][p];
+    d[j] = v;
+  }
+  for (int j = 0; j < m; ++j) {
+    double v = 0.0;
+    for (int l = 0; l < m; ++l) v = v + (q_hinv(m, j, l) * d[l]) / q_pow(tau, 2 * m - j - l - 1);
+    lam[j] = v;
+  }
+  double zi = 0.0;
+  for (int q = m - 1; q >= i; --q) zi = zi + (z0[q] * q_pow(t, q - i)) / q_fact(q - i);
+  int a = m - 1 - i;
+  double u = tau - t;
+  for (int j = 0; j < m; ++j) {
+    int b = m - 1 - j;
+    double I = 0.0;
+    for (int r = 0; r <= b; ++r) {
+      double num = (q_pow(u, b - r) / q_fact(b - r)) * q_pow(t, a + r + 1);
+      double den = ((double)(a + r + 1) * q_fact(a)) * q_fact(r);
+      I = I + num / den;
+    }
+    zi = zi + lam[j] * I;
+  }
+  double v = zi;
+  if (c == 0 && i >= 2) v = zi / P->g;
+  if (c == 1 && i >= 2) v = -(zi / P->g);
+  if (idx < 3) return v;
+  return 0.5 * (v / q_range(idx, P) + 1.0);
+}
+
+/* Brute-force directed r-disk graph of the quadrotor (as oracle_build_di_graph). */
+int oracle_build_quad_graph(const double* coords, int32_t n, const gmt_quad_params* P, double radius,
+                            int64_t* num_edges, int64_t* out_ptr, int32_t* out_col, double* out_cost,
+                            double* out_tau) {
+  int64_t e = 0;
+  for (int32_t u = 0; u < n; ++u) {
+    if (out_ptr) out_ptr[u] = e;
+    for (int32_t v = 0; v < n; ++v) {
+      if (v == u) continue;
+      double t;
+      double c = oracle_quad_cost(coords + (int64_t)u * 12, coords + (int64_t)v * 12, P, &t);
+      if (!(c <= radius)) continue;
+      if (out_col) {
+        out_col[e] = v;
+        out_cost[e] = c;
+        out_tau[e] = t;
+      }
+      ++e;
+    }
+  }
+  if (out_ptr) out_ptr[n] = e;
+  *num_edges = e;
+  return GMT_OK;
+}
+
+void oracle_quad_paths(const double* coords, int32_t n, const int64_t* ptr, const int32_t* col,
+                       const double* tau, const gmt_quad_params* P, double* pts) {
+  int M = P->segments;
+  for (int32_t u = 0; u < n; ++u)
+    for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e)
+      for (int k = 0; k <= M; ++k)
+        for (int i = 0; i < 12; ++i)
+          pts[(e * (M + 1) + k) * 12 + i] =
+              oracle_quad_coord(coords + (int64_t)u * 12, coords + (int64_t)col[e] * 12, tau[e], k, i, P);
+}

@@ -549,7 +549,7 @@ int ref_random_problem_get(void* h, double* box_lo, double* box_hi, double* goal
 extern "C" int ref_struct_sizes(int64_t* out, int32_t count) {
   const int64_t sizes[] = {sizeof(gmt_scene),     sizeof(gmt_sample_source), sizeof(gmt_graph_view),
                            sizeof(gmt_plan_out),  sizeof(gmt_plan_summary),  sizeof(gmt_problem),
-                           sizeof(gmt_di_params), sizeof(gmt_batch_host)};
+                           sizeof(gmt_di_params), sizeof(gmt_batch_host),    sizeof(gmt_quad_params)};
   const int32_t n = static_cast<int32_t>(sizeof(sizes) / sizeof(sizes[0]));
   for (int32_t i = 0; i < count && i < n; ++i) out[i] = sizes[i];
   return n;

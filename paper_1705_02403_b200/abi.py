@@ -113,12 +113,27 @@ class PlanSummary(C.Structure):
 
 STEER_EUCLIDEAN = 0
 STEER_DOUBLE_INTEGRATOR = 2
+STEER_QUADROTOR = 3
 
 
 class DiParams(C.Structure):
     """gmt_di_params: 6D double integrator (NEW model)."""
     _fields_ = [
         ("vmax", C.c_double),
+        ("weight", C.c_double),
+        ("segments", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+class QuadParams(C.Structure):
+    """gmt_quad_params: 12D linearised quadrotor (NEW model)."""
+    _fields_ = [
+        ("g", C.c_double),
+        ("vmax", C.c_double),
+        ("amax", C.c_double),
+        ("ymax", C.c_double),
+        ("wmax", C.c_double),
         ("weight", C.c_double),
         ("segments", C.c_int32),
         ("reserved", C.c_int32),
@@ -139,6 +154,7 @@ class Problem(C.Structure):
         ("steering", C.c_int32),
         ("reserved", C.c_int32),
         ("di", DiParams),
+        ("quad", QuadParams),
     ]
 
 

@@ -108,7 +108,7 @@ extern "C" int gmt_abi_version(void) { return GMT_B200_ABI_VERSION; }
 extern "C" int gmt_struct_sizes(int64_t* out, int32_t count) {
   const int64_t sizes[] = {sizeof(gmt_scene),        sizeof(gmt_sample_source), sizeof(gmt_graph_view),
                            sizeof(gmt_plan_out),     sizeof(gmt_plan_summary),  sizeof(gmt_problem),
-                           sizeof(gmt_di_params),    sizeof(gmt_batch_host)};
+                           sizeof(gmt_di_params),    sizeof(gmt_batch_host),    sizeof(gmt_quad_params)};
   const int32_t n = static_cast<int32_t>(sizeof(sizes) / sizeof(sizes[0]));
   for (int32_t i = 0; i < count && i < n; ++i) out[i] = sizes[i];
   return n;
@@ -663,7 +663,7 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
   if (b->cluster == 0) {
     b->cluster = 1;
     for (int q = 0; q < count; ++q)
-      if (insts[q]->desc.steering == GMT_STEER_DOUBLE_INTEGRATOR) b->cluster = 2;
+      if (insts[q]->desc.steering != GMT_STEER_EUCLIDEAN) b->cluster = 2;
   }
   int rc = plan_smem(ctx, max_n, max_d, max_nb, b->cluster, &b->smem, &b->obs);
   if (rc == GMT_OK)

@@ -44,14 +44,15 @@ struct DevInstance {
   const int32_t* in_path; // may be null (all exact edges)
   const int64_t* path_ptr;
   const double* path_pts;
-  // Double-integrator instances built on the device (steering == 2) keep
-  // each in-edge's duration instead of a cached polyline; the solve kernel
-  // regenerates the trajectory waypoints of the one edge it checks (di.cuh).
+  // Kinodynamic instances built on the device (steering 2 = double
+  // integrator, 3 = quadrotor) keep each in-edge's duration instead of a
+  // cached polyline; the solve kernel regenerates the trajectory waypoints
+  // of the one edge it checks (di.cuh, quad.cuh).  kin_p: DI {vmax, weight},
+  // quadrotor {g, vmax, amax, ymax, wmax, weight}.
   const double* in_tau;
   int32_t steering;
-  int32_t di_segments;
-  double di_vmax;
-  double di_weight;
+  int32_t kin_segments;
+  double kin_p[6];
 };
 
 // Scalars of one PlanResult (planner.hpp:43-51).

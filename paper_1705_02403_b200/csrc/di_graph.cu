@@ -1,12 +1,14 @@
-// di_graph.cu -- the directed r-disk graph of the 6D double integrator
-// built on the device, in the reference's
+// di_graph.cu -- the directed r-disk graphs of the kinodynamic steering
+// models (the 6D double integrator, di.cuh, and the
+// 12D linearised quadrotor, quad.cuh) built on the device, in the reference's
 // NeighborGraph conventions (graph.cpp:117-188): out-row u = targets v != u
 // with cost(u -> v) <= r ascending, in-row x = sources u with
 // cost(u -> x) <= r ascending (the sequential merge order), path ids in
 // (source, target) order (graph.cpp:172-183).
 //
-// Kernels: warp per row, lanes over 32 consecutive columns, the steering
-// solve per pair (di.cuh), ballot + popc ordered compaction; a count pass,
+// Kernels (templated on the model): warp per row, lanes over 32 consecutive
+// columns, the model's exact-safe prefilter then its steering solve per
+// pair, ballot + popc ordered compaction; a count pass,
 // an exclusive scan, a fill pass, for the out-rows and (roles swapped) the
 // in-rows; optionally every out-edge's waypoint polyline.
 #include <cuda_runtime.h>
@@ -17,6 +19,7 @@
 
 #include "common.cuh"
 #include "di.cuh"
+#include "quad.cuh"
 #include "internal.cuh"
 #include "offline.cuh"
 
@@ -43,12 +46,40 @@ __device__ __forceinline__ bool di_may_connect(const double* x0, const double* x
   return true;
 }
 
+struct DiModel {
+  static constexpr int kDim = kDiDim;
+  DiParams P;
+  double bound;  // di_prefilter_bound
+  __device__ bool may(const double* a, const double* b) const { return di_may_connect(a, b, bound); }
+  __device__ double cost_tau(const double* a, const double* b, double* t) const {
+    return di_cost_tau(a, b, P, t);
+  }
+  __device__ double coord(const double* a, const double* b, double tau, int k, int i) const {
+    return di_coord(a, b, tau, k, i, P);
+  }
+  int segments() const { return P.segments; }
+};
+
+struct QuadModel {
+  static constexpr int kDim = kQuadDim;
+  QuadParams P;
+  double radius;
+  __device__ bool may(const double* a, const double* b) const { return quad_may_connect(a, b, P, radius); }
+  __device__ double cost_tau(const double* a, const double* b, double* t) const {
+    return quad_cost_tau(a, b, P, t);
+  }
+  __device__ double coord(const double* a, const double* b, double tau, int k, int i) const {
+    return quad_coord(a, b, tau, k, i, P);
+  }
+  int segments() const { return P.segments; }
+};
+
 // SWAP = false: row r lists targets c with cost(r -> c) <= radius.
 // SWAP = true:  row r lists sources c with cost(c -> r) <= radius.
-template <bool SWAP, bool FILL>
-__global__ void __launch_bounds__(256) di_rows_kernel(const double* __restrict__ coords, int n,
-                                                      DiParams P, double radius, double bound,
-                                                      int64_t* __restrict__ counts,
+template <class Model, bool SWAP, bool FILL>
+__global__ void __launch_bounds__(256) kino_rows_kernel(const double* __restrict__ coords, int n,
+                                                        Model model, double radius,
+                                                        int64_t* __restrict__ counts,
                                                       const int64_t* __restrict__ row_ptr,
                                                       int32_t* __restrict__ col,
                                                       double* __restrict__ cost,
@@ -56,20 +87,21 @@ __global__ void __launch_bounds__(256) di_rows_kernel(const double* __restrict__
   const int lane = threadIdx.x & 31;
   const int warps = (blockDim.x >> 5) * gridDim.x;
   for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
-    double xr[kDiDim];
-    for (int k = 0; k < kDiDim; ++k) xr[k] = __ldg(coords + static_cast<int64_t>(r) * kDiDim + k);
+    constexpr int kD = Model::kDim;
+    double xr[kD];
+    for (int k = 0; k < kD; ++k) xr[k] = __ldg(coords + static_cast<int64_t>(r) * kD + k);
     int64_t out = FILL ? row_ptr[r] : 0;
     for (int base = 0; base < n; base += 32) {
       const int c = base + lane;
       bool keep = false;
       double cc = 0.0, tc = 0.0;
       if (c < n && c != r) {
-        double xc[kDiDim];
-        for (int k = 0; k < kDiDim; ++k) xc[k] = __ldg(coords + static_cast<int64_t>(c) * kDiDim + k);
+        double xc[kD];
+        for (int k = 0; k < kD; ++k) xc[k] = __ldg(coords + static_cast<int64_t>(c) * kD + k);
         const double* from = SWAP ? xc : xr;
         const double* to = SWAP ? xr : xc;
-        if (di_may_connect(from, to, bound)) {
-          cc = di_cost_tau(from, to, P, &tc);
+        if (model.may(from, to)) {
+          cc = model.cost_tau(from, to, &tc);
           keep = cc <= radius;
         }
       }
@@ -105,29 +137,33 @@ __global__ void in_path_kernel(const int64_t* __restrict__ in_ptr, const int32_t
   }
 }
 
-// Waypoints of every out-edge: path e = pts[e*(M+1)*6 ...] (M+1 states,
+// Waypoints of every out-edge: path e = pts[e*(M+1)*D ...] (M+1 states,
 // the degenerate zero-duration edge repeats its single state).
-__global__ void di_paths_kernel(const double* __restrict__ coords, const int64_t* __restrict__ out_ptr,
-                                const int32_t* __restrict__ out_col, const double* __restrict__ out_tau,
-                                int n, DiParams P, double* __restrict__ pts) {
-  const int M = P.segments;
+template <class Model>
+__global__ void kino_paths_kernel(const double* __restrict__ coords, const int64_t* __restrict__ out_ptr,
+                                  const int32_t* __restrict__ out_col, const double* __restrict__ out_tau,
+                                  int n, Model model, int M, double* __restrict__ pts) {
+  constexpr int kD = Model::kDim;
   for (int u = blockIdx.x; u < n; u += gridDim.x) {
-    const double* x0 = coords + static_cast<int64_t>(u) * kDiDim;
+    const double* x0 = coords + static_cast<int64_t>(u) * kD;
     for (int64_t e = out_ptr[u] + threadIdx.x; e < out_ptr[u + 1]; e += blockDim.x) {
-      const double* x1 = coords + static_cast<int64_t>(out_col[e]) * kDiDim;
-      double* p = pts + e * (M + 1) * kDiDim;
-      for (int k = 0; k <= M; ++k) di_waypoint(x0, x1, out_tau[e], k, P, p + k * kDiDim);
+      const double* x1 = coords + static_cast<int64_t>(out_col[e]) * kD;
+      double* p = pts + e * (M + 1) * kD;
+      for (int k = 0; k <= M; ++k)
+        for (int i = 0; i < kD; ++i) p[k * kD + i] = model.coord(x0, x1, out_tau[e], k, i);
     }
   }
 }
 
-__global__ void di_pairs_kernel(const double* __restrict__ x0s, const double* __restrict__ x1s,
-                                int64_t count, DiParams P, double* __restrict__ cost,
-                                double* __restrict__ tau) {
+template <class Model>
+__global__ void kino_pairs_kernel(const double* __restrict__ x0s, const double* __restrict__ x1s,
+                                  int64_t count, Model model, double* __restrict__ cost,
+                                  double* __restrict__ tau) {
+  constexpr int kD = Model::kDim;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double t;
-    cost[i] = di_cost_tau(x0s + i * kDiDim, x1s + i * kDiDim, P, &t);
+    cost[i] = model.cost_tau(x0s + i * kD, x1s + i * kD, &t);
     tau[i] = t;
   }
 }
@@ -167,8 +203,9 @@ __global__ void __launch_bounds__(1024) scan_rows_kernel(const int64_t* __restri
   if (tid == 0) row_ptr[n] = carry;
 }
 
-int rows_pass(gmt_ctx* ctx, bool swap, const double* coords, int n, const DiParams& P, double radius,
-              double bound, Arena& mem, DiRows* rows, bool with_tau) {
+template <class Model>
+int rows_pass(gmt_ctx* ctx, bool swap, const double* coords, int n, const Model& model, double radius,
+              Arena& mem, DiRows* rows, bool with_tau) {
   cudaStream_t s = ctx->stream;
   const int blocks = std::max(1, std::min((n + 7) / 8, ctx->sm_count * 8));
   Arena cnt;
@@ -176,11 +213,11 @@ int rows_pass(gmt_ctx* ctx, bool swap, const double* coords, int n, const DiPara
   if (rc) return rc;
   int64_t* counts = static_cast<int64_t*>(cnt.ptr);
   if (swap)
-    di_rows_kernel<true, false><<<blocks, 256, 0, s>>>(coords, n, P, radius, bound, counts, nullptr,
-                                                       nullptr, nullptr, nullptr);
+    kino_rows_kernel<Model, true, false><<<blocks, 256, 0, s>>>(coords, n, model, radius, counts, nullptr,
+                                                                nullptr, nullptr, nullptr);
   else
-    di_rows_kernel<false, false><<<blocks, 256, 0, s>>>(coords, n, P, radius, bound, counts, nullptr,
-                                                        nullptr, nullptr, nullptr);
+    kino_rows_kernel<Model, false, false><<<blocks, 256, 0, s>>>(coords, n, model, radius, counts, nullptr,
+                                                                 nullptr, nullptr, nullptr);
   GMT_CUDA(cudaGetLastError());
   Arena rp;
   rc = rp.reserve(sizeof(int64_t) * (n + 1));
@@ -213,11 +250,11 @@ int rows_pass(gmt_ctx* ctx, bool swap, const double* coords, int n, const DiPara
   rows->edges = E;
   GMT_CUDA(cudaMemcpyAsync(rows->ptr, rp.ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
   if (swap)
-    di_rows_kernel<true, true><<<blocks, 256, 0, s>>>(coords, n, P, radius, bound, nullptr, rows->ptr,
-                                                      rows->col, rows->cost, rows->tau);
+    kino_rows_kernel<Model, true, true><<<blocks, 256, 0, s>>>(coords, n, model, radius, nullptr, rows->ptr,
+                                                               rows->col, rows->cost, rows->tau);
   else
-    di_rows_kernel<false, true><<<blocks, 256, 0, s>>>(coords, n, P, radius, bound, nullptr, rows->ptr,
-                                                       rows->col, rows->cost, rows->tau);
+    kino_rows_kernel<Model, false, true><<<blocks, 256, 0, s>>>(coords, n, model, radius, nullptr,
+                                                                rows->ptr, rows->col, rows->cost, rows->tau);
   GMT_CUDA(cudaGetLastError());
   ++ctx->launches;
   GMT_CUDA(cudaStreamSynchronize(s));
@@ -226,24 +263,14 @@ int rows_pass(gmt_ctx* ctx, bool swap, const double* coords, int n, const DiPara
   return GMT_OK;
 }
 
-}  // namespace
-
-DiParams to_di(const gmt_di_params* p) {
-  DiParams P;
-  P.vmax = p->vmax;
-  P.weight = p->weight;
-  P.segments = p->segments;
-  P.reserved = 0;
-  return P;
-}
-
-int validate_di(const gmt_di_params* p) {
-  if (!p) return set_error(GMT_E_INVALID_INPUT, "double-integrator parameters are null");
-  if (!(p->vmax > 0.0)) return set_error(GMT_E_INVALID_INPUT, "di.vmax must be positive");
-  if (!(p->weight > 0.0)) return set_error(GMT_E_INVALID_INPUT, "di.weight must be positive");
-  if (p->segments < 1 || p->segments > 64)
-    return set_error(GMT_E_INVALID_INPUT, "di.segments must be in [1, 64]");
-  return GMT_OK;
+template <class Model>
+int build_kino_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const Model& model, double radius,
+                         Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in) {
+  if (!(radius > 0.0)) return set_error(GMT_E_INVALID_INPUT, "connection radius must be positive");
+  if (n < 1) return set_error(GMT_E_INVALID_INPUT, "cannot build a graph over zero samples");
+  int rc = rows_pass(ctx, false, d_coords, n, model, radius, out_mem, out, true);
+  if (rc) return rc;
+  return rows_pass(ctx, true, d_coords, n, model, radius, in_mem, in, true);
 }
 
 double di_prefilter_bound(const DiParams& P, double radius) {
@@ -251,39 +278,38 @@ double di_prefilter_bound(const DiParams& P, double radius) {
   return (P.vmax * radius + radius * radius / (2.0 * std::sqrt(3.0 * P.weight))) * (1.0 + 1e-9) + 1e-12;
 }
 
-int build_di_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const DiParams& P, double radius,
-                       Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in) {
-  if (!(radius > 0.0)) return set_error(GMT_E_INVALID_INPUT, "connection radius must be positive");
-  if (n < 1) return set_error(GMT_E_INVALID_INPUT, "cannot build a graph over zero samples");
-  const double bound = di_prefilter_bound(P, radius);
-  int rc = rows_pass(ctx, false, d_coords, n, P, radius, bound, out_mem, out, true);
-  if (rc) return rc;
-  return rows_pass(ctx, true, d_coords, n, P, radius, bound, in_mem, in, true);
+DiModel di_model(const gmt_di_params* p, double radius) {
+  DiModel m;
+  m.P = to_di(p);
+  m.bound = di_prefilter_bound(m.P, radius);
+  return m;
 }
 
-}  // namespace gmtb
+QuadModel quad_model(const gmt_quad_params* p, double radius) {
+  QuadModel m;
+  m.P = to_quad(p);
+  m.radius = radius;
+  return m;
+}
 
-using namespace gmtb;
-
-extern "C" int gmt_di_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count,
-                            const gmt_di_params* params, double* cost_out, double* tau_out) {
-  int rc = validate_di(params);
-  if (rc) return rc;
+template <class Model>
+int kino_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count, const Model& model,
+               double* cost_out, double* tau_out) {
   if (count <= 0) return GMT_OK;
-  const DiParams P = to_di(params);
+  constexpr int kD = Model::kDim;
   Arena buf;
-  const size_t xs = sizeof(double) * kDiDim * static_cast<size_t>(count);
-  rc = buf.reserve(2 * xs + 2 * sizeof(double) * count);
+  const size_t xs = sizeof(double) * kD * static_cast<size_t>(count);
+  int rc = buf.reserve(2 * xs + 2 * sizeof(double) * count);
   if (rc) return rc;
   double* d0 = static_cast<double*>(buf.ptr);
-  double* d1 = d0 + kDiDim * count;
-  double* dc = d1 + kDiDim * count;
+  double* d1 = d0 + kD * count;
+  double* dc = d1 + kD * count;
   double* dt = dc + count;
   cudaStream_t s = ctx->stream;
   GMT_CUDA(cudaMemcpyAsync(d0, x0s, xs, cudaMemcpyHostToDevice, s));
   GMT_CUDA(cudaMemcpyAsync(d1, x1s, xs, cudaMemcpyHostToDevice, s));
   const int blocks = static_cast<int>(std::min<int64_t>((count + 255) / 256, 4096));
-  di_pairs_kernel<<<blocks, 256, 0, s>>>(d0, d1, count, P, dc, dt);
+  kino_pairs_kernel<Model><<<blocks, 256, 0, s>>>(d0, d1, count, model, dc, dt);
   GMT_CUDA(cudaGetLastError());
   ++ctx->launches;
   GMT_CUDA(cudaMemcpyAsync(cost_out, dc, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
@@ -293,24 +319,23 @@ extern "C" int gmt_di_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, 
   return GMT_OK;
 }
 
-extern "C" int gmt_build_di_graph(gmt_ctx* ctx, const double* coords, int32_t n,
-                                  const gmt_di_params* params, double radius, int64_t* num_edges,
-                                  int64_t* out_ptr, int32_t* out_col, double* out_cost,
-                                  double* out_tau, int64_t* in_ptr, int32_t* in_col,
-                                  double* in_cost, int32_t* in_path, double* path_pts) {
-  int rc = validate_di(params);
-  if (rc) return rc;
+template <class Model>
+int build_kino_graph_host(gmt_ctx* ctx, const double* coords, int32_t n, const Model& model, double radius,
+                          int64_t* num_edges, int64_t* out_ptr, int32_t* out_col, double* out_cost,
+                          double* out_tau, int64_t* in_ptr, int32_t* in_col, double* in_cost,
+                          int32_t* in_path, double* path_pts) {
   if (n < 1) return set_error(GMT_E_INVALID_INPUT, "cannot build a graph over zero samples");
-  const DiParams P = to_di(params);
+  constexpr int kD = Model::kDim;
+  const int M = model.segments();
   cudaStream_t s = ctx->stream;
   Arena cbuf;
-  rc = cbuf.reserve(sizeof(double) * kDiDim * static_cast<size_t>(n));
+  int rc = cbuf.reserve(sizeof(double) * kD * static_cast<size_t>(n));
   if (rc) return rc;
-  GMT_CUDA(cudaMemcpyAsync(cbuf.ptr, coords, sizeof(double) * kDiDim * n, cudaMemcpyHostToDevice, s));
+  GMT_CUDA(cudaMemcpyAsync(cbuf.ptr, coords, sizeof(double) * kD * n, cudaMemcpyHostToDevice, s));
   const double* dc = static_cast<const double*>(cbuf.ptr);
   Arena om, im;
   DiRows o, in;
-  rc = build_di_graph_dev(ctx, dc, n, P, radius, om, &o, im, &in);
+  rc = build_kino_graph_dev(ctx, dc, n, model, radius, om, &o, im, &in);
   if (rc) {
     cbuf.release();
     return rc;
@@ -331,7 +356,7 @@ extern "C" int gmt_build_di_graph(gmt_ctx* ctx, const double* coords, int32_t n,
     get(in_cost, in.cost, sizeof(double) * E);
     Arena extra;
     if (in_path || path_pts) {
-      const size_t pts_bytes = path_pts ? sizeof(double) * E * (P.segments + 1) * kDiDim : 0;
+      const size_t pts_bytes = path_pts ? sizeof(double) * E * (M + 1) * kD : 0;
       rc = extra.reserve(sizeof(int32_t) * E + pts_bytes + 16);
       if (rc) return rc;
       int32_t* ip = static_cast<int32_t*>(extra.ptr);
@@ -344,7 +369,8 @@ extern "C" int gmt_build_di_graph(gmt_ctx* ctx, const double* coords, int32_t n,
         get(in_path, ip, sizeof(int32_t) * E);
       }
       if (path_pts) {
-        di_paths_kernel<<<std::max(1, std::min(n, 4096)), 128, 0, s>>>(dc, o.ptr, o.col, o.tau, n, P, pp);
+        kino_paths_kernel<Model><<<std::max(1, std::min(n, 4096)), 128, 0, s>>>(dc, o.ptr, o.col, o.tau, n,
+                                                                               model, M, pp);
         GMT_CUDA(cudaGetLastError());
         ++ctx->launches;
         get(path_pts, pp, pts_bytes);
@@ -358,4 +384,97 @@ extern "C" int gmt_build_di_graph(gmt_ctx* ctx, const double* coords, int32_t n,
   im.release();
   cbuf.release();
   return GMT_OK;
+}
+
+}  // namespace
+
+DiParams to_di(const gmt_di_params* p) {
+  DiParams P;
+  P.vmax = p->vmax;
+  P.weight = p->weight;
+  P.segments = p->segments;
+  P.reserved = 0;
+  return P;
+}
+
+QuadParams to_quad(const gmt_quad_params* p) {
+  QuadParams P;
+  P.g = p->g;
+  P.vmax = p->vmax;
+  P.amax = p->amax;
+  P.ymax = p->ymax;
+  P.wmax = p->wmax;
+  P.weight = p->weight;
+  P.segments = p->segments;
+  P.reserved = 0;
+  return P;
+}
+
+int validate_di(const gmt_di_params* p) {
+  if (!p) return set_error(GMT_E_INVALID_INPUT, "double-integrator parameters are null");
+  if (!(p->vmax > 0.0)) return set_error(GMT_E_INVALID_INPUT, "di.vmax must be positive");
+  if (!(p->weight > 0.0)) return set_error(GMT_E_INVALID_INPUT, "di.weight must be positive");
+  if (p->segments < 1 || p->segments > 64)
+    return set_error(GMT_E_INVALID_INPUT, "di.segments must be in [1, 64]");
+  return GMT_OK;
+}
+
+int validate_quad(const gmt_quad_params* p) {
+  if (!p) return set_error(GMT_E_INVALID_INPUT, "quadrotor parameters are null");
+  if (!(p->g > 0.0) || !(p->vmax > 0.0) || !(p->amax > 0.0) || !(p->ymax > 0.0) || !(p->wmax > 0.0) ||
+      !(p->weight > 0.0))
+    return set_error(GMT_E_INVALID_INPUT, "quad.g, vmax, amax, ymax, wmax, weight must be positive");
+  if (p->segments < 1 || p->segments > 64)
+    return set_error(GMT_E_INVALID_INPUT, "quad.segments must be in [1, 64]");
+  return GMT_OK;
+}
+
+int build_di_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const gmt_di_params* p, double radius,
+                       Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in) {
+  return build_kino_graph_dev(ctx, d_coords, n, di_model(p, radius), radius, out_mem, out, in_mem, in);
+}
+
+int build_quad_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const gmt_quad_params* p,
+                         double radius, Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in) {
+  return build_kino_graph_dev(ctx, d_coords, n, quad_model(p, radius), radius, out_mem, out, in_mem, in);
+}
+
+}  // namespace gmtb
+
+using namespace gmtb;
+
+extern "C" int gmt_di_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count,
+                            const gmt_di_params* params, double* cost_out, double* tau_out) {
+  int rc = validate_di(params);
+  if (rc) return rc;
+  return kino_costs(ctx, x0s, x1s, count, di_model(params, 1.0), cost_out, tau_out);
+}
+
+extern "C" int gmt_quad_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count,
+                              const gmt_quad_params* params, double* cost_out, double* tau_out) {
+  int rc = validate_quad(params);
+  if (rc) return rc;
+  return kino_costs(ctx, x0s, x1s, count, quad_model(params, 1.0), cost_out, tau_out);
+}
+
+extern "C" int gmt_build_di_graph(gmt_ctx* ctx, const double* coords, int32_t n,
+                                  const gmt_di_params* params, double radius, int64_t* num_edges,
+                                  int64_t* out_ptr, int32_t* out_col, double* out_cost,
+                                  double* out_tau, int64_t* in_ptr, int32_t* in_col,
+                                  double* in_cost, int32_t* in_path, double* path_pts) {
+  int rc = validate_di(params);
+  if (rc) return rc;
+  return build_kino_graph_host(ctx, coords, n, di_model(params, radius), radius, num_edges, out_ptr,
+                               out_col, out_cost, out_tau, in_ptr, in_col, in_cost, in_path, path_pts);
+}
+
+extern "C" int gmt_build_quad_graph(gmt_ctx* ctx, const double* coords, int32_t n,
+                                    const gmt_quad_params* params, double radius, int64_t* num_edges,
+                                    int64_t* out_ptr, int32_t* out_col, double* out_cost,
+                                    double* out_tau, int64_t* in_ptr, int32_t* in_col,
+                                    double* in_cost, int32_t* in_path, double* path_pts) {
+  int rc = validate_quad(params);
+  if (rc) return rc;
+  return build_kino_graph_host(ctx, coords, n, quad_model(params, radius), radius, num_edges, out_ptr,
+                               out_col, out_cost, out_tau, in_ptr, in_col, in_cost, in_path, path_pts);
 }

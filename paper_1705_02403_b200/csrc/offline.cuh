@@ -24,7 +24,7 @@ struct DevSamples {
 int sample_free_dev(gmt_ctx* ctx, int32_t n, const gmt_scene* scene, const gmt_sample_source* src,
                     Arena& out, DevSamples* s);
 
-// Double-integrator graphs (di_graph.cu): one direction's compressed rows.
+// Kinodynamic graphs (di_graph.cu): one direction's compressed rows.
 struct DiRows {
   int64_t* ptr = nullptr;
   int32_t* col = nullptr;
@@ -33,10 +33,15 @@ struct DiRows {
   int64_t edges = 0;
 };
 struct DiParams;
+struct QuadParams;
 DiParams to_di(const gmt_di_params* p);
+QuadParams to_quad(const gmt_quad_params* p);
 int validate_di(const gmt_di_params* p);
-int build_di_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const DiParams& P, double radius,
+int validate_quad(const gmt_quad_params* p);
+int build_di_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const gmt_di_params* p, double radius,
                        Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in);
+int build_quad_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const gmt_quad_params* p,
+                         double radius, Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in);
 
 // append_init on device samples (sampling.cpp:144-154).
 int append_init_dev(gmt_ctx* ctx, int dim, DevSamples* s, const double* init, int has_heading,

@@ -21,6 +21,7 @@
 #include "internal.cuh"
 #include "di.cuh"
 #include "offline.cuh"
+#include "quad.cuh"
 
 namespace gmtb {
 
@@ -619,7 +620,8 @@ extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instan
     samples.release();
     return rc;
   }
-  const bool di = p->steering == GMT_STEER_DOUBLE_INTEGRATOR;
+  const bool quad = p->steering == GMT_STEER_QUADROTOR;
+  const bool di = p->steering == GMT_STEER_DOUBLE_INTEGRATOR || quad;  // kinodynamic, directed
   if (p->steering != GMT_STEER_EUCLIDEAN && !di) {
     samples.release();
     return set_error(GMT_E_INVALID_INPUT, "unsupported steering model");
@@ -629,7 +631,7 @@ extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instan
     if (di) {  // the Theorem 1 radius assumes straight-line costs
       samples.release();
       return set_error(GMT_E_INVALID_INPUT,
-                       "the double integrator needs radius_override (a cost threshold)");
+                       "kinodynamic steering needs radius_override (a cost threshold)");
     }
     rc = gmt_connection_radius(d, p->n, p->eta, 1.0 /* free_measure_upper_bound, space.cpp:101-104 */,
                                &radius);
@@ -644,12 +646,18 @@ extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instan
   double* cost = nullptr;
   DiRows dout, din;
   if (di) {
-    if (d != kDiDim) {
+    if (d != (quad ? kQuadDim : kDiDim)) {
       samples.release();
-      return set_error(GMT_E_INVALID_INPUT, "the double integrator needs dimension 6");
+      return set_error(GMT_E_INVALID_INPUT, quad ? "the quadrotor needs dimension 12"
+                                                 : "the double integrator needs dimension 6");
     }
-    rc = validate_di(&p->di);
-    if (rc == GMT_OK) rc = build_di_graph_dev(ctx, S.coords, S.n, to_di(&p->di), radius, g, &dout, g2, &din);
+    if (quad) {
+      rc = validate_quad(&p->quad);
+      if (rc == GMT_OK) rc = build_quad_graph_dev(ctx, S.coords, S.n, &p->quad, radius, g, &dout, g2, &din);
+    } else {
+      rc = validate_di(&p->di);
+      if (rc == GMT_OK) rc = build_di_graph_dev(ctx, S.coords, S.n, &p->di, radius, g, &dout, g2, &din);
+    }
     E = dout.edges;
     rp = dout.ptr;
     col = dout.col;
@@ -716,10 +724,20 @@ extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instan
       D.in_col = din.col;
       D.in_cost = din.cost;
       D.in_tau = din.tau;
-      D.steering = GMT_STEER_DOUBLE_INTEGRATOR;
-      D.di_segments = p->di.segments;
-      D.di_vmax = p->di.vmax;
-      D.di_weight = p->di.weight;
+      D.steering = p->steering;
+      if (quad) {
+        D.kin_segments = p->quad.segments;
+        D.kin_p[0] = p->quad.g;
+        D.kin_p[1] = p->quad.vmax;
+        D.kin_p[2] = p->quad.amax;
+        D.kin_p[3] = p->quad.ymax;
+        D.kin_p[4] = p->quad.wmax;
+        D.kin_p[5] = p->quad.weight;
+      } else {
+        D.kin_segments = p->di.segments;
+        D.kin_p[0] = p->di.vmax;
+        D.kin_p[1] = p->di.weight;
+      }
     }
     inst->goal_idx_dev = reinterpret_cast<const int32_t*>(b + o_gidx);
     inst->graph_n = n;

@@ -36,6 +36,8 @@
 
 #include "common.cuh"
 #include "di.cuh"
+#include "quad.cuh"
+#include "gmt_b200.h"
 #include "solve.cuh"
 
 namespace cg = cooperative_groups;
@@ -274,27 +276,50 @@ __device__ bool polyline_free_warp(const DevInstance& I, int d, const Boxes& bx,
   return true;
 }
 
-// The same test for a double-integrator edge whose polyline is not stored:
-// lanes 0..5 and 16..21 evaluate the coordinates of waypoints s and s+1
-// (di_coord, the very function that materialises stored paths), then the
-// segment goes through segment_free_staged.
+// The same test for a kinodynamic edge whose polyline is not stored (double
+// integrator, quadrotor): lanes 0..dim-1 and 16..16+dim-1 evaluate the
+// coordinates of waypoints s and s+1 (di_coord / quad_coord, the very
+// functions that materialise stored paths), then the segment goes through
+// segment_free_staged.
 template <int D>
-__device__ bool di_edge_free_warp(const DevInstance& I, const Boxes& bx, int from, int to,
-                                  double tau, int lane, double* seg) {
-  DiParams P;
-  P.vmax = I.di_vmax;
-  P.weight = I.di_weight;
-  P.segments = I.di_segments;
-  P.reserved = 0;
-  const double* x0 = I.coords + static_cast<int64_t>(from) * kDiDim;
-  const double* x1 = I.coords + static_cast<int64_t>(to) * kDiDim;
-  if (tau == 0.0) return point_free_warp<D>(x0, kDiDim, bx, lane, seg);
-  for (int s = 0; s < P.segments; ++s) {
+__device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int from, int to,
+                                    double tau, int lane, double* seg) {
+  // Only the generic-dimension kernel can see a 12D quadrotor instance.
+  const bool quad = D == 0 && I.steering == GMT_STEER_QUADROTOR;
+  const int dim = quad ? kQuadDim : kDiDim;
+  const double* x0 = I.coords + static_cast<int64_t>(from) * dim;
+  const double* x1 = I.coords + static_cast<int64_t>(to) * dim;
+  if (tau == 0.0) return point_free_warp<D>(x0, dim, bx, lane, seg);
+  const int M = I.kin_segments;
+  const int i = lane & 15;
+  const int k = lane >> 4;
+  for (int s = 0; s < M; ++s) {
     __syncwarp();
-    if (lane < kDiDim) seg[lane] = di_coord(x0, x1, tau, s, lane, P);
-    if (lane >= 16 && lane < 16 + kDiDim) seg[lane] = di_coord(x0, x1, tau, s + 1, lane - 16, P);
+    if (i < dim) {
+      double v;
+      if (quad) {
+        QuadParams P;
+        P.g = I.kin_p[0];
+        P.vmax = I.kin_p[1];
+        P.amax = I.kin_p[2];
+        P.ymax = I.kin_p[3];
+        P.wmax = I.kin_p[4];
+        P.weight = I.kin_p[5];
+        P.segments = M;
+        P.reserved = 0;
+        v = quad_coord(x0, x1, tau, s + k, i, P);
+      } else {
+        DiParams P;
+        P.vmax = I.kin_p[0];
+        P.weight = I.kin_p[1];
+        P.segments = M;
+        P.reserved = 0;
+        v = di_coord(x0, x1, tau, s + k, i, P);
+      }
+      seg[lane] = v;
+    }
     __syncwarp();
-    if (!segment_free_staged<D>(kDiDim, bx, lane, seg)) return false;
+    if (!segment_free_staged<D>(dim, bx, lane, seg)) return false;
   }
   return true;
 }
@@ -726,8 +751,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
           ++my_checks;
           const int32_t pid = I.in_path ? __ldg(I.in_path + be) : -1;
           bool ok;
-          if (I.in_tau) {  // double integrator: regenerated polyline (di.cuh)
-            ok = di_edge_free_warp<D>(I, bx, by, x, __ldg(I.in_tau + be), lane, seg);
+          if ((D == 0 || D == 6) && I.in_tau) {  // kinodynamic: regenerated polyline (di.cuh, quad.cuh)
+            ok = kino_edge_free_warp<D>(I, bx, by, x, __ldg(I.in_tau + be), lane, seg);
           } else if (pid < 0) {  // straight edge: segment_free (planner.cpp:59)
             if (lane < d) seg[lane] = __ldg(I.coords + static_cast<int64_t>(by) * d + lane);
             __syncwarp();

@@ -46,6 +46,10 @@ SIGNATURES = [
     ("gmt_build_neighbor_graph", C.c_int, [_vp, _dp, C.c_int32, C.c_int32, C.c_double, _i64p,
                                            _i64p, _i32p, _dp]),
     ("gmt_di_costs", C.c_int, [_vp, _dp, _dp, C.c_int64, _P(abi.DiParams), _dp, _dp]),
+    ("gmt_quad_costs", C.c_int, [_vp, _dp, _dp, C.c_int64, _P(abi.QuadParams), _dp, _dp]),
+    ("gmt_build_quad_graph", C.c_int, [_vp, _dp, C.c_int32, _P(abi.QuadParams), C.c_double,
+                                       _i64p, _i64p, _i32p, _dp, _dp, _i64p, _i32p, _dp, _i32p,
+                                       _dp]),
     ("gmt_build_di_graph", C.c_int, [_vp, _dp, C.c_int32, _P(abi.DiParams), C.c_double, _i64p,
                                      _i64p, _i32p, _dp, _dp, _i64p, _i32p, _dp, _i32p, _dp]),
     ("gmt_instance_upload", C.c_int, [_vp, _P(abi.Scene), _dp, C.c_int32, C.c_int32,
@@ -271,44 +275,55 @@ class Context:
     # ---- double integrator (NEW model) ----------------------
     def di_costs(self, x0s, x1s, params: abi.DiParams):
         """Device cost and duration of each state pair (rows of x0s, x1s)."""
-        x0s, x1s = abi.f64(x0s).reshape(-1, 6), abi.f64(x1s).reshape(-1, 6)
-        m = x0s.shape[0]
-        cost, tau = np.zeros(m), np.zeros(m)
-        check(lib().gmt_di_costs(self.h, abi.ptr(x0s, C.c_double), abi.ptr(x1s, C.c_double), m,
-                                 C.byref(params), abi.ptr(cost, C.c_double),
-                                 abi.ptr(tau, C.c_double)))
-        return cost, tau
+        return self._kino_costs(lib().gmt_di_costs, 6, x0s, x1s, params)
 
     def build_di_graph(self, coords, params: abi.DiParams, radius: float,
                        paths: bool = True) -> Graph:
         """Directed DI graph (out-rows, in-rows, optional waypoint paths) as a
         reference-shaped Graph: path ids = out-edge indices."""
+        return self._kino_graph(lib().gmt_build_di_graph, 6, coords, params, radius, paths)
+
+    # ---- quadrotor (NEW model, DESIGN.md §3.3) ------------------------------
+    def quad_costs(self, x0s, x1s, params: abi.QuadParams):
+        return self._kino_costs(lib().gmt_quad_costs, 12, x0s, x1s, params)
+
+    def build_quad_graph(self, coords, params: abi.QuadParams, radius: float,
+                         paths: bool = True) -> Graph:
+        return self._kino_graph(lib().gmt_build_quad_graph, 12, coords, params, radius, paths)
+
+    def _kino_costs(self, fn, dim, x0s, x1s, params):
+        x0s, x1s = abi.f64(x0s).reshape(-1, dim), abi.f64(x1s).reshape(-1, dim)
+        m = x0s.shape[0]
+        cost, tau = np.zeros(m), np.zeros(m)
+        check(fn(self.h, abi.ptr(x0s, C.c_double), abi.ptr(x1s, C.c_double), m, C.byref(params),
+                 abi.ptr(cost, C.c_double), abi.ptr(tau, C.c_double)))
+        return cost, tau
+
+    def _kino_graph(self, fn, dim, coords, params, radius, paths) -> Graph:
         coords = abi.f64(coords)
         n = coords.shape[0]
         ne = C.c_int64()
         z = lambda t: abi.ptr(None, t)  # noqa: E731
-        check(lib().gmt_build_di_graph(self.h, abi.ptr(coords, C.c_double), n, C.byref(params),
-                                       radius, C.byref(ne), z(C.c_int64), z(C.c_int32),
-                                       z(C.c_double), z(C.c_double), z(C.c_int64), z(C.c_int32),
-                                       z(C.c_double), z(C.c_int32), z(C.c_double)))
+        check(fn(self.h, abi.ptr(coords, C.c_double), n, C.byref(params), radius, C.byref(ne),
+                 z(C.c_int64), z(C.c_int32), z(C.c_double), z(C.c_double), z(C.c_int64),
+                 z(C.c_int32), z(C.c_double), z(C.c_int32), z(C.c_double)))
         E = ne.value
         M1 = params.segments + 1
         optr, iptr = np.zeros(n + 1, np.int64), np.zeros(n + 1, np.int64)
         ocol, icol = np.zeros(max(E, 1), np.int32), np.zeros(max(E, 1), np.int32)
         ocost, icost, otau = np.zeros(max(E, 1)), np.zeros(max(E, 1)), np.zeros(max(E, 1))
         ipath = np.zeros(max(E, 1), np.int32) if paths else None
-        pts = np.zeros(max(E, 1) * M1 * 6) if paths else None
-        check(lib().gmt_build_di_graph(
-            self.h, abi.ptr(coords, C.c_double), n, C.byref(params), radius, C.byref(ne),
-            abi.ptr(optr, C.c_int64), abi.ptr(ocol, C.c_int32), abi.ptr(ocost, C.c_double),
-            abi.ptr(otau, C.c_double), abi.ptr(iptr, C.c_int64), abi.ptr(icol, C.c_int32),
-            abi.ptr(icost, C.c_double), abi.ptr(ipath, C.c_int32), abi.ptr(pts, C.c_double)))
-        g = Graph(n, radius, optr, ocol[:E], ocost[:E], dim=6, directed=True, in_ptr=iptr,
+        pts = np.zeros(max(E, 1) * M1 * dim) if paths else None
+        check(fn(self.h, abi.ptr(coords, C.c_double), n, C.byref(params), radius, C.byref(ne),
+                 abi.ptr(optr, C.c_int64), abi.ptr(ocol, C.c_int32), abi.ptr(ocost, C.c_double),
+                 abi.ptr(otau, C.c_double), abi.ptr(iptr, C.c_int64), abi.ptr(icol, C.c_int32),
+                 abi.ptr(icost, C.c_double), abi.ptr(ipath, C.c_int32), abi.ptr(pts, C.c_double)))
+        g = Graph(n, radius, optr, ocol[:E], ocost[:E], dim=dim, directed=True, in_ptr=iptr,
                   in_col=icol[:E], in_cost=icost[:E],
                   out_path=np.arange(E, dtype=np.int32) if paths else None,
                   in_path=None if ipath is None else ipath[:E],
                   path_ptr=np.arange(E + 1, dtype=np.int64) * M1 if paths else None,
-                  path_pts=None if pts is None else pts[: E * M1 * 6])
+                  path_pts=None if pts is None else pts[: E * M1 * dim])
         g.out_tau = otau[:E]
         return g
 

@@ -18,6 +18,10 @@ import numpy as np
 from . import abi
 from .errors import InvalidInputError
 
+# 12D quadrotor units: the unit workspace cube is 10 m, so g = 0.981 per s^2.
+QUAD_G = 0.981
+QUAD_RADIUS = 3.5
+
 SCHEMA = "gmt-problem/1"
 MASK64 = (1 << 64) - 1
 
@@ -74,11 +78,26 @@ class ProblemSpec:
     di_vmax: float = 0.5
     di_weight: float = 1.0
     di_segments: int = 8
+    quad_g: float = QUAD_G
+    quad_vmax: float = 0.5
+    quad_amax: float = 0.5
+    quad_ymax: float = math.pi
+    quad_wmax: float = 1.0
+    quad_weight: float = 0.1
+    quad_segments: int = 8
     _keep: list = field(default_factory=list, repr=False)
 
     def di_params(self) -> abi.DiParams:
         p = abi.DiParams()
         p.vmax, p.weight, p.segments, p.reserved = self.di_vmax, self.di_weight, self.di_segments, 0
+        return p
+
+    def quad_params(self) -> abi.QuadParams:
+        p = abi.QuadParams()
+        p.g, p.vmax, p.amax, p.ymax, p.wmax, p.weight = (
+            self.quad_g, self.quad_vmax, self.quad_amax, self.quad_ymax, self.quad_wmax,
+            self.quad_weight)
+        p.segments, p.reserved = self.quad_segments, 0
         return p
 
     @property
@@ -124,6 +143,7 @@ class ProblemSpec:
         p.steering = self.steering
         p.reserved = 0
         p.di = self.di_params()
+        p.quad = self.quad_params()
         return p
 
     def with_n(self, n: int) -> "ProblemSpec":
@@ -489,6 +509,54 @@ def random_di_query(master: int, q: int, n: int = 4000, pillars: int = 60,
                        goal_hi=np.concatenate([base.goal_hi, np.full(3, 0.75)]),
                        init=np.concatenate([base.init, np.full(3, 0.5)]), n=n,
                        radius_override=radius, steering=abi.STEER_DOUBLE_INTEGRATOR)
+
+
+def quad_scene(seed: int = 5, n: int = 8000, pillars: int = 90, beams: int = 40,
+               radius: float = QUAD_RADIUS, position_goal: bool = False) -> ProblemSpec:
+    """C4 "12D linearised quadrotor, complex box scene":
+    a 3D scene of `pillars` forest pillars plus `beams` horizontal beams
+    (Pcg32(seed)), extruded over the full range of the nine non-position
+    coordinates; start hovering at rest in the low corner, goal = a position
+    box in the far corner with |v| < 0.8 vmax, |roll|, |pitch| < 0.8 amax,
+    any yaw, |rates| < 0.8 wmax (about 15 goal samples at n = 8000);
+    Halton samples; the connection radius is a cost threshold.
+    position_goal: the goal constrains the position only (small-n tests)."""
+    rng = Pcg32(seed)
+    lo, hi = [], []
+    for _ in range(pillars):
+        cx = 0.1 + 0.8 * rng.next_double()
+        cy = 0.1 + 0.8 * rng.next_double()
+        hw = 0.02 + 0.03 * rng.next_double()
+        h = 0.5 + 0.5 * rng.next_double()
+        lo.append([cx - hw, cy - hw, 0.0])
+        hi.append([cx + hw, cy + hw, h])
+    for _ in range(beams):  # axis-aligned beams at random heights
+        ax = rng.next_u32() % 2
+        c = 0.1 + 0.8 * rng.next_double()
+        z = 0.1 + 0.8 * rng.next_double()
+        a = 0.8 * rng.next_double()
+        ln = 0.1 + 0.3 * rng.next_double()
+        hw = 0.01 + 0.02 * rng.next_double()
+        if ax == 0:
+            lo.append([a, c - hw, z - hw])
+            hi.append([min(a + ln, 1.0), c + hw, z + hw])
+        else:
+            lo.append([c - hw, a, z - hw])
+            hi.append([c + hw, min(a + ln, 1.0), z + hw])
+    B = len(lo)
+    box_lo = np.concatenate([np.array(lo).reshape(B, 3), np.zeros((B, 9))], axis=1)
+    box_hi = np.concatenate([np.array(hi).reshape(B, 3), np.ones((B, 9))], axis=1)
+    init = np.array([0.03, 0.03, 0.5] + [0.5] * 9)
+    glo = np.array([0.85, 0.85, 0.25] + [0.1] * 5 + [0.0] + [0.1] * 3)
+    ghi = np.array([1.0, 1.0, 0.75] + [0.9] * 5 + [1.0] + [0.9] * 3)
+    if position_goal:
+        glo[3:], ghi[3:] = 0.0, 1.0
+    spec = ProblemSpec(dim=12, box_lo=box_lo, box_hi=box_hi, goal_lo=glo, goal_hi=ghi, init=init,
+                       n=n, radius_override=radius, steering=abi.STEER_QUADROTOR,
+                       notes=f"12D quadrotor, {pillars} pillars + {beams} beams, Pcg32({seed}).")
+    if not spec.point_free(init):
+        raise InvalidInputError("quadrotor init collides")
+    return spec
 
 
 def connection_radius_py(dim: int, n: int, eta: float = 0.0, mu: float = 1.0) -> float:
