@@ -136,37 +136,6 @@ __device__ __forceinline__ bool any_box_contains(const double* p, int d, const B
   return __any_sync(kFull, in);
 }
 
-// segment_hits_box (space.cpp:60-78), closed slab clipping, axis loop
-// unrolled for a fixed dimension.
-template <int D>
-__device__ __forceinline__ bool clip_hits(const double* a, const double* b, int d_rt,
-                                          const double* lo, const double* hi, int st) {
-  const int d = dims<D>(d_rt);
-  double tmin = 0.0, tmax = 1.0;
-  // Not unrolled: the clip only runs for boxes that survive the separation
-  // pre-test, and its divisions are register-hungry.
-#pragma unroll 1
-  for (int k = 0; k < d; ++k) {
-    const double dk = __dsub_rn(b[k], a[k]);
-    const double l = lo[k * st], h = hi[k * st];
-    if (dk == 0.0) {
-      if (a[k] < l || a[k] > h) return false;
-    } else {
-      double t0 = __ddiv_rn(__dsub_rn(l, a[k]), dk);
-      double t1 = __ddiv_rn(__dsub_rn(h, a[k]), dk);
-      if (t0 > t1) {
-        const double t = t0;
-        t0 = t1;
-        t1 = t;
-      }
-      tmin = (tmin < t0) ? t0 : tmin;  // std::max(tmin, t0)
-      tmax = (t1 < tmax) ? t1 : tmax;  // std::min(tmax, t1)
-      if (tmin > tmax) return false;
-    }
-  }
-  return true;
-}
-
 // segment_free (space.cpp:80-90) of the segment staged in the warp's `seg`
 // scratch (a = seg[0..15], b = seg[16..31]).  Coordinate predicates run
 // lane-per-axis, boxes lane-per-box.
@@ -211,19 +180,28 @@ __device__ bool segment_free_staged(int d_rt, const Boxes& bx, int lane, const d
       mx[k] = x < y ? y : x;
     }
   }
+  // Boxes that survive the pre-test are clipped lane-parallel: lane
+  // (slot, axis) computes one axis' slab interval of the slot-th surviving
+  // box, and the d lanes of a slot combine max(0, t0_k) / min(1, t1_k) and
+  // the dk == 0 misses.  The clip's result is a function of those order-free
+  // max/min values, so this equals the reference's sequential axis loop.
+  const int per = kWarp / d;
+  const int slot = lane / d, axis = lane - slot * d;
   bool hit = false;
-  for (int i = lane; i < bx.count && !hit; i += kWarp) {
-    bool sep = false;
+  for (int i0 = 0; i0 < bx.count && !hit; i0 += kWarp) {
+    const int i = i0 + lane;
+    bool sep = i >= bx.count;
+    const int ic = sep ? bx.count - 1 : i;  // idle lanes read a valid box
 #pragma unroll
     for (int k = 0; k < (D > 0 ? D : kMaxSolveDim); ++k) {
       if (D == 0 && k >= d) break;
       double lo_k, hi_k;
       if (bx.lom) {
-        lo_k = bx.lom[i * bx.bs + k * bx.as];
-        hi_k = bx.him[i * bx.bs + k * bx.as];
+        lo_k = bx.lom[ic * bx.bs + k * bx.as];
+        hi_k = bx.him[ic * bx.bs + k * bx.as];
       } else {
-        lo_k = bx.lo[i * bx.bs + k * bx.as] - kSepMargin;
-        hi_k = bx.hi[i * bx.bs + k * bx.as] + kSepMargin;
+        lo_k = bx.lo[ic * bx.bs + k * bx.as] - kSepMargin;
+        hi_k = bx.hi[ic * bx.bs + k * bx.as] + kSepMargin;
       }
       double smin, smax;
       if constexpr (D > 0 && D <= 6) {
@@ -236,9 +214,47 @@ __device__ bool segment_free_staged(int d_rt, const Boxes& bx, int lane, const d
       }
       sep = sep || smax < lo_k || smin > hi_k;
     }
-    if (!sep) hit = clip_hits<D>(a, b, d, bx.lo + i * bx.bs, bx.hi + i * bx.bs, bx.as);
+    uint32_t cm = __ballot_sync(kFull, !sep);
+    while (cm) {
+      const int nc = __popc(cm);
+      const int take = nc < per ? nc : per;
+      bool miss = false;
+      double t0 = 0.0, t1 = 1.0;
+      if (slot < take) {
+        const int bi = i0 + static_cast<int>(__fns(cm, 0, slot + 1));
+        const double ak = a[axis];
+        const double dk = __dsub_rn(b[axis], ak);
+        const double l = bx.lo[bi * bx.bs + axis * bx.as], h = bx.hi[bi * bx.bs + axis * bx.as];
+        if (dk == 0.0) {
+          miss = ak < l || ak > h;
+        } else {
+          t0 = __ddiv_rn(__dsub_rn(l, ak), dk);
+          t1 = __ddiv_rn(__dsub_rn(h, ak), dk);
+          if (t0 > t1) {
+            const double t = t0;
+            t0 = t1;
+            t1 = t;
+          }
+        }
+      }
+      // Slot leaders (axis 0) fold in the other d - 1 axes' own values.
+      double tmin = t0, tmax = t1;
+      bool m = miss;
+      const int mi = miss ? 1 : 0;
+      for (int o = 1; o < d; ++o) {
+        const double u0 = __shfl_down_sync(kFull, t0, o);
+        const double u1 = __shfl_down_sync(kFull, t1, o);
+        const int um = __shfl_down_sync(kFull, mi, o);
+        tmin = (tmin < u0) ? u0 : tmin;
+        tmax = (u1 < tmax) ? u1 : tmax;
+        m = m || um != 0;
+      }
+      hit = __any_sync(kFull, axis == 0 && slot < take && !m && !(tmin > tmax));
+      if (hit || take == nc) break;
+      cm &= ~((1u << __fns(cm, 0, take + 1)) - 1u);  // drop the `take` boxes done
+    }
   }
-  return !__any_sync(kFull, hit);
+  return !hit;
 }
 
 template <int D>
@@ -379,7 +395,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   constexpr int kMaxWarps = WIDE ? 16 : 8;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
-  __shared__ double seg_s[kMaxWarps * 32];
+  __shared__ double seg_s[kMaxWarps * 64];  // per warp: two staged segments
 
   const int q = blockIdx.x / CS;
   int rank = 0;
@@ -413,7 +429,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  double* seg = seg_s + warp * 32;
+  double* seg = seg_s + warp * 64;
 
   Boxes bx;
   bx.count = nb;
@@ -603,43 +619,58 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       }
     }
 
+    // Rows are processed two at a time per warp: half-warp h (lanes 16h ..
+    // 16h+15) streams row k + h, so two rows' loads are in flight together.
+    const int h = lane >> 4, hl = lane & 15;
+
     // P4: mark unexplored out-neighbours of the owned group members
     // (planner.cpp:159-166).
     {
       const int own = sh.own_count;
-      int k = warp;
-      int64_t e0 = 0, e1 = 0;
-      if (k < own) {
-        const int g = list[k];
+      int k = 2 * warp;
+      int64_t e0 = 0;
+      int len = 0;
+      if (k + h < own) {
+        const int g = list[k + h];
         e0 = __ldg(I.out_ptr + g);
-        e1 = __ldg(I.out_ptr + g + 1);
+        len = static_cast<int>(__ldg(I.out_ptr + g + 1) - e0);
       }
       while (k < own) {
-        const int kn = k + nw;
-        int64_t n0 = 0, n1 = 0;
-        if (kn < own) {  // next row's offsets in flight during this row
-          const int gn = list[kn];
+        const int kn = k + 2 * nw;
+        int64_t n0 = 0;
+        int nlen = 0;
+        if (kn + h < own) {  // next rows' offsets in flight during these rows
+          const int gn = list[kn + h];
           n0 = __ldg(I.out_ptr + gn);
-          n1 = __ldg(I.out_ptr + gn + 1);
+          nlen = static_cast<int>(__ldg(I.out_ptr + gn + 1) - n0);
         }
-        for (int64_t base = e0; base < e1; base += kWarp * kUnroll) {
+        const int other = __shfl_xor_sync(kFull, len, 16);
+        const int lmax = len > other ? len : other;
+        for (int off = 0; off < lmax; off += 16 * kUnroll) {
           int xs[kUnroll];
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
-            const int64_t e = base + u * kWarp + lane;
-            xs[u] = e < e1 ? __ldg(I.out_col + e) : -1;
+            const int p = off + u * 16 + hl;
+            xs[u] = p < len ? __ldg(I.out_col + e0 + p) : -1;
           }
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
-            if (base + u * kWarp >= e1) break;  // warp-uniform
+            if (off + u * 16 >= lmax) break;  // warp-uniform
             const int x = xs[u];
             const bool valid = x >= 0;
             cnt_out += valid ? 1 : 0;
+            if constexpr (CS == 1) {
+              // One CTA: a shared-memory atomic per edge; explored targets
+              // are masked out when the candidate list is built.
+              if (valid) atomicOr(cand_w + (x >> 5), 1u << (x & 31));
+              continue;
+            }
             const int w = valid ? (x >> 5) : (-1 - lane);
             uint32_t bit = 0u;
             if (valid && !(((open_w[w] | closed_w[w]) >> (x & 31)) & 1u)) bit = 1u << (x & 31);
-            // Rows are sorted, so equal words form runs: suffix-OR each run
-            // into its first lane, which sets the word once.
+            // Each half's row is sorted, so equal words form runs: suffix-OR
+            // each run into its first lane, which sets the word once (an
+            // equal word in the other half only adds more of its own bits).
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
               const uint32_t ob = __shfl_down_sync(kFull, bit, o);
@@ -654,7 +685,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         }
         k = kn;
         e0 = n0;
-        e1 = n1;
+        len = nlen;
       }
     }
     cluster_barrier<CS>();  // [1] candidate marks complete
@@ -664,6 +695,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       uint32_t bits = cand_w[w];
       if (bits) {
         cand_w[w] = 0u;
+        if constexpr (CS == 1) bits &= ~(open_w[w] | closed_w[w]);
         int base = atomicAdd(&sh.cand_count, __popc(bits));
         while (bits) {
           const int b = __ffs(bits) - 1;
@@ -676,44 +708,50 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
     const int ccount = sh.cand_count;
 
     // P5 + P6: connect_candidate (planner.cpp:62-90) and commit (178-189).
+    // Half h scans candidate k + h's in-row and reduces its (cost, position)
+    // argmin; then the whole warp lazily checks the two chosen edges in turn.
     int my_checks = 0, my_added = 0;
     {
-      int k = warp;
-      int x = 0;
-      int64_t e0 = 0, e1 = 0;
-      if (k < ccount) {
-        x = list[k];
+      double* segh = seg + 32 * h;  // half h's segment: a = [0..15], b = [16..31]
+      int k = 2 * warp;
+      int x = -1;
+      int64_t e0 = 0;
+      int len = 0;
+      if (k + h < ccount) {
+        x = list[k + h];
         e0 = __ldg(I.in_ptr + x);
-        e1 = __ldg(I.in_ptr + x + 1);
+        len = static_cast<int>(__ldg(I.in_ptr + x + 1) - e0);
       }
       while (k < ccount) {
-        const int kn = k + nw;
-        int xn = 0;
-        int64_t n0 = 0, n1 = 0;
-        if (kn < ccount) {
-          xn = list[kn];
+        const int kn = k + 2 * nw;
+        int xn = -1;
+        int64_t n0 = 0;
+        int nlen = 0;
+        if (kn + h < ccount) {
+          xn = list[kn + h];
           n0 = __ldg(I.in_ptr + xn);
-          n1 = __ldg(I.in_ptr + xn + 1);
+          nlen = static_cast<int>(__ldg(I.in_ptr + xn + 1) - n0);
         }
         // The segment's B endpoint (the candidate) is staged while the row
         // streams in; the A endpoint (the chosen parent) after the argmin.
         __syncwarp();
-        if (lane >= 16 && lane - 16 < d)
-          seg[lane] = __ldg(I.coords + static_cast<int64_t>(x) * d + (lane - 16));
+        if (x >= 0 && hl < d) segh[16 + hl] = __ldg(I.coords + static_cast<int64_t>(x) * d + hl);
         double bv = kInf;
         int bo = -1;  // position of the lane's best edge within the row
         int by = -1;
-        for (int64_t base = e0; base < e1; base += kWarp * kUnroll) {
+        const int other = __shfl_xor_sync(kFull, len, 16);
+        const int lmax = len > other ? len : other;
+        for (int off = 0; off < lmax; off += 16 * kUnroll) {
           int ys[kUnroll];
           double cs[kUnroll];
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
-            const int64_t e = base + u * kWarp + lane;
+            const int p = off + u * 16 + hl;
             ys[u] = -1;
             cs[u] = 0.0;
-            if (e < e1) {
-              ys[u] = __ldg(I.in_col + e);
-              cs[u] = __ldg(I.in_cost + e);
+            if (p < len) {
+              ys[u] = __ldg(I.in_col + e0 + p);
+              cs[u] = __ldg(I.in_cost + e0 + p);
             }
           }
 #pragma unroll
@@ -726,60 +764,68 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
                 const double c = __dadd_rn(cost_s[y], cs[u]);
                 if (c < bv) {
                   bv = c;
-                  bo = static_cast<int>(base - e0) + u * kWarp + lane;
+                  bo = off + u * 16 + hl;
                   by = y;
                 }
               }
             }
           }
         }
-        // Warp argmin of (cost, position): costs are >= 0, so their IEEE bit
-        // patterns order like the values; three REDUX.MIN steps pick the
-        // smallest cost, then the earliest position among exact ties.
-        const unsigned long long key =
-            bo >= 0 ? static_cast<unsigned long long>(__double_as_longlong(bv)) : ~0ull;
-        const uint32_t khi = static_cast<uint32_t>(key >> 32), klo = static_cast<uint32_t>(key);
-        const uint32_t mhi = __reduce_min_sync(kFull, khi);
-        const uint32_t mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xffffffffu);
-        const bool tie = khi == mhi && klo == mlo;
-        const uint32_t mbo = __reduce_min_sync(kFull, tie ? static_cast<uint32_t>(bo) : 0xffffffffu);
-        if (mhi != 0xffffffffu || mlo != 0xffffffffu) {  // else: no open in-neighbour, not checked
-          const int src = __ffs(__ballot_sync(kFull, tie && static_cast<uint32_t>(bo) == mbo)) - 1;
-          bv = __shfl_sync(kFull, bv, src);
-          by = __shfl_sync(kFull, by, src);
-          const int64_t be = e0 + mbo;
+        // Half-warp argmin of (cost, position) == the reference's strict-<
+        // first-in-list rule; every lane of the half ends with the result.
+#pragma unroll
+        for (int o = 8; o; o >>= 1) {
+          const double ov = __shfl_xor_sync(kFull, bv, o);
+          const int oo = __shfl_xor_sync(kFull, bo, o);
+          const int oy = __shfl_xor_sync(kFull, by, o);
+          if (oo >= 0 && (bo < 0 || ov < bv || (ov == bv && oo < bo))) {
+            bv = ov;
+            bo = oo;
+            by = oy;
+          }
+        }
+        // Both chosen parents' coordinates in flight together.
+        if (bo >= 0 && hl < d) segh[hl] = __ldg(I.coords + static_cast<int64_t>(by) * d + hl);
+        __syncwarp();
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          const int boc = __shfl_sync(kFull, bo, 16 * c);
+          if (boc < 0) continue;  // no open in-neighbour (or no candidate): not checked
+          const int xc = __shfl_sync(kFull, x, 16 * c);
+          const int byc = __shfl_sync(kFull, by, 16 * c);
+          const double bvc = __shfl_sync(kFull, bv, 16 * c);
+          const int64_t bec = __shfl_sync(kFull, e0, 16 * c) + boc;
+          double* sc = seg + 32 * c;
           ++my_checks;
-          const int32_t pid = I.in_path ? __ldg(I.in_path + be) : -1;
+          const int32_t pid = I.in_path ? __ldg(I.in_path + bec) : -1;
           bool ok;
           if ((D == 0 || D == 6) && I.in_tau) {  // kinodynamic: regenerated polyline (di.cuh, quad.cuh)
-            ok = kino_edge_free_warp<D>(I, bx, by, x, __ldg(I.in_tau + be), lane, seg);
+            ok = kino_edge_free_warp<D>(I, bx, byc, xc, __ldg(I.in_tau + bec), lane, sc);
           } else if (pid < 0) {  // straight edge: segment_free (planner.cpp:59)
-            if (lane < d) seg[lane] = __ldg(I.coords + static_cast<int64_t>(by) * d + lane);
-            __syncwarp();
-            ok = segment_free_staged<D>(d, bx, lane, seg);
+            ok = segment_free_staged<D>(d, bx, lane, sc);
           } else {  // cached path: polyline_free (planner.cpp:56-58)
-            ok = polyline_free_warp<D>(I, d, bx, pid, lane, seg);
+            ok = polyline_free_warp<D>(I, d, bx, pid, lane, sc);
           }
           if (ok) {
             ++my_added;
             if (lane < CS) {
-              remote<CS>(cost_s, lane)[x] = bv;
-              atomicOr(remote<CS>(newopen_w, lane) + (x >> 5), 1u << (x & 31));
+              remote<CS>(cost_s, lane)[xc] = bvc;
+              atomicOr(remote<CS>(newopen_w, lane) + (xc >> 5), 1u << (xc & 31));
             }
             if (lane == 0) {
               if constexpr (kParentSmem) {
-                remote<CS>(parent_s, 0)[x] = static_cast<uint16_t>(by);
+                remote<CS>(parent_s, 0)[xc] = static_cast<uint16_t>(byc);
               } else {
-                R.parent[x] = by;
+                R.parent[xc] = byc;
               }
-              if (R.iter_added) R.iter_added[x] = i;
+              if (R.iter_added) R.iter_added[xc] = i;
             }
           }
         }
         k = kn;
         x = xn;
         e0 = n0;
-        e1 = n1;
+        len = nlen;
       }
     }
     if (lane == 0 && (my_checks | my_added)) {
