@@ -48,8 +48,28 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int32_t kNone = 0x7fffffff;
-constexpr int kUnroll = 4;        // row chunks in flight per lane
+#ifndef GMT_UNROLL
+#define GMT_UNROLL 4
+#endif
+constexpr int kUnroll = GMT_UNROLL;  // row chunks in flight per lane
 constexpr double kSepMargin = 1e-9;  // see segment_free_staged
+#ifndef GMT_ROWS_PER_WARP
+#define GMT_ROWS_PER_WARP 2
+#endif
+constexpr int kRows = GMT_ROWS_PER_WARP;  // rows streamed concurrently per warp (P4, P5)
+constexpr int kLanesPerRow = kWarp / kRows;
+
+// Longest of the rows the lane groups of a warp are streaming.
+__device__ __forceinline__ int rows_max(int len) {
+  if constexpr (kRows == 1) {
+    return len;
+  } else if constexpr (kRows == 2) {
+    const int other = __shfl_xor_sync(0xffffffffu, len, 16);
+    return len > other ? len : other;
+  } else {
+    return static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<uint32_t>(len)));
+  }
+}
 
 struct CtaShared {
   double red_min[32];
@@ -61,6 +81,16 @@ struct CtaShared {
   unsigned long long checks_acc;  // rank 0: cluster-wide checks of this pass
   int32_t added_acc;              // rank 0: cluster-wide additions of this pass
   int32_t feasible;
+  // Loop state kept in shared memory rather than in every thread's
+  // registers (the solve is register-bound): the threshold index i, the
+  // pass number, the running check total (tid 0), per-warp check / commit
+  // counts and the traffic counters.
+  long long iter;
+  long long total_checks;
+  int32_t pass;
+  int32_t wchecks[16];
+  int32_t wadded[16];
+  unsigned long long cnt_in, cnt_out;
 };
 
 // Boxes: box b, axis k at base[b*bs + k*as].  lom/him hold lo - m and
@@ -395,7 +425,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   constexpr int kMaxWarps = WIDE ? 16 : 8;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
-  __shared__ double seg_s[kMaxWarps * 64];  // per warp: two staged segments
+  __shared__ double seg_s[kMaxWarps * 32 * kRows];  // per warp: kRows staged segments
 
   const int q = blockIdx.x / CS;
   int rank = 0;
@@ -429,10 +459,11 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  double* seg = seg_s + warp * 64;
+  double* seg = seg_s + warp * 32 * kRows;
 
-  Boxes bx;
-  bx.count = nb;
+  __shared__ Boxes bx_s;
+  Boxes bxl;
+  bxl.count = nb;
   if (obs_in_smem) {
     // Stage the boxes axis-major, with the separation bounds lo - m, hi + m.
     double* lo = reinterpret_cast<double*>(smem + L.off_obs);
@@ -447,9 +478,9 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       lom[k * nb + b] = l - kSepMargin;
       him[k * nb + b] = h + kSepMargin;
     }
-    bx.lo = lo, bx.hi = hi, bx.lom = lom, bx.him = him, bx.bs = 1, bx.as = nb;
+    bxl.lo = lo, bxl.hi = hi, bxl.lom = lom, bxl.him = him, bxl.bs = 1, bxl.as = nb;
   } else {
-    bx.lo = I.box_lo, bx.hi = I.box_hi, bx.lom = nullptr, bx.him = nullptr, bx.bs = d, bx.as = 1;
+    bxl.lo = I.box_lo, bxl.hi = I.box_hi, bxl.lom = nullptr, bxl.him = nullptr, bxl.bs = d, bxl.as = 1;
   }
 
   // make_wavefront (planner.cpp:25-35) on every replica.
@@ -480,8 +511,19 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
     sh.cand_count = 0;
     sh.checks_acc = 0ull;
     sh.added_acc = 0;
+    sh.iter = 0;
+    sh.total_checks = 0;
+    sh.pass = 0;
+    sh.cnt_in = 0ull;
+    sh.cnt_out = 0ull;
+    bx_s = bxl;
+  }
+  if (tid < 16) {
+    sh.wchecks[tid] = 0;
+    sh.wadded[tid] = 0;
   }
   __syncthreads();
+  const Boxes& bx = bx_s;  // read from shared memory where used
 
   // infeasible_input (planner.cpp:39-41, 108): empty tree.
   if (warp == 0) {
@@ -524,18 +566,17 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   cluster_barrier<CS>();  // every replica initialised before any remote access
 
   const double delta = __dmul_rn(job.lambda, job.radius);  // GmtParams::delta
-  long long i = 0;
-  int pass = 0;
   int status = 1;
   int goal = -1;
-  int gsize = 0;
-  long long total_checks = 0;
   // Traffic counters for the roofline's algorithmic bytes:
-  // per-lane counts of out-row edges (P4), in-row edges (P5) and in-edges
-  // whose source was open (the cost[y] gathers).
-  int cnt_out = 0, cnt_in = 0, cnt_open = 0;
+  // out-row edges (P4) and in-row edges (P5) are summed per row into
+  // shared memory; in-edges whose source was open (the cost[y] gathers) per
+  // lane.
+  const bool counting = R.counters != nullptr;
+  int cnt_open = 0;
 
   for (;;) {
+    long long i = sh.iter;  // written by tid 0 only, behind the pass barriers
     if (job.mode == kModeFmt) {
       // fmt_plan (planner.cpp:207-225): z = first minimum-cost open node;
       // the "group" is {z}; no thresholds.
@@ -549,10 +590,10 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         status = 1;
         break;
       }
-      gsize = 1;
       if ((goal_w[z >> 5] >> (z & 31)) & 1u) {
         status = 0;
         goal = z;
+        if (tid == 0) sh.group_count = 1;  // the final group's size
         break;
       }
       if (tid == 0) {
@@ -584,6 +625,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         while (m > __dmul_rn(static_cast<double>(i), delta)) ++i;
       }
       const double thr = __dmul_rn(static_cast<double>(i), delta);
+      if (tid == 0) sh.iter = i;  // every thread read sh.iter before block_min's barrier
 
       // P2 + P3: group bitmask/list and min-cost goal member (planner.cpp:137-149).
       double gc = kInf;
@@ -611,7 +653,6 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         }
       }
       block_argmin(gc, gv, sh, lane, warp, nw);
-      gsize = sh.group_count;
       if (gv != kNone) {  // planner.cpp:150-156
         status = 0;
         goal = gv;
@@ -619,15 +660,16 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       }
     }
 
-    // Rows are processed two at a time per warp: half-warp h (lanes 16h ..
-    // 16h+15) streams row k + h, so two rows' loads are in flight together.
-    const int h = lane >> 4, hl = lane & 15;
+    // Rows are processed kRows at a time per warp: lane group h (lanes
+    // kLanesPerRow*h ...) streams row k + h, so kRows rows' loads are in
+    // flight together.
+    const int h = lane / kLanesPerRow, hl = lane % kLanesPerRow;
 
     // P4: mark unexplored out-neighbours of the owned group members
     // (planner.cpp:159-166).
     {
       const int own = sh.own_count;
-      int k = 2 * warp;
+      int k = kRows * warp;
       int64_t e0 = 0;
       int len = 0;
       if (k + h < own) {
@@ -636,7 +678,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         len = static_cast<int>(__ldg(I.out_ptr + g + 1) - e0);
       }
       while (k < own) {
-        const int kn = k + 2 * nw;
+        const int kn = k + kRows * nw;
         int64_t n0 = 0;
         int nlen = 0;
         if (kn + h < own) {  // next rows' offsets in flight during these rows
@@ -644,21 +686,20 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
           n0 = __ldg(I.out_ptr + gn);
           nlen = static_cast<int>(__ldg(I.out_ptr + gn + 1) - n0);
         }
-        const int other = __shfl_xor_sync(kFull, len, 16);
-        const int lmax = len > other ? len : other;
-        for (int off = 0; off < lmax; off += 16 * kUnroll) {
+        const int lmax = rows_max(len);
+        if (counting && hl == 0 && len > 0) atomicAdd(&sh.cnt_out, static_cast<unsigned long long>(len));
+        for (int off = 0; off < lmax; off += kLanesPerRow * kUnroll) {
           int xs[kUnroll];
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
-            const int p = off + u * 16 + hl;
+            const int p = off + u * kLanesPerRow + hl;
             xs[u] = p < len ? __ldg(I.out_col + e0 + p) : -1;
           }
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
-            if (off + u * 16 >= lmax) break;  // warp-uniform
+            if (off + u * kLanesPerRow >= lmax) break;  // warp-uniform
             const int x = xs[u];
             const bool valid = x >= 0;
-            cnt_out += valid ? 1 : 0;
             if constexpr (CS == 1) {
               // One CTA: a shared-memory atomic per edge; explored targets
               // are masked out when the candidate list is built.
@@ -710,10 +751,9 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
     // P5 + P6: connect_candidate (planner.cpp:62-90) and commit (178-189).
     // Half h scans candidate k + h's in-row and reduces its (cost, position)
     // argmin; then the whole warp lazily checks the two chosen edges in turn.
-    int my_checks = 0, my_added = 0;
     {
-      double* segh = seg + 32 * h;  // half h's segment: a = [0..15], b = [16..31]
-      int k = 2 * warp;
+      double* segh = seg + 32 * h;  // group h's segment: a = [0..15], b = [16..31]
+      int k = kRows * warp;
       int x = -1;
       int64_t e0 = 0;
       int len = 0;
@@ -723,7 +763,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         len = static_cast<int>(__ldg(I.in_ptr + x + 1) - e0);
       }
       while (k < ccount) {
-        const int kn = k + 2 * nw;
+        const int kn = k + kRows * nw;
         int xn = -1;
         int64_t n0 = 0;
         int nlen = 0;
@@ -735,18 +775,23 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         // The segment's B endpoint (the candidate) is staged while the row
         // streams in; the A endpoint (the chosen parent) after the argmin.
         __syncwarp();
-        if (x >= 0 && hl < d) segh[16 + hl] = __ldg(I.coords + static_cast<int64_t>(x) * d + hl);
+        if constexpr (kLanesPerRow >= kMaxSolveDim) {
+          if (x >= 0 && hl < d) segh[16 + hl] = __ldg(I.coords + static_cast<int64_t>(x) * d + hl);
+        } else {
+          for (int t = hl; x >= 0 && t < d; t += kLanesPerRow)
+            segh[16 + t] = __ldg(I.coords + static_cast<int64_t>(x) * d + t);
+        }
         double bv = kInf;
         int bo = -1;  // position of the lane's best edge within the row
         int by = -1;
-        const int other = __shfl_xor_sync(kFull, len, 16);
-        const int lmax = len > other ? len : other;
-        for (int off = 0; off < lmax; off += 16 * kUnroll) {
+        const int lmax = rows_max(len);
+        if (counting && hl == 0 && len > 0) atomicAdd(&sh.cnt_in, static_cast<unsigned long long>(len));
+        for (int off = 0; off < lmax; off += kLanesPerRow * kUnroll) {
           int ys[kUnroll];
           double cs[kUnroll];
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
-            const int p = off + u * 16 + hl;
+            const int p = off + u * kLanesPerRow + hl;
             ys[u] = -1;
             cs[u] = 0.0;
             if (p < len) {
@@ -758,23 +803,22 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
           for (int u = 0; u < kUnroll; ++u) {
             const int y = ys[u];
             if (y >= 0) {
-              ++cnt_in;
               if ((open_w[y >> 5] >> (y & 31)) & 1u) {
                 ++cnt_open;
                 const double c = __dadd_rn(cost_s[y], cs[u]);
                 if (c < bv) {
                   bv = c;
-                  bo = off + u * 16 + hl;
+                  bo = off + u * kLanesPerRow + hl;
                   by = y;
                 }
               }
             }
           }
         }
-        // Half-warp argmin of (cost, position) == the reference's strict-<
-        // first-in-list rule; every lane of the half ends with the result.
+        // Group argmin of (cost, position) == the reference's strict-<
+        // first-in-list rule; every lane of the group ends with the result.
 #pragma unroll
-        for (int o = 8; o; o >>= 1) {
+        for (int o = kLanesPerRow / 2; o; o >>= 1) {
           const double ov = __shfl_xor_sync(kFull, bv, o);
           const int oo = __shfl_xor_sync(kFull, bo, o);
           const int oy = __shfl_xor_sync(kFull, by, o);
@@ -785,18 +829,24 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
           }
         }
         // Both chosen parents' coordinates in flight together.
-        if (bo >= 0 && hl < d) segh[hl] = __ldg(I.coords + static_cast<int64_t>(by) * d + hl);
+        if constexpr (kLanesPerRow >= kMaxSolveDim) {
+          if (bo >= 0 && hl < d) segh[hl] = __ldg(I.coords + static_cast<int64_t>(by) * d + hl);
+        } else {
+          for (int t = hl; bo >= 0 && t < d; t += kLanesPerRow)
+            segh[t] = __ldg(I.coords + static_cast<int64_t>(by) * d + t);
+        }
         __syncwarp();
 #pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          const int boc = __shfl_sync(kFull, bo, 16 * c);
+        for (int c = 0; c < kRows; ++c) {
+          const int src = kLanesPerRow * c;
+          const int boc = __shfl_sync(kFull, bo, src);
           if (boc < 0) continue;  // no open in-neighbour (or no candidate): not checked
-          const int xc = __shfl_sync(kFull, x, 16 * c);
-          const int byc = __shfl_sync(kFull, by, 16 * c);
-          const double bvc = __shfl_sync(kFull, bv, 16 * c);
-          const int64_t bec = __shfl_sync(kFull, e0, 16 * c) + boc;
+          const int xc = __shfl_sync(kFull, x, src);
+          const int byc = __shfl_sync(kFull, by, src);
+          const double bvc = __shfl_sync(kFull, bv, src);
+          const int64_t bec = __shfl_sync(kFull, e0, src) + boc;
           double* sc = seg + 32 * c;
-          ++my_checks;
+          if (lane == 0) ++sh.wchecks[warp];
           const int32_t pid = I.in_path ? __ldg(I.in_path + bec) : -1;
           bool ok;
           if ((D == 0 || D == 6) && I.in_tau) {  // kinodynamic: regenerated polyline (di.cuh, quad.cuh)
@@ -807,7 +857,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
             ok = polyline_free_warp<D>(I, d, bx, pid, lane, sc);
           }
           if (ok) {
-            ++my_added;
+            if (lane == 0) ++sh.wadded[warp];
             if (lane < CS) {
               remote<CS>(cost_s, lane)[xc] = bvc;
               atomicOr(remote<CS>(newopen_w, lane) + (xc >> 5), 1u << (xc & 31));
@@ -818,7 +868,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
               } else {
                 R.parent[xc] = byc;
               }
-              if (R.iter_added) R.iter_added[xc] = i;
+              if (R.iter_added) R.iter_added[xc] = sh.iter;
             }
           }
         }
@@ -828,19 +878,25 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         len = nlen;
       }
     }
-    if (lane == 0 && (my_checks | my_added)) {
-      atomicAdd(remote<CS>(&sh.checks_acc, 0), static_cast<unsigned long long>(my_checks));
-      atomicAdd(remote<CS>(&sh.added_acc, 0), my_added);
+    if (lane == 0) {
+      const int my_checks = sh.wchecks[warp], my_added = sh.wadded[warp];
+      if (my_checks | my_added) {
+        atomicAdd(remote<CS>(&sh.checks_acc, 0), static_cast<unsigned long long>(my_checks));
+        atomicAdd(remote<CS>(&sh.added_acc, 0), my_added);
+        sh.wchecks[warp] = 0;
+        sh.wadded[warp] = 0;
+      }
     }
     cluster_barrier<CS>();  // [2] commits visible in every replica
 
     if (rank == 0 && tid == 0) {  // IterationStats (planner.cpp:192-194)
       if (R.group_sizes) {
-        R.group_sizes[pass] = gsize;
-        R.nodes_added[pass] = sh.added_acc;
-        R.checks[pass] = static_cast<int64_t>(sh.checks_acc);
+        const int p = sh.pass;
+        R.group_sizes[p] = job.mode == kModeFmt ? 1 : sh.group_count;
+        R.nodes_added[p] = sh.added_acc;
+        R.checks[p] = static_cast<int64_t>(sh.checks_acc);
       }
-      total_checks += static_cast<long long>(sh.checks_acc);
+      sh.total_checks += static_cast<long long>(sh.checks_acc);
       sh.added_acc = 0;
       sh.checks_acc = 0ull;
     }
@@ -856,23 +912,21 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       sh.group_count = 0;
       sh.own_count = 0;
       sh.cand_count = 0;
+      sh.iter = i + 1;
+      sh.pass = sh.pass + 1;
     }
     __syncthreads();
-    ++i;
-    ++pass;
   }
 
-  if (R.counters) {
-    long long a = cnt_in, b = cnt_out, c = cnt_open;
-    for (int o = 16; o; o >>= 1) {
-      a += __shfl_xor_sync(kFull, a, o);
-      b += __shfl_xor_sync(kFull, b, o);
-      c += __shfl_xor_sync(kFull, c, o);
-    }
+  if (counting) {
+    long long c = cnt_open;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
     if (lane == 0) {
-      atomicAdd(reinterpret_cast<unsigned long long*>(R.counters + 0), static_cast<unsigned long long>(a));
-      atomicAdd(reinterpret_cast<unsigned long long*>(R.counters + 1), static_cast<unsigned long long>(b));
       atomicAdd(reinterpret_cast<unsigned long long*>(R.counters + 2), static_cast<unsigned long long>(c));
+    }
+    if (tid == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(R.counters + 0), sh.cnt_in);
+      atomicAdd(reinterpret_cast<unsigned long long*>(R.counters + 1), sh.cnt_out);
     }
   }
   if (rank != 0) return;
@@ -889,14 +943,15 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
     ResultScalars s;
     s.status = status;
     s.goal_node = goal;
-    s.iterations = i;
+    const int pass = sh.pass;
+    s.iterations = sh.iter;
     s.tree_size = n;
     s.reserved = 0;
     s.num_stats = pass;
-    s.total_checks = total_checks;
+    s.total_checks = sh.total_checks;
     if (status == 0) {
       if (R.group_sizes) {  // final group pushes 0/0 (planner.cpp:151-152)
-        R.group_sizes[pass] = gsize;
+        R.group_sizes[pass] = sh.group_count;
         R.nodes_added[pass] = 0;
         R.checks[pass] = 0;
       }
