@@ -56,10 +56,9 @@ constexpr double kSepMargin = 1e-9;  // see segment_free_staged
 #ifndef GMT_ROWS_PER_WARP
 #define GMT_ROWS_PER_WARP 2
 #endif
-constexpr int kRows = GMT_ROWS_PER_WARP;  // rows streamed concurrently per warp (P4, P5)
-constexpr int kLanesPerRow = kWarp / kRows;
 
-// Longest of the rows the lane groups of a warp are streaming.
+// Longest of the rows the kRows lane groups of a warp are streaming.
+template <int kRows>
 __device__ __forceinline__ int rows_max(int len) {
   if constexpr (kRows == 1) {
     return len;
@@ -425,6 +424,11 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   constexpr int kMaxWarps = WIDE ? 16 : 8;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
+  // Rows streamed concurrently per warp in P4/P5: two for batched
+  // single-CTA solves (latency hiding), one for clusters (few candidates per
+  // warp; the pass critical path matters).
+  constexpr int kRows = CS == 1 ? GMT_ROWS_PER_WARP : 1;
+  constexpr int kLanesPerRow = kWarp / kRows;
   __shared__ double seg_s[kMaxWarps * 32 * kRows];  // per warp: kRows staged segments
 
   const int q = blockIdx.x / CS;
@@ -686,7 +690,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
           n0 = __ldg(I.out_ptr + gn);
           nlen = static_cast<int>(__ldg(I.out_ptr + gn + 1) - n0);
         }
-        const int lmax = rows_max(len);
+        const int lmax = rows_max<kRows>(len);
         if (counting && hl == 0 && len > 0) atomicAdd(&sh.cnt_out, static_cast<unsigned long long>(len));
         for (int off = 0; off < lmax; off += kLanesPerRow * kUnroll) {
           int xs[kUnroll];
@@ -784,7 +788,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         double bv = kInf;
         int bo = -1;  // position of the lane's best edge within the row
         int by = -1;
-        const int lmax = rows_max(len);
+        const int lmax = rows_max<kRows>(len);
         if (counting && hl == 0 && len > 0) atomicAdd(&sh.cnt_in, static_cast<unsigned long long>(len));
         for (int off = 0; off < lmax; off += kLanesPerRow * kUnroll) {
           int ys[kUnroll];
@@ -817,15 +821,36 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         }
         // Group argmin of (cost, position) == the reference's strict-<
         // first-in-list rule; every lane of the group ends with the result.
+        if constexpr (kRows == 1) {
+          // Whole warp: costs are >= 0, so their IEEE bit patterns order
+          // like the values; three REDUX.MIN steps pick the smallest cost,
+          // then the earliest position among exact ties.
+          const unsigned long long key =
+              bo >= 0 ? static_cast<unsigned long long>(__double_as_longlong(bv)) : ~0ull;
+          const uint32_t khi = static_cast<uint32_t>(key >> 32), klo = static_cast<uint32_t>(key);
+          const uint32_t mhi = __reduce_min_sync(kFull, khi);
+          const uint32_t mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xffffffffu);
+          const bool tie = khi == mhi && klo == mlo;
+          const uint32_t mbo = __reduce_min_sync(kFull, tie ? static_cast<uint32_t>(bo) : 0xffffffffu);
+          if (mhi != 0xffffffffu || mlo != 0xffffffffu) {
+            const int src = __ffs(__ballot_sync(kFull, tie && static_cast<uint32_t>(bo) == mbo)) - 1;
+            bv = __shfl_sync(kFull, bv, src);
+            by = __shfl_sync(kFull, by, src);
+            bo = static_cast<int>(mbo);
+          } else {
+            bo = -1;
+          }
+        } else {
 #pragma unroll
-        for (int o = kLanesPerRow / 2; o; o >>= 1) {
-          const double ov = __shfl_xor_sync(kFull, bv, o);
-          const int oo = __shfl_xor_sync(kFull, bo, o);
-          const int oy = __shfl_xor_sync(kFull, by, o);
-          if (oo >= 0 && (bo < 0 || ov < bv || (ov == bv && oo < bo))) {
-            bv = ov;
-            bo = oo;
-            by = oy;
+          for (int o = kLanesPerRow / 2; o; o >>= 1) {
+            const double ov = __shfl_xor_sync(kFull, bv, o);
+            const int oo = __shfl_xor_sync(kFull, bo, o);
+            const int oy = __shfl_xor_sync(kFull, by, o);
+            if (oo >= 0 && (bo < 0 || ov < bv || (ov == bv && oo < bo))) {
+              bv = ov;
+              bo = oo;
+              by = oy;
+            }
           }
         }
         // Both chosen parents' coordinates in flight together.
@@ -839,22 +864,28 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
 #pragma unroll 1
         for (int c = 0; c < kRows; ++c) {
           const int src = kLanesPerRow * c;
-          const int boc = __shfl_sync(kFull, bo, src);
+          // (one row per warp: the values are already warp-uniform)
+          const int boc = kRows == 1 ? bo : __shfl_sync(kFull, bo, src);
           if (boc < 0) continue;  // no open in-neighbour (or no candidate): not checked
-          const int xc = __shfl_sync(kFull, x, src);
-          const int byc = __shfl_sync(kFull, by, src);
-          const double bvc = __shfl_sync(kFull, bv, src);
-          const int64_t bec = __shfl_sync(kFull, e0, src) + boc;
+          const int xc = kRows == 1 ? x : __shfl_sync(kFull, x, src);
+          const int byc = kRows == 1 ? by : __shfl_sync(kFull, by, src);
+          const double bvc = kRows == 1 ? bv : __shfl_sync(kFull, bv, src);
+          const int64_t bec = (kRows == 1 ? e0 : __shfl_sync(kFull, e0, src)) + boc;
           double* sc = seg + 32 * c;
           if (lane == 0) ++sh.wchecks[warp];
           const int32_t pid = I.in_path ? __ldg(I.in_path + bec) : -1;
+          auto edge_free = [&](const Boxes& B) -> bool {
+            if ((D == 0 || D == 6) && I.in_tau)  // kinodynamic: regenerated polyline (di.cuh, quad.cuh)
+              return kino_edge_free_warp<D>(I, B, byc, xc, __ldg(I.in_tau + bec), lane, sc);
+            if (pid < 0) return segment_free_staged<D>(d, B, lane, sc);  // segment_free (planner.cpp:59)
+            return polyline_free_warp<D>(I, d, B, pid, lane, sc);       // polyline_free (planner.cpp:56-58)
+          };
           bool ok;
-          if ((D == 0 || D == 6) && I.in_tau) {  // kinodynamic: regenerated polyline (di.cuh, quad.cuh)
-            ok = kino_edge_free_warp<D>(I, bx, byc, xc, __ldg(I.in_tau + bec), lane, sc);
-          } else if (pid < 0) {  // straight edge: segment_free (planner.cpp:59)
-            ok = segment_free_staged<D>(d, bx, lane, sc);
-          } else {  // cached path: polyline_free (planner.cpp:56-58)
-            ok = polyline_free_warp<D>(I, d, bx, pid, lane, sc);
+          if constexpr (WIDE) {  // registers to spare: the descriptor off the check's critical path
+            const Boxes breg = bx_s;
+            ok = edge_free(breg);
+          } else {
+            ok = edge_free(bx_s);
           }
           if (ok) {
             if (lane == 0) ++sh.wadded[warp];
