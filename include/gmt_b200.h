@@ -40,7 +40,8 @@ typedef enum gmt_error {
   GMT_E_GOAL_BLOCKED = 3,         /* gmt::GoalBlockedError         (errors.hpp:19-21) */
   GMT_E_CUDA = 4,                 /* CUDA runtime failure (no reference analogue)     */
   GMT_E_NO_DEVICE = 5,            /* no usable sm_100 device: the ABI never falls back */
-  GMT_E_INTERNAL = 6
+  GMT_E_INTERNAL = 6,
+  GMT_E_IO = 7                    /* graph-cache file I/O (the reference returns false) */
 } gmt_error;
 
 /* PlanStatus, same order as planner.hpp:14. */
@@ -293,6 +294,20 @@ int gmt_build_quad_graph(gmt_ctx* ctx, const double* coords, int32_t n,
                          int64_t* in_ptr, int32_t* in_col, double* in_cost, int32_t* in_path,
                          double* path_pts);
 
+/* ---- GMTG v1 graph cache (graph.hpp:56-65, graph.cpp:190-343) --------- */
+/* problem_key (problem.cpp:281-303) of a Euclidean problem: the cache key
+ * the reference's build_instance uses.                                   */
+int gmt_problem_key(const gmt_problem* problem, uint64_t* key_out);
+/* save_graph_cache (graph.cpp:240-276) of a host CSR (out-rows sorted by
+ * target): little-endian GMTG v1, written to file.tmp and renamed.       */
+int gmt_graph_cache_save(const char* file, uint64_t key, int32_t n, double radius,
+                         const int64_t* row_ptr, const int32_t* col, const double* cost);
+/* load_graph_cache (graph.cpp:278-343), Euclidean: *hit = 0 on a missing
+ * file, any header mismatch (key, n, radius, model) or corruption.  Two-call
+ * pattern: NULL row_ptr returns *hit and *num_edges only.                */
+int gmt_graph_cache_load(const char* file, uint64_t key, int32_t n, double radius, int32_t* hit,
+                         int64_t* num_edges, int64_t* row_ptr, int32_t* col, double* cost);
+
 /* ---- device-resident instances (ProblemInstance, problem.hpp:52-57) --- */
 /* Upload host samples + graph + scene.  goal_count is samples.goal_indices
  * .size() (only its emptiness matters, planner.cpp:39-41).               */
@@ -300,6 +315,14 @@ int gmt_instance_upload(gmt_ctx* ctx, const gmt_scene* scene, const double* coor
                         int32_t goal_count, const gmt_graph_view* graph, gmt_instance** out);
 /* build_instance (problem.cpp:336-363) entirely on the device. */
 int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* problem, gmt_instance** out);
+/* build_instance(problem, workers, cache_file) (problem.cpp:336-363),
+ * Euclidean: on a cache hit the graph comes from the file (uploaded), else
+ * it is built on the device and saved (a failed save is ignored, like the
+ * reference's).  *cache_hit (may be NULL) reports which.                   */
+int gmt_instance_build_cached(gmt_ctx* ctx, const gmt_problem* problem, const char* cache_file,
+                              gmt_instance** out, int32_t* cache_hit);
+/* save_graph_cache of a device instance's graph (Euclidean). */
+int gmt_instance_cache_save(gmt_ctx* ctx, const gmt_instance* inst, const char* file, uint64_t key);
 int gmt_instance_info(const gmt_instance* inst, int32_t* n, int32_t* dim, int32_t* init_index,
                       double* radius, int64_t* num_edges, int32_t* goal_count);
 /* Copy samples / goal indices / graph of an instance back to the host

@@ -15,7 +15,9 @@
 //   unit_ball_volume      graph.hpp:22
 //   connection_radius     graph.hpp:25
 //   build_neighbor_graph  graph.hpp:53-54     (Euclidean model)
-//   build_instance        problem.hpp:59-60   (Euclidean model, no cache file)
+//   build_instance        problem.hpp:59-60   (Euclidean model, GMTG v1 cache file)
+//   problem_key           problem.hpp:43
+//   save_graph_cache / load_graph_cache   graph.hpp:60-65 (Euclidean)
 // Exceptions: InvalidInputError / InfeasibleSamplingError / GoalBlockedError
 // (errors.hpp:9-21); CUDA failures throw gmt_b200::CudaError.  There is no
 // CPU fallback: without a B200 every call throws NoDeviceError.
@@ -569,11 +571,94 @@ struct ProblemInstance {
   NeighborGraph graph;
 };
 
+namespace detail {
+// A gmt_problem view of a ProblemFile (arrays owned by the FlatScene).
+struct FlatProblem {
+  FlatScene scene;
+  gmt_problem p{};
+  explicit FlatProblem(const ProblemFile& f) : scene(f.obstacles, f.goal) {
+    p.scene = scene.s;
+    p.init = f.init.coords.data();
+    p.init_has_heading = f.init.heading ? 1 : 0;
+    p.init_heading = f.init.heading ? *f.init.heading : 0.0;
+    p.n = f.n;
+    p.lambda = f.lambda;
+    p.eta = f.eta;
+    p.radius_override = f.radius_override ? *f.radius_override : 0.0;
+    p.sampling.kind = f.sampling.kind == SampleSource::Kind::uniform ? GMT_SAMPLE_UNIFORM : GMT_SAMPLE_HALTON;
+    p.sampling.with_heading = f.sampling.with_heading ? 1 : 0;
+    p.sampling.start_index = f.sampling.start_index;
+    p.sampling.seed = f.sampling.seed;
+    p.steering = GMT_STEER_EUCLIDEAN;
+  }
+};
+
+inline NeighborGraph graph_from_csr(int n, double radius, const SteeringModel& m,
+                                    const std::vector<int64_t>& ptr, const std::vector<int32_t>& col,
+                                    const std::vector<double>& cost) {
+  NeighborGraph g;
+  g.n = n;
+  g.radius = radius;
+  g.model = m;
+  g.out.resize(n);
+  g.in.resize(n);
+  for (int u = 0; u < n; ++u)
+    for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) g.out[u].push_back({col[e], cost[e], -1});
+  for (int u = 0; u < n; ++u)  // sequential in-list merge, graph.cpp:184-186
+    for (const auto& e : g.out[u]) g.in[e.other].push_back({u, e.cost, e.path_id});
+  return g;
+}
+}  // namespace detail
+
+// problem_key (problem.cpp:281-303), Euclidean problems.
+inline std::uint64_t problem_key(const ProblemFile& p) {
+  if (p.steering.kind != SteeringModel::Kind::euclidean)
+    throw InvalidInputError("the graph cache covers the Euclidean steering model only");
+  detail::FlatProblem fp(p);
+  std::uint64_t k = 0;
+  check(gmt_problem_key(&fp.p, &k));
+  return k;
+}
+
+// save_graph_cache (graph.cpp:240-276): false when the file cannot be written.
+inline bool save_graph_cache(const NeighborGraph& g, const std::string& file, std::uint64_t key) {
+  if (g.model.kind != SteeringModel::Kind::euclidean)
+    throw InvalidInputError("the graph cache covers the Euclidean steering model only");
+  std::vector<int64_t> ptr(g.n + 1, 0);
+  std::vector<int32_t> col;
+  std::vector<double> cost;
+  for (int u = 0; u < g.n; ++u) {
+    for (const auto& e : g.out[u]) {
+      col.push_back(e.other);
+      cost.push_back(e.cost);
+    }
+    ptr[u + 1] = static_cast<int64_t>(col.size());
+  }
+  return gmt_graph_cache_save(file.c_str(), key, g.n, g.radius, ptr.data(), col.data(), cost.data()) ==
+         GMT_OK;
+}
+
+// load_graph_cache (graph.cpp:278-343): empty on any mismatch or corruption.
+inline std::optional<NeighborGraph> load_graph_cache(const std::string& file, std::uint64_t key,
+                                                     const std::vector<State>& states,
+                                                     const SteeringModel& m, double radius) {
+  if (m.kind != SteeringModel::Kind::euclidean) return std::nullopt;
+  const int n = static_cast<int>(states.size());
+  int32_t hit = 0;
+  int64_t E = 0;
+  check(gmt_graph_cache_load(file.c_str(), key, n, radius, &hit, &E, nullptr, nullptr, nullptr));
+  if (!hit) return std::nullopt;
+  std::vector<int64_t> ptr(n + 1);
+  std::vector<int32_t> col(E);
+  std::vector<double> cost(E);
+  check(gmt_graph_cache_load(file.c_str(), key, n, radius, &hit, &E, ptr.data(), col.data(), cost.data()));
+  return detail::graph_from_csr(n, radius, m, ptr, col, cost);
+}
+
 inline ProblemInstance build_instance(const ProblemFile& p, int workers = 1,
                                       const std::string& cache_file = "",
                                       Context& ctx = Context::thread_default()) {
   (void)workers;
-  if (!cache_file.empty()) throw InvalidInputError("graph cache files are not supported yet");
   if (p.steering.kind != SteeringModel::Kind::euclidean)
     throw InvalidInputError("dubins_airplane problems are not supported on the device yet");
   // Same call sequence as problem.cpp:336-363, every step on the device.
@@ -591,6 +676,18 @@ inline ProblemInstance build_instance(const ProblemFile& p, int workers = 1,
     rp.eta = p.eta;
     rp.mu_free = 1.0;  // free_measure_upper_bound (space.cpp:101-104)
     inst.radius = connection_radius(rp);
+  }
+  // Graph cache (problem.cpp:353-362): load on a key / shape match, else
+  // build and save (a failed save is ignored, as in the reference).
+  if (!cache_file.empty()) {
+    const std::uint64_t key = problem_key(p);
+    if (auto cached = load_graph_cache(cache_file, key, inst.samples.states, p.steering, inst.radius)) {
+      inst.graph = std::move(*cached);
+      return inst;
+    }
+    inst.graph = build_neighbor_graph(inst.samples.states, p.steering, inst.radius, workers, ctx);
+    save_graph_cache(inst.graph, cache_file, key);
+    return inst;
   }
   inst.graph = build_neighbor_graph(inst.samples.states, p.steering, inst.radius, workers, ctx);
   return inst;

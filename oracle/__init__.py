@@ -343,6 +343,15 @@ class RefLib(_Lib):
         L.ref_instance_info.argtypes = [C.c_void_p, _i32p, _i32p, _dp, _i64p, _i32p]
         L.ref_instance_download.restype = C.c_int
         L.ref_instance_download.argtypes = [C.c_void_p, _dp, _i32p, _i64p, _i32p, _dp]
+        L.ref_problem_key.restype = C.c_int
+        L.ref_problem_key.argtypes = [_P(abi.Problem), _P(C.c_uint64)]
+        L.ref_instance_build_cached.restype = C.c_int
+        L.ref_instance_build_cached.argtypes = [_P(abi.Problem), C.c_char_p, _P(C.c_void_p)]
+        L.ref_save_graph_cache.restype = C.c_int
+        L.ref_save_graph_cache.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, _i32p]
+        L.ref_load_graph_cache.restype = C.c_int
+        L.ref_load_graph_cache.argtypes = [C.c_char_p, C.c_uint64, _dp, C.c_int32, C.c_int32,
+                                           C.c_double, _i32p, _i64p, _i64p, _i32p, _dp]
         L.ref_instance_plan.restype = C.c_int
         L.ref_instance_plan.argtypes = [C.c_void_p, C.c_double, C.c_int32, _P(abi.PlanOut)]
         L.ref_plan_many.restype = C.c_int
@@ -386,6 +395,39 @@ class RefLib(_Lib):
         p = spec.flat()
         self._check(self.lib.ref_instance_build(C.byref(p), workers, C.byref(h)))
         return RefInstance(self, h)
+
+    # ---- graph cache (graph.cpp:190-343) and problem_key (problem.cpp:281-303)
+    def problem_key(self, spec) -> int:
+        k = C.c_uint64()
+        p = spec.flat()
+        self._check(self.lib.ref_problem_key(C.byref(p), C.byref(k)))
+        return k.value
+
+    def instance_build_cached(self, spec, cache_file: str) -> "RefInstance":
+        h = C.c_void_p()
+        p = spec.flat()
+        self._check(self.lib.ref_instance_build_cached(C.byref(p), os.fsencode(cache_file), C.byref(h)))
+        return RefInstance(self, h)
+
+    def load_graph_cache(self, file: str, key: int, coords, radius: float):
+        """-> (out_ptr, out_col, out_cost) or None on a miss."""
+        coords = abi.f64(coords)
+        n, dim = coords.shape
+        hit, ne = C.c_int32(), C.c_int64()
+        z = lambda t: abi.ptr(None, t)  # noqa: E731
+        self._check(self.lib.ref_load_graph_cache(os.fsencode(file), key, abi.ptr(coords, C.c_double),
+                                                  n, dim, radius, C.byref(hit), C.byref(ne),
+                                                  z(C.c_int64), z(C.c_int32), z(C.c_double)))
+        if not hit.value:
+            return None
+        E = ne.value
+        ptr = np.zeros(n + 1, np.int64)
+        col, cost = np.zeros(max(E, 1), np.int32), np.zeros(max(E, 1))
+        self._check(self.lib.ref_load_graph_cache(os.fsencode(file), key, abi.ptr(coords, C.c_double),
+                                                  n, dim, radius, C.byref(hit), C.byref(ne),
+                                                  abi.ptr(ptr, C.c_int64), abi.ptr(col, C.c_int32),
+                                                  abi.ptr(cost, C.c_double)))
+        return ptr, col[:E], cost[:E]
 
     def instance_build_many(self, specs, threads: int):
         arr = (abi.Problem * len(specs))(*[s.flat() for s in specs])
@@ -476,6 +518,11 @@ class RefInstance:
     def __init__(self, lib: RefLib, h):
         self.lib = lib
         self.h = h
+
+    def save_cache(self, file: str, key: int) -> bool:
+        ok = C.c_int32()
+        self.lib._check(self.lib.lib.ref_save_graph_cache(self.h, os.fsencode(file), key, C.byref(ok)))
+        return bool(ok.value)
 
     def info(self):
         n, ii, gc = C.c_int32(), C.c_int32(), C.c_int32()

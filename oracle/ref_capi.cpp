@@ -387,6 +387,60 @@ int ref_instance_download(void* h, double* coords, int32_t* goal_idx, int64_t* o
   });
 }
 
+// ---- graph cache (GMTG v1, graph.cpp:190-343) and problem_key (problem.cpp:281-303)
+int ref_problem_key(const gmt_problem* p, uint64_t* out) {
+  return guard([&] { *out = problem_key(to_problem(p)); });
+}
+
+// build_instance with a cache file (problem.cpp:354-362): loads on a key /
+// shape match, else builds and saves.
+int ref_instance_build_cached(const gmt_problem* p, const char* cache_file, void** out) {
+  return guard([&] {
+    auto* ri = new RefInstance;
+    try {
+      ri->problem = to_problem(p);
+      ri->inst = build_instance(ri->problem, 1, cache_file);
+    } catch (...) {
+      delete ri;
+      throw;
+    }
+    *out = ri;
+  });
+}
+
+int ref_save_graph_cache(void* h, const char* file, uint64_t key, int32_t* ok) {
+  return guard([&] {
+    auto* ri = static_cast<RefInstance*>(h);
+    *ok = save_graph_cache(ri->inst.graph, file, key) ? 1 : 0;
+  });
+}
+
+// load_graph_cache for a Euclidean graph over host states; *hit = 0 on any
+// mismatch.  Two-call pattern like ref_build_neighbor_graph.
+int ref_load_graph_cache(const char* file, uint64_t key, const double* coords, int32_t n, int32_t dim,
+                         double radius, int32_t* hit, int64_t* num_edges, int64_t* out_ptr,
+                         int32_t* out_col, double* out_cost) {
+  return guard([&] {
+    std::vector<State> st(n);
+    for (int i = 0; i < n; ++i) st[i].coords.assign(coords + static_cast<size_t>(i) * dim, coords + static_cast<size_t>(i + 1) * dim);
+    auto g = load_graph_cache(file, key, st, SteeringModel{}, radius);
+    *hit = g ? 1 : 0;
+    *num_edges = g ? static_cast<int64_t>(g->edge_count()) : 0;
+    if (g && out_ptr) {
+      int64_t e = 0;
+      for (int u = 0; u < g->n; ++u) {
+        out_ptr[u] = e;
+        for (const auto& ed : g->out[u]) {
+          out_col[e] = ed.other;
+          out_cost[e] = ed.cost;
+          ++e;
+        }
+      }
+      out_ptr[g->n] = e;
+    }
+  });
+}
+
 int ref_instance_plan(void* h, double lambda, int32_t workers, gmt_plan_out* out) {
   return guard([&] {
     auto* ri = static_cast<RefInstance*>(h);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -42,6 +43,13 @@ int build_di_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const gmt_di
                        Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in);
 int build_quad_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const gmt_quad_params* p,
                          double radius, Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in);
+
+// GMTG v1 graph cache (cache.cu).
+int problem_key_of(const gmt_problem* p, uint64_t* out);
+int cache_write(const char* file, uint64_t key, int32_t n, double radius, const int64_t* ptr,
+                const int32_t* col, const double* cost);
+int cache_read(const char* file, uint64_t key, int32_t n, double radius, std::vector<int64_t>& ptr,
+               std::vector<int32_t>& col, std::vector<double>& cost, bool* hit);
 
 // append_init on device samples (sampling.cpp:144-154).
 int append_init_dev(gmt_ctx* ctx, int dim, DevSamples* s, const double* init, int has_heading,

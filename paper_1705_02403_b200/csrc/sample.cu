@@ -603,8 +603,10 @@ extern "C" int gmt_append_init(gmt_ctx* ctx, int32_t dim, double* coords, double
 
 // build_instance (problem.cpp:336-363): sample -> append init -> radius ->
 // graph, every step on the device; the instance keeps its goal list.
-extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instance** out) {
+static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_file,
+                          gmt_instance** out, int32_t* cache_hit) {
   *out = nullptr;
+  if (cache_hit) *cache_hit = 0;
   const gmt_scene* scene = &p->scene;
   const int d = scene->dim, nb = scene->num_boxes;
   int rc = validate_scene(scene);
@@ -645,7 +647,48 @@ extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instan
   int32_t* col = nullptr;
   double* cost = nullptr;
   DiRows dout, din;
-  if (di) {
+  // Graph cache (problem.cpp:354-360): a key / shape match supplies the graph.
+  bool hit = false;
+  uint64_t key = 0;
+  if (cache_file) {
+    if (di) {
+      samples.release();
+      return set_error(GMT_E_INVALID_INPUT, "the graph cache covers the Euclidean steering model only");
+    }
+    std::vector<int64_t> hp;
+    std::vector<int32_t> hc;
+    std::vector<double> hw;
+    rc = problem_key_of(p, &key);
+    if (rc == GMT_OK) rc = cache_read(cache_file, key, S.n, radius, hp, hc, hw, &hit);
+    if (rc == GMT_OK && hit) {
+      E = static_cast<int64_t>(hc.size());
+      const size_t o_col = align16(sizeof(int64_t) * (S.n + 1));
+      const size_t o_cost = o_col + align16(sizeof(int32_t) * static_cast<size_t>(E));
+      rc = g.reserve(o_cost + sizeof(double) * static_cast<size_t>(E) + 16);
+      if (rc == GMT_OK) {
+        char* b = static_cast<char*>(g.ptr);
+        rp = reinterpret_cast<int64_t*>(b);
+        col = reinterpret_cast<int32_t*>(b + o_col);
+        cost = reinterpret_cast<double*>(b + o_cost);
+        cudaStream_t s0 = ctx->stream;
+        cudaError_t e = cudaMemcpyAsync(rp, hp.data(), sizeof(int64_t) * hp.size(), cudaMemcpyHostToDevice, s0);
+        if (e == cudaSuccess && E)
+          e = cudaMemcpyAsync(col, hc.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, s0);
+        if (e == cudaSuccess && E)
+          e = cudaMemcpyAsync(cost, hw.data(), sizeof(double) * E, cudaMemcpyHostToDevice, s0);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s0);
+        if (e != cudaSuccess) rc = cuda_error(e, "graph cache upload");
+      }
+    }
+    if (rc) {
+      samples.release();
+      g.release();
+      return rc;
+    }
+  }
+  if (hit) {
+    // graph supplied by the cache file
+  } else if (di) {
     if (d != (quad ? kQuadDim : kDiDim)) {
       samples.release();
       return set_error(GMT_E_INVALID_INPUT, quad ? "the quadrotor needs dimension 12"
@@ -760,6 +803,21 @@ extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instan
     delete inst;
     return rc;
   }
+  if (cache_file && !hit) {
+    // save_graph_cache's result is ignored by build_instance (problem.cpp:361).
+    if (gmt_instance_cache_save(ctx, inst, cache_file, key) != GMT_OK) g_last_error.clear();
+  }
+  if (cache_hit) *cache_hit = hit ? 1 : 0;
   *out = inst;
   return GMT_OK;
+}
+
+extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instance** out) {
+  return instance_build(ctx, p, nullptr, out, nullptr);
+}
+
+extern "C" int gmt_instance_build_cached(gmt_ctx* ctx, const gmt_problem* p, const char* cache_file,
+                                         gmt_instance** out, int32_t* cache_hit) {
+  if (!cache_file) return set_error(GMT_E_INVALID_INPUT, "gmt_instance_build_cached: null cache file");
+  return instance_build(ctx, p, cache_file, out, cache_hit);
 }

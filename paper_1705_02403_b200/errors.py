@@ -28,6 +28,7 @@ _CODES = {
     3: GoalBlockedError,
     4: CudaError,
     5: NoDeviceError,
+    7: OSError,
 }
 
 

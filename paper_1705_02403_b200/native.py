@@ -52,6 +52,13 @@ SIGNATURES = [
                                        _dp]),
     ("gmt_build_di_graph", C.c_int, [_vp, _dp, C.c_int32, _P(abi.DiParams), C.c_double, _i64p,
                                      _i64p, _i32p, _dp, _dp, _i64p, _i32p, _dp, _i32p, _dp]),
+    ("gmt_problem_key", C.c_int, [_P(abi.Problem), _P(C.c_uint64)]),
+    ("gmt_graph_cache_save", C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, C.c_double, _i64p, _i32p,
+                                       _dp]),
+    ("gmt_graph_cache_load", C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, C.c_double, _i32p, _i64p,
+                                       _i64p, _i32p, _dp]),
+    ("gmt_instance_build_cached", C.c_int, [_vp, _P(abi.Problem), C.c_char_p, _P(_vp), _i32p]),
+    ("gmt_instance_cache_save", C.c_int, [_vp, _vp, C.c_char_p, C.c_uint64]),
     ("gmt_instance_upload", C.c_int, [_vp, _P(abi.Scene), _dp, C.c_int32, C.c_int32,
                                       _P(abi.GraphView), _P(_vp)]),
     ("gmt_instance_build", C.c_int, [_vp, _P(abi.Problem), _P(_vp)]),
@@ -123,6 +130,10 @@ class Instance:
                                       C.byref(ne), C.byref(gc)))
         self.n, self.dim, self.init_index = n.value, d.value, ii.value
         self.radius, self.num_edges, self.goal_count = r.value, ne.value, gc.value
+
+    def cache_save(self, file: str, key: int) -> None:
+        """save_graph_cache (graph.cpp:240-276) of this instance's graph."""
+        check(lib().gmt_instance_cache_save(self.ctx.h, self.h, os.fsencode(file), key))
 
     def download(self, goal: bool = True):
         """-> (coords [n, dim], goal_idx, Graph)"""
@@ -335,6 +346,16 @@ class Context:
         check(lib().gmt_instance_build(self.h, C.byref(p), C.byref(h)))
         return Instance(self, h, spec)
 
+    def build_instance_cached(self, spec, cache_file: str):
+        """build_instance(p, workers, cache_file) (problem.cpp:336-363) ->
+        (Instance, cache_hit)."""
+        h = C.c_void_p()
+        hit = C.c_int32()
+        p = spec.flat()
+        check(lib().gmt_instance_build_cached(self.h, C.byref(p), os.fsencode(cache_file), C.byref(h),
+                                              C.byref(hit)))
+        return Instance(self, h, spec), bool(hit.value)
+
     def upload(self, spec, coords, goal_count: int, graph: Graph) -> Instance:
         coords = abi.f64(coords)
         h = C.c_void_p()
@@ -494,3 +515,38 @@ def plan_batch_host(ctx: Context, pb: PackedBatch, lam: float = 1.0):
                                     opt(pb.tree_cost, C.c_double), opt(pb.parent, C.c_int32),
                                     opt(pb.iteration_added, C.c_int64)))
     return pb.summaries
+
+
+# ---- GMTG v1 graph cache (graph.cpp:190-343); host-only, no device needed ----
+def problem_key(spec) -> int:
+    """problem_key (problem.cpp:281-303) of a Euclidean problem."""
+    k = C.c_uint64()
+    p = spec.flat()
+    check(lib().gmt_problem_key(C.byref(p), C.byref(k)))
+    return k.value
+
+
+def graph_cache_save(file: str, key: int, graph: Graph) -> None:
+    """save_graph_cache (graph.cpp:240-276) of a host CSR graph."""
+    check(lib().gmt_graph_cache_save(os.fsencode(file), key, graph.n, graph.radius,
+                                     abi.ptr(graph.out_ptr, C.c_int64),
+                                     abi.ptr(graph.out_col, C.c_int32),
+                                     abi.ptr(graph.out_cost, C.c_double)))
+
+
+def graph_cache_load(file: str, key: int, n: int, radius: float, dim: int = 0):
+    """load_graph_cache (graph.cpp:278-343): the Graph, or None on a miss."""
+    hit, ne = C.c_int32(), C.c_int64()
+    z = lambda t: abi.ptr(None, t)  # noqa: E731
+    check(lib().gmt_graph_cache_load(os.fsencode(file), key, n, radius, C.byref(hit), C.byref(ne),
+                                     z(C.c_int64), z(C.c_int32), z(C.c_double)))
+    if not hit.value:
+        return None
+    E = ne.value
+    ptr = np.zeros(n + 1, np.int64)
+    col, cost = np.zeros(max(E, 1), np.int32), np.zeros(max(E, 1))
+    check(lib().gmt_graph_cache_load(os.fsencode(file), key, n, radius, C.byref(hit), C.byref(ne),
+                                     abi.ptr(ptr, C.c_int64), abi.ptr(col, C.c_int32),
+                                     abi.ptr(cost, C.c_double)))
+    return Graph(n, radius, ptr, col[:E], cost[:E], dim=dim)
+

@@ -289,7 +289,36 @@ static void c1_known_answer() {
   CHECK(same);
 }
 
+// build_instance with a cache file (problem.cpp:353-362): miss -> build +
+// save, hit -> the same graph; load_graph_cache rejects a different key.
+static void graph_cache_roundtrip() {
+  ProblemFile p;
+  p.dimension = 2;
+  p.obstacles.dim = 2;
+  p.obstacles.boxes = {Aabb{{0.20, 0.00}, {0.40, 0.60}}, Aabb{{0.45, 0.40}, {0.65, 1.00}}};
+  p.init = State{{0.05, 0.30}, std::nullopt};
+  p.goal = goal_box({0.92, 0.25}, {0.99, 0.40});
+  p.n = 600;
+  const std::string file = "/tmp/gmt_b200_shim_cache.gmtg";
+  std::remove(file.c_str());
+  ProblemInstance a = build_instance(p, 1, file);
+  ProblemInstance b = build_instance(p, 1, file);
+  CHECK(a.graph.edge_count() == b.graph.edge_count());
+  bool same = a.graph.n == b.graph.n;
+  for (int u = 0; same && u < a.graph.n; ++u) {
+    same = a.graph.out[u].size() == b.graph.out[u].size();
+    for (std::size_t j = 0; same && j < a.graph.out[u].size(); ++j)
+      same = a.graph.out[u][j].other == b.graph.out[u][j].other && a.graph.out[u][j].cost == b.graph.out[u][j].cost;
+  }
+  CHECK(same);
+  const std::uint64_t key = problem_key(p);
+  CHECK(load_graph_cache(file, key, a.samples.states, p.steering, a.radius).has_value());
+  CHECK(!load_graph_cache(file, key + 1, a.samples.states, p.steering, a.radius).has_value());
+  std::remove(file.c_str());
+}
+
 int main() {
+  graph_cache_roundtrip();
   open_field();
   init_in_goal();
   infeasible_and_sealed();

@@ -201,3 +201,27 @@ def test_golden_plans_end_to_end(ctx):
         f = ctx.fmt_plan(inst)
         assert np.float64(f.cost).tobytes().hex() == rec["plans"]["fmt"]["cost"]
         assert sha(f.tree_cost) == rec["plans"]["fmt"]["cost_sha"]
+
+
+@pytest.mark.parametrize("name,n", [("rectangles_2d", 2000), ("maze_3d", 1500)])
+def test_build_instance_with_graph_cache(tmp_path, ctx, ref, name, n):
+    """build_instance(p, workers, cache_file) (problem.cpp:336-363): the
+    first device build misses, builds on the GPU and writes exactly the file
+    the reference writes; the second hits and plans identically; a cache
+    file written by the reference seeds a device instance."""
+    from paper_1705_02403_b200 import native
+    spec = scene(name, n)
+    ours, theirs = str(tmp_path / "ours.gmtg"), str(tmp_path / "theirs.gmtg")
+    a, hit_a = ctx.build_instance_cached(spec, ours)
+    assert not hit_a
+    ri = ref.instance_build_cached(spec, theirs)
+    assert open(ours, "rb").read() == open(theirs, "rb").read()
+    b, hit_b = ctx.build_instance_cached(spec, theirs)
+    assert hit_b and b.num_edges == a.num_edges
+    want = ri.plan(spec.lam)
+    assert not abi.full_parity(ctx.plan(a, lam=spec.lam), want)
+    assert not abi.full_parity(ctx.plan(b, lam=spec.lam), want)
+    # an instance's graph saved explicitly is the same file again
+    again = str(tmp_path / "again.gmtg")
+    a.cache_save(again, native.problem_key(spec))
+    assert open(again, "rb").read() == open(theirs, "rb").read()
