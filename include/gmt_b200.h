@@ -346,6 +346,10 @@ int gmt_plan_host(gmt_ctx* ctx, const gmt_scene* scene, const double* coords, in
 /* fmt_plan (planner.cpp:200-262): the lambda -> 0 baseline, one node per
  * iteration, on the device.                                              */
 int gmt_fmt_plan(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, gmt_plan_out* out);
+/* dijkstra_oracle (planner.hpp:76-79, planner.cpp:264-334): every out-edge
+ * checked eagerly on the device (Euclidean pairs share one check), then
+ * exact Dijkstra from init over the surviving edges; iterations = pops.   */
+int gmt_dijkstra_oracle(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, gmt_plan_out* out);
 
 /* Batched independent queries: one CTA (or cluster) per query, one launch.
  * init_index may be NULL (use each instance's built init index).          */

@@ -298,6 +298,8 @@ int fill_instance(gmt_ctx* ctx, Arena& arena, DevInstance& desc, const gmt_scene
   }
   const bool has_in_path = paths && (directed ? g->in_path != nullptr : g->out_path != nullptr);
   const size_t o_ipath = has_in_path ? c.take<int32_t>(Ein) : 0;
+  const bool has_out_path = paths && directed && g->out_path != nullptr;
+  const size_t o_opath = has_out_path ? c.take<int32_t>(E) : 0;
   const size_t o_pptr = paths ? c.take<int64_t>(g->num_paths + 1) : 0;
   const size_t o_ppts = paths ? c.take<double>(static_cast<size_t>(npts) * d) : 0;
   GMT_TRY(arena.reserve(c.off));
@@ -323,6 +325,7 @@ int fill_instance(gmt_ctx* ctx, Arena& arena, DevInstance& desc, const gmt_scene
     GMT_TRY(put(o_icost, g->in_cost, sizeof(double) * Ein));
   }
   if (has_in_path) GMT_TRY(put(o_ipath, directed ? g->in_path : g->out_path, sizeof(int32_t) * Ein));
+  if (has_out_path) GMT_TRY(put(o_opath, g->out_path, sizeof(int32_t) * E));
   if (paths) {
     GMT_TRY(put(o_pptr, g->path_ptr, sizeof(int64_t) * (g->num_paths + 1)));
     GMT_TRY(put(o_ppts, g->path_pts, sizeof(double) * npts * d));
@@ -349,6 +352,7 @@ int fill_instance(gmt_ctx* ctx, Arena& arena, DevInstance& desc, const gmt_scene
   desc.in_col = directed ? at<int32_t>(base, o_icol) : desc.out_col;
   desc.in_cost = directed ? at<double>(base, o_icost) : desc.out_cost;
   desc.in_path = has_in_path ? at<int32_t>(base, o_ipath) : nullptr;
+  desc.out_path = has_out_path ? at<int32_t>(base, o_opath) : (directed ? nullptr : desc.in_path);
   desc.path_ptr = paths ? at<int64_t>(base, o_pptr) : nullptr;
   desc.path_pts = paths ? at<double>(base, o_ppts) : nullptr;
   return GMT_OK;
@@ -592,6 +596,45 @@ extern "C" int gmt_fmt_plan(gmt_ctx* ctx, const gmt_instance* inst, int32_t init
                             gmt_plan_out* out) {
   if (!inst) return set_error(GMT_E_INVALID_INPUT, "instance is null");
   return plan_on(ctx, inst, init_index, 1.0, inst->desc.radius, out, kModeFmt);
+}
+
+extern "C" int gmt_dijkstra_oracle(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index,
+                                   gmt_plan_out* out) {
+  // validate_plan_inputs (planner.cpp:17-23), then eager checks + Dijkstra.
+  if (!inst) return set_error(GMT_E_INVALID_INPUT, "instance is null");
+  if (inst->graph_n != inst->desc.n)
+    return set_error(GMT_E_INVALID_INPUT, "graph was built over a different sample count");
+  if (init_index < 0 || init_index >= inst->desc.n)
+    return set_error(GMT_E_INVALID_INPUT, "init_index " + std::to_string(init_index) + " out of range");
+  const DevInstance& D = inst->desc;
+  if (D.dim > kMaxSolveDim) return set_error(GMT_E_INVALID_INPUT, "dimension above 16 is not supported");
+  int64_t node_off[2] = {0, D.n};
+  std::vector<DevResult> res;
+  ResultScalars* sc;
+  GMT_TRY(carve_results(ctx->res, 1, node_off, true, false, res, &sc, nullptr));
+  SolveJob job{};
+  job.inst = static_cast<const DevInstance*>(inst->desc_mem.ptr);
+  job.res = res[0];
+  job.init_index = init_index;
+  job.mode = kModeGmt;
+  job.lambda = 1.0;
+  job.radius = D.radius;
+  GMT_TRY(ctx->jobs.reserve(sizeof(SolveJob)));
+  GMT_TRY(ctx->pinned_jobs.reserve(sizeof(SolveJob)));
+  std::memcpy(ctx->pinned_jobs.ptr, &job, sizeof(SolveJob));
+  cudaStream_t s = ctx->stream;
+  GMT_CUDA(cudaMemcpyAsync(ctx->jobs.ptr, ctx->pinned_jobs.ptr, sizeof(SolveJob), cudaMemcpyHostToDevice, s));
+  Arena buf;
+  GMT_TRY(buf.reserve(16 + static_cast<size_t>(D.num_edges)));
+  auto* checks = static_cast<unsigned long long*>(buf.ptr);
+  auto* ok = static_cast<uint8_t*>(buf.ptr) + 16;
+  GMT_CUDA(cudaMemsetAsync(checks, 0, sizeof(unsigned long long), s));
+  GMT_CUDA(launch_dijkstra(job.inst, static_cast<const SolveJob*>(ctx->jobs.ptr), D.n, D.dim, ok, checks,
+                           ctx->sm_count, s));
+  ctx->launches += 2;
+  const int rc = download_result(ctx, res[0], D.n, out);
+  buf.release();
+  return rc;
 }
 
 extern "C" int gmt_plan_host(gmt_ctx* ctx, const gmt_scene* scene, const double* coords, int32_t n,

@@ -50,6 +50,10 @@ struct DevInstance {
   // of the one edge it checks (di.cuh, quad.cuh).  kin_p: DI {vmax, weight},
   // quadrotor {g, vmax, amax, ymax, wmax, weight}.
   const double* in_tau;
+  // Out-edge views for the eager Dijkstra oracle: path ids of out-edges
+  // (uploaded path graphs) and out-edge durations (kinodynamic).
+  const int32_t* out_path;
+  const double* out_tau;
   int32_t steering;
   int32_t kin_segments;
   double kin_p[6];

@@ -767,6 +767,7 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
       D.in_col = din.col;
       D.in_cost = din.cost;
       D.in_tau = din.tau;
+      D.out_tau = dout.tau;
       D.steering = p->steering;
       if (quad) {
         D.kin_segments = p->quad.segments;

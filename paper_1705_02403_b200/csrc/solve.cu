@@ -32,6 +32,7 @@
 // per-axis loops of the geometry unroll into registers.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -1008,6 +1009,191 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       s.path_len = 0;
     }
     *R.scalars = s;
+  }
+}
+
+// ---- dijkstra_oracle (planner.cpp:264-334) -------------------------------------
+// Eager phase: every out-edge's motion is checked up front, warp per row,
+// lanes per box (the same exact segment / polyline / trajectory tests the
+// lazy check uses).  Euclidean graphs are symmetric: edge (u, v) with v < u
+// reuses the check of (v, u), i.e. segment_free(x_v, x_u), and is not
+// counted (planner.cpp:283-292).
+template <int D>
+__global__ void __launch_bounds__(256) eager_check_kernel(const DevInstance* __restrict__ inst,
+                                                          uint8_t* __restrict__ ok,
+                                                          unsigned long long* __restrict__ checks) {
+  __shared__ DevInstance I_s;
+  __shared__ Boxes bx_s;
+  __shared__ double seg_s[8 * 32];
+  if (threadIdx.x == 0) {
+    I_s = *inst;
+    Boxes b;
+    b.lo = I_s.box_lo;
+    b.hi = I_s.box_hi;
+    b.lom = nullptr;
+    b.him = nullptr;
+    b.bs = I_s.dim;
+    b.as = 1;
+    b.count = I_s.num_boxes;
+    bx_s = b;
+  }
+  __syncthreads();
+  const DevInstance& I = I_s;
+  const int d = dims<D>(I.dim);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* seg = seg_s + warp * 32;
+  const bool symmetric = !I.directed;
+  unsigned long long mine = 0;
+  for (int u = blockIdx.x * 8 + warp; u < I.n; u += gridDim.x * 8) {
+    for (int64_t e = I.out_ptr[u]; e < I.out_ptr[u + 1]; ++e) {
+      const int v = I.out_col[e];
+      const int a = (symmetric && v < u) ? v : u, b = (symmetric && v < u) ? u : v;
+      if (!(symmetric && v < u)) ++mine;
+      bool free;
+      if ((D == 0 || D == 6) && I.out_tau) {
+        free = kino_edge_free_warp<D>(I, bx_s, u, v, I.out_tau[e], lane, seg);
+      } else if (I.out_path) {
+        free = polyline_free_warp<D>(I, d, bx_s, I.out_path[e], lane, seg);
+      } else {
+        free = segment_free_warp<D>(I.coords + static_cast<int64_t>(a) * d,
+                                    I.coords + static_cast<int64_t>(b) * d, d, bx_s, lane, seg);
+      }
+      if (lane == 0) ok[e] = free ? 1 : 0;
+    }
+  }
+  if (lane == 0 && mine) atomicAdd(checks, mine);
+}
+
+// Search phase: Dijkstra over the surviving edges from init, one CTA.  The
+// reference's heap pops unsettled nodes in lexicographic (tentative cost,
+// index) order, so each pop is a block argmin over the open nodes; the row
+// of the popped node relaxes in parallel (each target appears once per row).
+// Labels / costs / parents live in the result arrays (HBM).
+template <int D>
+__global__ void __launch_bounds__(1024) dijkstra_kernel(const SolveJob* __restrict__ jobs,
+                                                        const uint8_t* __restrict__ ok,
+                                                        const unsigned long long* __restrict__ checks) {
+  __shared__ CtaShared sh;
+  __shared__ double seg_s[32];
+  __shared__ DevInstance I_s;
+  __shared__ Boxes bx_s;
+  const SolveJob job = jobs[blockIdx.x];
+  if (threadIdx.x == 0) {
+    I_s = *job.inst;
+    Boxes b;
+    b.lo = I_s.box_lo;
+    b.hi = I_s.box_hi;
+    b.lom = nullptr;
+    b.him = nullptr;
+    b.bs = I_s.dim;
+    b.as = 1;
+    b.count = I_s.num_boxes;
+    bx_s = b;
+  }
+  __syncthreads();
+  const DevInstance& I = I_s;
+  const DevResult& R = job.res;
+  const int n = I.n, d = dims<D>(I.dim);
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int init = job.init_index;
+  if (warp == 0) {  // infeasible_input (planner.cpp:39-41, 269): empty tree
+    const bool feas = I.goal_count > 0 &&
+                      point_free_warp<D>(I.coords + static_cast<int64_t>(init) * d, d, bx_s, lane, seg_s);
+    if (lane == 0) sh.feasible = feas ? 1 : 0;
+  }
+  __syncthreads();
+  if (!sh.feasible) {
+    if (tid == 0) {
+      ResultScalars s{};
+      s.status = 2;
+      s.goal_node = -1;
+      s.cost = kInf;
+      *R.scalars = s;
+    }
+    return;
+  }
+  for (int v = tid; v < n; v += nt) {  // make_wavefront (planner.cpp:25-35)
+    R.label[v] = v == init ? 1 : 0;
+    R.tree_cost[v] = v == init ? 0.0 : kInf;
+    R.parent[v] = -1;
+    R.iter_added[v] = v == init ? 0 : -1;
+  }
+  __syncthreads();
+  long long pops = 0;
+  int status = 1, goal = -1;
+  for (;;) {
+    double zc = kInf;
+    int32_t z = kNone;
+    for (int v = tid; v < n; v += nt)
+      if (R.label[v] == 1) argmin_step(zc, z, R.tree_cost[v], v);
+    block_argmin(zc, z, sh, lane, warp, nw);
+    if (z == kNone) break;  // failure_open_empty
+    ++pops;
+    __syncthreads();  // every thread has read the labels before z closes
+    if (tid == 0) R.label[z] = 2;
+    if (box_contains(I.goal_lo, I.goal_hi, d, I.coords + static_cast<int64_t>(z) * d)) {
+      status = 0;
+      goal = z;
+      break;
+    }
+    const double cz = R.tree_cost[z];
+    for (int64_t e = I.out_ptr[z] + tid; e < I.out_ptr[z + 1]; e += nt) {
+      if (!ok[e]) continue;
+      const int v = I.out_col[e];
+      if (v == z || R.label[v] == 2) continue;
+      const double c = __dadd_rn(cz, I.out_cost[e]);
+      if (c < R.tree_cost[v]) {
+        R.tree_cost[v] = c;
+        R.parent[v] = z;
+        if (R.label[v] == 0) R.label[v] = 1;
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    ResultScalars s{};
+    s.status = status;
+    s.goal_node = goal;
+    s.iterations = pops;
+    s.total_checks = static_cast<long long>(*checks);
+    s.tree_size = n;
+    s.num_stats = 0;  // the reference records no per-pass stats here
+    if (status == 0) {
+      s.cost = R.tree_cost[goal];
+      int len = 0;
+      for (int v = goal; v >= 0; v = R.parent[v]) ++len;
+      int k = len;
+      if (R.path)
+        for (int v = goal; v >= 0; v = R.parent[v]) R.path[--k] = v;
+      s.path_len = len;
+    } else {
+      s.cost = kInf;
+      s.path_len = 0;
+    }
+    *R.scalars = s;
+  }
+}
+
+template <int D>
+static cudaError_t launch_dijkstra_d(const DevInstance* inst, const SolveJob* job, int n,
+                                     uint8_t* ok, unsigned long long* checks, int sm_count,
+                                     cudaStream_t stream) {
+  const int blocks = std::max(1, std::min((n + 7) / 8, sm_count * 8));
+  eager_check_kernel<D><<<blocks, 256, 0, stream>>>(inst, ok, checks);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dijkstra_kernel<D><<<1, 1024, 0, stream>>>(job, ok, checks);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dijkstra(const DevInstance* inst, const SolveJob* job, int n, int dim, uint8_t* ok,
+                            unsigned long long* checks, int sm_count, cudaStream_t stream) {
+  switch (dim) {
+    case 2: return launch_dijkstra_d<2>(inst, job, n, ok, checks, sm_count, stream);
+    case 3: return launch_dijkstra_d<3>(inst, job, n, ok, checks, sm_count, stream);
+    case 6: return launch_dijkstra_d<6>(inst, job, n, ok, checks, sm_count, stream);
+    default: return launch_dijkstra_d<0>(inst, job, n, ok, checks, sm_count, stream);
   }
 }
 

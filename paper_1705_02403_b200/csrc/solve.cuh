@@ -55,4 +55,9 @@ __host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool o
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
                          int obs_in_smem, int dim, cudaStream_t stream);
 
+// dijkstra_oracle (planner.cpp:264-334): eager edge checks into ok[E] (and
+// the check count), then the Dijkstra search for job[0] (one CTA).
+cudaError_t launch_dijkstra(const DevInstance* inst, const SolveJob* job, int n, int dim, uint8_t* ok,
+                            unsigned long long* checks, int sm_count, cudaStream_t stream);
+
 }  // namespace gmtb

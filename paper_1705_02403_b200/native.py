@@ -69,6 +69,7 @@ SIGNATURES = [
     ("gmt_plan_host", C.c_int, [_vp, _P(abi.Scene), _dp, C.c_int32, C.c_int32, _P(abi.GraphView),
                                 C.c_int32, C.c_double, C.c_double, _P(abi.PlanOut)]),
     ("gmt_fmt_plan", C.c_int, [_vp, _vp, C.c_int32, _P(abi.PlanOut)]),
+    ("gmt_dijkstra_oracle", C.c_int, [_vp, _vp, C.c_int32, _P(abi.PlanOut)]),
     ("gmt_batch_create", C.c_int, [_vp, C.c_int32, _P(_vp), _i32p, C.c_double, _P(_vp)]),
     ("gmt_batch_launch", C.c_int, [_vp, _vp]),
     ("gmt_batch_summaries", C.c_int, [_vp, _vp, _P(abi.PlanSummary)]),
@@ -378,6 +379,14 @@ class Context:
         buf = abi.PlanBuffers(inst.n)
         ii = inst.init_index if init_index is None else init_index
         check(lib().gmt_fmt_plan(self.h, inst.h, ii, C.byref(buf.out)))
+        return buf.result()
+
+    def dijkstra_oracle(self, inst: Instance, init_index: int | None = None) -> abi.PlanResultPy:
+        """dijkstra_oracle (planner.cpp:264-334) on the device: eager checks
+        of every edge, then exact Dijkstra."""
+        buf = abi.PlanBuffers(inst.n)
+        ii = inst.init_index if init_index is None else init_index
+        check(lib().gmt_dijkstra_oracle(self.h, inst.h, ii, C.byref(buf.out)))
         return buf.result()
 
     def plan_host(self, spec, coords, goal_count, graph: Graph, init_index, lam, radius):
