@@ -204,6 +204,39 @@ typedef struct gmt_problem {
   gmt_quad_params quad;
 } gmt_problem;
 
+/* Replanning simulator (simulator.hpp:14-80): ScenarioConfig with its
+ * PlanningSetup flattened.  scene = the static obstacles at t = 0 and the
+ * goal; radius_override <= 0 means connection_radius.                    */
+typedef struct gmt_scenario {
+  gmt_scene scene;
+  const double* init;       /* dim coords */
+  int32_t n;                /* fresh samples per replan */
+  int32_t trials;           /* per campaign cell */
+  double lambda;
+  double eta;
+  double radius_override;
+  double collapse_rate;     /* expected obstacle spawns per second */
+  double spawn_box_size;
+  double disturbance_sigma;
+  double replan_latency;
+  double control_dt;
+  double robot_speed;
+  double time_limit;
+  uint64_t seed;            /* campaign master seed */
+} gmt_scenario;
+
+/* TrialOutcome::Result, same order as simulator.hpp:41. */
+enum { GMT_TRIAL_REACHED_GOAL = 0, GMT_TRIAL_COLLIDED = 1, GMT_TRIAL_TIMED_OUT = 2 };
+
+typedef struct gmt_trial_outcome {
+  int32_t result;
+  int32_t replans;
+  int32_t spawned;
+  int32_t noise_outliers;
+  double time;
+  int64_t path_len;         /* states in path_travelled (init included) */
+} gmt_trial_outcome;
+
 typedef struct gmt_ctx gmt_ctx;
 typedef struct gmt_instance gmt_instance;
 typedef struct gmt_batch gmt_batch;
@@ -293,6 +326,22 @@ int gmt_build_quad_graph(gmt_ctx* ctx, const double* coords, int32_t n,
                          int64_t* out_ptr, int32_t* out_col, double* out_cost, double* out_tau,
                          int64_t* in_ptr, int32_t* in_col, double* in_cost, int32_t* in_path,
                          double* path_pts);
+
+/* ---- replanning simulator (simulator.hpp:53-74) -------------------------- */
+/* run_trial (simulator.cpp:66-176): the trial state machine on the host,
+ * bit-identical to the reference, every replan (sample_free -> append_init
+ * -> graph -> gmt_plan) on the device.  path (may be NULL) receives up to
+ * path_cap states of path_travelled (dim doubles each).                  */
+int gmt_run_trial(gmt_ctx* ctx, const gmt_scenario* cfg, uint64_t trial_seed, gmt_trial_outcome* out,
+                  double* path, int64_t path_cap);
+/* run_campaign (simulator.cpp:178-227): the (latency x rate x sigma) grid,
+ * cfg->trials trials per cell, seeds from the cell parameters; `workers`
+ * host threads, each with its own context / stream on `device`.
+ * successes[num_latencies * num_rates * num_sigmas], cell order as the
+ * reference (latency outermost).                                         */
+int gmt_run_campaign(int device, const gmt_scenario* cfg, const double* latencies,
+                     int32_t num_latencies, const double* rates, int32_t num_rates,
+                     const double* sigmas, int32_t num_sigmas, int32_t workers, int32_t* successes);
 
 /* ---- GMTG v1 graph cache (graph.hpp:56-65, graph.cpp:190-343) --------- */
 /* problem_key (problem.cpp:281-303) of a Euclidean problem: the cache key

@@ -343,6 +343,11 @@ class RefLib(_Lib):
         L.ref_instance_info.argtypes = [C.c_void_p, _i32p, _i32p, _dp, _i64p, _i32p]
         L.ref_instance_download.restype = C.c_int
         L.ref_instance_download.argtypes = [C.c_void_p, _dp, _i32p, _i64p, _i32p, _dp]
+        L.ref_run_trial.restype = C.c_int
+        L.ref_run_trial.argtypes = [_P(abi.Scenario), C.c_uint64, _P(abi.TrialOutcome), _dp, C.c_int64]
+        L.ref_run_campaign.restype = C.c_int
+        L.ref_run_campaign.argtypes = [_P(abi.Scenario), _dp, C.c_int32, _dp, C.c_int32, _dp, C.c_int32,
+                                       C.c_int32, _i32p]
         L.ref_problem_key.restype = C.c_int
         L.ref_problem_key.argtypes = [_P(abi.Problem), _P(C.c_uint64)]
         L.ref_instance_build_cached.restype = C.c_int
@@ -395,6 +400,26 @@ class RefLib(_Lib):
         p = spec.flat()
         self._check(self.lib.ref_instance_build(C.byref(p), workers, C.byref(h)))
         return RefInstance(self, h)
+
+    # ---- simulator (simulator.cpp:66-227) ----------------------------------
+    def run_trial(self, scenario, seed: int, path_cap: int = 100000):
+        sc = scenario.flat()
+        out = abi.TrialOutcome()
+        path = np.zeros(path_cap * scenario.spec.dim)
+        self._check(self.lib.ref_run_trial(C.byref(sc), seed, C.byref(out), abi.ptr(path, C.c_double),
+                                           path_cap))
+        k = min(out.path_len, path_cap)
+        return out, path[: k * scenario.spec.dim].reshape(k, scenario.spec.dim)
+
+    def run_campaign(self, scenario, latencies, rates, sigmas, workers: int = 8):
+        sc = scenario.flat()
+        lat, rat, sig = abi.f64(latencies), abi.f64(rates), abi.f64(sigmas)
+        out = np.zeros(len(lat) * len(rat) * len(sig), np.int32)
+        self._check(self.lib.ref_run_campaign(C.byref(sc), abi.ptr(lat, C.c_double), len(lat),
+                                              abi.ptr(rat, C.c_double), len(rat),
+                                              abi.ptr(sig, C.c_double), len(sig), workers,
+                                              abi.ptr(out, C.c_int32)))
+        return out.reshape(len(lat), len(rat), len(sig))
 
     # ---- graph cache (graph.cpp:190-343) and problem_key (problem.cpp:281-303)
     def problem_key(self, spec) -> int:

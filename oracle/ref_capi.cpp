@@ -20,6 +20,7 @@
 #include "gmtplan/graph.hpp"
 #include "gmtplan/parallel.hpp"
 #include "gmtplan/planner.hpp"
+#include "gmtplan/simulator.hpp"
 #include "gmtplan/problem.hpp"
 #include "gmtplan/sampling.hpp"
 #include "gmtplan/space.hpp"
@@ -384,6 +385,54 @@ int ref_instance_download(void* h, double* coords, int32_t* goal_idx, int64_t* o
       }
       out_ptr[g.n] = e;
     }
+  });
+}
+
+// ---- simulator (simulator.cpp:66-227) ---------------------------------------
+ScenarioConfig to_scenario(const gmt_scenario* c) {
+  ScenarioConfig cfg;
+  cfg.base.obstacles = to_obs(&c->scene);
+  cfg.base.goal = to_goal(&c->scene);
+  cfg.base.init.coords.assign(c->init, c->init + c->scene.dim);
+  cfg.base.n = c->n;
+  cfg.base.lambda = c->lambda;
+  cfg.base.eta = c->eta;
+  if (c->radius_override > 0.0) cfg.base.radius_override = c->radius_override;
+  cfg.collapse_rate = c->collapse_rate;
+  cfg.spawn_box_size = c->spawn_box_size;
+  cfg.disturbance_sigma = c->disturbance_sigma;
+  cfg.replan_latency = c->replan_latency;
+  cfg.control_dt = c->control_dt;
+  cfg.robot_speed = c->robot_speed;
+  cfg.time_limit = c->time_limit;
+  cfg.trials = c->trials;
+  cfg.seed = c->seed;
+  return cfg;
+}
+
+int ref_run_trial(const gmt_scenario* c, uint64_t seed, gmt_trial_outcome* out, double* path,
+                  int64_t cap) {
+  return guard([&] {
+    TrialOutcome o = run_trial(to_scenario(c), seed);
+    out->result = static_cast<int32_t>(o.result);
+    out->replans = o.replans;
+    out->spawned = o.spawned;
+    out->noise_outliers = o.noise_outliers;
+    out->time = o.time;
+    out->path_len = static_cast<int64_t>(o.path_travelled.size());
+    const int d = c->scene.dim;
+    for (int64_t k = 0; path && k < cap && k < out->path_len; ++k)
+      std::copy(o.path_travelled[k].coords.begin(), o.path_travelled[k].coords.end(), path + k * d);
+  });
+}
+
+int ref_run_campaign(const gmt_scenario* c, const double* lat, int32_t nl, const double* rates,
+                     int32_t nr, const double* sig, int32_t ns, int32_t workers, int32_t* successes) {
+  return guard([&] {
+    auto cells = run_campaign(to_scenario(c), std::vector<double>(lat, lat + nl),
+                              std::vector<double>(rates, rates + nr), std::vector<double>(sig, sig + ns),
+                              workers);
+    for (size_t k = 0; k < cells.size(); ++k) successes[k] = cells[k].successes;
   });
 }
 

@@ -298,3 +298,40 @@ def full_parity(a: PlanResultPy, b: PlanResultPy) -> list[str]:
         if not np.array_equal(x, y):
             bad.append(f)
     return bad
+
+
+class Scenario(C.Structure):
+    """gmt_scenario: ScenarioConfig + PlanningSetup (simulator.hpp:14-36)."""
+    _fields_ = [
+        ("scene", Scene),
+        ("init", _dp),
+        ("n", C.c_int32),
+        ("trials", C.c_int32),
+        ("lambda_", C.c_double),
+        ("eta", C.c_double),
+        ("radius_override", C.c_double),
+        ("collapse_rate", C.c_double),
+        ("spawn_box_size", C.c_double),
+        ("disturbance_sigma", C.c_double),
+        ("replan_latency", C.c_double),
+        ("control_dt", C.c_double),
+        ("robot_speed", C.c_double),
+        ("time_limit", C.c_double),
+        ("seed", C.c_uint64),
+    ]
+
+
+class TrialOutcome(C.Structure):
+    """gmt_trial_outcome (simulator.hpp:40-51)."""
+    _fields_ = [
+        ("result", C.c_int32),
+        ("replans", C.c_int32),
+        ("spawned", C.c_int32),
+        ("noise_outliers", C.c_int32),
+        ("time", C.c_double),
+        ("path_len", C.c_int64),
+    ]
+
+
+TRIAL_REACHED_GOAL, TRIAL_COLLIDED, TRIAL_TIMED_OUT = 0, 1, 2
+

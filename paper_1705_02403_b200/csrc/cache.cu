@@ -241,6 +241,7 @@ extern "C" int gmt_graph_cache_load(const char* file, uint64_t key, int32_t n, d
 
 extern "C" int gmt_instance_cache_save(gmt_ctx* ctx, const gmt_instance* inst, const char* file,
                                        uint64_t key) {
+  gmtb::AllocScope alloc_scope_(ctx);
   const DevInstance& D = inst->desc;
   if (D.directed) return set_error(GMT_E_INVALID_INPUT, "the graph cache covers the Euclidean steering model only");
   const int n = D.n;

@@ -47,20 +47,32 @@ int cuda_error(cudaError_t e, const char* what) {
 // ---- device arena -----------------------------------------------------------
 namespace gmtb {
 
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
+AllocScope::AllocScope(gmt_ctx* ctx) : prev(g_alloc_stream) {
+  g_alloc_stream = ctx ? ctx->stream : nullptr;
+}
+
 int Arena::reserve(size_t bytes) {
   if (bytes <= cap) return GMT_OK;
-  if (ptr) cudaFree(ptr);
-  ptr = nullptr;
-  cap = 0;
+  release();
   size_t want = std::max(bytes, static_cast<size_t>(1) << 20);
-  cudaError_t e = cudaMalloc(&ptr, want);
-  if (e != cudaSuccess) return cuda_error(e, "cudaMalloc");
+  const cudaError_t e = g_alloc_stream ? cudaMallocAsync(&ptr, want, g_alloc_stream) : cudaMalloc(&ptr, want);
+  if (e != cudaSuccess) {
+    ptr = nullptr;
+    return cuda_error(e, "device allocation");
+  }
   cap = want;
   return GMT_OK;
 }
 
 void Arena::release() {
-  if (ptr) cudaFree(ptr);
+  if (ptr) {
+    if (g_alloc_stream)
+      cudaFreeAsync(ptr, g_alloc_stream);
+    else
+      cudaFree(ptr);
+  }
   ptr = nullptr;
   cap = 0;
 }
@@ -131,6 +143,13 @@ extern "C" int gmt_ctx_create(int device, gmt_ctx** out) {
                                           "for sm_100a only");
   }
   GMT_CUDA(cudaSetDevice(device));
+  {  // keep freed pool memory for reuse instead of returning it at every sync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   auto* ctx = new gmt_ctx;
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
@@ -157,9 +176,17 @@ extern "C" void gmt_ctx_destroy(gmt_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  ctx->res.release();
-  ctx->scratch.release();
-  ctx->jobs.release();
+  {
+    AllocScope scope(ctx);
+    ctx->res.release();
+    ctx->scratch.release();
+    ctx->jobs.release();
+    ctx->plan_inst.mem.release();
+    ctx->plan_inst.desc_mem.release();
+    ctx->plan_inst.aux.release();
+    ctx->plan_inst.mem2.release();
+  }
+  cudaStreamSynchronize(ctx->stream);
   ctx->pinned.release();
   ctx->pinned2.release();
   ctx->pinned_jobs.release();
@@ -174,6 +201,7 @@ extern "C" void gmt_ctx_destroy(gmt_ctx* ctx) {
 extern "C" void* gmt_ctx_stream(gmt_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 
 extern "C" int gmt_ctx_synchronize(gmt_ctx* ctx) {
+  gmtb::AllocScope alloc_scope_(ctx);
   GMT_CUDA(cudaStreamSynchronize(ctx->stream));
   return GMT_OK;
 }
@@ -181,6 +209,7 @@ extern "C" int gmt_ctx_synchronize(gmt_ctx* ctx) {
 extern "C" int64_t gmt_launch_count(const gmt_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 extern "C" int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value) {
+  gmtb::AllocScope alloc_scope_(ctx);
   switch (option) {
     case GMT_OPT_CLUSTER:
       if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8 && value != 16)
@@ -210,6 +239,7 @@ extern "C" int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value) {
 }
 
 extern "C" int gmt_ctx_counters(gmt_ctx* ctx, int64_t* out, int32_t reset) {
+  gmtb::AllocScope alloc_scope_(ctx);
   GMT_CUDA(cudaStreamSynchronize(ctx->stream));
   GMT_CUDA(cudaMemcpy(out, ctx->counters, sizeof(int64_t) * 3, cudaMemcpyDeviceToHost));
   if (reset) GMT_CUDA(cudaMemset(ctx->counters, 0, sizeof(int64_t) * 4));
@@ -370,6 +400,7 @@ int push_desc(gmt_ctx* ctx, gmt_instance* inst) {
 extern "C" int gmt_instance_upload(gmt_ctx* ctx, const gmt_scene* scene, const double* coords,
                                    int32_t n, int32_t goal_count, const gmt_graph_view* graph,
                                    gmt_instance** out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   *out = nullptr;
   auto* inst = new gmt_instance;
   int rc = fill_instance(ctx, inst->mem, inst->desc, scene, coords, n, goal_count, graph);
@@ -403,6 +434,7 @@ extern "C" int gmt_instance_info(const gmt_instance* inst, int32_t* n, int32_t* 
 extern "C" int gmt_instance_download(gmt_ctx* ctx, const gmt_instance* inst, double* coords,
                                      int32_t* goal_idx, int64_t* out_ptr, int32_t* out_col,
                                      double* out_cost) {
+  gmtb::AllocScope alloc_scope_(ctx);
   const DevInstance& D = inst->desc;
   cudaStream_t s = ctx->stream;
   if (coords)
@@ -518,8 +550,13 @@ int launch_jobs(gmt_ctx* ctx, const std::vector<SolveJob>& jobs, int cluster, in
   std::memcpy(ctx->pinned_jobs.ptr, jobs.data(), bytes);
   GMT_CUDA(cudaMemcpyAsync(ctx->jobs.ptr, ctx->pinned_jobs.ptr, bytes, cudaMemcpyHostToDevice,
                            ctx->stream));
-  GMT_CUDA(launch_solve(static_cast<const SolveJob*>(ctx->jobs.ptr), static_cast<int>(jobs.size()),
-                        cluster, threads, smem, obs_in_smem, dim, ctx->stream));
+  const cudaError_t e = launch_solve(static_cast<const SolveJob*>(ctx->jobs.ptr), static_cast<int>(jobs.size()),
+                                     cluster, threads, smem, obs_in_smem, dim, ctx->stream);
+  if (e != cudaSuccess) {
+    return set_error(GMT_E_CUDA, std::string("solve launch (cluster ") + std::to_string(cluster) + ", " +
+                                     std::to_string(threads) + " threads, " + std::to_string(smem) +
+                                     " B smem, dim " + std::to_string(dim) + "): " + cudaGetErrorString(e));
+  }
   ++ctx->launches;
   return GMT_OK;
 }
@@ -589,17 +626,20 @@ int plan_on(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, double l
 
 extern "C" int gmt_plan(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, double lambda,
                         double radius, gmt_plan_out* out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   return plan_on(ctx, inst, init_index, lambda, radius, out);
 }
 
 extern "C" int gmt_fmt_plan(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index,
                             gmt_plan_out* out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   if (!inst) return set_error(GMT_E_INVALID_INPUT, "instance is null");
   return plan_on(ctx, inst, init_index, 1.0, inst->desc.radius, out, kModeFmt);
 }
 
 extern "C" int gmt_dijkstra_oracle(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index,
                                    gmt_plan_out* out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   // validate_plan_inputs (planner.cpp:17-23), then eager checks + Dijkstra.
   if (!inst) return set_error(GMT_E_INVALID_INPUT, "instance is null");
   if (inst->graph_n != inst->desc.n)
@@ -640,6 +680,7 @@ extern "C" int gmt_dijkstra_oracle(gmt_ctx* ctx, const gmt_instance* inst, int32
 extern "C" int gmt_plan_host(gmt_ctx* ctx, const gmt_scene* scene, const double* coords, int32_t n,
                              int32_t goal_count, const gmt_graph_view* graph, int32_t init_index,
                              double lambda, double radius, gmt_plan_out* out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   // planner.cpp:17-23 checks come first, before anything is uploaded.
   if (!graph) return set_error(GMT_E_INVALID_INPUT, "graph is null");
   if (graph->n != n) return set_error(GMT_E_INVALID_INPUT, "graph was built over a different sample count");
@@ -677,6 +718,7 @@ struct gmt_batch {
 
 extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const* insts,
                                 const int32_t* init_index, double lambda, gmt_batch** out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   *out = nullptr;
   if (count < 1) return set_error(GMT_E_INVALID_INPUT, "batch needs at least one query");
   auto* b = new gmt_batch;
@@ -742,6 +784,7 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
 }
 
 extern "C" int gmt_batch_launch(gmt_ctx* ctx, gmt_batch* b) {
+  gmtb::AllocScope alloc_scope_(ctx);
   GMT_CUDA(launch_solve(static_cast<const SolveJob*>(b->jobs_mem.ptr), static_cast<int>(b->jobs.size()),
                         b->cluster, b->threads, b->smem, b->obs, b->dim, ctx->stream));
   ++ctx->launches;
@@ -759,6 +802,7 @@ static void to_summary(const ResultScalars& s, gmt_plan_summary* o) {
 }
 
 extern "C" int gmt_batch_summaries(gmt_ctx* ctx, gmt_batch* b, gmt_plan_summary* out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   const size_t count = b->jobs.size();
   std::vector<ResultScalars> sc(count);
   GMT_CUDA(cudaMemcpyAsync(sc.data(), b->scalars, sizeof(ResultScalars) * count,
@@ -769,6 +813,7 @@ extern "C" int gmt_batch_summaries(gmt_ctx* ctx, gmt_batch* b, gmt_plan_summary*
 }
 
 extern "C" int gmt_batch_result(gmt_ctx* ctx, gmt_batch* b, int32_t q, gmt_plan_out* out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   if (q < 0 || q >= static_cast<int32_t>(b->jobs.size()))
     return set_error(GMT_E_INVALID_INPUT, "query index out of range");
   const int n = static_cast<int>(b->node_off[q + 1] - b->node_off[q]);
@@ -781,6 +826,7 @@ extern "C" void gmt_batch_destroy(gmt_batch* b) { delete b; }
 extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double lambda,
                                    gmt_plan_summary* summaries, int32_t* paths, uint8_t* label,
                                    double* tree_cost, int32_t* parent, int64_t* iteration_added) {
+  gmtb::AllocScope alloc_scope_(ctx);
   const int count = B->count, d = B->dim;
   if (count < 1) return set_error(GMT_E_INVALID_INPUT, "batch needs at least one query");
   if (d < 1) return set_error(GMT_E_INVALID_INPUT, "dimension must be >= 1");
@@ -816,6 +862,10 @@ extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double
   const size_t o_cost = c.take<double>(total_edges);
   const size_t o_desc = c.take<DevInstance>(count);
   GMT_TRY(ctx->scratch.reserve(c.off));
+  // The (stream-ordered) scratch allocation happens on ctx->stream; the
+  // copy stream may only write it after that point.
+  GMT_CUDA(cudaEventRecord(ctx->copy_done[0], ctx->stream));
+  GMT_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_done[0], 0));
   void* base = ctx->scratch.ptr;
   cudaStream_t s = ctx->stream, cs = ctx->copy_stream;
 

@@ -445,6 +445,7 @@ using namespace gmtb;
 
 extern "C" int gmt_di_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count,
                             const gmt_di_params* params, double* cost_out, double* tau_out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   int rc = validate_di(params);
   if (rc) return rc;
   return kino_costs(ctx, x0s, x1s, count, di_model(params, 1.0), cost_out, tau_out);
@@ -452,6 +453,7 @@ extern "C" int gmt_di_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, 
 
 extern "C" int gmt_quad_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count,
                               const gmt_quad_params* params, double* cost_out, double* tau_out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   int rc = validate_quad(params);
   if (rc) return rc;
   return kino_costs(ctx, x0s, x1s, count, quad_model(params, 1.0), cost_out, tau_out);
@@ -462,6 +464,7 @@ extern "C" int gmt_build_di_graph(gmt_ctx* ctx, const double* coords, int32_t n,
                                   int64_t* out_ptr, int32_t* out_col, double* out_cost,
                                   double* out_tau, int64_t* in_ptr, int32_t* in_col,
                                   double* in_cost, int32_t* in_path, double* path_pts) {
+  gmtb::AllocScope alloc_scope_(ctx);
   int rc = validate_di(params);
   if (rc) return rc;
   return build_kino_graph_host(ctx, coords, n, di_model(params, radius), radius, num_edges, out_ptr,
@@ -473,6 +476,7 @@ extern "C" int gmt_build_quad_graph(gmt_ctx* ctx, const double* coords, int32_t 
                                     int64_t* out_ptr, int32_t* out_col, double* out_cost,
                                     double* out_tau, int64_t* in_ptr, int32_t* in_col,
                                     double* in_cost, int32_t* in_path, double* path_pts) {
+  gmtb::AllocScope alloc_scope_(ctx);
   int rc = validate_quad(params);
   if (rc) return rc;
   return build_kino_graph_host(ctx, coords, n, quad_model(params, radius), radius, num_edges, out_ptr,

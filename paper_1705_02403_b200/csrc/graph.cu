@@ -237,6 +237,7 @@ using namespace gmtb;
 extern "C" int gmt_build_neighbor_graph(gmt_ctx* ctx, const double* coords, int32_t n, int32_t dim,
                                         double radius, int64_t* num_edges, int64_t* out_ptr,
                                         int32_t* out_col, double* out_cost) {
+  gmtb::AllocScope alloc_scope_(ctx);
   if (n < 1) return set_error(GMT_E_INVALID_INPUT, "cannot build a graph over zero samples");
   if (dim < 1) return set_error(GMT_E_INVALID_INPUT, "dimension must be >= 1");
   Arena in;

@@ -17,6 +17,13 @@ extern thread_local std::string g_last_error;
 int set_error(int code, const std::string& msg);
 int cuda_error(cudaError_t e, const char* what);
 
+// Device allocations are stream-ordered (cudaMallocAsync / cudaFreeAsync
+// from the device's memory pool) on the stream of the context the current
+// C-ABI call runs on, so building and freeing instances never synchronises
+// the whole device (concurrent contexts overlap).  Outside a call (e.g.
+// gmt_instance_destroy) the synchronous cudaMalloc / cudaFree are used.
+extern thread_local cudaStream_t g_alloc_stream;
+
 // Growable device allocation (never shrinks).
 struct Arena {
   void* ptr = nullptr;
@@ -37,6 +44,15 @@ struct HostPinned {
 
 struct gmt_instance;
 struct gmt_ctx;
+
+namespace gmtb {
+// Makes `ctx`'s stream the allocation stream for the duration of a call.
+struct AllocScope {
+  cudaStream_t prev;
+  explicit AllocScope(gmt_ctx* ctx);
+  ~AllocScope() { g_alloc_stream = prev; }
+};
+}  // namespace gmtb
 
 namespace gmtb {
 int validate_scene(const gmt_scene* s);

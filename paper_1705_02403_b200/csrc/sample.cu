@@ -542,6 +542,7 @@ extern "C" int gmt_sample_free(gmt_ctx* ctx, int32_t n, const gmt_scene* scene,
                                const gmt_sample_source* src, double* coords_out,
                                double* heading_out, int32_t* goal_idx_out,
                                int32_t* goal_count_out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   Arena out;
   DevSamples S;
   int rc = sample_free_dev(ctx, n, scene, src, out, &S);
@@ -564,6 +565,7 @@ extern "C" int gmt_append_init(gmt_ctx* ctx, int32_t dim, double* coords, double
                                int32_t* n, const double* init, int32_t init_has_heading,
                                double init_heading, const double* goal_lo, const double* goal_hi,
                                int32_t* goal_idx, int32_t* goal_count, int32_t* index_out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   const int n0 = *n;
   Arena buf;
   int rc = buf.reserve(align16(sizeof(double) * (n0 + 1) * dim) + sizeof(double) * (n0 + 1) +
@@ -814,11 +816,13 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
 }
 
 extern "C" int gmt_instance_build(gmt_ctx* ctx, const gmt_problem* p, gmt_instance** out) {
+  gmtb::AllocScope alloc_scope_(ctx);
   return instance_build(ctx, p, nullptr, out, nullptr);
 }
 
 extern "C" int gmt_instance_build_cached(gmt_ctx* ctx, const gmt_problem* p, const char* cache_file,
                                          gmt_instance** out, int32_t* cache_hit) {
+  gmtb::AllocScope alloc_scope_(ctx);
   if (!cache_file) return set_error(GMT_E_INVALID_INPUT, "gmt_instance_build_cached: null cache file");
   return instance_build(ctx, p, cache_file, out, cache_hit);
 }

@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
 
 #include "common.cuh"
 #include "di.cuh"
@@ -1201,12 +1202,26 @@ template <int CS, int D, bool WIDE>
 static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_t smem,
                              int obs_in_smem, cudaStream_t stream) {
   auto kern = gmt_solve_kernel<CS, D, WIDE>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-  if (err != cudaSuccess) return err;
-  if (CS > 8) {
-    err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (err != cudaSuccess) return err;
+  // Function attributes are process-wide: the dynamic shared-memory limit
+  // only ever grows (under a lock), so concurrent launches from several host
+  // threads (each with its own context / stream) never see it shrink below
+  // what they need.
+  static std::mutex mu;
+  static size_t granted = 0;
+  static bool cluster_ok = false;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem > granted) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      granted = smem;
+    }
+    if (CS > 8 && !cluster_ok) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      cluster_ok = true;
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(count) * CS, 1, 1);

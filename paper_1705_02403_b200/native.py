@@ -53,6 +53,10 @@ SIGNATURES = [
     ("gmt_build_di_graph", C.c_int, [_vp, _dp, C.c_int32, _P(abi.DiParams), C.c_double, _i64p,
                                      _i64p, _i32p, _dp, _dp, _i64p, _i32p, _dp, _i32p, _dp]),
     ("gmt_problem_key", C.c_int, [_P(abi.Problem), _P(C.c_uint64)]),
+    ("gmt_run_trial", C.c_int, [_vp, _P(abi.Scenario), C.c_uint64, _P(abi.TrialOutcome), _dp,
+                                C.c_int64]),
+    ("gmt_run_campaign", C.c_int, [C.c_int, _P(abi.Scenario), _dp, C.c_int32, _dp, C.c_int32, _dp,
+                                   C.c_int32, C.c_int32, _i32p]),
     ("gmt_graph_cache_save", C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, C.c_double, _i64p, _i32p,
                                        _dp]),
     ("gmt_graph_cache_load", C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, C.c_double, _i32p, _i64p,
@@ -389,6 +393,16 @@ class Context:
         check(lib().gmt_dijkstra_oracle(self.h, inst.h, ii, C.byref(buf.out)))
         return buf.result()
 
+    def run_trial(self, scenario, seed: int, path_cap: int = 100000):
+        """run_trial (simulator.cpp:66-176) -> (TrialOutcome, path_travelled [k, dim])."""
+        sc = scenario.flat()
+        out = abi.TrialOutcome()
+        path = np.zeros(path_cap * scenario.spec.dim)
+        check(lib().gmt_run_trial(self.h, C.byref(sc), seed, C.byref(out), abi.ptr(path, C.c_double),
+                                  path_cap))
+        k = min(out.path_len, path_cap)
+        return out, path[: k * scenario.spec.dim].reshape(k, scenario.spec.dim)
+
     def plan_host(self, spec, coords, goal_count, graph: Graph, init_index, lam, radius):
         coords = abi.f64(coords)
         buf = abi.PlanBuffers(coords.shape[0])
@@ -558,4 +572,16 @@ def graph_cache_load(file: str, key: int, n: int, radius: float, dim: int = 0):
                                      abi.ptr(ptr, C.c_int64), abi.ptr(col, C.c_int32),
                                      abi.ptr(cost, C.c_double)))
     return Graph(n, radius, ptr, col[:E], cost[:E], dim=dim)
+
+
+def run_campaign(scenario, latencies, rates, sigmas, workers: int = 8, device: int = 0):
+    """run_campaign (simulator.cpp:178-227) -> successes per cell, shape
+    (len(latencies), len(rates), len(sigmas))."""
+    sc = scenario.flat()
+    lat, rat, sig = abi.f64(latencies), abi.f64(rates), abi.f64(sigmas)
+    out = np.zeros(len(lat) * len(rat) * len(sig), np.int32)
+    check(lib().gmt_run_campaign(device, C.byref(sc), abi.ptr(lat, C.c_double), len(lat),
+                                 abi.ptr(rat, C.c_double), len(rat), abi.ptr(sig, C.c_double),
+                                 len(sig), workers, abi.ptr(out, C.c_int32)))
+    return out.reshape(len(lat), len(rat), len(sig))
 

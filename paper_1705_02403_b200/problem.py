@@ -566,3 +566,38 @@ def connection_radius_py(dim: int, n: int, eta: float = 0.0, mu: float = 1.0) ->
     zeta = math.pi ** (0.5 * dim) / math.gamma(0.5 * dim + 1.0)
     return (4.0 * (1.0 + eta) ** inv_d * inv_d ** inv_d * (mu / zeta) ** inv_d
             * (math.log(n) / n) ** inv_d)
+
+
+@dataclass
+class Scenario:
+    """ScenarioConfig (simulator.hpp:25-36) over a planning setup given as a
+    ProblemSpec (obstacles at t = 0, goal, init, n, lambda, eta, radius)."""
+    spec: ProblemSpec
+    collapse_rate: float = 0.0
+    spawn_box_size: float = 0.08
+    disturbance_sigma: float = 0.0
+    replan_latency: float = 0.1
+    control_dt: float = 0.05
+    robot_speed: float = 0.1
+    time_limit: float = 30.0
+    trials: int = 50
+    seed: int = 0
+    _keep: list = field(default_factory=list, repr=False)
+
+    def flat(self) -> abi.Scenario:
+        s = abi.Scenario()
+        s.scene = self.spec.scene()
+        init = abi.f64(self.spec.init)
+        self._keep = [init, self.spec._keep]
+        s.init = abi.ptr(init, abi.C.c_double)
+        s.n = self.spec.n
+        s.trials = self.trials
+        s.lambda_ = self.spec.lam
+        s.eta = self.spec.eta
+        s.radius_override = self.spec.radius_override or 0.0
+        for f in ("collapse_rate", "spawn_box_size", "disturbance_sigma", "replan_latency",
+                  "control_dt", "robot_speed", "time_limit"):
+            setattr(s, f, getattr(self, f))
+        s.seed = self.seed
+        return s
+
