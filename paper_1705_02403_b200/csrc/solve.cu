@@ -50,10 +50,14 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int32_t kNone = 0x7fffffff;
-#ifndef GMT_UNROLL
-#define GMT_UNROLL 4
+// Row chunks in flight per lane: batched solves cover a typical in-row
+// (~130 edges for C2) in one round with 16 lanes x 8; clusters use 32 lanes.
+#ifndef GMT_UNROLL_BATCH
+#define GMT_UNROLL_BATCH 8
 #endif
-constexpr int kUnroll = GMT_UNROLL;  // row chunks in flight per lane
+#ifndef GMT_UNROLL_CLUSTER
+#define GMT_UNROLL_CLUSTER 4
+#endif
 constexpr double kSepMargin = 1e-9;  // see segment_free_staged
 #ifndef GMT_ROWS_PER_WARP
 #define GMT_ROWS_PER_WARP 2
@@ -431,6 +435,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   // warp; the pass critical path matters).
   constexpr int kRows = CS == 1 ? GMT_ROWS_PER_WARP : 1;
   constexpr int kLanesPerRow = kWarp / kRows;
+  constexpr int kUnroll = CS == 1 ? GMT_UNROLL_BATCH : GMT_UNROLL_CLUSTER;
   __shared__ double seg_s[kMaxWarps * 32 * kRows];  // per warp: kRows staged segments
 
   const int q = blockIdx.x / CS;
