@@ -83,6 +83,8 @@ struct CtaShared {
   int32_t group_count;
   int32_t own_count;  // group members this CTA expands in P4
   int32_t cand_count;
+  int32_t next_own;   // dynamic work distribution (clusters): next P4 row group
+  int32_t next_cand;  // next P5 candidate group
   unsigned long long checks_acc;  // rank 0: cluster-wide checks of this pass
   int32_t added_acc;              // rank 0: cluster-wide additions of this pass
   int32_t feasible;
@@ -436,6 +438,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   constexpr int kRows = CS == 1 ? GMT_ROWS_PER_WARP : 1;
   constexpr int kLanesPerRow = kWarp / kRows;
   constexpr int kUnroll = CS == 1 ? GMT_UNROLL_BATCH : GMT_UNROLL_CLUSTER;
+  constexpr bool kDynamic = CS > 1;  // dynamic row / candidate distribution
   __shared__ double seg_s[kMaxWarps * 32 * kRows];  // per warp: kRows staged segments
 
   const int q = blockIdx.x / CS;
@@ -524,6 +527,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
     sh.added_acc = 0;
     sh.iter = 0;
     sh.total_checks = 0;
+    sh.next_own = kRows * (static_cast<int>(blockDim.x) >> 5);
+    sh.next_cand = kRows * (static_cast<int>(blockDim.x) >> 5);
     sh.pass = 0;
     sh.cnt_in = 0ull;
     sh.cnt_out = 0ull;
@@ -689,7 +694,13 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         len = static_cast<int>(__ldg(I.out_ptr + g + 1) - e0);
       }
       while (k < own) {
-        const int kn = k + kRows * nw;
+        // Clusters take the next row pair from a shared counter (their few,
+        // uneven rows balance better); batched CTAs stride statically.
+        int kn = k + kRows * nw;
+        if constexpr (kDynamic) {
+          if (lane == 0) kn = atomicAdd(&sh.next_own, kRows);
+          kn = __shfl_sync(kFull, kn, 0);
+        }
         int64_t n0 = 0;
         int nlen = 0;
         if (kn + h < own) {  // next rows' offsets in flight during these rows
@@ -774,7 +785,11 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         len = static_cast<int>(__ldg(I.in_ptr + x + 1) - e0);
       }
       while (k < ccount) {
-        const int kn = k + kRows * nw;
+        int kn = k + kRows * nw;
+        if constexpr (kDynamic) {
+          if (lane == 0) kn = atomicAdd(&sh.next_cand, kRows);
+          kn = __shfl_sync(kFull, kn, 0);
+        }
         int xn = -1;
         int64_t n0 = 0;
         int nlen = 0;
@@ -952,6 +967,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       sh.cand_count = 0;
       sh.iter = i + 1;
       sh.pass = sh.pass + 1;
+      sh.next_own = kRows * nw;
+      sh.next_cand = kRows * nw;
     }
     __syncthreads();
   }
