@@ -158,6 +158,7 @@ typedef struct gmt_plan_summary {
  * trajectory polylines for the lazy check.                                 */
 typedef enum gmt_steering {
   GMT_STEER_EUCLIDEAN = 0,
+  GMT_STEER_DUBINS_AIRPLANE = 1,  /* steering.hpp:10, dubins.cpp (see gmt_dubins_params) */
   GMT_STEER_DOUBLE_INTEGRATOR = 2,
   GMT_STEER_QUADROTOR = 3
 } gmt_steering;
@@ -168,6 +169,19 @@ typedef struct gmt_di_params {
   int32_t segments;
   int32_t reserved;
 } gmt_di_params;
+
+/* GMT_STEER_DUBINS_AIRPLANE (SteeringModel, steering.hpp:9-23): planar
+ * Dubins paths of turning radius rho in (x, y), altitude (coordinate 2, if
+ * present) linear in arc length; cost sqrt(Lp^2 + dz^2) (or Lp when
+ * planar_cost_only); paths discretised every discretization_step (0 means
+ * rho / 10).  Samples carry a heading.  Costs match the reference to a few
+ * ulps (its sin/cos/atan2/acos come from glibc).          */
+typedef struct gmt_dubins_params {
+  double rho;
+  double discretization_step;
+  int32_t planar_cost_only;
+  int32_t reserved;
+} gmt_dubins_params;
 
 /* GMT_STEER_QUADROTOR: the NEW 12D linearised quadrotor of SURVEY.md §8 row
  * a22.  State [p(3), v(3), roll/pitch/yaw(3), rates(3)] in
@@ -202,6 +216,7 @@ typedef struct gmt_problem {
   int32_t reserved;
   gmt_di_params di;
   gmt_quad_params quad;
+  gmt_dubins_params dubins;
 } gmt_problem;
 
 /* Replanning simulator (simulator.hpp:14-80): ScenarioConfig with its
@@ -246,8 +261,8 @@ const char* gmt_last_error(void);
 int gmt_abi_version(void);
 /* sizeof of the ABI structs, in the order gmt_scene, gmt_sample_source,
  * gmt_graph_view, gmt_plan_out, gmt_plan_summary, gmt_problem,
- * gmt_di_params, gmt_batch_host, gmt_quad_params (bindings check their
- * layouts with it).                                                        */
+ * gmt_di_params, gmt_batch_host, gmt_quad_params, gmt_scenario,
+ * gmt_trial_outcome, gmt_dubins_params (bindings check their layouts).    */
 int gmt_struct_sizes(int64_t* out, int32_t count);
 int gmt_ctx_create(int device, gmt_ctx** out);
 void gmt_ctx_destroy(gmt_ctx* ctx);
@@ -342,6 +357,13 @@ int gmt_run_trial(gmt_ctx* ctx, const gmt_scenario* cfg, uint64_t trial_seed, gm
 int gmt_run_campaign(int device, const gmt_scenario* cfg, const double* latencies,
                      int32_t num_latencies, const double* rates, int32_t num_rates,
                      const double* sigmas, int32_t num_sigmas, int32_t workers, int32_t* successes);
+
+/* Dubins-airplane steering on the device (connect_cost, steering.cpp:104-112;
+ * connect's segment count, steering.cpp:83): states are (x, y[, z],
+ * heading), dim = position coordinates (2 or 3).  segments_out[i] = 0 for
+ * the degenerate pair (path = {a}).                                      */
+int gmt_dubins_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count, int32_t dim,
+                     const gmt_dubins_params* params, double* cost_out, int32_t* segments_out);
 
 /* ---- GMTG v1 graph cache (graph.hpp:56-65, graph.cpp:190-343) --------- */
 /* problem_key (problem.cpp:281-303) of a Euclidean problem: the cache key

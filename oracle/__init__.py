@@ -343,6 +343,11 @@ class RefLib(_Lib):
         L.ref_instance_info.argtypes = [C.c_void_p, _i32p, _i32p, _dp, _i64p, _i32p]
         L.ref_instance_download.restype = C.c_int
         L.ref_instance_download.argtypes = [C.c_void_p, _dp, _i32p, _i64p, _i32p, _dp]
+        L.ref_dubins_costs.restype = C.c_int
+        L.ref_dubins_costs.argtypes = [_dp, _dp, C.c_int64, C.c_int32, _P(abi.DubinsParams), _dp, _i32p]
+        L.ref_instance_download_paths.restype = C.c_int
+        L.ref_instance_download_paths.argtypes = [C.c_void_p, _i64p, _i32p, _dp, _i32p, _i32p, _i64p, _dp,
+                                                  _i64p, _i64p]
         L.ref_run_trial.restype = C.c_int
         L.ref_run_trial.argtypes = [_P(abi.Scenario), C.c_uint64, _P(abi.TrialOutcome), _dp, C.c_int64]
         L.ref_run_campaign.restype = C.c_int
@@ -400,6 +405,16 @@ class RefLib(_Lib):
         p = spec.flat()
         self._check(self.lib.ref_instance_build(C.byref(p), workers, C.byref(h)))
         return RefInstance(self, h)
+
+    def dubins_costs(self, x0s, x1s, dim: int, params):
+        x0s = abi.f64(x0s).reshape(-1, dim + 1)
+        x1s = abi.f64(x1s).reshape(-1, dim + 1)
+        m = x0s.shape[0]
+        cost, segs = np.zeros(m), np.zeros(m, np.int32)
+        self._check(self.lib.ref_dubins_costs(abi.ptr(x0s, C.c_double), abi.ptr(x1s, C.c_double), m, dim,
+                                              C.byref(params), abi.ptr(cost, C.c_double),
+                                              abi.ptr(segs, C.c_int32)))
+        return cost, segs
 
     # ---- simulator (simulator.cpp:66-227) ----------------------------------
     def run_trial(self, scenario, seed: int, path_cap: int = 100000):
@@ -543,6 +558,33 @@ class RefInstance:
     def __init__(self, lib: RefLib, h):
         self.lib = lib
         self.h = h
+
+    def graph(self, dim: int):
+        """The instance's NeighborGraph as a Graph with in-rows and cached
+        edge paths (directed Dubins graphs)."""
+        from paper_1705_02403_b200.graph import Graph
+        info = self.info()
+        n, E = info["n"], info["num_edges"]
+        coords, gidx, optr, ocol, ocost = self.download(dim)
+        npaths, npts = C.c_int64(), C.c_int64()
+        z = lambda t: abi.ptr(None, t)  # noqa: E731
+        self.lib._check(self.lib.lib.ref_instance_download_paths(self.h, z(C.c_int64), z(C.c_int32),
+                                                                 z(C.c_double), z(C.c_int32),
+                                                                 z(C.c_int32), z(C.c_int64),
+                                                                 z(C.c_double), C.byref(npaths),
+                                                                 C.byref(npts)))
+        iptr, icol, icost = np.zeros(n + 1, np.int64), np.zeros(max(E, 1), np.int32), np.zeros(max(E, 1))
+        ipath, opath = np.zeros(max(E, 1), np.int32), np.zeros(max(E, 1), np.int32)
+        pptr = np.zeros(npaths.value + 1, np.int64)
+        pts = np.zeros(max(npts.value, 1) * dim)
+        self.lib._check(self.lib.lib.ref_instance_download_paths(
+            self.h, abi.ptr(iptr, C.c_int64), abi.ptr(icol, C.c_int32), abi.ptr(icost, C.c_double),
+            abi.ptr(ipath, C.c_int32), abi.ptr(opath, C.c_int32), abi.ptr(pptr, C.c_int64),
+            abi.ptr(pts, C.c_double), C.byref(npaths), C.byref(npts)))
+        g = Graph(n, info["radius"], optr, ocol, ocost, dim=dim, directed=True, in_ptr=iptr,
+                  in_col=icol[:E], in_cost=icost[:E], out_path=opath[:E], in_path=ipath[:E],
+                  path_ptr=pptr, path_pts=pts[: npts.value * dim])
+        return coords, gidx, g
 
     def save_cache(self, file: str, key: int) -> bool:
         ok = C.c_int32()

@@ -173,6 +173,12 @@ ProblemFile to_problem(const gmt_problem* p) {
   f.eta = p->eta;
   if (p->radius_override > 0.0) f.radius_override = p->radius_override;
   f.sampling = to_src(&p->sampling);
+  if (p->steering == 1) {  // GMT_STEER_DUBINS_AIRPLANE
+    f.steering.kind = SteeringModel::Kind::dubins_airplane;
+    f.steering.rho = p->dubins.rho;
+    f.steering.discretization_step = p->dubins.discretization_step;
+    f.steering.planar_cost_only = p->dubins.planar_cost_only != 0;
+  }
   return f;
 }
 
@@ -388,6 +394,29 @@ int ref_instance_download(void* h, double* coords, int32_t* goal_idx, int64_t* o
   });
 }
 
+// ---- Dubins steering (steering.cpp:53-112) -----------------------------------
+// connect_cost and connect's segment count for state pairs (x, y[, z], heading).
+int ref_dubins_costs(const double* x0s, const double* x1s, int64_t count, int32_t dim,
+                     const gmt_dubins_params* prm, double* cost, int32_t* segments) {
+  return guard([&] {
+    SteeringModel m;
+    m.kind = SteeringModel::Kind::dubins_airplane;
+    m.rho = prm->rho;
+    m.discretization_step = prm->discretization_step;
+    m.planar_cost_only = prm->planar_cost_only != 0;
+    for (int64_t i = 0; i < count; ++i) {
+      State a, b;
+      a.coords.assign(x0s + i * (dim + 1), x0s + i * (dim + 1) + dim);
+      b.coords.assign(x1s + i * (dim + 1), x1s + i * (dim + 1) + dim);
+      a.heading = x0s[i * (dim + 1) + dim];
+      b.heading = x1s[i * (dim + 1) + dim];
+      Connection c = connect(a, b, m);
+      cost[i] = c.cost;
+      segments[i] = c.path.size() == 1 ? 0 : static_cast<int32_t>(c.path.size()) - 1;
+    }
+  });
+}
+
 // ---- simulator (simulator.cpp:66-227) ---------------------------------------
 ScenarioConfig to_scenario(const gmt_scenario* c) {
   ScenarioConfig cfg;
@@ -487,6 +516,46 @@ int ref_load_graph_cache(const char* file, uint64_t key, const double* coords, i
       }
       out_ptr[g->n] = e;
     }
+  });
+}
+
+// The directed part of an instance's graph: in-rows, path ids and the
+// cached edge paths (positions only).  NULL arrays: sizes only.
+int ref_instance_download_paths(void* h, int64_t* in_ptr, int32_t* in_col, double* in_cost,
+                                int32_t* in_path, int32_t* out_path, int64_t* path_ptr, double* path_pts,
+                                int64_t* num_paths, int64_t* num_points) {
+  return guard([&] {
+    auto* ri = static_cast<RefInstance*>(h);
+    const auto& g = ri->inst.graph;
+    const int d = ri->problem.dimension;
+    *num_paths = static_cast<int64_t>(g.paths.size());
+    int64_t pts = 0;
+    for (const auto& p : g.paths) pts += static_cast<int64_t>(p.size());
+    *num_points = pts;
+    if (!in_ptr) return;
+    int64_t e = 0;
+    for (int x = 0; x < g.n; ++x) {
+      in_ptr[x] = e;
+      for (const auto& ed : g.in[x]) {
+        in_col[e] = ed.other;
+        in_cost[e] = ed.cost;
+        in_path[e] = ed.path_id;
+        ++e;
+      }
+    }
+    in_ptr[g.n] = e;
+    e = 0;
+    for (int u = 0; u < g.n; ++u)
+      for (const auto& ed : g.out[u]) out_path[e++] = ed.path_id;
+    int64_t q = 0;
+    for (size_t p = 0; p < g.paths.size(); ++p) {
+      path_ptr[p] = q;
+      for (const auto& st : g.paths[p]) {
+        std::copy(st.coords.begin(), st.coords.begin() + d, path_pts + q * d);
+        ++q;
+      }
+    }
+    path_ptr[g.paths.size()] = q;
   });
 }
 
@@ -652,7 +721,8 @@ int ref_random_problem_get(void* h, double* box_lo, double* box_hi, double* goal
 extern "C" int ref_struct_sizes(int64_t* out, int32_t count) {
   const int64_t sizes[] = {sizeof(gmt_scene),     sizeof(gmt_sample_source), sizeof(gmt_graph_view),
                            sizeof(gmt_plan_out),  sizeof(gmt_plan_summary),  sizeof(gmt_problem),
-                           sizeof(gmt_di_params), sizeof(gmt_batch_host),    sizeof(gmt_quad_params)};
+                           sizeof(gmt_di_params), sizeof(gmt_batch_host),    sizeof(gmt_quad_params),
+                           sizeof(gmt_scenario),  sizeof(gmt_trial_outcome), sizeof(gmt_dubins_params)};
   const int32_t n = static_cast<int32_t>(sizeof(sizes) / sizeof(sizes[0]));
   for (int32_t i = 0; i < count && i < n; ++i) out[i] = sizes[i];
   return n;

@@ -112,6 +112,7 @@ class PlanSummary(C.Structure):
 
 
 STEER_EUCLIDEAN = 0
+STEER_DUBINS_AIRPLANE = 1
 STEER_DOUBLE_INTEGRATOR = 2
 STEER_QUADROTOR = 3
 
@@ -140,6 +141,16 @@ class QuadParams(C.Structure):
     ]
 
 
+class DubinsParams(C.Structure):
+    """gmt_dubins_params (SteeringModel, steering.hpp:9-23)."""
+    _fields_ = [
+        ("rho", C.c_double),
+        ("discretization_step", C.c_double),
+        ("planar_cost_only", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
 class Problem(C.Structure):
     _fields_ = [
         ("scene", Scene),
@@ -155,6 +166,7 @@ class Problem(C.Structure):
         ("reserved", C.c_int32),
         ("di", DiParams),
         ("quad", QuadParams),
+        ("dubins", DubinsParams),
     ]
 
 

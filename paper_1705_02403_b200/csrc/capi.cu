@@ -120,7 +120,8 @@ extern "C" int gmt_abi_version(void) { return GMT_B200_ABI_VERSION; }
 extern "C" int gmt_struct_sizes(int64_t* out, int32_t count) {
   const int64_t sizes[] = {sizeof(gmt_scene),        sizeof(gmt_sample_source), sizeof(gmt_graph_view),
                            sizeof(gmt_plan_out),     sizeof(gmt_plan_summary),  sizeof(gmt_problem),
-                           sizeof(gmt_di_params),    sizeof(gmt_batch_host),    sizeof(gmt_quad_params)};
+                           sizeof(gmt_di_params),    sizeof(gmt_batch_host),    sizeof(gmt_quad_params),
+                           sizeof(gmt_scenario),     sizeof(gmt_trial_outcome), sizeof(gmt_dubins_params)};
   const int32_t n = static_cast<int32_t>(sizeof(sizes) / sizeof(sizes[0]));
   for (int32_t i = 0; i < count && i < n; ++i) out[i] = sizes[i];
   return n;
@@ -185,6 +186,7 @@ extern "C" void gmt_ctx_destroy(gmt_ctx* ctx) {
     ctx->plan_inst.desc_mem.release();
     ctx->plan_inst.aux.release();
     ctx->plan_inst.mem2.release();
+    ctx->plan_inst.mem3.release();
   }
   cudaStreamSynchronize(ctx->stream);
   ctx->pinned.release();

@@ -16,10 +16,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 #include "di.cuh"
 #include "quad.cuh"
+#include "dubins.cuh"
 #include "internal.cuh"
 #include "offline.cuh"
 
@@ -72,6 +74,36 @@ struct QuadModel {
     return quad_coord(a, b, tau, k, i, P);
   }
   int segments() const { return P.segments; }
+};
+
+// Dubins airplane (dubins.cuh) over augmented states (x, y[, z], heading);
+// `tau` carries connect()'s segment count (0 = degenerate pair).
+template <int PD>
+struct DubinsModel {
+  static constexpr int kDim = PD + 1;
+  DubinsParams P;
+  double radius;
+  // within_radius's straight-line lower bound (steering.cpp:114-121),
+  // widened by 1e-12 relative: it only prunes pairs the cost test rejects.
+  __device__ bool may(const double* a, const double* b) const {
+    double sq = 0.0;
+    const int m = P.planar_cost_only ? 2 : PD;
+    for (int k = 0; k < m; ++k) {
+      const double d = a[k] - b[k];
+      sq += d * d;
+    }
+    return sqrt(sq) <= radius * (1.0 + 1e-12);
+  }
+  __device__ double cost_tau(const double* a, const double* b, double* t) const {
+    int segs;
+    DubinsPath path;
+    double dz;
+    const double c = dubins_connect(a, a[PD], b, b[PD], P, &segs, &path, &dz);
+    *t = static_cast<double>(segs);
+    return c;
+  }
+  __device__ double coord(const double*, const double*, double, int, int) const { return 0.0; }
+  int segments() const { return 0; }
 };
 
 // SWAP = false: row r lists targets c with cost(r -> c) <= radius.
@@ -201,6 +233,50 @@ __global__ void __launch_bounds__(1024) scan_rows_kernel(const int64_t* __restri
     __syncthreads();
   }
   if (tid == 0) row_ptr[n] = carry;
+}
+
+// Dubins edge paths (graph.cpp:152-156, 172-183): path e = out-edge e,
+// segments + 1 states (the degenerate pair: its single state); positions
+// only (the lazy check reads coordinates).
+__global__ void dubins_path_count_kernel(const double* __restrict__ out_tau, int64_t E,
+                                         int64_t* __restrict__ counts) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < E;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int segs = static_cast<int>(out_tau[e]);
+    counts[e] = segs == 0 ? 1 : segs + 1;
+  }
+}
+
+template <int PD>
+__global__ void dubins_path_fill_kernel(const double* __restrict__ aug, const int64_t* __restrict__ out_ptr,
+                                        const int32_t* __restrict__ out_col, int n, DubinsParams P,
+                                        const int64_t* __restrict__ path_ptr, double* __restrict__ pts,
+                                        int32_t* __restrict__ out_path) {
+  for (int u = blockIdx.x; u < n; u += gridDim.x) {
+    const double* a = aug + static_cast<int64_t>(u) * (PD + 1);
+    for (int64_t e = out_ptr[u] + threadIdx.x; e < out_ptr[u + 1]; e += blockDim.x) {
+      out_path[e] = static_cast<int32_t>(e);
+      const double* b = aug + static_cast<int64_t>(out_col[e]) * (PD + 1);
+      int segs;
+      DubinsPath path;
+      double dz;
+      dubins_connect(a, a[PD], b, b[PD], P, &segs, &path, &dz);
+      double* out = pts + path_ptr[e] * PD;
+      if (segs == 0) {
+        for (int k = 0; k < PD; ++k) out[k] = a[k];
+        continue;
+      }
+      for (int i = 0; i <= segs; ++i) dubins_waypoint(a, b, path, dz, segs, i, P, out + i * PD);
+    }
+  }
+}
+
+__global__ void augment_kernel(const double* __restrict__ coords, const double* __restrict__ heading, int n,
+                               int pd, double* __restrict__ aug) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    for (int k = 0; k < pd; ++k) aug[static_cast<int64_t>(i) * (pd + 1) + k] = coords[static_cast<int64_t>(i) * pd + k];
+    aug[static_cast<int64_t>(i) * (pd + 1) + pd] = heading[i];
+  }
 }
 
 template <class Model>
@@ -439,6 +515,104 @@ int build_quad_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const gmt_
   return build_kino_graph_dev(ctx, d_coords, n, quad_model(p, radius), radius, out_mem, out, in_mem, in);
 }
 
+DubinsParams to_dubins(const gmt_dubins_params* p, int pd) {
+  DubinsParams P;
+  P.rho = p->rho;
+  P.step = p->discretization_step > 0.0 ? p->discretization_step : p->rho / 10.0;  // step()
+  P.planar_cost_only = p->planar_cost_only != 0;
+  P.dim = pd;
+  return P;
+}
+
+int validate_dubins(const gmt_dubins_params* p, int pd) {
+  if (!p) return set_error(GMT_E_INVALID_INPUT, "dubins parameters are null");
+  if (pd != 2 && pd != 3) return set_error(GMT_E_INVALID_INPUT, "dubins steering needs 2 or 3 position coordinates");
+  if (!(p->rho > 0.0)) return set_error(GMT_E_INVALID_INPUT, "dubins turning radius must be positive");
+  return GMT_OK;
+}
+
+// The directed Dubins graph of device samples (positions + headings):
+// out-/in-rows as build_kino_graph_dev, plus every out-edge's path.
+int build_dubins_graph_dev(gmt_ctx* ctx, const double* d_coords, const double* d_heading, int n, int pd,
+                           const gmt_dubins_params* p, double radius, Arena& out_mem, DiRows* out,
+                           Arena& in_mem, DiRows* in, Arena& path_mem, DubinsGraphPaths* paths) {
+  int rc = validate_dubins(p, pd);
+  if (rc) return rc;
+  const DubinsParams P = to_dubins(p, pd);
+  cudaStream_t s = ctx->stream;
+  Arena aug;
+  rc = aug.reserve(sizeof(double) * static_cast<size_t>(n) * (pd + 1));
+  if (rc) return rc;
+  augment_kernel<<<std::max(1, std::min((n + 255) / 256, 1024)), 256, 0, s>>>(d_coords, d_heading, n, pd,
+                                                                            static_cast<double*>(aug.ptr));
+  GMT_CUDA(cudaGetLastError());
+  ++ctx->launches;
+  const double* A = static_cast<const double*>(aug.ptr);
+  if (pd == 2) {
+    DubinsModel<2> m{P, radius};
+    rc = build_kino_graph_dev(ctx, A, n, m, radius, out_mem, out, in_mem, in);
+  } else {
+    DubinsModel<3> m{P, radius};
+    rc = build_kino_graph_dev(ctx, A, n, m, radius, out_mem, out, in_mem, in);
+  }
+  if (rc) {
+    aug.release();
+    return rc;
+  }
+  const int64_t E = out->edges;
+  Arena cnt;
+  rc = cnt.reserve(sizeof(int64_t) * (E + 1));
+  if (rc) {
+    aug.release();
+    return rc;
+  }
+  int64_t* counts = static_cast<int64_t*>(cnt.ptr);
+  const int eb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((E + 255) / 256, 4096)));
+  dubins_path_count_kernel<<<eb, 256, 0, s>>>(out->tau, E, counts);
+  // path_ptr [E+1], in_path [E], out_path [E], then the points
+  const size_t o_pp = 0;
+  const size_t o_ip = align16(sizeof(int64_t) * (E + 1));
+  const size_t o_op = o_ip + align16(sizeof(int32_t) * E);
+  const size_t o_pts = o_op + align16(sizeof(int32_t) * E);
+  Arena pp;
+  rc = pp.reserve(sizeof(int64_t) * (E + 1));
+  if (rc == GMT_OK) {
+    scan_rows_kernel<<<1, 1024, 0, s>>>(counts, static_cast<int>(E), static_cast<int64_t*>(pp.ptr));
+    GMT_CUDA(cudaGetLastError());
+    ctx->launches += 2;
+    int64_t total = 0;
+    GMT_CUDA(cudaMemcpyAsync(&total, static_cast<int64_t*>(pp.ptr) + E, sizeof(total), cudaMemcpyDeviceToHost, s));
+    GMT_CUDA(cudaStreamSynchronize(s));
+    rc = path_mem.reserve(o_pts + sizeof(double) * static_cast<size_t>(total) * pd + 16);
+    if (rc == GMT_OK) {
+      char* b = static_cast<char*>(path_mem.ptr);
+      paths->path_ptr = reinterpret_cast<int64_t*>(b + o_pp);
+      paths->in_path = reinterpret_cast<int32_t*>(b + o_ip);
+      paths->out_path = reinterpret_cast<int32_t*>(b + o_op);
+      paths->pts = reinterpret_cast<double*>(b + o_pts);
+      paths->num_points = total;
+      GMT_CUDA(cudaMemcpyAsync(paths->path_ptr, pp.ptr, sizeof(int64_t) * (E + 1), cudaMemcpyDeviceToDevice, s));
+      const int nb = std::max(1, std::min(n, 4096));
+      if (pd == 2)
+        dubins_path_fill_kernel<2><<<nb, 128, 0, s>>>(A, out->ptr, out->col, n, P, paths->path_ptr, paths->pts,
+                                                      paths->out_path);
+      else
+        dubins_path_fill_kernel<3><<<nb, 128, 0, s>>>(A, out->ptr, out->col, n, P, paths->path_ptr, paths->pts,
+                                                      paths->out_path);
+      GMT_CUDA(cudaGetLastError());
+      in_path_kernel<<<std::max(1, std::min((n + 255) / 256, 1024)), 256, 0, s>>>(in->ptr, in->col, out->ptr,
+                                                                             out->col, n, paths->in_path);
+      GMT_CUDA(cudaGetLastError());
+      ctx->launches += 2;
+      GMT_CUDA(cudaStreamSynchronize(s));
+    }
+  }
+  pp.release();
+  cnt.release();
+  aug.release();
+  return rc;
+}
+
 }  // namespace gmtb
 
 using namespace gmtb;
@@ -482,3 +656,21 @@ extern "C" int gmt_build_quad_graph(gmt_ctx* ctx, const double* coords, int32_t 
   return build_kino_graph_host(ctx, coords, n, quad_model(params, radius), radius, num_edges, out_ptr,
                                out_col, out_cost, out_tau, in_ptr, in_col, in_cost, in_path, path_pts);
 }
+
+extern "C" int gmt_dubins_costs(gmt_ctx* ctx, const double* x0s, const double* x1s, int64_t count, int32_t dim,
+                                const gmt_dubins_params* params, double* cost_out, int32_t* segments_out) {
+  gmtb::AllocScope alloc_scope_(ctx);
+  int rc = validate_dubins(params, dim);
+  if (rc) return rc;
+  if (count <= 0) return GMT_OK;
+  std::vector<double> segs(static_cast<size_t>(count));
+  const DubinsParams P = to_dubins(params, dim);
+  if (dim == 2)
+    rc = kino_costs(ctx, x0s, x1s, count, DubinsModel<2>{P, 0.0}, cost_out, segs.data());
+  else
+    rc = kino_costs(ctx, x0s, x1s, count, DubinsModel<3>{P, 0.0}, cost_out, segs.data());
+  if (rc) return rc;
+  for (int64_t i = 0; i < count; ++i) segments_out[i] = static_cast<int32_t>(segs[i]);
+  return GMT_OK;
+}
+

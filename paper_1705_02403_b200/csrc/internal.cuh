@@ -64,6 +64,7 @@ struct gmt_instance {
   gmtb::Arena desc_mem;  // the device copy of `desc`
   gmtb::Arena aux;       // device-built instances: goal index list etc.
   gmtb::Arena mem2;      // device-built directed graphs: the in-rows
+  gmtb::Arena mem3;      // device-built Dubins graphs: edge paths
   gmtb::DevInstance desc{};
   int32_t graph_n = 0;
   const int32_t* goal_idx_dev = nullptr;
@@ -72,6 +73,7 @@ struct gmt_instance {
     desc_mem.release();
     aux.release();
     mem2.release();
+    mem3.release();
   }
 };
 

@@ -44,6 +44,19 @@ int build_di_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const gmt_di
 int build_quad_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const gmt_quad_params* p,
                          double radius, Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in);
 
+// Dubins-airplane graphs (di_graph.cu): rows as above plus edge paths.
+struct DubinsGraphPaths {
+  int64_t* path_ptr = nullptr;  // [E+1], path e = out-edge e
+  int32_t* in_path = nullptr;   // [E] in-edge -> path id
+  int32_t* out_path = nullptr;  // [E] identity
+  double* pts = nullptr;        // [num_points * dim] positions
+  int64_t num_points = 0;
+};
+int validate_dubins(const gmt_dubins_params* p, int pd);
+int build_dubins_graph_dev(gmt_ctx* ctx, const double* d_coords, const double* d_heading, int n, int pd,
+                           const gmt_dubins_params* p, double radius, Arena& out_mem, DiRows* out,
+                           Arena& in_mem, DiRows* in, Arena& path_mem, DubinsGraphPaths* paths);
+
 // GMTG v1 graph cache (cache.cu).
 int problem_key_of(const gmt_problem* p, uint64_t* out);
 int cache_write(const char* file, uint64_t key, int32_t n, double radius, const int64_t* ptr,

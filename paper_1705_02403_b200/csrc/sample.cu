@@ -613,9 +613,17 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
   const int d = scene->dim, nb = scene->num_boxes;
   int rc = validate_scene(scene);
   if (rc) return rc;
+  const bool dubins = p->steering == GMT_STEER_DUBINS_AIRPLANE;
+  // build_instance samples headings exactly for Dubins problems (problem.cpp:338-339).
+  gmt_sample_source src = p->sampling;
+  src.with_heading = dubins ? 1 : 0;
+  if (dubins) {
+    rc = validate_dubins(&p->dubins, d);
+    if (rc) return rc;
+  }
   Arena samples;
   DevSamples S;
-  rc = sample_free_dev(ctx, p->n, scene, &p->sampling, samples, &S);
+  rc = sample_free_dev(ctx, p->n, scene, &src, samples, &S);
   if (rc) return rc;
   int32_t init_index = -1;
   rc = append_init_dev(ctx, d, &S, p->init, p->init_has_heading, p->init_heading, scene->goal_lo,
@@ -626,7 +634,7 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
   }
   const bool quad = p->steering == GMT_STEER_QUADROTOR;
   const bool di = p->steering == GMT_STEER_DOUBLE_INTEGRATOR || quad;  // kinodynamic, directed
-  if (p->steering != GMT_STEER_EUCLIDEAN && !di) {
+  if (p->steering != GMT_STEER_EUCLIDEAN && !di && !dubins) {
     samples.release();
     return set_error(GMT_E_INVALID_INPUT, "unsupported steering model");
   }
@@ -644,7 +652,8 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
       return rc;
     }
   }
-  Arena g, g2;
+  Arena g, g2, g3;
+  DubinsGraphPaths dpaths;
   int64_t E = 0, *rp = nullptr;
   int32_t* col = nullptr;
   double* cost = nullptr;
@@ -653,7 +662,7 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
   bool hit = false;
   uint64_t key = 0;
   if (cache_file) {
-    if (di) {
+    if (di || dubins) {
       samples.release();
       return set_error(GMT_E_INVALID_INPUT, "the graph cache covers the Euclidean steering model only");
     }
@@ -690,6 +699,13 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
   }
   if (hit) {
     // graph supplied by the cache file
+  } else if (dubins) {
+    rc = build_dubins_graph_dev(ctx, S.coords, S.heading, S.n, d, &p->dubins, radius, g, &dout, g2, &din, g3,
+                                &dpaths);
+    E = dout.edges;
+    rp = dout.ptr;
+    col = dout.col;
+    cost = dout.cost;
   } else if (di) {
     if (d != (quad ? kQuadDim : kDiDim)) {
       samples.release();
@@ -714,6 +730,7 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
     samples.release();
     g.release();
     g2.release();
+    g3.release();
     return rc;
   }
   auto* inst = new gmt_instance;
@@ -785,6 +802,17 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
         D.kin_p[1] = p->di.weight;
       }
     }
+    if (dubins) {
+      D.directed = 1;
+      D.in_ptr = din.ptr;
+      D.in_col = din.col;
+      D.in_cost = din.cost;
+      D.in_path = dpaths.in_path;
+      D.out_path = dpaths.out_path;
+      D.path_ptr = dpaths.path_ptr;
+      D.path_pts = dpaths.pts;
+      D.steering = GMT_STEER_DUBINS_AIRPLANE;
+    }
     inst->goal_idx_dev = reinterpret_cast<const int32_t*>(b + o_gidx);
     inst->graph_n = n;
   }
@@ -794,6 +822,8 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
     g.ptr = nullptr;
     inst->mem2 = g2;
     g2.ptr = nullptr;
+    inst->mem3 = g3;
+    g3.ptr = nullptr;
     rc = push_desc(ctx, inst);
     if (rc == GMT_OK) {
       cudaError_t e = cudaStreamSynchronize(s);
@@ -803,6 +833,7 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
   if (rc != GMT_OK) {
     g.release();
     g2.release();
+    g3.release();
     delete inst;
     return rc;
   }

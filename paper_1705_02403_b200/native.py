@@ -53,6 +53,8 @@ SIGNATURES = [
     ("gmt_build_di_graph", C.c_int, [_vp, _dp, C.c_int32, _P(abi.DiParams), C.c_double, _i64p,
                                      _i64p, _i32p, _dp, _dp, _i64p, _i32p, _dp, _i32p, _dp]),
     ("gmt_problem_key", C.c_int, [_P(abi.Problem), _P(C.c_uint64)]),
+    ("gmt_dubins_costs", C.c_int, [_vp, _dp, _dp, C.c_int64, C.c_int32, _P(abi.DubinsParams), _dp,
+                                   _i32p]),
     ("gmt_run_trial", C.c_int, [_vp, _P(abi.Scenario), C.c_uint64, _P(abi.TrialOutcome), _dp,
                                 C.c_int64]),
     ("gmt_run_campaign", C.c_int, [C.c_int, _P(abi.Scenario), _dp, C.c_int32, _dp, C.c_int32, _dp,
@@ -300,6 +302,17 @@ class Context:
         """Directed DI graph (out-rows, in-rows, optional waypoint paths) as a
         reference-shaped Graph: path ids = out-edge indices."""
         return self._kino_graph(lib().gmt_build_di_graph, 6, coords, params, radius, paths)
+
+    # ---- Dubins airplane (steering.cpp:53-112) ------------------------------
+    def dubins_costs(self, x0s, x1s, dim: int, params: abi.DubinsParams):
+        """connect_cost and segment counts of (x, y[, z], heading) state pairs."""
+        x0s = abi.f64(x0s).reshape(-1, dim + 1)
+        x1s = abi.f64(x1s).reshape(-1, dim + 1)
+        m = x0s.shape[0]
+        cost, segs = np.zeros(m), np.zeros(m, np.int32)
+        check(lib().gmt_dubins_costs(self.h, abi.ptr(x0s, C.c_double), abi.ptr(x1s, C.c_double), m, dim,
+                                     C.byref(params), abi.ptr(cost, C.c_double), abi.ptr(segs, C.c_int32)))
+        return cost, segs
 
     # ---- quadrotor (NEW model, DESIGN.md §3.3) ------------------------------
     def quad_costs(self, x0s, x1s, params: abi.QuadParams):

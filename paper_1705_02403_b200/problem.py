@@ -84,6 +84,10 @@ class ProblemSpec:
     quad_ymax: float = math.pi
     quad_wmax: float = 1.0
     quad_weight: float = 0.1
+    init_heading: float | None = None  # Dubins problems (State::heading)
+    dubins_rho: float = 0.1
+    dubins_step: float = 0.0
+    dubins_planar: bool = False
     quad_segments: int = 8
     _keep: list = field(default_factory=list, repr=False)
 
@@ -122,7 +126,7 @@ class ProblemSpec:
     def source(self) -> abi.SampleSource:
         s = abi.SampleSource()
         s.kind = self.sampling_kind
-        s.with_heading = 0
+        s.with_heading = 1 if self.steering == abi.STEER_DUBINS_AIRPLANE else 0  # problem.cpp:197
         s.start_index = self.start_index
         s.seed = self.seed
         return s
@@ -133,8 +137,8 @@ class ProblemSpec:
         init = abi.f64(self.init)
         self._keep.append(init)
         p.init = abi.ptr(init, abi.C.c_double)
-        p.init_has_heading = 0
-        p.init_heading = 0.0
+        p.init_has_heading = 0 if self.init_heading is None else 1
+        p.init_heading = 0.0 if self.init_heading is None else float(self.init_heading)
         p.n = self.n
         p.lambda_ = self.lam
         p.eta = self.eta
@@ -144,7 +148,14 @@ class ProblemSpec:
         p.reserved = 0
         p.di = self.di_params()
         p.quad = self.quad_params()
+        p.dubins = self.dubins_params()
         return p
+
+    def dubins_params(self) -> abi.DubinsParams:
+        d = abi.DubinsParams()
+        d.rho, d.discretization_step = self.dubins_rho, self.dubins_step
+        d.planar_cost_only, d.reserved = int(self.dubins_planar), 0
+        return d
 
     def with_n(self, n: int) -> "ProblemSpec":
         q = ProblemSpec(**{k: getattr(self, k) for k in self.__dataclass_fields__ if k != "_keep"})
@@ -240,8 +251,9 @@ def _parse_box(v, path, dim):
 
 
 def parse_problem(text: str) -> ProblemSpec:
-    """parse_problem (problem.cpp:102-223) for the euclidean model.  The
-    dubins_airplane model parses but is rejected: it is a §8(f) "next" row."""
+    """parse_problem (problem.cpp:102-223): euclidean and dubins_airplane
+    steering (the latter with its rho / discretization_step /
+    planar_cost_only fields and a required init heading)."""
     try:
         doc = json.loads(text)
     except json.JSONDecodeError as e:
@@ -259,6 +271,7 @@ def parse_problem(text: str) -> ProblemSpec:
     if dim < 1:
         _fail("dimension", "must be at least 1")
     steering = _member(doc, "", "steering")
+    dubins = {}
     if not isinstance(steering, dict):
         _fail("steering", "expected an object")
     _reject_unknown(steering, "steering", ("model", "rho", "discretization_step", "planar_cost_only"))
@@ -269,9 +282,23 @@ def parse_problem(text: str) -> ProblemSpec:
         for key in ("rho", "discretization_step", "planar_cost_only"):
             if key in steering:
                 _fail(f"steering.{key}", "only the dubins_airplane model uses this field")
-    elif model == "dubins_airplane":
-        raise InvalidInputError("steering.model: dubins_airplane is not supported by the B200 "
-                                "build yet (SURVEY.md §8(f) row 1)")
+    elif model == "dubins_airplane":  # problem.cpp:132-151
+        if dim not in (2, 3):
+            _fail("dimension", "dubins_airplane needs dimension 2 or 3")
+        if "rho" in steering:
+            rho = _as_double(steering["rho"], "steering.rho")
+            if not rho > 0.0:
+                _fail("steering.rho", "must be positive")
+            dubins["rho"] = rho
+        if "discretization_step" in steering:
+            st = _as_double(steering["discretization_step"], "steering.discretization_step")
+            if st < 0.0:
+                _fail("steering.discretization_step", "must be non-negative")
+            dubins["step"] = st
+        if "planar_cost_only" in steering:
+            if not isinstance(steering["planar_cost_only"], bool):
+                _fail("steering.planar_cost_only", "expected a boolean")
+            dubins["planar"] = steering["planar_cost_only"]
     else:
         _fail("steering.model", 'expected "euclidean" or "dubins_airplane"')
     obstacles = _member(doc, "", "obstacles")
@@ -289,14 +316,26 @@ def parse_problem(text: str) -> ProblemSpec:
         _fail("init", "expected an object with coords")
     _reject_unknown(init, "init", ("coords", "heading"))
     init_c = _as_vector(_member(init, "init", "coords"), "init.coords", dim)
-    if "heading" in init:
-        _fail("init.heading", "only the dubins_airplane model uses a heading")
+    is_dubins = steering.get("model") == "dubins_airplane"
+    init_heading = None
+    if "heading" in init:  # problem.cpp:165-173
+        if not is_dubins:
+            _fail("init.heading", "only the dubins_airplane model uses a heading")
+        init_heading = _as_double(init["heading"], "init.heading")
+    elif is_dubins:
+        _fail("init.heading", "required field is missing")
     goal_lo, goal_hi = _parse_box(_member(doc, "", "goal"), "goal", dim)
     n = _as_int(_member(doc, "", "n"), "n")
     if n < 1:
         _fail("n", "must be at least 1")
     spec = ProblemSpec(dim=dim, box_lo=box_lo, box_hi=box_hi, goal_lo=goal_lo, goal_hi=goal_hi,
                        init=init_c, n=n)
+    if is_dubins:
+        spec.steering = abi.STEER_DUBINS_AIRPLANE
+        spec.init_heading = init_heading
+        spec.dubins_rho = dubins.get("rho", 0.1)
+        spec.dubins_step = dubins.get("step", 0.0)
+        spec.dubins_planar = bool(dubins.get("planar", False))
     if not spec.point_free(init_c):
         _fail("init", "start state is not in free space")
     if "lambda" in doc:

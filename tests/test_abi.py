@@ -71,7 +71,7 @@ def test_missing_library_raises(monkeypatch, tmp_path):
 
 
 ABI_STRUCTS = ("Scene", "SampleSource", "GraphView", "PlanOut", "PlanSummary", "Problem",
-               "DiParams", "BatchHost", "QuadParams")
+               "DiParams", "BatchHost", "QuadParams", "Scenario", "TrialOutcome", "DubinsParams")
 
 
 def _sizes(fn):
