@@ -215,23 +215,24 @@ GMT_HD double quad_pow(double t, int e) {
 }
 
 // Coordinate idx (0..11) of waypoint k (0..M) of the optimal trajectory.
-GMT_HD double quad_coord(const double* x0, const double* x1, double tau, int k, int idx,
-                         const QuadParams& P) {
-  const int M = P.segments;
-  if (k <= 0 || tau == 0.0) return x0[idx];
-  if (k >= M) return x1[idx];
-  int c = 0, i = 0;
+// Chain and component of normalised coordinate idx.
+GMT_HD void quad_locate(int idx, int* c, int* i) {
+  *c = 0;
+  *i = 0;
   for (int cc = 0; cc < 4; ++cc)
     for (int ii = 0; ii < quad_chain_order(cc); ++ii)
-      if (quad_coord_index(cc, ii) == idx) c = cc, i = ii;
+      if (quad_coord_index(cc, ii) == idx) *c = cc, *i = ii;
+}
+
+// Per-edge, per-chain part of the trajectory: the chain's start state z0 and
+// lambda = G^-1 d, G^-1_jl = H^-1_jl / tau^(2m - j - l - 1).
+GMT_HD void quad_chain_lambda(const double* x0, const double* x1, double tau, int c, const QuadParams& P,
+                              double* z0, double* lam) {
   const int m = quad_chain_order(c);
-  const double t = di_div(di_mul(tau, static_cast<double>(k)), static_cast<double>(M));
-  double z0[4], z1[4], delta[4][4];
+  double z1[4], delta[4][4], d[4];
   quad_chain_state(x0, c, P, z0);
   quad_chain_state(x1, c, P, z1);
   quad_delta(z0, z1, m, delta);
-  // lambda = G^-1 d, G^-1_jl = H^-1_jl / tau^(2m - j - l - 1)
-  double d[4], lam[4];
   for (int j = 0; j < m; ++j) {
     double v = 0.0;
     for (int p = m - j - 1; p >= 0; --p) v = di_add(di_mul(v, tau), delta[j][p]);
@@ -243,8 +244,15 @@ GMT_HD double quad_coord(const double* x0, const double* x1, double tau, int k, 
       v = di_add(v, di_div(di_mul(quad_hinv(m, j, l), d[l]), quad_pow(tau, 2 * m - j - l - 1)));
     lam[j] = v;
   }
-  // z_i(t) = (e^(A t) z0)_i + sum_j lam_j I(a = m-1-i, b = m-1-j), with
-  // I(a,b) = sum_{r=0..b} (tau-t)^(b-r)/(b-r)! t^(a+r+1) / ((a+r+1) a! r!)
+}
+
+// Component i of chain c at waypoint k (0 < k < M) from quad_chain_lambda's
+// z0 / lambda:  z_i(t) = (e^(A t) z0)_i + sum_j lam_j I(a = m-1-i, b = m-1-j),
+// I(a,b) = sum_{r=0..b} (tau-t)^(b-r)/(b-r)! t^(a+r+1) / ((a+r+1) a! r!).
+GMT_HD double quad_chain_coord(const double* z0, const double* lam, double tau, int k, int c, int i,
+                               const QuadParams& P) {
+  const int m = quad_chain_order(c);
+  const double t = di_div(di_mul(tau, static_cast<double>(k)), static_cast<double>(P.segments));
   double zi = 0.0;
   for (int q = m - 1; q >= i; --q) zi = di_add(zi, di_div(di_mul(z0[q], quad_pow(t, q - i)), quad_fact(q - i)));
   const int a = m - 1 - i;
@@ -260,6 +268,19 @@ GMT_HD double quad_coord(const double* x0, const double* x1, double tau, int k, 
     zi = di_add(zi, di_mul(lam[j], I));
   }
   return quad_chain_to_norm(c, i, zi, P);
+}
+
+// Coordinate idx (0..11) of waypoint k (0..M) of the optimal trajectory.
+GMT_HD double quad_coord(const double* x0, const double* x1, double tau, int k, int idx,
+                         const QuadParams& P) {
+  const int M = P.segments;
+  if (k <= 0 || tau == 0.0) return x0[idx];
+  if (k >= M) return x1[idx];
+  int c, i;
+  quad_locate(idx, &c, &i);
+  double z0[4], lam[4];
+  quad_chain_lambda(x0, x1, tau, c, P, z0, lam);
+  return quad_chain_coord(z0, lam, tau, k, c, i, P);
 }
 
 // Necessary condition for cost(x0 -> x1) <= r: for every chain component,

@@ -190,10 +190,8 @@ __device__ __forceinline__ bool any_box_contains(const double* p, int d, const B
 // 2^-53 |lo|, which only matters for |lo| > 1 where lo - b > 1 anyway.)
 // Boxes that pass the pre-test go through the exact clip.
 template <int D>
-__device__ bool segment_free_staged(int d_rt, const Boxes& bx, int lane, const double* seg) {
+__device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const double* a, const double* b) {
   const int d = dims<D>(d_rt);
-  const double* a = seg;
-  const double* b = seg + 16;
   bool eq = true, cube_a = true, cube_b = true;
   if (lane < d) {
     const double x = a[lane], y = b[lane];
@@ -295,6 +293,11 @@ __device__ bool segment_free_staged(int d_rt, const Boxes& bx, int lane, const d
 }
 
 template <int D>
+__device__ __forceinline__ bool segment_free_staged(int d_rt, const Boxes& bx, int lane, const double* seg) {
+  return segment_free_ab<D>(d_rt, bx, lane, seg, seg + 16);
+}
+
+template <int D>
 __device__ bool segment_free_warp(const double* A, const double* B, int d, const Boxes& bx,
                                   int lane, double* seg) {
   __syncwarp();
@@ -336,7 +339,8 @@ __device__ bool polyline_free_warp(const DevInstance& I, int d, const Boxes& bx,
 // segment_free_staged.
 template <int D>
 __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int from, int to,
-                                    double tau, int lane, double* seg) {
+                                    double tau, int lane, double* seg, double* tab = nullptr,
+                                    int tab_cap = 0) {
   // Only the generic-dimension kernel can see a 12D quadrotor instance.
   const bool quad = D == 0 && I.steering == GMT_STEER_QUADROTOR;
   const int dim = quad ? kQuadDim : kDiDim;
@@ -344,33 +348,56 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
   const double* x1 = I.coords + static_cast<int64_t>(to) * dim;
   if (tau == 0.0) return point_free_warp<D>(x0, dim, bx, lane, seg);
   const int M = I.kin_segments;
+  QuadParams QP;
+  DiParams DP;
+  if (quad) {
+    QP.g = I.kin_p[0];
+    QP.vmax = I.kin_p[1];
+    QP.amax = I.kin_p[2];
+    QP.ymax = I.kin_p[3];
+    QP.wmax = I.kin_p[4];
+    QP.weight = I.kin_p[5];
+    QP.segments = M;
+    QP.reserved = 0;
+  } else {
+    DP.vmax = I.kin_p[0];
+    DP.weight = I.kin_p[1];
+    DP.segments = M;
+    DP.reserved = 0;
+  }
+  if (tab && (M + 1) * dim <= tab_cap) {
+    // Waypoint table: every waypoint once, lane-parallel over (waypoint,
+    // coordinate); the quadrotor's per-chain lambda first (lanes 0-3, into
+    // the seg scratch).  Same arithmetic as di_coord / quad_coord.
+    __syncwarp();
+    if (quad && lane < 4) quad_chain_lambda(x0, x1, tau, lane, QP, seg + 8 * lane, seg + 8 * lane + 4);
+    __syncwarp();
+    for (int e = lane; e < (M + 1) * dim; e += kWarp) {
+      const int k = e / dim, i = e - k * dim;
+      double v;
+      if (k == 0) {
+        v = x0[i];
+      } else if (k == M) {
+        v = x1[i];
+      } else if (quad) {
+        int c, ci;
+        quad_locate(i, &c, &ci);
+        v = quad_chain_coord(seg + 8 * c, seg + 8 * c + 4, tau, k, c, ci, QP);
+      } else {
+        v = di_coord(x0, x1, tau, k, i, DP);
+      }
+      tab[e] = v;
+    }
+    __syncwarp();
+    for (int s = 0; s < M; ++s)
+      if (!segment_free_ab<D>(dim, bx, lane, tab + s * dim, tab + (s + 1) * dim)) return false;
+    return true;
+  }
   const int i = lane & 15;
   const int k = lane >> 4;
   for (int s = 0; s < M; ++s) {
     __syncwarp();
-    if (i < dim) {
-      double v;
-      if (quad) {
-        QuadParams P;
-        P.g = I.kin_p[0];
-        P.vmax = I.kin_p[1];
-        P.amax = I.kin_p[2];
-        P.ymax = I.kin_p[3];
-        P.wmax = I.kin_p[4];
-        P.weight = I.kin_p[5];
-        P.segments = M;
-        P.reserved = 0;
-        v = quad_coord(x0, x1, tau, s + k, i, P);
-      } else {
-        DiParams P;
-        P.vmax = I.kin_p[0];
-        P.weight = I.kin_p[1];
-        P.segments = M;
-        P.reserved = 0;
-        v = di_coord(x0, x1, tau, s + k, i, P);
-      }
-      seg[lane] = v;
-    }
+    if (i < dim) seg[lane] = quad ? quad_coord(x0, x1, tau, s + k, i, QP) : di_coord(x0, x1, tau, s + k, i, DP);
     __syncwarp();
     if (!segment_free_staged<D>(dim, bx, lane, seg)) return false;
   }
@@ -440,6 +467,9 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   constexpr int kUnroll = CS == 1 ? GMT_UNROLL_BATCH : GMT_UNROLL_CLUSTER;
   constexpr bool kDynamic = CS > 1;  // dynamic row / candidate distribution
   __shared__ double seg_s[kMaxWarps * 32 * kRows];  // per warp: kRows staged segments
+  // Kinodynamic waypoint tables (double integrator: D = 6; quadrotor: D = 0).
+  constexpr int kTabCap = D == 6 ? 64 : (D == 0 ? 144 : 1);
+  __shared__ double tab_s[(D == 0 || D == 6) ? kMaxWarps * kTabCap : 1];
 
   const int q = blockIdx.x / CS;
   int rank = 0;
@@ -898,7 +928,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
           const int32_t pid = I.in_path ? __ldg(I.in_path + bec) : -1;
           auto edge_free = [&](const Boxes& B) -> bool {
             if ((D == 0 || D == 6) && I.in_tau)  // kinodynamic: regenerated polyline (di.cuh, quad.cuh)
-              return kino_edge_free_warp<D>(I, B, byc, xc, __ldg(I.in_tau + bec), lane, sc);
+              return kino_edge_free_warp<D>(I, B, byc, xc, __ldg(I.in_tau + bec), lane, sc,
+                                            tab_s + ((D == 0 || D == 6) ? warp * kTabCap : 0), kTabCap);
             if (pid < 0) return segment_free_staged<D>(d, B, lane, sc);  // segment_free (planner.cpp:59)
             return polyline_free_warp<D>(I, d, B, pid, lane, sc);       // polyline_free (planner.cpp:56-58)
           };
