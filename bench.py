@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--single-reps", type=int, default=101)
     ap.add_argument("--cpu-sample", type=int, default=64, help="queries in the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--di-queries", type=int, default=148,
+    ap.add_argument("--di-queries", type=int, default=296,
                     help="batched 6D double-integrator queries per GPU (0: skip the DI legs)")
     ap.add_argument("--no-quad", action="store_true", help="skip the 12D quadrotor leg (configs[3])")
     return ap.parse_args()
