@@ -25,6 +25,7 @@
 // (normalised coordinates outside [0,1]) block the edge.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 
 #if defined(__CUDACC__)
@@ -106,8 +107,78 @@ GMT_HD double di_c(const DiCoef& c, double t) {
   return di_add(t, di_div(di_add(di_div(di_add(di_div(c.c0, t), c.b), t), c.a), t));
 }
 
+// The duration search shared by the kinodynamic models: the geometric grid
+// tau_j = T q^j (j = 0..kDiGrid, each point the rounded product of the
+// previous one) walked from large to small tau; every bracket
+// [tau_{j+1}, tau_j] with g(tau_{j+1}) <= 0 < g(tau_j) is refined by
+// kDiBisect bisection steps; the refined root with the smallest c wins (ties
+// to the smaller tau, i.e. the later bracket).  Returns c(tau*) and tau*.
+//
+// cap < inf (graph construction, where only c <= cap matters): brackets with
+// tau_{j+1} > cap are skipped -- their roots exceed cap, so c = tau + effort
+// > cap there and they can never be the minimum of a pair that is kept; a
+// kept pair's (c, tau) is therefore bit-identical to the uncapped search.
+// When no bracket lies below cap: if g(T) > 0 >= g(tau_min) the uncapped
+// search has a bracket, all above cap, and the pair is rejected (+inf);
+// otherwise the uncapped search runs.
+template <class GF, class CF>
+GMT_HD double kino_min_scan(double T, const GF& g, const CF& cfun, double cap, double* tau_out) {
+  double best_c = 0.0, best_t = 0.0;
+  bool have = false;
+  double t_hi = T;
+  int j = 1;
+  if (cap < INFINITY) {
+    while (j <= kDiGrid) {
+      const double t_lo = di_mul(t_hi, 0.75);
+      if (t_lo <= cap) break;
+      t_hi = t_lo;
+      ++j;
+    }
+  }
+  double g_hi = g(t_hi);
+  const double g_top = t_hi == T ? g_hi : (cap < INFINITY ? g(T) : g_hi);
+  for (; j <= kDiGrid; ++j) {
+    const double t_lo = di_mul(t_hi, 0.75);
+    const double g_lo = g(t_lo);
+    if (g_lo <= 0.0 && g_hi > 0.0) {
+      double lo = t_lo, hi = t_hi;
+      for (int it = 0; it < kDiBisect; ++it) {
+        const double mid = di_mul(0.5, di_add(lo, hi));
+        if (g(mid) > 0.0) {
+          hi = mid;
+        } else {
+          lo = mid;
+        }
+      }
+      const double ct = cfun(hi);
+      if (!have || ct <= best_c) {
+        best_c = ct;
+        best_t = hi;
+        have = true;
+      }
+    }
+    t_hi = t_lo;
+    g_hi = g_lo;
+  }
+  if (!have && cap < INFINITY) {
+    if (g_top > 0.0 && g_hi <= 0.0) {  // every bracket of the full search lies above cap
+      *tau_out = 0.0;
+      return INFINITY;
+    }
+    return kino_min_scan(T, g, cfun, INFINITY, tau_out);
+  }
+  if (!have) {  // g > 0 on the whole grid: be total
+    best_t = t_hi;
+    best_c = cfun(best_t);
+  }
+  *tau_out = best_t;
+  return best_c;
+}
+
 // Minimum cost and its duration; cost 0 / tau 0 for identical states at rest.
-GMT_HD double di_cost_tau(const double* x0, const double* x1, const DiParams& P, double* tau_out) {
+// cap: see kino_min_scan (INFINITY = the exact minimum for every pair).
+GMT_HD double di_cost_tau(const double* x0, const double* x1, const DiParams& P, double* tau_out,
+                          double cap = INFINITY) {
   const DiCoef c = di_coef(x0, x1, P);
   if (c.a == 0.0 && c.b == 0.0 && c.c0 == 0.0) {
     *tau_out = 0.0;
@@ -119,43 +190,8 @@ GMT_HD double di_cost_tau(const double* x0, const double* x1, const DiParams& P,
   if (b2 > T) T = b2;
   if (c3 > T) T = c3;
   T = di_add(1.0, T);
-  // Geometric grid tau_j = T q^j (j = 0..kDiGrid, each point the rounded
-  // product of the previous one), walked from large to small tau; brackets
-  // [tau_{j+1}, tau_j] with g(tau_{j+1}) <= 0 < g(tau_j).  The choice (min c,
-  // ties to the smaller tau) does not depend on the walk direction.
-  double best_c = 0.0, best_t = 0.0;
-  bool have = false;
-  double t_hi = T;
-  double g_hi = di_g(c, t_hi);
-  for (int j = 1; j <= kDiGrid; ++j) {
-    const double t_lo = di_mul(t_hi, 0.75);
-    const double g_lo = di_g(c, t_lo);
-    if (g_lo <= 0.0 && g_hi > 0.0) {
-      double lo = t_lo, hi = t_hi;
-      for (int it = 0; it < kDiBisect; ++it) {
-        const double mid = di_mul(0.5, di_add(lo, hi));
-        if (di_g(c, mid) > 0.0) {
-          hi = mid;
-        } else {
-          lo = mid;
-        }
-      }
-      const double ct = di_c(c, hi);
-      if (!have || ct <= best_c) {  // later brackets have smaller tau
-        best_c = ct;
-        best_t = hi;
-        have = true;
-      }
-    }
-    t_hi = t_lo;
-    g_hi = g_lo;
-  }
-  if (!have) {  // g > 0 on the whole grid cannot happen for c0 > 0; be total
-    best_t = t_hi;
-    best_c = di_c(c, best_t);
-  }
-  *tau_out = best_t;
-  return best_c;
+  return kino_min_scan(
+      T, [&](double t) { return di_g(c, t); }, [&](double t) { return di_c(c, t); }, cap, tau_out);
 }
 
 // State at time t on the optimal trajectory x0 -> x1 of duration tau

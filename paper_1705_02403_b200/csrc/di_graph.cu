@@ -56,6 +56,9 @@ struct DiModel {
   __device__ double cost_tau(const double* a, const double* b, double* t) const {
     return di_cost_tau(a, b, P, t);
   }
+  __device__ double cost_within(const double* a, const double* b, double r, double* t) const {
+    return di_cost_tau(a, b, P, t, r);
+  }
   __device__ double coord(const double* a, const double* b, double tau, int k, int i) const {
     return di_coord(a, b, tau, k, i, P);
   }
@@ -69,6 +72,9 @@ struct QuadModel {
   __device__ bool may(const double* a, const double* b) const { return quad_may_connect(a, b, P, radius); }
   __device__ double cost_tau(const double* a, const double* b, double* t) const {
     return quad_cost_tau(a, b, P, t);
+  }
+  __device__ double cost_within(const double* a, const double* b, double r, double* t) const {
+    return quad_cost_tau(a, b, P, t, r);
   }
   __device__ double coord(const double* a, const double* b, double tau, int k, int i) const {
     return quad_coord(a, b, tau, k, i, P);
@@ -102,6 +108,9 @@ struct DubinsModel {
     *t = static_cast<double>(segs);
     return c;
   }
+  __device__ double cost_within(const double* a, const double* b, double, double* t) const {
+    return cost_tau(a, b, t);
+  }
   __device__ double coord(const double*, const double*, double, int, int) const { return 0.0; }
   int segments() const { return 0; }
 };
@@ -133,7 +142,7 @@ __global__ void __launch_bounds__(256) kino_rows_kernel(const double* __restrict
         const double* from = SWAP ? xc : xr;
         const double* to = SWAP ? xr : xc;
         if (model.may(from, to)) {
-          cc = model.cost_tau(from, to, &tc);
+          cc = model.cost_within(from, to, radius, &tc);
           keep = cc <= radius;
         }
       }
@@ -339,14 +348,187 @@ int rows_pass(gmt_ctx* ctx, bool swap, const double* coords, int n, const Model&
   return GMT_OK;
 }
 
+// One evaluation per pair: warp per source row u, the keep bit of every
+// target chunk goes into an n x ceil(n/32) bit matrix (the ballot word),
+// with out-degrees and in-degrees counted on the way.
+template <class Model>
+__global__ void __launch_bounds__(256) kino_eval_kernel(const double* __restrict__ coords, int n,
+                                                        Model model, double radius,
+                                                        uint32_t* __restrict__ bits, int W,
+                                                        int64_t* __restrict__ out_counts,
+                                                        int64_t* __restrict__ in_counts) {
+  constexpr int kD = Model::kDim;
+  const int lane = threadIdx.x & 31;
+  const int warps = (blockDim.x >> 5) * gridDim.x;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    double xr[kD];
+    for (int k = 0; k < kD; ++k) xr[k] = __ldg(coords + static_cast<int64_t>(r) * kD + k);
+    int64_t cnt = 0;
+    for (int w = 0; w < W; ++w) {
+      const int c = w * 32 + lane;
+      bool keep = false;
+      if (c < n && c != r) {
+        double xc[kD];
+        for (int k = 0; k < kD; ++k) xc[k] = __ldg(coords + static_cast<int64_t>(c) * kD + k);
+        if (model.may(xr, xc)) {
+          double tc;
+          keep = model.cost_within(xr, xc, radius, &tc) <= radius;
+        }
+      }
+      const uint32_t m = __ballot_sync(kFull, keep);
+      if (lane == 0) bits[static_cast<int64_t>(r) * W + w] = m;
+      if (keep) atomicAdd(reinterpret_cast<unsigned long long*>(in_counts + c), 1ull);
+      cnt += __popc(m);
+    }
+    if (lane == 0) out_counts[r] = cnt;
+  }
+}
+
+// Out-rows from the bit matrix: only kept pairs are evaluated again (the
+// same capped search, so the same cost and duration).
+template <class Model>
+__global__ void __launch_bounds__(256) kino_out_fill_kernel(const double* __restrict__ coords, int n,
+                                                            Model model, double radius,
+                                                            const uint32_t* __restrict__ bits, int W,
+                                                            const int64_t* __restrict__ row_ptr,
+                                                            int32_t* __restrict__ col,
+                                                            double* __restrict__ cost,
+                                                            double* __restrict__ tau) {
+  constexpr int kD = Model::kDim;
+  const int lane = threadIdx.x & 31;
+  const int warps = (blockDim.x >> 5) * gridDim.x;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    double xr[kD];
+    for (int k = 0; k < kD; ++k) xr[k] = __ldg(coords + static_cast<int64_t>(r) * kD + k);
+    int64_t out = row_ptr[r];
+    for (int w = 0; w < W; ++w) {
+      const uint32_t m = __ldg(bits + static_cast<int64_t>(r) * W + w);
+      if (!m) continue;
+      if ((m >> lane) & 1u) {
+        const int c = w * 32 + lane;
+        double xc[kD];
+        for (int k = 0; k < kD; ++k) xc[k] = __ldg(coords + static_cast<int64_t>(c) * kD + k);
+        double tc;
+        const double cc = model.cost_within(xr, xc, radius, &tc);
+        const int64_t slot = out + __popc(m & ((1u << lane) - 1u));
+        col[slot] = c;
+        cost[slot] = cc;
+        tau[slot] = tc;
+      }
+      out += __popc(m);
+    }
+  }
+}
+
+// In-rows = the bit matrix's columns, sources ascending (the reference's
+// sequential merge order, graph.cpp:184-186); each entry copies the
+// out-edge's cost and duration (the same pair, the same computation).
+__global__ void __launch_bounds__(256) kino_in_fill_kernel(const uint32_t* __restrict__ bits, int W, int n,
+                                                           const int64_t* __restrict__ out_ptr,
+                                                           const int32_t* __restrict__ out_col,
+                                                           const double* __restrict__ out_cost,
+                                                           const double* __restrict__ out_tau,
+                                                           const int64_t* __restrict__ in_ptr,
+                                                           int32_t* __restrict__ in_col,
+                                                           double* __restrict__ in_cost,
+                                                           double* __restrict__ in_tau) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (blockDim.x >> 5) * gridDim.x;
+  for (int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); x < n; x += warps) {
+    const int wx = x >> 5;
+    const uint32_t bx = 1u << (x & 31);
+    int64_t out = in_ptr[x];
+    for (int base = 0; base < n; base += 32) {
+      const int u = base + lane;
+      const bool kept = u < n && (__ldg(bits + static_cast<int64_t>(u) * W + wx) & bx);
+      const uint32_t m = __ballot_sync(kFull, kept);
+      if (kept) {
+        int64_t lo = out_ptr[u], hi = out_ptr[u + 1];
+        while (lo < hi) {  // NeighborGraph::edge_path lookup (graph.cpp:34-40)
+          const int64_t mid = (lo + hi) >> 1;
+          if (out_col[mid] < x) lo = mid + 1; else hi = mid;
+        }
+        const int64_t slot = out + __popc(m & ((1u << lane) - 1u));
+        in_col[slot] = u;
+        in_cost[slot] = out_cost[lo];
+        in_tau[slot] = out_tau[lo];
+      }
+      out += __popc(m);
+    }
+  }
+}
+
+int carve_rows(Arena& mem, int n, int64_t E, DiRows* rows) {
+  const size_t o_col = align16(sizeof(int64_t) * (n + 1));
+  const size_t o_cost = o_col + align16(sizeof(int32_t) * E);
+  const size_t o_tau = o_cost + align16(sizeof(double) * E);
+  const size_t total = o_tau + align16(sizeof(double) * E);
+  const int rc = mem.reserve(total);
+  if (rc) return rc;
+  char* b = static_cast<char*>(mem.ptr);
+  rows->ptr = reinterpret_cast<int64_t*>(b);
+  rows->col = reinterpret_cast<int32_t*>(b + o_col);
+  rows->cost = reinterpret_cast<double*>(b + o_cost);
+  rows->tau = reinterpret_cast<double*>(b + o_tau);
+  rows->edges = E;
+  return GMT_OK;
+}
+
 template <class Model>
 int build_kino_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const Model& model, double radius,
                          Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in) {
   if (!(radius > 0.0)) return set_error(GMT_E_INVALID_INPUT, "connection radius must be positive");
   if (n < 1) return set_error(GMT_E_INVALID_INPUT, "cannot build a graph over zero samples");
-  int rc = rows_pass(ctx, false, d_coords, n, model, radius, out_mem, out, true);
+  const int W = (n + 31) / 32;
+  const size_t bit_bytes = sizeof(uint32_t) * static_cast<size_t>(n) * W;
+  if (bit_bytes > (size_t(1) << 31)) {  // very large n: two evaluations per pair per direction
+    int rc = rows_pass(ctx, false, d_coords, n, model, radius, out_mem, out, true);
+    if (rc) return rc;
+    return rows_pass(ctx, true, d_coords, n, model, radius, in_mem, in, true);
+  }
+  cudaStream_t s = ctx->stream;
+  const size_t o_oc = align16(bit_bytes);
+  const size_t o_ic = o_oc + align16(sizeof(int64_t) * (n + 1));
+  const size_t o_op = o_ic + align16(sizeof(int64_t) * (n + 1));
+  const size_t o_ip = o_op + align16(sizeof(int64_t) * (n + 1));
+  Arena tmp;
+  int rc = tmp.reserve(o_ip + sizeof(int64_t) * (n + 1));
   if (rc) return rc;
-  return rows_pass(ctx, true, d_coords, n, model, radius, in_mem, in, true);
+  char* b = static_cast<char*>(tmp.ptr);
+  auto* bits = reinterpret_cast<uint32_t*>(b);
+  auto* oc = reinterpret_cast<int64_t*>(b + o_oc);
+  auto* ic = reinterpret_cast<int64_t*>(b + o_ic);
+  auto* op = reinterpret_cast<int64_t*>(b + o_op);
+  auto* ip = reinterpret_cast<int64_t*>(b + o_ip);
+  GMT_CUDA(cudaMemsetAsync(ic, 0, sizeof(int64_t) * (n + 1), s));
+  const int blocks = std::max(1, std::min((n + 7) / 8, ctx->sm_count * 8));
+  kino_eval_kernel<Model><<<blocks, 256, 0, s>>>(d_coords, n, model, radius, bits, W, oc, ic);
+  GMT_CUDA(cudaGetLastError());
+  scan_rows_kernel<<<1, 1024, 0, s>>>(oc, n, op);
+  scan_rows_kernel<<<1, 1024, 0, s>>>(ic, n, ip);
+  GMT_CUDA(cudaGetLastError());
+  ctx->launches += 3;
+  int64_t E = 0;
+  GMT_CUDA(cudaMemcpyAsync(&E, op + n, sizeof(E), cudaMemcpyDeviceToHost, s));
+  GMT_CUDA(cudaStreamSynchronize(s));
+  rc = carve_rows(out_mem, n, E, out);
+  if (rc == GMT_OK) rc = carve_rows(in_mem, n, E, in);
+  if (rc) {
+    tmp.release();
+    return rc;
+  }
+  GMT_CUDA(cudaMemcpyAsync(out->ptr, op, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+  GMT_CUDA(cudaMemcpyAsync(in->ptr, ip, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+  kino_out_fill_kernel<Model><<<blocks, 256, 0, s>>>(d_coords, n, model, radius, bits, W, out->ptr, out->col,
+                                                     out->cost, out->tau);
+  GMT_CUDA(cudaGetLastError());
+  kino_in_fill_kernel<<<blocks, 256, 0, s>>>(bits, W, n, out->ptr, out->col, out->cost, out->tau, in->ptr,
+                                             in->col, in->cost, in->tau);
+  GMT_CUDA(cudaGetLastError());
+  ctx->launches += 2;
+  GMT_CUDA(cudaStreamSynchronize(s));
+  tmp.release();
+  return GMT_OK;
 }
 
 double di_prefilter_bound(const DiParams& P, double radius) {

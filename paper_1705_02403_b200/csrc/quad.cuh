@@ -157,7 +157,8 @@ GMT_HD double quad_c(const double* C, double t) {
   return di_add(t, r);
 }
 
-GMT_HD double quad_cost_tau(const double* x0, const double* x1, const QuadParams& P, double* tau_out) {
+GMT_HD double quad_cost_tau(const double* x0, const double* x1, const QuadParams& P, double* tau_out,
+                            double cap = INFINITY) {
   double C[kQuadK + 1];
   quad_coef(x0, x1, P, C);
   bool zero = true;
@@ -173,39 +174,8 @@ GMT_HD double quad_cost_tau(const double* x0, const double* x1, const QuadParams
     if (a > T) T = a;
   }
   T = di_add(1.0, T);
-  double best_c = 0.0, best_t = 0.0;
-  bool have = false;
-  double t_hi = T;
-  double g_hi = quad_g(C, t_hi);
-  for (int j = 1; j <= kDiGrid; ++j) {
-    const double t_lo = di_mul(t_hi, 0.75);
-    const double g_lo = quad_g(C, t_lo);
-    if (g_lo <= 0.0 && g_hi > 0.0) {
-      double lo = t_lo, hi = t_hi;
-      for (int it = 0; it < kDiBisect; ++it) {
-        const double mid = di_mul(0.5, di_add(lo, hi));
-        if (quad_g(C, mid) > 0.0) {
-          hi = mid;
-        } else {
-          lo = mid;
-        }
-      }
-      const double ct = quad_c(C, hi);
-      if (!have || ct <= best_c) {
-        best_c = ct;
-        best_t = hi;
-        have = true;
-      }
-    }
-    t_hi = t_lo;
-    g_hi = g_lo;
-  }
-  if (!have) {
-    best_t = t_hi;
-    best_c = quad_c(C, best_t);
-  }
-  *tau_out = best_t;
-  return best_c;
+  return kino_min_scan(
+      T, [&](double t) { return quad_g(C, t); }, [&](double t) { return quad_c(C, t); }, cap, tau_out);
 }
 
 GMT_HD double quad_pow(double t, int e) {
