@@ -342,6 +342,19 @@ int gmt_build_quad_graph(gmt_ctx* ctx, const double* coords, int32_t n,
                          int64_t* in_ptr, int32_t* in_col, double* in_cost, int32_t* in_path,
                          double* path_pts);
 
+/* build_instance + gmt_plan for a batch of Euclidean problems (one common
+ * dimension): samples, init append and r-disk graphs of all problems are
+ * built in batched device launches, then ONE batched solve.  Problems that
+ * need sample_free's rare paths (more candidates than the first chunk,
+ * exact duplicates, goal substitution) use the single-instance builder, so
+ * every result equals gmt_instance_build + gmt_plan bit for bit.
+ * status_out[q]: GMT_OK, or the query's own build outcome
+ * (GMT_E_GOAL_BLOCKED / GMT_E_INFEASIBLE_SAMPLING; summaries[q] is then
+ * not written).  path_states (may be NULL): up to path_cap path states
+ * (dim doubles each) of query q at q * path_cap * dim.  lambda per problem. */
+int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int32_t count, int32_t* status_out,
+                      gmt_plan_summary* summaries, int32_t path_cap, double* path_states);
+
 /* ---- replanning simulator (simulator.hpp:53-74) -------------------------- */
 /* run_trial (simulator.cpp:66-176): the trial state machine on the host,
  * bit-identical to the reference, every replan (sample_free -> append_init

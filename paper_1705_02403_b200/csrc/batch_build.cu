@@ -1,0 +1,719 @@
+// batch_build.cu -- build_instance + gmt_plan for many Euclidean problems at
+// once (SURVEY.md §8(e) batched queries, §8(f) row 3 simulator replans).
+//
+// One launch per stage for the whole batch, problem-major:
+//   gen    candidate j of problem p (Halton index / PCG jump-ahead, exactly
+//          CandidateStream::draw, sampling.cpp:64-76) and its point_free flag
+//   pack   one CTA per problem: the first n free candidates, in order
+//   dedup  (uniform sampling) any exact duplicate among them
+//   goal   any sample in the goal box; append_init (sampling.cpp:144-154)
+//   rdisk  count / fill of every problem's r-disk rows (graph.cpp:117-188,
+//          the predicate of graph.cu), one global scan in between
+//   desc   the DevInstance of every problem, then ONE batched solve.
+// Problems that need sample_free's rare paths -- more candidates than the
+// first chunk, an exact duplicate, goal substitution (sampling.cpp:115-141),
+// or an infeasible / goal-blocked outcome -- are rebuilt by the
+// single-instance builder, so every problem's instance is bit-identical to
+// gmt_instance_build's (and the reference's build_instance).
+#include <cuda_runtime.h>
+
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "gmt_b200.h"
+#include "internal.cuh"
+#include "sample_dev.cuh"
+#include "solve.cuh"
+
+namespace gmtb {
+
+int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, int cluster, size_t* smem, int* obs_in_smem);
+int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, bool stats,
+                  std::vector<DevResult>& out, ResultScalars** scalars_base, int64_t* counters);
+int launch_jobs(gmt_ctx* ctx, const std::vector<SolveJob>& jobs, int cluster, int threads, size_t smem,
+                int obs_in_smem, int dim);
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kMaxDimB = 16;
+
+#define GMT_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_error(_e, #call); \
+  } while (0)
+
+struct BProb {
+  int kind, d, dd, nb, n, K, need_dedup, pad;
+  uint64_t start_index, s0;
+  int64_t box_off;   // first box of the problem
+  int64_t cand_off;  // first candidate row
+  int64_t row_off;   // first coordinate row (n + 1 rows reserved)
+  double radius, r2_hi;
+};
+
+// Per-problem outcome of the batched stages.
+struct BOut {
+  int32_t fallback;  // 1: rebuild with the single-instance builder
+  int32_t V;         // vertices (n, or n + 1 with the appended init)
+  int32_t init_index;
+  int32_t goal_any;
+};
+
+__device__ __forceinline__ bool free_point(const double* p, int d, const double* lo, const double* hi, int nb) {
+  if (!point_in_cube(p, d)) return false;  // space.cpp:47-54
+  for (int b = 0; b < nb; ++b)
+    if (box_contains(lo + b * d, hi + b * d, d, p)) return false;
+  return true;
+}
+
+__global__ void gen_batch_kernel(const BProb* __restrict__ probs, const double* __restrict__ box_lo,
+                                 const double* __restrict__ box_hi, const uint32_t* __restrict__ primes,
+                                 double* __restrict__ cand, uint8_t* __restrict__ flag) {
+  const BProb P = probs[blockIdx.y];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.K) return;
+  double c[kMaxDimB];
+  const int d = P.d;
+  if (P.kind == GMT_SAMPLE_HALTON) {
+    const uint64_t idx = P.start_index + static_cast<uint64_t>(j);
+    for (int k = 0; k < d; ++k) c[k] = halton_dev(idx, primes[k]);
+  } else {
+    uint64_t st = pcg_advance(P.s0, static_cast<uint64_t>(j) * static_cast<uint64_t>(P.dd));
+    for (int k = 0; k < d; ++k) {
+      c[k] = static_cast<double>(pcg_out(st)) * 0x1p-32;  // next_double (rng.hpp:33)
+      st = st * kPcgMult + kPcgInc;
+    }
+  }
+  double* out = cand + (P.cand_off + j) * d;
+  for (int k = 0; k < d; ++k) out[k] = c[k];
+  flag[P.cand_off + j] =
+      free_point(c, d, box_lo + P.box_off * d, box_hi + P.box_off * d, P.nb) ? 1 : 0;
+}
+
+// One CTA per problem: ordered compaction of the first n free candidates.
+__global__ void __launch_bounds__(1024) pack_batch_kernel(const BProb* __restrict__ probs,
+                                                          const uint8_t* __restrict__ flag,
+                                                          const double* __restrict__ cand,
+                                                          double* __restrict__ coords, BOut* __restrict__ res) {
+  __shared__ int warp_cnt[32];
+  __shared__ int base_s;
+  const BProb P = probs[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) base_s = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < P.K && base_s < P.n; b0 += blockDim.x) {
+    const int i = b0 + tid;
+    const bool f = i < P.K && flag[P.cand_off + i];
+    const uint32_t m = __ballot_sync(kFull, f);
+    if (lane == 0) warp_cnt[warp] = __popc(m);
+    __syncthreads();
+    int before = base_s;
+    for (int w = 0; w < warp; ++w) before += warp_cnt[w];
+    const int slot = before + __popc(m & ((1u << lane) - 1u));
+    if (f && slot < P.n)
+      for (int k = 0; k < P.d; ++k) coords[(P.row_off + slot) * P.d + k] = cand[(P.cand_off + i) * P.d + k];
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int w = 0; w < nw; ++w) tot += warp_cnt[w];
+      base_s += tot;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    res[blockIdx.x].fallback = base_s < P.n ? 1 : 0;  // needs more than the first chunk
+    res[blockIdx.x].V = P.n;
+  }
+}
+
+// Exact duplicates among a problem's first n samples (uniform sampling):
+// sample_free would skip them, so the problem takes the single path.
+__global__ void dedup_batch_kernel(const BProb* __restrict__ probs, const double* __restrict__ coords,
+                                   BOut* __restrict__ res) {
+  const BProb P = probs[blockIdx.y];
+  if (!P.need_dedup || res[blockIdx.y].fallback) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  const double* p = coords + (P.row_off + i) * P.d;
+  for (int j = 0; j < i; ++j) {
+    const double* q = coords + (P.row_off + j) * P.d;
+    bool eq = true;
+    for (int k = 0; k < P.d; ++k) eq = eq && p[k] == q[k];
+    if (eq) {
+      res[blockIdx.y].fallback = 1;
+      return;
+    }
+  }
+}
+
+// Goal membership and append_init (sampling.cpp:110-112, 144-154).
+__global__ void __launch_bounds__(256) goal_init_batch_kernel(const BProb* __restrict__ probs,
+                                                              double* __restrict__ coords,
+                                                              const double* __restrict__ goal_lo,
+                                                              const double* __restrict__ goal_hi,
+                                                              const double* __restrict__ inits,
+                                                              BOut* __restrict__ res) {
+  __shared__ int first;
+  const int p = blockIdx.x;
+  const BProb P = probs[p];
+  if (res[p].fallback) return;
+  const double* glo = goal_lo + static_cast<int64_t>(p) * P.d;
+  const double* ghi = goal_hi + static_cast<int64_t>(p) * P.d;
+  const double* init = inits + static_cast<int64_t>(p) * P.d;
+  if (threadIdx.x == 0) first = 0x7fffffff;
+  __syncthreads();
+  bool in_goal = false;
+  for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
+    const double* c = coords + (P.row_off + i) * P.d;
+    in_goal = in_goal || box_contains(glo, ghi, P.d, c);
+    bool eq = true;
+    for (int k = 0; k < P.d; ++k) eq = eq && c[k] == init[k];
+    if (eq) atomicMin(&first, i);
+  }
+  const int any_goal = __syncthreads_or(in_goal ? 1 : 0);
+  if (threadIdx.x == 0) {
+    if (!any_goal) res[p].fallback = 1;  // goal substitution: the single path
+    if (first != 0x7fffffff) {
+      res[p].init_index = first;
+      res[p].V = P.n;
+    } else {
+      for (int k = 0; k < P.d; ++k) coords[(P.row_off + P.n) * P.d + k] = init[k];
+      res[p].init_index = P.n;
+      res[p].V = P.n + 1;
+    }
+    res[p].goal_any = any_goal;
+  }
+}
+
+// Euclidean r-disk rows of every problem (the predicate of graph.cu:
+// correctly rounded squared distance in axis order, sq <= r^2 (1 + 1e-12)
+// pre-test, sqrt_rn(sq) <= r).  Flat rows r = row_off[p] + u, u <= n.
+template <int D, bool FILL>
+__global__ void __launch_bounds__(256) rdisk_batch_kernel(const BProb* __restrict__ probs,
+                                                          const int64_t* __restrict__ row_start, int P_count,
+                                                          int64_t R, const double* __restrict__ coords,
+                                                          const BOut* __restrict__ res,
+                                                          int64_t* __restrict__ counts,
+                                                          const int64_t* __restrict__ row_ptr,
+                                                          int32_t* __restrict__ col, double* __restrict__ cost) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(blockDim.x >> 5) * gridDim.x;
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); r < R; r += warps) {
+    int lo = 0, hi = P_count - 1;  // problem of row r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (row_start[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const int p = lo;
+    const BProb& P = probs[p];
+    const int d = D > 0 ? D : P.d;
+    const int u = static_cast<int>(r - P.row_off);
+    const int V = res[p].fallback ? 0 : res[p].V;
+    int64_t out = FILL ? row_ptr[r] : 0;
+    if (u < V) {
+      double a[D > 0 ? D : kMaxDimB];
+#pragma unroll
+      for (int k = 0; k < (D > 0 ? D : kMaxDimB); ++k)
+        if (D > 0 || k < d) a[k] = __ldg(coords + (P.row_off + u) * d + k);
+      for (int base = 0; base < V; base += 32) {
+        const int v = base + lane;
+        bool keep = false;
+        double c = 0.0;
+        if (v < V && v != u) {
+          double sq = 0.0;
+#pragma unroll
+          for (int k = 0; k < (D > 0 ? D : kMaxDimB); ++k) {
+            if (D > 0 || k < d) {
+              const double t = __dsub_rn(a[k], __ldg(coords + (P.row_off + v) * d + k));
+              sq = __dadd_rn(sq, __dmul_rn(t, t));
+            }
+          }
+          if (sq <= P.r2_hi) {
+            c = __dsqrt_rn(sq);
+            keep = c <= P.radius;
+          }
+        }
+        const uint32_t m = __ballot_sync(kFull, keep);
+        if (FILL && keep) {
+          const int64_t slot = out + __popc(m & ((1u << lane) - 1u));
+          col[slot] = v;
+          cost[slot] = c;
+        }
+        out += __popc(m);
+      }
+    }
+    if (!FILL && lane == 0) counts[r] = out;
+  }
+}
+
+__global__ void desc_batch_kernel(const BProb* __restrict__ probs, const BOut* __restrict__ res,
+                                  const double* __restrict__ coords, const double* __restrict__ box_lo,
+                                  const double* __restrict__ box_hi, const double* __restrict__ goal_lo,
+                                  const double* __restrict__ goal_hi, const int64_t* __restrict__ row_ptr,
+                                  const int32_t* __restrict__ col, const double* __restrict__ cost, int count,
+                                  DevInstance* __restrict__ descs) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= count) return;
+  const BProb P = probs[p];
+  DevInstance D{};
+  D.n = res[p].V;
+  D.dim = P.d;
+  D.num_boxes = P.nb;
+  D.directed = 0;
+  D.goal_count = res[p].goal_any;
+  D.init_index = res[p].init_index;
+  D.radius = P.radius;
+  D.num_edges = row_ptr[P.row_off + D.n] - row_ptr[P.row_off];
+  D.coords = coords + P.row_off * P.d;
+  D.box_lo = box_lo + P.box_off * P.d;
+  D.box_hi = box_hi + P.box_off * P.d;
+  D.goal_lo = goal_lo + static_cast<int64_t>(p) * P.d;
+  D.goal_hi = goal_hi + static_cast<int64_t>(p) * P.d;
+  D.out_ptr = row_ptr + P.row_off;
+  D.out_col = col;
+  D.out_cost = cost;
+  D.in_ptr = D.out_ptr;
+  D.in_col = col;
+  D.in_cost = cost;
+  descs[p] = D;
+}
+
+// Path states of every solved query (up to cap states each).
+__global__ void gather_paths_kernel(const DevResult* __restrict__ rs, const DevInstance* const* __restrict__ insts,
+                                    int count, int cap, int d, double* __restrict__ out) {
+  const int q = blockIdx.x;
+  if (q >= count) return;
+  const DevResult R = rs[q];
+  const ResultScalars sc = *R.scalars;
+  if (sc.status != 0) return;
+  const DevInstance* I = insts[q];
+  const int len = sc.path_len < cap ? sc.path_len : cap;
+  for (int e = threadIdx.x; e < len * d; e += blockDim.x) {
+    const int k = e / d, i = e - k * d;
+    out[(static_cast<int64_t>(q) * cap + k) * d + i] = I->coords[static_cast<int64_t>(R.path[k]) * d + i];
+  }
+}
+
+// Register-blocked variant for d = 2, 3: a warp takes RB consecutive rows
+// of one problem; each lane loads one target's coordinates once and tests
+// it against all RB rows (RB x fewer coordinate loads); per row the ballot
+// word orders the accepted targets exactly as the one-row kernel does.
+template <int D, int RB, bool FILL>
+__global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __restrict__ probs,
+                                                             const int64_t* __restrict__ row_start, int P_count,
+                                                             int64_t R, const double* __restrict__ coords,
+                                                             const BOut* __restrict__ res,
+                                                             int64_t* __restrict__ counts,
+                                                             const int64_t* __restrict__ row_ptr,
+                                                             int32_t* __restrict__ col, double* __restrict__ cost) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(blockDim.x >> 5) * gridDim.x;
+  const int64_t groups = (R + RB - 1) / RB;
+  for (int64_t gidx = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); gidx < groups;
+       gidx += warps) {
+    const int64_t r0 = gidx * RB;
+    int lo = 0, hi = P_count - 1;  // problem of row r0 (rows of a group may spill into the next problem)
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (row_start[mid] <= r0) lo = mid; else hi = mid - 1;
+    }
+    const int p = lo;
+    const BProb& P = probs[p];
+    const int u0 = static_cast<int>(r0 - P.row_off);
+    const int V = res[p].fallback ? 0 : res[p].V;
+    const int rows_here = static_cast<int>(min(static_cast<int64_t>(RB), row_start[p + 1] - r0));
+    double a[RB][D];
+    int64_t out[RB];
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int u = u0 + j;
+      out[j] = (FILL && j < rows_here) ? row_ptr[r0 + j] : 0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) a[j][k] = (j < rows_here && u < V) ? __ldg(coords + (P.row_off + u) * D + k) : 0.0;
+    }
+    for (int base = 0; base < V; base += 32) {
+      const int v = base + lane;
+      double b[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) b[k] = v < V ? __ldg(coords + (P.row_off + v) * D + k) : 0.0;
+#pragma unroll
+      for (int j = 0; j < RB; ++j) {
+        const int u = u0 + j;
+        bool keep = false;
+        double c = 0.0;
+        if (j < rows_here && u < V && v < V && v != u) {
+          double sq = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const double t = __dsub_rn(a[j][k], b[k]);
+            sq = __dadd_rn(sq, __dmul_rn(t, t));
+          }
+          if (sq <= P.r2_hi) {
+            c = __dsqrt_rn(sq);
+            keep = c <= P.radius;
+          }
+        }
+        const uint32_t m = __ballot_sync(kFull, keep);
+        if (FILL && keep) {
+          const int64_t slot = out[j] + __popc(m & ((1u << lane) - 1u));
+          col[slot] = v;
+          cost[slot] = c;
+        }
+        out[j] += __popc(m);
+      }
+    }
+    if (!FILL && lane == 0) {
+#pragma unroll
+      for (int j = 0; j < RB; ++j)
+        if (j < rows_here) counts[r0 + j] = out[j];
+    }
+    // rows of the group beyond this problem's rows belong to the next one
+    for (int64_t r = r0 + rows_here; r < r0 + RB && r < R; ++r) {
+      int lo2 = 0, hi2 = P_count - 1;
+      while (lo2 < hi2) {
+        const int mid = (lo2 + hi2 + 1) >> 1;
+        if (row_start[mid] <= r) lo2 = mid; else hi2 = mid - 1;
+      }
+      const BProb& Q = probs[lo2];
+      const int uq = static_cast<int>(r - Q.row_off);
+      const int Vq = res[lo2].fallback ? 0 : res[lo2].V;
+      int64_t o = FILL ? row_ptr[r] : 0;
+      if (uq < Vq) {
+        double aq[D];
+        for (int k = 0; k < D; ++k) aq[k] = __ldg(coords + (Q.row_off + uq) * D + k);
+        for (int base = 0; base < Vq; base += 32) {
+          const int v = base + lane;
+          bool keep = false;
+          double c = 0.0;
+          if (v < Vq && v != uq) {
+            double sq = 0.0;
+            for (int k = 0; k < D; ++k) {
+              const double t = __dsub_rn(aq[k], __ldg(coords + (Q.row_off + v) * D + k));
+              sq = __dadd_rn(sq, __dmul_rn(t, t));
+            }
+            if (sq <= Q.r2_hi) {
+              c = __dsqrt_rn(sq);
+              keep = c <= Q.radius;
+            }
+          }
+          const uint32_t m = __ballot_sync(kFull, keep);
+          if (FILL && keep) {
+            const int64_t slot = o + __popc(m & ((1u << lane) - 1u));
+            col[slot] = v;
+            cost[slot] = c;
+          }
+          o += __popc(m);
+        }
+      }
+      if (!FILL && lane == 0) counts[r] = o;
+    }
+  }
+}
+
+template <bool FILL>
+cudaError_t launch_rdisk_batch(int d, int blocks, cudaStream_t s, const BProb* probs, const int64_t* row_start,
+                               int P_count, int64_t R, const double* coords, const BOut* res, int64_t* counts,
+                               const int64_t* row_ptr, int32_t* col, double* cost) {
+  switch (d) {
+    case 2:
+      rdisk_batch_rb_kernel<2, 8, FILL><<<blocks, 256, 0, s>>>(probs, row_start, P_count, R, coords, res, counts,
+                                                               row_ptr, col, cost);
+      break;
+    case 3:
+      rdisk_batch_rb_kernel<3, 8, FILL><<<blocks, 256, 0, s>>>(probs, row_start, P_count, R, coords, res, counts,
+                                                               row_ptr, col, cost);
+      break;
+    default:
+      rdisk_batch_kernel<0, FILL><<<blocks, 256, 0, s>>>(probs, row_start, P_count, R, coords, res, counts,
+                                                         row_ptr, col, cost);
+      break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+}  // namespace gmtb
+
+using namespace gmtb;
+
+extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int32_t count,
+                                 int32_t* status_out, gmt_plan_summary* summaries, int32_t path_cap,
+                                 double* path_states) {
+  gmtb::AllocScope alloc_scope_(ctx);
+  if (count < 1) return set_error(GMT_E_INVALID_INPUT, "gmt_plan_problems needs at least one problem");
+  const int d = problems[0].scene.dim;
+  if (d < 1 || d > kMaxDimB) return set_error(GMT_E_INVALID_INPUT, "dimension must be in [1, 16]");
+  cudaStream_t s = ctx->stream;
+
+  // ---- host: per-problem parameters and the packed scene arrays ----------
+  std::vector<BProb> probs(count);
+  std::vector<double> box_lo, box_hi, goal_lo(static_cast<size_t>(count) * d), goal_hi(goal_lo.size()),
+      inits(goal_lo.size());
+  std::vector<int64_t> row_start(count + 1, 0);
+  int64_t cand_total = 0, box_total = 0;
+  int max_K = 1;
+  for (int q = 0; q < count; ++q) {
+    const gmt_problem& pr = problems[q];
+    if (pr.scene.dim != d) return set_error(GMT_E_INVALID_INPUT, "all problems of a batch share the dimension");
+    if (pr.steering != GMT_STEER_EUCLIDEAN)
+      return set_error(GMT_E_INVALID_INPUT, "gmt_plan_problems covers the Euclidean steering model");
+    int rc = validate_scene(&pr.scene);
+    if (rc) return rc;
+    if (pr.n < 1) return set_error(GMT_E_INVALID_INPUT, "sample count must be >= 1");
+    if (!(pr.lambda > 0.0 && pr.lambda <= 1.0)) return set_error(GMT_E_INVALID_INPUT, "lambda must be in (0, 1]");
+    if (pr.sampling.kind != GMT_SAMPLE_HALTON && pr.sampling.kind != GMT_SAMPLE_UNIFORM)
+      return set_error(GMT_E_INVALID_INPUT, "unknown sample kind");
+    if (pr.sampling.kind == GMT_SAMPLE_HALTON && pr.sampling.start_index == 0)
+      return set_error(GMT_E_INVALID_INPUT, "halton start_index is 1-based; got 0");
+    BProb& P = probs[q];
+    std::memset(&P, 0, sizeof(P));
+    P.kind = pr.sampling.kind;
+    P.d = d;
+    P.dd = d;  // Euclidean problems sample no heading (problem.cpp:338-339)
+    P.nb = pr.scene.num_boxes;
+    P.n = pr.n;
+    const uint64_t budget = 1000ULL * static_cast<uint64_t>(pr.n);
+    P.K = static_cast<int>(std::min<uint64_t>(budget, 2ull * pr.n + 256));
+    P.need_dedup = (pr.sampling.kind == GMT_SAMPLE_UNIFORM ||
+                    pr.sampling.start_index + budget >= (1ULL << 53)) ? 1 : 0;
+    P.start_index = pr.sampling.start_index;
+    P.s0 = pcg_seed_state(pr.sampling.seed);
+    P.box_off = box_total;
+    P.cand_off = cand_total;
+    P.row_off = row_start[q];
+    double radius = pr.radius_override;
+    if (!(radius > 0.0)) {
+      rc = gmt_connection_radius(d, pr.n, pr.eta, 1.0, &radius);  // free_measure_upper_bound = 1
+      if (rc) return rc;
+    }
+    P.radius = radius;
+    P.r2_hi = radius * radius * (1.0 + 1e-12);
+    box_lo.insert(box_lo.end(), pr.scene.box_lo, pr.scene.box_lo + static_cast<size_t>(P.nb) * d);
+    box_hi.insert(box_hi.end(), pr.scene.box_hi, pr.scene.box_hi + static_cast<size_t>(P.nb) * d);
+    std::copy(pr.scene.goal_lo, pr.scene.goal_lo + d, goal_lo.begin() + static_cast<size_t>(q) * d);
+    std::copy(pr.scene.goal_hi, pr.scene.goal_hi + d, goal_hi.begin() + static_cast<size_t>(q) * d);
+    std::copy(pr.init, pr.init + d, inits.begin() + static_cast<size_t>(q) * d);
+    box_total += P.nb;
+    cand_total += P.K;
+    row_start[q + 1] = row_start[q] + pr.n + 1;
+    max_K = std::max(max_K, P.K);
+  }
+  const int64_t R = row_start[count];
+  std::vector<uint32_t> primes(kMaxDimB);
+  for (int k = 0; k < kMaxDimB; ++k) primes[k] = nth_prime_h(k + 1);
+
+  // ---- device arena ----------------------------------------------------------
+  auto al = [](size_t x) { return align16(x); };
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = al(off + bytes);
+    return o;
+  };
+  const size_t o_probs = take(sizeof(BProb) * count);
+  const size_t o_rs = take(sizeof(int64_t) * (count + 1));
+  const size_t o_blo = take(sizeof(double) * std::max<int64_t>(box_total, 1) * d);
+  const size_t o_bhi = take(sizeof(double) * std::max<int64_t>(box_total, 1) * d);
+  const size_t o_glo = take(sizeof(double) * goal_lo.size());
+  const size_t o_ghi = take(sizeof(double) * goal_hi.size());
+  const size_t o_init = take(sizeof(double) * inits.size());
+  const size_t o_pr = take(sizeof(uint32_t) * kMaxDimB);
+  const size_t o_cand = take(sizeof(double) * cand_total * d);
+  const size_t o_flag = take(cand_total);
+  const size_t o_coords = take(sizeof(double) * R * d);
+  const size_t o_res = take(sizeof(BOut) * count);
+  const size_t o_cnt = take(sizeof(int64_t) * (R + 1));
+  const size_t o_rp = take(sizeof(int64_t) * (R + 1));
+  const size_t o_desc = take(sizeof(DevInstance) * count);
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, static_cast<int64_t*>(nullptr),
+                                static_cast<int64_t*>(nullptr), static_cast<int>(R + 1));
+  const size_t o_scan = take(scan_bytes);
+  Arena work;
+  int rc = work.reserve(off);
+  if (rc) return rc;
+  char* B = static_cast<char*>(work.ptr);
+  auto* d_probs = reinterpret_cast<BProb*>(B + o_probs);
+  auto* d_rs = reinterpret_cast<int64_t*>(B + o_rs);
+  auto* d_blo = reinterpret_cast<double*>(B + o_blo);
+  auto* d_bhi = reinterpret_cast<double*>(B + o_bhi);
+  auto* d_glo = reinterpret_cast<double*>(B + o_glo);
+  auto* d_ghi = reinterpret_cast<double*>(B + o_ghi);
+  auto* d_init = reinterpret_cast<double*>(B + o_init);
+  auto* d_pr = reinterpret_cast<uint32_t*>(B + o_pr);
+  auto* d_cand = reinterpret_cast<double*>(B + o_cand);
+  auto* d_flag = reinterpret_cast<uint8_t*>(B + o_flag);
+  auto* d_coords = reinterpret_cast<double*>(B + o_coords);
+  auto* d_res = reinterpret_cast<BOut*>(B + o_res);
+  auto* d_cnt = reinterpret_cast<int64_t*>(B + o_cnt);
+  auto* d_rp = reinterpret_cast<int64_t*>(B + o_rp);
+  auto* d_desc = reinterpret_cast<DevInstance*>(B + o_desc);
+  void* d_scan = B + o_scan;
+  auto put = [&](void* dst, const void* src, size_t bytes) -> int {
+    if (bytes) GMT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return GMT_OK;
+  };
+  if ((rc = put(d_probs, probs.data(), sizeof(BProb) * count)) ||
+      (rc = put(d_rs, row_start.data(), sizeof(int64_t) * (count + 1))) ||
+      (rc = put(d_blo, box_lo.data(), sizeof(double) * box_lo.size())) ||
+      (rc = put(d_bhi, box_hi.data(), sizeof(double) * box_hi.size())) ||
+      (rc = put(d_glo, goal_lo.data(), sizeof(double) * goal_lo.size())) ||
+      (rc = put(d_ghi, goal_hi.data(), sizeof(double) * goal_hi.size())) ||
+      (rc = put(d_init, inits.data(), sizeof(double) * inits.size())) ||
+      (rc = put(d_pr, primes.data(), sizeof(uint32_t) * kMaxDimB))) {
+    work.release();
+    return rc;
+  }
+
+  // ---- batched offline phase ------------------------------------------------
+  gen_batch_kernel<<<dim3((max_K + 255) / 256, count), 256, 0, s>>>(d_probs, d_blo, d_bhi, d_pr, d_cand, d_flag);
+  pack_batch_kernel<<<count, 1024, 0, s>>>(d_probs, d_flag, d_cand, d_coords, d_res);
+  int max_n = 0;
+  for (const auto& P : probs) max_n = std::max(max_n, P.n);
+  dedup_batch_kernel<<<dim3((max_n + 255) / 256, count), 256, 0, s>>>(d_probs, d_coords, d_res);
+  goal_init_batch_kernel<<<count, 256, 0, s>>>(d_probs, d_coords, d_glo, d_ghi, d_init, d_res);
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((R + 7) / 8, ctx->sm_count * 16)));
+  GMT_CUDA(launch_rdisk_batch<false>(d, blocks, s, d_probs, d_rs, count, R, d_coords, d_res, d_cnt, nullptr,
+                                     nullptr, nullptr));
+  GMT_CUDA(cudaMemsetAsync(d_cnt + R, 0, sizeof(int64_t), s));
+  GMT_CUDA(cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, d_cnt, d_rp, static_cast<int>(R + 1), s));
+  ctx->launches += 6;
+  int64_t E = 0;
+  std::vector<BOut> res(count);
+  GMT_CUDA(cudaMemcpyAsync(&E, d_rp + R, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  GMT_CUDA(cudaMemcpyAsync(res.data(), d_res, sizeof(BOut) * count, cudaMemcpyDeviceToHost, s));
+  GMT_CUDA(cudaStreamSynchronize(s));
+  Arena edges;
+  rc = edges.reserve(al(sizeof(int32_t) * std::max<int64_t>(E, 1)) + sizeof(double) * std::max<int64_t>(E, 1));
+  if (rc) {
+    work.release();
+    return rc;
+  }
+  auto* d_col = static_cast<int32_t*>(edges.ptr);
+  auto* d_cost = reinterpret_cast<double*>(static_cast<char*>(edges.ptr) + al(sizeof(int32_t) * std::max<int64_t>(E, 1)));
+  GMT_CUDA(launch_rdisk_batch<true>(d, blocks, s, d_probs, d_rs, count, R, d_coords, d_res, nullptr, d_rp, d_col,
+                                    d_cost));
+  desc_batch_kernel<<<(count + 127) / 128, 128, 0, s>>>(d_probs, d_res, d_coords, d_blo, d_bhi, d_glo, d_ghi, d_rp,
+                                                        d_col, d_cost, count, d_desc);
+  GMT_CUDA(cudaGetLastError());
+  ctx->launches += 2;
+
+  // ---- the rare paths: the single-instance builder ---------------------------
+  std::vector<gmt_instance*> single(count, nullptr);
+  std::vector<SolveJob> jobs;
+  std::vector<int> job_q;
+  std::vector<int64_t> node_off(1, 0);
+  int max_V = 0, max_nb = 0;
+  for (int q = 0; q < count; ++q) {
+    status_out[q] = GMT_OK;
+    const DevInstance* inst_ptr = d_desc + q;
+    int V = res[q].V, ii = res[q].init_index;
+    if (res[q].fallback) {
+      rc = gmt_instance_build(ctx, &problems[q], &single[q]);
+      if (rc == GMT_E_GOAL_BLOCKED || rc == GMT_E_INFEASIBLE_SAMPLING) {
+        status_out[q] = rc;  // the query's own build outcome (sampling.cpp:97-141)
+        continue;
+      }
+      if (rc) {
+        for (auto* p : single) gmt_instance_destroy(p);
+        edges.release();
+        work.release();
+        return rc;
+      }
+      inst_ptr = static_cast<const DevInstance*>(single[q]->desc_mem.ptr);
+      V = single[q]->desc.n;
+      ii = single[q]->desc.init_index;
+    }
+    SolveJob job{};
+    job.inst = inst_ptr;
+    job.init_index = ii;
+    job.mode = kModeGmt;
+    job.lambda = problems[q].lambda;
+    job.radius = probs[q].radius;
+    jobs.push_back(job);
+    job_q.push_back(q);
+    node_off.push_back(node_off.back() + V);
+    max_V = std::max(max_V, V);
+    max_nb = std::max(max_nb, probs[q].nb);
+  }
+
+  // ---- one batched solve -----------------------------------------------------
+  const int J = static_cast<int>(jobs.size());
+  if (J > 0) {
+    size_t smem = 0;
+    int obs = 0;
+    const int cluster = ctx->batch_cluster ? ctx->batch_cluster : 1;
+    rc = plan_smem(ctx, max_V, d, max_nb, cluster, &smem, &obs);
+    std::vector<DevResult> rs;
+    ResultScalars* sc = nullptr;
+    if (rc == GMT_OK) rc = carve_results(ctx->res, J, node_off.data(), false, false, rs, &sc, nullptr);
+    if (rc == GMT_OK) {
+      for (int k = 0; k < J; ++k) jobs[k].res = rs[k];
+      rc = launch_jobs(ctx, jobs, cluster, ctx->batch_threads ? ctx->batch_threads : (cluster > 1 ? 512 : 256),
+                       smem, obs, d);
+    }
+    std::vector<ResultScalars> hs(J);
+    if (rc == GMT_OK) {
+      cudaError_t e = cudaMemcpyAsync(hs.data(), sc, sizeof(ResultScalars) * J, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess && path_states && path_cap > 0) {
+        // path states straight from the device (results + instance descriptors)
+        Arena pg;
+        const size_t o_r = 0, o_i = al(sizeof(DevResult) * J), o_o = o_i + al(sizeof(void*) * J);
+        rc = pg.reserve(o_o + sizeof(double) * static_cast<size_t>(J) * path_cap * d);
+        if (rc == GMT_OK) {
+          std::vector<const DevInstance*> ip(J);
+          for (int k = 0; k < J; ++k) ip[k] = jobs[k].inst;
+          char* g = static_cast<char*>(pg.ptr);
+          e = cudaMemcpyAsync(g + o_r, rs.data(), sizeof(DevResult) * J, cudaMemcpyHostToDevice, s);
+          if (e == cudaSuccess) e = cudaMemcpyAsync(g + o_i, ip.data(), sizeof(void*) * J, cudaMemcpyHostToDevice, s);
+          if (e == cudaSuccess) {
+            gather_paths_kernel<<<J, 128, 0, s>>>(reinterpret_cast<const DevResult*>(g + o_r),
+                                                  reinterpret_cast<const DevInstance* const*>(g + o_i), J, path_cap,
+                                                  d, reinterpret_cast<double*>(g + o_o));
+            e = cudaGetLastError();
+            ++ctx->launches;
+          }
+          std::vector<double> hp(static_cast<size_t>(J) * path_cap * d);
+          if (e == cudaSuccess)
+            e = cudaMemcpyAsync(hp.data(), g + o_o, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, s);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+          if (e == cudaSuccess)
+            for (int k = 0; k < J; ++k)
+              std::memcpy(path_states + static_cast<size_t>(job_q[k]) * path_cap * d,
+                          hp.data() + static_cast<size_t>(k) * path_cap * d, sizeof(double) * path_cap * d);
+          pg.release();
+        }
+      }
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) rc = cuda_error(e, "gmt_plan_problems results");
+    }
+    if (rc == GMT_OK) {
+      for (int k = 0; k < J; ++k) {
+        gmt_plan_summary& o = summaries[job_q[k]];
+        o.status = hs[k].status;
+        o.goal_node = hs[k].goal_node;
+        o.cost = hs[k].cost;
+        o.iterations = hs[k].iterations;
+        o.total_collision_checks = hs[k].total_checks;
+        o.path_len = hs[k].path_len;
+        o.num_stats = hs[k].num_stats;
+      }
+    }
+  } else {
+    GMT_CUDA(cudaStreamSynchronize(s));
+  }
+  for (auto* p : single) gmt_instance_destroy(p);
+  edges.release();
+  work.release();
+  return rc;
+}

@@ -55,6 +55,8 @@ SIGNATURES = [
     ("gmt_problem_key", C.c_int, [_P(abi.Problem), _P(C.c_uint64)]),
     ("gmt_dubins_costs", C.c_int, [_vp, _dp, _dp, C.c_int64, C.c_int32, _P(abi.DubinsParams), _dp,
                                    _i32p]),
+    ("gmt_plan_problems", C.c_int, [_vp, _P(abi.Problem), C.c_int32, _i32p, _P(abi.PlanSummary),
+                                    C.c_int32, _dp]),
     ("gmt_run_trial", C.c_int, [_vp, _P(abi.Scenario), C.c_uint64, _P(abi.TrialOutcome), _dp,
                                 C.c_int64]),
     ("gmt_run_campaign", C.c_int, [C.c_int, _P(abi.Scenario), _dp, C.c_int32, _dp, C.c_int32, _dp,
@@ -405,6 +407,23 @@ class Context:
         ii = inst.init_index if init_index is None else init_index
         check(lib().gmt_dijkstra_oracle(self.h, inst.h, ii, C.byref(buf.out)))
         return buf.result()
+
+    def plan_problems(self, specs, path_cap: int = 0):
+        """build_instance + gmt_plan for a batch of Euclidean problems (one
+        batched offline phase, one batched solve).  -> (status codes,
+        summaries, path states [count, path_cap, dim] or None)."""
+        count = len(specs)
+        probs = (abi.Problem * count)()
+        for q, sp in enumerate(specs):
+            probs[q] = sp.flat()
+        status = np.zeros(count, np.int32)
+        summ = (abi.PlanSummary * count)()
+        d = specs[0].dim
+        paths = np.zeros(max(count * path_cap * d, 1)) if path_cap > 0 else None
+        check(lib().gmt_plan_problems(self.h, probs, count, abi.ptr(status, C.c_int32), summ, path_cap,
+                                      abi.ptr(paths, C.c_double)))
+        return status, list(summ), (paths[: count * path_cap * d].reshape(count, path_cap, d)
+                                    if paths is not None else None)
 
     def run_trial(self, scenario, seed: int, path_cap: int = 100000):
         """run_trial (simulator.cpp:66-176) -> (TrialOutcome, path_travelled [k, dim])."""

@@ -1,0 +1,71 @@
+"""GPU: the batched build_instance + gmt_plan (gmt_plan_problems) equals
+gmt_instance_build + gmt_plan problem by problem -- statuses, costs,
+iterations, checks and the path states -- including the problems that take
+sample_free's rare paths (goal substitution, goal blocked, exhausted
+budget), uniform and Halton sampling, and the reference on a sample."""
+import numpy as np
+import pytest
+
+from paper_1705_02403_b200 import abi, problem as P
+from paper_1705_02403_b200.errors import GoalBlockedError, InfeasibleSamplingError
+from helpers import scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _mixed_specs():
+    specs = [P.random_forest_query(20171005, q, n=1500) for q in range(24)]
+    for seed in (3, 9, 27):
+        u = scene("rectangles_2d", 400)
+        u.sampling_kind, u.seed = abi.SAMPLE_UNIFORM, seed
+        specs.append(u)
+    tiny = scene("rectangles_2d", 300)  # goal too small for any sample: substitution
+    tiny.goal_lo, tiny.goal_hi = np.array([0.95, 0.30]), np.array([0.9501, 0.3001])
+    specs.append(tiny)
+    blocked = scene("rectangles_2d", 300)  # goal inside an obstacle: GoalBlockedError
+    blocked.goal_lo, blocked.goal_hi = np.array([0.25, 0.1]), np.array([0.3, 0.2])
+    specs.append(blocked)
+    crowded = scene("rectangles_2d", 200)  # nearly all space blocked: more than the first chunk
+    crowded.box_lo = np.vstack([crowded.box_lo, [[0.0, 0.0]]])
+    crowded.box_hi = np.vstack([crowded.box_hi, [[1.0, 0.97]]])
+    crowded.init = np.array([0.05, 0.99])
+    crowded.goal_lo, crowded.goal_hi = np.array([0.9, 0.98]), np.array([1.0, 1.0])
+    specs.append(crowded)
+    specs.append(scene("maze_3d", 800).with_n(800) if False else P.forest_3d(3, 900))
+    return specs
+
+
+def test_plan_problems_matches_single_builds(ctx):
+    specs = [s for s in _mixed_specs() if s.dim == 3][:20]
+    specs2 = [s for s in _mixed_specs() if s.dim == 2]
+    for group in (specs, specs2):
+        cap = 4096
+        status, summ, paths = ctx.plan_problems(group, path_cap=cap)
+        for q, sp in enumerate(group):
+            try:
+                inst = ctx.build_instance(sp)
+            except GoalBlockedError:
+                assert status[q] == 3
+                continue
+            except InfeasibleSamplingError:
+                assert status[q] == 2
+                continue
+            assert status[q] == 0
+            want = ctx.plan(inst, lam=sp.lam)
+            got = summ[q]
+            assert (got.status, got.iterations, got.total_collision_checks, got.path_len) == (
+                want.status, want.iterations, want.total_collision_checks, len(want.path_indices))
+            assert got.cost == want.cost or (np.isinf(got.cost) and np.isinf(want.cost))
+            if want.status == abi.PLAN_SUCCESS:
+                c, _, _ = inst.download()
+                assert paths[q, :got.path_len].tobytes() == c[want.path_indices].tobytes()
+
+
+def test_plan_problems_matches_reference(ctx, ref):
+    specs = [P.random_forest_query(7, q, n=1200) for q in range(6)]
+    status, summ, _ = ctx.plan_problems(specs)
+    for q, sp in enumerate(specs):
+        want = ref.instance_build(sp).plan(sp.lam)
+        assert status[q] == 0
+        assert (summ[q].status, summ[q].cost, summ[q].iterations, summ[q].total_collision_checks) == (
+            want.status, want.cost, want.iterations, want.total_collision_checks)
