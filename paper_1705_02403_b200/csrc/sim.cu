@@ -288,6 +288,195 @@ int run_trial(gmt_ctx* ctx, const gmt_scenario& cfg, uint64_t trial_seed, gmt_tr
   return GMT_OK;
 }
 
+// ---- lockstep campaigns: many trials, replans batched -----------------------
+// The trial state machine of run_trial (simulator.cpp:66-176) split at its
+// replan points: every trial advances until it needs a plan, the pending
+// plan_from requests of all trials go through ONE gmt_plan_problems call
+// (batched sampling / graphs / solve), and each trial resumes with its
+// result.  Each trial consumes its own generator in exactly the reference's
+// order, so outcomes are identical to run_trial's.
+struct LockTrial {
+  gmt_scenario cfg{};
+  Rng rng{0};
+  Obstacles obstacles;
+  std::vector<double> pos, lo, hi;
+  std::vector<std::vector<double>> plan;
+  size_t waypoint = 1;
+  double t = 0.0, next_replan = 0.0, half = 0.0;
+  bool goal_blocked = false;
+  gmt_trial_outcome o{};
+  int phase = 0;  // 0 initial plan pending, 1 running, 2 replan pending, 3 done
+  uint64_t pending_seed = 0;
+  explicit LockTrial(const gmt_scenario& c, uint64_t seed) : cfg(c), rng(seed) {
+    const int d = cfg.scene.dim;
+    obstacles.d = d;
+    obstacles.lo.assign(cfg.scene.box_lo, cfg.scene.box_lo + static_cast<size_t>(cfg.scene.num_boxes) * d);
+    obstacles.hi.assign(cfg.scene.box_hi, cfg.scene.box_hi + static_cast<size_t>(cfg.scene.num_boxes) * d);
+    pos.assign(cfg.init, cfg.init + d);
+    lo.resize(d);
+    hi.resize(d);
+    o.result = GMT_TRIAL_TIMED_OUT;
+    next_replan = cfg.replan_latency;
+    half = 0.5 * cfg.spawn_box_size;
+    pending_seed = draw_seed(rng);  // the initial plan's seed (simulator.cpp:82)
+  }
+  // After a plan result: the rest of the step, then steps until the next
+  // replan request or the end.
+  void resume(bool found, std::vector<std::vector<double>>&& fresh) {
+    if (phase == 0) {
+      if (!found) {
+        phase = 3;
+        return;
+      }
+      plan = std::move(fresh);
+      waypoint = 1;
+      phase = 1;
+    } else if (phase == 2) {
+      if (found) {
+        plan = std::move(fresh);
+        waypoint = 1;
+      }
+      finish_step();
+      if (phase == 3) return;
+      phase = 1;
+    }
+    run();
+  }
+  void finish_step() {  // (c) bookkeeping + (d) end conditions
+    next_replan += cfg.replan_latency;
+    if (next_replan <= t) next_replan = t + cfg.replan_latency;
+    check_end();
+  }
+  void check_end() {
+    o.time = t;
+    if (!point_free(pos, obstacles)) {
+      o.result = GMT_TRIAL_COLLIDED;
+      phase = 3;
+    } else if (box_contains(cfg.scene.goal_lo, cfg.scene.goal_hi, pos)) {
+      o.result = GMT_TRIAL_REACHED_GOAL;
+      phase = 3;
+    } else if (t >= cfg.time_limit - 1e-9) {
+      o.result = GMT_TRIAL_TIMED_OUT;
+      phase = 3;
+    }
+  }
+  void run() {
+    const int d = cfg.scene.dim;
+    while (phase == 1) {
+      const int events = rng.poisson(cfg.collapse_rate * cfg.control_dt);  // (a)
+      for (int e = 0; e < events; ++e) {
+        for (int attempt = 0; attempt < 1000; ++attempt) {
+          for (int k = 0; k < d; ++k) {
+            const double c = rng.next_double();
+            lo[k] = c - half;
+            hi[k] = c + half;
+          }
+          if (box_contains(lo.data(), hi.data(), pos)) continue;
+          obstacles.lo.insert(obstacles.lo.end(), lo.begin(), lo.end());
+          obstacles.hi.insert(obstacles.hi.end(), hi.begin(), hi.end());
+          ++o.spawned;
+          break;
+        }
+      }
+      double advance = cfg.robot_speed * cfg.control_dt;  // (b)
+      while (advance > 0.0 && waypoint < plan.size()) {
+        const double seg_len = euclid(pos, plan[waypoint]);
+        if (seg_len <= advance) {
+          pos = plan[waypoint];
+          advance -= seg_len;
+          ++waypoint;
+        } else {
+          const double f = advance / seg_len;
+          for (int k = 0; k < d; ++k) pos[k] += f * (plan[waypoint][k] - pos[k]);
+          advance = 0.0;
+        }
+      }
+      if (cfg.disturbance_sigma > 0.0) {
+        double norm_sq = 0.0;
+        for (int k = 0; k < d; ++k) {
+          const double g = std::clamp(rng.gaussian(), -6.0, 6.0);
+          const double dx = g * cfg.disturbance_sigma;
+          pos[k] += dx;
+          norm_sq += dx * dx;
+        }
+        if (std::sqrt(norm_sq) > 3.0 * cfg.disturbance_sigma) ++o.noise_outliers;
+      }
+      for (int k = 0; k < d; ++k) pos[k] = std::clamp(pos[k], 0.0, 1.0);
+      t += cfg.control_dt;
+      if (t >= next_replan - 1e-9) {  // (c)
+        if (!goal_blocked) {
+          ++o.replans;
+          pending_seed = draw_seed(rng);
+          phase = 2;  // wait for the batched plan
+          return;
+        }
+        finish_step();
+      } else {
+        check_end();
+      }
+    }
+  }
+};
+
+int run_lockstep(gmt_ctx* ctx, std::vector<LockTrial>& trials) {
+  const int d = trials.empty() ? 0 : trials[0].cfg.scene.dim;
+  std::vector<gmt_problem> probs;
+  std::vector<int> who;
+  std::vector<int32_t> status;
+  std::vector<gmt_plan_summary> summ;
+  std::vector<double> paths;
+  for (;;) {
+    probs.clear();
+    who.clear();
+    for (size_t k = 0; k < trials.size(); ++k) {
+      LockTrial& T = trials[k];
+      if (T.phase != 0 && T.phase != 2) continue;
+      gmt_problem p{};  // plan_from (simulator.cpp:32-64)
+      p.scene = T.cfg.scene;
+      p.scene.num_boxes = T.obstacles.count();
+      p.scene.box_lo = T.obstacles.lo.data();
+      p.scene.box_hi = T.obstacles.hi.data();
+      p.init = T.pos.data();
+      p.n = T.cfg.n;
+      p.lambda = T.cfg.lambda;
+      p.eta = T.cfg.eta;
+      p.radius_override = T.cfg.radius_override;
+      p.sampling.kind = GMT_SAMPLE_UNIFORM;
+      p.sampling.start_index = 1;
+      p.sampling.seed = T.pending_seed;
+      p.steering = GMT_STEER_EUCLIDEAN;
+      probs.push_back(p);
+      who.push_back(static_cast<int>(k));
+    }
+    if (probs.empty()) return GMT_OK;
+    const int m = static_cast<int>(probs.size());
+    int cap = 0;
+    for (const auto& p : probs) cap = std::max(cap, p.n + 1);
+    status.assign(m, 0);
+    summ.assign(m, gmt_plan_summary{});
+    paths.assign(static_cast<size_t>(m) * cap * d, 0.0);
+    const int rc = gmt_plan_problems(ctx, probs.data(), m, status.data(), summ.data(), cap, paths.data());
+    if (rc) return rc;
+    for (int q = 0; q < m; ++q) {
+      LockTrial& T = trials[who[q]];
+      bool found = false;
+      std::vector<std::vector<double>> fresh;
+      if (status[q] == GMT_E_GOAL_BLOCKED) {
+        T.goal_blocked = true;
+      } else if (status[q] == GMT_OK && summ[q].status == 0) {
+        found = true;
+        for (int k = 0; k < summ[q].path_len; ++k) {
+          const double* s = paths.data() + (static_cast<size_t>(q) * cap + k) * d;
+          fresh.emplace_back(s, s + d);
+        }
+      } else if (status[q] != GMT_OK && status[q] != GMT_E_INFEASIBLE_SAMPLING) {
+        return set_error(status[q], "replan failed");
+      }
+      T.resume(found, std::move(fresh));
+    }
+  }
+}
+
 }  // namespace
 
 }  // namespace gmtb
@@ -340,11 +529,19 @@ extern "C" int gmt_run_campaign(int device, const gmt_scenario* cfg, const doubl
     key = mix64(key, bits_of(cells[c].sigma));
     for (int t = 0; t < cfg->trials; ++t) tasks.push_back({c, mix64(key, static_cast<uint64_t>(t))});
   }
+  for (const Cell& cell : cells) {  // run_trial's parameter check, per cell (simulator.cpp:67-72)
+    gmt_scenario c = *cfg;
+    c.replan_latency = cell.latency;
+    c.collapse_rate = cell.rate;
+    c.disturbance_sigma = cell.sigma;
+    rc = validate_scenario(&c);
+    if (rc) return rc;
+  }
   std::vector<uint8_t> success(tasks.size(), 0);
   const int W = std::max(1, std::min<int>(workers, static_cast<int>(tasks.size())));
-  std::atomic<size_t> next{0};
   std::atomic<int> failed{GMT_OK};
   std::vector<std::string> errors(W);
+  // Worker w runs tasks w, w + W, ... in lockstep (batched replans).
   auto work = [&](int w) {
     gmt_ctx* ctx = nullptr;
     int r = gmt_ctx_create(device, &ctx);
@@ -353,21 +550,26 @@ extern "C" int gmt_run_campaign(int device, const gmt_scenario* cfg, const doubl
       failed = r;
       return;
     }
-    gmtb::AllocScope scope(ctx);
-    std::vector<double> travelled;
-    for (size_t k; (k = next.fetch_add(1)) < tasks.size() && failed == GMT_OK;) {
-      gmt_scenario c = *cfg;
-      c.replan_latency = cells[tasks[k].cell].latency;
-      c.collapse_rate = cells[tasks[k].cell].rate;
-      c.disturbance_sigma = cells[tasks[k].cell].sigma;
-      gmt_trial_outcome o{};
-      r = run_trial(ctx, c, tasks[k].seed, &o, &travelled);
+    {
+      gmtb::AllocScope scope(ctx);
+      std::vector<LockTrial> trials;
+      std::vector<size_t> ids;
+      for (size_t k = static_cast<size_t>(w); k < tasks.size(); k += static_cast<size_t>(W)) {
+        gmt_scenario c = *cfg;
+        c.replan_latency = cells[tasks[k].cell].latency;
+        c.collapse_rate = cells[tasks[k].cell].rate;
+        c.disturbance_sigma = cells[tasks[k].cell].sigma;
+        trials.emplace_back(c, tasks[k].seed);
+        ids.push_back(k);
+      }
+      r = run_lockstep(ctx, trials);
       if (r) {
         errors[w] = gmt_last_error();
         failed = r;
-        break;
+      } else {
+        for (size_t j = 0; j < trials.size(); ++j)
+          success[ids[j]] = trials[j].o.result == GMT_TRIAL_REACHED_GOAL ? 1 : 0;
       }
-      success[k] = o.result == GMT_TRIAL_REACHED_GOAL ? 1 : 0;
     }
     gmt_ctx_destroy(ctx);
   };
