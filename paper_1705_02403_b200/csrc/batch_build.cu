@@ -6,13 +6,14 @@
 //          CandidateStream::draw, sampling.cpp:64-76) and its point_free flag
 //   pack   one CTA per problem: the first n free candidates, in order
 //   dedup  (uniform sampling) any exact duplicate among them
-//   goal   any sample in the goal box; append_init (sampling.cpp:144-154)
+//   goal   any sample in the goal box, else goal substitution (the first
+//          1024 candidates of sampling.cpp:115-141); append_init (:144-154)
 //   rdisk  count / fill of every problem's r-disk rows (graph.cpp:117-188,
 //          the predicate of graph.cu), one global scan in between
 //   desc   the DevInstance of every problem, then ONE batched solve.
 // Problems that need sample_free's rare paths -- more candidates than the
-// first chunk, an exact duplicate, goal substitution (sampling.cpp:115-141),
-// or an infeasible / goal-blocked outcome -- are rebuilt by the
+// first chunk, an exact duplicate, a goal substitution beyond the first
+// 1024 candidates, or an infeasible / goal-blocked outcome -- are rebuilt by the
 // single-instance builder, so every problem's instance is bit-identical to
 // gmt_instance_build's (and the reference's build_instance).
 #include <cuda_runtime.h>
@@ -155,33 +156,100 @@ __global__ void dedup_batch_kernel(const BProb* __restrict__ probs, const double
   }
 }
 
-// Goal membership and append_init (sampling.cpp:110-112, 144-154).
-__global__ void __launch_bounds__(256) goal_init_batch_kernel(const BProb* __restrict__ probs,
-                                                              double* __restrict__ coords,
-                                                              const double* __restrict__ goal_lo,
-                                                              const double* __restrict__ goal_hi,
-                                                              const double* __restrict__ inits,
-                                                              BOut* __restrict__ res) {
-  __shared__ int first;
+// Goal membership (sampling.cpp:110-112).
+__global__ void __launch_bounds__(256) goal_batch_kernel(const BProb* __restrict__ probs,
+                                                         const double* __restrict__ coords,
+                                                         const double* __restrict__ goal_lo,
+                                                         const double* __restrict__ goal_hi, BOut* __restrict__ res) {
   const int p = blockIdx.x;
   const BProb P = probs[p];
   if (res[p].fallback) return;
   const double* glo = goal_lo + static_cast<int64_t>(p) * P.d;
   const double* ghi = goal_hi + static_cast<int64_t>(p) * P.d;
+  bool in_goal = false;
+  for (int i = threadIdx.x; i < P.n; i += blockDim.x)
+    in_goal = in_goal || box_contains(glo, ghi, P.d, coords + (P.row_off + i) * P.d);
+  const int any = __syncthreads_or(in_goal ? 1 : 0);
+  if (threadIdx.x == 0) res[p].goal_any = any;
+}
+
+// Goal substitution (sampling.cpp:115-141) for problems without a goal
+// sample: the first of the goal centre and the goal-box Halton points that
+// is free and no exact duplicate of samples 0 .. n-2 replaces sample n-1.
+// The first kSubst candidates are searched here; beyond them the problem
+// takes the single path.
+constexpr int kSubst = 1024;
+
+__global__ void __launch_bounds__(256) subst_batch_kernel(const BProb* __restrict__ probs,
+                                                          double* __restrict__ coords,
+                                                          const double* __restrict__ box_lo,
+                                                          const double* __restrict__ box_hi,
+                                                          const double* __restrict__ goal_lo,
+                                                          const double* __restrict__ goal_hi,
+                                                          const uint32_t* __restrict__ primes,
+                                                          BOut* __restrict__ res) {
+  __shared__ int best;
+  const int p = blockIdx.x;
+  const BProb P = probs[p];
+  if (res[p].fallback || res[p].goal_any) return;
+  const int d = P.d;
+  const double* glo = goal_lo + static_cast<int64_t>(p) * d;
+  const double* ghi = goal_hi + static_cast<int64_t>(p) * d;
+  if (threadIdx.x == 0) best = 0x7fffffff;
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSubst; i += blockDim.x) {
+    double c[kMaxDimB];
+    if (i == 0) {  // Aabb::center (space.cpp:18-22)
+      for (int k = 0; k < d; ++k) c[k] = __dmul_rn(0.5, __dadd_rn(glo[k], ghi[k]));
+    } else {  // lo + q * (hi - lo) (sampling.cpp:122-124)
+      for (int k = 0; k < d; ++k)
+        c[k] = __dadd_rn(glo[k], __dmul_rn(halton_dev(static_cast<uint64_t>(i), primes[k]), __dsub_rn(ghi[k], glo[k])));
+    }
+    if (!free_point(c, d, box_lo + P.box_off * d, box_hi + P.box_off * d, P.nb)) continue;
+    bool dup = false;
+    for (int j = 0; j < P.n - 1 && !dup; ++j) {
+      const double* q = coords + (P.row_off + j) * d;
+      bool eq = true;
+      for (int k = 0; k < d; ++k) eq = eq && c[k] == q[k];
+      dup = eq;
+    }
+    if (!dup) atomicMin(&best, i);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (best == 0x7fffffff) {
+      res[p].fallback = 1;
+    } else {
+      const int i = best;
+      double* out = coords + (P.row_off + P.n - 1) * d;
+      for (int k = 0; k < d; ++k)
+        out[k] = i == 0 ? __dmul_rn(0.5, __dadd_rn(glo[k], ghi[k]))
+                        : __dadd_rn(glo[k], __dmul_rn(halton_dev(static_cast<uint64_t>(i), primes[k]),
+                                                      __dsub_rn(ghi[k], glo[k])));
+      res[p].goal_any = 1;
+    }
+  }
+}
+
+// append_init (sampling.cpp:144-154): the first exact duplicate of the
+// init, else the init appended as vertex n.
+__global__ void __launch_bounds__(256) init_batch_kernel(const BProb* __restrict__ probs, double* __restrict__ coords,
+                                                         const double* __restrict__ inits, BOut* __restrict__ res) {
+  __shared__ int first;
+  const int p = blockIdx.x;
+  const BProb P = probs[p];
+  if (res[p].fallback) return;
   const double* init = inits + static_cast<int64_t>(p) * P.d;
   if (threadIdx.x == 0) first = 0x7fffffff;
   __syncthreads();
-  bool in_goal = false;
   for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
     const double* c = coords + (P.row_off + i) * P.d;
-    in_goal = in_goal || box_contains(glo, ghi, P.d, c);
     bool eq = true;
     for (int k = 0; k < P.d; ++k) eq = eq && c[k] == init[k];
     if (eq) atomicMin(&first, i);
   }
-  const int any_goal = __syncthreads_or(in_goal ? 1 : 0);
+  __syncthreads();
   if (threadIdx.x == 0) {
-    if (!any_goal) res[p].fallback = 1;  // goal substitution: the single path
     if (first != 0x7fffffff) {
       res[p].init_index = first;
       res[p].V = P.n;
@@ -190,7 +258,6 @@ __global__ void __launch_bounds__(256) goal_init_batch_kernel(const BProb* __res
       res[p].init_index = P.n;
       res[p].V = P.n + 1;
     }
-    res[p].goal_any = any_goal;
   }
 }
 
@@ -307,6 +374,9 @@ __global__ void gather_paths_kernel(const DevResult* __restrict__ rs, const DevI
 // of one problem; each lane loads one target's coordinates once and tests
 // it against all RB rows (RB x fewer coordinate loads); per row the ballot
 // word orders the accepted targets exactly as the one-row kernel does.
+// FILL = false: counts, and the first C accepted targets of every row into
+// the row's scratch slots; FILL = true: only rows with more than C accepted
+// targets are evaluated again, straight into the CSR.
 template <int D, int RB, bool FILL>
 __global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __restrict__ probs,
                                                              const int64_t* __restrict__ row_start, int P_count,
@@ -314,7 +384,9 @@ __global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __rest
                                                              const BOut* __restrict__ res,
                                                              int64_t* __restrict__ counts,
                                                              const int64_t* __restrict__ row_ptr,
-                                                             int32_t* __restrict__ col, double* __restrict__ cost) {
+                                                             int32_t* __restrict__ col, double* __restrict__ cost,
+                                                             int32_t* __restrict__ scol, double* __restrict__ scost,
+                                                             int C) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(blockDim.x >> 5) * gridDim.x;
   const int64_t groups = (R + RB - 1) / RB;
@@ -333,14 +405,18 @@ __global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __rest
     const int rows_here = static_cast<int>(min(static_cast<int64_t>(RB), row_start[p + 1] - r0));
     double a[RB][D];
     int64_t out[RB];
+    bool act[RB];
+    bool any_act = false;
 #pragma unroll
     for (int j = 0; j < RB; ++j) {
       const int u = u0 + j;
-      out[j] = (FILL && j < rows_here) ? row_ptr[r0 + j] : 0;
+      act[j] = j < rows_here && u < V && (!FILL || counts[r0 + j] > C);
+      any_act = any_act || act[j];
+      out[j] = (FILL && act[j]) ? row_ptr[r0 + j] : 0;
 #pragma unroll
-      for (int k = 0; k < D; ++k) a[j][k] = (j < rows_here && u < V) ? __ldg(coords + (P.row_off + u) * D + k) : 0.0;
+      for (int k = 0; k < D; ++k) a[j][k] = act[j] ? __ldg(coords + (P.row_off + u) * D + k) : 0.0;
     }
-    for (int base = 0; base < V; base += 32) {
+    for (int base = 0; any_act && base < V; base += 32) {
       const int v = base + lane;
       double b[D];
 #pragma unroll
@@ -350,7 +426,7 @@ __global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __rest
         const int u = u0 + j;
         bool keep = false;
         double c = 0.0;
-        if (j < rows_here && u < V && v < V && v != u) {
+        if (act[j] && v < V && v != u) {
           double sq = 0.0;
 #pragma unroll
           for (int k = 0; k < D; ++k) {
@@ -363,10 +439,15 @@ __global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __rest
           }
         }
         const uint32_t m = __ballot_sync(kFull, keep);
-        if (FILL && keep) {
+        if (keep) {
           const int64_t slot = out[j] + __popc(m & ((1u << lane) - 1u));
-          col[slot] = v;
-          cost[slot] = c;
+          if (FILL) {
+            col[slot] = v;
+            cost[slot] = c;
+          } else if (slot < C) {
+            scol[(r0 + j) * C + slot] = v;
+            scost[(r0 + j) * C + slot] = c;
+          }
         }
         out[j] += __popc(m);
       }
@@ -386,6 +467,7 @@ __global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __rest
       const BProb& Q = probs[lo2];
       const int uq = static_cast<int>(r - Q.row_off);
       const int Vq = res[lo2].fallback ? 0 : res[lo2].V;
+      if (FILL && counts[r] <= C) continue;
       int64_t o = FILL ? row_ptr[r] : 0;
       if (uq < Vq) {
         double aq[D];
@@ -406,10 +488,15 @@ __global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __rest
             }
           }
           const uint32_t m = __ballot_sync(kFull, keep);
-          if (FILL && keep) {
+          if (keep) {
             const int64_t slot = o + __popc(m & ((1u << lane) - 1u));
-            col[slot] = v;
-            cost[slot] = c;
+            if (FILL) {
+              col[slot] = v;
+              cost[slot] = c;
+            } else if (slot < C) {
+              scol[r * C + slot] = v;
+              scost[r * C + slot] = c;
+            }
           }
           o += __popc(m);
         }
@@ -419,18 +506,37 @@ __global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __rest
   }
 }
 
+// Rows with at most C targets: scratch slots -> CSR.
+__global__ void compact_rows_batch_kernel(const int64_t* __restrict__ counts, const int64_t* __restrict__ row_ptr,
+                                          int64_t R, int C, const int32_t* __restrict__ scol,
+                                          const double* __restrict__ scost, int32_t* __restrict__ col,
+                                          double* __restrict__ cost) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(blockDim.x >> 5) * gridDim.x;
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); r < R; r += warps) {
+    const int64_t n = counts[r];
+    if (n > C) continue;
+    const int64_t o = row_ptr[r];
+    for (int64_t k = lane; k < n; k += 32) {
+      col[o + k] = scol[r * C + k];
+      cost[o + k] = scost[r * C + k];
+    }
+  }
+}
+
 template <bool FILL>
 cudaError_t launch_rdisk_batch(int d, int blocks, cudaStream_t s, const BProb* probs, const int64_t* row_start,
                                int P_count, int64_t R, const double* coords, const BOut* res, int64_t* counts,
-                               const int64_t* row_ptr, int32_t* col, double* cost) {
+                               const int64_t* row_ptr, int32_t* col, double* cost, int32_t* scol, double* scost,
+                               int C) {
   switch (d) {
     case 2:
       rdisk_batch_rb_kernel<2, 8, FILL><<<blocks, 256, 0, s>>>(probs, row_start, P_count, R, coords, res, counts,
-                                                               row_ptr, col, cost);
+                                                               row_ptr, col, cost, scol, scost, C);
       break;
     case 3:
       rdisk_batch_rb_kernel<3, 8, FILL><<<blocks, 256, 0, s>>>(probs, row_start, P_count, R, coords, res, counts,
-                                                               row_ptr, col, cost);
+                                                               row_ptr, col, cost, scol, scost, C);
       break;
     default:
       rdisk_batch_kernel<0, FILL><<<blocks, 256, 0, s>>>(probs, row_start, P_count, R, coords, res, counts,
@@ -535,6 +641,21 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   const size_t o_cnt = take(sizeof(int64_t) * (R + 1));
   const size_t o_rp = take(sizeof(int64_t) * (R + 1));
   const size_t o_desc = take(sizeof(DevInstance) * count);
+  // Row scratch for d <= 3: the first C accepted targets of every row are
+  // kept from the counting pass, so only rows with more than C are
+  // evaluated twice.  C ~ twice the expected degree of the densest problem.
+  int C = -1;
+  if (d <= 3) {
+    double deg = 0.0;
+    for (const auto& P : probs) {
+      double vol = 0.0;
+      gmt_unit_ball_volume(d, &vol);
+      deg = std::max(deg, vol * std::pow(P.radius, d) * (P.n + 1));
+    }
+    C = static_cast<int>(std::min(256.0, std::max(32.0, 2.0 * deg + 32.0)));
+  }
+  const size_t o_scol = take(C > 0 ? sizeof(int32_t) * static_cast<size_t>(R) * C : 0);
+  const size_t o_scost = take(C > 0 ? sizeof(double) * static_cast<size_t>(R) * C : 0);
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, static_cast<int64_t*>(nullptr),
                                 static_cast<int64_t*>(nullptr), static_cast<int>(R + 1));
@@ -559,6 +680,8 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   auto* d_rp = reinterpret_cast<int64_t*>(B + o_rp);
   auto* d_desc = reinterpret_cast<DevInstance*>(B + o_desc);
   void* d_scan = B + o_scan;
+  auto* d_scol = C > 0 ? reinterpret_cast<int32_t*>(B + o_scol) : nullptr;
+  auto* d_scost = C > 0 ? reinterpret_cast<double*>(B + o_scost) : nullptr;
   auto put = [&](void* dst, const void* src, size_t bytes) -> int {
     if (bytes) GMT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return GMT_OK;
@@ -581,13 +704,15 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   int max_n = 0;
   for (const auto& P : probs) max_n = std::max(max_n, P.n);
   dedup_batch_kernel<<<dim3((max_n + 255) / 256, count), 256, 0, s>>>(d_probs, d_coords, d_res);
-  goal_init_batch_kernel<<<count, 256, 0, s>>>(d_probs, d_coords, d_glo, d_ghi, d_init, d_res);
+  goal_batch_kernel<<<count, 256, 0, s>>>(d_probs, d_coords, d_glo, d_ghi, d_res);
+  subst_batch_kernel<<<count, 256, 0, s>>>(d_probs, d_coords, d_blo, d_bhi, d_glo, d_ghi, d_pr, d_res);
+  init_batch_kernel<<<count, 256, 0, s>>>(d_probs, d_coords, d_init, d_res);
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((R + 7) / 8, ctx->sm_count * 16)));
   GMT_CUDA(launch_rdisk_batch<false>(d, blocks, s, d_probs, d_rs, count, R, d_coords, d_res, d_cnt, nullptr,
-                                     nullptr, nullptr));
+                                     nullptr, nullptr, d_scol, d_scost, C));
   GMT_CUDA(cudaMemsetAsync(d_cnt + R, 0, sizeof(int64_t), s));
   GMT_CUDA(cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, d_cnt, d_rp, static_cast<int>(R + 1), s));
-  ctx->launches += 6;
+  ctx->launches += 8;
   int64_t E = 0;
   std::vector<BOut> res(count);
   GMT_CUDA(cudaMemcpyAsync(&E, d_rp + R, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -601,8 +726,12 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   }
   auto* d_col = static_cast<int32_t*>(edges.ptr);
   auto* d_cost = reinterpret_cast<double*>(static_cast<char*>(edges.ptr) + al(sizeof(int32_t) * std::max<int64_t>(E, 1)));
-  GMT_CUDA(launch_rdisk_batch<true>(d, blocks, s, d_probs, d_rs, count, R, d_coords, d_res, nullptr, d_rp, d_col,
-                                    d_cost));
+  if (C > 0) {
+    compact_rows_batch_kernel<<<blocks, 256, 0, s>>>(d_cnt, d_rp, R, C, d_scol, d_scost, d_col, d_cost);
+    ++ctx->launches;
+  }
+  GMT_CUDA(launch_rdisk_batch<true>(d, blocks, s, d_probs, d_rs, count, R, d_coords, d_res, d_cnt, d_rp, d_col,
+                                    d_cost, d_scol, d_scost, C));
   desc_batch_kernel<<<(count + 127) / 128, 128, 0, s>>>(d_probs, d_res, d_coords, d_blo, d_bhi, d_glo, d_ghi, d_rp,
                                                         d_col, d_cost, count, d_desc);
   GMT_CUDA(cudaGetLastError());
