@@ -14,9 +14,14 @@ so no step reads a graph another step left in L2).
 
   value      plans/s over all ranks, device-resident inputs (CUDA events on
              the library stream, max over ranks)
-  e2e        the same metric through the C ABI drop-in gmt_plan_batch_host:
+  e2e        the same metric end to end from problem descriptions through
+             gmt_plan_problems: the step's scenes (boxes, goal, init, n,
+             sampling) go in from the host, the whole offline phase (sampling,
+             init append, r-disk graphs) and the batched solve run on the
+             device inside the timed region, summaries come back
+  e2e_host_graphs  the same through the C ABI drop-in gmt_plan_batch_host:
              host-resident (pinned) samples + CSR graphs copied H2D, solved,
-             summaries + paths + full trees copied D2H inside the timed region
+             summaries + paths + full trees copied D2H (PCIe-bound)
   p50        single-query latency of the canonical C2 instance (Pcg32(3)
              forest) on a cluster of CTAs, p50 over --single-reps launches
   roofline   HBM roofline of the solve kernel with SURVEY.md §8(d)'s
@@ -294,13 +299,31 @@ def run_b200(args):
         plan_batch_host(ctx, pb, 1.0)  # synchronous: returns with results on the host
         t.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(sum(t))
-    e2e_value = world * Q * e2e_steps / e2e_s
+    e2e_graph_value = world * Q * e2e_steps / e2e_s
+    # ---- e2e from problem descriptions: gmt_plan_problems (the step's scenes
+    # in, summaries out; the offline phase -- sampling, init append, r-disk
+    # graphs -- is inside the timed region, batched on the device) ----------
+    for _ in range(max(1, args.warmup)):
+        ctx.plan_problems(specs)
+    barrier_sync()
+    tp = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        pst, psum, _ = ctx.plan_problems(specs)
+        tp.append(time.perf_counter() - t0)
+    e2e_value = world * Q * e2e_steps / max_over_ranks(sum(tp))
+    prob_h2d = sum(96 + 8 + 16 * s.dim * s.num_boxes + 24 * s.dim for s in specs)
+    prob_d2h = Q * (40 + 16) + 8
     # parity spot check of the e2e results against the device-resident ones
     dev0 = batch.summaries()
     mism = sum(1 for a, b in zip(dev0, pb.summaries) if (a.status, a.cost, a.iterations) !=
                (b.status, b.cost, b.iterations))
     if mism:
         raise SystemExit(f"e2e results differ from device-resident results in {mism} queries")
+    mism = sum(1 for a, st, b in zip(dev0, pst, psum) if st != 0 or (a.status, a.cost, a.iterations) !=
+               (b.status, b.cost, b.iterations))
+    if mism:
+        raise SystemExit(f"problem-path results differ from device-resident results in {mism} queries")
 
     # ---- single-query latency (configs[1] canonical instance) -------------
     def single_p50(inst):
@@ -412,8 +435,12 @@ def run_b200(args):
             "double_integrator_6d": di,
             "quadrotor_12d": quad,
             "single_solve_ms": single,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": pb.h2d_bytes,
-                    "d2h_bytes_per_step": pb.d2h_bytes},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": prob_h2d,
+                    "d2h_bytes_per_step": prob_d2h,
+                    "path": "gmt_plan_problems: scenes in (host), summaries out; offline build + solve timed"},
+            "e2e_host_graphs": {"value": e2e_graph_value, "unit": UNIT, "h2d_bytes_per_step": pb.h2d_bytes,
+                                "d2h_bytes_per_step": pb.d2h_bytes,
+                                "path": "gmt_plan_batch_host: host samples + CSR graphs in, summaries/paths/trees out"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_kind": peak_kind,
