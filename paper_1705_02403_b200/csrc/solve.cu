@@ -62,6 +62,9 @@ constexpr double kSepMargin = 1e-9;  // see segment_free_staged
 #ifndef GMT_ROWS_PER_WARP
 #define GMT_ROWS_PER_WARP 2
 #endif
+#ifndef GMT_ROWS_CLUSTER
+#define GMT_ROWS_CLUSTER 1
+#endif
 
 // Longest of the rows the kRows lane groups of a warp are streaming.
 template <int kRows>
@@ -462,7 +465,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   // Rows streamed concurrently per warp in P4/P5: two for batched
   // single-CTA solves (latency hiding), one for clusters (few candidates per
   // warp; the pass critical path matters).
-  constexpr int kRows = CS == 1 ? GMT_ROWS_PER_WARP : 1;
+  constexpr int kRows = CS == 1 ? GMT_ROWS_PER_WARP : GMT_ROWS_CLUSTER;
   constexpr int kLanesPerRow = kWarp / kRows;
   constexpr int kUnroll = CS == 1 ? GMT_UNROLL_BATCH : GMT_UNROLL_CLUSTER;
   constexpr bool kDynamic = CS > 1;  // dynamic row / candidate distribution

@@ -69,3 +69,19 @@ def test_plan_problems_matches_reference(ctx, ref):
         assert status[q] == 0
         assert (summ[q].status, summ[q].cost, summ[q].iterations, summ[q].total_collision_checks) == (
             want.status, want.cost, want.iterations, want.total_collision_checks)
+
+
+def test_plan_problems_generic_dimension_and_errors(ctx):
+    """d = 6 takes the generic r-disk kernel (no row scratch); steering
+    models other than Euclidean and mixed dimensions are rejected."""
+    specs = [scene("rectangles_6d", 400 + 50 * k) for k in range(4)]
+    status, summ, _ = ctx.plan_problems(specs)
+    for q, sp in enumerate(specs):
+        want = ctx.plan(ctx.build_instance(sp), lam=sp.lam)
+        assert status[q] == 0
+        assert (summ[q].status, summ[q].cost, summ[q].iterations) == (want.status, want.cost, want.iterations)
+    from paper_1705_02403_b200.errors import InvalidInputError
+    with pytest.raises(InvalidInputError):
+        ctx.plan_problems([P.di_forest(3, 300)])
+    with pytest.raises(InvalidInputError):
+        ctx.plan_problems([scene("rectangles_2d", 200), scene("rectangles_3d", 200)])
