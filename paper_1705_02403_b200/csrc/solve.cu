@@ -624,6 +624,11 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   const bool counting = R.counters != nullptr;
   int cnt_open = 0;
 
+#ifdef GMT_PHASE_TIMING
+  __shared__ long long sh_ph[4];
+  long long ph_t = clock64();
+  if (tid == 0) sh_ph[0] = sh_ph[1] = sh_ph[2] = sh_ph[3] = 0;
+#endif
   for (;;) {
     long long i = sh.iter;  // written by tid 0 only, behind the pass barriers
     if (job.mode == kModeFmt) {
@@ -709,6 +714,9 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       }
     }
 
+#ifdef GMT_PHASE_TIMING
+    if (tid == 0) { const long long t_ = clock64(); sh_ph[0] += t_ - ph_t; ph_t = t_; }
+#endif
     // Rows are processed kRows at a time per warp: lane group h (lanes
     // kLanesPerRow*h ...) streams row k + h, so kRows rows' loads are in
     // flight together.
@@ -785,6 +793,9 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       }
     }
     cluster_barrier<CS>();  // [1] candidate marks complete
+#ifdef GMT_PHASE_TIMING
+    if (tid == 0) { const long long t_ = clock64(); sh_ph[1] += t_ - ph_t; ph_t = t_; }
+#endif
 
     // Own candidates (words w = rank mod CS) -> list.
     for (int w = rank + CS * tid; w < W; w += CS * nt) {
@@ -802,6 +813,9 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
     }
     __syncthreads();
     const int ccount = sh.cand_count;
+#ifdef GMT_PHASE_TIMING
+    if (tid == 0) { const long long t_ = clock64(); sh_ph[2] += t_ - ph_t; ph_t = t_; }
+#endif
 
     // P5 + P6: connect_candidate (planner.cpp:62-90) and commit (178-189).
     // Half h scans candidate k + h's in-row and reduces its (cost, position)
@@ -975,6 +989,9 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       }
     }
     cluster_barrier<CS>();  // [2] commits visible in every replica
+#ifdef GMT_PHASE_TIMING
+    if (tid == 0) { const long long t_ = clock64(); sh_ph[3] += t_ - ph_t; ph_t = t_; }
+#endif
 
     if (rank == 0 && tid == 0) {  // IterationStats (planner.cpp:192-194)
       if (R.group_sizes) {
@@ -1007,6 +1024,11 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
     __syncthreads();
   }
 
+#ifdef GMT_PHASE_TIMING
+  if (tid == 0 && rank == 0 && R.counters)
+    for (int k = 0; k < 4; ++k)
+      atomicAdd(reinterpret_cast<unsigned long long*>(R.counters) + 4 + k, static_cast<unsigned long long>(sh_ph[k]));
+#endif
   if (counting) {
     long long c = cnt_open;
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
