@@ -751,13 +751,13 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         }
         const int lmax = rows_max<kRows>(len);
         if (counting && hl == 0 && len > 0) atomicAdd(&sh.cnt_out, static_cast<unsigned long long>(len));
+        const int32_t* ocol = I.out_col + e0 + hl;  // lane base pointer (see P5)
+        const int lim = len - hl;
         for (int off = 0; off < lmax; off += kLanesPerRow * kUnroll) {
           int xs[kUnroll];
 #pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
-            const int p = off + u * kLanesPerRow + hl;
-            xs[u] = p < len ? __ldg(I.out_col + e0 + p) : -1;
-          }
+          for (int u = 0; u < kUnroll; ++u)
+            xs[u] = off + u * kLanesPerRow < lim ? __ldg(ocol + off + u * kLanesPerRow) : -1;
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
             if (off + u * kLanesPerRow >= lmax) break;  // warp-uniform
@@ -859,32 +859,33 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         int by = -1;
         const int lmax = rows_max<kRows>(len);
         if (counting && hl == 0 && len > 0) atomicAdd(&sh.cnt_in, static_cast<unsigned long long>(len));
+        // Lane base pointers, formed once per row: the chunk loads below are
+        // then immediate offsets from them (no per-element address math).
+        const int32_t* rcol = I.in_col + e0 + hl;
+        const double* rcost = I.in_cost + e0 + hl;
+        const int lim = len - hl;  // element u of chunk `off` exists iff off + u * kLanesPerRow < lim
         for (int off = 0; off < lmax; off += kLanesPerRow * kUnroll) {
           int ys[kUnroll];
           double cs[kUnroll];
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
-            const int p = off + u * kLanesPerRow + hl;
-            ys[u] = -1;
-            cs[u] = 0.0;
-            if (p < len) {
-              ys[u] = __ldg(I.in_col + e0 + p);
-              cs[u] = __ldg(I.in_cost + e0 + p);
-            }
+            const bool in = off + u * kLanesPerRow < lim;
+            ys[u] = in ? __ldg(rcol + off + u * kLanesPerRow) : -1;
+            cs[u] = in ? __ldg(rcost + off + u * kLanesPerRow) : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
+            // Branch-free: the open bit and the (always in-bounds) cost
+            // gather are formed for every element, the min update predicated.
             const int y = ys[u];
-            if (y >= 0) {
-              if ((open_w[y >> 5] >> (y & 31)) & 1u) {
-                ++cnt_open;
-                const double c = __dadd_rn(cost_s[y], cs[u]);
-                if (c < bv) {
-                  bv = c;
-                  bo = off + u * kLanesPerRow + hl;
-                  by = y;
-                }
-              }
+            const int ys0 = y >= 0 ? y : 0;
+            const bool op = y >= 0 && ((open_w[ys0 >> 5] >> (ys0 & 31)) & 1u);
+            cnt_open += op ? 1 : 0;
+            const double c = __dadd_rn(cost_s[ys0], cs[u]);
+            if (op && c < bv) {
+              bv = c;
+              bo = off + u * kLanesPerRow + hl;
+              by = y;
             }
           }
         }
