@@ -557,7 +557,8 @@ int launch_jobs(gmt_ctx* ctx, const std::vector<SolveJob>& jobs, int cluster, in
   GMT_CUDA(cudaMemcpyAsync(ctx->jobs.ptr, ctx->pinned_jobs.ptr, bytes, cudaMemcpyHostToDevice,
                            ctx->stream));
   const cudaError_t e = launch_solve(static_cast<const SolveJob*>(ctx->jobs.ptr), static_cast<int>(jobs.size()),
-                                     cluster, threads, smem, obs_in_smem, dim, ctx->stream);
+                                     cluster, threads, smem, obs_in_smem, dim, ctx->stream,
+                                     jobs[0].res.counters != nullptr);
   if (e != cudaSuccess) {
     return set_error(GMT_E_CUDA, std::string("solve launch (cluster ") + std::to_string(cluster) + ", " +
                                      std::to_string(threads) + " threads, " + std::to_string(smem) +
@@ -792,7 +793,8 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
 extern "C" int gmt_batch_launch(gmt_ctx* ctx, gmt_batch* b) {
   gmtb::AllocScope alloc_scope_(ctx);
   GMT_CUDA(launch_solve(static_cast<const SolveJob*>(b->jobs_mem.ptr), static_cast<int>(b->jobs.size()),
-                        b->cluster, b->threads, b->smem, b->obs, b->dim, ctx->stream));
+                        b->cluster, b->threads, b->smem, b->obs, b->dim, ctx->stream,
+                        b->jobs[0].res.counters != nullptr));
   ++ctx->launches;
   return GMT_OK;
 }
@@ -957,7 +959,7 @@ extern "C" int gmt_plan_batch_host(gmt_ctx* ctx, const gmt_batch_host* B, double
     GMT_CUDA(cudaEventRecord(ctx->copy_done[ch], cs));
     GMT_CUDA(cudaStreamWaitEvent(s, ctx->copy_done[ch], 0));
     GMT_CUDA(launch_solve(static_cast<const SolveJob*>(ctx->jobs.ptr) + q0, q1 - q0, cluster, threads,
-                          smem, obs, d, s));
+                          smem, obs, d, s, jobs[q0].res.counters != nullptr));
     ++ctx->launches;
     auto get = [&](void* dst, const void* src, size_t elem, int64_t first, int64_t last) -> int {
       if (!dst || last <= first) return GMT_OK;

@@ -259,7 +259,9 @@ __device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const doubl
       bool miss = false;
       double t0 = 0.0, t1 = 1.0;
       if (slot < take) {
-        const int bi = i0 + static_cast<int>(__fns(cm, 0, slot + 1));
+        uint32_t mm = cm;  // the slot-th surviving box (slot < take, usually 0-2)
+        for (int t = 0; t < slot; ++t) mm &= mm - 1u;
+        const int bi = i0 + __ffs(mm) - 1;
         const double ak = a[axis];
         const double dk = __dsub_rn(b[axis], ak);
         const double l = bx.lo[bi * bx.bs + axis * bx.as], h = bx.hi[bi * bx.bs + axis * bx.as];
@@ -289,7 +291,7 @@ __device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const doubl
       }
       hit = __any_sync(kFull, axis == 0 && slot < take && !m && !(tmin > tmax));
       if (hit || take == nc) break;
-      cm &= ~((1u << __fns(cm, 0, take + 1)) - 1u);  // drop the `take` boxes done
+      for (int t = 0; t < take; ++t) cm &= cm - 1u;  // drop the `take` boxes done
     }
   }
   return !hit;
@@ -455,7 +457,10 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 #ifndef GMT_BATCH_MIN_BLOCKS
 #define GMT_BATCH_MIN_BLOCKS 4
 #endif
-template <int CS, int D, bool WIDE>
+// COUNT: single-CTA solves count the open-source gathers only in the
+// instantiation launched while traffic counters are on (GMT_OPT_COUNTERS);
+// cluster solves always can.
+template <int CS, int D, bool WIDE, bool COUNT>
 __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLOCKS)
     gmt_solve_kernel(const SolveJob* __restrict__ jobs, int obs_in_smem) {
   constexpr bool kParentSmem = CS > 1;  // single-CTA solves keep parents in HBM
@@ -880,7 +885,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
             const int y = ys[u];
             const int ys0 = y >= 0 ? y : 0;
             const bool op = y >= 0 && ((open_w[ys0 >> 5] >> (ys0 & 31)) & 1u);
-            cnt_open += op ? 1 : 0;
+            if constexpr (COUNT || CS > 1) cnt_open += op ? 1 : 0;
             const double c = __dadd_rn(cost_s[ys0], cs[u]);
             if (op && c < bv) {
               bv = c;
@@ -1277,10 +1282,10 @@ cudaError_t launch_dijkstra(const DevInstance* inst, const SolveJob* job, int n,
   }
 }
 
-template <int CS, int D, bool WIDE>
+template <int CS, int D, bool WIDE, bool COUNT>
 static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_t smem,
                              int obs_in_smem, cudaStream_t stream) {
-  auto kern = gmt_solve_kernel<CS, D, WIDE>;
+  auto kern = gmt_solve_kernel<CS, D, WIDE, COUNT>;
   // Function attributes are process-wide: the dynamic shared-memory limit
   // only ever grows (under a lock), so concurrent launches from several host
   // threads (each with its own context / stream) never see it shrink below
@@ -1319,21 +1324,24 @@ static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_
   return cudaLaunchKernelEx(&cfg, kern, jobs, obs_in_smem);
 }
 
-template <int CS, bool WIDE>
+template <int CS, bool WIDE, bool COUNT = false>
 static cudaError_t launch_dim(const SolveJob* jobs, int count, int threads, size_t smem,
                               int obs_in_smem, int dim, cudaStream_t stream) {
   switch (dim) {
-    case 2: return launch_cs<CS, 2, WIDE>(jobs, count, threads, smem, obs_in_smem, stream);
-    case 3: return launch_cs<CS, 3, WIDE>(jobs, count, threads, smem, obs_in_smem, stream);
-    case 6: return launch_cs<CS, 6, WIDE>(jobs, count, threads, smem, obs_in_smem, stream);
-    default: return launch_cs<CS, 0, WIDE>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 2: return launch_cs<CS, 2, WIDE, COUNT>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 3: return launch_cs<CS, 3, WIDE, COUNT>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 6: return launch_cs<CS, 6, WIDE, COUNT>(jobs, count, threads, smem, obs_in_smem, stream);
+    default: return launch_cs<CS, 0, WIDE, COUNT>(jobs, count, threads, smem, obs_in_smem, stream);
   }
 }
 
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
-                         int obs_in_smem, int dim, cudaStream_t stream) {
+                         int obs_in_smem, int dim, cudaStream_t stream, bool count_traffic) {
   switch (cluster) {
     case 1:
+      if (count_traffic)
+        return threads > 256 ? launch_dim<1, true, true>(jobs, count, threads, smem, obs_in_smem, dim, stream)
+                             : launch_dim<1, false, true>(jobs, count, threads, smem, obs_in_smem, dim, stream);
       return threads > 256 ? launch_dim<1, true>(jobs, count, threads, smem, obs_in_smem, dim, stream)
                            : launch_dim<1, false>(jobs, count, threads, smem, obs_in_smem, dim, stream);
     case 2: return launch_dim<2, true>(jobs, count, threads, smem, obs_in_smem, dim, stream);

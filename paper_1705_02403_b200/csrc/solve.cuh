@@ -52,8 +52,9 @@ __host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool o
 
 // dim: the common dimension of every job (selects the specialised kernel;
 // 0 = generic).
+// count_traffic: the jobs carry traffic counters (GMT_OPT_COUNTERS).
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
-                         int obs_in_smem, int dim, cudaStream_t stream);
+                         int obs_in_smem, int dim, cudaStream_t stream, bool count_traffic = false);
 
 // dijkstra_oracle (planner.cpp:264-334): eager edge checks into ok[E] (and
 // the check count), then the Dijkstra search for job[0] (one CTA).
