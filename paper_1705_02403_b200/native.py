@@ -125,6 +125,21 @@ def check(rc: int) -> None:
         raise_for(rc, lib().gmt_last_error().decode())
 
 
+class ProblemBatch:
+    """gmt_problem structs of many ProblemSpecs, flattened once (the specs
+    keep the arrays the structs point to alive)."""
+
+    def __init__(self, specs):
+        self.specs = list(specs)
+        self.count = len(self.specs)
+        self.dim = self.specs[0].dim
+        self.array = (abi.Problem * self.count)()
+        self._keep = []
+        for q, sp in enumerate(self.specs):
+            self.array[q] = sp.flat()
+            self._keep.append(sp._keep)  # the arrays this struct points to
+
+
 class Instance:
     """A device-resident ProblemInstance (problem.hpp:52-57)."""
 
@@ -410,15 +425,15 @@ class Context:
 
     def plan_problems(self, specs, path_cap: int = 0):
         """build_instance + gmt_plan for a batch of Euclidean problems (one
-        batched offline phase, one batched solve).  -> (status codes,
+        batched offline phase, one batched solve).  `specs`: ProblemSpecs or
+        a ProblemBatch (flattened once, reusable).  -> (status codes,
         summaries, path states [count, path_cap, dim] or None)."""
-        count = len(specs)
-        probs = (abi.Problem * count)()
-        for q, sp in enumerate(specs):
-            probs[q] = sp.flat()
+        pb = specs if isinstance(specs, ProblemBatch) else ProblemBatch(specs)
+        count = pb.count
+        probs = pb.array
         status = np.zeros(count, np.int32)
         summ = (abi.PlanSummary * count)()
-        d = specs[0].dim
+        d = pb.dim
         paths = np.zeros(max(count * path_cap * d, 1)) if path_cap > 0 else None
         check(lib().gmt_plan_problems(self.h, probs, count, abi.ptr(status, C.c_int32), summ, path_cap,
                                       abi.ptr(paths, C.c_double)))
