@@ -23,7 +23,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -53,12 +56,14 @@ constexpr int kMaxDimB = 16;
   } while (0)
 
 struct BProb {
-  int kind, d, dd, nb, n, K, need_dedup, pad;
+  int kind, d, dd, nb, n, K, need_dedup, G;  // G: grid cells per axis (r-disk binning)
   uint64_t start_index, s0;
   int64_t box_off;   // first box of the problem
   int64_t cand_off;  // first candidate row
   int64_t row_off;   // first coordinate row (n + 1 rows reserved)
+  int64_t cell_off;  // first entry of the problem's cell_start array (G^d + 1 entries)
   double radius, r2_hi;
+  double r2_lo;  // sq <= r2_lo implies sqrt_rn(sq) <= radius (no square root needed)
 };
 
 // Per-problem outcome of the batched stages.
@@ -188,44 +193,63 @@ __global__ void __launch_bounds__(256) subst_batch_kernel(const BProb* __restric
                                                           const double* __restrict__ goal_hi,
                                                           const uint32_t* __restrict__ primes,
                                                           BOut* __restrict__ res) {
-  __shared__ int best;
+  __shared__ int best, dup;
   const int p = blockIdx.x;
   const BProb P = probs[p];
   if (res[p].fallback || res[p].goal_any) return;
   const int d = P.d;
   const double* glo = goal_lo + static_cast<int64_t>(p) * d;
   const double* ghi = goal_hi + static_cast<int64_t>(p) * d;
-  if (threadIdx.x == 0) best = 0x7fffffff;
-  __syncthreads();
-  for (int i = threadIdx.x; i < kSubst; i += blockDim.x) {
-    double c[kMaxDimB];
+  auto candidate = [&](int i, double* c) {
     if (i == 0) {  // Aabb::center (space.cpp:18-22)
       for (int k = 0; k < d; ++k) c[k] = __dmul_rn(0.5, __dadd_rn(glo[k], ghi[k]));
     } else {  // lo + q * (hi - lo) (sampling.cpp:122-124)
       for (int k = 0; k < d; ++k)
         c[k] = __dadd_rn(glo[k], __dmul_rn(halton_dev(static_cast<uint64_t>(i), primes[k]), __dsub_rn(ghi[k], glo[k])));
     }
-    if (!free_point(c, d, box_lo + P.box_off * d, box_hi + P.box_off * d, P.nb)) continue;
-    bool dup = false;
-    for (int j = 0; j < P.n - 1 && !dup; ++j) {
+  };
+  // The first free candidate that duplicates no sample: the first free one is
+  // found block-wide, then checked against the samples block-wide (an exact
+  // duplicate is rare; the search then resumes after it).
+  int last = -1, found = -1;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      best = 0x7fffffff;
+      dup = 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSubst; i += blockDim.x) {
+      if (i <= last) continue;
+      double c[kMaxDimB];
+      candidate(i, c);
+      if (free_point(c, d, box_lo + P.box_off * d, box_hi + P.box_off * d, P.nb)) atomicMin(&best, i);
+    }
+    __syncthreads();
+    const int b = best;
+    if (b == 0x7fffffff) break;
+    double c[kMaxDimB];
+    candidate(b, c);
+    for (int j = threadIdx.x; j < P.n - 1; j += blockDim.x) {
       const double* q = coords + (P.row_off + j) * d;
       bool eq = true;
       for (int k = 0; k < d; ++k) eq = eq && c[k] == q[k];
-      dup = eq;
+      if (eq) dup = 1;
     }
-    if (!dup) atomicMin(&best, i);
+    __syncthreads();
+    const int was_dup = dup;
+    __syncthreads();  // everyone has read best / dup before the next round resets them
+    if (!was_dup) {
+      found = b;
+      break;
+    }
+    last = b;
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    if (best == 0x7fffffff) {
+    if (found < 0) {
       res[p].fallback = 1;
     } else {
-      const int i = best;
       double* out = coords + (P.row_off + P.n - 1) * d;
-      for (int k = 0; k < d; ++k)
-        out[k] = i == 0 ? __dmul_rn(0.5, __dadd_rn(glo[k], ghi[k]))
-                        : __dadd_rn(glo[k], __dmul_rn(halton_dev(static_cast<uint64_t>(i), primes[k]),
-                                                      __dsub_rn(ghi[k], glo[k])));
+      candidate(found, out);
       res[p].goal_any = 1;
     }
   }
@@ -506,6 +530,230 @@ __global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __rest
   }
 }
 
+// ---- r-disk rows through a uniform grid (d = 2, 3) ---------------------------
+// Cells of side 1/G >= r / kGridReach (slightly more, against rounding), so
+// every target within r of u lies in the (2 kGridReach + 1)^d cells around
+// u's cell.  A CTA takes one cell
+// of one problem; a warp marks, for up to 8 rows of that cell at once, the
+// accepted targets of the neighbour cells in per-row bitmasks (the exact
+// predicate of rdisk_batch_kernel), then emits every row in target order
+// from its bitmask, recomputing the accepted costs -- so rows are
+// bit-identical to the brute-force scan.
+constexpr int kGridMaxCells = 4096;
+constexpr int kGridMaxV = 8192;
+#ifndef GMT_GRID_ROWS
+#define GMT_GRID_ROWS 8
+#endif
+constexpr int kGridRows = GMT_GRID_ROWS;
+constexpr int kGridReach = 2;
+constexpr int kGridSpan = 2 * kGridReach + 1;
+
+template <int D>
+__device__ __forceinline__ int grid_cell(const double* c, int G) {
+  int cell = 0, mul = 1;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    int q = static_cast<int>(floor(c[k] * G));
+    q = q < 0 ? 0 : (q >= G ? G - 1 : q);
+    cell += q * mul;
+    mul *= G;
+  }
+  return cell;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) grid_build_kernel(const BProb* __restrict__ probs,
+                                                         const double* __restrict__ coords,
+                                                         const BOut* __restrict__ res,
+                                                         int32_t* __restrict__ cell_start,
+                                                         int32_t* __restrict__ cell_list) {
+  __shared__ int cnt[kGridMaxCells + 1];
+  const int p = blockIdx.x;
+  const BProb P = probs[p];
+  const int V = res[p].fallback ? 0 : res[p].V;
+  int cells = 1;
+  for (int k = 0; k < D; ++k) cells *= P.G;
+  for (int c = threadIdx.x; c <= cells; c += blockDim.x) cnt[c] = 0;
+  __syncthreads();
+  for (int v = threadIdx.x; v < V; v += blockDim.x)
+    atomicAdd(&cnt[grid_cell<D>(coords + (P.row_off + v) * D, P.G)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan (cells <= 4096, once per problem)
+    int run = 0;
+    for (int c = 0; c < cells; ++c) {
+      const int t = cnt[c];
+      cnt[c] = run;
+      cell_start[P.cell_off + c] = run;
+      run += t;
+    }
+    cell_start[P.cell_off + cells] = run;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const int c = grid_cell<D>(coords + (P.row_off + v) * D, P.G);
+    cell_list[P.row_off + atomicAdd(&cnt[c], 1)] = v;
+  }
+}
+
+// Squared distance in the reference's operation order (sum over axes of
+// (a - b)^2, left to right); the leading 0.0 + x of the reference's
+// accumulation is exact for x >= +0 and is skipped.
+template <int D>
+__device__ __forceinline__ double sq_dist(const double* a, const double* b) {
+  double t = __dsub_rn(a[0], b[0]);
+  double sq = __dmul_rn(t, t);
+#pragma unroll
+  for (int k = 1; k < D; ++k) {
+    t = __dsub_rn(a[k], b[k]);
+    sq = __dadd_rn(sq, __dmul_rn(t, t));
+  }
+  return sq;
+}
+
+#ifndef GMT_GRID_MINB
+#define GMT_GRID_MINB 3
+#endif
+template <int D>
+__global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BProb* __restrict__ probs,
+                                                            const double* __restrict__ coords,
+                                                            const BOut* __restrict__ res,
+                                                            const int32_t* __restrict__ cell_start,
+                                                            const int32_t* __restrict__ cell_list, int W,
+                                                            int64_t* __restrict__ counts,
+                                                            int32_t* __restrict__ scol, double* __restrict__ scost,
+                                                            int C) {
+  // shared memory per warp: kGridRows bitmask rows of W words, 64 ints of
+  // run bookkeeping, C ints of emission buffer
+  extern __shared__ uint32_t bm_all[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int p = blockIdx.y, cell = blockIdx.x * nw + warp;  // one warp per (problem, cell)
+  const BProb P = probs[p];
+  const int G = P.G;
+  int cells = 1;
+  for (int k = 0; k < D; ++k) cells *= G;
+  if (cell >= cells || res[p].fallback) return;
+  uint32_t* bm = bm_all + static_cast<size_t>(warp) * (kGridRows * W + 64 + C);
+  int* run_s = reinterpret_cast<int*>(bm + kGridRows * W);
+  int* pre = run_s + 32;
+  int* ebuf = run_s + 64;
+  const int32_t* cs = cell_start + P.cell_off;
+  const int32_t* cl = cell_list + P.row_off;
+  const double* X = coords + P.row_off * D;
+  const int c0 = cs[cell], c1 = cs[cell + 1];
+  if (c0 == c1) return;
+  // The neighbour cells as runs of consecutive cell indices (x fastest): the
+  // targets of a run are one contiguous stretch of cell_list.  A target's run
+  // is found by binary search over the run-length prefix.
+  constexpr int kRuns = D == 3 ? kGridSpan * kGridSpan : kGridSpan;
+  const int cx = cell % G, cy = (cell / G) % G, cz = D == 3 ? cell / (G * G) : 0;
+  const int xlo = max(cx - kGridReach, 0), xhi = min(cx + kGridReach, G - 1);
+  if (lane < kRuns) {
+    const int ny = cy + lane % kGridSpan - kGridReach;
+    const int nz = D == 3 ? cz + lane / kGridSpan - kGridReach : 0;
+    int len = 0, st = 0;
+    if (ny >= 0 && ny < G && nz >= 0 && nz < (D == 3 ? G : 1)) {
+      const int base = (ny + nz * G) * G;
+      st = cs[base + xlo];
+      len = cs[base + xhi + 1] - st;
+    }
+    int incl = len;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu >> (32 - kRuns), incl, o);
+      if (lane >= o) incl += y;
+    }
+    run_s[lane] = st;
+    pre[lane] = incl - len;
+    if (lane == kRuns - 1) pre[kRuns] = incl;
+  }
+  __syncwarp();
+  const int total = pre[kRuns];
+  const double r2_lo = P.r2_lo, r2_hi = P.r2_hi, radius = P.radius;
+  for (int g0 = c0; g0 < c1; g0 += kGridRows) {
+    const int rows = min(kGridRows, c1 - g0);
+    // rows past the cell's end sit far away (their squared distances overflow
+    // to +inf and accept nothing)
+    double a[kGridRows][D];
+#pragma unroll
+    for (int j = 0; j < kGridRows; ++j) {
+      const int u = j < rows ? cl[g0 + j] : 0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) a[j][k] = j < rows ? X[u * D + k] : 1e300;
+    }
+    for (int w = lane; w < kGridRows * W; w += 32) bm[w] = 0u;
+    __syncwarp();
+    // mark: the flattened neighbour targets, 32 per step (a row's own bit is
+    // set here and cleared below)
+    for (int t = lane; t < total; t += 32) {
+      int lo = 0, hi = kRuns - 1;  // last run with pre[q] <= t
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (pre[mid] <= t) lo = mid; else hi = mid - 1;
+      }
+      const int v = cl[run_s[lo] + t - pre[lo]];
+      double b[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) b[k] = X[v * D + k];
+      uint32_t* wp = bm + (v >> 5);
+      const uint32_t bit = 1u << (v & 31);
+#pragma unroll
+      for (int j = 0; j < kGridRows; ++j) {
+        const double sq = sq_dist<D>(a[j], b);
+        bool keep = sq <= r2_lo;
+        if (!keep && sq <= r2_hi) keep = __dsqrt_rn(sq) <= radius;  // the rounding band
+        if (keep) atomicOr(wp + j * W, bit);
+      }
+    }
+    __syncwarp();
+    if (lane < rows) {
+      const int u = cl[g0 + lane];
+      bm[lane * W + (u >> 5)] &= ~(1u << (u & 31));
+    }
+    __syncwarp();
+    // emit: each row in target order -- lanes own consecutive words, write
+    // their targets into the emission buffer at their prefix offset, then the
+    // first C targets get their costs (recomputed exactly) 32 at a time.
+    const int per = (W + 31) >> 5;
+    for (int j = 0; j < rows; ++j) {
+      const int u = cl[g0 + j];  // (not us[j]: a dynamic index would put the row arrays in local memory)
+      double au[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) au[k] = X[u * D + k];
+      const int64_t r = P.row_off + u;
+      const uint32_t* row = bm + j * W;
+      int cnt = 0;
+      for (int i = 0; i < per; ++i) {
+        const int w = lane * per + i;
+        cnt += w < W ? __popc(row[w]) : 0;
+      }
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int n_row = __shfl_sync(kFull, incl, 31);
+      int slot = incl - cnt;
+      for (int i = 0; i < per && slot < C; ++i) {
+        const int w = lane * per + i;
+        if (w >= W) break;
+        for (uint32_t bits = row[w]; bits && slot < C; bits &= bits - 1u) ebuf[slot++] = w * 32 + __ffs(bits) - 1;
+      }
+      __syncwarp();
+      const int m = min(n_row, C);
+      for (int e = lane; e < m; e += 32) {
+        const int v = ebuf[e];
+        double b[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) b[k] = X[v * D + k];
+        scol[r * C + e] = v;
+        scost[r * C + e] = __dsqrt_rn(sq_dist<D>(au, b));
+      }
+      if (lane == 0) counts[r] = n_row;
+      __syncwarp();
+    }
+  }
+}
+
 // Rows with at most C targets: scratch slots -> CSR.
 __global__ void compact_rows_batch_kernel(const int64_t* __restrict__ counts, const int64_t* __restrict__ row_ptr,
                                           int64_t R, int C, const int32_t* __restrict__ scol,
@@ -522,6 +770,19 @@ __global__ void compact_rows_batch_kernel(const int64_t* __restrict__ counts, co
       cost[o + k] = scost[r * C + k];
     }
   }
+}
+
+// Dynamic shared memory above 48 KB needs the kernel attribute; grown
+// monotonically under a mutex (concurrent contexts share the kernels).
+cudaError_t raise_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& c = cur[fn];
+  if (bytes <= c || bytes <= 48 * 1024) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) c = bytes;
+  return e;
 }
 
 template <bool FILL>
@@ -566,8 +827,9 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   std::vector<double> box_lo, box_hi, goal_lo(static_cast<size_t>(count) * d), goal_hi(goal_lo.size()),
       inits(goal_lo.size());
   std::vector<int64_t> row_start(count + 1, 0);
-  int64_t cand_total = 0, box_total = 0;
-  int max_K = 1;
+  int64_t cand_total = 0, box_total = 0, cell_total = 0;
+  int max_K = 1, max_cells = 1, max_rows = 1;
+  bool grid_ok = d == 2 || d == 3;
   for (int q = 0; q < count; ++q) {
     const gmt_problem& pr = problems[q];
     if (pr.scene.dim != d) return set_error(GMT_E_INVALID_INPUT, "all problems of a batch share the dimension");
@@ -604,6 +866,24 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
     }
     P.radius = radius;
     P.r2_hi = radius * radius * (1.0 + 1e-12);
+    P.r2_lo = radius * radius * (1.0 - 1e-12);
+    {  // r-disk grid: cell side 1/G > r, at most kGridMaxCells cells
+      double g = std::floor(kGridReach / (radius * (1.0 + 1e-9)));
+      int G = g >= 1.0 ? static_cast<int>(std::min(g, 4096.0)) : 1;
+      auto cells_of = [&](int gg) {
+        int64_t c = 1;
+        for (int k = 0; k < d; ++k) c *= gg;
+        return c;
+      };
+      while (G > 1 && cells_of(G) > kGridMaxCells) --G;
+      P.G = G;
+      P.cell_off = cell_total;
+      const int64_t cells = std::min<int64_t>(cells_of(G), kGridMaxCells);
+      cell_total += cells + 1;
+      max_cells = std::max<int>(max_cells, static_cast<int>(cells));
+      max_rows = std::max(max_rows, pr.n + 1);
+      if (pr.n + 1 > kGridMaxV) grid_ok = false;
+    }
     box_lo.insert(box_lo.end(), pr.scene.box_lo, pr.scene.box_lo + static_cast<size_t>(P.nb) * d);
     box_hi.insert(box_hi.end(), pr.scene.box_hi, pr.scene.box_hi + static_cast<size_t>(P.nb) * d);
     std::copy(pr.scene.goal_lo, pr.scene.goal_lo + d, goal_lo.begin() + static_cast<size_t>(q) * d);
@@ -641,6 +921,8 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   const size_t o_cnt = take(sizeof(int64_t) * (R + 1));
   const size_t o_rp = take(sizeof(int64_t) * (R + 1));
   const size_t o_desc = take(sizeof(DevInstance) * count);
+  const size_t o_cs = take(sizeof(int32_t) * cell_total);
+  const size_t o_cl = take(sizeof(int32_t) * R);
   // Row scratch for d <= 3: the first C accepted targets of every row are
   // kept from the counting pass, so only rows with more than C are
   // evaluated twice.  C ~ twice the expected degree of the densest problem.
@@ -654,6 +936,7 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
     }
     C = static_cast<int>(std::min(256.0, std::max(32.0, 2.0 * deg + 32.0)));
   }
+  if (C <= 0 || std::getenv("GMT_NO_RDISK_GRID")) grid_ok = false;
   const size_t o_scol = take(C > 0 ? sizeof(int32_t) * static_cast<size_t>(R) * C : 0);
   const size_t o_scost = take(C > 0 ? sizeof(double) * static_cast<size_t>(R) * C : 0);
   size_t scan_bytes = 0;
@@ -679,6 +962,8 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   auto* d_cnt = reinterpret_cast<int64_t*>(B + o_cnt);
   auto* d_rp = reinterpret_cast<int64_t*>(B + o_rp);
   auto* d_desc = reinterpret_cast<DevInstance*>(B + o_desc);
+  auto* d_cs = reinterpret_cast<int32_t*>(B + o_cs);
+  auto* d_cl = reinterpret_cast<int32_t*>(B + o_cl);
   void* d_scan = B + o_scan;
   auto* d_scol = C > 0 ? reinterpret_cast<int32_t*>(B + o_scol) : nullptr;
   auto* d_scost = C > 0 ? reinterpret_cast<double*>(B + o_scost) : nullptr;
@@ -708,8 +993,28 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   subst_batch_kernel<<<count, 256, 0, s>>>(d_probs, d_coords, d_blo, d_bhi, d_glo, d_ghi, d_pr, d_res);
   init_batch_kernel<<<count, 256, 0, s>>>(d_probs, d_coords, d_init, d_res);
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((R + 7) / 8, ctx->sm_count * 16)));
-  GMT_CUDA(launch_rdisk_batch<false>(d, blocks, s, d_probs, d_rs, count, R, d_coords, d_res, d_cnt, nullptr,
-                                     nullptr, nullptr, d_scol, d_scost, C));
+  if (grid_ok) {
+    // counting pass through the cell grid (rows outside [0, V) stay 0)
+    const int W = (max_rows + 31) / 32;
+    const size_t smem = sizeof(uint32_t) * 8 * (kGridRows * static_cast<size_t>(W) + 64 + C);
+    GMT_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * (R + 1), s));
+    const dim3 ggrid((max_cells + 7) / 8, count);
+    if (d == 2) {
+      grid_build_kernel<2><<<count, 256, 0, s>>>(d_probs, d_coords, d_res, d_cs, d_cl);
+      GMT_CUDA(raise_smem(reinterpret_cast<const void*>(&rdisk_grid_kernel<2>), smem));
+      rdisk_grid_kernel<2><<<ggrid, 256, smem, s>>>(d_probs, d_coords, d_res, d_cs, d_cl, W, d_cnt, d_scol,
+                                                     d_scost, C);
+    } else {
+      grid_build_kernel<3><<<count, 256, 0, s>>>(d_probs, d_coords, d_res, d_cs, d_cl);
+      GMT_CUDA(raise_smem(reinterpret_cast<const void*>(&rdisk_grid_kernel<3>), smem));
+      rdisk_grid_kernel<3><<<ggrid, 256, smem, s>>>(d_probs, d_coords, d_res, d_cs, d_cl, W, d_cnt, d_scol,
+                                                     d_scost, C);
+    }
+    ctx->launches += 1;
+  } else {
+    GMT_CUDA(launch_rdisk_batch<false>(d, blocks, s, d_probs, d_rs, count, R, d_coords, d_res, d_cnt, nullptr,
+                                       nullptr, nullptr, d_scol, d_scost, C));
+  }
   GMT_CUDA(cudaMemsetAsync(d_cnt + R, 0, sizeof(int64_t), s));
   GMT_CUDA(cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, d_cnt, d_rp, static_cast<int>(R + 1), s));
   ctx->launches += 8;

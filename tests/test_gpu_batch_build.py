@@ -85,3 +85,29 @@ def test_plan_problems_generic_dimension_and_errors(ctx):
         ctx.plan_problems([P.di_forest(3, 300)])
     with pytest.raises(InvalidInputError):
         ctx.plan_problems([scene("rectangles_2d", 200), scene("rectangles_3d", 200)])
+
+
+def test_plan_problems_rdisk_grid_equals_brute_scan(ctx, monkeypatch):
+    """The grid-binned r-disk pass (d = 2, 3) against the all-pairs scan
+    (GMT_NO_RDISK_GRID): summaries and paths bit for bit, over radii from
+    one cell (G = 1) to the cell cap, and sizes past the grid's row limit
+    (which take the scan)."""
+    import dataclasses
+    specs = [P.random_forest_query(11, q, n=4000) for q in range(6)]
+    specs += [dataclasses.replace(P.random_forest_query(12, q, n=2500), radius_override=r)
+              for q, r in enumerate((0.9, 0.3, 0.05, 0.02))]
+    specs2 = [scene("rectangles_2d", n) for n in (300, 2000, 6000)]
+    specs2 += [dataclasses.replace(scene("rectangles_2d", 3000), radius_override=r) for r in (1.5, 0.004)]
+    big = [P.random_forest_query(13, q, n=9000) for q in range(2)]
+    for group in (specs, specs2, big):
+        cap = 2048
+        got = ctx.plan_problems(group, path_cap=cap)
+        monkeypatch.setenv("GMT_NO_RDISK_GRID", "1")
+        want = ctx.plan_problems(group, path_cap=cap)
+        monkeypatch.delenv("GMT_NO_RDISK_GRID")
+        assert got[0].tolist() == want[0].tolist()
+        for a, b in zip(got[1], want[1]):
+            assert (a.status, a.iterations, a.total_collision_checks, a.path_len) == (
+                b.status, b.iterations, b.total_collision_checks, b.path_len)
+            assert a.cost == b.cost or (np.isinf(a.cost) and np.isinf(b.cost))
+        assert got[2].tobytes() == want[2].tobytes()

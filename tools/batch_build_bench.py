@@ -18,6 +18,14 @@ for rep in range(3):
     t1 = time.perf_counter()
 print(f"gmt_plan_problems: {q} problems in {1e3 * (t1 - t0):.1f} ms -> {q / (t1 - t0):.0f} plans/s "
       f"(solved {sum(1 for s in summ if s.status == 0)}, non-OK builds {int((status != 0).sum())})", flush=True)
+pb = native.ProblemBatch(specs)
+ts = []
+for rep in range(5):
+    t0 = time.perf_counter()
+    ctx.plan_problems(pb)
+    ts.append(time.perf_counter() - t0)
+t = min(ts)
+print(f"gmt_plan_problems (ProblemBatch, flattened once): {1e3 * t:.1f} ms -> {q / t:.0f} plans/s", flush=True)
 t0 = time.perf_counter()
 insts = [ctx.build_instance(s) for s in specs]
 b = ctx.batch(insts, 1.0)
