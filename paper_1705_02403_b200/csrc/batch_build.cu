@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
                                                             const int32_t* __restrict__ cell_list, int W,
                                                             int64_t* __restrict__ counts,
                                                             int32_t* __restrict__ scol, double* __restrict__ scost,
-                                                            int C) {
+                                                            int C, int32_t* __restrict__ overflow) {
   // shared memory per warp: kGridRows bitmask rows of W words, 64 ints of
   // run bookkeeping, C ints of emission buffer
   extern __shared__ uint32_t bm_all[];
@@ -748,7 +748,10 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
         scol[r * C + e] = v;
         scost[r * C + e] = __dsqrt_rn(sq_dist<D>(au, b));
       }
-      if (lane == 0) counts[r] = n_row;
+      if (lane == 0) {
+        counts[r] = n_row;
+        if (n_row > C) *overflow = 1;  // the row needs the fill pass
+      }
       __syncwarp();
     }
   }
@@ -923,6 +926,7 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   const size_t o_desc = take(sizeof(DevInstance) * count);
   const size_t o_cs = take(sizeof(int32_t) * cell_total);
   const size_t o_cl = take(sizeof(int32_t) * R);
+  const size_t o_ovf = take(sizeof(int32_t));
   // Row scratch for d <= 3: the first C accepted targets of every row are
   // kept from the counting pass, so only rows with more than C are
   // evaluated twice.  C ~ twice the expected degree of the densest problem.
@@ -964,6 +968,7 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   auto* d_desc = reinterpret_cast<DevInstance*>(B + o_desc);
   auto* d_cs = reinterpret_cast<int32_t*>(B + o_cs);
   auto* d_cl = reinterpret_cast<int32_t*>(B + o_cl);
+  auto* d_ovf = reinterpret_cast<int32_t*>(B + o_ovf);
   void* d_scan = B + o_scan;
   auto* d_scol = C > 0 ? reinterpret_cast<int32_t*>(B + o_scol) : nullptr;
   auto* d_scost = C > 0 ? reinterpret_cast<double*>(B + o_scost) : nullptr;
@@ -998,17 +1003,18 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
     const int W = (max_rows + 31) / 32;
     const size_t smem = sizeof(uint32_t) * 8 * (kGridRows * static_cast<size_t>(W) + 64 + C);
     GMT_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * (R + 1), s));
+    GMT_CUDA(cudaMemsetAsync(d_ovf, 0, sizeof(int32_t), s));
     const dim3 ggrid((max_cells + 7) / 8, count);
     if (d == 2) {
       grid_build_kernel<2><<<count, 256, 0, s>>>(d_probs, d_coords, d_res, d_cs, d_cl);
       GMT_CUDA(raise_smem(reinterpret_cast<const void*>(&rdisk_grid_kernel<2>), smem));
       rdisk_grid_kernel<2><<<ggrid, 256, smem, s>>>(d_probs, d_coords, d_res, d_cs, d_cl, W, d_cnt, d_scol,
-                                                     d_scost, C);
+                                                     d_scost, C, d_ovf);
     } else {
       grid_build_kernel<3><<<count, 256, 0, s>>>(d_probs, d_coords, d_res, d_cs, d_cl);
       GMT_CUDA(raise_smem(reinterpret_cast<const void*>(&rdisk_grid_kernel<3>), smem));
       rdisk_grid_kernel<3><<<ggrid, 256, smem, s>>>(d_probs, d_coords, d_res, d_cs, d_cl, W, d_cnt, d_scol,
-                                                     d_scost, C);
+                                                     d_scost, C, d_ovf);
     }
     ctx->launches += 1;
   } else {
@@ -1019,8 +1025,10 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   GMT_CUDA(cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, d_cnt, d_rp, static_cast<int>(R + 1), s));
   ctx->launches += 8;
   int64_t E = 0;
+  int32_t overflow = 1;  // (the all-pairs count pass does not report it)
   std::vector<BOut> res(count);
   GMT_CUDA(cudaMemcpyAsync(&E, d_rp + R, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  if (grid_ok) GMT_CUDA(cudaMemcpyAsync(&overflow, d_ovf, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   GMT_CUDA(cudaMemcpyAsync(res.data(), d_res, sizeof(BOut) * count, cudaMemcpyDeviceToHost, s));
   GMT_CUDA(cudaStreamSynchronize(s));
   Arena edges;
@@ -1035,12 +1043,15 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
     compact_rows_batch_kernel<<<blocks, 256, 0, s>>>(d_cnt, d_rp, R, C, d_scol, d_scost, d_col, d_cost);
     ++ctx->launches;
   }
-  GMT_CUDA(launch_rdisk_batch<true>(d, blocks, s, d_probs, d_rs, count, R, d_coords, d_res, d_cnt, d_rp, d_col,
-                                    d_cost, d_scol, d_scost, C));
+  if (overflow || C <= 0) {  // rows with more than C targets: evaluated again, straight into the CSR
+    GMT_CUDA(launch_rdisk_batch<true>(d, blocks, s, d_probs, d_rs, count, R, d_coords, d_res, d_cnt, d_rp, d_col,
+                                      d_cost, d_scol, d_scost, C));
+    ++ctx->launches;
+  }
   desc_batch_kernel<<<(count + 127) / 128, 128, 0, s>>>(d_probs, d_res, d_coords, d_blo, d_bhi, d_glo, d_ghi, d_rp,
                                                         d_col, d_cost, count, d_desc);
   GMT_CUDA(cudaGetLastError());
-  ctx->launches += 2;
+  ++ctx->launches;
 
   // ---- the rare paths: the single-instance builder ---------------------------
   std::vector<gmt_instance*> single(count, nullptr);

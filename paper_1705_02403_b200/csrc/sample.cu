@@ -196,22 +196,31 @@ __device__ __forceinline__ void subst_candidate(const SubstParams& P, uint64_t i
   }
 }
 
-// Goal substitution search: smallest candidate index (0 = centre) that is
-// free and not an exact duplicate of a kept sample.
+// Goal substitution search (sampling.cpp:115-141): the smallest candidate
+// index (0 = centre) that is free and not an exact duplicate of a kept
+// sample.  subst_kernel finds the first free candidate of a chunk;
+// subst_dup_kernel then checks that one candidate against the kept samples
+// (a duplicate is rare: the host resumes the search after it).
 __global__ void subst_kernel(SubstParams P, unsigned long long* best) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.count) return;
   const uint64_t i = P.i0 + t;
   double c[kMaxDimS];
   subst_candidate(P, i, c);
-  if (!point_free_serial(c, P.d, P.box_lo, P.box_hi, P.nb)) return;
-  for (int j = 0; j < P.nseen; ++j) {
-    const double* q = P.coords + static_cast<int64_t>(j) * P.d;
-    bool eq = true;
-    for (int k = 0; k < P.d; ++k) eq = eq && (c[k] == q[k]);
-    if (eq) return;
-  }
-  atomicMin(best, static_cast<unsigned long long>(i));
+  if (point_free_serial(c, P.d, P.box_lo, P.box_hi, P.nb)) atomicMin(best, static_cast<unsigned long long>(i));
+}
+
+__global__ void subst_dup_kernel(SubstParams P, const unsigned long long* best, int* dup) {
+  const unsigned long long i = *best;
+  if (i == ~0ull) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.nseen) return;
+  double c[kMaxDimS];
+  subst_candidate(P, i, c);
+  const double* q = P.coords + static_cast<int64_t>(j) * P.d;
+  bool eq = true;
+  for (int k = 0; k < P.d; ++k) eq = eq && (c[k] == q[k]);
+  if (eq) *dup = 1;
 }
 
 __global__ void subst_write_kernel(SubstParams P, uint64_t i, double* coords, double* head,
@@ -289,6 +298,7 @@ int sample_free_dev(gmt_ctx* ctx, int32_t n, const gmt_scene* scene, const gmt_s
   int* d_valid = d_kept + 1;
   int* d_gcount = d_kept + 2;
   unsigned long long* d_best = reinterpret_cast<unsigned long long*>(base + o_cnt + 16);
+  int* d_dup = reinterpret_cast<int*>(base + o_cnt + 24);
 
   auto fail = [&](int code) {
     tmp.release();
@@ -405,12 +415,21 @@ int sample_free_dev(gmt_ctx* ctx, int32_t n, const gmt_scene* scene, const gmt_s
       Q.i0 = i0;
       Q.count = count;
       GMT_CUDA_T(cudaMemsetAsync(d_best, 0xff, sizeof(unsigned long long), s));
+      GMT_CUDA_T(cudaMemsetAsync(d_dup, 0, sizeof(int), s));
       subst_kernel<<<(count + 255) / 256, 256, 0, s>>>(Q, d_best);
+      if (Q.nseen > 0) subst_dup_kernel<<<(Q.nseen + 255) / 256, 256, 0, s>>>(Q, d_best, d_dup);
       GMT_CUDA_T(cudaGetLastError());
-      ++ctx->launches;
+      ctx->launches += 2;
+      int dup = 0;
       GMT_CUDA_T(cudaMemcpyAsync(&best, d_best, sizeof(best), cudaMemcpyDeviceToHost, s));
+      GMT_CUDA_T(cudaMemcpyAsync(&dup, d_dup, sizeof(int), cudaMemcpyDeviceToHost, s));
       GMT_CUDA_T(cudaStreamSynchronize(s));
-      i0 += count;
+      if (best != ~0ull && dup) {  // a duplicate: resume right after it
+        i0 = best + 1;
+        best = ~0ull;
+      } else {
+        i0 += count;
+      }
     }
     if (best == ~0ull) {
       return fail(set_error(GMT_E_GOAL_BLOCKED,
