@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 #include <string>
 #include <vector>
@@ -547,6 +548,7 @@ constexpr int kGridMaxV = 8192;
 constexpr int kGridRows = GMT_GRID_ROWS;
 constexpr int kGridReach = 2;
 constexpr int kGridSpan = 2 * kGridReach + 1;
+constexpr int kGridStride = kGridMaxV / 32;  // bitmask words per row (a compile-time stride: immediate offsets)
 
 template <int D>
 __device__ __forceinline__ int grid_cell(const double* c, int G) {
@@ -632,8 +634,8 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
   int cells = 1;
   for (int k = 0; k < D; ++k) cells *= G;
   if (cell >= cells || res[p].fallback) return;
-  uint32_t* bm = bm_all + static_cast<size_t>(warp) * (kGridRows * W + 64 + C);
-  int* run_s = reinterpret_cast<int*>(bm + kGridRows * W);
+  uint32_t* bm = bm_all + static_cast<size_t>(warp) * (kGridRows * kGridStride + 64 + C);
+  int* run_s = reinterpret_cast<int*>(bm + kGridRows * kGridStride);
   int* pre = run_s + 32;
   int* ebuf = run_s + 64;
   const int32_t* cs = cell_start + P.cell_off;
@@ -679,34 +681,67 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
 #pragma unroll
       for (int k = 0; k < D; ++k) a[j][k] = j < rows ? X[u * D + k] : 1e300;
     }
-    for (int w = lane; w < kGridRows * W; w += 32) bm[w] = 0u;
+#pragma unroll
+    for (int j = 0; j < kGridRows; ++j)
+      for (int w = lane; w < W; w += 32) bm[j * kGridStride + w] = 0u;
     __syncwarp();
     // mark: the flattened neighbour targets, 32 per step (a row's own bit is
     // set here and cleared below)
-    for (int t = lane; t < total; t += 32) {
+    // (software-pipelined: the next chunk's target index and coordinates are
+    // loaded while the current chunk is tested)
+    auto fetch = [&](int t, int& v, double* b) {
       int lo = 0, hi = kRuns - 1;  // last run with pre[q] <= t
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (pre[mid] <= t) lo = mid; else hi = mid - 1;
       }
-      const int v = cl[run_s[lo] + t - pre[lo]];
-      double b[D];
+      v = cl[run_s[lo] + t - pre[lo]];
 #pragma unroll
       for (int k = 0; k < D; ++k) b[k] = X[v * D + k];
-      uint32_t* wp = bm + (v >> 5);
-      const uint32_t bit = 1u << (v & 31);
+    };
+    // Fast pass: sq <= r2_lo accepts with no square root, branch-free; a pair
+    // in the rounding band (r2_lo, r2_hi] only raises a flag, and a flagged
+    // group runs the exact pass, which decides band pairs by sqrt_rn(sq) <= r
+    // (re-setting already-set bits is idempotent).
+    auto mark = [&](auto exact_tag) {
+      constexpr bool kExact = decltype(exact_tag)::value;
+      bool band_seen = false;
+      int vn = 0;
+      double bn[D];
 #pragma unroll
-      for (int j = 0; j < kGridRows; ++j) {
-        const double sq = sq_dist<D>(a[j], b);
-        bool keep = sq <= r2_lo;
-        if (!keep && sq <= r2_hi) keep = __dsqrt_rn(sq) <= radius;  // the rounding band
-        if (keep) atomicOr(wp + j * W, bit);
+      for (int k = 0; k < D; ++k) bn[k] = 1e300;
+      if (lane < total) fetch(lane, vn, bn);
+      for (int t = lane; t - lane < total; t += 32) {
+        const int v = vn;
+        double b[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) b[k] = bn[k];
+        if (t + 32 < total) fetch(t + 32, vn, bn);
+        // one 32-bit shared address per target; row j at an immediate offset
+        const uint32_t wa = static_cast<uint32_t>(__cvta_generic_to_shared(bm + (v >> 5)));
+        const uint32_t bit = 1u << (v & 31);
+#pragma unroll
+        for (int j = 0; j < kGridRows; ++j) {
+          const double sq = sq_dist<D>(a[j], b);  // (lanes past the end repeat their last target: idempotent)
+          const bool in = sq <= r2_lo;
+          const bool band = !in && sq <= r2_hi;
+          bool keep = in;
+          if (kExact) {
+            if (band) keep = __dsqrt_rn(sq) <= radius;
+          } else {
+            band_seen = band_seen || band;
+          }
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}"
+                       ::"r"(wa + j * kGridStride * 4), "r"(bit), "r"(static_cast<uint32_t>(keep)) : "memory");
+        }
       }
-    }
+      return band_seen;
+    };
+    if (__any_sync(kFull, mark(std::false_type{}))) mark(std::true_type{});
     __syncwarp();
     if (lane < rows) {
       const int u = cl[g0 + lane];
-      bm[lane * W + (u >> 5)] &= ~(1u << (u & 31));
+      bm[lane * kGridStride + (u >> 5)] &= ~(1u << (u & 31));
     }
     __syncwarp();
     // emit: each row in target order -- lanes own consecutive words, write
@@ -719,7 +754,7 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
 #pragma unroll
       for (int k = 0; k < D; ++k) au[k] = X[u * D + k];
       const int64_t r = P.row_off + u;
-      const uint32_t* row = bm + j * W;
+      const uint32_t* row = bm + j * kGridStride;
       int cnt = 0;
       for (int i = 0; i < per; ++i) {
         const int w = lane * per + i;
@@ -1001,7 +1036,7 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   if (grid_ok) {
     // counting pass through the cell grid (rows outside [0, V) stay 0)
     const int W = (max_rows + 31) / 32;
-    const size_t smem = sizeof(uint32_t) * 8 * (kGridRows * static_cast<size_t>(W) + 64 + C);
+    const size_t smem = sizeof(uint32_t) * 8 * (kGridRows * static_cast<size_t>(kGridStride) + 64 + C);
     GMT_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * (R + 1), s));
     GMT_CUDA(cudaMemsetAsync(d_ovf, 0, sizeof(int32_t), s));
     const dim3 ggrid((max_cells + 7) / 8, count);
