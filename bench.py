@@ -401,25 +401,38 @@ def run_b200(args):
         s3 = single_p50(c3)
         di_insts = [ctx.build_instance(P.random_di_query(MASTER_SEED, q, n=args.n))
                     for q in weak_range(args.di_queries, rank)]
-        bdi = ctx.batch(di_insts, 1.0)
+        bdis = [(c, st, c.batch(di_insts, 1.0)) for c, st, _ in lanes]  # same --inflight as the C2 leg
+        bdi = bdis[0][2]
         for _ in range(args.warmup):
-            bdi.launch()
+            for _, _, b in bdis:
+                b.launch()
+        for c, _, _ in bdis:
+            c.synchronize()
         barrier_sync()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for _ in range(5):
-                bdi.launch()
-            e1.record(stream)
+        di_launches = 6 * len(bdis)
+        e0.record(stream)
+        for _, st, _ in bdis[1:]:
+            st.wait_event(e0)
+        for k in range(di_launches):
+            bdis[k % len(bdis)][2].launch()
+        for _, st, _ in bdis[1:]:
+            j = torch.cuda.Event()
+            j.record(st)
+            stream.wait_event(j)
+        e1.record(stream)
         barrier_sync()
-        di_ms = max_over_ranks(e0.elapsed_time(e1) / 5)
+        for c, _, _ in bdis:
+            c.synchronize()
+        di_ms = max_over_ranks(e0.elapsed_time(e1) / di_launches)
         di = {"workload": "di6d_forest_n4000 (configs[2]) / batched random DI queries (configs[4])",
               "radius": c3.radius, "mean_out_degree": c3.num_edges / c3.n,
               "device_build_ms": build_ms, "p50_ms_single_solve": min(s3.values()),
               "single_solve_ms": s3, "batched_plans_per_s": world * len(di_insts) / (di_ms / 1e3),
-              "batched_queries_per_gpu": len(di_insts),
+              "batched_queries_per_gpu": len(di_insts), "batches_in_flight": len(bdis),
               "solved": sum(1 for s in bdi.summaries() if s.status == abi.PLAN_SUCCESS)}
-        bdi.close()
+        for _, _, b in bdis:
+            b.close()
 
     # ---- configs[3]: the 12D linearised quadrotor, n = 8000 ---------------
     quad = None
