@@ -352,6 +352,7 @@ __global__ void desc_batch_kernel(const BProb* __restrict__ probs, const BOut* _
                                   const double* __restrict__ box_hi, const double* __restrict__ goal_lo,
                                   const double* __restrict__ goal_hi, const int64_t* __restrict__ row_ptr,
                                   const int32_t* __restrict__ col, const double* __restrict__ cost, int count,
+                                  const int64_t* __restrict__ rstart, const int64_t* __restrict__ rend,
                                   DevInstance* __restrict__ descs) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= count) return;
@@ -370,10 +371,12 @@ __global__ void desc_batch_kernel(const BProb* __restrict__ probs, const BOut* _
   D.box_hi = box_hi + P.box_off * P.d;
   D.goal_lo = goal_lo + static_cast<int64_t>(p) * P.d;
   D.goal_hi = goal_hi + static_cast<int64_t>(p) * P.d;
-  D.out_ptr = row_ptr + P.row_off;
+  D.out_ptr = rstart ? rstart + P.row_off : row_ptr + P.row_off;  // row-padded scratch, or the CSR
+  D.out_end = rstart ? rend + P.row_off : nullptr;
   D.out_col = col;
   D.out_cost = cost;
   D.in_ptr = D.out_ptr;
+  D.in_end = D.out_end;
   D.in_col = col;
   D.in_cost = cost;
   descs[p] = D;
@@ -623,7 +626,8 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
                                                             const int32_t* __restrict__ cell_list, int W,
                                                             int64_t* __restrict__ counts,
                                                             int32_t* __restrict__ scol, double* __restrict__ scost,
-                                                            int C, int32_t* __restrict__ overflow) {
+                                                            int C, int32_t* __restrict__ overflow,
+                                                            int64_t* __restrict__ rstart, int64_t* __restrict__ rend) {
   // shared memory per warp: kGridRows bitmask rows of W words, 64 ints of
   // run bookkeeping, C ints of emission buffer
   extern __shared__ uint32_t bm_all[];
@@ -785,6 +789,8 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
       }
       if (lane == 0) {
         counts[r] = n_row;
+        rstart[r] = r * C;  // the row in the padded scratch (used when no row overflows)
+        rend[r] = r * C + min(n_row, C);
         if (n_row > C) *overflow = 1;  // the row needs the fill pass
       }
       __syncwarp();
@@ -962,6 +968,8 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   const size_t o_cs = take(sizeof(int32_t) * cell_total);
   const size_t o_cl = take(sizeof(int32_t) * R);
   const size_t o_ovf = take(sizeof(int32_t));
+  const size_t o_rst = take(sizeof(int64_t) * R);
+  const size_t o_ren = take(sizeof(int64_t) * R);
   // Row scratch for d <= 3: the first C accepted targets of every row are
   // kept from the counting pass, so only rows with more than C are
   // evaluated twice.  C ~ twice the expected degree of the densest problem.
@@ -1004,6 +1012,8 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   auto* d_cs = reinterpret_cast<int32_t*>(B + o_cs);
   auto* d_cl = reinterpret_cast<int32_t*>(B + o_cl);
   auto* d_ovf = reinterpret_cast<int32_t*>(B + o_ovf);
+  auto* d_rst = reinterpret_cast<int64_t*>(B + o_rst);
+  auto* d_ren = reinterpret_cast<int64_t*>(B + o_ren);
   void* d_scan = B + o_scan;
   auto* d_scol = C > 0 ? reinterpret_cast<int32_t*>(B + o_scol) : nullptr;
   auto* d_scost = C > 0 ? reinterpret_cast<double*>(B + o_scost) : nullptr;
@@ -1039,17 +1049,19 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
     const size_t smem = sizeof(uint32_t) * 8 * (kGridRows * static_cast<size_t>(kGridStride) + 64 + C);
     GMT_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * (R + 1), s));
     GMT_CUDA(cudaMemsetAsync(d_ovf, 0, sizeof(int32_t), s));
+    GMT_CUDA(cudaMemsetAsync(d_rst, 0, sizeof(int64_t) * R, s));
+    GMT_CUDA(cudaMemsetAsync(d_ren, 0, sizeof(int64_t) * R, s));
     const dim3 ggrid((max_cells + 7) / 8, count);
     if (d == 2) {
       grid_build_kernel<2><<<count, 256, 0, s>>>(d_probs, d_coords, d_res, d_cs, d_cl);
       GMT_CUDA(raise_smem(reinterpret_cast<const void*>(&rdisk_grid_kernel<2>), smem));
       rdisk_grid_kernel<2><<<ggrid, 256, smem, s>>>(d_probs, d_coords, d_res, d_cs, d_cl, W, d_cnt, d_scol,
-                                                     d_scost, C, d_ovf);
+                                                     d_scost, C, d_ovf, d_rst, d_ren);
     } else {
       grid_build_kernel<3><<<count, 256, 0, s>>>(d_probs, d_coords, d_res, d_cs, d_cl);
       GMT_CUDA(raise_smem(reinterpret_cast<const void*>(&rdisk_grid_kernel<3>), smem));
       rdisk_grid_kernel<3><<<ggrid, 256, smem, s>>>(d_probs, d_coords, d_res, d_cs, d_cl, W, d_cnt, d_scol,
-                                                     d_scost, C, d_ovf);
+                                                     d_scost, C, d_ovf, d_rst, d_ren);
     }
     ctx->launches += 1;
   } else {
@@ -1066,25 +1078,33 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   if (grid_ok) GMT_CUDA(cudaMemcpyAsync(&overflow, d_ovf, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   GMT_CUDA(cudaMemcpyAsync(res.data(), d_res, sizeof(BOut) * count, cudaMemcpyDeviceToHost, s));
   GMT_CUDA(cudaStreamSynchronize(s));
+  // No row overflowed the scratch: the solve reads the rows in place
+  // (row-padded adjacency, DevInstance::out_end); else compact into a CSR.
+  const bool padded = grid_ok && !overflow && std::getenv("GMT_BATCH_CSR") == nullptr;
   Arena edges;
-  rc = edges.reserve(al(sizeof(int32_t) * std::max<int64_t>(E, 1)) + sizeof(double) * std::max<int64_t>(E, 1));
-  if (rc) {
-    work.release();
-    return rc;
+  if (!padded) {
+    rc = edges.reserve(al(sizeof(int32_t) * std::max<int64_t>(E, 1)) + sizeof(double) * std::max<int64_t>(E, 1));
+    if (rc) {
+      work.release();
+      return rc;
+    }
   }
-  auto* d_col = static_cast<int32_t*>(edges.ptr);
-  auto* d_cost = reinterpret_cast<double*>(static_cast<char*>(edges.ptr) + al(sizeof(int32_t) * std::max<int64_t>(E, 1)));
-  if (C > 0) {
+  auto* d_col = padded ? d_scol : static_cast<int32_t*>(edges.ptr);
+  auto* d_cost = padded ? d_scost
+                        : reinterpret_cast<double*>(static_cast<char*>(edges.ptr) +
+                                                    al(sizeof(int32_t) * std::max<int64_t>(E, 1)));
+  if (!padded && C > 0) {
     compact_rows_batch_kernel<<<blocks, 256, 0, s>>>(d_cnt, d_rp, R, C, d_scol, d_scost, d_col, d_cost);
     ++ctx->launches;
   }
-  if (overflow || C <= 0) {  // rows with more than C targets: evaluated again, straight into the CSR
+  if (!padded && (overflow || C <= 0)) {  // rows with more than C targets: evaluated again, straight into the CSR
     GMT_CUDA(launch_rdisk_batch<true>(d, blocks, s, d_probs, d_rs, count, R, d_coords, d_res, d_cnt, d_rp, d_col,
                                       d_cost, d_scol, d_scost, C));
     ++ctx->launches;
   }
   desc_batch_kernel<<<(count + 127) / 128, 128, 0, s>>>(d_probs, d_res, d_coords, d_blo, d_bhi, d_glo, d_ghi, d_rp,
-                                                        d_col, d_cost, count, d_desc);
+                                                        d_col, d_cost, count, padded ? d_rst : nullptr,
+                                                        padded ? d_ren : nullptr, d_desc);
   GMT_CUDA(cudaGetLastError());
   ++ctx->launches;
 

@@ -41,6 +41,11 @@ struct DevInstance {
   const int64_t* in_ptr;  // == out_* when !directed
   const int32_t* in_col;
   const double* in_cost;
+  // Row ends: null for CSR (row x ends at ptr[x + 1]); set for row-padded
+  // adjacency (row x = [ptr[x], end[x]) with gaps between rows), which the
+  // batched builder hands to the solve without compacting its row scratch.
+  const int64_t* out_end;
+  const int64_t* in_end;
   const int32_t* in_path; // may be null (all exact edges)
   const int64_t* path_ptr;
   const double* path_pts;

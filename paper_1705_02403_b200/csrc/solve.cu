@@ -490,6 +490,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   if (threadIdx.x == 0) {
     job_s = jobs[q];
     inst_s = *job_s.inst;
+    if (!inst_s.out_end) inst_s.out_end = inst_s.out_ptr + 1;  // CSR: row x ends at ptr[x + 1]
+    if (!inst_s.in_end) inst_s.in_end = inst_s.in_ptr + 1;
   }
   __syncthreads();
   const SolveJob& job = job_s;
@@ -737,7 +739,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       if (k + h < own) {
         const int g = list[k + h];
         e0 = __ldg(I.out_ptr + g);
-        len = static_cast<int>(__ldg(I.out_ptr + g + 1) - e0);
+        len = static_cast<int>(__ldg(I.out_end + g) - e0);
       }
       while (k < own) {
         // Clusters take the next row pair from a shared counter (their few,
@@ -752,7 +754,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         if (kn + h < own) {  // next rows' offsets in flight during these rows
           const int gn = list[kn + h];
           n0 = __ldg(I.out_ptr + gn);
-          nlen = static_cast<int>(__ldg(I.out_ptr + gn + 1) - n0);
+          nlen = static_cast<int>(__ldg(I.out_end + gn) - n0);
         }
         const int lmax = rows_max<kRows>(len);
         if (counting && hl == 0 && len > 0) atomicAdd(&sh.cnt_out, static_cast<unsigned long long>(len));
@@ -834,7 +836,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
       if (k + h < ccount) {
         x = list[k + h];
         e0 = __ldg(I.in_ptr + x);
-        len = static_cast<int>(__ldg(I.in_ptr + x + 1) - e0);
+        len = static_cast<int>(__ldg(I.in_end + x) - e0);
       }
       while (k < ccount) {
         int kn = k + kRows * nw;
@@ -848,7 +850,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
         if (kn + h < ccount) {
           xn = list[kn + h];
           n0 = __ldg(I.in_ptr + xn);
-          nlen = static_cast<int>(__ldg(I.in_ptr + xn + 1) - n0);
+          nlen = static_cast<int>(__ldg(I.in_end + xn) - n0);
         }
         // The segment's B endpoint (the candidate) is staged while the row
         // streams in; the A endpoint (the chosen parent) after the argmin.
@@ -1130,7 +1132,7 @@ __global__ void __launch_bounds__(256) eager_check_kernel(const DevInstance* __r
   const bool symmetric = !I.directed;
   unsigned long long mine = 0;
   for (int u = blockIdx.x * 8 + warp; u < I.n; u += gridDim.x * 8) {
-    for (int64_t e = I.out_ptr[u]; e < I.out_ptr[u + 1]; ++e) {
+    for (int64_t e = I.out_ptr[u]; e < (I.out_end ? I.out_end[u] : I.out_ptr[u + 1]); ++e) {
       const int v = I.out_col[e];
       const int a = (symmetric && v < u) ? v : u, b = (symmetric && v < u) ? u : v;
       if (!(symmetric && v < u)) ++mine;
@@ -1222,7 +1224,7 @@ __global__ void __launch_bounds__(1024) dijkstra_kernel(const SolveJob* __restri
       break;
     }
     const double cz = R.tree_cost[z];
-    for (int64_t e = I.out_ptr[z] + tid; e < I.out_ptr[z + 1]; e += nt) {
+    for (int64_t e = I.out_ptr[z] + tid; e < (I.out_end ? I.out_end[z] : I.out_ptr[z + 1]); e += nt) {
       if (!ok[e]) continue;
       const int v = I.out_col[e];
       if (v == z || R.label[v] == 2) continue;

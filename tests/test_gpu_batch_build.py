@@ -101,13 +101,17 @@ def test_plan_problems_rdisk_grid_equals_brute_scan(ctx, monkeypatch):
     big = [P.random_forest_query(13, q, n=9000) for q in range(2)]
     for group in (specs, specs2, big):
         cap = 2048
-        got = ctx.plan_problems(group, path_cap=cap)
+        got = ctx.plan_problems(group, path_cap=cap)  # grid rows, solved in place (row-padded) when none overflows
+        monkeypatch.setenv("GMT_BATCH_CSR", "1")
+        csr = ctx.plan_problems(group, path_cap=cap)  # grid rows compacted into a CSR
         monkeypatch.setenv("GMT_NO_RDISK_GRID", "1")
-        want = ctx.plan_problems(group, path_cap=cap)
+        want = ctx.plan_problems(group, path_cap=cap)  # all-pairs rows, CSR
         monkeypatch.delenv("GMT_NO_RDISK_GRID")
-        assert got[0].tolist() == want[0].tolist()
-        for a, b in zip(got[1], want[1]):
-            assert (a.status, a.iterations, a.total_collision_checks, a.path_len) == (
-                b.status, b.iterations, b.total_collision_checks, b.path_len)
-            assert a.cost == b.cost or (np.isinf(a.cost) and np.isinf(b.cost))
-        assert got[2].tobytes() == want[2].tobytes()
+        monkeypatch.delenv("GMT_BATCH_CSR")
+        for other in (got, csr):
+            assert other[0].tolist() == want[0].tolist()
+            for a, b in zip(other[1], want[1]):
+                assert (a.status, a.iterations, a.total_collision_checks, a.path_len) == (
+                    b.status, b.iterations, b.total_collision_checks, b.path_len)
+                assert a.cost == b.cost or (np.isinf(a.cost) and np.isinf(b.cost))
+            assert other[2].tobytes() == want[2].tobytes()
