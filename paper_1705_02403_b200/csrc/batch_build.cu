@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(256) rdisk_batch_rb_kernel(const BProb* __rest
 constexpr int kGridMaxCells = 4096;
 constexpr int kGridMaxV = 8192;
 #ifndef GMT_GRID_ROWS
-#define GMT_GRID_ROWS 8
+#define GMT_GRID_ROWS 4
 #endif
 constexpr int kGridRows = GMT_GRID_ROWS;
 constexpr int kGridReach = 2;
@@ -616,7 +616,7 @@ __device__ __forceinline__ double sq_dist(const double* a, const double* b) {
 }
 
 #ifndef GMT_GRID_MINB
-#define GMT_GRID_MINB 3
+#define GMT_GRID_MINB 4
 #endif
 template <int D>
 __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BProb* __restrict__ probs,
