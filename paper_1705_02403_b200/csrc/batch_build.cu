@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
   int cells = 1;
   for (int k = 0; k < D; ++k) cells *= G;
   if (cell >= cells || res[p].fallback) return;
-  uint32_t* bm = bm_all + static_cast<size_t>(warp) * (kGridRows * kGridStride + 64 + C);
+  uint32_t* bm = bm_all + static_cast<size_t>(warp) * (kGridRows * kGridStride + 64 + ((C + 3) & ~3));  // 16 B aligned
   int* run_s = reinterpret_cast<int*>(bm + kGridRows * kGridStride);
   int* pre = run_s + 32;
   int* ebuf = run_s + 64;
@@ -685,9 +685,10 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
 #pragma unroll
       for (int k = 0; k < D; ++k) a[j][k] = j < rows ? X[u * D + k] : 1e300;
     }
+    const int per4 = (W + 127) >> 7;  // 16-byte word groups per lane in the emission
 #pragma unroll
     for (int j = 0; j < kGridRows; ++j)
-      for (int w = lane; w < W; w += 32) bm[j * kGridStride + w] = 0u;
+      for (int q = lane; q < per4 * 32; q += 32) reinterpret_cast<uint4*>(bm + j * kGridStride)[q] = make_uint4(0, 0, 0, 0);
     __syncwarp();
     // mark: the flattened neighbour targets, 32 per step (a row's own bit is
     // set here and cleared below)
@@ -751,7 +752,6 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
     // emit: each row in target order -- lanes own consecutive words, write
     // their targets into the emission buffer at their prefix offset, then the
     // first C targets get their costs (recomputed exactly) 32 at a time.
-    const int per = (W + 31) >> 5;
     for (int j = 0; j < rows; ++j) {
       const int u = cl[g0 + j];  // (not us[j]: a dynamic index would put the row arrays in local memory)
       double au[D];
@@ -759,10 +759,12 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
       for (int k = 0; k < D; ++k) au[k] = X[u * D + k];
       const int64_t r = P.row_off + u;
       const uint32_t* row = bm + j * kGridStride;
+      // lane owns words [4 per4 lane, 4 per4 (lane + 1)): 16-byte loads, no bank conflicts
+      const uint4* row4 = reinterpret_cast<const uint4*>(row) + lane * per4;
       int cnt = 0;
-      for (int i = 0; i < per; ++i) {
-        const int w = lane * per + i;
-        cnt += w < W ? __popc(row[w]) : 0;
+      for (int i = 0; i < per4; ++i) {
+        const uint4 q = row4[i];
+        cnt += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
       }
       int incl = cnt;
 #pragma unroll
@@ -772,10 +774,14 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
       }
       const int n_row = __shfl_sync(kFull, incl, 31);
       int slot = incl - cnt;
-      for (int i = 0; i < per && slot < C; ++i) {
-        const int w = lane * per + i;
-        if (w >= W) break;
-        for (uint32_t bits = row[w]; bits && slot < C; bits &= bits - 1u) ebuf[slot++] = w * 32 + __ffs(bits) - 1;
+      for (int i = 0; i < per4 && slot < C; ++i) {
+        const uint4 q = row4[i];
+        const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int w = (lane * per4 + i) * 4 + h;
+          for (uint32_t bits = ws[h]; bits && slot < C; bits &= bits - 1u) ebuf[slot++] = w * 32 + __ffs(bits) - 1;
+        }
       }
       __syncwarp();
       const int m = min(n_row, C);
@@ -1046,7 +1052,7 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   if (grid_ok) {
     // counting pass through the cell grid (rows outside [0, V) stay 0)
     const int W = (max_rows + 31) / 32;
-    const size_t smem = sizeof(uint32_t) * 8 * (kGridRows * static_cast<size_t>(kGridStride) + 64 + C);
+    const size_t smem = sizeof(uint32_t) * 8 * (kGridRows * static_cast<size_t>(kGridStride) + 64 + ((C + 3) & ~3));
     GMT_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * (R + 1), s));
     GMT_CUDA(cudaMemsetAsync(d_ovf, 0, sizeof(int32_t), s));
     GMT_CUDA(cudaMemsetAsync(d_rst, 0, sizeof(int64_t) * R, s));
