@@ -92,18 +92,33 @@ struct Cursor {
 
 }  // namespace
 
+CacheModel cache_model_of(const gmt_problem* p) {
+  CacheModel m;
+  if (p->steering == GMT_STEER_DUBINS_AIRPLANE) {
+    m.dubins = 1;
+    m.rho = p->dubins.rho;
+    m.step_raw = p->dubins.discretization_step;
+    m.planar = p->dubins.planar_cost_only != 0 ? 1 : 0;
+  } else {
+    m.rho = kRho;
+  }
+  return m;
+}
+
 int problem_key_of(const gmt_problem* p, uint64_t* out) {
   if (!p || !out) return set_error(GMT_E_INVALID_INPUT, "problem_key: null argument");
-  if (p->steering != GMT_STEER_EUCLIDEAN)
-    return set_error(GMT_E_INVALID_INPUT, "the graph cache covers the Euclidean steering model only");
+  if (p->steering != GMT_STEER_EUCLIDEAN && p->steering != GMT_STEER_DUBINS_AIRPLANE)
+    return set_error(GMT_E_INVALID_INPUT,
+                     "the graph cache covers the reference's steering models (Euclidean, Dubins airplane)");
+  const CacheModel m = cache_model_of(p);
   const gmt_scene& s = p->scene;
   const int d = s.dim;
   uint64_t h = mix64(0x676d742d70726f62ULL);  // stable salt (problem.cpp:282)
   h = fold(h, static_cast<uint64_t>(d));
-  h = fold(h, 0);  // SteeringModel::Kind::euclidean
-  h = fold_f(h, kRho);
-  h = fold_f(h, kRho / 10.0);
-  h = fold(h, 0);  // planar_cost_only
+  h = fold(h, static_cast<uint64_t>(m.dubins));  // SteeringModel::Kind (steering.hpp:10)
+  h = fold_f(h, m.rho);
+  h = fold_f(h, m.step_raw > 0.0 ? m.step_raw : m.rho / 10.0);  // step() (steering.hpp:22)
+  h = fold(h, static_cast<uint64_t>(m.planar));
   h = fold(h, static_cast<uint64_t>(s.num_boxes));
   for (int b = 0; b < s.num_boxes; ++b) {
     for (int k = 0; k < d; ++k) h = fold_f(h, s.box_lo[static_cast<size_t>(b) * d + k]);
@@ -117,13 +132,14 @@ int problem_key_of(const gmt_problem* p, uint64_t* out) {
   h = fold(h, static_cast<uint64_t>(p->sampling.kind));
   h = fold(h, p->sampling.start_index);
   h = fold(h, p->sampling.seed);
-  h = fold(h, static_cast<uint64_t>(p->sampling.with_heading != 0));
+  // load_problem sets with_heading exactly for Dubins problems (problem.cpp:197)
+  h = fold(h, static_cast<uint64_t>(p->sampling.with_heading != 0 || m.dubins));
   *out = h;
   return GMT_OK;
 }
 
 int cache_write(const char* file, uint64_t key, int32_t n, double radius, const int64_t* ptr,
-                const int32_t* col, const double* cost) {
+                const int32_t* col, const double* cost, const CacheModel& m) {
   if (!file) return set_error(GMT_E_INVALID_INPUT, "graph cache: null file name");
   std::string b;
   b.reserve(41 + static_cast<size_t>(n) * 4 + static_cast<size_t>(ptr[n]) * 12);
@@ -132,10 +148,10 @@ int cache_write(const char* file, uint64_t key, int32_t n, double radius, const 
   put_u64(b, key);
   put_u32(b, static_cast<uint32_t>(n));
   put_f64(b, radius);
-  b.push_back(0);  // not dubins_airplane
-  put_f64(b, kRho);
-  put_f64(b, 0.0);  // the raw discretization_step field (0 = rho / 10), not step()
-  b.push_back(0);
+  b.push_back(static_cast<char>(m.dubins ? 1 : 0));
+  put_f64(b, m.rho);
+  put_f64(b, m.step_raw);  // the raw discretization_step field (0 = rho / 10), not step()
+  b.push_back(static_cast<char>(m.planar ? 1 : 0));
   for (int32_t u = 0; u < n; ++u) {
     put_u32(b, static_cast<uint32_t>(ptr[u + 1] - ptr[u]));
     for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) {
@@ -156,7 +172,7 @@ int cache_write(const char* file, uint64_t key, int32_t n, double radius, const 
 }
 
 int cache_read(const char* file, uint64_t key, int32_t n, double radius, std::vector<int64_t>& ptr,
-               std::vector<int32_t>& col, std::vector<double>& cost, bool* hit) {
+               std::vector<int32_t>& col, std::vector<double>& cost, bool* hit, const CacheModel& m) {
   *hit = false;
   if (!file) return set_error(GMT_E_INVALID_INPUT, "graph cache: null file name");
   std::FILE* f = std::fopen(file, "rb");
@@ -178,8 +194,10 @@ int cache_read(const char* file, uint64_t key, int32_t n, double radius, std::ve
   if (!r.u64(k) || k != key) return GMT_OK;
   if (!r.u32(nn) || nn != static_cast<uint32_t>(n)) return GMT_OK;
   if (!r.f64(rad) || rad != radius) return GMT_OK;
-  if (!r.u8(kind) || kind == 1) return GMT_OK;  // a Dubins graph for a Euclidean problem
+  if (!r.u8(kind) || (kind == 1) != (m.dubins != 0)) return GMT_OK;  // the model kind must match
   if (!r.f64(rho) || !r.f64(step) || !r.u8(planar)) return GMT_OK;
+  if (m.dubins && (rho != m.rho || step != m.step_raw || (planar != 0) != (m.planar != 0)))
+    return GMT_OK;  // graph.cpp:317-320
   ptr.assign(static_cast<size_t>(n) + 1, 0);
   col.clear();
   cost.clear();
@@ -243,7 +261,9 @@ extern "C" int gmt_instance_cache_save(gmt_ctx* ctx, const gmt_instance* inst, c
                                        uint64_t key) {
   gmtb::AllocScope alloc_scope_(ctx);
   const DevInstance& D = inst->desc;
-  if (D.directed) return set_error(GMT_E_INVALID_INPUT, "the graph cache covers the Euclidean steering model only");
+  if (D.directed && D.steering != GMT_STEER_DUBINS_AIRPLANE)
+    return set_error(GMT_E_INVALID_INPUT,
+                     "the graph cache covers the reference's steering models (Euclidean, Dubins airplane)");
   const int n = D.n;
   std::vector<int64_t> p(static_cast<size_t>(n) + 1);
   cudaStream_t s = ctx->stream;
@@ -259,5 +279,5 @@ extern "C" int gmt_instance_cache_save(gmt_ctx* ctx, const gmt_instance* inst, c
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_error(e, "graph cache download");
   }
-  return cache_write(file, key, n, D.radius, p.data(), c.data(), w.data());
+  return cache_write(file, key, n, D.radius, p.data(), c.data(), w.data(), inst->cache_model);
 }

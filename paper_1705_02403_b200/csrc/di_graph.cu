@@ -280,6 +280,24 @@ __global__ void dubins_path_fill_kernel(const double* __restrict__ aug, const in
   }
 }
 
+// Segment counts of given out-edges (a cache hit): the builder's tau.
+template <int PD>
+__global__ void dubins_tau_kernel(const double* __restrict__ aug, const int64_t* __restrict__ out_ptr,
+                                  const int32_t* __restrict__ out_col, int n, DubinsParams P,
+                                  double* __restrict__ tau) {
+  for (int u = blockIdx.x; u < n; u += gridDim.x) {
+    const double* a = aug + static_cast<int64_t>(u) * (PD + 1);
+    for (int64_t e = out_ptr[u] + threadIdx.x; e < out_ptr[u + 1]; e += blockDim.x) {
+      const double* b = aug + static_cast<int64_t>(out_col[e]) * (PD + 1);
+      int segs;
+      DubinsPath path;
+      double dz;
+      dubins_connect(a, a[PD], b, b[PD], P, &segs, &path, &dz);
+      tau[e] = static_cast<double>(segs);
+    }
+  }
+}
+
 __global__ void augment_kernel(const double* __restrict__ coords, const double* __restrict__ heading, int n,
                                int pd, double* __restrict__ aug) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -713,11 +731,58 @@ int validate_dubins(const gmt_dubins_params* p, int pd) {
   return GMT_OK;
 }
 
+// Out-rows from a graph cache file (graph.cpp:322-341): costs as stored;
+// in-rows = the transpose with sources ascending (g.in[e.other].push_back
+// in u order); segment counts recomputed on the device.
+int dubins_rows_from_host(gmt_ctx* ctx, const double* A, int n, int pd, const DubinsParams& P, const HostRows& h,
+                          Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in) {
+  const std::vector<int64_t>& hp = *h.ptr;
+  const std::vector<int32_t>& hc = *h.col;
+  const std::vector<double>& hw = *h.cost;
+  const int64_t E = static_cast<int64_t>(hc.size());
+  int rc = carve_rows(out_mem, n, E, out);
+  if (rc == GMT_OK) rc = carve_rows(in_mem, n, E, in);
+  if (rc) return rc;
+  std::vector<int64_t> ip(static_cast<size_t>(n) + 1, 0);
+  for (int64_t e = 0; e < E; ++e) ++ip[static_cast<size_t>(hc[e]) + 1];
+  for (int v = 0; v < n; ++v) ip[v + 1] += ip[v];
+  std::vector<int64_t> at(ip.begin(), ip.end() - 1);
+  std::vector<int32_t> ic(static_cast<size_t>(E));
+  std::vector<double> iw(static_cast<size_t>(E));
+  for (int u = 0; u < n; ++u)
+    for (int64_t e = hp[u]; e < hp[u + 1]; ++e) {
+      const int64_t k = at[hc[e]]++;
+      ic[k] = u;
+      iw[k] = hw[e];
+    }
+  cudaStream_t s = ctx->stream;
+  GMT_CUDA(cudaMemcpyAsync(out->ptr, hp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+  GMT_CUDA(cudaMemcpyAsync(in->ptr, ip.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+  if (E) {
+    GMT_CUDA(cudaMemcpyAsync(out->col, hc.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, s));
+    GMT_CUDA(cudaMemcpyAsync(out->cost, hw.data(), sizeof(double) * E, cudaMemcpyHostToDevice, s));
+    GMT_CUDA(cudaMemcpyAsync(in->col, ic.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, s));
+    GMT_CUDA(cudaMemcpyAsync(in->cost, iw.data(), sizeof(double) * E, cudaMemcpyHostToDevice, s));
+    GMT_CUDA(cudaMemsetAsync(in->tau, 0, sizeof(double) * E, s));
+    const int nb = std::max(1, std::min(n, 4096));
+    if (pd == 2)
+      dubins_tau_kernel<2><<<nb, 128, 0, s>>>(A, out->ptr, out->col, n, P, out->tau);
+    else
+      dubins_tau_kernel<3><<<nb, 128, 0, s>>>(A, out->ptr, out->col, n, P, out->tau);
+    GMT_CUDA(cudaGetLastError());
+    ++ctx->launches;
+  }
+  GMT_CUDA(cudaStreamSynchronize(s));  // (the host vectors go out of scope)
+  return GMT_OK;
+}
+
 // The directed Dubins graph of device samples (positions + headings):
-// out-/in-rows as build_kino_graph_dev, plus every out-edge's path.
+// out-/in-rows as build_kino_graph_dev (or as a cache file gives them), plus
+// every out-edge's path.
 int build_dubins_graph_dev(gmt_ctx* ctx, const double* d_coords, const double* d_heading, int n, int pd,
                            const gmt_dubins_params* p, double radius, Arena& out_mem, DiRows* out,
-                           Arena& in_mem, DiRows* in, Arena& path_mem, DubinsGraphPaths* paths) {
+                           Arena& in_mem, DiRows* in, Arena& path_mem, DubinsGraphPaths* paths,
+                           const HostRows* cached) {
   int rc = validate_dubins(p, pd);
   if (rc) return rc;
   const DubinsParams P = to_dubins(p, pd);
@@ -730,7 +795,9 @@ int build_dubins_graph_dev(gmt_ctx* ctx, const double* d_coords, const double* d
   GMT_CUDA(cudaGetLastError());
   ++ctx->launches;
   const double* A = static_cast<const double*>(aug.ptr);
-  if (pd == 2) {
+  if (cached) {
+    rc = dubins_rows_from_host(ctx, A, n, pd, P, *cached, out_mem, out, in_mem, in);
+  } else if (pd == 2) {
     DubinsModel<2> m{P, radius};
     rc = build_kino_graph_dev(ctx, A, n, m, radius, out_mem, out, in_mem, in);
   } else {

@@ -55,6 +55,15 @@ struct AllocScope {
 }  // namespace gmtb
 
 namespace gmtb {
+// GMTG v1 graph cache (cache.cu).  CacheModel: the file's model fields
+// (graph.cpp:251-254): Euclidean = {0, 0.1, 0.0, 0}; Dubins = the problem's
+// rho, raw discretization_step and planar_cost_only.
+struct CacheModel {
+  int dubins = 0;
+  double rho = 0.1;
+  double step_raw = 0.0;
+  int planar = 0;
+};
 int validate_scene(const gmt_scene* s);
 int push_desc(gmt_ctx* ctx, gmt_instance* inst);
 }  // namespace gmtb
@@ -68,6 +77,7 @@ struct gmt_instance {
   gmtb::DevInstance desc{};
   int32_t graph_n = 0;
   const int32_t* goal_idx_dev = nullptr;
+  gmtb::CacheModel cache_model{};  // the steering fields a graph cache file records
   ~gmt_instance() {
     mem.release();
     desc_mem.release();

@@ -53,16 +53,26 @@ struct DubinsGraphPaths {
   int64_t num_points = 0;
 };
 int validate_dubins(const gmt_dubins_params* p, int pd);
+// Host out-rows (a graph cache hit): the rows are taken as given, and only
+// the in-rows, segment counts and edge paths are derived on the device.
+struct HostRows {
+  const std::vector<int64_t>* ptr;
+  const std::vector<int32_t>* col;
+  const std::vector<double>* cost;
+};
 int build_dubins_graph_dev(gmt_ctx* ctx, const double* d_coords, const double* d_heading, int n, int pd,
                            const gmt_dubins_params* p, double radius, Arena& out_mem, DiRows* out,
-                           Arena& in_mem, DiRows* in, Arena& path_mem, DubinsGraphPaths* paths);
+                           Arena& in_mem, DiRows* in, Arena& path_mem, DubinsGraphPaths* paths,
+                           const HostRows* cached = nullptr);
 
-// GMTG v1 graph cache (cache.cu).
+// GMTG v1 graph cache (cache.cu); CacheModel: internal.cuh.
+CacheModel cache_model_of(const gmt_problem* p);
 int problem_key_of(const gmt_problem* p, uint64_t* out);
 int cache_write(const char* file, uint64_t key, int32_t n, double radius, const int64_t* ptr,
-                const int32_t* col, const double* cost);
+                const int32_t* col, const double* cost, const CacheModel& m = CacheModel{});
 int cache_read(const char* file, uint64_t key, int32_t n, double radius, std::vector<int64_t>& ptr,
-               std::vector<int32_t>& col, std::vector<double>& cost, bool* hit);
+               std::vector<int32_t>& col, std::vector<double>& cost, bool* hit,
+               const CacheModel& m = CacheModel{});
 
 // append_init on device samples (sampling.cpp:144-154).
 int append_init_dev(gmt_ctx* ctx, int dim, DevSamples* s, const double* init, int has_heading,

@@ -633,17 +633,18 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
   // Graph cache (problem.cpp:354-360): a key / shape match supplies the graph.
   bool hit = false;
   uint64_t key = 0;
+  std::vector<int64_t> hp;
+  std::vector<int32_t> hc;
+  std::vector<double> hw;
   if (cache_file) {
-    if (di || dubins) {
+    if (di) {
       samples.release();
-      return set_error(GMT_E_INVALID_INPUT, "the graph cache covers the Euclidean steering model only");
+      return set_error(GMT_E_INVALID_INPUT,
+                       "the graph cache covers the reference's steering models (Euclidean, Dubins airplane)");
     }
-    std::vector<int64_t> hp;
-    std::vector<int32_t> hc;
-    std::vector<double> hw;
     rc = problem_key_of(p, &key);
-    if (rc == GMT_OK) rc = cache_read(cache_file, key, S.n, radius, hp, hc, hw, &hit);
-    if (rc == GMT_OK && hit) {
+    if (rc == GMT_OK) rc = cache_read(cache_file, key, S.n, radius, hp, hc, hw, &hit, cache_model_of(p));
+    if (rc == GMT_OK && hit && !dubins) {  // (a Dubins hit: rows go through the Dubins builder below)
       E = static_cast<int64_t>(hc.size());
       const size_t o_col = align16(sizeof(int64_t) * (S.n + 1));
       const size_t o_cost = o_col + align16(sizeof(int32_t) * static_cast<size_t>(E));
@@ -669,11 +670,12 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
       return rc;
     }
   }
-  if (hit) {
+  if (hit && !dubins) {
     // graph supplied by the cache file
   } else if (dubins) {
+    const HostRows cached{&hp, &hc, &hw};  // a cache hit: rows and costs from the file, paths recomputed
     rc = build_dubins_graph_dev(ctx, S.coords, S.heading, S.n, d, &p->dubins, radius, g, &dout, g2, &din, g3,
-                                &dpaths);
+                                &dpaths, hit ? &cached : nullptr);
     E = dout.edges;
     rp = dout.ptr;
     col = dout.col;
@@ -787,6 +789,7 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
     }
     inst->goal_idx_dev = reinterpret_cast<const int32_t*>(b + o_gidx);
     inst->graph_n = n;
+    inst->cache_model = cache_model_of(p);
   }
   samples.release();
   if (rc == GMT_OK) {

@@ -62,3 +62,16 @@ def random_ref_problem(ref, rng, **kw):
 
 def bits(a: np.ndarray) -> bytes:
     return np.ascontiguousarray(a).view(np.uint64).tobytes()
+
+
+def forest_dubins(n: int = 600) -> P.ProblemSpec:
+    """proj/scenes/forest_dubins.json (8 square pillars, rho = 0.08, pinned
+    radius 0.2, Halton samples with headings)."""
+    from paper_1705_02403_b200 import abi
+    lo = [[0.21, 0.21], [0.21, 0.56], [0.26, 0.81], [0.46, 0.36], [0.51, 0.71], [0.61, 0.11],
+          [0.71, 0.51], [0.81, 0.76]]
+    box_lo = np.array(lo)
+    return P.ProblemSpec(dim=2, box_lo=box_lo, box_hi=box_lo + 0.08, goal_lo=np.array([0.88, 0.88]),
+                         goal_hi=np.array([0.98, 0.98]), init=np.array([0.05, 0.05]), n=n,
+                         radius_override=0.2, steering=abi.STEER_DUBINS_AIRPLANE, init_heading=0.0,
+                         dubins_rho=0.08)

@@ -8,7 +8,7 @@ import pytest
 
 from paper_1705_02403_b200 import abi, native, problem as P
 from paper_1705_02403_b200.graph import Graph
-from helpers import SCENE_NAMES, oracle_instance, scene
+from helpers import SCENE_NAMES, forest_dubins, oracle_instance, scene
 
 
 def _specs():
@@ -30,6 +30,20 @@ def test_problem_key_matches_reference(ref):
         assert k == ref.problem_key(spec)
         keys.add(k)
     assert len(keys) == len(_specs())  # every field change moves the key
+
+
+def test_problem_key_dubins_matches_reference(ref):
+    """Dubins problems key on kind, rho, step() and planar_cost_only
+    (problem.cpp:284-287) and carry with_heading (problem.cpp:197)."""
+    specs = [forest_dubins()]
+    for f, v in (("dubins_rho", 0.1), ("dubins_step", 0.004), ("dubins_planar", 1)):
+        s = forest_dubins()
+        setattr(s, f, v)
+        specs.append(s)
+    keys = {native.problem_key(s) for s in specs}
+    assert len(keys) == len(specs)
+    for s in specs:
+        assert native.problem_key(s) == ref.problem_key(s)
 
 
 def test_problem_key_rejects_kinodynamic():

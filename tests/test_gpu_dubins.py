@@ -8,23 +8,10 @@ reference's own Dubins graph (cached paths, uploaded) are checked exactly."""
 import numpy as np
 import pytest
 
-from paper_1705_02403_b200 import abi, problem as P
+from paper_1705_02403_b200 import abi, native, problem as P
+from helpers import forest_dubins
 
 pytestmark = pytest.mark.gpu
-
-
-def forest_dubins(n=600):
-    """proj/scenes/forest_dubins.json (8 square pillars, rho = 0.08, pinned
-    radius 0.2, Halton samples with headings)."""
-    lo = [[0.21, 0.21], [0.21, 0.56], [0.26, 0.81], [0.46, 0.36], [0.51, 0.71], [0.61, 0.11],
-          [0.71, 0.51], [0.81, 0.76]]
-    box_lo = np.array(lo)
-    box_hi = box_lo + 0.08
-    spec = P.ProblemSpec(dim=2, box_lo=box_lo, box_hi=box_hi, goal_lo=np.array([0.88, 0.88]),
-                         goal_hi=np.array([0.98, 0.98]), init=np.array([0.05, 0.05]), n=n,
-                         radius_override=0.2, steering=abi.STEER_DUBINS_AIRPLANE, init_heading=0.0,
-                         dubins_rho=0.08)
-    return spec
 
 
 def _params(rho=0.08, step=0.0, planar=False):
@@ -83,3 +70,39 @@ def test_forest_dubins_graph_and_plan(ctx, ref):
     assert not abi.full_parity(ctx.fmt_plan(up, ii), ref.fmt_plan(spec, coords, len(gidx), G, ii))
     assert not abi.full_parity(ctx.dijkstra_oracle(up, ii),
                                ref.dijkstra_oracle(spec, coords, len(gidx), G, ii))
+
+
+def test_dubins_graph_cache_with_reference(tmp_path, ctx, ref):
+    """GMTG v1 files for Dubins problems (graph.cpp:245-343): the header and
+    key match the reference's; the reference loads our file; a reference
+    file seeds a device instance with the reference's exact costs (paths
+    recomputed on load, as the reference does), which then plans exactly
+    like the reference; an instance saved again is the same file."""
+    spec = forest_dubins()
+    key = native.problem_key(spec)
+    assert key == ref.problem_key(spec)
+    ours, theirs, again = (str(tmp_path / f) for f in ("ours.gmtg", "theirs.gmtg", "again.gmtg"))
+    a, hit_a = ctx.build_instance_cached(spec, ours)
+    assert not hit_a
+    ri = ref.instance_build_cached(spec, theirs)
+    ob, tb = open(ours, "rb").read(), open(theirs, "rb").read()
+    header = 4 + 4 + 8 + 4 + 8 + 1 + 8 + 8 + 1
+    assert ob[:header] == tb[:header] and len(ob) == len(tb)  # same edge set; costs to a few ulps
+    coords, gidx, G = ri.graph(2)
+    _, _, ga = a.download()
+    assert np.array_equal(ga.out_col, G.out_col)
+    # the reference's build_instance loads our file: its graph carries our costs
+    _, _, G2 = ref.instance_build_cached(spec, ours).graph(2)
+    assert G2.out_cost.tobytes() == ga.out_cost.tobytes()
+    b, hit_b = ctx.build_instance_cached(spec, theirs)
+    assert hit_b and b.num_edges == a.num_edges
+    _, _, gb = b.download()
+    assert gb.out_cost.tobytes() == G.out_cost.tobytes()  # the reference's costs, exactly
+    assert not abi.full_parity(ctx.plan(b, lam=spec.lam), ri.plan(spec.lam))
+    b.cache_save(again, key)
+    assert open(again, "rb").read() == tb
+    # a Dubins file is a miss for the Euclidean problem over the same scene, and vice versa
+    eu = forest_dubins()
+    eu.steering = abi.STEER_EUCLIDEAN
+    _, hit_e = ctx.build_instance_cached(eu, theirs)
+    assert not hit_e
