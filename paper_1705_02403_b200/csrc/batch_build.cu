@@ -82,28 +82,73 @@ __device__ __forceinline__ bool free_point(const double* p, int d, const double*
   return true;
 }
 
-__global__ void gen_batch_kernel(const BProb* __restrict__ probs, const double* __restrict__ box_lo,
-                                 const double* __restrict__ box_hi, const uint32_t* __restrict__ primes,
-                                 double* __restrict__ cand, uint8_t* __restrict__ flag) {
+// Halton coordinate with the digit weights f_i = (((1 / b) / b) ... / b)
+// tabulated on the host (IEEE division, the same correctly rounded steps as
+// halton_dev's f /= base): r += f_i * (index % b), 32-bit digit arithmetic
+// while the index fits.
+constexpr int kHaltonDigits = 64;
+__device__ __forceinline__ double halton_tab(uint64_t index, uint32_t base, const double* __restrict__ f) {
+  double r = 0.0;
+  int i = 0;
+  while (index > 0xffffffffull) {
+    r = __dadd_rn(r, __dmul_rn(f[i++], static_cast<double>(index % base)));
+    index /= base;
+  }
+  uint32_t x = static_cast<uint32_t>(index);
+  while (x > 0) {
+    const uint32_t q = x / base;
+    r = __dadd_rn(r, __dmul_rn(f[i++], static_cast<double>(x - q * base)));
+    x = q;
+  }
+  return r;
+}
+
+// D = 0: any dimension (runtime d, arrays in local memory).
+template <int D>
+__global__ void __launch_bounds__(256) gen_batch_kernel(const BProb* __restrict__ probs,
+                                                        const double* __restrict__ box_lo,
+                                                        const double* __restrict__ box_hi,
+                                                        const uint32_t* __restrict__ primes,
+                                                        const double* __restrict__ fpow,
+                                                        double* __restrict__ cand, uint8_t* __restrict__ flag) {
   const BProb P = probs[blockIdx.y];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.K) return;
-  double c[kMaxDimB];
-  const int d = P.d;
+  double c[D > 0 ? D : kMaxDimB];
+  const int d = D > 0 ? D : P.d;
   if (P.kind == GMT_SAMPLE_HALTON) {
     const uint64_t idx = P.start_index + static_cast<uint64_t>(j);
-    for (int k = 0; k < d; ++k) c[k] = halton_dev(idx, primes[k]);
+#pragma unroll
+    for (int k = 0; k < (D > 0 ? D : kMaxDimB); ++k)
+      if (k < d) c[k] = halton_tab(idx, primes[k], fpow + k * kHaltonDigits);
   } else {
     uint64_t st = pcg_advance(P.s0, static_cast<uint64_t>(j) * static_cast<uint64_t>(P.dd));
-    for (int k = 0; k < d; ++k) {
-      c[k] = static_cast<double>(pcg_out(st)) * 0x1p-32;  // next_double (rng.hpp:33)
-      st = st * kPcgMult + kPcgInc;
+#pragma unroll
+    for (int k = 0; k < (D > 0 ? D : kMaxDimB); ++k) {
+      if (k < d) {
+        c[k] = static_cast<double>(pcg_out(st)) * 0x1p-32;  // next_double (rng.hpp:33)
+        st = st * kPcgMult + kPcgInc;
+      }
     }
   }
   double* out = cand + (P.cand_off + j) * d;
-  for (int k = 0; k < d; ++k) out[k] = c[k];
-  flag[P.cand_off + j] =
-      free_point(c, d, box_lo + P.box_off * d, box_hi + P.box_off * d, P.nb) ? 1 : 0;
+#pragma unroll
+  for (int k = 0; k < (D > 0 ? D : kMaxDimB); ++k)
+    if (k < d) out[k] = c[k];
+  bool ok = true;  // point_free (space.cpp:47-54): in the unit cube, in no box
+#pragma unroll
+  for (int k = 0; k < (D > 0 ? D : kMaxDimB); ++k)
+    if (k < d) ok = ok && c[k] >= 0.0 && c[k] <= 1.0;
+  const double* lo = box_lo + P.box_off * d;
+  const double* hi = box_hi + P.box_off * d;
+  for (int b = 0; ok && b < P.nb; ++b) {
+    bool in = true;
+#pragma unroll
+    for (int k = 0; k < (D > 0 ? D : kMaxDimB); ++k)
+      if (k < d) in = in && c[k] >= __ldg(lo + b * d + k) && c[k] <= __ldg(hi + b * d + k);
+    ok = !in;
+  }
+  flag[P.cand_off + j] = ok ? 1 : 0;
 }
 
 // One CTA per problem: ordered compaction of the first n free candidates.
@@ -901,7 +946,23 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
     P.nb = pr.scene.num_boxes;
     P.n = pr.n;
     const uint64_t budget = 1000ULL * static_cast<uint64_t>(pr.n);
-    P.K = static_cast<int>(std::min<uint64_t>(budget, 2ull * pr.n + 256));
+    {  // candidates drawn up front: n over the free-volume estimate (boxes
+       // clipped to the unit cube; overlaps make it low, i.e. K larger),
+       // +5 % + 256; a problem that still runs short takes the single builder
+      double blocked = 0.0;
+      for (int b = 0; b < pr.scene.num_boxes; ++b) {
+        double v = 1.0;
+        for (int k = 0; k < d; ++k) {
+          const double lo = std::max(0.0, pr.scene.box_lo[static_cast<size_t>(b) * d + k]);
+          const double hi = std::min(1.0, pr.scene.box_hi[static_cast<size_t>(b) * d + k]);
+          v *= std::max(0.0, hi - lo);
+        }
+        blocked += v;
+      }
+      const double free_est = std::max(0.05, 1.0 - blocked);
+      const double want = std::min(2.0 * pr.n, pr.n / free_est * 1.05) + 256.0;
+      P.K = static_cast<int>(std::min<double>(static_cast<double>(budget), std::ceil(want)));
+    }
     P.need_dedup = (pr.sampling.kind == GMT_SAMPLE_UNIFORM ||
                     pr.sampling.start_index + budget >= (1ULL << 53)) ? 1 : 0;
     P.start_index = pr.sampling.start_index;
@@ -947,6 +1008,14 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   const int64_t R = row_start[count];
   std::vector<uint32_t> primes(kMaxDimB);
   for (int k = 0; k < kMaxDimB; ++k) primes[k] = nth_prime_h(k + 1);
+  std::vector<double> fpow(static_cast<size_t>(kMaxDimB) * kHaltonDigits);
+  for (int k = 0; k < kMaxDimB; ++k) {
+    volatile double f = 1.0;  // (volatile: one IEEE division per step, as on the device)
+    for (int i = 0; i < kHaltonDigits; ++i) {
+      f = f / static_cast<double>(primes[k]);
+      fpow[static_cast<size_t>(k) * kHaltonDigits + i] = f;
+    }
+  }
 
   // ---- device arena ----------------------------------------------------------
   auto al = [](size_t x) { return align16(x); };
@@ -964,6 +1033,7 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   const size_t o_ghi = take(sizeof(double) * goal_hi.size());
   const size_t o_init = take(sizeof(double) * inits.size());
   const size_t o_pr = take(sizeof(uint32_t) * kMaxDimB);
+  const size_t o_fp = take(sizeof(double) * kMaxDimB * kHaltonDigits);
   const size_t o_cand = take(sizeof(double) * cand_total * d);
   const size_t o_flag = take(cand_total);
   const size_t o_coords = take(sizeof(double) * R * d);
@@ -1008,6 +1078,7 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   auto* d_ghi = reinterpret_cast<double*>(B + o_ghi);
   auto* d_init = reinterpret_cast<double*>(B + o_init);
   auto* d_pr = reinterpret_cast<uint32_t*>(B + o_pr);
+  auto* d_fp = reinterpret_cast<double*>(B + o_fp);
   auto* d_cand = reinterpret_cast<double*>(B + o_cand);
   auto* d_flag = reinterpret_cast<uint8_t*>(B + o_flag);
   auto* d_coords = reinterpret_cast<double*>(B + o_coords);
@@ -1034,13 +1105,22 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
       (rc = put(d_glo, goal_lo.data(), sizeof(double) * goal_lo.size())) ||
       (rc = put(d_ghi, goal_hi.data(), sizeof(double) * goal_hi.size())) ||
       (rc = put(d_init, inits.data(), sizeof(double) * inits.size())) ||
-      (rc = put(d_pr, primes.data(), sizeof(uint32_t) * kMaxDimB))) {
+      (rc = put(d_pr, primes.data(), sizeof(uint32_t) * kMaxDimB)) ||
+      (rc = put(d_fp, fpow.data(), sizeof(double) * fpow.size()))) {
     work.release();
     return rc;
   }
 
   // ---- batched offline phase ------------------------------------------------
-  gen_batch_kernel<<<dim3((max_K + 255) / 256, count), 256, 0, s>>>(d_probs, d_blo, d_bhi, d_pr, d_cand, d_flag);
+  {
+    const dim3 gg((max_K + 255) / 256, count);
+    if (d == 2)
+      gen_batch_kernel<2><<<gg, 256, 0, s>>>(d_probs, d_blo, d_bhi, d_pr, d_fp, d_cand, d_flag);
+    else if (d == 3)
+      gen_batch_kernel<3><<<gg, 256, 0, s>>>(d_probs, d_blo, d_bhi, d_pr, d_fp, d_cand, d_flag);
+    else
+      gen_batch_kernel<0><<<gg, 256, 0, s>>>(d_probs, d_blo, d_bhi, d_pr, d_fp, d_cand, d_flag);
+  }
   pack_batch_kernel<<<count, 1024, 0, s>>>(d_probs, d_flag, d_cand, d_coords, d_res);
   int max_n = 0;
   for (const auto& P : probs) max_n = std::max(max_n, P.n);
