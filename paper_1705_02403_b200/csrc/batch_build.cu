@@ -628,15 +628,37 @@ __global__ void __launch_bounds__(256) grid_build_kernel(const BProb* __restrict
   for (int v = threadIdx.x; v < V; v += blockDim.x)
     atomicAdd(&cnt[grid_cell<D>(coords + (P.row_off + v) * D, P.G)], 1);
   __syncthreads();
-  if (threadIdx.x == 0) {  // exclusive scan (cells <= 4096, once per problem)
-    int run = 0;
-    for (int c = 0; c < cells; ++c) {
-      const int t = cnt[c];
-      cnt[c] = run;
-      cell_start[P.cell_off + c] = run;
-      run += t;
+  {  // exclusive scan of the cell counts: 16 consecutive cells per thread
+    __shared__ int wsum[8];
+    constexpr int kPer = (kGridMaxCells + 255) / 256;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int c0 = t * kPer;
+    int local[kPer];
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      local[i] = c0 + i < cells ? cnt[c0 + i] : 0;
+      sum += local[i];
     }
-    cell_start[P.cell_off + cells] = run;
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int base = incl - sum;
+    for (int w = 0; w < warp; ++w) base += wsum[w];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      if (c0 + i < cells) {
+        cnt[c0 + i] = base;
+        cell_start[P.cell_off + c0 + i] = base;
+      }
+      base += local[i];
+    }
+    if (c0 < cells && c0 + kPer >= cells) cell_start[P.cell_off + cells] = base;  // the thread holding the last cell
   }
   __syncthreads();
   for (int v = threadIdx.x; v < V; v += blockDim.x) {
