@@ -596,7 +596,13 @@ constexpr int kGridMaxV = 8192;
 constexpr int kGridRows = GMT_GRID_ROWS;
 constexpr int kGridReach = 2;
 constexpr int kGridSpan = 2 * kGridReach + 1;
-constexpr int kGridStride = kGridMaxV / 32;  // bitmask words per row (a compile-time stride: immediate offsets)
+constexpr int kGridStride = kGridMaxV / 32;  // bitmask words per row, V <= 8192 (compile-time: immediate offsets)
+constexpr int kGridCand = 768;  // a cell's flattened neighbour targets kept in shared memory (u16) up to this many
+// 32-bit words of shared memory per warp: bitmask rows (S words each), run
+// bookkeeping (64), emission buffer (C, padded to 4), target list (u16)
+__host__ __device__ constexpr int grid_warp_words(int S, int C) {
+  return kGridRows * S + 64 + ((C + 3) & ~3) + kGridCand / 2;
+}
 
 template <int D>
 __device__ __forceinline__ int grid_cell(const double* c, int G) {
@@ -685,7 +691,7 @@ __device__ __forceinline__ double sq_dist(const double* a, const double* b) {
 #ifndef GMT_GRID_MINB
 #define GMT_GRID_MINB 4
 #endif
-template <int D>
+template <int D, int S>  // S: bitmask words per row (128 when V <= 4096, else 256)
 __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BProb* __restrict__ probs,
                                                             const double* __restrict__ coords,
                                                             const BOut* __restrict__ res,
@@ -705,10 +711,11 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
   int cells = 1;
   for (int k = 0; k < D; ++k) cells *= G;
   if (cell >= cells || res[p].fallback) return;
-  uint32_t* bm = bm_all + static_cast<size_t>(warp) * (kGridRows * kGridStride + 64 + ((C + 3) & ~3));  // 16 B aligned
-  int* run_s = reinterpret_cast<int*>(bm + kGridRows * kGridStride);
+  uint32_t* bm = bm_all + static_cast<size_t>(warp) * grid_warp_words(S, C);  // 16 B aligned
+  int* run_s = reinterpret_cast<int*>(bm + kGridRows * S);
   int* pre = run_s + 32;
   int* ebuf = run_s + 64;
+  uint16_t* tlist = reinterpret_cast<uint16_t*>(ebuf + ((C + 3) & ~3));
   const int32_t* cs = cell_start + P.cell_off;
   const int32_t* cl = cell_list + P.row_off;
   const double* X = coords + P.row_off * D;
@@ -740,6 +747,17 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
   }
   __syncwarp();
   const int total = pre[kRuns];
+  // The flattened target list, once per cell (every row group of the cell
+  // reuses it): run q's targets at [pre[q], pre[q + 1]); longer neighbourhoods
+  // find a target's run by binary search instead.
+  const bool listed = total <= kGridCand;
+  if (listed) {
+    for (int q = 0; q < kRuns; ++q) {
+      const int st = run_s[q], b0 = pre[q], len = pre[q + 1] - b0;
+      for (int i = lane; i < len; i += 32) tlist[b0 + i] = static_cast<uint16_t>(cl[st + i]);
+    }
+    __syncwarp();
+  }
   const double r2_lo = P.r2_lo, r2_hi = P.r2_hi, radius = P.radius;
   for (int g0 = c0; g0 < c1; g0 += kGridRows) {
     const int rows = min(kGridRows, c1 - g0);
@@ -755,19 +773,23 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
     const int per4 = (W + 127) >> 7;  // 16-byte word groups per lane in the emission
 #pragma unroll
     for (int j = 0; j < kGridRows; ++j)
-      for (int q = lane; q < per4 * 32; q += 32) reinterpret_cast<uint4*>(bm + j * kGridStride)[q] = make_uint4(0, 0, 0, 0);
+      for (int q = lane; q < per4 * 32; q += 32) reinterpret_cast<uint4*>(bm + j * S)[q] = make_uint4(0, 0, 0, 0);
     __syncwarp();
     // mark: the flattened neighbour targets, 32 per step (a row's own bit is
     // set here and cleared below)
     // (software-pipelined: the next chunk's target index and coordinates are
     // loaded while the current chunk is tested)
     auto fetch = [&](int t, int& v, double* b) {
-      int lo = 0, hi = kRuns - 1;  // last run with pre[q] <= t
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (pre[mid] <= t) lo = mid; else hi = mid - 1;
+      if (listed) {
+        v = tlist[t];
+      } else {
+        int lo = 0, hi = kRuns - 1;  // last run with pre[q] <= t
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (pre[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        v = cl[run_s[lo] + t - pre[lo]];
       }
-      v = cl[run_s[lo] + t - pre[lo]];
 #pragma unroll
       for (int k = 0; k < D; ++k) b[k] = X[v * D + k];
     };
@@ -804,7 +826,7 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
             band_seen = band_seen || band;
           }
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}"
-                       ::"r"(wa + j * kGridStride * 4), "r"(bit), "r"(static_cast<uint32_t>(keep)) : "memory");
+                       ::"r"(wa + j * S * 4), "r"(bit), "r"(static_cast<uint32_t>(keep)) : "memory");
         }
       }
       return band_seen;
@@ -813,7 +835,7 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
     __syncwarp();
     if (lane < rows) {
       const int u = cl[g0 + lane];
-      bm[lane * kGridStride + (u >> 5)] &= ~(1u << (u & 31));
+      bm[lane * S + (u >> 5)] &= ~(1u << (u & 31));
     }
     __syncwarp();
     // emit: each row in target order -- lanes own consecutive words, write
@@ -825,7 +847,7 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
 #pragma unroll
       for (int k = 0; k < D; ++k) au[k] = X[u * D + k];
       const int64_t r = P.row_off + u;
-      const uint32_t* row = bm + j * kGridStride;
+      const uint32_t* row = bm + j * S;
       // lane owns words [4 per4 lane, 4 per4 (lane + 1)): 16-byte loads, no bank conflicts
       const uint4* row4 = reinterpret_cast<const uint4*>(row) + lane * per4;
       int cnt = 0;
@@ -1154,22 +1176,26 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   if (grid_ok) {
     // counting pass through the cell grid (rows outside [0, V) stay 0)
     const int W = (max_rows + 31) / 32;
-    const size_t smem = sizeof(uint32_t) * 8 * (kGridRows * static_cast<size_t>(kGridStride) + 64 + ((C + 3) & ~3));
+    const int S = max_rows <= 4096 ? 128 : kGridStride;
+    const size_t smem = sizeof(uint32_t) * 8 * static_cast<size_t>(grid_warp_words(S, C));
     GMT_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * (R + 1), s));
     GMT_CUDA(cudaMemsetAsync(d_ovf, 0, sizeof(int32_t), s));
     GMT_CUDA(cudaMemsetAsync(d_rst, 0, sizeof(int64_t) * R, s));
     GMT_CUDA(cudaMemsetAsync(d_ren, 0, sizeof(int64_t) * R, s));
     const dim3 ggrid((max_cells + 7) / 8, count);
+    auto launch = [&](auto kern) -> cudaError_t {
+      cudaError_t e = raise_smem(reinterpret_cast<const void*>(kern), smem);
+      if (e != cudaSuccess) return e;
+      kern<<<ggrid, 256, smem, s>>>(d_probs, d_coords, d_res, d_cs, d_cl, W, d_cnt, d_scol, d_scost, C, d_ovf,
+                                    d_rst, d_ren);
+      return cudaGetLastError();
+    };
     if (d == 2) {
       grid_build_kernel<2><<<count, 256, 0, s>>>(d_probs, d_coords, d_res, d_cs, d_cl);
-      GMT_CUDA(raise_smem(reinterpret_cast<const void*>(&rdisk_grid_kernel<2>), smem));
-      rdisk_grid_kernel<2><<<ggrid, 256, smem, s>>>(d_probs, d_coords, d_res, d_cs, d_cl, W, d_cnt, d_scol,
-                                                     d_scost, C, d_ovf, d_rst, d_ren);
+      GMT_CUDA(S == 128 ? launch(&rdisk_grid_kernel<2, 128>) : launch(&rdisk_grid_kernel<2, kGridStride>));
     } else {
       grid_build_kernel<3><<<count, 256, 0, s>>>(d_probs, d_coords, d_res, d_cs, d_cl);
-      GMT_CUDA(raise_smem(reinterpret_cast<const void*>(&rdisk_grid_kernel<3>), smem));
-      rdisk_grid_kernel<3><<<ggrid, 256, smem, s>>>(d_probs, d_coords, d_res, d_cs, d_cl, W, d_cnt, d_scol,
-                                                     d_scost, C, d_ovf, d_rst, d_ren);
+      GMT_CUDA(S == 128 ? launch(&rdisk_grid_kernel<3, 128>) : launch(&rdisk_grid_kernel<3, kGridStride>));
     }
     ctx->launches += 1;
   } else {
