@@ -11,6 +11,10 @@ from paper_1705_02403_b200.native import Context  # noqa: E402
 
 K = 40
 ctxs = [Context(0) for _ in range(4)]
+if os.environ.get("BATCH_THREADS"):
+    from paper_1705_02403_b200.native import OPT_BATCH_THREADS
+    for c in ctxs:
+        c.set_option(OPT_BATCH_THREADS, int(os.environ["BATCH_THREADS"]))
 insts = [ctxs[0].build_instance(P.random_forest_query(20171005, q, n=4000)) for q in range(512)]
 ctxs[0].synchronize()
 for S in (1, 2, 3, 4):
