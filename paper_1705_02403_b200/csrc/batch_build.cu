@@ -1110,7 +1110,7 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, static_cast<int64_t*>(nullptr),
                                 static_cast<int64_t*>(nullptr), static_cast<int>(R + 1));
   const size_t o_scan = take(scan_bytes);
-  Arena work;
+  Arena& work = ctx->pp_work;  // kept across calls (grows, never shrinks)
   int rc = work.reserve(off);
   if (rc) return rc;
   char* B = static_cast<char*>(work.ptr);
@@ -1151,7 +1151,6 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
       (rc = put(d_init, inits.data(), sizeof(double) * inits.size())) ||
       (rc = put(d_pr, primes.data(), sizeof(uint32_t) * kMaxDimB)) ||
       (rc = put(d_fp, fpow.data(), sizeof(double) * fpow.size()))) {
-    work.release();
     return rc;
   }
 
@@ -1218,10 +1217,7 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   Arena edges;
   if (!padded) {
     rc = edges.reserve(al(sizeof(int32_t) * std::max<int64_t>(E, 1)) + sizeof(double) * std::max<int64_t>(E, 1));
-    if (rc) {
-      work.release();
-      return rc;
-    }
+    if (rc) return rc;
   }
   auto* d_col = padded ? d_scol : static_cast<int32_t*>(edges.ptr);
   auto* d_cost = padded ? d_scost
@@ -1261,7 +1257,6 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
       if (rc) {
         for (auto* p : single) gmt_instance_destroy(p);
         edges.release();
-        work.release();
         return rc;
       }
       inst_ptr = static_cast<const DevInstance*>(single[q]->desc_mem.ptr);
@@ -1348,6 +1343,5 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   }
   for (auto* p : single) gmt_instance_destroy(p);
   edges.release();
-  work.release();
   return rc;
 }

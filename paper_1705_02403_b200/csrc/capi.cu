@@ -182,6 +182,7 @@ extern "C" void gmt_ctx_destroy(gmt_ctx* ctx) {
     ctx->res.release();
     ctx->scratch.release();
     ctx->jobs.release();
+    ctx->pp_work.release();
     ctx->plan_inst.mem.release();
     ctx->plan_inst.desc_mem.release();
     ctx->plan_inst.aux.release();

@@ -104,6 +104,7 @@ struct gmt_ctx {
   gmtb::Arena res;        // single-query / host-batch results
   gmtb::Arena scratch;    // host-batch inputs, offline build scratch
   gmtb::Arena jobs;       // SolveJob table
+  gmtb::Arena pp_work;    // gmt_plan_problems: the batched offline phase's scratch + padded rows
   gmtb::HostPinned pinned;
   gmtb::HostPinned pinned2;
   gmtb::HostPinned pinned_jobs;
