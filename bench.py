@@ -95,7 +95,38 @@ class ClockSampler:
         self.stop = threading.Event()
         self.t = threading.Thread(target=self.run, daemon=True)
 
+    def _nvml(self):
+        """NVML handle of this rank's GPU (by PCI bus id), or None."""
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            try:
+                import torch
+                p = torch.cuda.get_device_properties(self.device)
+                bus = "%08x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+                return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.device)
+        except Exception:
+            return None
+
     def run(self):
+        nv = self._nvml()
+        if nv is not None:  # NVML: ~1 ms per sample, so short timed regions get many
+            pynvml, h = nv
+            bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+            while not self.stop.is_set():
+                try:
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append([str(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                      str(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))] +
+                                     ["Active" if r & b else "Not Active" for b in bits])
+                except Exception:
+                    break
+                self.stop.wait(0.01)
+            if self.rows:
+                return
         while not self.stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
