@@ -434,12 +434,11 @@ __global__ void gather_paths_kernel(const DevResult* __restrict__ rs, const DevI
   if (q >= count) return;
   const DevResult R = rs[q];
   const ResultScalars sc = *R.scalars;
-  if (sc.status != 0) return;
   const DevInstance* I = insts[q];
-  const int len = sc.path_len < cap ? sc.path_len : cap;
-  for (int e = threadIdx.x; e < len * d; e += blockDim.x) {
+  const int len = sc.status != 0 ? 0 : (sc.path_len < cap ? sc.path_len : cap);
+  for (int e = threadIdx.x; e < cap * d; e += blockDim.x) {  // zeros past the path: a deterministic buffer
     const int k = e / d, i = e - k * d;
-    out[(static_cast<int64_t>(q) * cap + k) * d + i] = I->coords[static_cast<int64_t>(R.path[k]) * d + i];
+    out[static_cast<int64_t>(q) * cap * d + e] = k < len ? I->coords[static_cast<int64_t>(R.path[k]) * d + i] : 0.0;
   }
 }
 

@@ -115,3 +115,38 @@ def test_plan_problems_rdisk_grid_equals_brute_scan(ctx, monkeypatch):
                     b.status, b.iterations, b.total_collision_checks, b.path_len)
                 assert a.cost == b.cost or (np.isinf(a.cost) and np.isinf(b.cost))
             assert other[2].tobytes() == want[2].tobytes()
+
+
+def test_plan_problems_concurrent_contexts_and_scratch_reuse(ctx):
+    """Reentrancy (simulator.cpp:212 plans from several threads): two
+    contexts calling gmt_plan_problems from two host threads, with batches
+    of different sizes so each context's kept scratch is reused, grown and
+    reused again, give exactly the one-thread results."""
+    import threading
+    from paper_1705_02403_b200 import native
+    groups = [[P.random_forest_query(11, q, n=1000 + 250 * (k % 2)) for q in range(8 + 8 * k)] for k in range(4)]
+    want = [ctx.plan_problems(g, path_cap=256) for g in groups]
+    ctxs = [ctx, native.Context(0)]
+    got = [[None] * len(groups) for _ in ctxs]
+
+    def work(i):
+        order = range(len(groups)) if i == 0 else reversed(range(len(groups)))
+        for _ in range(2):
+            for k in order:
+                got[i][k] = ctxs[i].plan_problems(groups[k], path_cap=256)
+
+    try:
+        th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    finally:
+        ctxs[1].close()
+    for i in range(2):
+        for k, (ws, wsum, wp) in enumerate(want):
+            gs, gsum, gp = got[i][k]
+            assert list(gs) == list(ws)
+            assert [(a.status, a.cost, a.iterations, a.total_collision_checks, a.path_len) for a in gsum] == \
+                [(b.status, b.cost, b.iterations, b.total_collision_checks, b.path_len) for b in wsum]
+            assert gp.tobytes() == wp.tobytes()
