@@ -751,9 +751,11 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
   // find a target's run by binary search instead.
   const bool listed = total <= kGridCand;
   if (listed) {
-    for (int q = 0; q < kRuns; ++q) {
+#pragma unroll 5
+    for (int q = 0; q < kRuns; ++q) {  // (first 32 of each run predicated: the runs' loads overlap)
       const int st = run_s[q], b0 = pre[q], len = pre[q + 1] - b0;
-      for (int i = lane; i < len; i += 32) tlist[b0 + i] = static_cast<uint16_t>(cl[st + i]);
+      if (lane < len) tlist[b0 + lane] = static_cast<uint16_t>(cl[st + lane]);
+      for (int i = lane + 32; i < len; i += 32) tlist[b0 + i] = static_cast<uint16_t>(cl[st + i]);
     }
     __syncwarp();
   }
@@ -873,13 +875,22 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
       }
       __syncwarp();
       const int m = min(n_row, C);
-      for (int e = lane; e < m; e += 32) {
-        const int v = ebuf[e];
-        double b[D];
+      // (software-pipelined: the next target's coordinates load while the
+      // current cost is computed and stored)
+      int v = lane < m ? ebuf[lane] : 0;
+      double b[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) b[k] = X[v * D + k];
+      for (int k = 0; k < D; ++k) b[k] = lane < m ? X[v * D + k] : 0.0;
+      for (int e = lane; e < m; e += 32) {
+        const int vn = e + 32 < m ? ebuf[e + 32] : 0;
+        double bn[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) bn[k] = e + 32 < m ? X[vn * D + k] : 0.0;
         scol[r * C + e] = v;
         scost[r * C + e] = __dsqrt_rn(sq_dist<D>(au, b));
+        v = vn;
+#pragma unroll
+        for (int k = 0; k < D; ++k) b[k] = bn[k];
       }
       if (lane == 0) {
         counts[r] = n_row;
