@@ -780,17 +780,17 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
     // set here and cleared below)
     // (software-pipelined: the next chunk's target index and coordinates are
     // loaded while the current chunk is tested)
-    auto fetch = [&](int t, int& v, double* b) {
-      if (listed) {
-        v = tlist[t];
-      } else {
-        int lo = 0, hi = kRuns - 1;  // last run with pre[q] <= t
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (pre[mid] <= t) lo = mid; else hi = mid - 1;
-        }
-        v = cl[run_s[lo] + t - pre[lo]];
+    auto target = [&](int t) -> int {
+      if (listed) return tlist[t];
+      int lo = 0, hi = kRuns - 1;  // last run with pre[q] <= t
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (pre[mid] <= t) lo = mid; else hi = mid - 1;
       }
+      return cl[run_s[lo] + t - pre[lo]];
+    };
+    auto fetch = [&](int t, int& v, double* b) {
+      v = target(t);
 #pragma unroll
       for (int k = 0; k < D; ++k) b[k] = X[v * D + k];
     };
@@ -806,12 +806,18 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
 #pragma unroll
       for (int k = 0; k < D; ++k) bn[k] = 1e300;
       if (lane < total) fetch(lane, vn, bn);
+      int vnn = lane + 32 < total ? target(lane + 32) : 0;  // (the index two chunks ahead)
       for (int t = lane; t - lane < total; t += 32) {
         const int v = vn;
         double b[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) b[k] = bn[k];
-        if (t + 32 < total) fetch(t + 32, vn, bn);
+        if (t + 32 < total) {
+          vn = vnn;
+#pragma unroll
+          for (int k = 0; k < D; ++k) bn[k] = X[vn * D + k];
+        }
+        if (t + 64 < total) vnn = target(t + 64);
         // one 32-bit shared address per target; row j at an immediate offset
         const uint32_t wa = static_cast<uint32_t>(__cvta_generic_to_shared(bm + (v >> 5)));
         const uint32_t bit = 1u << (v & 31);
