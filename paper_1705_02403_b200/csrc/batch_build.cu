@@ -887,8 +887,10 @@ __global__ void __launch_bounds__(256, GMT_GRID_MINB) rdisk_grid_kernel(const BP
       double b[D];
 #pragma unroll
       for (int k = 0; k < D; ++k) b[k] = lane < m ? X[v * D + k] : 0.0;
+      int vnn = lane + 32 < m ? ebuf[lane + 32] : 0;  // (the index two targets ahead)
       for (int e = lane; e < m; e += 32) {
-        const int vn = e + 32 < m ? ebuf[e + 32] : 0;
+        const int vn = vnn;
+        vnn = e + 64 < m ? ebuf[e + 64] : 0;
         double bn[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) bn[k] = e + 32 < m ? X[vn * D + k] : 0.0;
