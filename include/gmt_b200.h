@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define GMT_B200_ABI_VERSION 1
+#define GMT_B200_ABI_VERSION 2
 
 /* Error codes.  Reference exception types: errors.hpp:9-21. */
 typedef enum gmt_error {
@@ -388,9 +388,24 @@ int gmt_graph_cache_save(const char* file, uint64_t key, int32_t n, double radiu
                          const int64_t* row_ptr, const int32_t* col, const double* cost);
 /* load_graph_cache (graph.cpp:278-343), Euclidean: *hit = 0 on a missing
  * file, any header mismatch (key, n, radius, model) or corruption.  Two-call
- * pattern: NULL row_ptr returns *hit and *num_edges only.                */
+ * pattern: NULL row_ptr returns *hit and *num_edges only; the second call
+ * passes row_ptr[n+1] and col/cost of edge_capacity entries and fails with
+ * GMT_E_INVALID_INPUT (*num_edges = the file's count) when the file now
+ * holds more edges than that.                                            */
 int gmt_graph_cache_load(const char* file, uint64_t key, int32_t n, double radius, int32_t* hit,
-                         int64_t* num_edges, int64_t* row_ptr, int32_t* col, double* cost);
+                         int64_t* num_edges, int64_t edge_capacity, int64_t* row_ptr, int32_t* col,
+                         double* cost);
+
+/* ---- exact geometry ---------------------------------------------------- */
+/* segment_free (space.hpp, space.cpp:80-90) of `count` independent segments
+ * a[i*dim ..] -> b[i*dim ..] against one obstacle set (closed boxes,
+ * box_lo/box_hi[b*dim + k]), evaluated on the device by the same warp test
+ * every lazy check runs: the closed slab clip (space.cpp:60-78), the
+ * endpoint cube test and the degenerate-point rule (point_free,
+ * space.cpp:47-54).  free_out[i] = 1 when the segment is free.          */
+int gmt_segment_free(gmt_ctx* ctx, int32_t dim, int32_t num_boxes, const double* box_lo,
+                     const double* box_hi, const double* a, const double* b, int64_t count,
+                     uint8_t* free_out);
 
 /* ---- device-resident instances (ProblemInstance, problem.hpp:52-57) --- */
 /* Upload host samples + graph + scene.  goal_count is samples.goal_indices
@@ -436,7 +451,9 @@ int gmt_fmt_plan(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, gmt
 int gmt_dijkstra_oracle(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, gmt_plan_out* out);
 
 /* Batched independent queries: one CTA (or cluster) per query, one launch.
- * init_index may be NULL (use each instance's built init index).          */
+ * init_index may be NULL (use each instance's built init index).
+ * Lifetime: the batch reads the instances' device memory on every launch;
+ * every instance must outlive the batch (destroy the batch first).       */
 int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const* insts,
                      const int32_t* init_index, double lambda, gmt_batch** out);
 int gmt_batch_launch(gmt_ctx* ctx, gmt_batch* batch); /* async on gmt_ctx_stream */

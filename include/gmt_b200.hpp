@@ -646,12 +646,16 @@ inline std::optional<NeighborGraph> load_graph_cache(const std::string& file, st
   const int n = static_cast<int>(states.size());
   int32_t hit = 0;
   int64_t E = 0;
-  check(gmt_graph_cache_load(file.c_str(), key, n, radius, &hit, &E, nullptr, nullptr, nullptr));
+  check(gmt_graph_cache_load(file.c_str(), key, n, radius, &hit, &E, 0, nullptr, nullptr, nullptr));
   if (!hit) return std::nullopt;
   std::vector<int64_t> ptr(n + 1);
   std::vector<int32_t> col(E);
   std::vector<double> cost(E);
-  check(gmt_graph_cache_load(file.c_str(), key, n, radius, &hit, &E, ptr.data(), col.data(), cost.data()));
+  check(gmt_graph_cache_load(file.c_str(), key, n, radius, &hit, &E, static_cast<int64_t>(col.size()),
+                             ptr.data(), col.data(), cost.data()));
+  if (!hit) return std::nullopt;  // replaced by a file that no longer matches
+  col.resize(E);
+  cost.resize(E);
   return detail::graph_from_csr(n, radius, m, ptr, col, cost);
 }
 

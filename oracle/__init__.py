@@ -388,6 +388,18 @@ class RefLib(_Lib):
                                         _dp, _dp, _dp, _i32p, _P(C.c_uint64), _P(C.c_uint64),
                                         _P(C.c_uint64), _i32p]
 
+    def segment_free_many(self, spec, a, b) -> np.ndarray:
+        """segment_free (space.cpp:80-90) of every row pair a[i] -> b[i]."""
+        a, b = abi.f64(a), abi.f64(b)
+        out = np.zeros(a.shape[0], np.uint8)
+        sc = spec.scene()
+        f = self.lib.ref_segment_free_many
+        f.restype = C.c_int
+        f.argtypes = [_P(abi.Scene), _dp, _dp, C.c_int64, _P(C.c_uint8)]
+        self._check(f(C.byref(sc), abi.ptr(a, C.c_double), abi.ptr(b, C.c_double), a.shape[0],
+                      abi.ptr(out, C.c_uint8)))
+        return out
+
     def dijkstra_oracle(self, spec, coords, goal_count, graph, init_index):
         coords = abi.f64(coords)
         n = coords.shape[0]

@@ -216,6 +216,20 @@ int ref_segment_free(const gmt_scene* s, const double* a, const double* b, int32
   });
 }
 
+// segment_free over `count` segments (the corpus form of the tests).
+int ref_segment_free_many(const gmt_scene* s, const double* a, const double* b, int64_t count,
+                          uint8_t* out) {
+  return guard([&] {
+    const ObstacleSet obs = to_obs(s);
+    const int d = s->dim;
+    for (int64_t i = 0; i < count; ++i) {
+      State sa{std::vector<double>(a + i * d, a + (i + 1) * d), std::nullopt};
+      State sb{std::vector<double>(b + i * d, b + (i + 1) * d), std::nullopt};
+      out[i] = segment_free(sa, sb, obs) ? 1 : 0;
+    }
+  });
+}
+
 // sample_free (sampling.cpp:81-142)
 int ref_sample_free(int32_t n, const gmt_scene* scene, const gmt_sample_source* src,
                     double* coords, double* heading, int32_t* goal_idx, int32_t* goal_count) {

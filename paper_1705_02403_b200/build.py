@@ -20,7 +20,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgmt_b200.so")
 OBJ = os.path.join(ROOT, "build", "obj")
 SOURCES = ["solve.cu", "graph.cu", "di_graph.cu", "sample.cu", "capi.cu", "cache.cu", "sim.cu", "batch_build.cu"]
-HEADERS = ["common.cuh", "solve.cuh", "internal.cuh", "offline.cuh", "di.cuh"]
+HEADERS = ["common.cuh", "solve.cuh", "internal.cuh", "offline.cuh", "di.cuh", "quad.cuh", "dubins.cuh",
+           "sample_dev.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
          "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
@@ -38,7 +39,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "gmt_b200.h")]
     objs = []
-    for src in SOURCES:
+    procs = []
+    for src in SOURCES:  # translation units compile in parallel
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src.replace(".cu", ".o"))
         objs.append(o)
@@ -46,7 +48,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
             cmd = [NVCC, *FLAGS, "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
+            procs.append((src, subprocess.Popen(cmd)))
+    failed = [src for src, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, "nvcc " + " ".join(failed))
     if force or _newer(LIB, objs):
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
                "-cudart", "static"]

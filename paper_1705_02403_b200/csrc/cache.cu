@@ -237,8 +237,8 @@ extern "C" int gmt_graph_cache_save(const char* file, uint64_t key, int32_t n, d
 }
 
 extern "C" int gmt_graph_cache_load(const char* file, uint64_t key, int32_t n, double radius,
-                                    int32_t* hit, int64_t* num_edges, int64_t* row_ptr, int32_t* col,
-                                    double* cost) {
+                                    int32_t* hit, int64_t* num_edges, int64_t edge_capacity,
+                                    int64_t* row_ptr, int32_t* col, double* cost) {
   std::vector<int64_t> p;
   std::vector<int32_t> c;
   std::vector<double> w;
@@ -248,6 +248,12 @@ extern "C" int gmt_graph_cache_load(const char* file, uint64_t key, int32_t n, d
   *hit = h ? 1 : 0;
   *num_edges = h ? static_cast<int64_t>(c.size()) : 0;
   if (h && row_ptr) {
+    // The file may have been replaced since the caller sized its buffers
+    // (the reference renames files into place): never write past them.
+    if (static_cast<int64_t>(c.size()) > edge_capacity)
+      return set_error(GMT_E_INVALID_INPUT, "graph cache: the file holds " + std::to_string(c.size()) +
+                                                " edges, more than the " + std::to_string(edge_capacity) +
+                                                " the buffers hold");
     std::memcpy(row_ptr, p.data(), sizeof(int64_t) * p.size());
     if (!c.empty()) {
       std::memcpy(col, c.data(), sizeof(int32_t) * c.size());

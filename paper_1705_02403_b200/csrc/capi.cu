@@ -465,6 +465,52 @@ extern "C" int gmt_instance_download(gmt_ctx* ctx, const gmt_instance* inst, dou
 
 extern "C" void gmt_instance_destroy(gmt_instance* inst) { delete inst; }
 
+// ---- exact geometry on the device -------------------------------------------------
+extern "C" int gmt_segment_free(gmt_ctx* ctx, int32_t dim, int32_t num_boxes, const double* box_lo,
+                                const double* box_hi, const double* a, const double* b, int64_t count,
+                                uint8_t* free_out) {
+  gmtb::AllocScope alloc_scope_(ctx);
+  if (!ctx) return set_error(GMT_E_INVALID_INPUT, "context is null");
+  // validate_obstacles / validate_box (space.cpp:18-38) and the dimension
+  // checks of segment_free (space.cpp:81-83).
+  if (dim < 1) return set_error(GMT_E_INVALID_INPUT, "obstacle set dimension must be >= 1");
+  if (dim > kMaxSolveDim) return set_error(GMT_E_INVALID_INPUT, "dimension above 16 is not supported");
+  if (num_boxes < 0 || count < 0) return set_error(GMT_E_INVALID_INPUT, "negative count");
+  for (int64_t i = 0; i < static_cast<int64_t>(num_boxes) * dim; ++i)
+    if (!(box_lo[i] <= box_hi[i]))
+      return set_error(GMT_E_INVALID_INPUT, "box has lo > hi on axis " + std::to_string(i % dim));
+  if (count == 0) return GMT_OK;
+  const size_t nbx = static_cast<size_t>(num_boxes) * dim, nseg = static_cast<size_t>(count) * dim;
+  Carver c;
+  const size_t o_lo = c.take<double>(nbx), o_hi = c.take<double>(nbx);
+  const size_t o_a = c.take<double>(nseg), o_b = c.take<double>(nseg);
+  const size_t o_out = c.take<uint8_t>(count);
+  Arena buf;
+  GMT_TRY(buf.reserve(c.off));
+  cudaStream_t s = ctx->stream;
+  void* base = buf.ptr;
+  int rc = GMT_OK;
+  auto cu = [&](cudaError_t e, const char* what) {
+    if (rc == GMT_OK && e != cudaSuccess) rc = cuda_error(e, what);
+  };
+  if (nbx) {
+    cu(cudaMemcpyAsync(at<double>(base, o_lo), box_lo, sizeof(double) * nbx, cudaMemcpyHostToDevice, s), "copy");
+    cu(cudaMemcpyAsync(at<double>(base, o_hi), box_hi, sizeof(double) * nbx, cudaMemcpyHostToDevice, s), "copy");
+  }
+  cu(cudaMemcpyAsync(at<double>(base, o_a), a, sizeof(double) * nseg, cudaMemcpyHostToDevice, s), "copy");
+  cu(cudaMemcpyAsync(at<double>(base, o_b), b, sizeof(double) * nseg, cudaMemcpyHostToDevice, s), "copy");
+  if (rc == GMT_OK) {
+    cu(launch_segment_free(at<double>(base, o_a), at<double>(base, o_b), count, dim, at<double>(base, o_lo),
+                           at<double>(base, o_hi), num_boxes, at<uint8_t>(base, o_out), ctx->sm_count, s),
+       "segment_free launch");
+    ++ctx->launches;
+  }
+  cu(cudaMemcpyAsync(free_out, at<uint8_t>(base, o_out), count, cudaMemcpyDeviceToHost, s), "copy");
+  cu(cudaStreamSynchronize(s), "segment_free");
+  buf.release();
+  return rc;
+}
+
 // ---- single-query solve ---------------------------------------------------------
 namespace gmtb {
 
@@ -779,8 +825,12 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
   b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
   rc = b->jobs_mem.reserve(sizeof(SolveJob) * count);
   if (rc == GMT_OK) {
-    cudaError_t e = cudaMemcpy(b->jobs_mem.ptr, b->jobs.data(), sizeof(SolveJob) * count,
-                               cudaMemcpyHostToDevice);
+    // jobs_mem comes from the stream-ordered pool of ctx->stream: write it on
+    // that stream (a block freed there earlier may still be read by work in
+    // flight on it) and wait, since b->jobs is pageable.
+    cudaError_t e = cudaMemcpyAsync(b->jobs_mem.ptr, b->jobs.data(), sizeof(SolveJob) * count,
+                                    cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) rc = cuda_error(e, "batch jobs");
   }
   if (rc != GMT_OK) {

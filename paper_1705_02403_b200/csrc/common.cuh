@@ -121,32 +121,6 @@ __device__ __forceinline__ bool box_contains(const double* lo, const double* hi,
   return true;
 }
 
-// segment_hits_box (space.cpp:60-78): closed slab clipping.  lo/hi are the
-// box's per-axis bounds with stride `st` (SoA in shared memory: st = B).
-__device__ __forceinline__ bool segment_hits_box(const double* a, const double* b, int d,
-                                                 const double* lo, const double* hi, int st) {
-  double tmin = 0.0, tmax = 1.0;
-  for (int k = 0; k < d; ++k) {
-    const double dk = __dsub_rn(b[k], a[k]);
-    const double l = lo[k * st], h = hi[k * st];
-    if (dk == 0.0) {
-      if (a[k] < l || a[k] > h) return false;
-    } else {
-      double t0 = __ddiv_rn(__dsub_rn(l, a[k]), dk);
-      double t1 = __ddiv_rn(__dsub_rn(h, a[k]), dk);
-      if (t0 > t1) {
-        const double t = t0;
-        t0 = t1;
-        t1 = t;
-      }
-      tmin = (tmin < t0) ? t0 : tmin;  // std::max(tmin, t0)
-      tmax = (t1 < tmax) ? t1 : tmax;  // std::min(tmax, t1)
-      if (tmin > tmax) return false;
-    }
-  }
-  return true;
-}
-
 // euclidean_distance (space.cpp:126-133): sequential sum of squares, sqrt.
 __device__ __forceinline__ double euclid_sq_seq(const double* a, const double* b, int d) {
   double sq = 0.0;

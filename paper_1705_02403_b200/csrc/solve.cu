@@ -275,6 +275,10 @@ __device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const doubl
             t0 = t1;
             t1 = t;
           }
+          // The clip starts from tmin = 0, tmax = 1 (space.cpp:62-63):
+          // clamp this axis' slab ends to the segment's own parameter range.
+          t0 = (0.0 < t0) ? t0 : 0.0;  // std::max(0.0, t0)
+          t1 = (t1 < 1.0) ? t1 : 1.0;  // std::min(1.0, t1)
         }
       }
       // Slot leaders (axis 0) fold in the other d - 1 axes' own values.
@@ -1149,6 +1153,47 @@ __global__ void __launch_bounds__(256) eager_check_kernel(const DevInstance* __r
     }
   }
   if (lane == 0 && mine) atomicAdd(checks, mine);
+}
+
+// segment_free / point_free (space.cpp:47-90) for `count` independent
+// segments against one obstacle set, warp per segment: the very
+// segment_free_ab the lazy checks run (the gmt_segment_free entry point).
+template <int D>
+__global__ void __launch_bounds__(256) segment_free_kernel(const double* __restrict__ a,
+                                                           const double* __restrict__ b, int64_t count,
+                                                           int d, const double* __restrict__ box_lo,
+                                                           const double* __restrict__ box_hi, int nb,
+                                                           uint8_t* __restrict__ out) {
+  __shared__ double seg_s[8 * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* seg = seg_s + warp * 32;
+  Boxes bx;
+  bx.lo = box_lo;
+  bx.hi = box_hi;
+  bx.lom = nullptr;
+  bx.him = nullptr;
+  bx.bs = d;
+  bx.as = 1;
+  bx.count = nb;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 8 + warp; i < count;
+       i += static_cast<int64_t>(gridDim.x) * 8) {
+    const bool free = segment_free_warp<D>(a + i * d, b + i * d, d, bx, lane, seg);
+    if (lane == 0) out[i] = free ? 1 : 0;
+  }
+}
+
+cudaError_t launch_segment_free(const double* a, const double* b, int64_t count, int d,
+                                const double* box_lo, const double* box_hi, int nb, uint8_t* out,
+                                int sm_count, cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((count + 7) / 8, sm_count * 8)));
+  switch (d) {
+    case 2: segment_free_kernel<2><<<blocks, 256, 0, stream>>>(a, b, count, d, box_lo, box_hi, nb, out); break;
+    case 3: segment_free_kernel<3><<<blocks, 256, 0, stream>>>(a, b, count, d, box_lo, box_hi, nb, out); break;
+    case 6: segment_free_kernel<6><<<blocks, 256, 0, stream>>>(a, b, count, d, box_lo, box_hi, nb, out); break;
+    default: segment_free_kernel<0><<<blocks, 256, 0, stream>>>(a, b, count, d, box_lo, box_hi, nb, out); break;
+  }
+  return cudaGetLastError();
 }
 
 // Search phase: Dijkstra over the surviving edges from init, one CTA.  The

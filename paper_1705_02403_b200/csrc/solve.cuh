@@ -61,4 +61,10 @@ cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threa
 cudaError_t launch_dijkstra(const DevInstance* inst, const SolveJob* job, int n, int dim, uint8_t* ok,
                             unsigned long long* checks, int sm_count, cudaStream_t stream);
 
+// segment_free (space.cpp:80-90) of count segments a[i*d..], b[i*d..] against
+// one AoS box array; out[i] = 1 when free.  Same device test as the lazy check.
+cudaError_t launch_segment_free(const double* a, const double* b, int64_t count, int d,
+                                const double* box_lo, const double* box_hi, int nb, uint8_t* out,
+                                int sm_count, cudaStream_t stream);
+
 }  // namespace gmtb

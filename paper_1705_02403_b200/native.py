@@ -63,7 +63,7 @@ SIGNATURES = [
                                    C.c_int32, C.c_int32, _i32p]),
     ("gmt_graph_cache_save", C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, C.c_double, _i64p, _i32p,
                                        _dp]),
-    ("gmt_graph_cache_load", C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, C.c_double, _i32p, _i64p,
+    ("gmt_graph_cache_load", C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, C.c_double, _i32p, _i64p, C.c_int64,
                                        _i64p, _i32p, _dp]),
     ("gmt_instance_build_cached", C.c_int, [_vp, _P(abi.Problem), C.c_char_p, _P(_vp), _i32p]),
     ("gmt_instance_cache_save", C.c_int, [_vp, _vp, C.c_char_p, C.c_uint64]),
@@ -85,6 +85,7 @@ SIGNATURES = [
     ("gmt_batch_destroy", None, [_vp]),
     ("gmt_plan_batch_host", C.c_int, [_vp, _P(abi.BatchHost), C.c_double, _P(abi.PlanSummary),
                                       _i32p, _u8p, _dp, _i32p, _i64p]),
+    ("gmt_segment_free", C.c_int, [_vp, C.c_int32, C.c_int32, _dp, _dp, _dp, _dp, C.c_int64, _u8p]),
     ("gmt_host_alloc", C.c_int, [C.c_size_t, _P(_vp)]),
     ("gmt_host_free", None, [_vp]),
 ]
@@ -187,8 +188,12 @@ class Instance:
 
 
 class Batch:
-    def __init__(self, ctx: "Context", handle, count: int, sizes):
+    """gmt_batch.  Its solve jobs point into the instances' device memory, so
+    the Batch holds a reference to every Instance for its own lifetime."""
+
+    def __init__(self, ctx: "Context", handle, count: int, sizes, instances=()):
         self.ctx, self.h, self.count, self.sizes = ctx, handle, count, sizes
+        self._insts = list(instances)
 
     def launch(self):
         check(lib().gmt_batch_launch(self.ctx.h, self.h))
@@ -293,6 +298,20 @@ class Context:
                                     abi.ptr(gl, C.c_double), abi.ptr(gh, C.c_double),
                                     abi.ptr(g, C.c_int32), C.byref(gc), C.byref(idx)))
         return buf[: n.value * dim].reshape(n.value, dim), g[: gc.value].copy(), idx.value
+
+    def segment_free(self, spec, a, b) -> np.ndarray:
+        """segment_free (space.cpp:80-90) of rows a[i] -> b[i] against
+        spec's boxes, on the device (the lazy check's own warp test)."""
+        a = abi.f64(a).reshape(-1, spec.dim)
+        b = abi.f64(b).reshape(-1, spec.dim)
+        if a.shape != b.shape:
+            raise ValueError("a and b differ in shape")
+        lo, hi = abi.f64(spec.box_lo).reshape(-1), abi.f64(spec.box_hi).reshape(-1)
+        out = np.zeros(a.shape[0], np.uint8)
+        check(lib().gmt_segment_free(self.h, spec.dim, spec.num_boxes, abi.ptr(lo, C.c_double),
+                                     abi.ptr(hi, C.c_double), abi.ptr(a, C.c_double),
+                                     abi.ptr(b, C.c_double), a.shape[0], abi.ptr(out, C.c_uint8)))
+        return out.astype(bool)
 
     def build_neighbor_graph(self, coords, radius: float) -> Graph:
         coords = abi.f64(coords)
@@ -466,7 +485,7 @@ class Context:
         h = C.c_void_p()
         check(lib().gmt_batch_create(self.h, len(instances), arr, abi.ptr(ii, C.c_int32), lam,
                                      C.byref(h)))
-        return Batch(self, h, len(instances), [i.n for i in instances])
+        return Batch(self, h, len(instances), [i.n for i in instances], instances)
 
 
 class PinnedArray:
@@ -608,16 +627,19 @@ def graph_cache_load(file: str, key: int, n: int, radius: float, dim: int = 0):
     """load_graph_cache (graph.cpp:278-343): the Graph, or None on a miss."""
     hit, ne = C.c_int32(), C.c_int64()
     z = lambda t: abi.ptr(None, t)  # noqa: E731
-    check(lib().gmt_graph_cache_load(os.fsencode(file), key, n, radius, C.byref(hit), C.byref(ne),
+    check(lib().gmt_graph_cache_load(os.fsencode(file), key, n, radius, C.byref(hit), C.byref(ne), 0,
                                      z(C.c_int64), z(C.c_int32), z(C.c_double)))
     if not hit.value:
         return None
     E = ne.value
     ptr = np.zeros(n + 1, np.int64)
     col, cost = np.zeros(max(E, 1), np.int32), np.zeros(max(E, 1))
-    check(lib().gmt_graph_cache_load(os.fsencode(file), key, n, radius, C.byref(hit), C.byref(ne),
+    check(lib().gmt_graph_cache_load(os.fsencode(file), key, n, radius, C.byref(hit), C.byref(ne), E,
                                      abi.ptr(ptr, C.c_int64), abi.ptr(col, C.c_int32),
                                      abi.ptr(cost, C.c_double)))
+    if not hit.value:
+        return None
+    E = ne.value
     return Graph(n, radius, ptr, col[:E], cost[:E], dim=dim)
 
 

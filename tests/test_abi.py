@@ -54,7 +54,7 @@ def test_library_is_sm100a_only():
 
 def test_abi_version_and_scalars():
     lib = native.lib()
-    assert lib.gmt_abi_version() == 1
+    assert lib.gmt_abi_version() == 2
     assert native.Context.connection_radius(2, 1000) == pytest.approx(0.13263, rel=1e-4)
 
 
