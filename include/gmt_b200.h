@@ -343,8 +343,10 @@ int gmt_build_quad_graph(gmt_ctx* ctx, const double* coords, int32_t n,
                          double* path_pts);
 
 /* build_instance + gmt_plan for a batch of Euclidean problems (one common
- * dimension): samples, init append and r-disk graphs of all problems are
- * built in batched device launches, then ONE batched solve.  Problems that
+ * dimension), or of double-integrator problems (derived from the shared
+ * sample pool, see gmt_batch_create_problems): samples, init append and
+ * graphs of all problems are built in batched device launches, then ONE
+ * batched solve.  Problems that
  * need sample_free's rare paths (more candidates than the first chunk,
  * exact duplicates, goal substitution) use the single-instance builder, so
  * every result equals gmt_instance_build + gmt_plan bit for bit.
@@ -456,6 +458,34 @@ int gmt_dijkstra_oracle(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_ind
  * every instance must outlive the batch (destroy the batch first).       */
 int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const* insts,
                      const int32_t* init_index, double lambda, gmt_batch** out);
+/* Batched independent PROBLEMS (scenes, not prebuilt instances): every
+ * problem's instance (build_instance, problem.cpp:336-363) is derived on the
+ * device, then solved by gmt_batch_launch.  Double-integrator problems with
+ * Halton sampling that share the start index, radius_override and model
+ * parameters take the shared sample pool of SURVEY.md §8(e): the context
+ * keeps the first K Halton points and their directed graph (built once,
+ * reused by later calls), and each query's graph is derived from it -- the
+ * induced subgraph on its first n free points, re-indexed by rank, plus the
+ * rows of its goal-substituted sample (sampling.cpp:115-141) and appended
+ * init (sampling.cpp:144-154) -- bit-identical to gmt_instance_build.  Every
+ * other problem (and the rare paths: pool too short, an init that duplicates
+ * a sample) is built by gmt_instance_build.  status_out[q]: GMT_OK or the
+ * query's own build error (GMT_E_GOAL_BLOCKED / GMT_E_INFEASIBLE_SAMPLING);
+ * failed queries are left out of the batch (its query index k counts the
+ * successful problems in order).  The batch owns the derived instances.   */
+int gmt_batch_create_problems(gmt_ctx* ctx, const gmt_problem* problems, int32_t count,
+                              int32_t* status_out, gmt_batch** out);
+/* The context's shared sample pool: points K, pool graph edges, and the
+ * wall time its last (re)build took (0 / 0 / 0 before first use).       */
+int gmt_ctx_pool_info(gmt_ctx* ctx, int32_t* pool_size, int64_t* num_edges, double* build_ms);
+/* Graph of batch query q as compressed rows (in-rows with costs and
+ * durations, out-row targets).  Two-call pattern: NULL in_ptr returns *n,
+ * *num_in and *num_out; then coords[n*dim] (may be NULL), in_ptr[n+1],
+ * in_col/in_cost/in_tau[num_in] (cost/tau may be NULL), out_ptr[n+1],
+ * out_col[num_out].                                                      */
+int gmt_batch_graph(gmt_ctx* ctx, gmt_batch* batch, int32_t query, int32_t* n, int64_t* num_in,
+                    int64_t* num_out, double* coords, int64_t* in_ptr, int32_t* in_col, double* in_cost,
+                    double* in_tau, int64_t* out_ptr, int32_t* out_col);
 int gmt_batch_launch(gmt_ctx* ctx, gmt_batch* batch); /* async on gmt_ctx_stream */
 int gmt_batch_summaries(gmt_ctx* ctx, gmt_batch* batch, gmt_plan_summary* out);
 int gmt_batch_result(gmt_ctx* ctx, gmt_batch* batch, int32_t query, gmt_plan_out* out);

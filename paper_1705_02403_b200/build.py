@@ -19,7 +19,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgmt_b200.so")
 OBJ = os.path.join(ROOT, "build", "obj")
-SOURCES = ["solve.cu", "graph.cu", "di_graph.cu", "sample.cu", "capi.cu", "cache.cu", "sim.cu", "batch_build.cu"]
+SOURCES = ["solve.cu", "graph.cu", "di_graph.cu", "sample.cu", "capi.cu", "cache.cu", "sim.cu", "batch_build.cu", "pool.cu"]
 HEADERS = ["common.cuh", "solve.cuh", "internal.cuh", "offline.cuh", "di.cuh", "quad.cuh", "dubins.cuh",
            "sample_dev.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -44,6 +44,8 @@ int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, b
                   std::vector<DevResult>& out, ResultScalars** scalars_base, int64_t* counters);
 int launch_jobs(gmt_ctx* ctx, const std::vector<SolveJob>& jobs, int cluster, int threads, size_t smem,
                 int obs_in_smem, int dim);
+int plan_problems_pool(gmt_ctx* ctx, const gmt_problem* problems, int32_t count, int32_t* status_out,
+                       gmt_plan_summary* summaries, int32_t path_cap, double* path_states);
 
 namespace {
 
@@ -977,6 +979,13 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
   if (count < 1) return set_error(GMT_E_INVALID_INPUT, "gmt_plan_problems needs at least one problem");
   const int d = problems[0].scene.dim;
   if (d < 1 || d > kMaxDimB) return set_error(GMT_E_INVALID_INPUT, "dimension must be in [1, 16]");
+  if (problems[0].steering == GMT_STEER_DOUBLE_INTEGRATOR) {  // the shared Halton pool (pool.cu)
+    for (int q = 1; q < count; ++q)
+      if (problems[q].steering != GMT_STEER_DOUBLE_INTEGRATOR)
+        return set_error(GMT_E_INVALID_INPUT,
+                         "gmt_plan_problems: a batch is all Euclidean or all double-integrator problems");
+    return plan_problems_pool(ctx, problems, count, status_out, summaries, path_cap, path_states);
+  }
   cudaStream_t s = ctx->stream;
 
   // ---- host: per-problem parameters and the packed scene arrays ----------
@@ -991,7 +1000,8 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
     const gmt_problem& pr = problems[q];
     if (pr.scene.dim != d) return set_error(GMT_E_INVALID_INPUT, "all problems of a batch share the dimension");
     if (pr.steering != GMT_STEER_EUCLIDEAN)
-      return set_error(GMT_E_INVALID_INPUT, "gmt_plan_problems covers the Euclidean steering model");
+      return set_error(GMT_E_INVALID_INPUT,
+                       "gmt_plan_problems: a batch is all Euclidean or all double-integrator problems");
     int rc = validate_scene(&pr.scene);
     if (rc) return rc;
     if (pr.n < 1) return set_error(GMT_E_INVALID_INPUT, "sample count must be >= 1");

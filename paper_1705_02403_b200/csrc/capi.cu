@@ -183,6 +183,9 @@ extern "C" void gmt_ctx_destroy(gmt_ctx* ctx) {
     ctx->scratch.release();
     ctx->jobs.release();
     ctx->pp_work.release();
+    ctx->pool_work.release();
+    destroy_pool(ctx->pool);
+    ctx->pool = nullptr;
     ctx->plan_inst.mem.release();
     ctx->plan_inst.desc_mem.release();
     ctx->plan_inst.aux.release();
@@ -750,26 +753,7 @@ extern "C" int gmt_plan_host(gmt_ctx* ctx, const gmt_scene* scene, const double*
   return plan_on(ctx, &inst, init_index, lambda, radius, out);
 }
 
-// ---- batches -----------------------------------------------------------------------
-struct gmt_batch {
-  gmt_ctx* ctx = nullptr;
-  Arena res;
-  Arena jobs_mem;
-  std::vector<SolveJob> jobs;
-  std::vector<DevResult> results;
-  std::vector<int64_t> node_off;
-  ResultScalars* scalars = nullptr;
-  size_t smem = 0;
-  int obs = 0;
-  int cluster = 1;
-  int threads = 256;
-  int dim = 0;  // common dimension of the queries (0: mixed)
-  ~gmt_batch() {
-    res.release();
-    jobs_mem.release();
-  }
-};
-
+// ---- batches (struct gmt_batch: internal.cuh) -------------------------------------------
 extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const* insts,
                                 const int32_t* init_index, double lambda, gmt_batch** out) {
   gmtb::AllocScope alloc_scope_(ctx);

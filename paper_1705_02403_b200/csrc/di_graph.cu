@@ -549,10 +549,15 @@ int build_kino_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const Mode
   return GMT_OK;
 }
 
+
+}  // namespace
+
 double di_prefilter_bound(const DiParams& P, double radius) {
   // vmax r + r^2 / (2 sqrt(3 w)), widened by 1e-9 relative against rounding.
   return (P.vmax * radius + radius * radius / (2.0 * std::sqrt(3.0 * P.weight))) * (1.0 + 1e-9) + 1e-12;
 }
+
+namespace {
 
 DiModel di_model(const gmt_di_params* p, double radius) {
   DiModel m;

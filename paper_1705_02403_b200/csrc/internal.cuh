@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "gmt_b200.h"
@@ -44,6 +45,12 @@ struct HostPinned {
 
 struct gmt_instance;
 struct gmt_ctx;
+
+namespace gmtb {
+// The shared Halton sample pool of a context (pool.cu).
+struct SamplePool;
+void destroy_pool(SamplePool* p);  // (call with the context's AllocScope active)
+}  // namespace gmtb
 
 namespace gmtb {
 // Makes `ctx`'s stream the allocation stream for the duration of a call.
@@ -105,8 +112,34 @@ struct gmt_ctx {
   gmtb::Arena scratch;    // host-batch inputs, offline build scratch
   gmtb::Arena jobs;       // SolveJob table
   gmtb::Arena pp_work;    // gmt_plan_problems: the batched offline phase's scratch + padded rows
+  gmtb::Arena pool_work;  // gmt_plan_problems over the shared pool: derived instances + scratch
+  gmtb::SamplePool* pool = nullptr;  // shared Halton pool + its graph (built on first use, reused)
   gmtb::HostPinned pinned;
   gmtb::HostPinned pinned2;
   gmtb::HostPinned pinned_jobs;
   gmt_instance plan_inst; // staging instance of gmt_plan_host
+};
+
+// A batch of independent queries (gmt_batch_create / gmt_batch_create_problems).
+struct gmt_batch {
+  gmt_ctx* ctx = nullptr;
+  gmtb::Arena res;
+  gmtb::Arena jobs_mem;
+  gmtb::Arena derived;                 // shared-pool batches: the derived per-query instances
+  std::vector<gmt_instance*> owned;    // shared-pool batches: queries built one by one (rare paths)
+  std::vector<gmtb::SolveJob> jobs;
+  std::vector<gmtb::DevResult> results;
+  std::vector<int64_t> node_off;
+  gmtb::ResultScalars* scalars = nullptr;
+  size_t smem = 0;
+  int obs = 0;
+  int cluster = 1;
+  int threads = 256;
+  int dim = 0;  // common dimension of the queries (0: mixed)
+  ~gmt_batch() {
+    res.release();
+    jobs_mem.release();
+    derived.release();
+    for (gmt_instance* i : owned) delete i;
+  }
 };

@@ -38,6 +38,8 @@ struct QuadParams;
 DiParams to_di(const gmt_di_params* p);
 QuadParams to_quad(const gmt_quad_params* p);
 int validate_di(const gmt_di_params* p);
+// |dp| bound of the double integrator's exact-safe pair prefilter (di_graph.cu).
+double di_prefilter_bound(const DiParams& P, double radius);
 int validate_quad(const gmt_quad_params* p);
 int build_di_graph_dev(gmt_ctx* ctx, const double* d_coords, int n, const gmt_di_params* p, double radius,
                        Arena& out_mem, DiRows* out, Arena& in_mem, DiRows* in);

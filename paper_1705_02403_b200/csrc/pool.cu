@@ -1,0 +1,1026 @@
+// pool.cu -- batched double-integrator queries over one shared Halton sample
+// pool (SURVEY.md §8(e), configs[4]).
+//
+// With Halton sampling every query's sample set is the first n free points
+// of the SAME stream (sample_free, sampling.cpp:97-108), and a kinodynamic
+// edge depends only on the two states and the cost threshold r.  So every
+// query's graph is the induced subgraph of one pool graph, re-indexed by the
+// monotone rank of the free points, plus two per-query rows:
+//   * the goal-substituted sample n-1 (sampling.cpp:115-141), when no free
+//     sample falls in the goal box, and
+//   * the appended init, vertex n (append_init, sampling.cpp:144-154).
+// Both are the largest indices, so they end every sorted out- and in-row
+// (graph.cpp:163-166, 184-186) they appear in.
+//
+// The pool (K Halton points + its directed graph, built once by the same
+// kinodynamic builder as every single instance) lives in the context and is
+// reused across calls.  Per call, for Q queries:
+//   pool_free_kernel     free flag of every (query, pool point)        Q x K
+//   pool_select_kernel   rank of every free point, the first n kept    Q blocks
+//   pool_subst_kernel    goal substitution (the reference's search)    Q blocks
+//   pool_init_kernel     append_init (exact-duplicate check)           Q blocks
+//   pool_special_kernel  out-/in-rows of the substituted goal and init  4 warps / query
+//   pool_rows_kernel     every derived row: the pool row filtered by
+//                        rank (ballot compaction) + the special entries warp / row
+//   pool_desc_kernel     the DevInstance of every query
+// Rows are padded: node x with pool point p starts at pool_ptr[p] + 2x of its
+// query's region (the two special entries fit behind the pool row), so no
+// scan is needed; DevInstance::in_end / out_end carry the row ends.  The
+// derived instances are bit-identical to gmt_instance_build of each problem
+// (tests/test_gpu_pool.py); queries off the fast path (pool too short, an
+// exact init duplicate, a long substitution search) take gmt_instance_build.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "di.cuh"
+#include "gmt_b200.h"
+#include "internal.cuh"
+#include "offline.cuh"
+#include "sample_dev.cuh"
+#include "solve.cuh"
+
+namespace gmtb {
+
+int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, int cluster, size_t* smem, int* obs_in_smem);
+int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, bool stats,
+                  std::vector<DevResult>& out, ResultScalars** scalars_base, int64_t* counters);
+
+struct SamplePool {
+  int K = 0;
+  uint64_t start_index = 1;
+  gmt_di_params gp{};
+  double radius = 0.0;
+  Arena coords;
+  Arena out_mem, in_mem;
+  DiRows out, in;
+  double build_ms = 0.0;
+};
+
+void destroy_pool(SamplePool* p) {
+  if (!p) return;
+  p->coords.release();
+  p->out_mem.release();
+  p->in_mem.release();
+  delete p;
+}
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kD = kDiDim;
+constexpr uint16_t kNoRank = 0xffffu;
+constexpr int kSpecCap = 1024;   // entries of one special row (larger: the single builder)
+constexpr int kSubstSearch = 1024;
+
+#define GMT_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_error(_e, #call); \
+  } while (0)
+
+struct Primes {
+  uint32_t p[kD];
+};
+
+// Sequential carving of one allocation into 16-byte aligned sections.
+struct Carver {
+  size_t off = 0;
+  template <typename T>
+  size_t take(size_t count) {
+    const size_t o = off;
+    off = align16(off + sizeof(T) * count);
+    return o;
+  }
+};
+
+// Per-query parameters (host -> device) and outcome (device -> host).
+struct PQ {
+  int32_t n;
+  int32_t nb;
+  int32_t skip;  // not on the pool path: the single builder
+  int32_t reserved;
+  int64_t box_off;   // first box (rows of kD doubles)
+  int64_t node_off;  // first node entry (n + 1 reserved)
+  int64_t slot_off;  // first slot of the query's row regions
+};
+struct PQOut {
+  int32_t fallback;
+  int32_t subst;
+  int32_t V;
+  int32_t init_index;
+  int32_t goal_any;
+  int32_t spec_len[4];  // out(g), in(g), out(init), in(init)
+  int32_t reserved;
+};
+
+__device__ __forceinline__ bool free_pt(const double* p, const double* lo, const double* hi, int nb) {
+  if (!point_in_cube(p, kD)) return false;  // point_free (space.cpp:47-54)
+  for (int b = 0; b < nb; ++b)
+    if (box_contains(lo + b * kD, hi + b * kD, kD, p)) return false;
+  return true;
+}
+
+// halton_point(start + p, 6) (sampling.cpp:46-51) for every pool point.
+__global__ void pool_points_kernel(int K, uint64_t start, Primes pr, double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K * kD; i += gridDim.x * blockDim.x) {
+    const int p = i / kD, k = i - p * kD;
+    out[i] = halton_dev(start + static_cast<uint64_t>(p), pr.p[k]);
+  }
+}
+
+// flags[q][p] = point_free(pool point p, boxes of q); the query's boxes are
+// staged in shared memory when they fit.
+__global__ void __launch_bounds__(256) pool_free_kernel(const PQ* __restrict__ pq, const double* __restrict__ P,
+                                                        int K, const double* __restrict__ box_lo,
+                                                        const double* __restrict__ box_hi, int stage_cap,
+                                                        uint8_t* __restrict__ flags) {
+  extern __shared__ double bsm[];
+  const int q = blockIdx.y;
+  const PQ Q = pq[q];
+  if (Q.skip) return;
+  const double* lo = box_lo + Q.box_off * kD;
+  const double* hi = box_hi + Q.box_off * kD;
+  if (Q.nb <= stage_cap) {
+    for (int i = threadIdx.x; i < Q.nb * kD; i += blockDim.x) {
+      bsm[i] = lo[i];
+      bsm[Q.nb * kD + i] = hi[i];
+    }
+    __syncthreads();
+    lo = bsm;
+    hi = bsm + Q.nb * kD;
+  }
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= K) return;
+  double x[kD];
+#pragma unroll
+  for (int k = 0; k < kD; ++k) x[k] = __ldg(P + static_cast<int64_t>(p) * kD + k);
+  flags[static_cast<int64_t>(q) * K + p] = free_pt(x, lo, hi, Q.nb) ? 1 : 0;
+}
+
+// The first n free pool points in stream order are the query's samples
+// 0..n-1 (sample_free's loop, sampling.cpp:97-108): ranks by a block scan.
+__global__ void __launch_bounds__(1024) pool_select_kernel(const PQ* __restrict__ pq, const double* __restrict__ P,
+                                                           int K, const uint8_t* __restrict__ flags,
+                                                           const double* __restrict__ goal_lo,
+                                                           const double* __restrict__ goal_hi,
+                                                           uint16_t* __restrict__ rank_of, int32_t* __restrict__ sel,
+                                                           double* __restrict__ qcoords, PQOut* __restrict__ out) {
+  __shared__ int warp_sum[32];
+  __shared__ int carry_s;
+  const int q = blockIdx.x;
+  const PQ Q = pq[q];
+  if (Q.skip) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* glo = goal_lo + static_cast<int64_t>(q) * kD;
+  const double* ghi = goal_hi + static_cast<int64_t>(q) * kD;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  bool in_goal = false;
+  for (int base = 0; base < K; base += blockDim.x) {
+    const int p = base + tid;
+    const int f = (p < K && flags[static_cast<int64_t>(q) * K + p]) ? 1 : 0;
+    const uint32_t m = __ballot_sync(kFull, f);
+    if (lane == 0) warp_sum[warp] = __popc(m);
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < static_cast<int>(blockDim.x >> 5) ? warp_sum[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sum[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    const int carry = carry_s;
+    const int rank = carry + (warp > 0 ? warp_sum[warp - 1] : 0) + __popc(m & ((1u << lane) - 1u));
+    const bool keep = f && rank < Q.n;
+    if (p < K) rank_of[static_cast<int64_t>(q) * K + p] = keep ? static_cast<uint16_t>(rank) : kNoRank;
+    if (keep) {
+      sel[Q.node_off + rank] = p;
+      double* c = qcoords + (Q.node_off + rank) * kD;
+#pragma unroll
+      for (int k = 0; k < kD; ++k) c[k] = P[static_cast<int64_t>(p) * kD + k];
+      in_goal = in_goal || box_contains(glo, ghi, kD, c);  // goal.contains (sampling.cpp:110-112)
+    }
+    __syncthreads();
+    if (tid == blockDim.x - 1) carry_s = carry + warp_sum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  const int any = __syncthreads_or(in_goal ? 1 : 0);
+  if (tid == 0) {
+    PQOut o{};
+    o.fallback = carry_s < Q.n ? 1 : 0;  // the pool holds fewer than n free points
+    o.goal_any = any;
+    o.V = Q.n + 1;
+    o.init_index = Q.n;
+    out[q] = o;
+  }
+}
+
+// Goal substitution (sampling.cpp:115-141): the first of the goal centre and
+// the goal-box Halton points that is free and no exact duplicate of samples
+// 0 .. n-2 replaces sample n-1 (whose pool point leaves the query).
+__global__ void __launch_bounds__(256) pool_subst_kernel(const PQ* __restrict__ pq, int K,
+                                                         const double* __restrict__ box_lo,
+                                                         const double* __restrict__ box_hi,
+                                                         const double* __restrict__ goal_lo,
+                                                         const double* __restrict__ goal_hi, Primes pr,
+                                                         uint16_t* __restrict__ rank_of, const int32_t* __restrict__ sel,
+                                                         double* __restrict__ qcoords, PQOut* __restrict__ out) {
+  __shared__ int best, dup;
+  const int q = blockIdx.x;
+  const PQ Q = pq[q];
+  if (Q.skip || out[q].fallback || out[q].goal_any) return;
+  const double* glo = goal_lo + static_cast<int64_t>(q) * kD;
+  const double* ghi = goal_hi + static_cast<int64_t>(q) * kD;
+  const double* lo = box_lo + Q.box_off * kD;
+  const double* hi = box_hi + Q.box_off * kD;
+  auto candidate = [&](int i, double* c) {
+    if (i == 0) {  // Aabb::center (space.cpp:18-22)
+      for (int k = 0; k < kD; ++k) c[k] = __dmul_rn(0.5, __dadd_rn(glo[k], ghi[k]));
+    } else {  // lo + q * (hi - lo) (sampling.cpp:122-124)
+      for (int k = 0; k < kD; ++k)
+        c[k] = __dadd_rn(glo[k], __dmul_rn(halton_dev(static_cast<uint64_t>(i), pr.p[k]), __dsub_rn(ghi[k], glo[k])));
+    }
+  };
+  int last = -1, found = -1;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      best = 0x7fffffff;
+      dup = 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSubstSearch; i += blockDim.x) {
+      if (i <= last) continue;
+      double c[kD];
+      candidate(i, c);
+      if (free_pt(c, lo, hi, Q.nb)) atomicMin(&best, i);
+    }
+    __syncthreads();
+    const int b = best;
+    if (b == 0x7fffffff) break;
+    double c[kD];
+    candidate(b, c);
+    for (int j = threadIdx.x; j < Q.n - 1; j += blockDim.x) {
+      const double* s = qcoords + (Q.node_off + j) * kD;
+      bool eq = true;
+      for (int k = 0; k < kD; ++k) eq = eq && c[k] == s[k];
+      if (eq) dup = 1;
+    }
+    __syncthreads();
+    const int was_dup = dup;
+    __syncthreads();
+    if (!was_dup) {
+      found = b;
+      break;
+    }
+    last = b;
+  }
+  if (threadIdx.x == 0) {
+    if (found < 0) {
+      out[q].fallback = 1;  // a longer search: the single builder
+    } else {
+      candidate(found, qcoords + (Q.node_off + Q.n - 1) * kD);
+      rank_of[static_cast<int64_t>(q) * K + sel[Q.node_off + Q.n - 1]] = kNoRank;
+      out[q].subst = 1;
+      out[q].goal_any = 1;
+    }
+  }
+}
+
+// append_init (sampling.cpp:144-154): an exact duplicate takes the single
+// builder (it would reuse the sample's index); else the init is vertex n.
+__global__ void __launch_bounds__(256) pool_init_kernel(const PQ* __restrict__ pq, const double* __restrict__ inits,
+                                                        double* __restrict__ qcoords, PQOut* __restrict__ out) {
+  __shared__ int dup;
+  const int q = blockIdx.x;
+  const PQ Q = pq[q];
+  if (Q.skip || out[q].fallback) return;
+  const double* init = inits + static_cast<int64_t>(q) * kD;
+  if (threadIdx.x == 0) dup = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < Q.n; i += blockDim.x) {
+    const double* c = qcoords + (Q.node_off + i) * kD;
+    bool eq = true;
+    for (int k = 0; k < kD; ++k) eq = eq && c[k] == init[k];
+    if (eq) dup = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (dup) {
+      out[q].fallback = 1;
+    } else {
+      for (int k = 0; k < kD; ++k) qcoords[(Q.node_off + Q.n) * kD + k] = init[k];
+    }
+  }
+}
+
+// The rows of the per-query vertices (list l: 0 out(g), 1 in(g), 2 out(init),
+// 3 in(init); g = n-1 when substituted, init = n): every other vertex x
+// tested with the builder's own prefilter and capped 2BVP solve, ascending x
+// (kino_rows_kernel's predicate and order, di_graph.cu).
+__global__ void __launch_bounds__(128) pool_special_kernel(const PQ* __restrict__ pq, DiParams P, double bound,
+                                                           double radius, const double* __restrict__ qcoords,
+                                                           int32_t* __restrict__ scol, double* __restrict__ scost,
+                                                           double* __restrict__ stau, PQOut* __restrict__ out) {
+  const int q = blockIdx.x;
+  const PQ Q = pq[q];
+  const int l = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (Q.skip || out[q].fallback) return;
+  if (l < 2 && !out[q].subst) return;
+  const int V = Q.n + 1;
+  const int s = l < 2 ? Q.n - 1 : Q.n;
+  const bool outgoing = (l & 1) == 0;
+  const double* base = qcoords + Q.node_off * kD;
+  double xs[kD];
+#pragma unroll
+  for (int k = 0; k < kD; ++k) xs[k] = base[static_cast<int64_t>(s) * kD + k];
+  const int64_t lb = (static_cast<int64_t>(q) * 4 + l) * kSpecCap;
+  int len = 0;
+  for (int b0 = 0; b0 < V; b0 += 32) {
+    const int x = b0 + lane;
+    bool keep = false;
+    double c = 0.0, t = 0.0;
+    if (x < V && x != s) {
+      double xx[kD];
+#pragma unroll
+      for (int k = 0; k < kD; ++k) xx[k] = base[static_cast<int64_t>(x) * kD + k];
+      const double* from = outgoing ? xs : xx;
+      const double* to = outgoing ? xx : xs;
+      bool may = true;
+      for (int k = 0; k < 3; ++k) {  // di_may_connect (di_graph.cu)
+        const double D = to[k] - from[k];
+        if (D > bound || -D > bound) may = false;
+      }
+      if (may) {
+        c = di_cost_tau(from, to, P, &t, radius);
+        keep = c <= radius;
+      }
+    }
+    const uint32_t m = __ballot_sync(kFull, keep);
+    const int slot = len + __popc(m & ((1u << lane) - 1u));
+    if (keep && slot < kSpecCap) {
+      scol[lb + slot] = x;
+      scost[lb + slot] = c;
+      stau[lb + slot] = t;
+    }
+    len += __popc(m);
+  }
+  if (lane == 0) {
+    out[q].spec_len[l] = len;
+    if (len > kSpecCap) out[q].fallback = 1;
+  }
+}
+
+__device__ __forceinline__ int find_sorted(const int32_t* a, int len, int x) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return (lo < len && a[lo] == x) ? lo : -1;
+}
+
+// Every derived row, warp per (query, vertex).  A pool vertex's rows are its
+// pool rows with non-member entries dropped (ballot compaction keeps their
+// ascending order, ranks being monotone) and member sources/targets mapped to
+// ranks, then the special vertices (n-1 before n) where the special rows hold
+// the edge.  A special vertex copies its own rows.
+__global__ void __launch_bounds__(256) pool_rows_kernel(
+    const PQ* __restrict__ pq, const PQOut* __restrict__ po, int K, int64_t Epool,
+    const int64_t* __restrict__ pin_ptr, const int32_t* __restrict__ pin_col, const double* __restrict__ pin_cost,
+    const double* __restrict__ pin_tau, const int64_t* __restrict__ pout_ptr, const int32_t* __restrict__ pout_col,
+    const uint16_t* __restrict__ rank_of, const int32_t* __restrict__ sel, const int32_t* __restrict__ scol,
+    const double* __restrict__ scost, const double* __restrict__ stau, int64_t* __restrict__ in_start,
+    int64_t* __restrict__ in_end, int64_t* __restrict__ out_start, int64_t* __restrict__ out_end,
+    int32_t* __restrict__ in_col, double* __restrict__ in_cost, double* __restrict__ in_tau,
+    int32_t* __restrict__ out_col) {
+  const int q = blockIdx.y;
+  const PQ Q = pq[q];
+  if (Q.skip) return;
+  const PQOut O = po[q];
+  if (O.fallback) return;
+  const int lane = threadIdx.x & 31;
+  const int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int n = Q.n;
+  if (x > n) return;
+  const int64_t so = Q.slot_off;
+  const int64_t lb = static_cast<int64_t>(q) * 4 * kSpecCap;
+  const bool subst = O.subst != 0;
+  const bool special = x == n || (subst && x == n - 1);
+  if (special) {
+    const int l = x == n ? 2 : 0;
+    const int64_t s0 = Epool + 2 * static_cast<int64_t>(n + 1) + (x == n ? kSpecCap : 0);
+    const int li = O.spec_len[l + 1], lo = O.spec_len[l];
+    for (int j = lane; j < li; j += 32) {
+      in_col[so + s0 + j] = scol[lb + (l + 1) * kSpecCap + j];
+      in_cost[so + s0 + j] = scost[lb + (l + 1) * kSpecCap + j];
+      in_tau[so + s0 + j] = stau[lb + (l + 1) * kSpecCap + j];
+    }
+    for (int j = lane; j < lo; j += 32) out_col[so + s0 + j] = scol[lb + l * kSpecCap + j];
+    if (lane == 0) {
+      in_start[Q.node_off + x] = s0;
+      in_end[Q.node_off + x] = s0 + li;
+      out_start[Q.node_off + x] = s0;
+      out_end[Q.node_off + x] = s0 + lo;
+    }
+    return;
+  }
+  const int p = sel[Q.node_off + x];
+  const uint16_t* rk = rank_of + static_cast<int64_t>(q) * K;
+  // in-row
+  {
+    const int64_t e0 = pin_ptr[p], e1 = pin_ptr[p + 1];
+    const int64_t s0 = e0 + 2 * static_cast<int64_t>(x);
+    int64_t w = s0;
+    for (int64_t b = e0; b < e1; b += 32) {
+      const int64_t e = b + lane;
+      uint16_t r = kNoRank;
+      if (e < e1) r = rk[pin_col[e]];
+      const bool keep = r != kNoRank;
+      const uint32_t m = __ballot_sync(kFull, keep);
+      if (keep) {
+        const int64_t slot = so + w + __popc(m & ((1u << lane) - 1u));
+        in_col[slot] = r;
+        in_cost[slot] = pin_cost[e];
+        in_tau[slot] = pin_tau[e];
+      }
+      w += __popc(m);
+    }
+    if (lane == 0) {  // edges from the special vertices: g (n-1) first, then init (n)
+      for (int l = subst ? 0 : 2; l <= 2; l += 2) {
+        const int j = find_sorted(scol + lb + l * kSpecCap, O.spec_len[l], x);
+        if (j >= 0) {
+          in_col[so + w] = l == 0 ? n - 1 : n;
+          in_cost[so + w] = scost[lb + l * kSpecCap + j];
+          in_tau[so + w] = stau[lb + l * kSpecCap + j];
+          ++w;
+        }
+      }
+      in_start[Q.node_off + x] = s0;
+      in_end[Q.node_off + x] = w;
+    }
+  }
+  // out-row
+  {
+    const int64_t e0 = pout_ptr[p], e1 = pout_ptr[p + 1];
+    const int64_t s0 = e0 + 2 * static_cast<int64_t>(x);
+    int64_t w = s0;
+    for (int64_t b = e0; b < e1; b += 32) {
+      const int64_t e = b + lane;
+      uint16_t r = kNoRank;
+      if (e < e1) r = rk[pout_col[e]];
+      const bool keep = r != kNoRank;
+      const uint32_t m = __ballot_sync(kFull, keep);
+      if (keep) out_col[so + w + __popc(m & ((1u << lane) - 1u))] = r;
+      w += __popc(m);
+    }
+    if (lane == 0) {  // edges into the special vertices
+      for (int l = subst ? 1 : 3; l <= 3; l += 2) {
+        if (find_sorted(scol + lb + l * kSpecCap, O.spec_len[l], x) >= 0) out_col[so + w++] = l == 1 ? n - 1 : n;
+      }
+      out_start[Q.node_off + x] = s0;
+      out_end[Q.node_off + x] = w;
+    }
+  }
+}
+
+__global__ void pool_desc_kernel(const PQ* __restrict__ pq, const PQOut* __restrict__ po, int count, double radius,
+                                 DiParams P, const double* __restrict__ qcoords, const double* __restrict__ box_lo,
+                                 const double* __restrict__ box_hi, const double* __restrict__ goal_lo,
+                                 const double* __restrict__ goal_hi, const int64_t* __restrict__ in_start,
+                                 const int64_t* __restrict__ in_end, const int64_t* __restrict__ out_start,
+                                 const int64_t* __restrict__ out_end, const int32_t* __restrict__ in_col,
+                                 const double* __restrict__ in_cost, const double* __restrict__ in_tau,
+                                 const int32_t* __restrict__ out_col, DevInstance* __restrict__ descs) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const PQ Q = pq[q];
+  if (Q.skip || po[q].fallback) return;
+  DevInstance D{};
+  D.n = Q.n + 1;
+  D.dim = kD;
+  D.num_boxes = Q.nb;
+  D.directed = 1;
+  D.goal_count = po[q].goal_any;
+  D.init_index = Q.n;
+  D.radius = radius;
+  D.num_edges = -1;  // (rows are padded; gmt_batch_graph counts them)
+  D.coords = qcoords + Q.node_off * kD;
+  D.box_lo = box_lo + Q.box_off * kD;
+  D.box_hi = box_hi + Q.box_off * kD;
+  D.goal_lo = goal_lo + static_cast<int64_t>(q) * kD;
+  D.goal_hi = goal_hi + static_cast<int64_t>(q) * kD;
+  D.out_ptr = out_start + Q.node_off;
+  D.out_end = out_end + Q.node_off;
+  D.out_col = out_col + Q.slot_off;
+  D.out_cost = nullptr;  // (the solve reads out-row targets only)
+  D.in_ptr = in_start + Q.node_off;
+  D.in_end = in_end + Q.node_off;
+  D.in_col = in_col + Q.slot_off;
+  D.in_cost = in_cost + Q.slot_off;
+  D.in_tau = in_tau + Q.slot_off;
+  D.steering = GMT_STEER_DOUBLE_INTEGRATOR;
+  D.kin_segments = P.segments;
+  D.kin_p[0] = P.vmax;
+  D.kin_p[1] = P.weight;
+  descs[q] = D;
+}
+
+__global__ void pool_gather_paths_kernel(const DevResult* __restrict__ rs, const DevInstance* const* __restrict__ insts,
+                                         int count, int cap, int d, double* __restrict__ out) {
+  const int q = blockIdx.x;
+  if (q >= count) return;
+  const DevResult R = rs[q];
+  const ResultScalars sc = *R.scalars;
+  const DevInstance* I = insts[q];
+  const int len = sc.status != 0 ? 0 : (sc.path_len < cap ? sc.path_len : cap);
+  for (int e = threadIdx.x; e < cap * d; e += blockDim.x) {
+    const int k = e / d, i = e - k * d;
+    out[static_cast<int64_t>(q) * cap * d + e] = k < len ? I->coords[static_cast<int64_t>(R.path[k]) * d + i] : 0.0;
+  }
+}
+
+bool same_params(const gmt_di_params& a, const gmt_di_params& b) {
+  return a.vmax == b.vmax && a.weight == b.weight && a.segments == b.segments;
+}
+
+// Problems that can take the shared pool of problems[0]'s sampling source.
+bool pool_eligible(const gmt_problem& p, const gmt_problem& p0) {
+  return p.steering == GMT_STEER_DOUBLE_INTEGRATOR && p.scene.dim == kD &&
+         p.sampling.kind == GMT_SAMPLE_HALTON && p.sampling.start_index == p0.sampling.start_index &&
+         p.radius_override > 0.0 && p.radius_override == p0.radius_override && same_params(p.di, p0.di) &&
+         p.n >= 2 && p.n < static_cast<int>(kNoRank) && p.sampling.with_heading == 0;
+}
+
+// Pool points needed for a problem: n over the free-volume estimate (boxes
+// clipped to the unit cube), +5 % + 256 (as gmt_plan_problems sizes its
+// candidates); a query that still runs short takes the single builder.
+int pool_need(const gmt_problem& pr) {
+  double blocked = 0.0;
+  for (int b = 0; b < pr.scene.num_boxes; ++b) {
+    double v = 1.0;
+    for (int k = 0; k < kD; ++k) {
+      const double lo = std::max(0.0, pr.scene.box_lo[static_cast<size_t>(b) * kD + k]);
+      const double hi = std::min(1.0, pr.scene.box_hi[static_cast<size_t>(b) * kD + k]);
+      v *= std::max(0.0, hi - lo);
+    }
+    blocked += v;
+  }
+  const double free_est = std::max(0.05, 1.0 - blocked);
+  return static_cast<int>(std::ceil(std::min(4.0 * pr.n, pr.n / free_est * 1.05) + 256.0));
+}
+
+// The context's pool for problems like p0 with at least K points.
+int get_pool(gmt_ctx* ctx, const gmt_problem& p0, int K, SamplePool** out) {
+  SamplePool* cur = ctx->pool;
+  if (cur && cur->start_index == p0.sampling.start_index && cur->radius == p0.radius_override &&
+      same_params(cur->gp, p0.di) && cur->K >= K) {
+    *out = cur;
+    return GMT_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  if (cur && cur->start_index == p0.sampling.start_index && cur->radius == p0.radius_override &&
+      same_params(cur->gp, p0.di))
+    K = std::max(K, cur->K + cur->K / 4);  // grow geometrically
+  K = (K + 1023) & ~1023;
+  auto* pool = new SamplePool;
+  pool->K = K;
+  pool->start_index = p0.sampling.start_index;
+  pool->gp = p0.di;
+  pool->radius = p0.radius_override;
+  int rc = pool->coords.reserve(sizeof(double) * static_cast<size_t>(K) * kD);
+  if (rc) {
+    destroy_pool(pool);
+    return rc;
+  }
+  Primes pr;
+  for (int k = 0; k < kD; ++k) pr.p[k] = nth_prime_h(k + 1);
+  pool_points_kernel<<<std::min((K * kD + 255) / 256, 4096), 256, 0, ctx->stream>>>(
+      K, pool->start_index, pr, static_cast<double*>(pool->coords.ptr));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    destroy_pool(pool);
+    return cuda_error(e, "pool points");
+  }
+  ++ctx->launches;
+  rc = build_di_graph_dev(ctx, static_cast<const double*>(pool->coords.ptr), K, &pool->gp, pool->radius,
+                          pool->out_mem, &pool->out, pool->in_mem, &pool->in);
+  if (rc) {
+    destroy_pool(pool);
+    return rc;
+  }
+  e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    destroy_pool(pool);
+    return cuda_error(e, "pool graph");
+  }
+  pool->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  destroy_pool(ctx->pool);
+  ctx->pool = pool;
+  *out = pool;
+  return GMT_OK;
+}
+
+}  // namespace
+
+// Derive the instances of `count` problems into `arena` (device).  On return
+// inst[q] is the device descriptor of query q (a derived one, or one of the
+// single-built instances appended to `owned`; null when the query's own build
+// failed with status[q] = GMT_E_GOAL_BLOCKED / GMT_E_INFEASIBLE_SAMPLING),
+// V[q] its vertex count and init[q] its init index.
+int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& arena,
+                std::vector<gmt_instance*>& owned, std::vector<const DevInstance*>& inst, std::vector<int>& V,
+                std::vector<int>& init, std::vector<double>& radius, std::vector<int32_t>& status, int* max_V,
+                int* max_nb) {
+  cudaStream_t s = ctx->stream;
+  const gmt_problem& p0 = problems[0];
+  inst.assign(count, nullptr);
+  V.assign(count, 0);
+  init.assign(count, 0);
+  radius.assign(count, 0.0);
+  status.assign(count, GMT_OK);
+  *max_V = 0;
+  *max_nb = 0;
+  std::vector<PQ> pq(count);
+  std::vector<double> box_lo, box_hi, goal_lo(static_cast<size_t>(count) * kD), goal_hi(goal_lo.size()),
+      inits(goal_lo.size());
+  int K = 0, eligible = 0, max_nbp = 0, max_n = 0;
+  for (int q = 0; q < count; ++q) {
+    const gmt_problem& pr = problems[q];
+    int rc = validate_scene(&pr.scene);
+    if (rc) return rc;
+    if (!(pr.lambda > 0.0 && pr.lambda <= 1.0)) return set_error(GMT_E_INVALID_INPUT, "lambda must be in (0, 1]");
+    PQ& Q = pq[q];
+    std::memset(&Q, 0, sizeof(Q));
+    Q.skip = pool_eligible(pr, p0) && validate_di(&pr.di) == GMT_OK ? 0 : 1;
+    if (Q.skip) continue;
+    ++eligible;
+    Q.n = pr.n;
+    Q.nb = pr.scene.num_boxes;
+    K = std::max(K, pool_need(pr));
+    max_nbp = std::max(max_nbp, Q.nb);
+    max_n = std::max(max_n, pr.n);
+  }
+  g_last_error.clear();
+  SamplePool* pool = nullptr;
+  if (eligible) {
+    int rc = get_pool(ctx, p0, K, &pool);
+    if (rc) return rc;
+    K = pool->K;
+  }
+  // host layout
+  int64_t box_total = 0, node_total = 0, slot_total = 0;
+  const int64_t Ep = pool ? pool->in.edges : 0;
+  for (int q = 0; q < count; ++q) {
+    PQ& Q = pq[q];
+    if (Q.skip) continue;
+    const gmt_problem& pr = problems[q];
+    Q.box_off = box_total;
+    Q.node_off = node_total;
+    Q.slot_off = slot_total;
+    box_lo.insert(box_lo.end(), pr.scene.box_lo, pr.scene.box_lo + static_cast<size_t>(Q.nb) * kD);
+    box_hi.insert(box_hi.end(), pr.scene.box_hi, pr.scene.box_hi + static_cast<size_t>(Q.nb) * kD);
+    std::copy(pr.scene.goal_lo, pr.scene.goal_lo + kD, goal_lo.begin() + static_cast<size_t>(q) * kD);
+    std::copy(pr.scene.goal_hi, pr.scene.goal_hi + kD, goal_hi.begin() + static_cast<size_t>(q) * kD);
+    std::copy(pr.init, pr.init + kD, inits.begin() + static_cast<size_t>(q) * kD);
+    box_total += Q.nb;
+    node_total += Q.n + 1;
+    slot_total += Ep + 2 * static_cast<int64_t>(Q.n + 1) + 2 * kSpecCap;
+  }
+  std::vector<PQOut> po(count);
+  if (eligible) {
+    Carver c;
+    const size_t o_pq = c.take<PQ>(count);
+    const size_t o_po = c.take<PQOut>(count);
+    const size_t o_blo = c.take<double>(std::max<int64_t>(box_total, 1) * kD);
+    const size_t o_bhi = c.take<double>(std::max<int64_t>(box_total, 1) * kD);
+    const size_t o_glo = c.take<double>(goal_lo.size());
+    const size_t o_ghi = c.take<double>(goal_hi.size());
+    const size_t o_init = c.take<double>(inits.size());
+    const size_t o_flag = c.take<uint8_t>(static_cast<size_t>(count) * K);
+    const size_t o_rank = c.take<uint16_t>(static_cast<size_t>(count) * K);
+    const size_t o_sel = c.take<int32_t>(node_total);
+    const size_t o_qc = c.take<double>(node_total * kD);
+    const size_t o_scol = c.take<int32_t>(static_cast<size_t>(count) * 4 * kSpecCap);
+    const size_t o_scost = c.take<double>(static_cast<size_t>(count) * 4 * kSpecCap);
+    const size_t o_stau = c.take<double>(static_cast<size_t>(count) * 4 * kSpecCap);
+    const size_t o_is = c.take<int64_t>(node_total);
+    const size_t o_ie = c.take<int64_t>(node_total);
+    const size_t o_os = c.take<int64_t>(node_total);
+    const size_t o_oe = c.take<int64_t>(node_total);
+    const size_t o_icol = c.take<int32_t>(slot_total);
+    const size_t o_icost = c.take<double>(slot_total);
+    const size_t o_itau = c.take<double>(slot_total);
+    const size_t o_ocol = c.take<int32_t>(slot_total);
+    const size_t o_desc = c.take<DevInstance>(count);
+    int rc = arena.reserve(c.off);
+    if (rc) return rc;
+    char* B = static_cast<char*>(arena.ptr);
+    auto* d_pq = reinterpret_cast<PQ*>(B + o_pq);
+    auto* d_po = reinterpret_cast<PQOut*>(B + o_po);
+    auto* d_blo = reinterpret_cast<double*>(B + o_blo);
+    auto* d_bhi = reinterpret_cast<double*>(B + o_bhi);
+    auto* d_glo = reinterpret_cast<double*>(B + o_glo);
+    auto* d_ghi = reinterpret_cast<double*>(B + o_ghi);
+    auto* d_init = reinterpret_cast<double*>(B + o_init);
+    auto* d_flag = reinterpret_cast<uint8_t*>(B + o_flag);
+    auto* d_rank = reinterpret_cast<uint16_t*>(B + o_rank);
+    auto* d_sel = reinterpret_cast<int32_t*>(B + o_sel);
+    auto* d_qc = reinterpret_cast<double*>(B + o_qc);
+    auto* d_scol = reinterpret_cast<int32_t*>(B + o_scol);
+    auto* d_scost = reinterpret_cast<double*>(B + o_scost);
+    auto* d_stau = reinterpret_cast<double*>(B + o_stau);
+    auto* d_is = reinterpret_cast<int64_t*>(B + o_is);
+    auto* d_ie = reinterpret_cast<int64_t*>(B + o_ie);
+    auto* d_os = reinterpret_cast<int64_t*>(B + o_os);
+    auto* d_oe = reinterpret_cast<int64_t*>(B + o_oe);
+    auto* d_icol = reinterpret_cast<int32_t*>(B + o_icol);
+    auto* d_icost = reinterpret_cast<double*>(B + o_icost);
+    auto* d_itau = reinterpret_cast<double*>(B + o_itau);
+    auto* d_ocol = reinterpret_cast<int32_t*>(B + o_ocol);
+    auto* d_desc = reinterpret_cast<DevInstance*>(B + o_desc);
+    auto put = [&](void* dst, const void* src, size_t bytes) -> int {
+      if (bytes) GMT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+      return GMT_OK;
+    };
+    if ((rc = put(d_pq, pq.data(), sizeof(PQ) * count)) ||
+        (rc = put(d_blo, box_lo.data(), sizeof(double) * box_lo.size())) ||
+        (rc = put(d_bhi, box_hi.data(), sizeof(double) * box_hi.size())) ||
+        (rc = put(d_glo, goal_lo.data(), sizeof(double) * goal_lo.size())) ||
+        (rc = put(d_ghi, goal_hi.data(), sizeof(double) * goal_hi.size())) ||
+        (rc = put(d_init, inits.data(), sizeof(double) * inits.size())))
+      return rc;
+    Primes pr;
+    for (int k = 0; k < kD; ++k) pr.p[k] = nth_prime_h(k + 1);
+    const double* P = static_cast<const double*>(pool->coords.ptr);
+    const int stage_cap = 2048;  // boxes staged in shared memory up to 2048 * 96 B
+    const int nb_st = std::min(max_nbp, stage_cap);
+    const size_t fsm = sizeof(double) * 2 * kD * static_cast<size_t>(std::max(nb_st, 1));
+    if (fsm > 48 * 1024)
+      GMT_CUDA(cudaFuncSetAttribute(pool_free_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsm)));
+    pool_free_kernel<<<dim3((K + 255) / 256, count), 256, fsm, s>>>(d_pq, P, K, d_blo, d_bhi, nb_st, d_flag);
+    pool_select_kernel<<<count, 1024, 0, s>>>(d_pq, P, K, d_flag, d_glo, d_ghi, d_rank, d_sel, d_qc, d_po);
+    pool_subst_kernel<<<count, 256, 0, s>>>(d_pq, K, d_blo, d_bhi, d_glo, d_ghi, pr, d_rank, d_sel, d_qc, d_po);
+    pool_init_kernel<<<count, 256, 0, s>>>(d_pq, d_init, d_qc, d_po);
+    const DiParams DP = to_di(&p0.di);
+    pool_special_kernel<<<count, 128, 0, s>>>(d_pq, DP, di_prefilter_bound(DP, pool->radius), pool->radius, d_qc,
+                                              d_scol, d_scost, d_stau, d_po);
+    pool_rows_kernel<<<dim3((max_n + 1 + 7) / 8, count), 256, 0, s>>>(
+        d_pq, d_po, K, Ep, pool->in.ptr, pool->in.col, pool->in.cost, pool->in.tau, pool->out.ptr, pool->out.col,
+        d_rank, d_sel, d_scol, d_scost, d_stau, d_is, d_ie, d_os, d_oe, d_icol, d_icost, d_itau, d_ocol);
+    pool_desc_kernel<<<(count + 127) / 128, 128, 0, s>>>(d_pq, d_po, count, pool->radius, DP, d_qc, d_blo, d_bhi,
+                                                         d_glo, d_ghi, d_is, d_ie, d_os, d_oe, d_icol, d_icost,
+                                                         d_itau, d_ocol, d_desc);
+    GMT_CUDA(cudaGetLastError());
+    ctx->launches += 8;
+    GMT_CUDA(cudaMemcpyAsync(po.data(), d_po, sizeof(PQOut) * count, cudaMemcpyDeviceToHost, s));
+    GMT_CUDA(cudaStreamSynchronize(s));
+    for (int q = 0; q < count; ++q) {
+      if (pq[q].skip || po[q].fallback) continue;
+      inst[q] = d_desc + q;
+      V[q] = pq[q].n + 1;
+      init[q] = pq[q].n;
+      radius[q] = pool->radius;
+      *max_V = std::max(*max_V, V[q]);
+      *max_nb = std::max(*max_nb, pq[q].nb);
+    }
+  }
+  // The rare paths and the problems off the pool: the single-instance builder.
+  for (int q = 0; q < count; ++q) {
+    if (!pq[q].skip && !po[q].fallback) continue;
+    gmt_instance* one = nullptr;
+    int rc = gmt_instance_build(ctx, &problems[q], &one);
+    if (rc == GMT_E_GOAL_BLOCKED || rc == GMT_E_INFEASIBLE_SAMPLING) {
+      status[q] = rc;  // the query's own build outcome (sampling.cpp:97-141)
+      continue;
+    }
+    if (rc) return rc;
+    owned.push_back(one);
+    inst[q] = static_cast<const DevInstance*>(one->desc_mem.ptr);
+    V[q] = one->desc.n;
+    init[q] = one->desc.init_index;
+    radius[q] = one->desc.radius;
+    *max_V = std::max(*max_V, V[q]);
+    *max_nb = std::max(*max_nb, one->desc.num_boxes);
+  }
+  return GMT_OK;
+}
+
+int pool_stats(const gmt_ctx* ctx, int32_t* K, int64_t* edges, double* build_ms) {
+  const SamplePool* p = ctx->pool;
+  if (K) *K = p ? p->K : 0;
+  if (edges) *edges = p ? p->out.edges : 0;
+  if (build_ms) *build_ms = p ? p->build_ms : 0.0;
+  return GMT_OK;
+}
+
+// Solve jobs for derived queries (status != OK entries are skipped).
+static int batch_from_derived(gmt_ctx* ctx, gmt_batch* b, const gmt_problem* problems, int count,
+                              const std::vector<const DevInstance*>& inst, const std::vector<int>& V,
+                              const std::vector<int>& init, const std::vector<double>& radius, int max_V,
+                              int max_nb, std::vector<int>& job_q) {
+  b->ctx = ctx;
+  b->node_off.assign(1, 0);
+  job_q.clear();
+  const int d = problems[0].scene.dim;
+  bool kino = false;
+  for (int q = 0; q < count; ++q) {
+    if (problems[q].scene.dim != d) return set_error(GMT_E_INVALID_INPUT, "all problems of a batch share the dimension");
+    kino = kino || problems[q].steering != GMT_STEER_EUCLIDEAN;
+    if (!inst[q]) continue;
+    SolveJob j{};
+    j.inst = inst[q];
+    j.init_index = init[q];
+    j.mode = kModeGmt;
+    j.lambda = problems[q].lambda;
+    j.radius = radius[q];
+    b->jobs.push_back(j);
+    b->node_off.push_back(b->node_off.back() + V[q]);
+    job_q.push_back(q);
+  }
+  const int J = static_cast<int>(b->jobs.size());
+  if (J == 0) return GMT_OK;
+  b->dim = d;
+  // (the shape gmt_batch_create picks: 2-CTA clusters for kinodynamic queries)
+  b->cluster = ctx->batch_cluster ? ctx->batch_cluster : (kino ? 2 : 1);
+  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
+  int rc = plan_smem(ctx, max_V, d, max_nb, b->cluster, &b->smem, &b->obs);
+  if (rc) return rc;
+  rc = carve_results(b->res, J, b->node_off.data(), true, true, b->results, &b->scalars,
+                     ctx->counting ? ctx->counters : nullptr);
+  if (rc) return rc;
+  for (int k = 0; k < J; ++k) b->jobs[k].res = b->results[k];
+  rc = b->jobs_mem.reserve(sizeof(SolveJob) * J);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(b->jobs_mem.ptr, b->jobs.data(), sizeof(SolveJob) * J, cudaMemcpyHostToDevice,
+                                  ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return cuda_error(e, "batch jobs");
+  return GMT_OK;
+}
+
+// gmt_plan_problems for double-integrator problems (batch_build.cu routes here).
+int plan_problems_pool(gmt_ctx* ctx, const gmt_problem* problems, int32_t count, int32_t* status_out,
+                       gmt_plan_summary* summaries, int32_t path_cap, double* path_states) {
+  std::vector<gmt_instance*> owned;
+  std::vector<const DevInstance*> inst;
+  std::vector<int> V, init, job_q;
+  std::vector<double> radius;
+  std::vector<int32_t> status;
+  int max_V = 0, max_nb = 0;
+  int rc = pool_derive(ctx, problems, count, ctx->pool_work, owned, inst, V, init, radius, status, &max_V, &max_nb);
+  gmt_batch b;
+  if (rc == GMT_OK) rc = batch_from_derived(ctx, &b, problems, count, inst, V, init, radius, max_V, max_nb, job_q);
+  const int J = static_cast<int>(b.jobs.size());
+  cudaStream_t s = ctx->stream;
+  if (rc == GMT_OK && J > 0) {
+    rc = gmt_batch_launch(ctx, &b);
+    std::vector<ResultScalars> hs(J);
+    cudaError_t e = cudaSuccess;
+    if (rc == GMT_OK) e = cudaMemcpyAsync(hs.data(), b.scalars, sizeof(ResultScalars) * J, cudaMemcpyDeviceToHost, s);
+    Arena pg;
+    if (rc == GMT_OK && e == cudaSuccess && path_states && path_cap > 0) {
+      const size_t o_r = 0, o_i = align16(sizeof(DevResult) * J), o_o = o_i + align16(sizeof(void*) * J);
+      rc = pg.reserve(o_o + sizeof(double) * static_cast<size_t>(J) * path_cap * kD);
+      if (rc == GMT_OK) {
+        std::vector<const DevInstance*> ip(J);
+        for (int k = 0; k < J; ++k) ip[k] = b.jobs[k].inst;
+        char* g = static_cast<char*>(pg.ptr);
+        e = cudaMemcpyAsync(g + o_r, b.results.data(), sizeof(DevResult) * J, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(g + o_i, ip.data(), sizeof(void*) * J, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) {
+          pool_gather_paths_kernel<<<J, 128, 0, s>>>(reinterpret_cast<const DevResult*>(g + o_r),
+                                                     reinterpret_cast<const DevInstance* const*>(g + o_i), J,
+                                                     path_cap, kD, reinterpret_cast<double*>(g + o_o));
+          e = cudaGetLastError();
+          ++ctx->launches;
+        }
+        std::vector<double> hp(static_cast<size_t>(J) * path_cap * kD);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(hp.data(), g + o_o, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e == cudaSuccess)
+          for (int k = 0; k < J; ++k)
+            std::memcpy(path_states + static_cast<size_t>(job_q[k]) * path_cap * kD,
+                        hp.data() + static_cast<size_t>(k) * path_cap * kD, sizeof(double) * path_cap * kD);
+      }
+    }
+    if (rc == GMT_OK && e == cudaSuccess) e = cudaStreamSynchronize(s);
+    pg.release();
+    if (rc == GMT_OK && e != cudaSuccess) rc = cuda_error(e, "gmt_plan_problems results");
+    if (rc == GMT_OK) {
+      for (int k = 0; k < J; ++k) {
+        gmt_plan_summary& o = summaries[job_q[k]];
+        o.status = hs[k].status;
+        o.goal_node = hs[k].goal_node;
+        o.cost = hs[k].cost;
+        o.iterations = hs[k].iterations;
+        o.total_collision_checks = hs[k].total_checks;
+        o.path_len = hs[k].path_len;
+        o.num_stats = hs[k].num_stats;
+      }
+    }
+  }
+  if (rc == GMT_OK)
+    for (int q = 0; q < count; ++q) status_out[q] = status[q];
+  b.res.release();
+  b.jobs_mem.release();
+  for (gmt_instance* i : owned) gmt_instance_destroy(i);
+  return rc;
+}
+
+}  // namespace gmtb
+
+using namespace gmtb;
+
+extern "C" int gmt_batch_create_problems(gmt_ctx* ctx, const gmt_problem* problems, int32_t count,
+                                         int32_t* status_out, gmt_batch** out) {
+  gmtb::AllocScope alloc_scope_(ctx);
+  *out = nullptr;
+  if (count < 1) return set_error(GMT_E_INVALID_INPUT, "batch needs at least one problem");
+  auto* b = new gmt_batch;
+  std::vector<const DevInstance*> inst;
+  std::vector<int> V, init, job_q;
+  std::vector<double> radius;
+  std::vector<int32_t> status;
+  int max_V = 0, max_nb = 0;
+  int rc = pool_derive(ctx, problems, count, b->derived, b->owned, inst, V, init, radius, status, &max_V, &max_nb);
+  if (rc == GMT_OK) rc = batch_from_derived(ctx, b, problems, count, inst, V, init, radius, max_V, max_nb, job_q);
+  if (rc == GMT_OK && b->jobs.empty()) rc = set_error(GMT_E_INVALID_INPUT, "no problem of the batch could be built");
+  if (rc != GMT_OK) {
+    delete b;
+    return rc;
+  }
+  for (int q = 0; q < count; ++q) status_out[q] = status[q];
+  *out = b;
+  return GMT_OK;
+}
+
+extern "C" int gmt_ctx_pool_info(gmt_ctx* ctx, int32_t* pool_size, int64_t* num_edges, double* build_ms) {
+  if (!ctx) return set_error(GMT_E_INVALID_INPUT, "context is null");
+  return pool_stats(ctx, pool_size, num_edges, build_ms);
+}
+
+// Rows of batch query q as compressed rows (host): the two-call pattern of
+// the graph entry points (NULL in_ptr: sizes only).
+extern "C" int gmt_batch_graph(gmt_ctx* ctx, gmt_batch* b, int32_t q, int32_t* n, int64_t* num_in, int64_t* num_out,
+                               double* coords, int64_t* in_ptr, int32_t* in_col, double* in_cost, double* in_tau,
+                               int64_t* out_ptr, int32_t* out_col) {
+  gmtb::AllocScope alloc_scope_(ctx);
+  if (!b || q < 0 || q >= static_cast<int32_t>(b->jobs.size()))
+    return set_error(GMT_E_INVALID_INPUT, "query index out of range");
+  cudaStream_t s = ctx->stream;
+  DevInstance D;
+  GMT_CUDA(cudaMemcpyAsync(&D, b->jobs[q].inst, sizeof(D), cudaMemcpyDeviceToHost, s));
+  GMT_CUDA(cudaStreamSynchronize(s));
+  const int V = D.n;
+  std::vector<int64_t> is(V + 1), ie(V), os(V + 1), oe(V);
+  GMT_CUDA(cudaMemcpyAsync(is.data(), D.in_ptr, sizeof(int64_t) * (D.in_end ? V : V + 1), cudaMemcpyDeviceToHost, s));
+  GMT_CUDA(cudaMemcpyAsync(os.data(), D.out_ptr, sizeof(int64_t) * (D.out_end ? V : V + 1), cudaMemcpyDeviceToHost, s));
+  if (D.in_end) GMT_CUDA(cudaMemcpyAsync(ie.data(), D.in_end, sizeof(int64_t) * V, cudaMemcpyDeviceToHost, s));
+  if (D.out_end) GMT_CUDA(cudaMemcpyAsync(oe.data(), D.out_end, sizeof(int64_t) * V, cudaMemcpyDeviceToHost, s));
+  GMT_CUDA(cudaStreamSynchronize(s));
+  for (int x = 0; x < V; ++x) {
+    if (!D.in_end) ie[x] = is[x + 1];
+    if (!D.out_end) oe[x] = os[x + 1];
+  }
+  int64_t ni = 0, no = 0;
+  for (int x = 0; x < V; ++x) {
+    ni += ie[x] - is[x];
+    no += oe[x] - os[x];
+  }
+  *n = V;
+  *num_in = ni;
+  *num_out = no;
+  if (!in_ptr) return GMT_OK;
+  if (coords) GMT_CUDA(cudaMemcpyAsync(coords, D.coords, sizeof(double) * V * D.dim, cudaMemcpyDeviceToHost, s));
+  int64_t wi = 0, wo = 0;
+  in_ptr[0] = 0;
+  out_ptr[0] = 0;
+  for (int x = 0; x < V; ++x) {
+    const int64_t li = ie[x] - is[x], lo = oe[x] - os[x];
+    if (li) {
+      GMT_CUDA(cudaMemcpyAsync(in_col + wi, D.in_col + is[x], sizeof(int32_t) * li, cudaMemcpyDeviceToHost, s));
+      if (in_cost && D.in_cost)
+        GMT_CUDA(cudaMemcpyAsync(in_cost + wi, D.in_cost + is[x], sizeof(double) * li, cudaMemcpyDeviceToHost, s));
+      if (in_tau && D.in_tau)
+        GMT_CUDA(cudaMemcpyAsync(in_tau + wi, D.in_tau + is[x], sizeof(double) * li, cudaMemcpyDeviceToHost, s));
+    }
+    if (lo && out_col)
+      GMT_CUDA(cudaMemcpyAsync(out_col + wo, D.out_col + os[x], sizeof(int32_t) * lo, cudaMemcpyDeviceToHost, s));
+    wi += li;
+    wo += lo;
+    in_ptr[x + 1] = wi;
+    out_ptr[x + 1] = wo;
+  }
+  GMT_CUDA(cudaStreamSynchronize(s));
+  return GMT_OK;
+}

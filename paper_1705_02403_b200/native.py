@@ -79,6 +79,10 @@ SIGNATURES = [
     ("gmt_fmt_plan", C.c_int, [_vp, _vp, C.c_int32, _P(abi.PlanOut)]),
     ("gmt_dijkstra_oracle", C.c_int, [_vp, _vp, C.c_int32, _P(abi.PlanOut)]),
     ("gmt_batch_create", C.c_int, [_vp, C.c_int32, _P(_vp), _i32p, C.c_double, _P(_vp)]),
+    ("gmt_batch_create_problems", C.c_int, [_vp, _P(abi.Problem), C.c_int32, _i32p, _P(_vp)]),
+    ("gmt_ctx_pool_info", C.c_int, [_vp, _i32p, _i64p, _dp]),
+    ("gmt_batch_graph", C.c_int, [_vp, _vp, C.c_int32, _i32p, _i64p, _i64p, _dp, _i64p, _i32p, _dp, _dp,
+                                  _i64p, _i32p]),
     ("gmt_batch_launch", C.c_int, [_vp, _vp]),
     ("gmt_batch_summaries", C.c_int, [_vp, _vp, _P(abi.PlanSummary)]),
     ("gmt_batch_result", C.c_int, [_vp, _vp, C.c_int32, _P(abi.PlanOut)]),
@@ -203,7 +207,32 @@ class Batch:
         check(lib().gmt_batch_summaries(self.ctx.h, self.h, out))
         return list(out)
 
+    def graph(self, q: int) -> dict:
+        """Query q's graph (gmt_batch_graph): coords, in-rows with costs and
+        durations, out-row targets, as host arrays."""
+        n, ni, no = C.c_int32(), C.c_int64(), C.c_int64()
+        z = lambda t: abi.ptr(None, t)  # noqa: E731
+        check(lib().gmt_batch_graph(self.ctx.h, self.h, q, C.byref(n), C.byref(ni), C.byref(no), z(C.c_double),
+                                    z(C.c_int64), z(C.c_int32), z(C.c_double), z(C.c_double), z(C.c_int64),
+                                    z(C.c_int32)))
+        V = n.value
+        g = dict(n=V, in_ptr=np.zeros(V + 1, np.int64), in_col=np.zeros(max(ni.value, 1), np.int32),
+                 in_cost=np.zeros(max(ni.value, 1)), in_tau=np.zeros(max(ni.value, 1)),
+                 out_ptr=np.zeros(V + 1, np.int64), out_col=np.zeros(max(no.value, 1), np.int32))
+        coords = np.zeros(V * 16)
+        check(lib().gmt_batch_graph(self.ctx.h, self.h, q, C.byref(n), C.byref(ni), C.byref(no),
+                                    abi.ptr(coords, C.c_double), abi.ptr(g["in_ptr"], C.c_int64),
+                                    abi.ptr(g["in_col"], C.c_int32), abi.ptr(g["in_cost"], C.c_double),
+                                    abi.ptr(g["in_tau"], C.c_double), abi.ptr(g["out_ptr"], C.c_int64),
+                                    abi.ptr(g["out_col"], C.c_int32)))
+        for k, m in (("in_col", ni.value), ("in_cost", ni.value), ("in_tau", ni.value), ("out_col", no.value)):
+            g[k] = g[k][:m]
+        g["coords"] = coords
+        return g
+
     def result(self, q: int) -> abi.PlanResultPy:
+        if self.sizes[q] is None:
+            self.sizes[q] = self.graph(q)["n"]
         buf = abi.PlanBuffers(self.sizes[q])
         check(lib().gmt_batch_result(self.ctx.h, self.h, q, C.byref(buf.out)))
         return buf.result()
@@ -443,8 +472,9 @@ class Context:
         return buf.result()
 
     def plan_problems(self, specs, path_cap: int = 0):
-        """build_instance + gmt_plan for a batch of Euclidean problems (one
-        batched offline phase, one batched solve).  `specs`: ProblemSpecs or
+        """build_instance + gmt_plan for a batch of Euclidean problems, or of
+        double-integrator problems over the shared sample pool (one batched
+        offline phase, one batched solve).  `specs`: ProblemSpecs or
         a ProblemBatch (flattened once, reusable).  -> (status codes,
         summaries, path states [count, path_cap, dim] or None)."""
         pb = specs if isinstance(specs, ProblemBatch) else ProblemBatch(specs)
@@ -458,6 +488,26 @@ class Context:
                                       abi.ptr(paths, C.c_double)))
         return status, list(summ), (paths[: count * path_cap * d].reshape(count, path_cap, d)
                                     if paths is not None else None)
+
+    def batch_problems(self, specs):
+        """gmt_batch_create_problems: every problem's instance derived on the
+        device (double-integrator problems from the shared Halton pool) into
+        one solvable batch.  -> (Batch, status codes); the batch's query k is
+        the k-th problem whose status is 0."""
+        pb = specs if isinstance(specs, ProblemBatch) else ProblemBatch(specs)
+        status = np.zeros(pb.count, np.int32)
+        h = C.c_void_p()
+        check(lib().gmt_batch_create_problems(self.h, pb.array, pb.count, abi.ptr(status, C.c_int32), C.byref(h)))
+        ok = int((status == 0).sum())
+        b = Batch(self, h, ok, [None] * ok)
+        b._problems = pb
+        return b, status
+
+    def pool_info(self) -> dict:
+        """The context's shared sample pool: points, edges, last build ms."""
+        k, e, ms = C.c_int32(), C.c_int64(), C.c_double()
+        check(lib().gmt_ctx_pool_info(self.h, C.byref(k), C.byref(e), C.byref(ms)))
+        return {"pool_size": k.value, "edges": e.value, "build_ms": ms.value}
 
     def run_trial(self, scenario, seed: int, path_cap: int = 100000):
         """run_trial (simulator.cpp:66-176) -> (TrialOutcome, path_travelled [k, dim])."""
