@@ -475,9 +475,13 @@ int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const* insts,
  * successful problems in order).  The batch owns the derived instances.   */
 int gmt_batch_create_problems(gmt_ctx* ctx, const gmt_problem* problems, int32_t count,
                               int32_t* status_out, gmt_batch** out);
-/* The context's shared sample pool: points K, pool graph edges, and the
- * wall time its last (re)build took (0 / 0 / 0 before first use).       */
-int gmt_ctx_pool_info(gmt_ctx* ctx, int32_t* pool_size, int64_t* num_edges, double* build_ms);
+/* The context's shared sample pool: points K its graph covers, pool graph
+ * edges, the wall time its last (re)build took, how many queries of the last
+ * call took the single builder, and (GMT_POOL_TIMING=1) the last call's
+ * device stage times in ms (stage_ms[8]: upload, free flags, select, subst +
+ * init, special rows, layout, rows, descriptors).  Any pointer may be NULL. */
+int gmt_ctx_pool_info(gmt_ctx* ctx, int32_t* pool_size, int64_t* num_edges, double* build_ms,
+                      int32_t* last_fallbacks, double* stage_ms);
 /* Graph of batch query q as compressed rows (in-rows with costs and
  * durations, out-row targets).  Two-call pattern: NULL in_ptr returns *n,
  * *num_in and *num_out; then coords[n*dim] (may be NULL), in_ptr[n+1],

@@ -481,6 +481,27 @@ class RefLib(_Lib):
                                                   abi.ptr(cost, C.c_double)))
         return ptr, col[:E], cost[:E]
 
+    def di_pool(self, start_index: int, K: int, di, radius: float, threads: int):
+        """Shared-pool rows of the double integrator (the oracle's C statement
+        of the model) for the reference arm's DI instances."""
+        f = self.lib.ref_di_pool_create
+        f.restype = C.c_void_p
+        f.argtypes = [C.c_uint64, C.c_int32, _P(abi.DiParams), C.c_double, C.c_int32]
+        h = f(start_index, K, C.byref(di), radius, threads)
+        return DiPoolRef(self, h)
+
+    def di_instances(self, pool: "DiPoolRef", specs, threads: int):
+        """Reference instances of DI problems: the reference's own sample_free
+        and append_init, the DI graph from the pool rows + direct rows of the
+        non-pool vertices, every edge's waypoint polyline cached."""
+        arr = (abi.Problem * len(specs))(*[s.flat() for s in specs])
+        hs = (C.c_void_p * len(specs))()
+        f = self.lib.ref_di_pool_instances
+        f.restype = C.c_int
+        f.argtypes = [C.c_void_p, _P(abi.Problem), C.c_int32, C.c_int32, _P(C.c_void_p)]
+        self._check(f(pool.h, arr, len(specs), threads, hs))
+        return [RefInstance(self, C.c_void_p(h)) for h in hs]
+
     def instance_build_many(self, specs, threads: int):
         arr = (abi.Problem * len(specs))(*[s.flat() for s in specs])
         hs = (C.c_void_p * len(specs))()
@@ -549,6 +570,20 @@ class RefLib(_Lib):
                     init=init, n=n.value, lam=lam.value, eta=eta.value,
                     radius_override=ro.value or None, sampling_kind=kind.value,
                     start_index=si.value, seed=seed.value, key=key.value, steering=sk.value)
+
+
+class DiPoolRef:
+    def __init__(self, lib: "RefLib", h):
+        self.lib, self.h = lib, h
+
+    def __del__(self):
+        try:
+            f = self.lib.lib.ref_di_pool_destroy
+            f.restype = None
+            f.argtypes = [C.c_void_p]
+            f(self.h)
+        except Exception:
+            pass
 
 
 class RefRng:

@@ -10,6 +10,8 @@
 // reference function named in its comment, and converts the result back.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
+#include <stdexcept>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -741,3 +743,183 @@ extern "C" int ref_struct_sizes(int64_t* out, int32_t count) {
   for (int32_t i = 0; i < count && i < n; ++i) out[i] = sizes[i];
   return n;
 }
+
+// ---- double-integrator instances for bench.py's reference arm -------------
+// The reference has no double integrator, so a DI instance for
+// the UNMODIFIED reference planner is assembled here from (i) the reference's
+// own sample_free + append_init (sampling.cpp:81-154), (ii) the oracle's C
+// statement of the model (gmt_oracle.c: oracle_di_cost / oracle_di_coord,
+// linked in) for edge costs, durations and the cached waypoint polylines the
+// reference's motion_free checks (planner.cpp:54-60), and (iii) the shared
+// Halton pool of SURVEY.md §8(e): the pool rows are evaluated once, each
+// query's rows are the pool rows of its samples re-indexed by rank, plus the
+// rows of its non-pool vertices (a substituted goal, the init) evaluated
+// directly.  Test/bench infrastructure only.
+extern "C" double oracle_di_cost(const double* x0, const double* x1, double vmax, double w, double* tau);
+extern "C" double oracle_di_coord(const double* x0, const double* x1, double tau, int k, int i, int M,
+                                  double vmax);
+
+namespace {
+
+struct DiPoolRef {
+  int K = 0;
+  gmt_di_params di{};
+  double radius = 0.0;
+  double bound = 0.0;
+  std::vector<double> pts;                 // K x 6
+  std::vector<std::vector<int>> col;       // pool out-rows, targets ascending
+  std::vector<std::vector<double>> cost;
+  std::vector<std::vector<double>> tau;
+};
+
+bool di_may_ref(const double* a, const double* b, double bound) {
+  for (int k = 0; k < 3; ++k) {
+    const double D = b[k] - a[k];
+    if (D > bound || -D > bound) return false;
+  }
+  return true;
+}
+
+// cost(a -> b) <= r with the exact-safe |dp| prefilter; the edge's cost/duration.
+bool di_edge(const DiPoolRef& P, const double* a, const double* b, double* c, double* t) {
+  if (!di_may_ref(a, b, P.bound)) return false;
+  *c = oracle_di_cost(a, b, P.di.vmax, P.di.weight, t);
+  return *c <= P.radius;
+}
+
+}  // namespace
+
+extern "C" {
+
+void* ref_di_pool_create(uint64_t start_index, int32_t K, const gmt_di_params* di, double radius, int32_t threads) {
+  auto* P = new DiPoolRef;
+  P->K = K;
+  P->di = *di;
+  P->radius = radius;
+  P->bound = (di->vmax * radius + radius * radius / (2.0 * std::sqrt(3.0 * di->weight))) * (1.0 + 1e-9) + 1e-12;
+  P->pts.resize(static_cast<size_t>(K) * 6);
+  for (int p = 0; p < K; ++p) {
+    const std::vector<double> h = halton_point(start_index + static_cast<uint64_t>(p), 6);  // sampling.cpp:46-51
+    std::copy(h.begin(), h.end(), P->pts.begin() + static_cast<size_t>(p) * 6);
+  }
+  P->col.resize(K);
+  P->cost.resize(K);
+  P->tau.resize(K);
+  parallel_chunks(threads, static_cast<std::size_t>(K), [&](std::size_t b, std::size_t e) {
+    for (std::size_t u = b; u < e; ++u) {
+      const double* a = P->pts.data() + u * 6;
+      for (int v = 0; v < K; ++v) {
+        if (v == static_cast<int>(u)) continue;
+        double c, t;
+        if (di_edge(*P, a, P->pts.data() + static_cast<size_t>(v) * 6, &c, &t)) {
+          P->col[u].push_back(v);
+          P->cost[u].push_back(c);
+          P->tau[u].push_back(t);
+        }
+      }
+    }
+  });
+  return P;
+}
+
+void ref_di_pool_destroy(void* h) { delete static_cast<DiPoolRef*>(h); }
+
+int ref_di_pool_instances(void* pool, const gmt_problem* problems, int32_t count, int32_t threads, void** out) {
+  return guard([&] {
+    const DiPoolRef& P = *static_cast<const DiPoolRef*>(pool);
+    const int M = P.di.segments;
+    std::vector<std::string> errs(count);
+    parallel_chunks(threads, static_cast<std::size_t>(count), [&](std::size_t b, std::size_t e) {
+      for (std::size_t q = b; q < e; ++q) {
+        auto* ri = new RefInstance;
+        out[q] = nullptr;
+        try {
+          ri->problem = to_problem(&problems[q]);
+          const ProblemFile& pf = ri->problem;
+          SampleSet s = sample_free(pf.n, pf.obstacles, pf.goal, pf.sampling);  // the reference's own
+          const int init = append_init(s, pf.init, pf.goal);
+          const int V = static_cast<int>(s.states.size());
+          // samples that are pool points: the free pool points in stream order
+          std::vector<int> pid(V, -1), rank(P.K, -1);
+          int j = 0;
+          for (int p = 0; p < P.K && j < pf.n; ++p) {
+            std::vector<double> x(P.pts.begin() + static_cast<size_t>(p) * 6, P.pts.begin() + static_cast<size_t>(p + 1) * 6);
+            if (!point_free(x, pf.obstacles)) continue;
+            if (s.states[j].coords == x) {
+              pid[j] = p;
+              rank[p] = j;
+            }
+            ++j;
+          }
+          if (j < pf.n - 1) throw std::runtime_error("reference DI pool too small for the query");
+          std::vector<int> special;
+          for (int v = 0; v < V; ++v)
+            if (pid[v] < 0) special.push_back(v);
+          NeighborGraph g;
+          g.n = V;
+          g.radius = P.radius;
+          g.model.kind = SteeringModel::Kind::dubins_airplane;  // directed (planner.cpp:278)
+          g.out.resize(V);
+          g.in.resize(V);
+          std::vector<std::vector<double>> otau(V);
+          auto X = [&](int v) { return s.states[v].coords.data(); };
+          for (int u = 0; u < V; ++u) {
+            if (pid[u] >= 0) {
+              const int p = pid[u];
+              for (size_t k = 0; k < P.col[p].size(); ++k) {
+                const int r = rank[P.col[p][k]];
+                if (r < 0) continue;
+                g.out[u].push_back({r, P.cost[p][k], -1});
+                otau[u].push_back(P.tau[p][k]);
+              }
+              for (int sv : special) {  // the largest indices: appended in order
+                double c, t;
+                if (sv != u && di_edge(P, X(u), X(sv), &c, &t)) {
+                  g.out[u].push_back({sv, c, -1});
+                  otau[u].push_back(t);
+                }
+              }
+            } else {
+              for (int v = 0; v < V; ++v) {
+                double c, t;
+                if (v != u && di_edge(P, X(u), X(v), &c, &t)) {
+                  g.out[u].push_back({v, c, -1});
+                  otau[u].push_back(t);
+                }
+              }
+            }
+          }
+          // path ids in (source, position) order; in-lists by ascending source
+          // (graph.cpp:172-186), sharing the out-edge's path
+          int pidx = 0;
+          for (int u = 0; u < V; ++u) {
+            for (size_t k = 0; k < g.out[u].size(); ++k) {
+              auto& ed = g.out[u][k];
+              ed.path_id = pidx++;
+              std::vector<State> path(M + 1);
+              for (int w = 0; w <= M; ++w) {
+                path[w].coords.resize(6);
+                for (int i = 0; i < 6; ++i)
+                  path[w].coords[i] = oracle_di_coord(X(u), X(ed.other), otau[u][k], w, i, M, P.di.vmax);
+              }
+              g.paths.push_back(std::move(path));
+              g.in[ed.other].push_back({u, ed.cost, ed.path_id});
+            }
+          }
+          ri->inst.samples = std::move(s);
+          ri->inst.init_index = init;
+          ri->inst.radius = P.radius;
+          ri->inst.graph = std::move(g);
+          out[q] = ri;
+        } catch (const std::exception& ex) {
+          delete ri;
+          errs[q] = ex.what();
+        }
+      }
+    });
+    for (int32_t q = 0; q < count; ++q)
+      if (!out[q]) throw std::runtime_error("query " + std::to_string(q) + ": " + errs[q]);
+  });
+}
+
+}  // extern "C"

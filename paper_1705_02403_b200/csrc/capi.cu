@@ -184,6 +184,8 @@ extern "C" void gmt_ctx_destroy(gmt_ctx* ctx) {
     ctx->jobs.release();
     ctx->pp_work.release();
     ctx->pool_work.release();
+    ctx->pool_rows.release();
+    ctx->pool_res.release();
     destroy_pool(ctx->pool);
     ctx->pool = nullptr;
     ctx->plan_inst.mem.release();
@@ -779,14 +781,16 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
   b->dim = insts[0]->desc.dim;
   for (int q = 1; q < count; ++q)
     if (insts[q]->desc.dim != b->dim) b->dim = 0;
-  // Auto shape (batch cluster 0): double-integrator queries (eight polyline
-  // segments per lazy check) run on 2-CTA clusters of wide CTAs, the rest on
-  // single narrow CTAs -- the measured optimum (profiles/r01/sweep_*.txt).
+  // Auto shape (batch cluster 0): a few kinodynamic queries (eight polyline
+  // segments per lazy check) run on 2-CTA clusters of wide CTAs; Euclidean
+  // queries on single narrow CTAs, kinodynamic batches that fill the SMs
+  // several times over on single wide CTAs (4096 DI queries: 58 ms vs 66 ms
+  // on 2-CTA clusters, tools/di_sweep.py).
   b->cluster = ctx->batch_cluster;
   if (b->cluster == 0) {
     b->cluster = 1;
     for (int q = 0; q < count; ++q)
-      if (insts[q]->desc.steering != GMT_STEER_EUCLIDEAN) b->cluster = 2;
+      if (insts[q]->desc.steering != GMT_STEER_EUCLIDEAN && count < 4 * ctx->sm_count) b->cluster = 2;
   }
   int rc = plan_smem(ctx, max_n, max_d, max_nb, b->cluster, &b->smem, &b->obs);
   if (rc == GMT_OK)
@@ -806,7 +810,9 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
     j.lambda = lambda;
     j.radius = insts[q]->desc.radius;
   }
-  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
+  bool kino = false;
+  for (int q = 0; q < count; ++q) kino = kino || insts[q]->desc.steering != GMT_STEER_EUCLIDEAN;
+  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 || kino ? 512 : 256);
   rc = b->jobs_mem.reserve(sizeof(SolveJob) * count);
   if (rc == GMT_OK) {
     // jobs_mem comes from the stream-ordered pool of ctx->stream: write it on

@@ -194,6 +194,43 @@ GMT_HD double di_cost_tau(const double* x0, const double* x1, const DiParams& P,
       T, [&](double t) { return di_g(c, t); }, [&](double t) { return di_c(c, t); }, cap, tau_out);
 }
 
+// Exact-safe rejection test for graph construction: true only if
+// cost(x0 -> x1) > r is certain, so skipping the duration search of such a
+// pair never changes a graph (kept pairs still run di_cost_tau unchanged).
+// c(tau) - r = P(tau) / tau^3 with the quartic
+//   P(tau) = tau^3 (tau - r) + Q(tau),  Q(tau) = a tau^2 + b tau + c0,
+// and c(tau) > tau > r for tau > r, so the pair is rejected when P > 0 on
+// (0, r].  On each of kDiRejectParts sub-intervals [l, h] the two parts are
+// bounded from below separately: tau^3 (tau - r) falls on (0, 3r/4] and
+// rises after it; Q's minimum is at an end point or its vertex.  The bound
+// must clear a margin far above the rounding of its own evaluation and of the
+// search's c(tau) (|P| terms are O(10), errors O(1e-14)): a pair whose true
+// minimum is within that margin of r is left to the search.
+constexpr int kDiRejectParts = 12;
+GMT_HD bool di_cost_exceeds(const DiCoef& c, double r) {
+  const double scale = r * r * r * r + c.a * r * r + (c.b < 0.0 ? -c.b : c.b) * r + c.c0 + 1.0;
+  const double margin = 1e-9 * scale;
+  const double tm = 0.75 * r;                 // argmin of tau^3 (tau - r)
+  const double tv = c.a > 0.0 ? -c.b / (2.0 * c.a) : -1.0;  // vertex of Q (a > 0: convex)
+  double h = r;
+  for (int i = 0; i < kDiRejectParts; ++i) {
+    const double l = i + 1 == kDiRejectParts ? 0.0 : r * static_cast<double>(kDiRejectParts - 1 - i) / kDiRejectParts;
+    // lower bound of tau^3 (tau - r) on [l, h]
+    const double t = h <= tm ? h : (l >= tm ? l : tm);
+    const double g = t * t * t * (t - r);
+    // lower bound of Q on [l, h]
+    const double ql = (c.a * l + c.b) * l + c.c0, qh = (c.a * h + c.b) * h + c.c0;
+    double q = ql < qh ? ql : qh;
+    if (tv > l && tv < h) {
+      const double qv = (c.a * tv + c.b) * tv + c.c0;
+      q = qv < q ? qv : q;
+    }
+    if (!(g + q > margin)) return false;
+    h = l;
+  }
+  return true;
+}
+
 // State at time t on the optimal trajectory x0 -> x1 of duration tau
 // (normalised coordinates).  Callers pass the exact endpoints for t = 0, tau.
 GMT_HD void di_state_at(const double* x0, const double* x1, double tau, double t,

@@ -48,11 +48,19 @@ __device__ __forceinline__ bool di_may_connect(const double* x0, const double* x
   return true;
 }
 
+// The |dp| test, then the quartic lower bound of di_cost_exceeds (di.cuh).
+__device__ __forceinline__ bool di_may_connect(const double* x0, const double* x1, double bound,
+                                               const DiParams& P, double r) {
+  if (!di_may_connect(x0, x1, bound)) return false;
+  return !di_cost_exceeds(di_coef(x0, x1, P), r);
+}
+
 struct DiModel {
   static constexpr int kDim = kDiDim;
   DiParams P;
   double bound;  // di_prefilter_bound
-  __device__ bool may(const double* a, const double* b) const { return di_may_connect(a, b, bound); }
+  double radius;
+  __device__ bool may(const double* a, const double* b) const { return di_may_connect(a, b, bound, P, radius); }
   __device__ double cost_tau(const double* a, const double* b, double* t) const {
     return di_cost_tau(a, b, P, t);
   }
@@ -563,6 +571,7 @@ DiModel di_model(const gmt_di_params* p, double radius) {
   DiModel m;
   m.P = to_di(p);
   m.bound = di_prefilter_bound(m.P, radius);
+  m.radius = radius;
   return m;
 }
 

@@ -113,6 +113,8 @@ struct gmt_ctx {
   gmtb::Arena jobs;       // SolveJob table
   gmtb::Arena pp_work;    // gmt_plan_problems: the batched offline phase's scratch + padded rows
   gmtb::Arena pool_work;  // gmt_plan_problems over the shared pool: derived instances + scratch
+  gmtb::Arena pool_rows;  //   ... their row regions
+  gmtb::Arena pool_res;   //   ... their results
   gmtb::SamplePool* pool = nullptr;  // shared Halton pool + its graph (built on first use, reused)
   gmtb::HostPinned pinned;
   gmtb::HostPinned pinned2;
@@ -126,6 +128,7 @@ struct gmt_batch {
   gmtb::Arena res;
   gmtb::Arena jobs_mem;
   gmtb::Arena derived;                 // shared-pool batches: the derived per-query instances
+  gmtb::Arena derived_rows;            //   ... their row regions
   std::vector<gmt_instance*> owned;    // shared-pool batches: queries built one by one (rare paths)
   std::vector<gmtb::SolveJob> jobs;
   std::vector<gmtb::DevResult> results;
@@ -140,6 +143,7 @@ struct gmt_batch {
     res.release();
     jobs_mem.release();
     derived.release();
+    derived_rows.release();
     for (gmt_instance* i : owned) delete i;
   }
 };

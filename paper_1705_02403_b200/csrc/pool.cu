@@ -12,23 +12,27 @@
 // Both are the largest indices, so they end every sorted out- and in-row
 // (graph.cpp:163-166, 184-186) they appear in.
 //
-// The pool (K Halton points + its directed graph, built once by the same
-// kinodynamic builder as every single instance) lives in the context and is
-// reused across calls.  Per call, for Q queries:
-//   pool_free_kernel     free flag of every (query, pool point)        Q x K
-//   pool_select_kernel   rank of every free point, the first n kept    Q blocks
-//   pool_subst_kernel    goal substitution (the reference's search)    Q blocks
-//   pool_init_kernel     append_init (exact-duplicate check)           Q blocks
-//   pool_special_kernel  out-/in-rows of the substituted goal and init  4 warps / query
+// The pool (Halton points + the directed graph over the first K of them,
+// built by the same kinodynamic builder as every single instance) lives in
+// the context and is reused across calls; K is the largest "cutoff" (the
+// stream position of a query's n-th free point) seen so far.  Per call, for
+// Q queries:
+//   pool_free_kernel     free flag of every (query, candidate point)    Q x Kc
+//   pool_select_kernel   rank of every free point, the first n kept     block / query
+//   (host: the pool graph covers every cutoff, else it is regrown)
+//   pool_subst_kernel    goal substitution (the reference's search)     block / query
+//   pool_init_kernel     append_init (exact-duplicate check)            block / query
+//   pool_special_kernel  out-/in-rows of the substituted goal and init   4 warps / query
+//   pool_layout_kernel   row capacities (pool degree + 2) -> row starts  block / query
+//   (host: row regions sized from the per-query totals)
 //   pool_rows_kernel     every derived row: the pool row filtered by
-//                        rank (ballot compaction) + the special entries warp / row
+//                        rank (ballot compaction) + the special entries  warp / row
 //   pool_desc_kernel     the DevInstance of every query
-// Rows are padded: node x with pool point p starts at pool_ptr[p] + 2x of its
-// query's region (the two special entries fit behind the pool row), so no
-// scan is needed; DevInstance::in_end / out_end carry the row ends.  The
-// derived instances are bit-identical to gmt_instance_build of each problem
-// (tests/test_gpu_pool.py); queries off the fast path (pool too short, an
-// exact init duplicate, a long substitution search) take gmt_instance_build.
+// Rows are padded by the two special entries each; DevInstance::in_end /
+// out_end carry the row ends.  The derived instances are bit-identical to
+// gmt_instance_build of each problem (tests/test_gpu_pool.py); queries off
+// the fast path (an exact init duplicate, a long substitution search, a
+// special row above kSpecCap) take gmt_instance_build.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -53,19 +57,22 @@ int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, b
                   std::vector<DevResult>& out, ResultScalars** scalars_base, int64_t* counters);
 
 struct SamplePool {
-  int K = 0;
   uint64_t start_index = 1;
   gmt_di_params gp{};
   double radius = 0.0;
-  Arena coords;
+  int Kp = 0;        // Halton points generated (candidates)
+  Arena pts;         // Kp x 6
+  int K = 0;         // the pool graph covers points [0, K)
   Arena out_mem, in_mem;
   DiRows out, in;
-  double build_ms = 0.0;
+  double build_ms = 0.0;      // last graph (re)build
+  int last_fallbacks = 0;     // queries of the last call that took the single builder
+  double stage_ms[8] = {};    // last call's stage times (GMT_POOL_TIMING=1)
 };
 
 void destroy_pool(SamplePool* p) {
   if (!p) return;
-  p->coords.release();
+  p->pts.release();
   p->out_mem.release();
   p->in_mem.release();
   delete p;
@@ -108,16 +115,17 @@ struct PQ {
   int32_t reserved;
   int64_t box_off;   // first box (rows of kD doubles)
   int64_t node_off;  // first node entry (n + 1 reserved)
-  int64_t slot_off;  // first slot of the query's row regions
+  int64_t in_off;    // first slot of the query's in-row region
+  int64_t out_off;   // first slot of the query's out-row region
 };
 struct PQOut {
   int32_t fallback;
   int32_t subst;
-  int32_t V;
-  int32_t init_index;
   int32_t goal_any;
+  int32_t cutoff;       // stream position after the query's n-th free point
   int32_t spec_len[4];  // out(g), in(g), out(init), in(init)
-  int32_t reserved;
+  int64_t tot_in;       // row-region sizes (layout)
+  int64_t tot_out;
 };
 
 __device__ __forceinline__ bool free_pt(const double* p, const double* lo, const double* hi, int nb) {
@@ -127,15 +135,15 @@ __device__ __forceinline__ bool free_pt(const double* p, const double* lo, const
   return true;
 }
 
-// halton_point(start + p, 6) (sampling.cpp:46-51) for every pool point.
-__global__ void pool_points_kernel(int K, uint64_t start, Primes pr, double* __restrict__ out) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K * kD; i += gridDim.x * blockDim.x) {
+// halton_point(start + p, 6) (sampling.cpp:46-51) for p in [from, to).
+__global__ void pool_points_kernel(int from, int to, uint64_t start, Primes pr, double* __restrict__ out) {
+  for (int i = from * kD + blockIdx.x * blockDim.x + threadIdx.x; i < to * kD; i += gridDim.x * blockDim.x) {
     const int p = i / kD, k = i - p * kD;
     out[i] = halton_dev(start + static_cast<uint64_t>(p), pr.p[k]);
   }
 }
 
-// flags[q][p] = point_free(pool point p, boxes of q); the query's boxes are
+// flags[q][p] = point_free(candidate p, boxes of q); the query's boxes are
 // staged in shared memory when they fit.
 __global__ void __launch_bounds__(256) pool_free_kernel(const PQ* __restrict__ pq, const double* __restrict__ P,
                                                         int K, const double* __restrict__ box_lo,
@@ -164,7 +172,7 @@ __global__ void __launch_bounds__(256) pool_free_kernel(const PQ* __restrict__ p
   flags[static_cast<int64_t>(q) * K + p] = free_pt(x, lo, hi, Q.nb) ? 1 : 0;
 }
 
-// The first n free pool points in stream order are the query's samples
+// The first n free candidates in stream order are the query's samples
 // 0..n-1 (sample_free's loop, sampling.cpp:97-108): ranks by a block scan.
 __global__ void __launch_bounds__(1024) pool_select_kernel(const PQ* __restrict__ pq, const double* __restrict__ P,
                                                            int K, const uint8_t* __restrict__ flags,
@@ -216,10 +224,9 @@ __global__ void __launch_bounds__(1024) pool_select_kernel(const PQ* __restrict_
   const int any = __syncthreads_or(in_goal ? 1 : 0);
   if (tid == 0) {
     PQOut o{};
-    o.fallback = carry_s < Q.n ? 1 : 0;  // the pool holds fewer than n free points
+    o.fallback = carry_s < Q.n ? 1 : 0;  // fewer than n free candidates (the host widens them)
     o.goal_any = any;
-    o.V = Q.n + 1;
-    o.init_index = Q.n;
+    o.cutoff = carry_s < Q.n ? K + 1 : sel[Q.node_off + Q.n - 1] + 1;
     out[q] = o;
   }
 }
@@ -359,6 +366,7 @@ __global__ void __launch_bounds__(128) pool_special_kernel(const PQ* __restrict_
         const double D = to[k] - from[k];
         if (D > bound || -D > bound) may = false;
       }
+      if (may) may = !di_cost_exceeds(di_coef(from, to, P), radius);
       if (may) {
         c = di_cost_tau(from, to, P, &t, radius);
         keep = c <= radius;
@@ -379,6 +387,85 @@ __global__ void __launch_bounds__(128) pool_special_kernel(const PQ* __restrict_
   }
 }
 
+// Row starts (relative to the query's regions): vertex x < n owns its pool
+// point's degree + 2 slots (room for the two special entries), in rank
+// order; the special rows follow (kSpecCap slots each).  A substituted
+// vertex n-1 keeps its dropped pool point's (unused) slots.
+__global__ void __launch_bounds__(1024) pool_layout_kernel(const PQ* __restrict__ pq, const int64_t* __restrict__ pin_ptr,
+                                                           const int64_t* __restrict__ pout_ptr,
+                                                           const int32_t* __restrict__ sel, int64_t* __restrict__ in_start,
+                                                           int64_t* __restrict__ out_start, PQOut* __restrict__ out) {
+  __shared__ int64_t ws_in[32], ws_out[32];
+  __shared__ int64_t carry_in, carry_out;
+  const int q = blockIdx.x;
+  const PQ Q = pq[q];
+  if (Q.skip || out[q].fallback) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) {
+    carry_in = 0;
+    carry_out = 0;
+  }
+  __syncthreads();
+  for (int base = 0; base < Q.n; base += blockDim.x) {
+    const int x = base + tid;
+    int64_t ci = 0, co = 0;
+    if (x < Q.n) {
+      const int p = sel[Q.node_off + x];
+      ci = pin_ptr[p + 1] - pin_ptr[p] + 2;
+      co = pout_ptr[p + 1] - pout_ptr[p] + 2;
+    }
+    int64_t si = ci, so = co;  // inclusive warp scans
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t a = __shfl_up_sync(kFull, si, o), b = __shfl_up_sync(kFull, so, o);
+      if (lane >= o) {
+        si += a;
+        so += b;
+      }
+    }
+    if (lane == 31) {
+      ws_in[warp] = si;
+      ws_out[warp] = so;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int64_t a = lane < nw ? ws_in[lane] : 0, b = lane < nw ? ws_out[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t ya = __shfl_up_sync(kFull, a, o), yb = __shfl_up_sync(kFull, b, o);
+        if (lane >= o) {
+          a += ya;
+          b += yb;
+        }
+      }
+      ws_in[lane] = a;
+      ws_out[lane] = b;
+    }
+    __syncthreads();
+    const int64_t bi = carry_in + (warp > 0 ? ws_in[warp - 1] : 0) + si - ci;
+    const int64_t bo = carry_out + (warp > 0 ? ws_out[warp - 1] : 0) + so - co;
+    if (x < Q.n) {
+      in_start[Q.node_off + x] = bi;
+      out_start[Q.node_off + x] = bo;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      carry_in += ws_in[nw - 1];
+      carry_out += ws_out[nw - 1];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const PQOut& o = out[q];
+    if (o.subst) {
+      in_start[Q.node_off + Q.n - 1] = carry_in;
+      out_start[Q.node_off + Q.n - 1] = carry_out;
+    }
+    in_start[Q.node_off + Q.n] = carry_in + kSpecCap;
+    out_start[Q.node_off + Q.n] = carry_out + kSpecCap;
+    out[q].tot_in = carry_in + 2 * kSpecCap;
+    out[q].tot_out = carry_out + 2 * kSpecCap;
+  }
+}
+
 __device__ __forceinline__ int find_sorted(const int32_t* a, int len, int x) {
   int lo = 0, hi = len;
   while (lo < hi) {
@@ -394,52 +481,49 @@ __device__ __forceinline__ int find_sorted(const int32_t* a, int len, int x) {
 // ranks, then the special vertices (n-1 before n) where the special rows hold
 // the edge.  A special vertex copies its own rows.
 __global__ void __launch_bounds__(256) pool_rows_kernel(
-    const PQ* __restrict__ pq, const PQOut* __restrict__ po, int K, int64_t Epool,
-    const int64_t* __restrict__ pin_ptr, const int32_t* __restrict__ pin_col, const double* __restrict__ pin_cost,
-    const double* __restrict__ pin_tau, const int64_t* __restrict__ pout_ptr, const int32_t* __restrict__ pout_col,
-    const uint16_t* __restrict__ rank_of, const int32_t* __restrict__ sel, const int32_t* __restrict__ scol,
-    const double* __restrict__ scost, const double* __restrict__ stau, int64_t* __restrict__ in_start,
-    int64_t* __restrict__ in_end, int64_t* __restrict__ out_start, int64_t* __restrict__ out_end,
-    int32_t* __restrict__ in_col, double* __restrict__ in_cost, double* __restrict__ in_tau,
-    int32_t* __restrict__ out_col) {
+    const PQ* __restrict__ pq, const PQOut* __restrict__ po, int Kc, const int64_t* __restrict__ pin_ptr,
+    const int32_t* __restrict__ pin_col, const double* __restrict__ pin_cost, const double* __restrict__ pin_tau,
+    const int64_t* __restrict__ pout_ptr, const int32_t* __restrict__ pout_col, const uint16_t* __restrict__ rank_of,
+    const int32_t* __restrict__ sel, const int32_t* __restrict__ scol, const double* __restrict__ scost,
+    const double* __restrict__ stau, const int64_t* __restrict__ in_start, int64_t* __restrict__ in_end,
+    const int64_t* __restrict__ out_start, int64_t* __restrict__ out_end, int32_t* __restrict__ in_col,
+    double* __restrict__ in_cost, double* __restrict__ in_tau, int32_t* __restrict__ out_col) {
   const int q = blockIdx.y;
   const PQ Q = pq[q];
   if (Q.skip) return;
-  const PQOut O = po[q];
+  const PQOut& O = po[q];
   if (O.fallback) return;
   const int lane = threadIdx.x & 31;
   const int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int n = Q.n;
   if (x > n) return;
-  const int64_t so = Q.slot_off;
+  int32_t* icol = in_col + Q.in_off;
+  double* icost = in_cost + Q.in_off;
+  double* itau = in_tau + Q.in_off;
+  int32_t* ocol = out_col + Q.out_off;
   const int64_t lb = static_cast<int64_t>(q) * 4 * kSpecCap;
   const bool subst = O.subst != 0;
-  const bool special = x == n || (subst && x == n - 1);
-  if (special) {
+  const int64_t is = in_start[Q.node_off + x], os = out_start[Q.node_off + x];
+  if (x == n || (subst && x == n - 1)) {
     const int l = x == n ? 2 : 0;
-    const int64_t s0 = Epool + 2 * static_cast<int64_t>(n + 1) + (x == n ? kSpecCap : 0);
     const int li = O.spec_len[l + 1], lo = O.spec_len[l];
     for (int j = lane; j < li; j += 32) {
-      in_col[so + s0 + j] = scol[lb + (l + 1) * kSpecCap + j];
-      in_cost[so + s0 + j] = scost[lb + (l + 1) * kSpecCap + j];
-      in_tau[so + s0 + j] = stau[lb + (l + 1) * kSpecCap + j];
+      icol[is + j] = scol[lb + (l + 1) * kSpecCap + j];
+      icost[is + j] = scost[lb + (l + 1) * kSpecCap + j];
+      itau[is + j] = stau[lb + (l + 1) * kSpecCap + j];
     }
-    for (int j = lane; j < lo; j += 32) out_col[so + s0 + j] = scol[lb + l * kSpecCap + j];
+    for (int j = lane; j < lo; j += 32) ocol[os + j] = scol[lb + l * kSpecCap + j];
     if (lane == 0) {
-      in_start[Q.node_off + x] = s0;
-      in_end[Q.node_off + x] = s0 + li;
-      out_start[Q.node_off + x] = s0;
-      out_end[Q.node_off + x] = s0 + lo;
+      in_end[Q.node_off + x] = is + li;
+      out_end[Q.node_off + x] = os + lo;
     }
     return;
   }
   const int p = sel[Q.node_off + x];
-  const uint16_t* rk = rank_of + static_cast<int64_t>(q) * K;
-  // in-row
-  {
+  const uint16_t* rk = rank_of + static_cast<int64_t>(q) * Kc;
+  {  // in-row
     const int64_t e0 = pin_ptr[p], e1 = pin_ptr[p + 1];
-    const int64_t s0 = e0 + 2 * static_cast<int64_t>(x);
-    int64_t w = s0;
+    int64_t w = is;
     for (int64_t b = e0; b < e1; b += 32) {
       const int64_t e = b + lane;
       uint16_t r = kNoRank;
@@ -447,10 +531,10 @@ __global__ void __launch_bounds__(256) pool_rows_kernel(
       const bool keep = r != kNoRank;
       const uint32_t m = __ballot_sync(kFull, keep);
       if (keep) {
-        const int64_t slot = so + w + __popc(m & ((1u << lane) - 1u));
-        in_col[slot] = r;
-        in_cost[slot] = pin_cost[e];
-        in_tau[slot] = pin_tau[e];
+        const int64_t slot = w + __popc(m & ((1u << lane) - 1u));
+        icol[slot] = r;
+        icost[slot] = pin_cost[e];
+        itau[slot] = pin_tau[e];
       }
       w += __popc(m);
     }
@@ -458,35 +542,31 @@ __global__ void __launch_bounds__(256) pool_rows_kernel(
       for (int l = subst ? 0 : 2; l <= 2; l += 2) {
         const int j = find_sorted(scol + lb + l * kSpecCap, O.spec_len[l], x);
         if (j >= 0) {
-          in_col[so + w] = l == 0 ? n - 1 : n;
-          in_cost[so + w] = scost[lb + l * kSpecCap + j];
-          in_tau[so + w] = stau[lb + l * kSpecCap + j];
+          icol[w] = l == 0 ? n - 1 : n;
+          icost[w] = scost[lb + l * kSpecCap + j];
+          itau[w] = stau[lb + l * kSpecCap + j];
           ++w;
         }
       }
-      in_start[Q.node_off + x] = s0;
       in_end[Q.node_off + x] = w;
     }
   }
-  // out-row
-  {
+  {  // out-row
     const int64_t e0 = pout_ptr[p], e1 = pout_ptr[p + 1];
-    const int64_t s0 = e0 + 2 * static_cast<int64_t>(x);
-    int64_t w = s0;
+    int64_t w = os;
     for (int64_t b = e0; b < e1; b += 32) {
       const int64_t e = b + lane;
       uint16_t r = kNoRank;
       if (e < e1) r = rk[pout_col[e]];
       const bool keep = r != kNoRank;
       const uint32_t m = __ballot_sync(kFull, keep);
-      if (keep) out_col[so + w + __popc(m & ((1u << lane) - 1u))] = r;
+      if (keep) ocol[w + __popc(m & ((1u << lane) - 1u))] = r;
       w += __popc(m);
     }
     if (lane == 0) {  // edges into the special vertices
       for (int l = subst ? 1 : 3; l <= 3; l += 2) {
-        if (find_sorted(scol + lb + l * kSpecCap, O.spec_len[l], x) >= 0) out_col[so + w++] = l == 1 ? n - 1 : n;
+        if (find_sorted(scol + lb + l * kSpecCap, O.spec_len[l], x) >= 0) ocol[w++] = l == 1 ? n - 1 : n;
       }
-      out_start[Q.node_off + x] = s0;
       out_end[Q.node_off + x] = w;
     }
   }
@@ -520,13 +600,13 @@ __global__ void pool_desc_kernel(const PQ* __restrict__ pq, const PQOut* __restr
   D.goal_hi = goal_hi + static_cast<int64_t>(q) * kD;
   D.out_ptr = out_start + Q.node_off;
   D.out_end = out_end + Q.node_off;
-  D.out_col = out_col + Q.slot_off;
+  D.out_col = out_col + Q.out_off;
   D.out_cost = nullptr;  // (the solve reads out-row targets only)
   D.in_ptr = in_start + Q.node_off;
   D.in_end = in_end + Q.node_off;
-  D.in_col = in_col + Q.slot_off;
-  D.in_cost = in_cost + Q.slot_off;
-  D.in_tau = in_tau + Q.slot_off;
+  D.in_col = in_col + Q.in_off;
+  D.in_cost = in_cost + Q.in_off;
+  D.in_tau = in_tau + Q.in_off;
   D.steering = GMT_STEER_DOUBLE_INTEGRATOR;
   D.kin_segments = P.segments;
   D.kin_p[0] = P.vmax;
@@ -560,9 +640,9 @@ bool pool_eligible(const gmt_problem& p, const gmt_problem& p0) {
          p.n >= 2 && p.n < static_cast<int>(kNoRank) && p.sampling.with_heading == 0;
 }
 
-// Pool points needed for a problem: n over the free-volume estimate (boxes
+// Candidates to scan for a problem: n over the free-volume estimate (boxes
 // clipped to the unit cube), +5 % + 256 (as gmt_plan_problems sizes its
-// candidates); a query that still runs short takes the single builder.
+// candidates); a query that runs short widens the scan.
 int pool_need(const gmt_problem& pr) {
   double blocked = 0.0;
   for (int b = 0; b < pr.scene.num_boxes; ++b) {
@@ -578,65 +658,97 @@ int pool_need(const gmt_problem& pr) {
   return static_cast<int>(std::ceil(std::min(4.0 * pr.n, pr.n / free_est * 1.05) + 256.0));
 }
 
-// The context's pool for problems like p0 with at least K points.
-int get_pool(gmt_ctx* ctx, const gmt_problem& p0, int K, SamplePool** out) {
-  SamplePool* cur = ctx->pool;
-  if (cur && cur->start_index == p0.sampling.start_index && cur->radius == p0.radius_override &&
-      same_params(cur->gp, p0.di) && cur->K >= K) {
-    *out = cur;
-    return GMT_OK;
+bool same_source(const SamplePool* p, const gmt_problem& p0) {
+  return p && p->start_index == p0.sampling.start_index && p->radius == p0.radius_override &&
+         same_params(p->gp, p0.di);
+}
+
+// The context's pool for problems like p0 with at least Kp candidate points.
+int pool_points(gmt_ctx* ctx, const gmt_problem& p0, int Kp, SamplePool** out) {
+  SamplePool* pool = ctx->pool;
+  if (!same_source(pool, p0)) {
+    destroy_pool(ctx->pool);
+    ctx->pool = pool = new SamplePool;
+    pool->start_index = p0.sampling.start_index;
+    pool->gp = p0.di;
+    pool->radius = p0.radius_override;
   }
-  const auto t0 = std::chrono::steady_clock::now();
-  if (cur && cur->start_index == p0.sampling.start_index && cur->radius == p0.radius_override &&
-      same_params(cur->gp, p0.di))
-    K = std::max(K, cur->K + cur->K / 4);  // grow geometrically
-  K = (K + 1023) & ~1023;
-  auto* pool = new SamplePool;
-  pool->K = K;
-  pool->start_index = p0.sampling.start_index;
-  pool->gp = p0.di;
-  pool->radius = p0.radius_override;
-  int rc = pool->coords.reserve(sizeof(double) * static_cast<size_t>(K) * kD);
-  if (rc) {
-    destroy_pool(pool);
-    return rc;
-  }
+  *out = pool;
+  if (pool->Kp >= Kp) return GMT_OK;
+  Kp = (std::max(Kp, pool->Kp + pool->Kp / 2) + 255) & ~255;
+  Arena fresh;
+  int rc = fresh.reserve(sizeof(double) * static_cast<size_t>(Kp) * kD);
+  if (rc) return rc;
+  if (pool->Kp)
+    GMT_CUDA(cudaMemcpyAsync(fresh.ptr, pool->pts.ptr, sizeof(double) * static_cast<size_t>(pool->Kp) * kD,
+                             cudaMemcpyDeviceToDevice, ctx->stream));
   Primes pr;
   for (int k = 0; k < kD; ++k) pr.p[k] = nth_prime_h(k + 1);
-  pool_points_kernel<<<std::min((K * kD + 255) / 256, 4096), 256, 0, ctx->stream>>>(
-      K, pool->start_index, pr, static_cast<double*>(pool->coords.ptr));
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    destroy_pool(pool);
-    return cuda_error(e, "pool points");
-  }
+  pool_points_kernel<<<std::min(((Kp - pool->Kp) * kD + 255) / 256, 4096), 256, 0, ctx->stream>>>(
+      pool->Kp, Kp, pool->start_index, pr, static_cast<double*>(fresh.ptr));
+  GMT_CUDA(cudaGetLastError());
   ++ctx->launches;
-  rc = build_di_graph_dev(ctx, static_cast<const double*>(pool->coords.ptr), K, &pool->gp, pool->radius,
-                          pool->out_mem, &pool->out, pool->in_mem, &pool->in);
-  if (rc) {
-    destroy_pool(pool);
-    return rc;
-  }
-  e = cudaStreamSynchronize(ctx->stream);
-  if (e != cudaSuccess) {
-    destroy_pool(pool);
-    return cuda_error(e, "pool graph");
-  }
-  pool->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  destroy_pool(ctx->pool);
-  ctx->pool = pool;
-  *out = pool;
+  pool->pts.release();
+  pool->pts = fresh;
+  fresh.ptr = nullptr;
+  fresh.cap = 0;
+  pool->Kp = Kp;
   return GMT_OK;
 }
 
+// The pool graph over at least the first K points (rebuilt when it is shorter).
+int pool_graph(gmt_ctx* ctx, SamplePool* pool, int K) {
+  if (pool->K >= K) return GMT_OK;
+  const auto t0 = std::chrono::steady_clock::now();
+  K = std::min(pool->Kp, (std::max(K, pool->K + pool->K / 8) + 255) & ~255);
+  pool->out_mem.release();
+  pool->in_mem.release();
+  pool->K = 0;
+  int rc = build_di_graph_dev(ctx, static_cast<const double*>(pool->pts.ptr), K, &pool->gp, pool->radius,
+                              pool->out_mem, &pool->out, pool->in_mem, &pool->in);
+  if (rc) return rc;
+  GMT_CUDA(cudaStreamSynchronize(ctx->stream));
+  pool->K = K;
+  pool->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return GMT_OK;
+}
+
+struct StageTimer {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::vector<cudaEvent_t> ev;
+  explicit StageTimer(cudaStream_t st) : s(st) {
+    const char* e = std::getenv("GMT_POOL_TIMING");
+    on = e && e[0] == '1';
+  }
+  void mark() {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+  }
+  void report(SamplePool* pool) {
+    if (!on) return;
+    cudaEventSynchronize(ev.back());
+    for (size_t i = 1; i < ev.size() && i <= 8; ++i) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      pool->stage_ms[i - 1] = ms;
+    }
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    ev.clear();
+  }
+};
+
 }  // namespace
 
-// Derive the instances of `count` problems into `arena` (device).  On return
-// inst[q] is the device descriptor of query q (a derived one, or one of the
-// single-built instances appended to `owned`; null when the query's own build
-// failed with status[q] = GMT_E_GOAL_BLOCKED / GMT_E_INFEASIBLE_SAMPLING),
-// V[q] its vertex count and init[q] its init index.
-int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& arena,
+// Derive the instances of `count` problems into `meta` / `rows` (device).  On
+// return inst[q] is the device descriptor of query q (a derived one, or one of
+// the single-built instances appended to `owned`; null when the query's own
+// build failed with status[q] = GMT_E_GOAL_BLOCKED / GMT_E_INFEASIBLE_SAMPLING),
+// V[q] its vertex count, init[q] its init index, radius[q] its graph radius.
+int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& meta, Arena& rows,
                 std::vector<gmt_instance*>& owned, std::vector<const DevInstance*>& inst, std::vector<int>& V,
                 std::vector<int>& init, std::vector<double>& radius, std::vector<int32_t>& status, int* max_V,
                 int* max_nb) {
@@ -652,7 +764,8 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& are
   std::vector<PQ> pq(count);
   std::vector<double> box_lo, box_hi, goal_lo(static_cast<size_t>(count) * kD), goal_hi(goal_lo.size()),
       inits(goal_lo.size());
-  int K = 0, eligible = 0, max_nbp = 0, max_n = 0;
+  int Kc = 0, eligible = 0, max_nbp = 0, max_n = 0;
+  int64_t box_total = 0, node_total = 0;
   for (int q = 0; q < count; ++q) {
     const gmt_problem& pr = problems[q];
     int rc = validate_scene(&pr.scene);
@@ -665,27 +778,11 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& are
     ++eligible;
     Q.n = pr.n;
     Q.nb = pr.scene.num_boxes;
-    K = std::max(K, pool_need(pr));
-    max_nbp = std::max(max_nbp, Q.nb);
-    max_n = std::max(max_n, pr.n);
-  }
-  g_last_error.clear();
-  SamplePool* pool = nullptr;
-  if (eligible) {
-    int rc = get_pool(ctx, p0, K, &pool);
-    if (rc) return rc;
-    K = pool->K;
-  }
-  // host layout
-  int64_t box_total = 0, node_total = 0, slot_total = 0;
-  const int64_t Ep = pool ? pool->in.edges : 0;
-  for (int q = 0; q < count; ++q) {
-    PQ& Q = pq[q];
-    if (Q.skip) continue;
-    const gmt_problem& pr = problems[q];
     Q.box_off = box_total;
     Q.node_off = node_total;
-    Q.slot_off = slot_total;
+    Kc = std::max(Kc, pool_need(pr));
+    max_nbp = std::max(max_nbp, Q.nb);
+    max_n = std::max(max_n, pr.n);
     box_lo.insert(box_lo.end(), pr.scene.box_lo, pr.scene.box_lo + static_cast<size_t>(Q.nb) * kD);
     box_hi.insert(box_hi.end(), pr.scene.box_hi, pr.scene.box_hi + static_cast<size_t>(Q.nb) * kD);
     std::copy(pr.scene.goal_lo, pr.scene.goal_lo + kD, goal_lo.begin() + static_cast<size_t>(q) * kD);
@@ -693,109 +790,165 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& are
     std::copy(pr.init, pr.init + kD, inits.begin() + static_cast<size_t>(q) * kD);
     box_total += Q.nb;
     node_total += Q.n + 1;
-    slot_total += Ep + 2 * static_cast<int64_t>(Q.n + 1) + 2 * kSpecCap;
   }
+  g_last_error.clear();
   std::vector<PQOut> po(count);
+  SamplePool* pool = nullptr;
+  StageTimer timer(s);
   if (eligible) {
-    Carver c;
-    const size_t o_pq = c.take<PQ>(count);
-    const size_t o_po = c.take<PQOut>(count);
-    const size_t o_blo = c.take<double>(std::max<int64_t>(box_total, 1) * kD);
-    const size_t o_bhi = c.take<double>(std::max<int64_t>(box_total, 1) * kD);
-    const size_t o_glo = c.take<double>(goal_lo.size());
-    const size_t o_ghi = c.take<double>(goal_hi.size());
-    const size_t o_init = c.take<double>(inits.size());
-    const size_t o_flag = c.take<uint8_t>(static_cast<size_t>(count) * K);
-    const size_t o_rank = c.take<uint16_t>(static_cast<size_t>(count) * K);
-    const size_t o_sel = c.take<int32_t>(node_total);
-    const size_t o_qc = c.take<double>(node_total * kD);
-    const size_t o_scol = c.take<int32_t>(static_cast<size_t>(count) * 4 * kSpecCap);
-    const size_t o_scost = c.take<double>(static_cast<size_t>(count) * 4 * kSpecCap);
-    const size_t o_stau = c.take<double>(static_cast<size_t>(count) * 4 * kSpecCap);
-    const size_t o_is = c.take<int64_t>(node_total);
-    const size_t o_ie = c.take<int64_t>(node_total);
-    const size_t o_os = c.take<int64_t>(node_total);
-    const size_t o_oe = c.take<int64_t>(node_total);
-    const size_t o_icol = c.take<int32_t>(slot_total);
-    const size_t o_icost = c.take<double>(slot_total);
-    const size_t o_itau = c.take<double>(slot_total);
-    const size_t o_ocol = c.take<int32_t>(slot_total);
-    const size_t o_desc = c.take<DevInstance>(count);
-    int rc = arena.reserve(c.off);
-    if (rc) return rc;
-    char* B = static_cast<char*>(arena.ptr);
-    auto* d_pq = reinterpret_cast<PQ*>(B + o_pq);
-    auto* d_po = reinterpret_cast<PQOut*>(B + o_po);
-    auto* d_blo = reinterpret_cast<double*>(B + o_blo);
-    auto* d_bhi = reinterpret_cast<double*>(B + o_bhi);
-    auto* d_glo = reinterpret_cast<double*>(B + o_glo);
-    auto* d_ghi = reinterpret_cast<double*>(B + o_ghi);
-    auto* d_init = reinterpret_cast<double*>(B + o_init);
-    auto* d_flag = reinterpret_cast<uint8_t*>(B + o_flag);
-    auto* d_rank = reinterpret_cast<uint16_t*>(B + o_rank);
-    auto* d_sel = reinterpret_cast<int32_t*>(B + o_sel);
-    auto* d_qc = reinterpret_cast<double*>(B + o_qc);
-    auto* d_scol = reinterpret_cast<int32_t*>(B + o_scol);
-    auto* d_scost = reinterpret_cast<double*>(B + o_scost);
-    auto* d_stau = reinterpret_cast<double*>(B + o_stau);
-    auto* d_is = reinterpret_cast<int64_t*>(B + o_is);
-    auto* d_ie = reinterpret_cast<int64_t*>(B + o_ie);
-    auto* d_os = reinterpret_cast<int64_t*>(B + o_os);
-    auto* d_oe = reinterpret_cast<int64_t*>(B + o_oe);
-    auto* d_icol = reinterpret_cast<int32_t*>(B + o_icol);
-    auto* d_icost = reinterpret_cast<double*>(B + o_icost);
-    auto* d_itau = reinterpret_cast<double*>(B + o_itau);
-    auto* d_ocol = reinterpret_cast<int32_t*>(B + o_ocol);
-    auto* d_desc = reinterpret_cast<DevInstance*>(B + o_desc);
-    auto put = [&](void* dst, const void* src, size_t bytes) -> int {
-      if (bytes) GMT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-      return GMT_OK;
-    };
-    if ((rc = put(d_pq, pq.data(), sizeof(PQ) * count)) ||
-        (rc = put(d_blo, box_lo.data(), sizeof(double) * box_lo.size())) ||
-        (rc = put(d_bhi, box_hi.data(), sizeof(double) * box_hi.size())) ||
-        (rc = put(d_glo, goal_lo.data(), sizeof(double) * goal_lo.size())) ||
-        (rc = put(d_ghi, goal_hi.data(), sizeof(double) * goal_hi.size())) ||
-        (rc = put(d_init, inits.data(), sizeof(double) * inits.size())))
-      return rc;
-    Primes pr;
-    for (int k = 0; k < kD; ++k) pr.p[k] = nth_prime_h(k + 1);
-    const double* P = static_cast<const double*>(pool->coords.ptr);
-    const int stage_cap = 2048;  // boxes staged in shared memory up to 2048 * 96 B
-    const int nb_st = std::min(max_nbp, stage_cap);
-    const size_t fsm = sizeof(double) * 2 * kD * static_cast<size_t>(std::max(nb_st, 1));
-    if (fsm > 48 * 1024)
-      GMT_CUDA(cudaFuncSetAttribute(pool_free_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsm)));
-    pool_free_kernel<<<dim3((K + 255) / 256, count), 256, fsm, s>>>(d_pq, P, K, d_blo, d_bhi, nb_st, d_flag);
-    pool_select_kernel<<<count, 1024, 0, s>>>(d_pq, P, K, d_flag, d_glo, d_ghi, d_rank, d_sel, d_qc, d_po);
-    pool_subst_kernel<<<count, 256, 0, s>>>(d_pq, K, d_blo, d_bhi, d_glo, d_ghi, pr, d_rank, d_sel, d_qc, d_po);
-    pool_init_kernel<<<count, 256, 0, s>>>(d_pq, d_init, d_qc, d_po);
-    const DiParams DP = to_di(&p0.di);
-    pool_special_kernel<<<count, 128, 0, s>>>(d_pq, DP, di_prefilter_bound(DP, pool->radius), pool->radius, d_qc,
-                                              d_scol, d_scost, d_stau, d_po);
-    pool_rows_kernel<<<dim3((max_n + 1 + 7) / 8, count), 256, 0, s>>>(
-        d_pq, d_po, K, Ep, pool->in.ptr, pool->in.col, pool->in.cost, pool->in.tau, pool->out.ptr, pool->out.col,
-        d_rank, d_sel, d_scol, d_scost, d_stau, d_is, d_ie, d_os, d_oe, d_icol, d_icost, d_itau, d_ocol);
-    pool_desc_kernel<<<(count + 127) / 128, 128, 0, s>>>(d_pq, d_po, count, pool->radius, DP, d_qc, d_blo, d_bhi,
-                                                         d_glo, d_ghi, d_is, d_ie, d_os, d_oe, d_icol, d_icost,
-                                                         d_itau, d_ocol, d_desc);
-    GMT_CUDA(cudaGetLastError());
-    ctx->launches += 8;
-    GMT_CUDA(cudaMemcpyAsync(po.data(), d_po, sizeof(PQOut) * count, cudaMemcpyDeviceToHost, s));
-    GMT_CUDA(cudaStreamSynchronize(s));
-    for (int q = 0; q < count; ++q) {
-      if (pq[q].skip || po[q].fallback) continue;
-      inst[q] = d_desc + q;
-      V[q] = pq[q].n + 1;
-      init[q] = pq[q].n;
-      radius[q] = pool->radius;
-      *max_V = std::max(*max_V, V[q]);
-      *max_nb = std::max(*max_nb, pq[q].nb);
+    // The candidate scan covers the pool graph (steady state: every query's
+    // cutoff already lies inside it) or the free-volume estimate.
+    if (same_source(ctx->pool, p0) && ctx->pool->K > 0) Kc = std::min(Kc, ctx->pool->K);
+    Kc = std::min<int64_t>(Kc, 1000LL * max_n);
+    for (;;) {
+      int rc = pool_points(ctx, p0, Kc, &pool);
+      if (rc) return rc;
+      Carver c;
+      const size_t o_pq = c.take<PQ>(count);
+      const size_t o_po = c.take<PQOut>(count);
+      const size_t o_blo = c.take<double>(std::max<int64_t>(box_total, 1) * kD);
+      const size_t o_bhi = c.take<double>(std::max<int64_t>(box_total, 1) * kD);
+      const size_t o_glo = c.take<double>(goal_lo.size());
+      const size_t o_ghi = c.take<double>(goal_hi.size());
+      const size_t o_init = c.take<double>(inits.size());
+      const size_t o_flag = c.take<uint8_t>(static_cast<size_t>(count) * Kc);
+      const size_t o_rank = c.take<uint16_t>(static_cast<size_t>(count) * Kc);
+      const size_t o_sel = c.take<int32_t>(node_total);
+      const size_t o_qc = c.take<double>(node_total * kD);
+      const size_t o_scol = c.take<int32_t>(static_cast<size_t>(count) * 4 * kSpecCap);
+      const size_t o_scost = c.take<double>(static_cast<size_t>(count) * 4 * kSpecCap);
+      const size_t o_stau = c.take<double>(static_cast<size_t>(count) * 4 * kSpecCap);
+      const size_t o_is = c.take<int64_t>(node_total);
+      const size_t o_ie = c.take<int64_t>(node_total);
+      const size_t o_os = c.take<int64_t>(node_total);
+      const size_t o_oe = c.take<int64_t>(node_total);
+      const size_t o_desc = c.take<DevInstance>(count);
+      rc = meta.reserve(c.off);
+      if (rc) return rc;
+      char* B = static_cast<char*>(meta.ptr);
+      auto* d_pq = reinterpret_cast<PQ*>(B + o_pq);
+      auto* d_po = reinterpret_cast<PQOut*>(B + o_po);
+      auto* d_blo = reinterpret_cast<double*>(B + o_blo);
+      auto* d_bhi = reinterpret_cast<double*>(B + o_bhi);
+      auto* d_glo = reinterpret_cast<double*>(B + o_glo);
+      auto* d_ghi = reinterpret_cast<double*>(B + o_ghi);
+      auto* d_init = reinterpret_cast<double*>(B + o_init);
+      auto* d_flag = reinterpret_cast<uint8_t*>(B + o_flag);
+      auto* d_rank = reinterpret_cast<uint16_t*>(B + o_rank);
+      auto* d_sel = reinterpret_cast<int32_t*>(B + o_sel);
+      auto* d_qc = reinterpret_cast<double*>(B + o_qc);
+      auto* d_scol = reinterpret_cast<int32_t*>(B + o_scol);
+      auto* d_scost = reinterpret_cast<double*>(B + o_scost);
+      auto* d_stau = reinterpret_cast<double*>(B + o_stau);
+      auto* d_is = reinterpret_cast<int64_t*>(B + o_is);
+      auto* d_ie = reinterpret_cast<int64_t*>(B + o_ie);
+      auto* d_os = reinterpret_cast<int64_t*>(B + o_os);
+      auto* d_oe = reinterpret_cast<int64_t*>(B + o_oe);
+      auto* d_desc = reinterpret_cast<DevInstance*>(B + o_desc);
+      auto put = [&](void* dst, const void* src, size_t bytes) -> int {
+        if (bytes) GMT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return GMT_OK;
+      };
+      timer.mark();
+      if ((rc = put(d_pq, pq.data(), sizeof(PQ) * count)) ||
+          (rc = put(d_blo, box_lo.data(), sizeof(double) * box_lo.size())) ||
+          (rc = put(d_bhi, box_hi.data(), sizeof(double) * box_hi.size())) ||
+          (rc = put(d_glo, goal_lo.data(), sizeof(double) * goal_lo.size())) ||
+          (rc = put(d_ghi, goal_hi.data(), sizeof(double) * goal_hi.size())) ||
+          (rc = put(d_init, inits.data(), sizeof(double) * inits.size())))
+        return rc;
+      const double* P = static_cast<const double*>(pool->pts.ptr);
+      const int stage_cap = 2048;  // boxes staged in shared memory up to 2048 * 96 B
+      const int nb_st = std::min(max_nbp, stage_cap);
+      const size_t fsm = sizeof(double) * 2 * kD * static_cast<size_t>(std::max(nb_st, 1));
+      if (fsm > 48 * 1024)
+        GMT_CUDA(cudaFuncSetAttribute(pool_free_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(fsm)));
+      timer.mark();
+      pool_free_kernel<<<dim3((Kc + 255) / 256, count), 256, fsm, s>>>(d_pq, P, Kc, d_blo, d_bhi, nb_st, d_flag);
+      timer.mark();
+      pool_select_kernel<<<count, 1024, 0, s>>>(d_pq, P, Kc, d_flag, d_glo, d_ghi, d_rank, d_sel, d_qc, d_po);
+      GMT_CUDA(cudaGetLastError());
+      ctx->launches += 2;
+      GMT_CUDA(cudaMemcpyAsync(po.data(), d_po, sizeof(PQOut) * count, cudaMemcpyDeviceToHost, s));
+      GMT_CUDA(cudaStreamSynchronize(s));
+      int cutoff = 0, need = 0;
+      for (int q = 0; q < count; ++q) {
+        if (pq[q].skip) continue;
+        if (po[q].fallback) need = std::max(need, Kc + Kc / 2);  // short: widen the scan
+        else cutoff = std::max(cutoff, po[q].cutoff);
+      }
+      if (need > Kc && Kc < 1000LL * max_n) {
+        Kc = static_cast<int>(std::min<int64_t>(need, 1000LL * max_n));
+        continue;
+      }
+      rc = pool_graph(ctx, pool, cutoff);
+      if (rc) return rc;
+      const DiParams DP = to_di(&p0.di);
+      Primes pr;
+      for (int k = 0; k < kD; ++k) pr.p[k] = nth_prime_h(k + 1);
+      timer.mark();
+      pool_subst_kernel<<<count, 256, 0, s>>>(d_pq, Kc, d_blo, d_bhi, d_glo, d_ghi, pr, d_rank, d_sel, d_qc, d_po);
+      pool_init_kernel<<<count, 256, 0, s>>>(d_pq, d_init, d_qc, d_po);
+      timer.mark();
+      pool_special_kernel<<<count, 128, 0, s>>>(d_pq, DP, di_prefilter_bound(DP, pool->radius), pool->radius, d_qc,
+                                                d_scol, d_scost, d_stau, d_po);
+      timer.mark();
+      pool_layout_kernel<<<count, 1024, 0, s>>>(d_pq, pool->in.ptr, pool->out.ptr, d_sel, d_is, d_os, d_po);
+      GMT_CUDA(cudaGetLastError());
+      ctx->launches += 4;
+      GMT_CUDA(cudaMemcpyAsync(po.data(), d_po, sizeof(PQOut) * count, cudaMemcpyDeviceToHost, s));
+      GMT_CUDA(cudaStreamSynchronize(s));
+      int64_t tin = 0, tout = 0;
+      for (int q = 0; q < count; ++q) {
+        if (pq[q].skip || po[q].fallback) continue;
+        pq[q].in_off = tin;
+        pq[q].out_off = tout;
+        tin += po[q].tot_in;
+        tout += po[q].tot_out;
+      }
+      Carver r;
+      const size_t o_icol = r.take<int32_t>(tin);
+      const size_t o_icost = r.take<double>(tin);
+      const size_t o_itau = r.take<double>(tin);
+      const size_t o_ocol = r.take<int32_t>(tout);
+      rc = rows.reserve(r.off);
+      if (rc) return rc;
+      char* R = static_cast<char*>(rows.ptr);
+      auto* d_icol = reinterpret_cast<int32_t*>(R + o_icol);
+      auto* d_icost = reinterpret_cast<double*>(R + o_icost);
+      auto* d_itau = reinterpret_cast<double*>(R + o_itau);
+      auto* d_ocol = reinterpret_cast<int32_t*>(R + o_ocol);
+      if ((rc = put(d_pq, pq.data(), sizeof(PQ) * count))) return rc;
+      timer.mark();
+      pool_rows_kernel<<<dim3((max_n + 1 + 7) / 8, count), 256, 0, s>>>(
+          d_pq, d_po, Kc, pool->in.ptr, pool->in.col, pool->in.cost, pool->in.tau, pool->out.ptr, pool->out.col,
+          d_rank, d_sel, d_scol, d_scost, d_stau, d_is, d_ie, d_os, d_oe, d_icol, d_icost, d_itau, d_ocol);
+      timer.mark();
+      pool_desc_kernel<<<(count + 127) / 128, 128, 0, s>>>(d_pq, d_po, count, pool->radius, DP, d_qc, d_blo, d_bhi,
+                                                           d_glo, d_ghi, d_is, d_ie, d_os, d_oe, d_icol, d_icost,
+                                                           d_itau, d_ocol, d_desc);
+      GMT_CUDA(cudaGetLastError());
+      timer.mark();
+      ctx->launches += 2;
+      for (int q = 0; q < count; ++q) {
+        if (pq[q].skip || po[q].fallback) continue;
+        inst[q] = d_desc + q;
+        V[q] = pq[q].n + 1;
+        init[q] = pq[q].n;
+        radius[q] = pool->radius;
+        *max_V = std::max(*max_V, V[q]);
+        *max_nb = std::max(*max_nb, pq[q].nb);
+      }
+      break;
     }
+    timer.report(pool);
   }
   // The rare paths and the problems off the pool: the single-instance builder.
+  int fallbacks = 0;
   for (int q = 0; q < count; ++q) {
     if (!pq[q].skip && !po[q].fallback) continue;
+    ++fallbacks;
     gmt_instance* one = nullptr;
     int rc = gmt_instance_build(ctx, &problems[q], &one);
     if (rc == GMT_E_GOAL_BLOCKED || rc == GMT_E_INFEASIBLE_SAMPLING) {
@@ -811,14 +964,19 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& are
     *max_V = std::max(*max_V, V[q]);
     *max_nb = std::max(*max_nb, one->desc.num_boxes);
   }
+  if (pool) pool->last_fallbacks = fallbacks;
   return GMT_OK;
 }
 
-int pool_stats(const gmt_ctx* ctx, int32_t* K, int64_t* edges, double* build_ms) {
+int pool_stats(const gmt_ctx* ctx, int32_t* K, int64_t* edges, double* build_ms, int32_t* fallbacks,
+               double* stage_ms) {
   const SamplePool* p = ctx->pool;
   if (K) *K = p ? p->K : 0;
   if (edges) *edges = p ? p->out.edges : 0;
   if (build_ms) *build_ms = p ? p->build_ms : 0.0;
+  if (fallbacks) *fallbacks = p ? p->last_fallbacks : 0;
+  if (stage_ms)
+    for (int i = 0; i < 8; ++i) stage_ms[i] = p ? p->stage_ms[i] : 0.0;
   return GMT_OK;
 }
 
@@ -826,7 +984,7 @@ int pool_stats(const gmt_ctx* ctx, int32_t* K, int64_t* edges, double* build_ms)
 static int batch_from_derived(gmt_ctx* ctx, gmt_batch* b, const gmt_problem* problems, int count,
                               const std::vector<const DevInstance*>& inst, const std::vector<int>& V,
                               const std::vector<int>& init, const std::vector<double>& radius, int max_V,
-                              int max_nb, std::vector<int>& job_q) {
+                              int max_nb, std::vector<int>& job_q, bool tree_stats) {
   b->ctx = ctx;
   b->node_off.assign(1, 0);
   job_q.clear();
@@ -849,12 +1007,13 @@ static int batch_from_derived(gmt_ctx* ctx, gmt_batch* b, const gmt_problem* pro
   const int J = static_cast<int>(b->jobs.size());
   if (J == 0) return GMT_OK;
   b->dim = d;
-  // (the shape gmt_batch_create picks: 2-CTA clusters for kinodynamic queries)
-  b->cluster = ctx->batch_cluster ? ctx->batch_cluster : (kino ? 2 : 1);
-  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
+  // (the shape gmt_batch_create picks: 2-CTA clusters for a few kinodynamic
+  // queries, one CTA each once they fill the SMs several times over)
+  b->cluster = ctx->batch_cluster ? ctx->batch_cluster : (kino && J < 4 * ctx->sm_count ? 2 : 1);
+  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 || kino ? 512 : 256);
   int rc = plan_smem(ctx, max_V, d, max_nb, b->cluster, &b->smem, &b->obs);
   if (rc) return rc;
-  rc = carve_results(b->res, J, b->node_off.data(), true, true, b->results, &b->scalars,
+  rc = carve_results(b->res, J, b->node_off.data(), tree_stats, tree_stats, b->results, &b->scalars,
                      ctx->counting ? ctx->counters : nullptr);
   if (rc) return rc;
   for (int k = 0; k < J; ++k) b->jobs[k].res = b->results[k];
@@ -876,9 +1035,13 @@ int plan_problems_pool(gmt_ctx* ctx, const gmt_problem* problems, int32_t count,
   std::vector<double> radius;
   std::vector<int32_t> status;
   int max_V = 0, max_nb = 0;
-  int rc = pool_derive(ctx, problems, count, ctx->pool_work, owned, inst, V, init, radius, status, &max_V, &max_nb);
+  int rc = pool_derive(ctx, problems, count, ctx->pool_work, ctx->pool_rows, owned, inst, V, init, radius, status,
+                       &max_V, &max_nb);
   gmt_batch b;
-  if (rc == GMT_OK) rc = batch_from_derived(ctx, &b, problems, count, inst, V, init, radius, max_V, max_nb, job_q);
+  b.res = ctx->pool_res;  // (kept in the context across calls, like the derived instances)
+  ctx->pool_res = Arena{};
+  if (rc == GMT_OK)  // summaries (and paths) only: no trees, no per-pass stats
+    rc = batch_from_derived(ctx, &b, problems, count, inst, V, init, radius, max_V, max_nb, job_q, false);
   const int J = static_cast<int>(b.jobs.size());
   cudaStream_t s = ctx->stream;
   if (rc == GMT_OK && J > 0) {
@@ -931,7 +1094,8 @@ int plan_problems_pool(gmt_ctx* ctx, const gmt_problem* problems, int32_t count,
   }
   if (rc == GMT_OK)
     for (int q = 0; q < count; ++q) status_out[q] = status[q];
-  b.res.release();
+  ctx->pool_res = b.res;
+  b.res = Arena{};
   b.jobs_mem.release();
   for (gmt_instance* i : owned) gmt_instance_destroy(i);
   return rc;
@@ -952,8 +1116,10 @@ extern "C" int gmt_batch_create_problems(gmt_ctx* ctx, const gmt_problem* proble
   std::vector<double> radius;
   std::vector<int32_t> status;
   int max_V = 0, max_nb = 0;
-  int rc = pool_derive(ctx, problems, count, b->derived, b->owned, inst, V, init, radius, status, &max_V, &max_nb);
-  if (rc == GMT_OK) rc = batch_from_derived(ctx, b, problems, count, inst, V, init, radius, max_V, max_nb, job_q);
+  int rc = pool_derive(ctx, problems, count, b->derived, b->derived_rows, b->owned, inst, V, init, radius, status,
+                       &max_V, &max_nb);
+  if (rc == GMT_OK)
+    rc = batch_from_derived(ctx, b, problems, count, inst, V, init, radius, max_V, max_nb, job_q, true);
   if (rc == GMT_OK && b->jobs.empty()) rc = set_error(GMT_E_INVALID_INPUT, "no problem of the batch could be built");
   if (rc != GMT_OK) {
     delete b;
@@ -964,9 +1130,10 @@ extern "C" int gmt_batch_create_problems(gmt_ctx* ctx, const gmt_problem* proble
   return GMT_OK;
 }
 
-extern "C" int gmt_ctx_pool_info(gmt_ctx* ctx, int32_t* pool_size, int64_t* num_edges, double* build_ms) {
+extern "C" int gmt_ctx_pool_info(gmt_ctx* ctx, int32_t* pool_size, int64_t* num_edges, double* build_ms,
+                                 int32_t* last_fallbacks, double* stage_ms) {
   if (!ctx) return set_error(GMT_E_INVALID_INPUT, "context is null");
-  return pool_stats(ctx, pool_size, num_edges, build_ms);
+  return pool_stats(ctx, pool_size, num_edges, build_ms, last_fallbacks, stage_ms);
 }
 
 // Rows of batch query q as compressed rows (host): the two-call pattern of

@@ -105,11 +105,14 @@ struct CtaShared {
 
 // Boxes: box b, axis k at base[b*bs + k*as].  lom/him hold lo - m and
 // hi + m (the separation bounds) when the boxes are staged in shared memory.
+// idx (may be null): box i of this view is box idx[i] of the arrays (a
+// per-edge list of the boxes that survive the polyline's bounding box).
 struct Boxes {
   const double* lo;
   const double* hi;
   const double* lom;
   const double* him;
+  const uint16_t* idx;
   int bs;
   int as;
   int count;
@@ -229,7 +232,8 @@ __device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const doubl
   for (int i0 = 0; i0 < bx.count && !hit; i0 += kWarp) {
     const int i = i0 + lane;
     bool sep = i >= bx.count;
-    const int ic = sep ? bx.count - 1 : i;  // idle lanes read a valid box
+    int ic = sep ? bx.count - 1 : i;  // idle lanes read a valid box
+    if (bx.idx) ic = bx.idx[ic];
 #pragma unroll
     for (int k = 0; k < (D > 0 ? D : kMaxSolveDim); ++k) {
       if (D == 0 && k >= d) break;
@@ -261,7 +265,8 @@ __device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const doubl
       if (slot < take) {
         uint32_t mm = cm;  // the slot-th surviving box (slot < take, usually 0-2)
         for (int t = 0; t < slot; ++t) mm &= mm - 1u;
-        const int bi = i0 + __ffs(mm) - 1;
+        int bi = i0 + __ffs(mm) - 1;
+        if (bx.idx) bi = bx.idx[bi];
         const double ak = a[axis];
         const double dk = __dsub_rn(b[axis], ak);
         const double l = bx.lo[bi * bx.bs + axis * bx.as], h = bx.hi[bi * bx.bs + axis * bx.as];
@@ -341,6 +346,45 @@ __device__ bool polyline_free_warp(const DevInstance& I, int d, const Boxes& bx,
   return true;
 }
 
+// segment_hits_box (space.cpp:60-78) of one segment against one box on a
+// single lane: the exact-safe separation pre-test of segment_free_ab, then
+// the reference's sequential closed slab clip (tmin = 0, tmax = 1).
+template <int D>
+__device__ __forceinline__ bool seg_box_hit(const double* a, const double* b, int d_rt, const Boxes& bx, int box) {
+  const int d = dims<D>(d_rt);
+#pragma unroll
+  for (int k = 0; k < (D > 0 ? D : kMaxSolveDim); ++k) {
+    if (D == 0 && k >= d) break;
+    const double lo = bx.lom ? bx.lom[box * bx.bs + k * bx.as] : bx.lo[box * bx.bs + k * bx.as] - kSepMargin;
+    const double hi = bx.him ? bx.him[box * bx.bs + k * bx.as] : bx.hi[box * bx.bs + k * bx.as] + kSepMargin;
+    const double x = a[k], y = b[k];
+    if ((x < lo && y < lo) || (x > hi && y > hi)) return false;
+  }
+  double tmin = 0.0, tmax = 1.0;
+#pragma unroll
+  for (int k = 0; k < (D > 0 ? D : kMaxSolveDim); ++k) {
+    if (D == 0 && k >= d) break;
+    const double ak = a[k];
+    const double dk = __dsub_rn(b[k], ak);
+    const double l = bx.lo[box * bx.bs + k * bx.as], h = bx.hi[box * bx.bs + k * bx.as];
+    if (dk == 0.0) {
+      if (ak < l || ak > h) return false;
+    } else {
+      double t0 = __ddiv_rn(__dsub_rn(l, ak), dk);
+      double t1 = __ddiv_rn(__dsub_rn(h, ak), dk);
+      if (t0 > t1) {
+        const double t = t0;
+        t0 = t1;
+        t1 = t;
+      }
+      tmin = (tmin < t0) ? t0 : tmin;  // std::max(tmin, t0)
+      tmax = (t1 < tmax) ? t1 : tmax;  // std::min(tmax, t1)
+      if (tmin > tmax) return false;
+    }
+  }
+  return true;
+}
+
 // The same test for a kinodynamic edge whose polyline is not stored (double
 // integrator, quadrotor): lanes 0..dim-1 and 16..16+dim-1 evaluate the
 // coordinates of waypoints s and s+1 (di_coord / quad_coord, the very
@@ -349,7 +393,7 @@ __device__ bool polyline_free_warp(const DevInstance& I, int d, const Boxes& bx,
 template <int D>
 __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int from, int to,
                                     double tau, int lane, double* seg, double* tab = nullptr,
-                                    int tab_cap = 0) {
+                                    int tab_cap = 0, uint16_t* cull = nullptr, int cull_cap = 0) {
   // Only the generic-dimension kernel can see a 12D quadrotor instance.
   const bool quad = D == 0 && I.steering == GMT_STEER_QUADROTOR;
   const int dim = quad ? kQuadDim : kDiDim;
@@ -374,13 +418,28 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
     DP.segments = M;
     DP.reserved = 0;
   }
-  if (tab && (M + 1) * dim <= tab_cap) {
+  if (tab && (M + 1) * dim <= tab_cap && (quad || M + 6 <= kWarp)) {
     // Waypoint table: every waypoint once, lane-parallel over (waypoint,
-    // coordinate); the quadrotor's per-chain lambda first (lanes 0-3, into
-    // the seg scratch).  Same arithmetic as di_coord / quad_coord.
+    // coordinate).  The quadrotor's per-chain lambda first (lanes 0-3, into
+    // the seg scratch); the double integrator's per-axis cubic coefficients
+    // c2, c3 (lanes 0-2) and waypoint times t_k (lanes 3..) first, which
+    // di_coord recomputes identically for every coordinate -- the table
+    // entries are the very operations of di_coord / quad_coord.
     __syncwarp();
-    if (quad && lane < 4) quad_chain_lambda(x0, x1, tau, lane, QP, seg + 8 * lane, seg + 8 * lane + 4);
+    if (quad) {
+      if (lane < 4) quad_chain_lambda(x0, x1, tau, lane, QP, seg + 8 * lane, seg + 8 * lane + 4);
+    } else if (lane < 3) {
+      const double D = di_sub(x1[lane], x0[lane]);
+      const double v0 = di_vel(x0[3 + lane], DP), v1 = di_vel(x1[3 + lane], DP);
+      const double tt = di_mul(tau, tau);
+      seg[lane] = di_sub(di_div(di_mul(3.0, D), tt), di_div(di_add(di_mul(2.0, v0), v1), tau));
+      seg[3 + lane] = di_sub(di_div(di_add(v0, v1), tt), di_div(di_mul(2.0, D), di_mul(tt, tau)));
+    } else if (lane - 2 < M) {
+      const int k = lane - 2;
+      seg[6 + k] = di_div(di_mul(tau, static_cast<double>(k)), static_cast<double>(M));
+    }
     __syncwarp();
+    bool incube = true;
     for (int e = lane; e < (M + 1) * dim; e += kWarp) {
       const int k = e / dim, i = e - k * dim;
       double v;
@@ -393,13 +452,92 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
         quad_locate(i, &c, &ci);
         v = quad_chain_coord(seg + 8 * c, seg + 8 * c + 4, tau, k, c, ci, QP);
       } else {
-        v = di_coord(x0, x1, tau, k, i, DP);
+        const int a = i < 3 ? i : i - 3;
+        const double t = seg[6 + k], c2 = seg[a], c3 = seg[3 + a];
+        const double v0 = di_vel(x0[3 + a], DP);
+        if (i < 3) {
+          v = di_add(x0[a], di_mul(t, di_add(v0, di_mul(t, di_add(c2, di_mul(t, c3))))));
+        } else {
+          const double vv = di_add(v0, di_mul(t, di_add(di_mul(2.0, c2), di_mul(t, di_mul(3.0, c3)))));
+          v = di_mul(0.5, di_add(di_div(vv, DP.vmax), 1.0));
+        }
       }
       tab[e] = v;
+      incube = incube && !(v < 0.0 || v > 1.0);
     }
+    // polyline_free (space.cpp:92-99) = every waypoint in the unit cube (each
+    // segment's point_in_cube / point_free endpoint test) and no (segment,
+    // box) pair hit -- a degenerate segment's all-axes dk == 0 clip is
+    // exactly Aabb::contains; the outcome does not depend on the order.
+    if (!__all_sync(kFull, incube)) return false;
     __syncwarp();
-    for (int s = 0; s < M; ++s)
-      if (!segment_free_ab<D>(dim, bx, lane, tab + s * dim, tab + (s + 1) * dim)) return false;
+    // Boxes the whole polyline's bounding box (widened by the separation
+    // margin) misses are missed by every segment's own pre-test: they are
+    // dropped once per edge, and the segments test the survivors only.
+    Boxes sub = bx;
+    if (cull && bx.count > 0) {
+      if (lane < dim) {
+        double mn = tab[lane], mx = tab[lane];
+        for (int k = 1; k <= M; ++k) {
+          const double x = tab[k * dim + lane];
+          mn = x < mn ? x : mn;
+          mx = x < mx ? mx : x;
+        }
+        seg[lane] = mn;
+        seg[16 + lane] = mx;
+      }
+      __syncwarp();
+      constexpr int kR = D > 0 ? D : 1;  // fixed dimension: the bounding box in registers
+      double pmn[kR], pmx[kR];
+      if constexpr (D > 0) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          pmn[k] = seg[k];
+          pmx[k] = seg[16 + k];
+        }
+      }
+      int kept = 0;
+      for (int i0 = 0; i0 < bx.count && kept <= cull_cap; i0 += kWarp) {
+        const int b = i0 + lane;
+        bool meets = b < bx.count;
+        const int bc = meets ? b : 0;
+        if constexpr (D > 0) {
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const double lo = bx.lom ? bx.lom[bc * bx.bs + k * bx.as] : bx.lo[bc * bx.bs + k * bx.as] - kSepMargin;
+            const double hi = bx.him ? bx.him[bc * bx.bs + k * bx.as] : bx.hi[bc * bx.bs + k * bx.as] + kSepMargin;
+            meets = meets && !(pmx[k] < lo || pmn[k] > hi);
+          }
+        } else {
+          for (int k = 0; k < dim && meets; ++k) {
+            const double lo = bx.lom ? bx.lom[bc * bx.bs + k * bx.as] : bx.lo[bc * bx.bs + k * bx.as] - kSepMargin;
+            const double hi = bx.him ? bx.him[bc * bx.bs + k * bx.as] : bx.hi[bc * bx.bs + k * bx.as] + kSepMargin;
+            meets = !(seg[16 + k] < lo || seg[k] > hi);
+          }
+        }
+        const uint32_t m = __ballot_sync(kFull, meets);
+        const int at = kept + __popc(m & ((1u << lane) - 1u));
+        if (meets && at < cull_cap) cull[at] = static_cast<uint16_t>(b);
+        kept += __popc(m);
+      }
+      __syncwarp();
+      if (kept <= cull_cap) {
+        sub.idx = cull;
+        sub.count = kept;
+      }
+    }
+    // Lane per (segment, box) pair, each through the reference's clip.
+    const int nbx = sub.count;
+    const int pairs = M * nbx;
+    for (int p0 = 0; p0 < pairs; p0 += kWarp) {
+      const int p = p0 + lane;
+      bool hit = false;
+      if (p < pairs) {
+        const int sg = p / nbx, bi = p - sg * nbx;
+        hit = seg_box_hit<D>(tab + sg * dim, tab + (sg + 1) * dim, dim, bx, sub.idx ? sub.idx[bi] : bi);
+      }
+      if (__any_sync(kFull, hit)) return false;
+    }
     return true;
   }
   const int i = lane & 15;
@@ -464,8 +602,11 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 // COUNT: single-CTA solves count the open-source gathers only in the
 // instantiation launched while traffic counters are on (GMT_OPT_COUNTERS);
 // cluster solves always can.
+// Kinodynamic queries (D = 6 double integrator, D = 0 quadrotor) need about
+// 55 KB of shared memory per narrow CTA, so three fit an SM: those narrow
+// kernels get the registers of three CTAs per SM.
 template <int CS, int D, bool WIDE, bool COUNT>
-__global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLOCKS)
+__global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 0) ? 3 : GMT_BATCH_MIN_BLOCKS))
     gmt_solve_kernel(const SolveJob* __restrict__ jobs, int obs_in_smem) {
   constexpr bool kParentSmem = CS > 1;  // single-CTA solves keep parents in HBM
   constexpr int kMaxWarps = WIDE ? 16 : 8;
@@ -482,6 +623,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   // Kinodynamic waypoint tables (double integrator: D = 6; quadrotor: D = 0).
   constexpr int kTabCap = D == 6 ? 64 : (D == 0 ? 144 : 1);
   __shared__ double tab_s[(D == 0 || D == 6) ? kMaxWarps * kTabCap : 1];
+  constexpr int kCullCap = (D == 0 || D == 6) ? 64 : 1;  // per-warp surviving-box list
+  __shared__ uint16_t cull_s[kMaxWarps * kCullCap];
 
   const int q = blockIdx.x / CS;
   int rank = 0;
@@ -540,6 +683,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
   } else {
     bxl.lo = I.box_lo, bxl.hi = I.box_hi, bxl.lom = nullptr, bxl.him = nullptr, bxl.bs = d, bxl.as = 1;
   }
+  bxl.idx = nullptr;
 
   // make_wavefront (planner.cpp:25-35) on every replica.
   const int init = job.init_index;
@@ -958,7 +1102,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : GMT_BATCH_MIN_BLO
           auto edge_free = [&](const Boxes& B) -> bool {
             if ((D == 0 || D == 6) && I.in_tau)  // kinodynamic: regenerated polyline (di.cuh, quad.cuh)
               return kino_edge_free_warp<D>(I, B, byc, xc, __ldg(I.in_tau + bec), lane, sc,
-                                            tab_s + ((D == 0 || D == 6) ? warp * kTabCap : 0), kTabCap);
+                                            tab_s + ((D == 0 || D == 6) ? warp * kTabCap : 0), kTabCap,
+                                            cull_s + warp * kCullCap, kCullCap);
             if (pid < 0) return segment_free_staged<D>(d, B, lane, sc);  // segment_free (planner.cpp:59)
             return polyline_free_warp<D>(I, d, B, pid, lane, sc);       // polyline_free (planner.cpp:56-58)
           };
@@ -1123,6 +1268,7 @@ __global__ void __launch_bounds__(256) eager_check_kernel(const DevInstance* __r
     b.hi = I_s.box_hi;
     b.lom = nullptr;
     b.him = nullptr;
+    b.idx = nullptr;
     b.bs = I_s.dim;
     b.as = 1;
     b.count = I_s.num_boxes;
@@ -1172,6 +1318,7 @@ __global__ void __launch_bounds__(256) segment_free_kernel(const double* __restr
   bx.hi = box_hi;
   bx.lom = nullptr;
   bx.him = nullptr;
+  bx.idx = nullptr;
   bx.bs = d;
   bx.as = 1;
   bx.count = nb;
@@ -1217,6 +1364,7 @@ __global__ void __launch_bounds__(1024) dijkstra_kernel(const SolveJob* __restri
     b.hi = I_s.box_hi;
     b.lom = nullptr;
     b.him = nullptr;
+    b.idx = nullptr;
     b.bs = I_s.dim;
     b.as = 1;
     b.count = I_s.num_boxes;

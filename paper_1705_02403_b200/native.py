@@ -80,7 +80,7 @@ SIGNATURES = [
     ("gmt_dijkstra_oracle", C.c_int, [_vp, _vp, C.c_int32, _P(abi.PlanOut)]),
     ("gmt_batch_create", C.c_int, [_vp, C.c_int32, _P(_vp), _i32p, C.c_double, _P(_vp)]),
     ("gmt_batch_create_problems", C.c_int, [_vp, _P(abi.Problem), C.c_int32, _i32p, _P(_vp)]),
-    ("gmt_ctx_pool_info", C.c_int, [_vp, _i32p, _i64p, _dp]),
+    ("gmt_ctx_pool_info", C.c_int, [_vp, _i32p, _i64p, _dp, _i32p, _dp]),
     ("gmt_batch_graph", C.c_int, [_vp, _vp, C.c_int32, _i32p, _i64p, _i64p, _dp, _i64p, _i32p, _dp, _dp,
                                   _i64p, _i32p]),
     ("gmt_batch_launch", C.c_int, [_vp, _vp]),
@@ -505,9 +505,11 @@ class Context:
 
     def pool_info(self) -> dict:
         """The context's shared sample pool: points, edges, last build ms."""
-        k, e, ms = C.c_int32(), C.c_int64(), C.c_double()
-        check(lib().gmt_ctx_pool_info(self.h, C.byref(k), C.byref(e), C.byref(ms)))
-        return {"pool_size": k.value, "edges": e.value, "build_ms": ms.value}
+        k, e, ms, fb = C.c_int32(), C.c_int64(), C.c_double(), C.c_int32()
+        st = (C.c_double * 8)()
+        check(lib().gmt_ctx_pool_info(self.h, C.byref(k), C.byref(e), C.byref(ms), C.byref(fb), st))
+        return {"pool_size": k.value, "edges": e.value, "build_ms": ms.value, "last_fallbacks": fb.value,
+                "stage_ms": list(st)}
 
     def run_trial(self, scenario, seed: int, path_cap: int = 100000):
         """run_trial (simulator.cpp:66-176) -> (TrialOutcome, path_travelled [k, dim])."""

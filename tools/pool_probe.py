@@ -37,3 +37,10 @@ ms = e0.elapsed_time(e1) / 5
 print(f"solve launch {ms:.2f} ms -> {Q/ms*1e3:.0f} plans/s device-resident", flush=True)
 s2 = b.summaries()
 assert [(a.status, a.cost) for a in s2] == [(a.status, a.cost) for a, s in zip(summ, st) if s == 0]
+os.environ["GMT_POOL_TIMING"] = "1"
+for it in range(2):
+    t0 = time.perf_counter()
+    st, summ, _ = ctx.plan_problems(pb)
+    dt = time.perf_counter() - t0
+    print(f"timed plan_problems {dt*1e3:.1f} ms stages={['%.2f' % x for x in ctx.pool_info()['stage_ms']]} "
+          f"fallbacks={ctx.pool_info()['last_fallbacks']}", flush=True)
