@@ -198,6 +198,7 @@ extern "C" void gmt_ctx_destroy(gmt_ctx* ctx) {
   ctx->pinned.release();
   ctx->pinned2.release();
   ctx->pinned_jobs.release();
+  ctx->pool_pinned.release();
   cudaFree(ctx->counters);
   for (int k = 0; k < kMaxCopyChunks; ++k)
     if (ctx->copy_done[k]) cudaEventDestroy(ctx->copy_done[k]);
@@ -783,9 +784,9 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
     if (insts[q]->desc.dim != b->dim) b->dim = 0;
   // Auto shape (batch cluster 0): a few kinodynamic queries (eight polyline
   // segments per lazy check) run on 2-CTA clusters of wide CTAs; Euclidean
-  // queries on single narrow CTAs, kinodynamic batches that fill the SMs
-  // several times over on single wide CTAs (4096 DI queries: 58 ms vs 66 ms
-  // on 2-CTA clusters, tools/di_sweep.py).
+  // queries, and kinodynamic batches that fill the SMs several times over,
+  // on single narrow CTAs (4096 DI queries: 47 ms vs 52 ms on wide CTAs and
+  // 66 ms on 2-CTA clusters, tools/di_sweep.py).
   b->cluster = ctx->batch_cluster;
   if (b->cluster == 0) {
     b->cluster = 1;
@@ -810,9 +811,7 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
     j.lambda = lambda;
     j.radius = insts[q]->desc.radius;
   }
-  bool kino = false;
-  for (int q = 0; q < count; ++q) kino = kino || insts[q]->desc.steering != GMT_STEER_EUCLIDEAN;
-  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 || kino ? 512 : 256);
+  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
   rc = b->jobs_mem.reserve(sizeof(SolveJob) * count);
   if (rc == GMT_OK) {
     // jobs_mem comes from the stream-ordered pool of ctx->stream: write it on

@@ -115,6 +115,7 @@ struct gmt_ctx {
   gmtb::Arena pool_work;  // gmt_plan_problems over the shared pool: derived instances + scratch
   gmtb::Arena pool_rows;  //   ... their row regions
   gmtb::Arena pool_res;   //   ... their results
+  gmtb::HostPinned pool_pinned;  //   ... the packed scene arrays (staging)
   gmtb::SamplePool* pool = nullptr;  // shared Halton pool + its graph (built on first use, reused)
   gmtb::HostPinned pinned;
   gmtb::HostPinned pinned2;

@@ -22,7 +22,8 @@
 //   (host: the pool graph covers every cutoff, else it is regrown)
 //   pool_subst_kernel    goal substitution (the reference's search)     block / query
 //   pool_init_kernel     append_init (exact-duplicate check)            block / query
-//   pool_special_kernel  out-/in-rows of the substituted goal and init   4 warps / query
+//   pool_special_cand_kernel / pool_special_kernel
+//                        out-/in-rows of the substituted goal and init   warp / row
 //   pool_layout_kernel   row capacities (pool degree + 2) -> row starts  block / query
 //   (host: row regions sized from the per-query totals)
 //   pool_rows_kernel     every derived row: the pool row filtered by
@@ -84,6 +85,7 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kD = kDiDim;
 constexpr uint16_t kNoRank = 0xffffu;
 constexpr int kSpecCap = 1024;   // entries of one special row (larger: the single builder)
+constexpr int kCandCap = 4096;   // prefilter survivors of one special row (larger: the single builder)
 constexpr int kSubstSearch = 1024;
 
 #define GMT_CUDA(call)                                   \
@@ -331,15 +333,17 @@ __global__ void __launch_bounds__(256) pool_init_kernel(const PQ* __restrict__ p
 
 // The rows of the per-query vertices (list l: 0 out(g), 1 in(g), 2 out(init),
 // 3 in(init); g = n-1 when substituted, init = n): every other vertex x
-// tested with the builder's own prefilter and capped 2BVP solve, ascending x
-// (kino_rows_kernel's predicate and order, di_graph.cu).
-__global__ void __launch_bounds__(128) pool_special_kernel(const PQ* __restrict__ pq, DiParams P, double bound,
-                                                           double radius, const double* __restrict__ qcoords,
-                                                           int32_t* __restrict__ scol, double* __restrict__ scost,
-                                                           double* __restrict__ stau, PQOut* __restrict__ out) {
-  const int q = blockIdx.x;
+// with cost(s -> x) (or cost(x -> s)) <= r, ascending x -- kino_rows_kernel's
+// predicate and order (di_graph.cu).  Two kernels: the exact-safe prefilters
+// (few registers, many warps) compact the surviving columns in order, then
+// the capped 2BVP solve runs lane-parallel over the survivors only.
+__global__ void __launch_bounds__(256) pool_special_cand_kernel(const PQ* __restrict__ pq, DiParams P, double bound,
+                                                                double radius, const double* __restrict__ qcoords,
+                                                                int32_t* __restrict__ cand, PQOut* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // (query, list)
+  const int q = gw >> 2, l = gw & 3;
   const PQ Q = pq[q];
-  const int l = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (Q.skip || out[q].fallback) return;
   if (l < 2 && !out[q].subst) return;
   const int V = Q.n + 1;
@@ -349,28 +353,68 @@ __global__ void __launch_bounds__(128) pool_special_kernel(const PQ* __restrict_
   double xs[kD];
 #pragma unroll
   for (int k = 0; k < kD; ++k) xs[k] = base[static_cast<int64_t>(s) * kD + k];
-  const int64_t lb = (static_cast<int64_t>(q) * 4 + l) * kSpecCap;
+  int32_t* cl = cand + (static_cast<int64_t>(q) * 4 + l) * kCandCap;
   int len = 0;
   for (int b0 = 0; b0 < V; b0 += 32) {
     const int x = b0 + lane;
-    bool keep = false;
-    double c = 0.0, t = 0.0;
-    if (x < V && x != s) {
+    bool may = x < V && x != s;
+    if (may) {
       double xx[kD];
 #pragma unroll
       for (int k = 0; k < kD; ++k) xx[k] = base[static_cast<int64_t>(x) * kD + k];
       const double* from = outgoing ? xs : xx;
       const double* to = outgoing ? xx : xs;
-      bool may = true;
       for (int k = 0; k < 3; ++k) {  // di_may_connect (di_graph.cu)
         const double D = to[k] - from[k];
         if (D > bound || -D > bound) may = false;
       }
       if (may) may = !di_cost_exceeds(di_coef(from, to, P), radius);
-      if (may) {
-        c = di_cost_tau(from, to, P, &t, radius);
-        keep = c <= radius;
-      }
+    }
+    const uint32_t m = __ballot_sync(kFull, may);
+    const int slot = len + __popc(m & ((1u << lane) - 1u));
+    if (may && slot < kCandCap) cl[slot] = x;
+    len += __popc(m);
+  }
+  if (lane == 0) {
+    out[q].spec_len[l] = len;  // (candidates here; the solve kernel overwrites it)
+    if (len > kCandCap) out[q].fallback = 1;
+  }
+}
+
+__global__ void __launch_bounds__(128) pool_special_kernel(const PQ* __restrict__ pq, DiParams P, double radius,
+                                                           const double* __restrict__ qcoords,
+                                                           const int32_t* __restrict__ cand,
+                                                           int32_t* __restrict__ scol, double* __restrict__ scost,
+                                                           double* __restrict__ stau, int32_t* __restrict__ sp_code,
+                                                           uint16_t* __restrict__ sp_j, PQOut* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int q = gw >> 2, l = gw & 3;
+  const PQ Q = pq[q];
+  if (Q.skip || out[q].fallback) return;
+  if (l < 2 && !out[q].subst) return;
+  const int s = l < 2 ? Q.n - 1 : Q.n;
+  const bool outgoing = (l & 1) == 0;
+  const double* base = qcoords + Q.node_off * kD;
+  double xs[kD];
+#pragma unroll
+  for (int k = 0; k < kD; ++k) xs[k] = base[static_cast<int64_t>(s) * kD + k];
+  const int32_t* cl = cand + (static_cast<int64_t>(q) * 4 + l) * kCandCap;
+  const int nc = out[q].spec_len[l];
+  const int64_t lb = (static_cast<int64_t>(q) * 4 + l) * kSpecCap;
+  int len = 0;
+  for (int b0 = 0; b0 < nc; b0 += 32) {
+    const int j = b0 + lane;
+    bool keep = false;
+    double c = 0.0, t = 0.0;
+    int x = 0;
+    if (j < nc) {
+      x = cl[j];
+      double xx[kD];
+#pragma unroll
+      for (int k = 0; k < kD; ++k) xx[k] = base[static_cast<int64_t>(x) * kD + k];
+      c = outgoing ? di_cost_tau(xs, xx, P, &t, radius) : di_cost_tau(xx, xs, P, &t, radius);
+      keep = c <= radius;
     }
     const uint32_t m = __ballot_sync(kFull, keep);
     const int slot = len + __popc(m & ((1u << lane) - 1u));
@@ -378,9 +422,15 @@ __global__ void __launch_bounds__(128) pool_special_kernel(const PQ* __restrict_
       scol[lb + slot] = x;
       scost[lb + slot] = c;
       stau[lb + slot] = t;
+      // per-vertex lookup for the rows kernel: bit l, and the entry of the
+      // edges the vertex's in-row takes from g (l = 0) or init (l = 2)
+      atomicOr(sp_code + Q.node_off + x, 1 << l);
+      if (l == 0) sp_j[2 * (Q.node_off + x)] = static_cast<uint16_t>(slot);
+      if (l == 2) sp_j[2 * (Q.node_off + x) + 1] = static_cast<uint16_t>(slot);
     }
     len += __popc(m);
   }
+  __syncwarp();
   if (lane == 0) {
     out[q].spec_len[l] = len;
     if (len > kSpecCap) out[q].fallback = 1;
@@ -466,109 +516,141 @@ __global__ void __launch_bounds__(1024) pool_layout_kernel(const PQ* __restrict_
   }
 }
 
-__device__ __forceinline__ int find_sorted(const int32_t* a, int len, int x) {
-  int lo = 0, hi = len;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1; else hi = mid;
-  }
-  return (lo < len && a[lo] == x) ? lo : -1;
-}
-
-// Every derived row, warp per (query, vertex).  A pool vertex's rows are its
+// Every derived row: an 8-lane group per (query, vertex), four vertices per
+// warp (their dependent load chains overlap).  A pool vertex's rows are its
 // pool rows with non-member entries dropped (ballot compaction keeps their
 // ascending order, ranks being monotone) and member sources/targets mapped to
 // ranks, then the special vertices (n-1 before n) where the special rows hold
-// the edge.  A special vertex copies its own rows.
+// the edge (sp_code / sp_j).  A special vertex copies its own rows.  The
+// outputs are written with streaming stores: they are read by the solve,
+// not here, and must not evict the pool graph from L2.
+constexpr int kRowTile = 512;  // vertices per block
+template <typename T>
+__device__ __forceinline__ void row_store(T* p, T v, bool stream) {
+  if (stream) {
+    __stcs(p, v);
+  } else {
+    *p = v;
+  }
+}
+template <int kRowLanes, bool kStream>
 __global__ void __launch_bounds__(256) pool_rows_kernel(
-    const PQ* __restrict__ pq, const PQOut* __restrict__ po, int Kc, const int64_t* __restrict__ pin_ptr,
+    const PQ* __restrict__ pq, const PQOut* __restrict__ po, int Kc, int stage_rank, const int64_t* __restrict__ pin_ptr,
     const int32_t* __restrict__ pin_col, const double* __restrict__ pin_cost, const double* __restrict__ pin_tau,
     const int64_t* __restrict__ pout_ptr, const int32_t* __restrict__ pout_col, const uint16_t* __restrict__ rank_of,
     const int32_t* __restrict__ sel, const int32_t* __restrict__ scol, const double* __restrict__ scost,
-    const double* __restrict__ stau, const int64_t* __restrict__ in_start, int64_t* __restrict__ in_end,
+    const double* __restrict__ stau, const int32_t* __restrict__ sp_code, const uint16_t* __restrict__ sp_j,
+    const int64_t* __restrict__ in_start, int64_t* __restrict__ in_end,
     const int64_t* __restrict__ out_start, int64_t* __restrict__ out_end, int32_t* __restrict__ in_col,
     double* __restrict__ in_cost, double* __restrict__ in_tau, int32_t* __restrict__ out_col) {
+  extern __shared__ uint16_t rank_s[];
   const int q = blockIdx.y;
   const PQ Q = pq[q];
-  if (Q.skip) return;
-  const PQOut& O = po[q];
-  if (O.fallback) return;
+  if (Q.skip || po[q].fallback) return;
+  // The query's rank map in shared memory (the in-/out-row gathers hit it
+  // once per pool edge); the block then walks kRowTile of its vertices.
+  const uint16_t* rk = rank_of + static_cast<int64_t>(q) * Kc;
+  if (stage_rank) {
+    for (int i = threadIdx.x; i < Kc; i += blockDim.x) rank_s[i] = rk[i];
+    __syncthreads();
+    rk = rank_s;
+  }
   const int lane = threadIdx.x & 31;
-  const int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int grp = lane / kRowLanes, gl = lane % kRowLanes;
+  const uint32_t gshift = static_cast<uint32_t>(grp * kRowLanes);
   const int n = Q.n;
-  if (x > n) return;
+  const int rows_per_pass = (blockDim.x >> 5) * (32 / kRowLanes);
+  for (int x0 = blockIdx.x * kRowTile; x0 < blockIdx.x * kRowTile + kRowTile && x0 <= n; x0 += rows_per_pass) {
+  const int x = x0 + (threadIdx.x >> 5) * (32 / kRowLanes) + grp;
+  const bool subst = po[q].subst != 0;
   int32_t* icol = in_col + Q.in_off;
   double* icost = in_cost + Q.in_off;
   double* itau = in_tau + Q.in_off;
   int32_t* ocol = out_col + Q.out_off;
   const int64_t lb = static_cast<int64_t>(q) * 4 * kSpecCap;
-  const bool subst = O.subst != 0;
-  const int64_t is = in_start[Q.node_off + x], os = out_start[Q.node_off + x];
-  if (x == n || (subst && x == n - 1)) {
+  const bool live = x <= n;
+  const bool special = live && (x == n || (subst && x == n - 1));
+  int64_t is = 0, os = 0, ie0 = 0, oe0 = 0;
+  int li = 0, lo = 0, code = 0;
+  if (live) {
+    is = in_start[Q.node_off + x];
+    os = out_start[Q.node_off + x];
+    if (special) {
+      const int l = x == n ? 2 : 0;
+      li = po[q].spec_len[l + 1];
+      lo = po[q].spec_len[l];
+    } else {
+      const int p = sel[Q.node_off + x];
+      ie0 = pin_ptr[p];
+      li = static_cast<int>(pin_ptr[p + 1] - ie0);
+      oe0 = pout_ptr[p];
+      lo = static_cast<int>(pout_ptr[p + 1] - oe0);
+      code = sp_code[Q.node_off + x];
+    }
+  }
+  if (special) {  // (the group copies the special row; group-uniform branch)
     const int l = x == n ? 2 : 0;
-    const int li = O.spec_len[l + 1], lo = O.spec_len[l];
-    for (int j = lane; j < li; j += 32) {
-      icol[is + j] = scol[lb + (l + 1) * kSpecCap + j];
-      icost[is + j] = scost[lb + (l + 1) * kSpecCap + j];
-      itau[is + j] = stau[lb + (l + 1) * kSpecCap + j];
+    for (int j = gl; j < li; j += kRowLanes) {
+      row_store(icol + is + j, scol[lb + (l + 1) * kSpecCap + j], kStream);
+      row_store(icost + is + j, scost[lb + (l + 1) * kSpecCap + j], kStream);
+      row_store(itau + is + j, stau[lb + (l + 1) * kSpecCap + j], kStream);
     }
-    for (int j = lane; j < lo; j += 32) ocol[os + j] = scol[lb + l * kSpecCap + j];
-    if (lane == 0) {
-      in_end[Q.node_off + x] = is + li;
-      out_end[Q.node_off + x] = os + lo;
-    }
-    return;
-  }
-  const int p = sel[Q.node_off + x];
-  const uint16_t* rk = rank_of + static_cast<int64_t>(q) * Kc;
-  {  // in-row
-    const int64_t e0 = pin_ptr[p], e1 = pin_ptr[p + 1];
-    int64_t w = is;
-    for (int64_t b = e0; b < e1; b += 32) {
-      const int64_t e = b + lane;
-      uint16_t r = kNoRank;
-      if (e < e1) r = rk[pin_col[e]];
-      const bool keep = r != kNoRank;
-      const uint32_t m = __ballot_sync(kFull, keep);
-      if (keep) {
-        const int64_t slot = w + __popc(m & ((1u << lane) - 1u));
-        icol[slot] = r;
-        icost[slot] = pin_cost[e];
-        itau[slot] = pin_tau[e];
-      }
-      w += __popc(m);
-    }
-    if (lane == 0) {  // edges from the special vertices: g (n-1) first, then init (n)
-      for (int l = subst ? 0 : 2; l <= 2; l += 2) {
-        const int j = find_sorted(scol + lb + l * kSpecCap, O.spec_len[l], x);
-        if (j >= 0) {
-          icol[w] = l == 0 ? n - 1 : n;
-          icost[w] = scost[lb + l * kSpecCap + j];
-          itau[w] = stau[lb + l * kSpecCap + j];
-          ++w;
-        }
-      }
-      in_end[Q.node_off + x] = w;
+    for (int j = gl; j < lo; j += kRowLanes) row_store(ocol + os + j, scol[lb + l * kSpecCap + j], kStream);
+    li = lo = 0;  // (no pool rows to scan)
+    if (gl == 0) {
+      const int l2 = x == n ? 2 : 0;
+      row_store(in_end + Q.node_off + x, is + po[q].spec_len[l2 + 1], kStream);
+      row_store(out_end + Q.node_off + x, os + po[q].spec_len[l2], kStream);
     }
   }
-  {  // out-row
-    const int64_t e0 = pout_ptr[p], e1 = pout_ptr[p + 1];
-    int64_t w = os;
-    for (int64_t b = e0; b < e1; b += 32) {
-      const int64_t e = b + lane;
-      uint16_t r = kNoRank;
-      if (e < e1) r = rk[pout_col[e]];
-      const bool keep = r != kNoRank;
-      const uint32_t m = __ballot_sync(kFull, keep);
-      if (keep) ocol[w + __popc(m & ((1u << lane) - 1u))] = r;
-      w += __popc(m);
+  int lmax = li > lo ? li : lo;
+  for (int o = kRowLanes; o < 32; o <<= 1) {  // the longest row of the warp
+    const int t = __shfl_xor_sync(kFull, lmax, o);
+    lmax = t > lmax ? t : lmax;
+  }
+  int wi = 0, wo = 0;
+  const uint32_t below = (1u << gl) - 1u;
+  for (int b0 = 0; b0 < lmax; b0 += kRowLanes) {
+    const int j = b0 + gl;
+    const int32_t ycol = j < li ? __ldg(pin_col + ie0 + j) : -1;
+    const int32_t vcol = j < lo ? __ldg(pout_col + oe0 + j) : -1;
+    const uint16_t ri = ycol >= 0 ? rk[ycol] : kNoRank;
+    const uint16_t ro = vcol >= 0 ? rk[vcol] : kNoRank;
+    constexpr uint32_t kGroupMask = kRowLanes == 32 ? 0xffffffffu : ((1u << kRowLanes) - 1u);
+    const uint32_t mi = (__ballot_sync(kFull, ri != kNoRank) >> gshift) & kGroupMask;
+    const uint32_t mo = (__ballot_sync(kFull, ro != kNoRank) >> gshift) & kGroupMask;
+    if (ri != kNoRank) {
+      const int64_t slot = is + wi + __popc(mi & below);
+      row_store(icol + slot, static_cast<int32_t>(ri), kStream);
+      row_store(icost + slot, __ldg(pin_cost + ie0 + j), kStream);
+      row_store(itau + slot, __ldg(pin_tau + ie0 + j), kStream);
     }
-    if (lane == 0) {  // edges into the special vertices
-      for (int l = subst ? 1 : 3; l <= 3; l += 2) {
-        if (find_sorted(scol + lb + l * kSpecCap, O.spec_len[l], x) >= 0) ocol[w++] = l == 1 ? n - 1 : n;
-      }
-      out_end[Q.node_off + x] = w;
+    if (ro != kNoRank) row_store(ocol + os + wo + __popc(mo & below), static_cast<int32_t>(ro), kStream);
+    wi += __popc(mi);
+    wo += __popc(mo);
+  }
+  if (live && !special && gl == 0) {
+    int64_t w = is + wi;
+    if (subst && (code & 1)) {  // g -> x (list 0), then init -> x (list 2)
+      const int j = sp_j[2 * (Q.node_off + x)];
+      row_store(icol + w, n - 1, kStream);
+      row_store(icost + w, scost[lb + j], kStream);
+      row_store(itau + w, stau[lb + j], kStream);
+      ++w;
     }
+    if (code & 4) {
+      const int j = sp_j[2 * (Q.node_off + x) + 1];
+      row_store(icol + w, n, kStream);
+      row_store(icost + w, scost[lb + 2 * kSpecCap + j], kStream);
+      row_store(itau + w, stau[lb + 2 * kSpecCap + j], kStream);
+      ++w;
+    }
+    row_store(in_end + Q.node_off + x, w, kStream);
+    int64_t v = os + wo;
+    if (subst && (code & 2)) row_store(ocol + v++, n - 1, kStream);  // x -> g (list 1), then x -> init (list 3)
+    if (code & 8) row_store(ocol + v++, n, kStream);
+    row_store(out_end + Q.node_off + x, v, kStream);
+  }
   }
 }
 
@@ -762,8 +844,20 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
   *max_V = 0;
   *max_nb = 0;
   std::vector<PQ> pq(count);
-  std::vector<double> box_lo, box_hi, goal_lo(static_cast<size_t>(count) * kD), goal_hi(goal_lo.size()),
-      inits(goal_lo.size());
+  // The scene arrays are packed straight into pinned memory (one async copy
+  // each at full link speed); the call synchronises before it returns, so
+  // the context's staging buffer is free again for the next call.
+  int64_t all_boxes = 0;
+  for (int q = 0; q < count; ++q) all_boxes += std::max(problems[q].scene.num_boxes, 0);
+  const size_t nbox_d = static_cast<size_t>(std::max<int64_t>(all_boxes, 1)) * kD;
+  const size_t nq_d = static_cast<size_t>(count) * kD;
+  int rc0 = ctx->pool_pinned.reserve(sizeof(double) * (2 * nbox_d + 3 * nq_d));
+  if (rc0) return rc0;
+  double* h_blo = static_cast<double*>(ctx->pool_pinned.ptr);
+  double* h_bhi = h_blo + nbox_d;
+  double* h_glo = h_bhi + nbox_d;
+  double* h_ghi = h_glo + nq_d;
+  double* h_init = h_ghi + nq_d;
   int Kc = 0, eligible = 0, max_nbp = 0, max_n = 0;
   int64_t box_total = 0, node_total = 0;
   for (int q = 0; q < count; ++q) {
@@ -783,11 +877,11 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
     Kc = std::max(Kc, pool_need(pr));
     max_nbp = std::max(max_nbp, Q.nb);
     max_n = std::max(max_n, pr.n);
-    box_lo.insert(box_lo.end(), pr.scene.box_lo, pr.scene.box_lo + static_cast<size_t>(Q.nb) * kD);
-    box_hi.insert(box_hi.end(), pr.scene.box_hi, pr.scene.box_hi + static_cast<size_t>(Q.nb) * kD);
-    std::copy(pr.scene.goal_lo, pr.scene.goal_lo + kD, goal_lo.begin() + static_cast<size_t>(q) * kD);
-    std::copy(pr.scene.goal_hi, pr.scene.goal_hi + kD, goal_hi.begin() + static_cast<size_t>(q) * kD);
-    std::copy(pr.init, pr.init + kD, inits.begin() + static_cast<size_t>(q) * kD);
+    std::memcpy(h_blo + box_total * kD, pr.scene.box_lo, sizeof(double) * static_cast<size_t>(Q.nb) * kD);
+    std::memcpy(h_bhi + box_total * kD, pr.scene.box_hi, sizeof(double) * static_cast<size_t>(Q.nb) * kD);
+    std::memcpy(h_glo + static_cast<size_t>(q) * kD, pr.scene.goal_lo, sizeof(double) * kD);
+    std::memcpy(h_ghi + static_cast<size_t>(q) * kD, pr.scene.goal_hi, sizeof(double) * kD);
+    std::memcpy(h_init + static_cast<size_t>(q) * kD, pr.init, sizeof(double) * kD);
     box_total += Q.nb;
     node_total += Q.n + 1;
   }
@@ -808,9 +902,9 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       const size_t o_po = c.take<PQOut>(count);
       const size_t o_blo = c.take<double>(std::max<int64_t>(box_total, 1) * kD);
       const size_t o_bhi = c.take<double>(std::max<int64_t>(box_total, 1) * kD);
-      const size_t o_glo = c.take<double>(goal_lo.size());
-      const size_t o_ghi = c.take<double>(goal_hi.size());
-      const size_t o_init = c.take<double>(inits.size());
+      const size_t o_glo = c.take<double>(nq_d);
+      const size_t o_ghi = c.take<double>(nq_d);
+      const size_t o_init = c.take<double>(nq_d);
       const size_t o_flag = c.take<uint8_t>(static_cast<size_t>(count) * Kc);
       const size_t o_rank = c.take<uint16_t>(static_cast<size_t>(count) * Kc);
       const size_t o_sel = c.take<int32_t>(node_total);
@@ -818,6 +912,9 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       const size_t o_scol = c.take<int32_t>(static_cast<size_t>(count) * 4 * kSpecCap);
       const size_t o_scost = c.take<double>(static_cast<size_t>(count) * 4 * kSpecCap);
       const size_t o_stau = c.take<double>(static_cast<size_t>(count) * 4 * kSpecCap);
+      const size_t o_cand = c.take<int32_t>(static_cast<size_t>(count) * 4 * kCandCap);
+      const size_t o_spc = c.take<int32_t>(node_total);
+      const size_t o_spj = c.take<uint16_t>(2 * node_total);
       const size_t o_is = c.take<int64_t>(node_total);
       const size_t o_ie = c.take<int64_t>(node_total);
       const size_t o_os = c.take<int64_t>(node_total);
@@ -840,6 +937,9 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       auto* d_scol = reinterpret_cast<int32_t*>(B + o_scol);
       auto* d_scost = reinterpret_cast<double*>(B + o_scost);
       auto* d_stau = reinterpret_cast<double*>(B + o_stau);
+      auto* d_cand = reinterpret_cast<int32_t*>(B + o_cand);
+      auto* d_spc = reinterpret_cast<int32_t*>(B + o_spc);
+      auto* d_spj = reinterpret_cast<uint16_t*>(B + o_spj);
       auto* d_is = reinterpret_cast<int64_t*>(B + o_is);
       auto* d_ie = reinterpret_cast<int64_t*>(B + o_ie);
       auto* d_os = reinterpret_cast<int64_t*>(B + o_os);
@@ -851,11 +951,11 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       };
       timer.mark();
       if ((rc = put(d_pq, pq.data(), sizeof(PQ) * count)) ||
-          (rc = put(d_blo, box_lo.data(), sizeof(double) * box_lo.size())) ||
-          (rc = put(d_bhi, box_hi.data(), sizeof(double) * box_hi.size())) ||
-          (rc = put(d_glo, goal_lo.data(), sizeof(double) * goal_lo.size())) ||
-          (rc = put(d_ghi, goal_hi.data(), sizeof(double) * goal_hi.size())) ||
-          (rc = put(d_init, inits.data(), sizeof(double) * inits.size())))
+          (rc = put(d_blo, h_blo, sizeof(double) * box_total * kD)) ||
+          (rc = put(d_bhi, h_bhi, sizeof(double) * box_total * kD)) ||
+          (rc = put(d_glo, h_glo, sizeof(double) * nq_d)) ||
+          (rc = put(d_ghi, h_ghi, sizeof(double) * nq_d)) ||
+          (rc = put(d_init, h_init, sizeof(double) * nq_d)))
         return rc;
       const double* P = static_cast<const double*>(pool->pts.ptr);
       const int stage_cap = 2048;  // boxes staged in shared memory up to 2048 * 96 B
@@ -891,12 +991,15 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       pool_subst_kernel<<<count, 256, 0, s>>>(d_pq, Kc, d_blo, d_bhi, d_glo, d_ghi, pr, d_rank, d_sel, d_qc, d_po);
       pool_init_kernel<<<count, 256, 0, s>>>(d_pq, d_init, d_qc, d_po);
       timer.mark();
-      pool_special_kernel<<<count, 128, 0, s>>>(d_pq, DP, di_prefilter_bound(DP, pool->radius), pool->radius, d_qc,
-                                                d_scol, d_scost, d_stau, d_po);
+      GMT_CUDA(cudaMemsetAsync(d_spc, 0, sizeof(int32_t) * node_total, s));
+      pool_special_cand_kernel<<<(4 * count + 7) / 8, 256, 0, s>>>(d_pq, DP, di_prefilter_bound(DP, pool->radius),
+                                                                    pool->radius, d_qc, d_cand, d_po);
+      pool_special_kernel<<<count, 128, 0, s>>>(d_pq, DP, pool->radius, d_qc, d_cand, d_scol, d_scost, d_stau, d_spc,
+                                                d_spj, d_po);
       timer.mark();
       pool_layout_kernel<<<count, 1024, 0, s>>>(d_pq, pool->in.ptr, pool->out.ptr, d_sel, d_is, d_os, d_po);
       GMT_CUDA(cudaGetLastError());
-      ctx->launches += 4;
+      ctx->launches += 5;
       GMT_CUDA(cudaMemcpyAsync(po.data(), d_po, sizeof(PQOut) * count, cudaMemcpyDeviceToHost, s));
       GMT_CUDA(cudaStreamSynchronize(s));
       int64_t tin = 0, tout = 0;
@@ -921,9 +1024,24 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       auto* d_ocol = reinterpret_cast<int32_t*>(R + o_ocol);
       if ((rc = put(d_pq, pq.data(), sizeof(PQ) * count))) return rc;
       timer.mark();
-      pool_rows_kernel<<<dim3((max_n + 1 + 7) / 8, count), 256, 0, s>>>(
-          d_pq, d_po, Kc, pool->in.ptr, pool->in.col, pool->in.cost, pool->in.tau, pool->out.ptr, pool->out.col,
-          d_rank, d_sel, d_scol, d_scost, d_stau, d_is, d_ie, d_os, d_oe, d_icol, d_icost, d_itau, d_ocol);
+      const size_t rsm = sizeof(uint16_t) * static_cast<size_t>(Kc);
+      const int stage_rank = rsm <= 96 * 1024 ? 1 : 0;
+      static const int variant = [] {
+        const char* e = std::getenv("GMT_ROWS_VARIANT");
+        return e ? std::atoi(e) : 0;
+      }();
+      auto rows_kern = variant == 1 ? pool_rows_kernel<8, true>
+                       : variant == 2 ? pool_rows_kernel<16, false>
+                       : variant == 3 ? pool_rows_kernel<16, true>
+                       : variant == 4 ? pool_rows_kernel<32, false>
+                                      : pool_rows_kernel<8, false>;
+      if (stage_rank && rsm > 48 * 1024)
+        GMT_CUDA(cudaFuncSetAttribute(rows_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(rsm)));
+      rows_kern<<<dim3((max_n + 1 + kRowTile - 1) / kRowTile, count), 256, stage_rank ? rsm : 0, s>>>(
+          d_pq, d_po, Kc, stage_rank, pool->in.ptr, pool->in.col, pool->in.cost, pool->in.tau, pool->out.ptr, pool->out.col,
+          d_rank, d_sel, d_scol, d_scost, d_stau, d_spc, d_spj, d_is, d_ie, d_os, d_oe, d_icol, d_icost, d_itau,
+          d_ocol);
       timer.mark();
       pool_desc_kernel<<<(count + 127) / 128, 128, 0, s>>>(d_pq, d_po, count, pool->radius, DP, d_qc, d_blo, d_bhi,
                                                            d_glo, d_ghi, d_is, d_ie, d_os, d_oe, d_icol, d_icost,
@@ -1010,7 +1128,7 @@ static int batch_from_derived(gmt_ctx* ctx, gmt_batch* b, const gmt_problem* pro
   // (the shape gmt_batch_create picks: 2-CTA clusters for a few kinodynamic
   // queries, one CTA each once they fill the SMs several times over)
   b->cluster = ctx->batch_cluster ? ctx->batch_cluster : (kino && J < 4 * ctx->sm_count ? 2 : 1);
-  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 || kino ? 512 : 256);
+  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
   int rc = plan_smem(ctx, max_V, d, max_nb, b->cluster, &b->smem, &b->obs);
   if (rc) return rc;
   rc = carve_results(b->res, J, b->node_off.data(), tree_stats, tree_stats, b->results, &b->scalars,

@@ -91,6 +91,7 @@ struct CtaShared {
   unsigned long long checks_acc;  // rank 0: cluster-wide checks of this pass
   int32_t added_acc;              // rank 0: cluster-wide additions of this pass
   int32_t feasible;
+  int32_t vfull;  // D = 6: every box spans [0, 1] on the three velocity axes
   // Loop state kept in shared memory rather than in every thread's
   // registers (the solve is register-bound): the threshold index i, the
   // pass number, the running check total (tid 0), per-warp check / commit
@@ -107,12 +108,18 @@ struct CtaShared {
 // hi + m (the separation bounds) when the boxes are staged in shared memory.
 // idx (may be null): box i of this view is box idx[i] of the arrays (a
 // per-edge list of the boxes that survive the polyline's bounding box).
+// full (may be null): per box, the axes k with lo <= 0 and hi >= 1.  Once
+// both endpoints are known to lie in the unit cube such an axis can neither
+// separate a segment from the box nor narrow its slab interval: its clamped
+// interval is [0, 1] (fl(lo - a) <= 0 <= a and fl(hi - a) >= fl(b - a) by
+// monotone rounding), and dk == 0 leaves a inside [lo, hi].
 struct Boxes {
   const double* lo;
   const double* hi;
   const double* lom;
   const double* him;
   const uint16_t* idx;
+  const uint32_t* full;
   int bs;
   int as;
   int count;
@@ -352,9 +359,11 @@ __device__ bool polyline_free_warp(const DevInstance& I, int d, const Boxes& bx,
 template <int D>
 __device__ __forceinline__ bool seg_box_hit(const double* a, const double* b, int d_rt, const Boxes& bx, int box) {
   const int d = dims<D>(d_rt);
+  const uint32_t full = bx.full ? bx.full[box] : 0u;  // (the caller has checked the cube)
 #pragma unroll
   for (int k = 0; k < (D > 0 ? D : kMaxSolveDim); ++k) {
     if (D == 0 && k >= d) break;
+    if ((full >> k) & 1u) continue;
     const double lo = bx.lom ? bx.lom[box * bx.bs + k * bx.as] : bx.lo[box * bx.bs + k * bx.as] - kSepMargin;
     const double hi = bx.him ? bx.him[box * bx.bs + k * bx.as] : bx.hi[box * bx.bs + k * bx.as] + kSepMargin;
     const double x = a[k], y = b[k];
@@ -364,6 +373,7 @@ __device__ __forceinline__ bool seg_box_hit(const double* a, const double* b, in
 #pragma unroll
   for (int k = 0; k < (D > 0 ? D : kMaxSolveDim); ++k) {
     if (D == 0 && k >= d) break;
+    if ((full >> k) & 1u) continue;
     const double ak = a[k];
     const double dk = __dsub_rn(b[k], ak);
     const double l = bx.lo[box * bx.bs + k * bx.as], h = bx.hi[box * bx.bs + k * bx.as];
@@ -393,12 +403,14 @@ __device__ __forceinline__ bool seg_box_hit(const double* a, const double* b, in
 template <int D>
 __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int from, int to,
                                     double tau, int lane, double* seg, double* tab = nullptr,
-                                    int tab_cap = 0, uint16_t* cull = nullptr, int cull_cap = 0) {
+                                    int tab_cap = 0, uint16_t* cull = nullptr, int cull_cap = 0,
+                                    bool staged = false, bool vfull = false) {
   // Only the generic-dimension kernel can see a 12D quadrotor instance.
   const bool quad = D == 0 && I.steering == GMT_STEER_QUADROTOR;
   const int dim = quad ? kQuadDim : kDiDim;
-  const double* x0 = I.coords + static_cast<int64_t>(from) * dim;
-  const double* x1 = I.coords + static_cast<int64_t>(to) * dim;
+  // staged: the caller holds the endpoints in seg[0..dim) and seg[16..16+dim)
+  const double* x0 = staged ? seg : I.coords + static_cast<int64_t>(from) * dim;
+  const double* x1 = staged ? seg + 16 : I.coords + static_cast<int64_t>(to) * dim;
   if (tau == 0.0) return point_free_warp<D>(x0, dim, bx, lane, seg);
   const int M = I.kin_segments;
   QuadParams QP;
@@ -426,6 +438,14 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
     // di_coord recomputes identically for every coordinate -- the table
     // entries are the very operations of di_coord / quad_coord.
     __syncwarp();
+    if (lane < dim) {  // the end points are waypoints 0 and M (and free seg for scratch)
+      const double a = x0[lane], b = x1[lane];
+      tab[lane] = a;
+      tab[M * dim + lane] = b;
+    }
+    __syncwarp();
+    x0 = tab;
+    x1 = tab + M * dim;
     if (quad) {
       if (lane < 4) quad_chain_lambda(x0, x1, tau, lane, QP, seg + 8 * lane, seg + 8 * lane + 4);
     } else if (lane < 3) {
@@ -443,10 +463,8 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
     for (int e = lane; e < (M + 1) * dim; e += kWarp) {
       const int k = e / dim, i = e - k * dim;
       double v;
-      if (k == 0) {
-        v = x0[i];
-      } else if (k == M) {
-        v = x1[i];
+      if (k == 0 || k == M) {
+        v = tab[e];
       } else if (quad) {
         int c, ci;
         quad_locate(i, &c, &ci);
@@ -459,7 +477,17 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
           v = di_add(x0[a], di_mul(t, di_add(v0, di_mul(t, di_add(c2, di_mul(t, c3))))));
         } else {
           const double vv = di_add(v0, di_mul(t, di_add(di_mul(2.0, c2), di_mul(t, di_mul(3.0, c3)))));
-          v = di_mul(0.5, di_add(di_div(vv, DP.vmax), 1.0));
+          const double av = vv < 0.0 ? -vv : vv;
+          if (vfull && av <= DP.vmax * (1.0 - 1e-14)) {
+            // Every box spans the velocity axes, so this coordinate only feeds
+            // the cube test, and |v| < vmax puts s = (v / vmax + 1) / 2 in
+            // [0, 1] for certain: no division (the value itself is never read).
+            v = 0.5;
+          } else if (vfull && av >= DP.vmax * (1.0 + 1e-14)) {
+            v = -1.0;  // outside [0, 1] for certain (the edge leaves the cube)
+          } else {
+            v = di_mul(0.5, di_add(di_div(vv, DP.vmax), 1.0));
+          }
         }
       }
       tab[e] = v;
@@ -502,8 +530,10 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
         bool meets = b < bx.count;
         const int bc = meets ? b : 0;
         if constexpr (D > 0) {
+          const uint32_t full = bx.full ? bx.full[bc] : 0u;
 #pragma unroll
           for (int k = 0; k < D; ++k) {
+            if ((full >> k) & 1u) continue;
             const double lo = bx.lom ? bx.lom[bc * bx.bs + k * bx.as] : bx.lo[bc * bx.bs + k * bx.as] - kSepMargin;
             const double hi = bx.him ? bx.him[bc * bx.bs + k * bx.as] : bx.hi[bc * bx.bs + k * bx.as] + kSepMargin;
             meets = meets && !(pmx[k] < lo || pmn[k] > hi);
@@ -547,6 +577,132 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
     if (i < dim) seg[lane] = quad ? quad_coord(x0, x1, tau, s + k, i, QP) : di_coord(x0, x1, tau, s + k, i, DP);
     __syncwarp();
     if (!segment_free_staged<D>(dim, bx, lane, seg)) return false;
+  }
+  return true;
+}
+
+// The double integrator's lazy check on a 16-lane group (a half warp), so
+// the two candidates a batched warp scans are checked concurrently: the same
+// steps as kino_edge_free_warp's table path (waypoint table from the cubic
+// coefficients, cube test, polyline bounding-box cull, one lane per
+// (segment, box) pair through the reference's clip) with group-masked votes.
+// seg: the group's 32 staged doubles (a = [0..6), b = [16..22)); tab: its
+// waypoint table ((M + 1) * 6 <= 64); cull: its box list.
+__device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double tau, int gl, uint32_t gmask,
+                                  int gbase, double* seg, double* tab, uint16_t* cull, int cull_cap, bool vfull) {
+  constexpr int G = 16, dim = kDiDim;
+  const int M = I.kin_segments;
+  DiParams DP;
+  DP.vmax = I.kin_p[0];
+  DP.weight = I.kin_p[1];
+  DP.segments = M;
+  DP.reserved = 0;
+  if (tau == 0.0) {  // point_free(x0) (the degenerate edge's single state)
+    bool cube = true;
+    if (gl < dim) cube = !(seg[gl] < 0.0 || seg[gl] > 1.0);
+    if (!__all_sync(gmask, cube)) return false;
+    bool in = false;
+    for (int b = gl; b < bx.count && !in; b += G) in = box_has<6>(seg, dim, bx, b);
+    return !__any_sync(gmask, in);
+  }
+  if (gl < dim) {
+    tab[gl] = seg[gl];
+    tab[M * dim + gl] = seg[16 + gl];
+  }
+  __syncwarp(gmask);
+  const double* x0 = tab;
+  const double* x1 = tab + M * dim;
+  if (gl < 3) {
+    const double D = di_sub(x1[gl], x0[gl]);
+    const double v0 = di_vel(x0[3 + gl], DP), v1 = di_vel(x1[3 + gl], DP);
+    const double tt = di_mul(tau, tau);
+    seg[gl] = di_sub(di_div(di_mul(3.0, D), tt), di_div(di_add(di_mul(2.0, v0), v1), tau));
+    seg[3 + gl] = di_sub(di_div(di_add(v0, v1), tt), di_div(di_mul(2.0, D), di_mul(tt, tau)));
+  } else if (gl - 2 < M) {
+    const int k = gl - 2;
+    seg[6 + k] = di_div(di_mul(tau, static_cast<double>(k)), static_cast<double>(M));
+  }
+  __syncwarp(gmask);
+  bool incube = true;
+  for (int e = gl + dim; e < M * dim; e += G) {  // interior waypoints (rows 1 .. M-1)
+    const int k = e / dim, i = e - k * dim;
+    const int a = i < 3 ? i : i - 3;
+    const double t = seg[6 + k], c2 = seg[a], c3 = seg[3 + a];
+    const double v0 = di_vel(x0[3 + a], DP);
+    double v;
+    if (i < 3) {
+      v = di_add(x0[a], di_mul(t, di_add(v0, di_mul(t, di_add(c2, di_mul(t, c3))))));
+    } else {
+      const double vv = di_add(v0, di_mul(t, di_add(di_mul(2.0, c2), di_mul(t, di_mul(3.0, c3)))));
+      const double av = vv < 0.0 ? -vv : vv;
+      if (vfull && av <= DP.vmax * (1.0 - 1e-14)) {
+        v = 0.5;  // (see kino_edge_free_warp: only the cube test reads it, and it passes)
+      } else if (vfull && av >= DP.vmax * (1.0 + 1e-14)) {
+        v = -1.0;
+      } else {
+        v = di_mul(0.5, di_add(di_div(vv, DP.vmax), 1.0));
+      }
+    }
+    tab[e] = v;
+    incube = incube && !(v < 0.0 || v > 1.0);
+  }
+  if (gl < dim) {
+    incube = incube && !(x0[gl] < 0.0 || x0[gl] > 1.0) && !(x1[gl] < 0.0 || x1[gl] > 1.0);
+  }
+  if (!__all_sync(gmask, incube)) return false;
+  __syncwarp(gmask);
+  // polyline bounding box -> the boxes it meets (exact-safe cull)
+  if (gl < dim) {
+    double mn = tab[gl], mx = tab[gl];
+    for (int k = 1; k <= M; ++k) {
+      const double x = tab[k * dim + gl];
+      mn = x < mn ? x : mn;
+      mx = x < mx ? mx : x;
+    }
+    seg[gl] = mn;
+    seg[16 + gl] = mx;
+  }
+  __syncwarp(gmask);
+  double pmn[dim], pmx[dim];
+#pragma unroll
+  for (int k = 0; k < dim; ++k) {
+    pmn[k] = seg[k];
+    pmx[k] = seg[16 + k];
+  }
+  Boxes sub = bx;
+  int kept = 0;
+  for (int i0 = 0; i0 < bx.count && kept <= cull_cap; i0 += G) {
+    const int b = i0 + gl;
+    bool meets = b < bx.count;
+    const int bc = meets ? b : 0;
+    const uint32_t full = bx.full ? bx.full[bc] : 0u;
+#pragma unroll
+    for (int k = 0; k < dim; ++k) {
+      if ((full >> k) & 1u) continue;
+      const double lo = bx.lom ? bx.lom[bc * bx.bs + k * bx.as] : bx.lo[bc * bx.bs + k * bx.as] - kSepMargin;
+      const double hi = bx.him ? bx.him[bc * bx.bs + k * bx.as] : bx.hi[bc * bx.bs + k * bx.as] + kSepMargin;
+      meets = meets && !(pmx[k] < lo || pmn[k] > hi);
+    }
+    const uint32_t m = (__ballot_sync(gmask, meets) >> gbase) & 0xffffu;
+    const int at = kept + __popc(m & ((1u << gl) - 1u));
+    if (meets && at < cull_cap) cull[at] = static_cast<uint16_t>(b);
+    kept += __popc(m);
+  }
+  __syncwarp(gmask);
+  if (kept <= cull_cap) {
+    sub.idx = cull;
+    sub.count = kept;
+  }
+  const int nbx = sub.count;
+  const int pairs = M * nbx;
+  for (int p0 = 0; p0 < pairs; p0 += G) {
+    const int p = p0 + gl;
+    bool hit = false;
+    if (p < pairs) {
+      const int sg = p / nbx, bi = p - sg * nbx;
+      hit = seg_box_hit<6>(tab + sg * dim, tab + (sg + 1) * dim, dim, bx, sub.idx ? sub.idx[bi] : bi);
+    }
+    if (__any_sync(gmask, hit)) return false;
   }
   return true;
 }
@@ -621,10 +777,12 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
   constexpr bool kDynamic = CS > 1;  // dynamic row / candidate distribution
   __shared__ double seg_s[kMaxWarps * 32 * kRows];  // per warp: kRows staged segments
   // Kinodynamic waypoint tables (double integrator: D = 6; quadrotor: D = 0).
+  // (batched DI solves check two edges per warp at once: two tables / lists)
   constexpr int kTabCap = D == 6 ? 64 : (D == 0 ? 144 : 1);
-  __shared__ double tab_s[(D == 0 || D == 6) ? kMaxWarps * kTabCap : 1];
+  constexpr int kKinSlots = (D == 6 && kRows == 2) ? 2 : 1;
+  __shared__ double tab_s[(D == 0 || D == 6) ? kMaxWarps * kTabCap * kKinSlots : 1];
   constexpr int kCullCap = (D == 0 || D == 6) ? 64 : 1;  // per-warp surviving-box list
-  __shared__ uint16_t cull_s[kMaxWarps * kCullCap];
+  __shared__ uint16_t cull_s[kMaxWarps * kCullCap * kKinSlots];
 
   const int q = blockIdx.x / CS;
   int rank = 0;
@@ -679,9 +837,26 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
       lom[k * nb + b] = l - kSepMargin;
       him[k * nb + b] = h + kSepMargin;
     }
+    uint32_t* full = reinterpret_cast<uint32_t*>(him + static_cast<size_t>(nb) * d);
+    for (int b = tid; b < nb; b += nt) {
+      uint32_t m = 0u;
+      for (int k = 0; k < d; ++k)
+        if (I.box_lo[b * d + k] <= 0.0 && I.box_hi[b * d + k] >= 1.0) m |= 1u << k;
+      full[b] = m;
+    }
     bxl.lo = lo, bxl.hi = hi, bxl.lom = lom, bxl.him = him, bxl.bs = 1, bxl.as = nb;
+    bxl.full = full;
+    if constexpr (D == 6) {
+      __syncthreads();
+      int vf = 1;
+      for (int b = tid; b < nb; b += nt) vf &= (full[b] & 0x38u) == 0x38u ? 1 : 0;
+      vf = __syncthreads_and(vf);
+      if (tid == 0) sh.vfull = vf;
+    }
   } else {
     bxl.lo = I.box_lo, bxl.hi = I.box_hi, bxl.lom = nullptr, bxl.him = nullptr, bxl.bs = d, bxl.as = 1;
+    bxl.full = nullptr;
+    if (tid == 0) sh.vfull = 0;
   }
   bxl.idx = nullptr;
 
@@ -1078,7 +1253,10 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
             }
           }
         }
-        // Both chosen parents' coordinates in flight together.
+        // The chosen in-edge's duration (kinodynamic graphs) and both chosen
+        // parents' coordinates in flight together.
+        double tau_b = 0.0;
+        if ((D == 0 || D == 6) && bo >= 0 && I.in_tau) tau_b = __ldg(I.in_tau + e0 + bo);
         if constexpr (kLanesPerRow >= kMaxSolveDim) {
           if (bo >= 0 && hl < d) segh[hl] = __ldg(I.coords + static_cast<int64_t>(by) * d + hl);
         } else {
@@ -1086,6 +1264,33 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
             segh[t] = __ldg(I.coords + static_cast<int64_t>(by) * d + t);
         }
         __syncwarp();
+        // Batched double-integrator solves: the two candidates are checked
+        // concurrently, one per half warp (their row scans and argmins
+        // already are); the values of half h are its own lanes'.
+        if constexpr (D == 6 && kRows == 2) {
+          if (I.in_tau && (I.kin_segments + 1) * 6 <= kTabCap && I.kin_segments <= 14) {
+            const uint32_t gmask = h ? 0xffff0000u : 0x0000ffffu;
+            if (bo >= 0) {
+              if (hl == 0) atomicAdd(&sh.wchecks[warp], 1);
+              const bool ok = di_edge_free_half(I, bx_s, tau_b, hl, gmask, 16 * h, segh,
+                                                tab_s + warp * kTabCap * 2 + h * kTabCap,
+                                                cull_s + warp * kCullCap * 2 + h * kCullCap, kCullCap, sh.vfull);
+              if (ok && hl == 0) {
+                atomicAdd(&sh.wadded[warp], 1);
+                cost_s[x] = bv;
+                atomicOr(newopen_w + (x >> 5), 1u << (x & 31));
+                R.parent[x] = by;
+                if (R.iter_added) R.iter_added[x] = sh.iter;
+              }
+            }
+            __syncwarp();
+            k = kn;
+            x = xn;
+            e0 = n0;
+            len = nlen;
+            continue;
+          }
+        }
 #pragma unroll 1
         for (int c = 0; c < kRows; ++c) {
           const int src = kLanesPerRow * c;
@@ -1100,10 +1305,13 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
           if (lane == 0) ++sh.wchecks[warp];
           const int32_t pid = I.in_path ? __ldg(I.in_path + bec) : -1;
           auto edge_free = [&](const Boxes& B) -> bool {
-            if ((D == 0 || D == 6) && I.in_tau)  // kinodynamic: regenerated polyline (di.cuh, quad.cuh)
-              return kino_edge_free_warp<D>(I, B, byc, xc, __ldg(I.in_tau + bec), lane, sc,
-                                            tab_s + ((D == 0 || D == 6) ? warp * kTabCap : 0), kTabCap,
-                                            cull_s + warp * kCullCap, kCullCap);
+            if ((D == 0 || D == 6) && I.in_tau) {  // kinodynamic: regenerated polyline (di.cuh, quad.cuh)
+              const double tc = kRows == 1 ? tau_b : __shfl_sync(kFull, tau_b, src);
+              // the endpoints are staged in sc when a lane group can hold them
+              return kino_edge_free_warp<D>(I, B, byc, xc, tc, lane, sc,
+                                            tab_s + ((D == 0 || D == 6) ? warp * kTabCap * kKinSlots : 0), kTabCap,
+                                            cull_s + warp * kCullCap * kKinSlots, kCullCap, true, D == 6 && sh.vfull);
+            }
             if (pid < 0) return segment_free_staged<D>(d, B, lane, sc);  // segment_free (planner.cpp:59)
             return polyline_free_warp<D>(I, d, B, pid, lane, sc);       // polyline_free (planner.cpp:56-58)
           };
@@ -1269,6 +1477,7 @@ __global__ void __launch_bounds__(256) eager_check_kernel(const DevInstance* __r
     b.lom = nullptr;
     b.him = nullptr;
     b.idx = nullptr;
+    b.full = nullptr;
     b.bs = I_s.dim;
     b.as = 1;
     b.count = I_s.num_boxes;
@@ -1319,6 +1528,7 @@ __global__ void __launch_bounds__(256) segment_free_kernel(const double* __restr
   bx.lom = nullptr;
   bx.him = nullptr;
   bx.idx = nullptr;
+  bx.full = nullptr;
   bx.bs = d;
   bx.as = 1;
   bx.count = nb;
@@ -1365,6 +1575,7 @@ __global__ void __launch_bounds__(1024) dijkstra_kernel(const SolveJob* __restri
     b.lom = nullptr;
     b.him = nullptr;
     b.idx = nullptr;
+    b.full = nullptr;
     b.bs = I_s.dim;
     b.as = 1;
     b.count = I_s.num_boxes;

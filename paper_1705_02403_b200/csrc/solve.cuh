@@ -22,7 +22,8 @@ constexpr int kMaxSolveDim = 16;
 //                      parents in HBM and walk them once at the end)
 //   bits   6 x u32[Wp] open, closed, group, newopen, cand, goal
 //   list   u16[32W]    owned group members (P4) / owned candidates (P5)
-//   obs    f64[4*B*d]  boxes lo, hi, lo - m, hi + m, axis-major (SoA), when they fit
+//   obs    f64[4*B*d]  boxes lo, hi, lo - m, hi + m, axis-major (SoA), when they fit,
+//          u32[B]      then each box's mask of "full" axes (lo <= 0 and hi >= 1)
 struct SolveLayout {
   int words;
   int words_pad;
@@ -45,7 +46,8 @@ __host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool o
   L.off_list = off;
   off = align16(off + sizeof(uint16_t) * nodes);
   L.off_obs = off;
-  if (obs_smem) off = align16(off + sizeof(double) * 4 * static_cast<size_t>(nb) * d);
+  if (obs_smem)
+    off = align16(off + sizeof(double) * 4 * static_cast<size_t>(nb) * d + sizeof(uint32_t) * static_cast<size_t>(nb));
   L.total = off;
   return L;
 }

@@ -83,3 +83,30 @@ def test_di_batch_queries(ctx, port):
     b.launch()
     for q, (s, inst) in enumerate(zip(specs, insts)):
         assert not abi.full_parity(b.result(q), ctx.plan(inst))
+
+
+@pytest.mark.parametrize("lam", [1.0, 0.5])
+def test_di_boxes_with_velocity_extent(ctx, port, ref, lam):
+    """Boxes that do not span the whole velocity range (the lazy check then
+    tests the trajectory's velocity coordinates against them too): device
+    plans equal the reference on the injected graph."""
+    spec = P.di_forest(7, 700, radius=2.3)
+    lo, hi = spec.box_lo.copy(), spec.box_hi.copy()
+    lo[::2, 3] = 0.55        # every other pillar only blocks fast +x motion
+    hi[1::3, 4] = 0.45       # some only block -y motion
+    spec.box_lo, spec.box_hi = lo, hi
+    # a few velocity-space slabs over the whole workspace
+    spec.box_lo = np.vstack([spec.box_lo, [[0, 0, 0, 0.93, 0, 0], [0, 0, 0, 0, 0, 0.0]]])
+    spec.box_hi = np.vstack([spec.box_hi, [[1, 1, 1, 1.0, 1, 1], [1, 1, 1, 1, 1, 0.04]]])
+    inst = ctx.build_instance(spec)
+    c, g, _ = inst.download()
+    wc, wg = port.sample_free(spec)
+    wc, wg, ii = port.append_init(wc, wg, spec.init, spec.goal_lo, spec.goal_hi)
+    assert bits(c) == bits(wc)
+    G = port.di_graph(wc, 2.3)
+    want = ref.gmt_plan(spec, wc, len(wg), G, ii, lam, 2.3)
+    got = ctx.plan(inst, lam=lam)
+    assert not abi.full_parity(got, want), abi.full_parity(got, want)
+    b = ctx.batch([inst], lam)
+    b.launch()
+    assert not abi.full_parity(b.result(0), want)
