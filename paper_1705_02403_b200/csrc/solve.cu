@@ -356,8 +356,41 @@ __device__ bool polyline_free_warp(const DevInstance& I, int d, const Boxes& bx,
 // segment_hits_box (space.cpp:60-78) of one segment against one box on a
 // single lane: the exact-safe separation pre-test of segment_free_ab, then
 // the reference's sequential closed slab clip (tmin = 0, tmax = 1).
-template <int D>
+// POS3: every box spans [0, 1] on axes 3.. (the DI velocity axes when the
+// solve's vfull holds): only the three position axes can separate or clip
+// (a full position axis is neutral too, so none is skipped there).
+template <int D, bool POS3 = false>
 __device__ __forceinline__ bool seg_box_hit(const double* a, const double* b, int d_rt, const Boxes& bx, int box) {
+  if constexpr (POS3) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double lo = bx.lom[box * bx.bs + k * bx.as], hi = bx.him[box * bx.bs + k * bx.as];
+      const double x = a[k], y = b[k];
+      if ((x < lo && y < lo) || (x > hi && y > hi)) return false;
+    }
+    double tmin = 0.0, tmax = 1.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double ak = a[k];
+      const double dk = __dsub_rn(b[k], ak);
+      const double l = bx.lo[box * bx.bs + k * bx.as], h = bx.hi[box * bx.bs + k * bx.as];
+      if (dk == 0.0) {
+        if (ak < l || ak > h) return false;
+      } else {
+        double t0 = __ddiv_rn(__dsub_rn(l, ak), dk);
+        double t1 = __ddiv_rn(__dsub_rn(h, ak), dk);
+        if (t0 > t1) {
+          const double t = t0;
+          t0 = t1;
+          t1 = t;
+        }
+        tmin = (tmin < t0) ? t0 : tmin;
+        tmax = (t1 < tmax) ? t1 : tmax;
+        if (tmin > tmax) return false;
+      }
+    }
+    return true;
+  }
   const int d = dims<D>(d_rt);
   const uint32_t full = bx.full ? bx.full[box] : 0u;  // (the caller has checked the cube)
 #pragma unroll
@@ -675,13 +708,19 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     const int b = i0 + gl;
     bool meets = b < bx.count;
     const int bc = meets ? b : 0;
-    const uint32_t full = bx.full ? bx.full[bc] : 0u;
+    if (vfull) {  // (boxes staged: lom / him set) only the position axes can separate
 #pragma unroll
-    for (int k = 0; k < dim; ++k) {
-      if ((full >> k) & 1u) continue;
-      const double lo = bx.lom ? bx.lom[bc * bx.bs + k * bx.as] : bx.lo[bc * bx.bs + k * bx.as] - kSepMargin;
-      const double hi = bx.him ? bx.him[bc * bx.bs + k * bx.as] : bx.hi[bc * bx.bs + k * bx.as] + kSepMargin;
-      meets = meets && !(pmx[k] < lo || pmn[k] > hi);
+      for (int k = 0; k < 3; ++k)
+        meets = meets && !(pmx[k] < bx.lom[bc * bx.bs + k * bx.as] || pmn[k] > bx.him[bc * bx.bs + k * bx.as]);
+    } else {
+      const uint32_t full = bx.full ? bx.full[bc] : 0u;
+#pragma unroll
+      for (int k = 0; k < dim; ++k) {
+        if ((full >> k) & 1u) continue;
+        const double lo = bx.lom ? bx.lom[bc * bx.bs + k * bx.as] : bx.lo[bc * bx.bs + k * bx.as] - kSepMargin;
+        const double hi = bx.him ? bx.him[bc * bx.bs + k * bx.as] : bx.hi[bc * bx.bs + k * bx.as] + kSepMargin;
+        meets = meets && !(pmx[k] < lo || pmn[k] > hi);
+      }
     }
     const uint32_t m = (__ballot_sync(gmask, meets) >> gbase) & 0xffffu;
     const int at = kept + __popc(m & ((1u << gl) - 1u));
@@ -700,7 +739,9 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     bool hit = false;
     if (p < pairs) {
       const int sg = p / nbx, bi = p - sg * nbx;
-      hit = seg_box_hit<6>(tab + sg * dim, tab + (sg + 1) * dim, dim, bx, sub.idx ? sub.idx[bi] : bi);
+      const int box = sub.idx ? sub.idx[bi] : bi;
+      hit = vfull ? seg_box_hit<6, true>(tab + sg * dim, tab + (sg + 1) * dim, dim, bx, box)
+                  : seg_box_hit<6>(tab + sg * dim, tab + (sg + 1) * dim, dim, bx, box);
     }
     if (__any_sync(gmask, hit)) return false;
   }
@@ -1174,6 +1215,15 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
           xn = list[kn + h];
           n0 = __ldg(I.in_ptr + xn);
           nlen = static_cast<int>(__ldg(I.in_end + xn) - n0);
+          if constexpr (D == 6 && kRows == 2) {
+            // (DI: a lazy check outlasts a row fetch -- the next rows are
+            // pulled into L2 by the TMA engine meanwhile)
+            if (hl == 0 && I.in_tau && nlen > 0) {
+              prefetch_l2(I.in_col + n0, sizeof(int32_t) * nlen);
+              prefetch_l2(I.in_cost + n0, sizeof(double) * nlen);
+              prefetch_l2(I.in_tau + n0, sizeof(double) * nlen);
+            }
+          }
         }
         // The segment's B endpoint (the candidate) is staged while the row
         // streams in; the A endpoint (the chosen parent) after the argmin.
