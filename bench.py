@@ -209,7 +209,8 @@ def reference_di(specs, threads: int, passes: int, warmup: int = 1):
     import oracle
     R = oracle.ref()
     t0 = time.perf_counter()
-    need = pool_need(specs)
+    from paper_1705_02403_b200.problem import halton_pool_size
+    need = halton_pool_size(specs)
     pool = R.di_pool(specs[0].start_index, need, specs[0].di_params(), specs[0].radius_override, threads)
     insts = R.di_instances(pool, specs, threads)
     build_s = time.perf_counter() - t0
@@ -251,19 +252,6 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-
-
-def pool_need(specs) -> int:
-    """Halton pool points the reference arm's DI instances need: n over the
-    free-volume estimate, +5 % + 256 (the device pool's own sizing)."""
-    import math
-    need = 0
-    for s in specs:
-        lo = s.box_lo.clip(0.0, 1.0)
-        hi = s.box_hi.clip(0.0, 1.0)
-        blocked = float((hi - lo).clip(0.0, None).prod(axis=1).sum())
-        need = max(need, math.ceil(min(4.0 * s.n, s.n / max(0.05, 1.0 - blocked) * 1.05) + 256))
-    return need
 
 
 def run_b200(args):

@@ -598,6 +598,20 @@ def quad_scene(seed: int = 5, n: int = 8000, pillars: int = 90, beams: int = 40,
     return spec
 
 
+def halton_pool_size(specs) -> int:
+    """Halton points a shared sample pool needs for `specs` (SURVEY.md
+    §8(e)): n over the free-volume estimate (boxes clipped to the unit cube,
+    overlaps counted twice), +5 % + 256 -- the device pool's own sizing
+    (csrc/pool.cu: pool_need)."""
+    need = 0
+    for s in specs:
+        lo = np.clip(s.box_lo, 0.0, 1.0)
+        hi = np.clip(s.box_hi, 0.0, 1.0)
+        blocked = float(np.clip(hi - lo, 0.0, None).prod(axis=1).sum()) if s.num_boxes else 0.0
+        need = max(need, int(math.ceil(min(4.0 * s.n, s.n / max(0.05, 1.0 - blocked) * 1.05) + 256)))
+    return need
+
+
 def connection_radius_py(dim: int, n: int, eta: float = 0.0, mu: float = 1.0) -> float:
     """Python float restatement of graph.cpp:19-32 (for quick checks only;
     the product computes it in C++ with the same libm calls)."""
