@@ -219,6 +219,21 @@ typedef struct gmt_problem {
   gmt_dubins_params dubins;
 } gmt_problem;
 
+/* ---- gmt-problem/1 scene files (problem.hpp:14-34) ---------------------- */
+/* parse_problem (problem.cpp:102-223) / load_problem (problem.cpp:225-231):
+ * the same strict validation -- unknown keys rejected, every error named by
+ * its field path (GMT_E_INVALID_INPUT with the reference's message, e.g.
+ * "obstacles[3].lo: expected 2 coordinates, got 3"; malformed JSON gives
+ * "invalid JSON: ..."), the Dubins-only fields, a free start state -- and
+ * the same defaults.  The handle owns the arrays; gmt_problem_file_view
+ * fills a flat gmt_problem pointing into it (valid until destroy) and the
+ * optional notes string.  radius_override <= 0 means none.               */
+typedef struct gmt_problem_file gmt_problem_file;
+int gmt_problem_parse(const char* json_text, size_t length, gmt_problem_file** out);
+int gmt_problem_load(const char* path, gmt_problem_file** out);
+int gmt_problem_file_view(const gmt_problem_file* file, gmt_problem* view, const char** notes);
+void gmt_problem_file_destroy(gmt_problem_file* file);
+
 /* Replanning simulator (simulator.hpp:14-80): ScenarioConfig with its
  * PlanningSetup flattened.  scene = the static obstacles at t = 0 and the
  * goal; radius_override <= 0 means connection_radius.                    */

@@ -659,6 +659,64 @@ inline std::optional<NeighborGraph> load_graph_cache(const std::string& file, st
   return detail::graph_from_csr(n, radius, m, ptr, col, cost);
 }
 
+namespace detail {
+inline ProblemFile problem_from_file(gmt_problem_file* h) {
+  gmt_problem v{};
+  const char* notes = nullptr;
+  const int rc = gmt_problem_file_view(h, &v, &notes);
+  if (rc != GMT_OK) {
+    gmt_problem_file_destroy(h);
+    check(rc);
+  }
+  ProblemFile p;
+  const int d = v.scene.dim;
+  p.dimension = d;
+  if (v.steering == GMT_STEER_DUBINS_AIRPLANE) {
+    p.steering.kind = SteeringModel::Kind::dubins_airplane;
+    p.steering.rho = v.dubins.rho;
+    p.steering.discretization_step = v.dubins.discretization_step;
+    p.steering.planar_cost_only = v.dubins.planar_cost_only != 0;
+  }
+  p.obstacles.dim = d;
+  for (int b = 0; b < v.scene.num_boxes; ++b) {
+    Aabb box;
+    box.lo.assign(v.scene.box_lo + static_cast<size_t>(b) * d, v.scene.box_lo + static_cast<size_t>(b + 1) * d);
+    box.hi.assign(v.scene.box_hi + static_cast<size_t>(b) * d, v.scene.box_hi + static_cast<size_t>(b + 1) * d);
+    p.obstacles.boxes.push_back(std::move(box));
+  }
+  p.goal.box.lo.assign(v.scene.goal_lo, v.scene.goal_lo + d);
+  p.goal.box.hi.assign(v.scene.goal_hi, v.scene.goal_hi + d);
+  p.init.coords.assign(v.init, v.init + d);
+  if (v.init_has_heading) p.init.heading = v.init_heading;
+  p.n = v.n;
+  p.lambda = v.lambda;
+  p.eta = v.eta;
+  if (v.radius_override > 0.0) p.radius_override = v.radius_override;
+  p.sampling.kind = v.sampling.kind == GMT_SAMPLE_UNIFORM ? SampleSource::Kind::uniform : SampleSource::Kind::halton;
+  p.sampling.start_index = v.sampling.start_index;
+  p.sampling.seed = v.sampling.seed;
+  p.sampling.with_heading = v.sampling.with_heading != 0;
+  p.notes = notes ? notes : "";
+  gmt_problem_file_destroy(h);
+  return p;
+}
+}  // namespace detail
+
+// parse_problem (problem.cpp:102-223): strict gmt-problem/1 parsing, the
+// reference's path-named InvalidInputError messages.
+inline ProblemFile parse_problem(const std::string& json_text) {
+  gmt_problem_file* h = nullptr;
+  check(gmt_problem_parse(json_text.data(), json_text.size(), &h));
+  return detail::problem_from_file(h);
+}
+
+// load_problem (problem.cpp:225-231).
+inline ProblemFile load_problem(const std::string& path) {
+  gmt_problem_file* h = nullptr;
+  check(gmt_problem_load(path.c_str(), &h));
+  return detail::problem_from_file(h);
+}
+
 inline ProblemInstance build_instance(const ProblemFile& p, int workers = 1,
                                       const std::string& cache_file = "",
                                       Context& ctx = Context::thread_default()) {

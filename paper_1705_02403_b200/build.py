@@ -19,7 +19,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgmt_b200.so")
 OBJ = os.path.join(ROOT, "build", "obj")
-SOURCES = ["solve.cu", "graph.cu", "di_graph.cu", "sample.cu", "capi.cu", "cache.cu", "sim.cu", "batch_build.cu", "pool.cu"]
+SOURCES = ["solve.cu", "graph.cu", "di_graph.cu", "sample.cu", "capi.cu", "cache.cu", "sim.cu", "batch_build.cu", "pool.cu",
+           "problem_file.cpp"]
 HEADERS = ["common.cuh", "solve.cuh", "internal.cuh", "offline.cuh", "di.cuh", "quad.cuh", "dubins.cuh",
            "sample_dev.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -42,7 +43,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     procs = []
     for src in SOURCES:  # translation units compile in parallel
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        o = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
         objs.append(o)
         if force or _newer(o, [s] + hdrs):
             cmd = [NVCC, *FLAGS, "-c", s, "-o", o]

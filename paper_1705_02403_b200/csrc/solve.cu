@@ -482,11 +482,11 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
     if (quad) {
       if (lane < 4) quad_chain_lambda(x0, x1, tau, lane, QP, seg + 8 * lane, seg + 8 * lane + 4);
     } else if (lane < 3) {
-      const double D = di_sub(x1[lane], x0[lane]);
+      const double dp = di_sub(x1[lane], x0[lane]);
       const double v0 = di_vel(x0[3 + lane], DP), v1 = di_vel(x1[3 + lane], DP);
       const double tt = di_mul(tau, tau);
-      seg[lane] = di_sub(di_div(di_mul(3.0, D), tt), di_div(di_add(di_mul(2.0, v0), v1), tau));
-      seg[3 + lane] = di_sub(di_div(di_add(v0, v1), tt), di_div(di_mul(2.0, D), di_mul(tt, tau)));
+      seg[lane] = di_sub(di_div(di_mul(3.0, dp), tt), di_div(di_add(di_mul(2.0, v0), v1), tau));
+      seg[3 + lane] = di_sub(di_div(di_add(v0, v1), tt), di_div(di_mul(2.0, dp), di_mul(tt, tau)));
     } else if (lane - 2 < M) {
       const int k = lane - 2;
       seg[6 + k] = di_div(di_mul(tau, static_cast<double>(k)), static_cast<double>(M));

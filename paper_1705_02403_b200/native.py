@@ -90,6 +90,10 @@ SIGNATURES = [
     ("gmt_plan_batch_host", C.c_int, [_vp, _P(abi.BatchHost), C.c_double, _P(abi.PlanSummary),
                                       _i32p, _u8p, _dp, _i32p, _i64p]),
     ("gmt_segment_free", C.c_int, [_vp, C.c_int32, C.c_int32, _dp, _dp, _dp, _dp, C.c_int64, _u8p]),
+    ("gmt_problem_parse", C.c_int, [C.c_char_p, C.c_size_t, _P(_vp)]),
+    ("gmt_problem_load", C.c_int, [C.c_char_p, _P(_vp)]),
+    ("gmt_problem_file_view", C.c_int, [_vp, _P(abi.Problem), _P(C.c_char_p)]),
+    ("gmt_problem_file_destroy", None, [_vp]),
     ("gmt_host_alloc", C.c_int, [C.c_size_t, _P(_vp)]),
     ("gmt_host_free", None, [_vp]),
 ]
@@ -693,6 +697,47 @@ def graph_cache_load(file: str, key: int, n: int, radius: float, dim: int = 0):
         return None
     E = ne.value
     return Graph(n, radius, ptr, col[:E], cost[:E], dim=dim)
+
+
+def _problem_file_spec(h):
+    from . import problem as P
+    v = abi.Problem()
+    notes = C.c_char_p()
+    try:
+        check(lib().gmt_problem_file_view(h, C.byref(v), C.byref(notes)))
+        d, nb = v.scene.dim, v.scene.num_boxes
+        arr = lambda p, m: np.ctypeslib.as_array(p, shape=(m,)).copy() if m else np.zeros(0)  # noqa: E731
+        spec = P.ProblemSpec(
+            dim=d, box_lo=arr(v.scene.box_lo, nb * d).reshape(nb, d), box_hi=arr(v.scene.box_hi, nb * d).reshape(nb, d),
+            goal_lo=arr(v.scene.goal_lo, d), goal_hi=arr(v.scene.goal_hi, d), init=arr(v.init, d), n=v.n,
+            lam=v.lambda_, eta=v.eta, radius_override=v.radius_override if v.radius_override > 0.0 else None,
+            sampling_kind=v.sampling.kind, start_index=v.sampling.start_index, seed=v.sampling.seed,
+            notes=(notes.value or b"").decode("utf-8"), steering=v.steering)
+        if v.steering == abi.STEER_DUBINS_AIRPLANE:
+            spec.init_heading = v.init_heading if v.init_has_heading else None
+            spec.dubins_rho = v.dubins.rho
+            spec.dubins_step = v.dubins.discretization_step
+            spec.dubins_planar = bool(v.dubins.planar_cost_only)
+        return spec
+    finally:
+        lib().gmt_problem_file_destroy(h)
+
+
+def parse_problem(text: str):
+    """parse_problem (problem.cpp:102-223) through the C ABI
+    (gmt_problem_parse) -> ProblemSpec; InvalidInputError with the
+    reference's path-named message on any error."""
+    data = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    check(lib().gmt_problem_parse(data, len(data), C.byref(h)))
+    return _problem_file_spec(h)
+
+
+def load_problem(path: str):
+    """load_problem (problem.cpp:225-231) through the C ABI."""
+    h = C.c_void_p()
+    check(lib().gmt_problem_load(os.fsencode(path), C.byref(h)))
+    return _problem_file_spec(h)
 
 
 def run_campaign(scenario, latencies, rates, sigmas, workers: int = 8, device: int = 0):

@@ -317,7 +317,52 @@ static void graph_cache_roundtrip() {
   std::remove(file.c_str());
 }
 
+// load_problem / parse_problem through the shim (problem.cpp:102-231): a
+// scene parsed, planned through build_instance + gmt_plan; the reference's
+// path-named errors.
+static void scene_files() {
+  const std::string text = R"({"schema": "gmt-problem/1", "dimension": 2,
+    "steering": {"model": "euclidean"},
+    "obstacles": [{"lo": [0.2, 0.0], "hi": [0.4, 0.6]}, {"lo": [0.45, 0.4], "hi": [0.65, 1.0]}],
+    "init": {"coords": [0.05, 0.3]}, "goal": {"lo": [0.92, 0.25], "hi": [0.99, 0.4]},
+    "n": 600, "lambda": 1.0, "notes": "two bars"})";
+  const ProblemFile p = parse_problem(text);
+  CHECK(p.dimension == 2 && p.obstacles.boxes.size() == 2 && p.n == 600);
+  CHECK(p.obstacles.boxes[1].lo[1] == 0.4 && p.goal.box.hi[0] == 0.99);
+  CHECK(!p.radius_override && p.sampling.kind == SampleSource::Kind::halton && p.sampling.start_index == 1);
+  CHECK(p.notes == "two bars");
+  const char* tmp = "/tmp/gmt_shim_scene.json";
+  if (FILE* f = std::fopen(tmp, "w")) {
+    std::fputs(text.c_str(), f);
+    std::fclose(f);
+  }
+  const ProblemFile q = load_problem(tmp);
+  CHECK(q.obstacles.boxes[0].hi[1] == 0.6 && q.init.coords[0] == 0.05);
+  const ProblemInstance inst = build_instance(q);
+  GmtParams params;
+  params.lambda = q.lambda;
+  params.radius = inst.radius;
+  const PlanResult r = gmt_plan(inst.samples, inst.graph, q.obstacles, q.goal, inst.init_index, params);
+  CHECK(r.status == PlanStatus::success);
+  auto msg = [&](const std::string& t) {
+    try {
+      parse_problem(t);
+    } catch (const InvalidInputError& e) {
+      return std::string(e.what());
+    }
+    return std::string("no error");
+  };
+  CHECK(msg(R"({"schema": "gmt-problem/1", "dimension": 2, "steering": {"model": "euclidean"},
+    "obstacles": [{"lo": [0.2], "hi": [0.4, 0.6]}], "init": {"coords": [0.05, 0.3]},
+    "goal": {"lo": [0.9, 0.2], "hi": [0.99, 0.4]}, "n": 10})") ==
+        "obstacles[0].lo: expected 2 coordinates, got 1");
+  CHECK(msg(R"({"schema": "gmt-problem/1", "dimensions": 2})") == "dimensions: unknown field");
+  CHECK(msg("{\"schema\": ").rfind("invalid JSON: ", 0) == 0);
+  CHECK(throws<InvalidInputError>([&] { load_problem("/nonexistent/scene.json"); }));
+}
+
 int main() {
+  scene_files();
   graph_cache_roundtrip();
   open_field();
   init_in_goal();
