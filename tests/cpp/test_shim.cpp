@@ -323,12 +323,12 @@ static void graph_cache_roundtrip() {
 static void scene_files() {
   const std::string text = R"({"schema": "gmt-problem/1", "dimension": 2,
     "steering": {"model": "euclidean"},
-    "obstacles": [{"lo": [0.2, 0.0], "hi": [0.4, 0.6]}, {"lo": [0.45, 0.4], "hi": [0.65, 1.0]}],
+    "obstacles": [{"lo": [0.2, 0.0], "hi": [0.4, 0.6]}, {"lo": [0.55, 0.4], "hi": [0.75, 1.0]}],
     "init": {"coords": [0.05, 0.3]}, "goal": {"lo": [0.92, 0.25], "hi": [0.99, 0.4]},
     "n": 600, "lambda": 1.0, "notes": "two bars"})";
   const ProblemFile p = parse_problem(text);
   CHECK(p.dimension == 2 && p.obstacles.boxes.size() == 2 && p.n == 600);
-  CHECK(p.obstacles.boxes[1].lo[1] == 0.4 && p.goal.box.hi[0] == 0.99);
+  CHECK(p.obstacles.boxes[1].lo[0] == 0.55 && p.goal.box.hi[0] == 0.99);
   CHECK(!p.radius_override && p.sampling.kind == SampleSource::Kind::halton && p.sampling.start_index == 1);
   CHECK(p.notes == "two bars");
   const char* tmp = "/tmp/gmt_shim_scene.json";
@@ -344,6 +344,10 @@ static void scene_files() {
   params.radius = inst.radius;
   const PlanResult r = gmt_plan(inst.samples, inst.graph, q.obstacles, q.goal, inst.init_index, params);
   CHECK(r.status == PlanStatus::success);
+  if (r.status != PlanStatus::success)
+    std::printf("scene_files: status %d, %zu samples, init %d, radius %.17g, iterations %lld\n",
+                static_cast<int>(r.status), inst.samples.states.size(), inst.init_index, inst.radius,
+                static_cast<long long>(r.iterations));
   auto msg = [&](const std::string& t) {
     try {
       parse_problem(t);
