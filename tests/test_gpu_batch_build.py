@@ -72,8 +72,10 @@ def test_plan_problems_matches_reference(ctx, ref):
 
 
 def test_plan_problems_generic_dimension_and_errors(ctx):
-    """d = 6 takes the generic r-disk kernel (no row scratch); steering
-    models other than Euclidean and mixed dimensions are rejected."""
+    """d = 6 takes the generic r-disk kernel (no row scratch); a batch mixing
+    Euclidean and double-integrator problems, and mixed dimensions, are
+    rejected (double-integrator batches take the shared pool,
+    tests/test_gpu_pool.py)."""
     specs = [scene("rectangles_6d", 400 + 50 * k) for k in range(4)]
     status, summ, _ = ctx.plan_problems(specs)
     for q, sp in enumerate(specs):
@@ -82,7 +84,11 @@ def test_plan_problems_generic_dimension_and_errors(ctx):
         assert (summ[q].status, summ[q].cost, summ[q].iterations) == (want.status, want.cost, want.iterations)
     from paper_1705_02403_b200.errors import InvalidInputError
     with pytest.raises(InvalidInputError):
-        ctx.plan_problems([P.di_forest(3, 300)])
+        ctx.plan_problems([scene("rectangles_6d", 300), P.di_forest(3, 300)])
+    di = P.di_forest(3, 300, radius=2.6)
+    status, summ, _ = ctx.plan_problems([di])
+    want = ctx.plan(ctx.build_instance(di))
+    assert status[0] == 0 and (summ[0].status, summ[0].cost) == (want.status, want.cost)
     with pytest.raises(InvalidInputError):
         ctx.plan_problems([scene("rectangles_2d", 200), scene("rectangles_3d", 200)])
 
