@@ -39,7 +39,9 @@
 
 namespace gmtb {
 
-int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, int cluster, size_t* smem, int* obs_in_smem);
+int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, int cluster, size_t* smem, int* obs_in_smem,
+              size_t* gstate = nullptr);
+int assign_gstate(Arena& arena, std::vector<SolveJob>& jobs, size_t bytes);
 int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, bool stats,
                   std::vector<DevResult>& out, ResultScalars** scalars_base, int64_t* counters);
 int launch_jobs(gmt_ctx* ctx, const std::vector<SolveJob>& jobs, int cluster, int threads, size_t smem,
@@ -1310,10 +1312,12 @@ extern "C" int gmt_plan_problems(gmt_ctx* ctx, const gmt_problem* problems, int3
     size_t smem = 0;
     int obs = 0;
     const int cluster = ctx->batch_cluster ? ctx->batch_cluster : 1;
-    rc = plan_smem(ctx, max_V, d, max_nb, cluster, &smem, &obs);
+    size_t gs = 0;
+    rc = plan_smem(ctx, max_V, d, max_nb, cluster, &smem, &obs, &gs);
     std::vector<DevResult> rs;
     ResultScalars* sc = nullptr;
     if (rc == GMT_OK) rc = carve_results(ctx->res, J, node_off.data(), false, false, rs, &sc, nullptr);
+    if (rc == GMT_OK && gs) rc = assign_gstate(ctx->gstate, jobs, gs);  // (too large for shared memory)
     if (rc == GMT_OK) {
       for (int k = 0; k < J; ++k) jobs[k].res = rs[k];
       rc = launch_jobs(ctx, jobs, cluster, ctx->batch_threads ? ctx->batch_threads : (cluster > 1 ? 512 : 256),

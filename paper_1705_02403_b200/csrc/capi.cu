@@ -186,6 +186,7 @@ extern "C" void gmt_ctx_destroy(gmt_ctx* ctx) {
     ctx->pool_work.release();
     ctx->pool_rows.release();
     ctx->pool_res.release();
+    ctx->gstate.release();
     destroy_pool(ctx->pool);
     ctx->pool = nullptr;
     ctx->plan_inst.mem.release();
@@ -535,14 +536,24 @@ int validate_plan(const gmt_instance* inst, int32_t init_index, double lambda, d
 
 // Shared-memory plan for a set of queries; errors when a query's wavefront
 // cannot live on chip.
+// gstate (may be null): when the state exceeds the opt-in, *gstate receives
+// the per-query bytes of a global-memory wavefront (one wide CTA per query,
+// launch_solve's gstate mode) instead of an error; 0 when it fits on chip.
 int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, int cluster, size_t* smem,
-              int* obs_in_smem) {
-  if (max_n > kMaxSolveNodes)
-    return set_error(GMT_E_INVALID_INPUT, "n = " + std::to_string(max_n) + " exceeds the " +
-                                              std::to_string(kMaxSolveNodes) +
-                                              "-node limit of the on-chip wavefront");
+              int* obs_in_smem, size_t* gstate = nullptr) {
+  if (gstate) *gstate = 0;
   if (max_d > kMaxSolveDim)
     return set_error(GMT_E_INVALID_INPUT, "dimension above 16 is not supported");
+  if (max_n > kMaxSolveNodes) {
+    if (!gstate)
+      return set_error(GMT_E_INVALID_INPUT, "n = " + std::to_string(max_n) + " exceeds the " +
+                                                std::to_string(kMaxSolveNodes) +
+                                                "-node limit of the on-chip wavefront");
+    *obs_in_smem = 1;  // global-memory wavefront with 32-bit work lists
+    *gstate = solve_layout(max_n, max_d, max_nb, true, false, 4).total;
+    *smem = 0;
+    return GMT_OK;
+  }
   const bool parent_smem = cluster > 1;
   const size_t obs_bytes = sizeof(double) * 4 * static_cast<size_t>(max_nb) * max_d;
   *obs_in_smem = obs_bytes <= 48 * 1024 ? 1 : 0;
@@ -550,6 +561,13 @@ int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, int cluster, size_
   if (L.total > ctx->smem_optin && *obs_in_smem) {
     *obs_in_smem = 0;
     L = solve_layout(max_n, max_d, max_nb, false, parent_smem);
+  }
+  if (L.total > ctx->smem_optin && gstate) {
+    *obs_in_smem = 1;  // (the boxes are staged into the global buffer)
+    L = solve_layout(max_n, max_d, max_nb, true, false, 4);
+    *gstate = L.total;
+    *smem = 0;
+    return GMT_OK;
   }
   if (L.total > ctx->smem_optin) {
     return set_error(GMT_E_INVALID_INPUT,
@@ -601,6 +619,14 @@ int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, b
   return GMT_OK;
 }
 
+// One global wavefront buffer per job (stride aligned to 256 bytes).
+int assign_gstate(Arena& arena, std::vector<SolveJob>& jobs, size_t bytes) {
+  const size_t stride = (bytes + 255) & ~static_cast<size_t>(255);
+  GMT_TRY(arena.reserve(stride * jobs.size()));
+  for (size_t q = 0; q < jobs.size(); ++q) jobs[q].gstate = static_cast<unsigned char*>(arena.ptr) + q * stride;
+  return GMT_OK;
+}
+
 int launch_jobs(gmt_ctx* ctx, const std::vector<SolveJob>& jobs, int cluster, int threads,
                 size_t smem, int obs_in_smem, int dim) {
   const size_t bytes = sizeof(SolveJob) * jobs.size();
@@ -609,9 +635,10 @@ int launch_jobs(gmt_ctx* ctx, const std::vector<SolveJob>& jobs, int cluster, in
   std::memcpy(ctx->pinned_jobs.ptr, jobs.data(), bytes);
   GMT_CUDA(cudaMemcpyAsync(ctx->jobs.ptr, ctx->pinned_jobs.ptr, bytes, cudaMemcpyHostToDevice,
                            ctx->stream));
+  const bool gs = jobs[0].gstate != nullptr;
   const cudaError_t e = launch_solve(static_cast<const SolveJob*>(ctx->jobs.ptr), static_cast<int>(jobs.size()),
-                                     cluster, threads, smem, obs_in_smem, dim, ctx->stream,
-                                     jobs[0].res.counters != nullptr);
+                                     gs ? 1 : cluster, gs ? 512 : threads, smem, obs_in_smem, dim, ctx->stream,
+                                     !gs && jobs[0].res.counters != nullptr, gs);
   if (e != cudaSuccess) {
     return set_error(GMT_E_CUDA, std::string("solve launch (cluster ") + std::to_string(cluster) + ", " +
                                      std::to_string(threads) + " threads, " + std::to_string(smem) +
@@ -661,9 +688,9 @@ int plan_on(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, double l
             double radius, gmt_plan_out* out, int mode = kModeGmt) {
   GMT_TRY(validate_plan(inst, init_index, lambda, radius));
   const DevInstance& D = inst->desc;
-  size_t smem;
+  size_t smem, gs = 0;
   int obs;
-  GMT_TRY(plan_smem(ctx, D.n, D.dim, D.num_boxes, ctx->cluster ? ctx->cluster : 8, &smem, &obs));
+  GMT_TRY(plan_smem(ctx, D.n, D.dim, D.num_boxes, ctx->cluster ? ctx->cluster : 8, &smem, &obs, &gs));
   int64_t node_off[2] = {0, D.n};
   std::vector<DevResult> res;
   ResultScalars* sc;
@@ -678,7 +705,9 @@ int plan_on(gmt_ctx* ctx, const gmt_instance* inst, int32_t init_index, double l
   job.radius = radius;
   const int cluster = ctx->cluster ? ctx->cluster : 8;
   int threads = ctx->threads ? ctx->threads : 512;
-  GMT_TRY(launch_jobs(ctx, {job}, cluster, threads, smem, obs, D.dim));
+  std::vector<SolveJob> jobs{job};
+  if (gs) GMT_TRY(assign_gstate(ctx->gstate, jobs, gs));  // (too large for shared memory)
+  GMT_TRY(launch_jobs(ctx, jobs, cluster, threads, smem, obs, D.dim));
   return download_result(ctx, res[0], D.n, out);
 }
 
@@ -793,7 +822,9 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
     for (int q = 0; q < count; ++q)
       if (insts[q]->desc.steering != GMT_STEER_EUCLIDEAN && count < 4 * ctx->sm_count) b->cluster = 2;
   }
-  int rc = plan_smem(ctx, max_n, max_d, max_nb, b->cluster, &b->smem, &b->obs);
+  size_t gs = 0;
+  int rc = plan_smem(ctx, max_n, max_d, max_nb, b->cluster, &b->smem, &b->obs, &gs);
+  if (rc == GMT_OK && gs) b->cluster = 1;
   if (rc == GMT_OK)
     rc = carve_results(b->res, count, b->node_off.data(), true, true, b->results, &b->scalars,
                        ctx->counting ? ctx->counters : nullptr);
@@ -812,6 +843,14 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
     j.radius = insts[q]->desc.radius;
   }
   b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
+  if (gs) {
+    b->threads = 512;
+    rc = assign_gstate(b->gstate_mem, b->jobs, gs);
+    if (rc != GMT_OK) {
+      delete b;
+      return rc;
+    }
+  }
   rc = b->jobs_mem.reserve(sizeof(SolveJob) * count);
   if (rc == GMT_OK) {
     // jobs_mem comes from the stream-ordered pool of ctx->stream: write it on
@@ -832,9 +871,10 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
 
 extern "C" int gmt_batch_launch(gmt_ctx* ctx, gmt_batch* b) {
   gmtb::AllocScope alloc_scope_(ctx);
+  const bool gs = b->jobs[0].gstate != nullptr;
   GMT_CUDA(launch_solve(static_cast<const SolveJob*>(b->jobs_mem.ptr), static_cast<int>(b->jobs.size()),
                         b->cluster, b->threads, b->smem, b->obs, b->dim, ctx->stream,
-                        b->jobs[0].res.counters != nullptr));
+                        !gs && b->jobs[0].res.counters != nullptr, gs));
   ++ctx->launches;
   return GMT_OK;
 }

@@ -102,6 +102,10 @@ struct SolveJob {
   int32_t mode;
   double lambda;
   double radius;  // params.radius (validated == graph radius on the host)
+  // Wavefront state in global memory (the solve's shared-memory layout, one
+  // block per query) for queries whose state exceeds the shared-memory
+  // opt-in; null: the state lives in shared memory.
+  unsigned char* gstate;
 };
 
 // ---- exact geometry (space.cpp) ------------------------------------------

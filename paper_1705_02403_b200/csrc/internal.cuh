@@ -116,6 +116,7 @@ struct gmt_ctx {
   gmtb::Arena pool_rows;  //   ... their row regions
   gmtb::Arena pool_res;   //   ... their results
   gmtb::HostPinned pool_pinned;  //   ... the packed scene arrays (staging)
+  gmtb::Arena gstate;     // global-memory wavefronts of queries too large for shared memory
   gmtb::SamplePool* pool = nullptr;  // shared Halton pool + its graph (built on first use, reused)
   gmtb::HostPinned pinned;
   gmtb::HostPinned pinned2;
@@ -130,6 +131,7 @@ struct gmt_batch {
   gmtb::Arena jobs_mem;
   gmtb::Arena derived;                 // shared-pool batches: the derived per-query instances
   gmtb::Arena derived_rows;            //   ... their row regions
+  gmtb::Arena gstate_mem;              // global-memory wavefronts (queries above the shared-memory opt-in)
   std::vector<gmt_instance*> owned;    // shared-pool batches: queries built one by one (rare paths)
   std::vector<gmtb::SolveJob> jobs;
   std::vector<gmtb::DevResult> results;
@@ -145,6 +147,7 @@ struct gmt_batch {
     jobs_mem.release();
     derived.release();
     derived_rows.release();
+    gstate_mem.release();
     for (gmt_instance* i : owned) delete i;
   }
 };

@@ -53,7 +53,9 @@
 
 namespace gmtb {
 
-int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, int cluster, size_t* smem, int* obs_in_smem);
+int plan_smem(gmt_ctx* ctx, int max_n, int max_d, int max_nb, int cluster, size_t* smem, int* obs_in_smem,
+              size_t* gstate = nullptr);
+int assign_gstate(Arena& arena, std::vector<SolveJob>& jobs, size_t bytes);
 int carve_results(Arena& arena, int count, const int64_t* node_off, bool tree, bool stats,
                   std::vector<DevResult>& out, ResultScalars** scalars_base, int64_t* counters);
 
@@ -1123,8 +1125,15 @@ static int batch_from_derived(gmt_ctx* ctx, gmt_batch* b, const gmt_problem* pro
   // queries, one CTA each once they fill the SMs several times over)
   b->cluster = ctx->batch_cluster ? ctx->batch_cluster : (kino && J < 4 * ctx->sm_count ? 2 : 1);
   b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
-  int rc = plan_smem(ctx, max_V, d, max_nb, b->cluster, &b->smem, &b->obs);
+  size_t gs = 0;
+  int rc = plan_smem(ctx, max_V, d, max_nb, b->cluster, &b->smem, &b->obs, &gs);
   if (rc) return rc;
+  if (gs) {  // too large for shared memory: global-memory wavefronts, one wide CTA each
+    b->cluster = 1;
+    b->threads = 512;
+    rc = assign_gstate(b->gstate_mem, b->jobs, gs);
+    if (rc) return rc;
+  }
   rc = carve_results(b->res, J, b->node_off.data(), tree_stats, tree_stats, b->results, &b->scalars,
                      ctx->counting ? ctx->counters : nullptr);
   if (rc) return rc;

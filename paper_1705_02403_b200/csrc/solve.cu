@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "di.cuh"
@@ -802,7 +803,10 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 // Kinodynamic queries (D = 6 double integrator, D = 0 quadrotor) need about
 // 55 KB of shared memory per narrow CTA, so three fit an SM: those narrow
 // kernels get the registers of three CTAs per SM.
-template <int CS, int D, bool WIDE, bool COUNT>
+// GS: the wavefront state (cost, bitmasks, lists, staged boxes) lives in a
+// per-query global buffer (SolveJob::gstate, L2-resident) instead of shared
+// memory -- queries too large for the shared-memory opt-in (single CTA).
+template <int CS, int D, bool WIDE, bool COUNT, bool GS = false>
 __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 0) ? 3 : GMT_BATCH_MIN_BLOCKS))
     gmt_solve_kernel(const SolveJob* __restrict__ jobs, int obs_in_smem) {
   constexpr bool kParentSmem = CS > 1;  // single-CTA solves keep parents in HBM
@@ -844,18 +848,20 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
   const DevInstance& I = inst_s;
   const DevResult& R = job_s.res;
   const int n = I.n, d = dims<D>(I.dim), nb = I.num_boxes;
-  const SolveLayout L = solve_layout(n, d, nb, obs_in_smem != 0, kParentSmem);
+  using ListT = typename std::conditional<GS, int32_t, uint16_t>::type;  // work-list vertex ids
+  const SolveLayout L = solve_layout(n, d, nb, obs_in_smem != 0, kParentSmem, GS ? 4 : 2);
   const int W = L.words;
+  unsigned char* const sbase = GS ? job_s.gstate : smem;  // (GS = false: shared memory)
 
-  double* cost_s = reinterpret_cast<double*>(smem + L.off_cost);
-  uint16_t* parent_s = reinterpret_cast<uint16_t*>(smem + L.off_parent);
-  uint32_t* open_w = reinterpret_cast<uint32_t*>(smem + L.off_bits);
+  double* cost_s = reinterpret_cast<double*>(sbase + L.off_cost);
+  uint16_t* parent_s = reinterpret_cast<uint16_t*>(sbase + L.off_parent);
+  uint32_t* open_w = reinterpret_cast<uint32_t*>(sbase + L.off_bits);
   uint32_t* closed_w = open_w + L.words_pad;
   uint32_t* group_w = closed_w + L.words_pad;
   uint32_t* newopen_w = group_w + L.words_pad;
   uint32_t* cand_w = newopen_w + L.words_pad;
   uint32_t* goal_w = cand_w + L.words_pad;
-  uint16_t* list = reinterpret_cast<uint16_t*>(smem + L.off_list);
+  ListT* list = reinterpret_cast<ListT*>(sbase + L.off_list);
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
@@ -866,7 +872,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
   bxl.count = nb;
   if (obs_in_smem) {
     // Stage the boxes axis-major, with the separation bounds lo - m, hi + m.
-    double* lo = reinterpret_cast<double*>(smem + L.off_obs);
+    double* lo = reinterpret_cast<double*>(sbase + L.off_obs);
     double* hi = lo + static_cast<size_t>(nb) * d;
     double* lom = hi + static_cast<size_t>(nb) * d;
     double* him = lom + static_cast<size_t>(nb) * d;
@@ -1024,7 +1030,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
       if (tid == 0) {
         group_w[z >> 5] = 1u << (z & 31);
         if (((z >> 5) & (CS - 1)) == rank) {
-          list[0] = static_cast<uint16_t>(z);
+          list[0] = static_cast<ListT>(z);
           sh.own_count = 1;
         }
       }
@@ -1072,7 +1078,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
           }
           base = __shfl_sync(kFull, base, 0);
           if (g) {
-            if (own) list[base + __popc(gb & ((1u << lane) - 1u))] = static_cast<uint16_t>(v);
+            if (own) list[base + __popc(gb & ((1u << lane) - 1u))] = static_cast<ListT>(v);
             if ((goal_w[w] >> lane) & 1u) argmin_step(gc, gv, cost_s[v], v);
           }
         }
@@ -1178,7 +1184,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
         while (bits) {
           const int b = __ffs(bits) - 1;
           bits &= bits - 1u;
-          list[base++] = static_cast<uint16_t>(w * 32 + b);
+          list[base++] = static_cast<ListT>(w * 32 + b);
         }
       }
     }
@@ -1218,10 +1224,10 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
           if constexpr (D == 6 && kRows == 2) {
             // (DI: a lazy check outlasts a row fetch -- the next rows are
             // pulled into L2 by the TMA engine meanwhile)
+            // (not in_tau: one duration per row is read, after the argmin)
             if (hl == 0 && I.in_tau && nlen > 0) {
               prefetch_l2(I.in_col + n0, sizeof(int32_t) * nlen);
               prefetch_l2(I.in_cost + n0, sizeof(double) * nlen);
-              prefetch_l2(I.in_tau + n0, sizeof(double) * nlen);
             }
           }
         }
@@ -1738,10 +1744,10 @@ cudaError_t launch_dijkstra(const DevInstance* inst, const SolveJob* job, int n,
   }
 }
 
-template <int CS, int D, bool WIDE, bool COUNT>
+template <int CS, int D, bool WIDE, bool COUNT, bool GS = false>
 static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_t smem,
                              int obs_in_smem, cudaStream_t stream) {
-  auto kern = gmt_solve_kernel<CS, D, WIDE, COUNT>;
+  auto kern = gmt_solve_kernel<CS, D, WIDE, COUNT, GS>;
   // Function attributes are process-wide: the dynamic shared-memory limit
   // only ever grows (under a lock), so concurrent launches from several host
   // threads (each with its own context / stream) never see it shrink below
@@ -1780,19 +1786,23 @@ static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_
   return cudaLaunchKernelEx(&cfg, kern, jobs, obs_in_smem);
 }
 
-template <int CS, bool WIDE, bool COUNT = false>
+template <int CS, bool WIDE, bool COUNT = false, bool GS = false>
 static cudaError_t launch_dim(const SolveJob* jobs, int count, int threads, size_t smem,
                               int obs_in_smem, int dim, cudaStream_t stream) {
   switch (dim) {
-    case 2: return launch_cs<CS, 2, WIDE, COUNT>(jobs, count, threads, smem, obs_in_smem, stream);
-    case 3: return launch_cs<CS, 3, WIDE, COUNT>(jobs, count, threads, smem, obs_in_smem, stream);
-    case 6: return launch_cs<CS, 6, WIDE, COUNT>(jobs, count, threads, smem, obs_in_smem, stream);
-    default: return launch_cs<CS, 0, WIDE, COUNT>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 2: return launch_cs<CS, 2, WIDE, COUNT, GS>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 3: return launch_cs<CS, 3, WIDE, COUNT, GS>(jobs, count, threads, smem, obs_in_smem, stream);
+    case 6: return launch_cs<CS, 6, WIDE, COUNT, GS>(jobs, count, threads, smem, obs_in_smem, stream);
+    default: return launch_cs<CS, 0, WIDE, COUNT, GS>(jobs, count, threads, smem, obs_in_smem, stream);
   }
 }
 
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
-                         int obs_in_smem, int dim, cudaStream_t stream, bool count_traffic) {
+                         int obs_in_smem, int dim, cudaStream_t stream, bool count_traffic, bool gstate) {
+  if (gstate) {  // global-memory wavefront: one wide CTA per query
+    if (cluster != 1 || threads != 512) return cudaErrorInvalidValue;
+    return launch_dim<1, true, false, true>(jobs, count, threads, 0, obs_in_smem, dim, stream);
+  }
   switch (cluster) {
     case 1:
       if (count_traffic)

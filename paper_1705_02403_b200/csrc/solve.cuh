@@ -11,7 +11,8 @@
 namespace gmtb {
 
 // Largest node count the on-chip wavefront supports (u16 node ids in the
-// work lists and the parent replica).
+// work lists and the parent replica); the global-memory variant takes
+// larger queries.
 constexpr int kMaxSolveNodes = 65535;
 constexpr int kMaxSolveDim = 16;
 
@@ -22,6 +23,7 @@ constexpr int kMaxSolveDim = 16;
 //                      parents in HBM and walk them once at the end)
 //   bits   6 x u32[Wp] open, closed, group, newopen, cand, goal
 //   list   u16[32W]    owned group members (P4) / owned candidates (P5)
+//                      (i32 in the global-memory variant, which has no u16 id limit)
 //   obs    f64[4*B*d]  boxes lo, hi, lo - m, hi + m, axis-major (SoA), when they fit,
 //          u32[B]      then each box's mask of "full" axes (lo <= 0 and hi >= 1)
 struct SolveLayout {
@@ -31,7 +33,7 @@ struct SolveLayout {
 };
 
 __host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool obs_smem,
-                                                    bool parent_smem) {
+                                                    bool parent_smem, int list_bytes = 2) {
   SolveLayout L;
   L.words = (n + 31) >> 5;
   L.words_pad = (L.words + 3) & ~3;
@@ -44,7 +46,7 @@ __host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool o
   L.off_bits = off;
   off = align16(off + sizeof(uint32_t) * 6 * static_cast<size_t>(L.words_pad));
   L.off_list = off;
-  off = align16(off + sizeof(uint16_t) * nodes);
+  off = align16(off + static_cast<size_t>(list_bytes) * nodes);
   L.off_obs = off;
   if (obs_smem)
     off = align16(off + sizeof(double) * 4 * static_cast<size_t>(nb) * d + sizeof(uint32_t) * static_cast<size_t>(nb));
@@ -55,8 +57,11 @@ __host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool o
 // dim: the common dimension of every job (selects the specialised kernel;
 // 0 = generic).
 // count_traffic: the jobs carry traffic counters (GMT_OPT_COUNTERS).
+// gstate: every job carries a global state buffer (SolveJob::gstate) of the
+// solve_layout size; cluster must be 1 and threads 512.
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
-                         int obs_in_smem, int dim, cudaStream_t stream, bool count_traffic = false);
+                         int obs_in_smem, int dim, cudaStream_t stream, bool count_traffic = false,
+                         bool gstate = false);
 
 // dijkstra_oracle (planner.cpp:264-334): eager edge checks into ok[E] (and
 // the check count), then the Dijkstra search for job[0] (one CTA).
