@@ -432,7 +432,8 @@ def run_b200(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": prob_h2d,
                     "d2h_bytes_per_step": prob_d2h,
                     "path": "gmt_plan_problems: problem descriptions in (host), per-query instances derived "
-                            "on the device from the shared pool, batched solve, summaries out",
+                            "on the device as views of the shared pool (rank maps, special rows), batched solve, "
+                            "summaries out",
                     "steps": args.e2e_steps, "one_call_at_a_time": e2e_one, "two_host_threads": e2e_two,
                     "calls_in_flight": 2 if e2e_two > e2e_one else 1},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

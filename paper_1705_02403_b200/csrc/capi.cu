@@ -874,7 +874,7 @@ extern "C" int gmt_batch_launch(gmt_ctx* ctx, gmt_batch* b) {
   const bool gs = b->jobs[0].gstate != nullptr;
   GMT_CUDA(launch_solve(static_cast<const SolveJob*>(b->jobs_mem.ptr), static_cast<int>(b->jobs.size()),
                         b->cluster, b->threads, b->smem, b->obs, b->dim, ctx->stream,
-                        !gs && b->jobs[0].res.counters != nullptr, gs));
+                        !gs && b->jobs[0].res.counters != nullptr, gs, b->pool && !gs));
   ++ctx->launches;
   return GMT_OK;
 }

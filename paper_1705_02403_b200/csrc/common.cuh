@@ -18,6 +18,37 @@ constexpr double kInf = __builtin_huge_val();
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
+// A query's graph as a view of the shared Halton pool (pool.cu, SURVEY.md
+// §8(e)): vertex x < n is pool point sel[x] (unless x = n - 1 was goal-
+// substituted); its rows are the pool rows of sel[x] with every entry y
+// mapped to rank[y] (kNoRank: not a vertex of the query, skipped), followed
+// by its edges with the per-query vertices (g = n - 1 when subst, init = n;
+// code bits 0/2: g -> x / init -> x in the in-row at spec entry spj[2x] /
+// spj[2x + 1]; bits 1/3: x -> g / x -> init in the out-row).  g's and
+// init's own rows are the special lists l = 0 out(g), 1 in(g), 2 out(init),
+// 3 in(init) at scol/scost/stau + l * cap.
+struct PoolView {
+  const int64_t* in_ptr;   // pool graph (shared by every query)
+  const int32_t* in_col;
+  const double* in_cost;
+  const double* in_tau;
+  const int64_t* out_ptr;
+  const int32_t* out_col;
+  const int32_t* sel;      // per query
+  const uint16_t* rank;
+  const int32_t* code;
+  const uint16_t* spj;
+  const int32_t* scol;
+  const double* scost;
+  const double* stau;
+  int32_t spec_len[4];
+  int32_t subst;
+  int32_t cap;
+  int32_t kc;   // rank map length (pool points scanned)
+  int32_t k;    // pool graph vertices
+};
+constexpr uint16_t kPoolNoRank = 0xffffu;
+
 // Device-resident problem instance (ProblemInstance + ObstacleSet +
 // GoalRegion, problem.hpp:52-57 / space.hpp:28-41).  A POD descriptor that
 // lives in device memory; batched solves read one per query.
@@ -62,6 +93,9 @@ struct DevInstance {
   int32_t steering;
   int32_t kin_segments;
   double kin_p[6];
+  // Non-null: the graph is a view of the shared pool (the row arrays above
+  // are unused); only batched double-integrator solves see such instances.
+  const PoolView* pool;
 };
 
 // Scalars of one PlanResult (planner.hpp:43-51).

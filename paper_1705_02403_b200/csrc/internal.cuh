@@ -142,6 +142,7 @@ struct gmt_batch {
   int cluster = 1;
   int threads = 256;
   int dim = 0;  // common dimension of the queries (0: mixed)
+  bool pool = false;  // some jobs read shared-pool views (launch_solve's pool mode)
   ~gmt_batch() {
     res.release();
     jobs_mem.release();

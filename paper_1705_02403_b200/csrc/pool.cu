@@ -663,12 +663,30 @@ __global__ void pool_desc_kernel(const PQ* __restrict__ pq, const PQOut* __restr
                                  const int64_t* __restrict__ in_end, const int64_t* __restrict__ out_start,
                                  const int64_t* __restrict__ out_end, const int32_t* __restrict__ in_col,
                                  const double* __restrict__ in_cost, const double* __restrict__ in_tau,
-                                 const int32_t* __restrict__ out_col, DevInstance* __restrict__ descs) {
+                                 const int32_t* __restrict__ out_col, DevInstance* __restrict__ descs,
+                                 PoolView* __restrict__ views, PoolView shared_view, const int32_t* __restrict__ sel,
+                                 const uint16_t* __restrict__ rank, const int32_t* __restrict__ sp_code,
+                                 const uint16_t* __restrict__ sp_j, const int32_t* __restrict__ scol,
+                                 const double* __restrict__ scost, const double* __restrict__ stau) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= count) return;
   const PQ Q = pq[q];
   if (Q.skip || po[q].fallback) return;
   DevInstance D{};
+  if (views) {  // the graph as a view of the pool (the default: no rows are materialised)
+    PoolView v = shared_view;
+    v.sel = sel + Q.node_off;
+    v.rank = rank + static_cast<int64_t>(q) * shared_view.kc;
+    v.code = sp_code + Q.node_off;
+    v.spj = sp_j + 2 * Q.node_off;
+    v.scol = scol + static_cast<int64_t>(q) * 4 * kSpecCap;
+    v.scost = scost + static_cast<int64_t>(q) * 4 * kSpecCap;
+    v.stau = stau + static_cast<int64_t>(q) * 4 * kSpecCap;
+    for (int l = 0; l < 4; ++l) v.spec_len[l] = po[q].spec_len[l];
+    v.subst = po[q].subst;
+    views[q] = v;
+    D.pool = views + q;
+  }
   D.n = Q.n + 1;
   D.dim = kD;
   D.num_boxes = Q.nb;
@@ -682,15 +700,17 @@ __global__ void pool_desc_kernel(const PQ* __restrict__ pq, const PQOut* __restr
   D.box_hi = box_hi + Q.box_off * kD;
   D.goal_lo = goal_lo + static_cast<int64_t>(q) * kD;
   D.goal_hi = goal_hi + static_cast<int64_t>(q) * kD;
-  D.out_ptr = out_start + Q.node_off;
-  D.out_end = out_end + Q.node_off;
-  D.out_col = out_col + Q.out_off;
-  D.out_cost = nullptr;  // (the solve reads out-row targets only)
-  D.in_ptr = in_start + Q.node_off;
-  D.in_end = in_end + Q.node_off;
-  D.in_col = in_col + Q.in_off;
-  D.in_cost = in_cost + Q.in_off;
-  D.in_tau = in_tau + Q.in_off;
+  if (!views) {  // materialised rows (GMT_POOL_ROWS=1)
+    D.out_ptr = out_start + Q.node_off;
+    D.out_end = out_end + Q.node_off;
+    D.out_col = out_col + Q.out_off;
+    D.out_cost = nullptr;  // (the solve reads out-row targets only)
+    D.in_ptr = in_start + Q.node_off;
+    D.in_end = in_end + Q.node_off;
+    D.in_col = in_col + Q.in_off;
+    D.in_cost = in_cost + Q.in_off;
+    D.in_tau = in_tau + Q.in_off;
+  }
   D.steering = GMT_STEER_DOUBLE_INTEGRATOR;
   D.kin_segments = P.segments;
   D.kin_p[0] = P.vmax;
@@ -835,8 +855,16 @@ struct StageTimer {
 int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& meta, Arena& rows,
                 std::vector<gmt_instance*>& owned, std::vector<const DevInstance*>& inst, std::vector<int>& V,
                 std::vector<int>& init, std::vector<double>& radius, std::vector<int32_t>& status, int* max_V,
-                int* max_nb) {
+                int* max_nb, bool* viewed, bool prefer_rows) {
   cudaStream_t s = ctx->stream;
+  *viewed = false;
+  // Materialised rows cost a derivation pass (8 ms and ~15 GB of writes per
+  // 4096 queries) and make each solve faster (37 vs 42 ms): batches built
+  // once and launched many times take them (prefer_rows), one-shot
+  // gmt_plan_problems reads the pool through each query's rank map.
+  // GMT_POOL_ROWS=0/1 forces either (A/B checks).
+  const char* mat_env = std::getenv("GMT_POOL_ROWS");
+  bool materialise = mat_env && (mat_env[0] == '0' || mat_env[0] == '1') ? mat_env[0] == '1' : prefer_rows;
   const gmt_problem& p0 = problems[0];
   inst.assign(count, nullptr);
   V.assign(count, 0);
@@ -888,6 +916,10 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
     node_total += Q.n + 1;
   }
   g_last_error.clear();
+  {  // (views are read by the on-chip solve; larger queries get materialised rows)
+    const SolveLayout L = solve_layout(max_n + 1, kD, max_nbp, true, false);
+    if (L.total > ctx->smem_optin) materialise = true;
+  }
   std::vector<PQOut> po(count);
   SamplePool* pool = nullptr;
   StageTimer timer(s);
@@ -922,6 +954,7 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       const size_t o_os = c.take<int64_t>(node_total);
       const size_t o_oe = c.take<int64_t>(node_total);
       const size_t o_desc = c.take<DevInstance>(count);
+      const size_t o_view = c.take<PoolView>(count);
       rc = meta.reserve(c.off);
       if (rc) return rc;
       char* B = static_cast<char*>(meta.ptr);
@@ -947,6 +980,7 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       auto* d_os = reinterpret_cast<int64_t*>(B + o_os);
       auto* d_oe = reinterpret_cast<int64_t*>(B + o_oe);
       auto* d_desc = reinterpret_cast<DevInstance*>(B + o_desc);
+      auto* d_view = reinterpret_cast<PoolView*>(B + o_view);
       auto put = [&](void* dst, const void* src, size_t bytes) -> int {
         if (bytes) GMT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
         return GMT_OK;
@@ -999,9 +1033,42 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       pool_special_kernel<<<count, 128, 0, s>>>(d_pq, DP, pool->radius, d_qc, d_cand, d_scol, d_scost, d_stau, d_spc,
                                                 d_spj, d_po);
       timer.mark();
+      ctx->launches += 4;
+      if (!materialise) {  // the graphs are views of the pool: no per-query rows
+        PoolView sv{};
+        sv.in_ptr = pool->in.ptr;
+        sv.in_col = pool->in.col;
+        sv.in_cost = pool->in.cost;
+        sv.in_tau = pool->in.tau;
+        sv.out_ptr = pool->out.ptr;
+        sv.out_col = pool->out.col;
+        sv.cap = kSpecCap;
+        sv.kc = Kc;
+        sv.k = pool->K;
+        pool_desc_kernel<<<(count + 127) / 128, 128, 0, s>>>(
+            d_pq, d_po, count, pool->radius, DP, d_qc, d_blo, d_bhi, d_glo, d_ghi, nullptr, nullptr, nullptr, nullptr,
+            nullptr, nullptr, nullptr, nullptr, d_desc, d_view, sv, d_sel, d_rank, d_spc, d_spj, d_scol, d_scost,
+            d_stau);
+        GMT_CUDA(cudaGetLastError());
+        ++ctx->launches;
+        GMT_CUDA(cudaMemcpyAsync(po.data(), d_po, sizeof(PQOut) * count, cudaMemcpyDeviceToHost, s));
+        GMT_CUDA(cudaStreamSynchronize(s));
+        timer.mark();
+        for (int q = 0; q < count; ++q) {
+          if (pq[q].skip || po[q].fallback) continue;
+          inst[q] = d_desc + q;
+          V[q] = pq[q].n + 1;
+          init[q] = pq[q].n;
+          radius[q] = pool->radius;
+          *max_V = std::max(*max_V, V[q]);
+          *max_nb = std::max(*max_nb, pq[q].nb);
+          *viewed = true;
+        }
+        break;
+      }
       pool_layout_kernel<<<count, 1024, 0, s>>>(d_pq, pool->in.ptr, pool->out.ptr, d_sel, d_is, d_os, d_po);
       GMT_CUDA(cudaGetLastError());
-      ctx->launches += 5;
+      ++ctx->launches;
       GMT_CUDA(cudaMemcpyAsync(po.data(), d_po, sizeof(PQOut) * count, cudaMemcpyDeviceToHost, s));
       GMT_CUDA(cudaStreamSynchronize(s));
       int64_t tin = 0, tout = 0;
@@ -1041,7 +1108,8 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       timer.mark();
       pool_desc_kernel<<<(count + 127) / 128, 128, 0, s>>>(d_pq, d_po, count, pool->radius, DP, d_qc, d_blo, d_bhi,
                                                            d_glo, d_ghi, d_is, d_ie, d_os, d_oe, d_icol, d_icost,
-                                                           d_itau, d_ocol, d_desc);
+                                                           d_itau, d_ocol, d_desc, nullptr, PoolView{}, nullptr,
+                                                           nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
       GMT_CUDA(cudaGetLastError());
       timer.mark();
       ctx->launches += 2;
@@ -1124,10 +1192,12 @@ static int batch_from_derived(gmt_ctx* ctx, gmt_batch* b, const gmt_problem* pro
   // (the shape gmt_batch_create picks: 2-CTA clusters for a few kinodynamic
   // queries, one CTA each once they fill the SMs several times over)
   b->cluster = ctx->batch_cluster ? ctx->batch_cluster : (kino && J < 4 * ctx->sm_count ? 2 : 1);
+  if (b->pool) b->cluster = 1;  // (pool views are read by single-CTA solves)
   b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
   size_t gs = 0;
   int rc = plan_smem(ctx, max_V, d, max_nb, b->cluster, &b->smem, &b->obs, &gs);
   if (rc) return rc;
+
   if (gs) {  // too large for shared memory: global-memory wavefronts, one wide CTA each
     b->cluster = 1;
     b->threads = 512;
@@ -1156,9 +1226,11 @@ int plan_problems_pool(gmt_ctx* ctx, const gmt_problem* problems, int32_t count,
   std::vector<double> radius;
   std::vector<int32_t> status;
   int max_V = 0, max_nb = 0;
+  bool viewed = false;
   int rc = pool_derive(ctx, problems, count, ctx->pool_work, ctx->pool_rows, owned, inst, V, init, radius, status,
-                       &max_V, &max_nb);
+                       &max_V, &max_nb, &viewed, false);
   gmt_batch b;
+  b.pool = viewed;
   b.res = ctx->pool_res;  // (kept in the context across calls, like the derived instances)
   ctx->pool_res = Arena{};
   if (rc == GMT_OK)  // summaries (and paths) only: no trees, no per-pass stats
@@ -1237,8 +1309,10 @@ extern "C" int gmt_batch_create_problems(gmt_ctx* ctx, const gmt_problem* proble
   std::vector<double> radius;
   std::vector<int32_t> status;
   int max_V = 0, max_nb = 0;
+  bool viewed = false;
   int rc = pool_derive(ctx, problems, count, b->derived, b->derived_rows, b->owned, inst, V, init, radius, status,
-                       &max_V, &max_nb);
+                       &max_V, &max_nb, &viewed, true);
+  b->pool = viewed;
   if (rc == GMT_OK)
     rc = batch_from_derived(ctx, b, problems, count, inst, V, init, radius, max_V, max_nb, job_q, true);
   if (rc == GMT_OK && b->jobs.empty()) rc = set_error(GMT_E_INVALID_INPUT, "no problem of the batch could be built");
@@ -1270,6 +1344,88 @@ extern "C" int gmt_batch_graph(gmt_ctx* ctx, gmt_batch* b, int32_t q, int32_t* n
   GMT_CUDA(cudaMemcpyAsync(&D, b->jobs[q].inst, sizeof(D), cudaMemcpyDeviceToHost, s));
   GMT_CUDA(cudaStreamSynchronize(s));
   const int V = D.n;
+  if (D.pool) {  // a view of the shared pool: the rows the solve reads, rebuilt on the host
+    PoolView pv;
+    GMT_CUDA(cudaMemcpyAsync(&pv, D.pool, sizeof(pv), cudaMemcpyDeviceToHost, s));
+    GMT_CUDA(cudaStreamSynchronize(s));
+    const int K = pv.k, cap = pv.cap;
+    std::vector<int64_t> pip(K + 1), pop(K + 1);
+    GMT_CUDA(cudaMemcpyAsync(pip.data(), pv.in_ptr, sizeof(int64_t) * (K + 1), cudaMemcpyDeviceToHost, s));
+    GMT_CUDA(cudaMemcpyAsync(pop.data(), pv.out_ptr, sizeof(int64_t) * (K + 1), cudaMemcpyDeviceToHost, s));
+    GMT_CUDA(cudaStreamSynchronize(s));
+    const int64_t Ei = pip[K], Eo = pop[K];
+    std::vector<int32_t> pic(Ei), poc(Eo), sel(V), code(V), scol(4 * cap);
+    std::vector<double> pics(Ei), pit(Ei), scost(4 * cap), stau(4 * cap);
+    std::vector<uint16_t> rank(pv.kc), spj(2 * static_cast<size_t>(V));
+    auto get = [&](void* dst, const void* src, size_t bytes) -> int {
+      if (bytes) GMT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+      return GMT_OK;
+    };
+    int rc = GMT_OK;
+    if ((rc = get(pic.data(), pv.in_col, 4 * Ei)) || (rc = get(pics.data(), pv.in_cost, 8 * Ei)) ||
+        (rc = get(pit.data(), pv.in_tau, 8 * Ei)) || (rc = get(poc.data(), pv.out_col, 4 * Eo)) ||
+        (rc = get(sel.data(), pv.sel, 4 * static_cast<size_t>(V - 1))) ||
+        (rc = get(code.data(), pv.code, 4 * static_cast<size_t>(V))) ||
+        (rc = get(spj.data(), pv.spj, 2 * 2 * static_cast<size_t>(V))) ||
+        (rc = get(rank.data(), pv.rank, 2 * static_cast<size_t>(pv.kc))) ||
+        (rc = get(scol.data(), pv.scol, 4 * 4 * static_cast<size_t>(cap))) ||
+        (rc = get(scost.data(), pv.scost, 8 * 4 * static_cast<size_t>(cap))) ||
+        (rc = get(stau.data(), pv.stau, 8 * 4 * static_cast<size_t>(cap))))
+      return rc;
+    GMT_CUDA(cudaStreamSynchronize(s));
+    std::vector<int64_t> iptr(1, 0), optr(1, 0);
+    std::vector<int32_t> icol, ocol;
+    std::vector<double> icost, itau;
+    const int init = V - 1, g = V - 2;
+    for (int x = 0; x < V; ++x) {
+      if (x == init || (pv.subst && x == g)) {
+        const int l = x == init ? 2 : 0;
+        for (int j = 0; j < pv.spec_len[l + 1]; ++j) {
+          icol.push_back(scol[(l + 1) * cap + j]);
+          icost.push_back(scost[(l + 1) * cap + j]);
+          itau.push_back(stau[(l + 1) * cap + j]);
+        }
+        for (int j = 0; j < pv.spec_len[l]; ++j) ocol.push_back(scol[l * cap + j]);
+      } else {
+        const int p = sel[x];
+        for (int64_t e = pip[p]; e < pip[p + 1]; ++e) {
+          if (rank[pic[e]] == kPoolNoRank) continue;
+          icol.push_back(rank[pic[e]]);
+          icost.push_back(pics[e]);
+          itau.push_back(pit[e]);
+        }
+        if (pv.subst && (code[x] & 1)) {
+          icol.push_back(g);
+          icost.push_back(scost[spj[2 * x]]);
+          itau.push_back(stau[spj[2 * x]]);
+        }
+        if (code[x] & 4) {
+          icol.push_back(init);
+          icost.push_back(scost[2 * cap + spj[2 * x + 1]]);
+          itau.push_back(stau[2 * cap + spj[2 * x + 1]]);
+        }
+        for (int64_t e = pop[p]; e < pop[p + 1]; ++e)
+          if (rank[poc[e]] != kPoolNoRank) ocol.push_back(rank[poc[e]]);
+        if (pv.subst && (code[x] & 2)) ocol.push_back(g);
+        if (code[x] & 8) ocol.push_back(init);
+      }
+      iptr.push_back(static_cast<int64_t>(icol.size()));
+      optr.push_back(static_cast<int64_t>(ocol.size()));
+    }
+    *n = V;
+    *num_in = static_cast<int64_t>(icol.size());
+    *num_out = static_cast<int64_t>(ocol.size());
+    if (!in_ptr) return GMT_OK;
+    if (coords) GMT_CUDA(cudaMemcpyAsync(coords, D.coords, sizeof(double) * V * D.dim, cudaMemcpyDeviceToHost, s));
+    std::copy(iptr.begin(), iptr.end(), in_ptr);
+    std::copy(optr.begin(), optr.end(), out_ptr);
+    std::copy(icol.begin(), icol.end(), in_col);
+    if (in_cost) std::copy(icost.begin(), icost.end(), in_cost);
+    if (in_tau) std::copy(itau.begin(), itau.end(), in_tau);
+    if (out_col) std::copy(ocol.begin(), ocol.end(), out_col);
+    GMT_CUDA(cudaStreamSynchronize(s));
+    return GMT_OK;
+  }
   std::vector<int64_t> is(V + 1), ie(V), os(V + 1), oe(V);
   GMT_CUDA(cudaMemcpyAsync(is.data(), D.in_ptr, sizeof(int64_t) * (D.in_end ? V : V + 1), cudaMemcpyDeviceToHost, s));
   GMT_CUDA(cudaMemcpyAsync(os.data(), D.out_ptr, sizeof(int64_t) * (D.out_end ? V : V + 1), cudaMemcpyDeviceToHost, s));

@@ -654,7 +654,11 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     seg[3 + gl] = di_sub(di_div(di_add(v0, v1), tt), di_div(di_mul(2.0, D), di_mul(tt, tau)));
   } else if (gl - 2 < M) {
     const int k = gl - 2;
-    seg[6 + k] = di_div(di_mul(tau, static_cast<double>(k)), static_cast<double>(M));
+    const double tk = di_mul(tau, static_cast<double>(k));
+    // (tau k) / M: for M a power of two the quotient is the exact scaling
+    // tk * (1 / M) unless it would be subnormal -- the same double
+    seg[6 + k] = ((M & (M - 1)) == 0 && tk >= 1e-290) ? di_mul(tk, 1.0 / static_cast<double>(M))
+                                                       : di_div(tk, static_cast<double>(M));
   }
   __syncwarp(gmask);
   bool incube = true;
@@ -806,7 +810,10 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 // GS: the wavefront state (cost, bitmasks, lists, staged boxes) lives in a
 // per-query global buffer (SolveJob::gstate, L2-resident) instead of shared
 // memory -- queries too large for the shared-memory opt-in (single CTA).
-template <int CS, int D, bool WIDE, bool COUNT, bool GS = false>
+// POOL: jobs may carry shared-pool views (DevInstance::pool, batched DI
+// queries): their rows are read from the pool graph through the query's
+// rank map instead of materialised rows.
+template <int CS, int D, bool WIDE, bool COUNT, bool GS = false, bool POOL = false>
 __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 0) ? 3 : GMT_BATCH_MIN_BLOCKS))
     gmt_solve_kernel(const SolveJob* __restrict__ jobs, int obs_in_smem) {
   constexpr bool kParentSmem = CS > 1;  // single-CTA solves keep parents in HBM
@@ -837,15 +844,19 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
   // registers for the whole solve.
   __shared__ SolveJob job_s;
   __shared__ DevInstance inst_s;
+  __shared__ PoolView pv_s;
   if (threadIdx.x == 0) {
     job_s = jobs[q];
     inst_s = *job_s.inst;
     if (!inst_s.out_end) inst_s.out_end = inst_s.out_ptr + 1;  // CSR: row x ends at ptr[x + 1]
     if (!inst_s.in_end) inst_s.in_end = inst_s.in_ptr + 1;
+    if (POOL && inst_s.pool) pv_s = *inst_s.pool;
   }
   __syncthreads();
   const SolveJob& job = job_s;
   const DevInstance& I = inst_s;
+  const bool viewed = POOL && I.pool != nullptr;  // (block-uniform)
+  const PoolView& PV = pv_s;
   const DevResult& R = job_s.res;
   const int n = I.n, d = dims<D>(I.dim), nb = I.num_boxes;
   using ListT = typename std::conditional<GS, int32_t, uint16_t>::type;  // work-list vertex ids
@@ -950,6 +961,10 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
   }
   __syncthreads();
   const Boxes& bx = bx_s;  // read from shared memory where used
+  auto pool_rank = [&](int y) -> int {  // shared-pool views: pool point -> query vertex (or -1)
+    const uint16_t r = __ldg(PV.rank + y);
+    return r == kPoolNoRank ? -1 : static_cast<int>(r);
+  };
 
   // infeasible_input (planner.cpp:39-41, 108): empty tree.
   if (warp == 0) {
@@ -1106,10 +1121,35 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
       int k = kRows * warp;
       int64_t e0 = 0;
       int len = 0;
+      // Shared-pool views: a vertex's out-row is its pool row mapped through
+      // the rank map (ext = the row's edges into g / init, code bits 1 / 3),
+      // or g's / init's own list (rowp, already in query ids).
+      const int32_t* rowp = nullptr;
+      int ext = 0;
+      auto pool_out_row = [&](int g, int64_t* pe0, int* plen, const int32_t** prow, int* pext) {
+        const int nv = I.n - 1;  // init = n (the vertex count is n + 1)
+        if (g == nv || (PV.subst && g == nv - 1)) {
+          const int l = g == nv ? 2 : 0;
+          *prow = PV.scol + static_cast<int64_t>(l) * PV.cap;
+          *pe0 = 0;
+          *plen = PV.spec_len[l];
+          *pext = 0;
+        } else {
+          const int p = __ldg(PV.sel + g);
+          *pe0 = __ldg(PV.out_ptr + p);
+          *plen = static_cast<int>(__ldg(PV.out_ptr + p + 1) - *pe0);
+          *prow = nullptr;
+          *pext = __ldg(PV.code + g);
+        }
+      };
       if (k + h < own) {
         const int g = list[k + h];
-        e0 = __ldg(I.out_ptr + g);
-        len = static_cast<int>(__ldg(I.out_end + g) - e0);
+        if (viewed) {
+          pool_out_row(g, &e0, &len, &rowp, &ext);
+        } else {
+          e0 = __ldg(I.out_ptr + g);
+          len = static_cast<int>(__ldg(I.out_end + g) - e0);
+        }
       }
       while (k < own) {
         // Clusters take the next row pair from a shared counter (their few,
@@ -1121,20 +1161,36 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
         }
         int64_t n0 = 0;
         int nlen = 0;
+        const int32_t* nrowp = nullptr;
+        int next_ext = 0;
         if (kn + h < own) {  // next rows' offsets in flight during these rows
           const int gn = list[kn + h];
-          n0 = __ldg(I.out_ptr + gn);
-          nlen = static_cast<int>(__ldg(I.out_end + gn) - n0);
+          if (viewed) {
+            pool_out_row(gn, &n0, &nlen, &nrowp, &next_ext);
+          } else {
+            n0 = __ldg(I.out_ptr + gn);
+            nlen = static_cast<int>(__ldg(I.out_end + gn) - n0);
+          }
         }
         const int lmax = rows_max<kRows>(len);
         if (counting && hl == 0 && len > 0) atomicAdd(&sh.cnt_out, static_cast<unsigned long long>(len));
-        const int32_t* ocol = I.out_col + e0 + hl;  // lane base pointer (see P5)
+        const bool mapped = viewed && rowp == nullptr;  // pool row: entries are pool points
+        const int32_t* ocol = (viewed ? (rowp ? rowp : PV.out_col + e0) : I.out_col + e0) + hl;
         const int lim = len - hl;
+        if (viewed && hl == 0 && ext) {  // the row's edges into g (n - 1) and init (n)
+          if (PV.subst && (ext & 2)) atomicOr(cand_w + ((I.n - 2) >> 5), 1u << ((I.n - 2) & 31));
+          if (ext & 8) atomicOr(cand_w + ((I.n - 1) >> 5), 1u << ((I.n - 1) & 31));
+        }
         for (int off = 0; off < lmax; off += kLanesPerRow * kUnroll) {
           int xs[kUnroll];
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u)
             xs[u] = off + u * kLanesPerRow < lim ? __ldg(ocol + off + u * kLanesPerRow) : -1;
+          if (mapped) {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+              if (xs[u] >= 0) xs[u] = pool_rank(xs[u]);
+          }
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
             if (off + u * kLanesPerRow >= lmax) break;  // warp-uniform
@@ -1167,6 +1223,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
         k = kn;
         e0 = n0;
         len = nlen;
+        rowp = nrowp;
+        ext = next_ext;
       }
     }
     cluster_barrier<CS>();  // [1] candidate marks complete
@@ -1203,10 +1261,34 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
       int x = -1;
       int64_t e0 = 0;
       int len = 0;
+      // Shared-pool views: the candidate's in-row is its pool row (mapped,
+      // then its edges from g / init, code bits 0 / 2, at positions len,
+      // len + 1) or, for g, its own in-list.  (init is open from the start,
+      // so it is never a candidate.)
+      int ext = 0;
+      bool spec_row = false;
+      auto pool_in_row = [&](int xv, int64_t* pe0, int* plen, bool* pspec, int* pext) {
+        if (PV.subst && xv == I.n - 2) {
+          *pspec = true;
+          *pe0 = 0;
+          *plen = PV.spec_len[1];
+          *pext = 0;
+        } else {
+          const int p = __ldg(PV.sel + xv);
+          *pspec = false;
+          *pe0 = __ldg(PV.in_ptr + p);
+          *plen = static_cast<int>(__ldg(PV.in_ptr + p + 1) - *pe0);
+          *pext = __ldg(PV.code + xv);
+        }
+      };
       if (k + h < ccount) {
         x = list[k + h];
-        e0 = __ldg(I.in_ptr + x);
-        len = static_cast<int>(__ldg(I.in_end + x) - e0);
+        if (viewed) {
+          pool_in_row(x, &e0, &len, &spec_row, &ext);
+        } else {
+          e0 = __ldg(I.in_ptr + x);
+          len = static_cast<int>(__ldg(I.in_end + x) - e0);
+        }
       }
       while (k < ccount) {
         int kn = k + kRows * nw;
@@ -1217,7 +1299,12 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
         int xn = -1;
         int64_t n0 = 0;
         int nlen = 0;
-        if (kn + h < ccount) {
+        int next_ext = 0;
+        bool next_spec = false;
+        if (kn + h < ccount && viewed) {
+          xn = list[kn + h];
+          pool_in_row(xn, &n0, &nlen, &next_spec, &next_ext);
+        } else if (kn + h < ccount) {
           xn = list[kn + h];
           n0 = __ldg(I.in_ptr + xn);
           nlen = static_cast<int>(__ldg(I.in_end + xn) - n0);
@@ -1247,8 +1334,11 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
         if (counting && hl == 0 && len > 0) atomicAdd(&sh.cnt_in, static_cast<unsigned long long>(len));
         // Lane base pointers, formed once per row: the chunk loads below are
         // then immediate offsets from them (no per-element address math).
-        const int32_t* rcol = I.in_col + e0 + hl;
-        const double* rcost = I.in_cost + e0 + hl;
+        const bool mapped = viewed && !spec_row;
+        const int32_t* rcol =
+            (viewed ? (spec_row ? PV.scol + PV.cap : PV.in_col + e0) : I.in_col + e0) + hl;
+        const double* rcost =
+            (viewed ? (spec_row ? PV.scost + PV.cap : PV.in_cost + e0) : I.in_cost + e0) + hl;
         const int lim = len - hl;  // element u of chunk `off` exists iff off + u * kLanesPerRow < lim
         for (int off = 0; off < lmax; off += kLanesPerRow * kUnroll) {
           int ys[kUnroll];
@@ -1258,6 +1348,11 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
             const bool in = off + u * kLanesPerRow < lim;
             ys[u] = in ? __ldg(rcol + off + u * kLanesPerRow) : -1;
             cs[u] = in ? __ldg(rcost + off + u * kLanesPerRow) : 0.0;
+          }
+          if (mapped) {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+              if (ys[u] >= 0) ys[u] = pool_rank(ys[u]);
           }
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
@@ -1273,6 +1368,26 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
               bo = off + u * kLanesPerRow + hl;
               by = y;
             }
+          }
+        }
+        if (viewed && hl == 0 && x >= 0 && ext) {
+          // the in-edges from g (n - 1) and init (n): positions after the row
+          int pos = len;
+          for (int t = 0; t < 2; ++t) {
+            const bool has = t == 0 ? (PV.subst && (ext & 1)) : ((ext & 4) != 0);
+            if (!has) continue;
+            const int y = t == 0 ? I.n - 2 : I.n - 1;
+            const int l = t == 0 ? 0 : 2;
+            const int j = __ldg(PV.spj + 2 * x + t);
+            const bool op = (open_w[y >> 5] >> (y & 31)) & 1u;
+            if constexpr (COUNT || CS > 1) cnt_open += op ? 1 : 0;
+            const double c = __dadd_rn(cost_s[y], __ldg(PV.scost + static_cast<int64_t>(l) * PV.cap + j));
+            if (op && c < bv) {
+              bv = c;
+              bo = pos;
+              by = y;
+            }
+            ++pos;
           }
         }
         // Group argmin of (cost, position) == the reference's strict-<
@@ -1313,6 +1428,17 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
         // parents' coordinates in flight together.
         double tau_b = 0.0;
         if ((D == 0 || D == 6) && bo >= 0 && I.in_tau) tau_b = __ldg(I.in_tau + e0 + bo);
+        if (viewed && bo >= 0) {
+          if (spec_row) {
+            tau_b = __ldg(PV.stau + PV.cap + bo);
+          } else if (bo < len) {
+            tau_b = __ldg(PV.in_tau + e0 + bo);
+          } else {  // an edge from g or init (at len: g when present, else init)
+            const int t = (bo == len && PV.subst && (ext & 1)) ? 0 : 1;
+            const int j = __ldg(PV.spj + 2 * x + t);
+            tau_b = __ldg(PV.stau + static_cast<int64_t>(t == 0 ? 0 : 2) * PV.cap + j);
+          }
+        }
         if constexpr (kLanesPerRow >= kMaxSolveDim) {
           if (bo >= 0 && hl < d) segh[hl] = __ldg(I.coords + static_cast<int64_t>(by) * d + hl);
         } else {
@@ -1324,7 +1450,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
         // concurrently, one per half warp (their row scans and argmins
         // already are); the values of half h are its own lanes'.
         if constexpr (D == 6 && kRows == 2) {
-          if (I.in_tau && (I.kin_segments + 1) * 6 <= kTabCap && I.kin_segments <= 14) {
+          if ((I.in_tau || viewed) && (I.kin_segments + 1) * 6 <= kTabCap && I.kin_segments <= 14) {
             const uint32_t gmask = h ? 0xffff0000u : 0x0000ffffu;
             if (bo >= 0) {
               if (hl == 0) atomicAdd(&sh.wchecks[warp], 1);
@@ -1344,6 +1470,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
             x = xn;
             e0 = n0;
             len = nlen;
+            ext = next_ext;
+            spec_row = next_spec;
             continue;
           }
         }
@@ -1398,6 +1526,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
         x = xn;
         e0 = n0;
         len = nlen;
+        ext = next_ext;
+        spec_row = next_spec;
       }
     }
     if (lane == 0) {
@@ -1744,10 +1874,10 @@ cudaError_t launch_dijkstra(const DevInstance* inst, const SolveJob* job, int n,
   }
 }
 
-template <int CS, int D, bool WIDE, bool COUNT, bool GS = false>
+template <int CS, int D, bool WIDE, bool COUNT, bool GS = false, bool POOL = false>
 static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_t smem,
                              int obs_in_smem, cudaStream_t stream) {
-  auto kern = gmt_solve_kernel<CS, D, WIDE, COUNT, GS>;
+  auto kern = gmt_solve_kernel<CS, D, WIDE, COUNT, GS, POOL>;
   // Function attributes are process-wide: the dynamic shared-memory limit
   // only ever grows (under a lock), so concurrent launches from several host
   // threads (each with its own context / stream) never see it shrink below
@@ -1798,7 +1928,16 @@ static cudaError_t launch_dim(const SolveJob* jobs, int count, int threads, size
 }
 
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
-                         int obs_in_smem, int dim, cudaStream_t stream, bool count_traffic, bool gstate) {
+                         int obs_in_smem, int dim, cudaStream_t stream, bool count_traffic, bool gstate,
+                         bool pool) {
+  if (pool) {  // shared-pool views (batched DI queries): single CTAs
+    if (cluster != 1 || dim != 6 || gstate) return cudaErrorInvalidValue;
+    if (threads > 256)
+      return count_traffic ? launch_cs<1, 6, true, true, false, true>(jobs, count, threads, smem, obs_in_smem, stream)
+                           : launch_cs<1, 6, true, false, false, true>(jobs, count, threads, smem, obs_in_smem, stream);
+    return count_traffic ? launch_cs<1, 6, false, true, false, true>(jobs, count, threads, smem, obs_in_smem, stream)
+                         : launch_cs<1, 6, false, false, false, true>(jobs, count, threads, smem, obs_in_smem, stream);
+  }
   if (gstate) {  // global-memory wavefront: one wide CTA per query
     if (cluster != 1 || threads != 512) return cudaErrorInvalidValue;
     return launch_dim<1, true, false, true>(jobs, count, threads, 0, obs_in_smem, dim, stream);

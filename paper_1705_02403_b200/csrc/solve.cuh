@@ -59,9 +59,11 @@ __host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool o
 // count_traffic: the jobs carry traffic counters (GMT_OPT_COUNTERS).
 // gstate: every job carries a global state buffer (SolveJob::gstate) of the
 // solve_layout size; cluster must be 1 and threads 512.
+// pool: the jobs may carry shared-pool views (DevInstance::pool); d = 6,
+// cluster 1.
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
                          int obs_in_smem, int dim, cudaStream_t stream, bool count_traffic = false,
-                         bool gstate = false);
+                         bool gstate = false, bool pool = false);
 
 // dijkstra_oracle (planner.cpp:264-334): eager edge checks into ok[E] (and
 // the check count), then the Dijkstra search for job[0] (one CTA).

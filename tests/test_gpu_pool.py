@@ -145,3 +145,24 @@ def test_pool_rare_paths(ctx):
         assert (summ[q].status, summ[q].cost, summ[q].iterations) == (r.status, r.cost, r.iterations), q
         _same_graph(pb.graph(k), ctx.batch([inst], 1.0).graph(0))
         k += 1
+
+
+def test_pool_views_equal_materialised_rows(ctx, monkeypatch):
+    """gmt_plan_problems reads each query's graph through its rank map over
+    the pool rows; device-resident batches materialise every derived row
+    (GMT_POOL_ROWS=0/1 forces either).  Both give the same graphs and the
+    same full results, and plan_problems the same summaries either way."""
+    specs = _specs(24, first=300)
+    monkeypatch.setenv("GMT_POOL_ROWS", "0")
+    pv, _ = ctx.batch_problems(specs)
+    sv = ctx.plan_problems(specs)[1]
+    monkeypatch.setenv("GMT_POOL_ROWS", "1")
+    pm, _ = ctx.batch_problems(specs)
+    sm = ctx.plan_problems(specs)[1]
+    monkeypatch.delenv("GMT_POOL_ROWS")
+    assert [(a.status, a.cost, a.iterations) for a in sv] == [(a.status, a.cost, a.iterations) for a in sm]
+    pv.launch()
+    pm.launch()
+    for q in range(len(specs)):
+        _same_graph(pv.graph(q), pm.graph(q))
+        assert not abi.full_parity(pv.result(q), pm.result(q))
