@@ -143,6 +143,7 @@ struct gmt_batch {
   int threads = 256;
   int dim = 0;  // common dimension of the queries (0: mixed)
   bool pool = false;  // some jobs read shared-pool views (launch_solve's pool mode)
+  bool lpt_done = false;  // the device job table is in largest-first order (gmt_batch_summaries)
   ~gmt_batch() {
     res.release();
     jobs_mem.release();
