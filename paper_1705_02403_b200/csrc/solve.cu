@@ -961,7 +961,10 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
   }
   __syncthreads();
   const Boxes& bx = bx_s;  // read from shared memory where used
-  auto pool_rank = [&](int y) -> int {  // shared-pool views: pool point -> query vertex (or -1)
+  // Shared-pool views: pool point y -> query vertex (or -1).  (A shared-
+  // memory bitmask + rank bases measured slower than this L1-cached gather:
+  // 46.6 vs 41.9 ms per 4096 queries.)
+  auto pool_rank = [&](int y) -> int {
     const uint16_t r = __ldg(PV.rank + y);
     return r == kPoolNoRank ? -1 : static_cast<int>(r);
   };
