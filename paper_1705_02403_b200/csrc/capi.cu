@@ -229,9 +229,11 @@ extern "C" int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value) {
     case GMT_OPT_THREADS:
     case GMT_OPT_BATCH_THREADS: {
       const int cap = 512;  // <= 256: narrow CTA shape, above: wide (solve.cu)
-      if (value != 0 && (value < 32 || value > cap || value % 32 != 0))
-        return set_error(GMT_E_INVALID_INPUT, "threads must be 0 or a multiple of 32 up to " +
-                                                  std::to_string(cap));
+      // (768: the 24-warp batched double-integrator shape, GMT_OPT_BATCH_THREADS only)
+      const bool di24 = option == GMT_OPT_BATCH_THREADS && value == 768;
+      if (value != 0 && !di24 && (value < 32 || value > cap || value % 32 != 0))
+        return set_error(GMT_E_INVALID_INPUT, "threads must be 0, a multiple of 32 up to " +
+                                                  std::to_string(cap) + ", or 768 (batched 6D)");
       (option == GMT_OPT_THREADS ? ctx->threads : ctx->batch_threads) = static_cast<int>(value);
       return GMT_OK;
     }
@@ -786,6 +788,14 @@ extern "C" int gmt_plan_host(gmt_ctx* ctx, const gmt_scene* scene, const double*
 }
 
 // ---- batches (struct gmt_batch: internal.cuh) -------------------------------------------
+// The common dimension of a batch's instances (0: mixed).
+static int b_dim_of(gmt_instance* const* insts, int count) {
+  int d = insts[0]->desc.dim;
+  for (int q = 1; q < count; ++q)
+    if (insts[q]->desc.dim != d) return 0;
+  return d;
+}
+
 extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const* insts,
                                 const int32_t* init_index, double lambda, gmt_batch** out) {
   gmtb::AllocScope alloc_scope_(ctx);
@@ -817,11 +827,10 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
   // on single narrow CTAs (4096 DI queries: 47 ms vs 52 ms on wide CTAs and
   // 66 ms on 2-CTA clusters, tools/di_sweep.py).
   b->cluster = ctx->batch_cluster;
-  if (b->cluster == 0) {
-    b->cluster = 1;
-    for (int q = 0; q < count; ++q)
-      if (insts[q]->desc.steering != GMT_STEER_EUCLIDEAN && count < 4 * ctx->sm_count) b->cluster = 2;
-  }
+  bool kino = false;
+  for (int q = 0; q < count; ++q) kino = kino || insts[q]->desc.steering != GMT_STEER_EUCLIDEAN;
+  const bool di6 = kino && b_dim_of(insts, count) == 6;
+  if (b->cluster == 0) b->cluster = di6 ? 1 : (kino && count < 4 * ctx->sm_count ? 2 : 1);
   size_t gs = 0;
   int rc = plan_smem(ctx, max_n, max_d, max_nb, b->cluster, &b->smem, &b->obs, &gs);
   if (rc == GMT_OK && gs) b->cluster = 1;
@@ -842,7 +851,8 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
     j.lambda = lambda;
     j.radius = insts[q]->desc.radius;
   }
-  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
+  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : (di6 ? 768 : 256));
+  if (b->threads == 768 && (b->cluster != 1 || !di6)) b->threads = b->cluster > 1 ? 512 : 256;
   if (gs) {
     b->threads = 512;
     rc = assign_gstate(b->gstate_mem, b->jobs, gs);

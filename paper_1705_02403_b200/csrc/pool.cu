@@ -1191,9 +1191,16 @@ static int batch_from_derived(gmt_ctx* ctx, gmt_batch* b, const gmt_problem* pro
   b->dim = d;
   // (the shape gmt_batch_create picks: 2-CTA clusters for a few kinodynamic
   // queries, one CTA each once they fill the SMs several times over)
-  b->cluster = ctx->batch_cluster ? ctx->batch_cluster : (kino && J < 4 * ctx->sm_count ? 2 : 1);
+  // Batched 6D double integrators: one 24-warp CTA per query (the shape
+  // that measured best at every batch size: 4096 queries 34.4 ms vs 36.1 on
+  // narrow CTAs, 512 queries 4.7 vs 5.8 ms; tools/scale_probe.py); other
+  // kinodynamic queries: 2-CTA clusters while they fill the SMs less than
+  // four times, single CTAs beyond.
+  const bool di6 = kino && d == 6;
+  b->cluster = ctx->batch_cluster ? ctx->batch_cluster : (di6 ? 1 : (kino && J < 4 * ctx->sm_count ? 2 : 1));
   if (b->pool) b->cluster = 1;  // (pool views are read by single-CTA solves)
-  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : 256);
+  b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : (di6 ? 768 : 256));
+  if (b->threads == 768 && (b->cluster != 1 || d != 6)) b->threads = b->cluster > 1 ? 512 : 256;
   size_t gs = 0;
   int rc = plan_smem(ctx, max_V, d, max_nb, b->cluster, &b->smem, &b->obs, &gs);
   if (rc) return rc;

@@ -100,8 +100,8 @@ struct CtaShared {
   long long iter;
   long long total_checks;
   int32_t pass;
-  int32_t wchecks[16];
-  int32_t wadded[16];
+  int32_t wchecks[32];
+  int32_t wadded[32];
   unsigned long long cnt_in, cnt_out;
 };
 
@@ -813,11 +813,15 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 // POOL: jobs may carry shared-pool views (DevInstance::pool, batched DI
 // queries): their rows are read from the pool graph through the query's
 // rank map instead of materialised rows.
-template <int CS, int D, bool WIDE, bool COUNT, bool GS = false, bool POOL = false>
-__global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 0) ? 3 : GMT_BATCH_MIN_BLOCKS))
+// NW != 0: a CTA of NW warps at one per SM (the batched double integrator's
+// latency shape for batches of a few waves: 24 warps = the SM's three narrow
+// CTAs' worth on one query, 80 registers).
+template <int CS, int D, bool WIDE, bool COUNT, bool GS = false, bool POOL = false, int NW = 0>
+__global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
+                                  NW ? 1 : (WIDE ? 1 : ((D == 6 || D == 0) ? 3 : GMT_BATCH_MIN_BLOCKS)))
     gmt_solve_kernel(const SolveJob* __restrict__ jobs, int obs_in_smem) {
   constexpr bool kParentSmem = CS > 1;  // single-CTA solves keep parents in HBM
-  constexpr int kMaxWarps = WIDE ? 16 : 8;
+  constexpr int kMaxWarps = NW ? NW : (WIDE ? 16 : 8);
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   // Rows streamed concurrently per warp in P4/P5: two for batched
@@ -955,7 +959,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : ((D == 6 || D == 
     sh.cnt_out = 0ull;
     bx_s = bxl;
   }
-  if (tid < 16) {
+  if (tid < 32) {
     sh.wchecks[tid] = 0;
     sh.wadded[tid] = 0;
   }
@@ -1877,10 +1881,10 @@ cudaError_t launch_dijkstra(const DevInstance* inst, const SolveJob* job, int n,
   }
 }
 
-template <int CS, int D, bool WIDE, bool COUNT, bool GS = false, bool POOL = false>
+template <int CS, int D, bool WIDE, bool COUNT, bool GS = false, bool POOL = false, int NW = 0>
 static cudaError_t launch_cs(const SolveJob* jobs, int count, int threads, size_t smem,
                              int obs_in_smem, cudaStream_t stream) {
-  auto kern = gmt_solve_kernel<CS, D, WIDE, COUNT, GS, POOL>;
+  auto kern = gmt_solve_kernel<CS, D, WIDE, COUNT, GS, POOL, NW>;
   // Function attributes are process-wide: the dynamic shared-memory limit
   // only ever grows (under a lock), so concurrent launches from several host
   // threads (each with its own context / stream) never see it shrink below
@@ -1933,6 +1937,13 @@ static cudaError_t launch_dim(const SolveJob* jobs, int count, int threads, size
 cudaError_t launch_solve(const SolveJob* jobs, int count, int cluster, int threads, size_t smem,
                          int obs_in_smem, int dim, cudaStream_t stream, bool count_traffic, bool gstate,
                          bool pool) {
+  if (cluster == 1 && dim == 6 && threads == 768 && !gstate) {  // the 24-warp latency shape (D = 6)
+    if (pool)
+      return count_traffic ? launch_cs<1, 6, false, true, false, true, 24>(jobs, count, threads, smem, obs_in_smem, stream)
+                           : launch_cs<1, 6, false, false, false, true, 24>(jobs, count, threads, smem, obs_in_smem, stream);
+    return count_traffic ? launch_cs<1, 6, false, true, false, false, 24>(jobs, count, threads, smem, obs_in_smem, stream)
+                         : launch_cs<1, 6, false, false, false, false, 24>(jobs, count, threads, smem, obs_in_smem, stream);
+  }
   if (pool) {  // shared-pool views (batched DI queries): single CTAs
     if (cluster != 1 || dim != 6 || gstate) return cudaErrorInvalidValue;
     if (threads > 256)
