@@ -337,7 +337,7 @@ def run_b200(args):
     peak, peak_kind = measured_peak_hbm()
     achieved = b_alg / (solo_ms / 1e3) / 1e9
     clocks = clk.summary()
-    kname = "gmt_solve_kernel<1,6,0,0,0>"
+    kname = "gmt_solve_kernel<1,6,0,0,0,0,24>"
     traffic, traffic_src = ncu_traffic(kname + ":di6d_q4096")
 
     batch.close()

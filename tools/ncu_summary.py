@@ -44,7 +44,9 @@ def main():
             doc = json.load(f)
     except Exception:
         doc = {"kernels": {}}
-    sha = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True).stdout.strip()
+    import os
+    sha = os.environ.get("GIT_SHA") or subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True,
+                                                      text=True).stdout.strip()
     for arg in sys.argv[2:]:
         label, spec = arg.split("=", 1)
         rep, _, kre = spec.partition(":")
