@@ -853,6 +853,14 @@ extern "C" int gmt_batch_create(gmt_ctx* ctx, int32_t count, gmt_instance* const
   }
   b->threads = ctx->batch_threads ? ctx->batch_threads : (b->cluster > 1 ? 512 : (di6 ? 768 : 256));
   if (b->threads == 768 && (b->cluster != 1 || !di6)) b->threads = b->cluster > 1 ? 512 : 256;
+  if (!gs && solve_dyn_scratch(b->threads, b->dim)) {  // (the 24-warp shape's scratch)
+    const size_t total = align16(b->smem) + solve_dyn_scratch(b->threads, b->dim);
+    if (total <= ctx->smem_optin) {
+      b->smem = total;
+    } else {
+      b->threads = 256;
+    }
+  }
   if (gs) {
     b->threads = 512;
     rc = assign_gstate(b->gstate_mem, b->jobs, gs);

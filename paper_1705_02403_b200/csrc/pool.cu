@@ -1204,6 +1204,14 @@ static int batch_from_derived(gmt_ctx* ctx, gmt_batch* b, const gmt_problem* pro
   size_t gs = 0;
   int rc = plan_smem(ctx, max_V, d, max_nb, b->cluster, &b->smem, &b->obs, &gs);
   if (rc) return rc;
+  if (!gs && solve_dyn_scratch(b->threads, d)) {  // (the 24-warp shape's scratch)
+    const size_t total = align16(b->smem) + solve_dyn_scratch(b->threads, d);
+    if (total <= ctx->smem_optin) {
+      b->smem = total;
+    } else {
+      b->threads = 256;  // (too large for the 24-warp shape's scratch)
+    }
+  }
 
   if (gs) {  // too large for shared memory: global-memory wavefronts, one wide CTA each
     b->cluster = 1;

@@ -67,6 +67,7 @@ constexpr double kSepMargin = 1e-9;  // see segment_free_staged
 #define GMT_ROWS_CLUSTER 1
 #endif
 
+
 // Longest of the rows the kRows lane groups of a warp are streaming.
 template <int kRows>
 __device__ __forceinline__ int rows_max(int len) {
@@ -615,16 +616,19 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
   return true;
 }
 
-// The double integrator's lazy check on a 16-lane group (a half warp), so
-// the two candidates a batched warp scans are checked concurrently: the same
+// The double integrator's lazy check on a G-lane group (half or quarter warp),
+// so the candidates a batched warp scans are checked concurrently: the same
 // steps as kino_edge_free_warp's table path (waypoint table from the cubic
 // coefficients, cube test, polyline bounding-box cull, one lane per
 // (segment, box) pair through the reference's clip) with group-masked votes.
 // seg: the group's 32 staged doubles (a = [0..6), b = [16..22)); tab: its
 // waypoint table ((M + 1) * 6 <= 64); cull: its box list.
+template <int G>
 __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double tau, int gl, uint32_t gmask,
                                   int gbase, double* seg, double* tab, uint16_t* cull, int cull_cap, bool vfull) {
-  constexpr int G = 16, dim = kDiDim;
+  constexpr int dim = kDiDim;
+  static_assert(G >= 8, "a group must hold a state's coordinates and the coefficient lanes");
+  constexpr uint32_t kGroupBits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
   const int M = I.kin_segments;
   DiParams DP;
   DP.vmax = I.kin_p[0];
@@ -652,13 +656,14 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     const double tt = di_mul(tau, tau);
     seg[gl] = di_sub(di_div(di_mul(3.0, D), tt), di_div(di_add(di_mul(2.0, v0), v1), tau));
     seg[3 + gl] = di_sub(di_div(di_add(v0, v1), tt), di_div(di_mul(2.0, D), di_mul(tt, tau)));
-  } else if (gl - 2 < M) {
-    const int k = gl - 2;
-    const double tk = di_mul(tau, static_cast<double>(k));
-    // (tau k) / M: for M a power of two the quotient is the exact scaling
-    // tk * (1 / M) unless it would be subnormal -- the same double
-    seg[6 + k] = ((M & (M - 1)) == 0 && tk >= 1e-290) ? di_mul(tk, 1.0 / static_cast<double>(M))
-                                                       : di_div(tk, static_cast<double>(M));
+  } else {
+    for (int k = gl - 2; k < M; k += G - 3) {
+      const double tk = di_mul(tau, static_cast<double>(k));
+      // (tau k) / M: for M a power of two the quotient is the exact scaling
+      // tk * (1 / M) unless it would be subnormal -- the same double
+      seg[6 + k] = ((M & (M - 1)) == 0 && tk >= 1e-290) ? di_mul(tk, 1.0 / static_cast<double>(M))
+                                                         : di_div(tk, static_cast<double>(M));
+    }
   }
   __syncwarp(gmask);
   bool incube = true;
@@ -727,7 +732,7 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
         meets = meets && !(pmx[k] < lo || pmn[k] > hi);
       }
     }
-    const uint32_t m = (__ballot_sync(gmask, meets) >> gbase) & 0xffffu;
+    const uint32_t m = (__ballot_sync(gmask, meets) >> gbase) & kGroupBits;
     const int at = kept + __popc(m & ((1u << gl) - 1u));
     if (meets && at < cull_cap) cull[at] = static_cast<uint16_t>(b);
     kept += __popc(m);
@@ -827,18 +832,26 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
   // Rows streamed concurrently per warp in P4/P5: two for batched
   // single-CTA solves (latency hiding), one for clusters (few candidates per
   // warp; the pass critical path matters).
-  constexpr int kRows = CS == 1 ? GMT_ROWS_PER_WARP : GMT_ROWS_CLUSTER;
+  // (the 24-warp batched DI shape streams and checks four candidates per warp)
+  constexpr int kRows = CS == 1 ? ((D == 6 && NW == 24) ? GMT_ROWS_DI24 : GMT_ROWS_PER_WARP) : GMT_ROWS_CLUSTER;
   constexpr int kLanesPerRow = kWarp / kRows;
   constexpr int kUnroll = CS == 1 ? GMT_UNROLL_BATCH : GMT_UNROLL_CLUSTER;
   constexpr bool kDynamic = CS > 1;  // dynamic row / candidate distribution
-  __shared__ double seg_s[kMaxWarps * 32 * kRows];  // per warp: kRows staged segments
-  // Kinodynamic waypoint tables (double integrator: D = 6; quadrotor: D = 0).
-  // (batched DI solves check two edges per warp at once: two tables / lists)
-  constexpr int kTabCap = D == 6 ? 64 : (D == 0 ? 144 : 1);
-  constexpr int kKinSlots = (D == 6 && kRows == 2) ? 2 : 1;
-  __shared__ double tab_s[(D == 0 || D == 6) ? kMaxWarps * kTabCap * kKinSlots : 1];
+  // Per-warp scratch: kRows staged segments, kinodynamic waypoint tables
+  // (double integrator: D = 6; quadrotor: D = 0) and surviving-box lists --
+  // batched DI solves check kRows edges per warp at once (one table / list
+  // each).  NW kernels (more than the 48 KB of static shared memory) keep it
+  // in dynamic shared memory after the solve layout (solve_dyn_scratch).
+  constexpr int kTabCap = D == 6 ? kDiTabCap : (D == 0 ? 144 : 1);
+  constexpr int kKinSlots = (D == 6 && kRows >= 2) ? kRows : 1;
   constexpr int kCullCap = (D == 0 || D == 6) ? 64 : 1;  // per-warp surviving-box list
-  __shared__ uint16_t cull_s[kMaxWarps * kCullCap * kKinSlots];
+  constexpr bool kDynScratch = NW != 0;
+  constexpr int kSegN = kMaxWarps * 32 * kRows;
+  constexpr int kTabN = (D == 0 || D == 6) ? kMaxWarps * kTabCap * kKinSlots : 1;
+  constexpr int kCullN = kMaxWarps * kCullCap * kKinSlots;
+  __shared__ double seg_st[kDynScratch ? 1 : kSegN];
+  __shared__ double tab_st[kDynScratch ? 1 : kTabN];
+  __shared__ uint16_t cull_st[kDynScratch ? 1 : kCullN];
 
   const int q = blockIdx.x / CS;
   int rank = 0;
@@ -877,6 +890,15 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
   uint32_t* cand_w = newopen_w + L.words_pad;
   uint32_t* goal_w = cand_w + L.words_pad;
   ListT* list = reinterpret_cast<ListT*>(sbase + L.off_list);
+  double* seg_s = seg_st;
+  double* tab_s = tab_st;
+  uint16_t* cull_s = cull_st;
+  if constexpr (kDynScratch) {
+    unsigned char* scratch = smem + align16(L.total);
+    seg_s = reinterpret_cast<double*>(scratch);
+    tab_s = seg_s + kSegN;
+    cull_s = reinterpret_cast<uint16_t*>(tab_s + kTabN);
+  }
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
@@ -1315,7 +1337,7 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
           xn = list[kn + h];
           n0 = __ldg(I.in_ptr + xn);
           nlen = static_cast<int>(__ldg(I.in_end + xn) - n0);
-          if constexpr (D == 6 && kRows == 2) {
+          if constexpr (D == 6 && kRows >= 2) {
             // (DI: a lazy check outlasts a row fetch -- the next rows are
             // pulled into L2 by the TMA engine meanwhile)
             // (not in_tau: one duration per row is read, after the argmin)
@@ -1456,14 +1478,15 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
         // Batched double-integrator solves: the two candidates are checked
         // concurrently, one per half warp (their row scans and argmins
         // already are); the values of half h are its own lanes'.
-        if constexpr (D == 6 && kRows == 2) {
+        if constexpr (D == 6 && kRows >= 2) {
           if ((I.in_tau || viewed) && (I.kin_segments + 1) * 6 <= kTabCap && I.kin_segments <= 14) {
-            const uint32_t gmask = h ? 0xffff0000u : 0x0000ffffu;
+            constexpr uint32_t kGroup = kLanesPerRow == 32 ? 0xffffffffu : ((1u << kLanesPerRow) - 1u);
+            const uint32_t gmask = kGroup << (kLanesPerRow * h);
             if (bo >= 0) {
               if (hl == 0) atomicAdd(&sh.wchecks[warp], 1);
-              const bool ok = di_edge_free_half(I, bx_s, tau_b, hl, gmask, 16 * h, segh,
-                                                tab_s + warp * kTabCap * 2 + h * kTabCap,
-                                                cull_s + warp * kCullCap * 2 + h * kCullCap, kCullCap, sh.vfull);
+              const bool ok = di_edge_free_half<kLanesPerRow>(
+                  I, bx_s, tau_b, hl, gmask, kLanesPerRow * h, segh, tab_s + (warp * kRows + h) * kTabCap,
+                  cull_s + (warp * kRows + h) * kCullCap, kCullCap, sh.vfull);
               if (ok && hl == 0) {
                 atomicAdd(&sh.wadded[warp], 1);
                 cost_s[x] = bv;

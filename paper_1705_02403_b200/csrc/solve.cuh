@@ -54,6 +54,20 @@ __host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool o
   return L;
 }
 
+// Dynamic shared memory the solve kernel appends after the layout for its
+// per-warp scratch (the 24-warp batched double-integrator shape, 768
+// threads: 24 warps x GMT_ROWS_DI24 concurrent checks x (32 + kDiTabCap)
+// doubles + 64 box ids);
+// 0 for the other shapes (static shared memory).
+#ifndef GMT_ROWS_DI24
+#define GMT_ROWS_DI24 4  // concurrent candidates (rows, checks) per warp of the 24-warp DI shape
+#endif
+constexpr int kDiTabCap = 56;  // doubles of one DI waypoint table ((segments + 1) * 6 <= 56)
+inline size_t solve_dyn_scratch(int threads, int dim) {
+  if (threads != 768 || dim != 6) return 0;
+  return static_cast<size_t>(24) * GMT_ROWS_DI24 * ((32 + kDiTabCap) * sizeof(double) + 64 * sizeof(uint16_t));
+}
+
 // dim: the common dimension of every job (selects the specialised kernel;
 // 0 = generic).
 // count_traffic: the jobs carry traffic counters (GMT_OPT_COUNTERS).

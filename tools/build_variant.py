@@ -12,11 +12,13 @@ from paper_1705_02403_b200 import build as B  # noqa: E402
 name, defs = sys.argv[1], sys.argv[2:]
 obj = os.path.join(ROOT, "build", "variants", name)
 os.makedirs(obj, exist_ok=True)
-objs = []
-for src in B.SOURCES:
-    o = os.path.join(obj, src.replace(".cu", ".o"))
-    subprocess.run([B.NVCC, *B.FLAGS, *defs, "-c", os.path.join(B.CSRC, src), "-o", o], check=True)
+objs, procs = [], []
+for src in B.SOURCES:  # (in parallel)
+    o = os.path.join(obj, os.path.splitext(src)[0] + ".o")
+    procs.append(subprocess.Popen([B.NVCC, *B.FLAGS, *defs, "-c", os.path.join(B.CSRC, src), "-o", o]))
     objs.append(o)
+if any(p.wait() for p in procs):
+    sys.exit("nvcc failed")
 lib = os.path.join(ROOT, "build", "variants", f"libgmt_b200_{name}.so")
 subprocess.run([B.NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs,
                 "-cudart", "static"], check=True)
