@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--radius", type=float, default=1.6)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--single-reps", type=int, default=101)
+    ap.add_argument("--ref-reps", type=int, default=21, help="reference single-solve calls per leg")
     ap.add_argument("--cpu-sample", type=int, default=64, help="queries in the CPU baseline sample")
     ap.add_argument("--cpu-threads", type=int, default=0, help="reference threads (0: every host core)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -458,7 +459,9 @@ def run_b200(args):
 
 
 def secondary_legs(args, ctx, stream):
-    """configs[1-3] on one GPU: the 3D forest batch, single-solve p50s."""
+    """configs[0-3] on one GPU: the 3D forest batch; single-solve p50s with
+    the reference's single solve on the same instance beside each."""
+    import numpy as np
     import torch
     from paper_1705_02403_b200 import problem as P
     from paper_1705_02403_b200.native import OPT_BATCH_CLUSTER, OPT_BATCH_THREADS, ProblemBatch
@@ -511,27 +514,67 @@ def secondary_legs(args, ctx, stream):
             b1.close()
         return res
 
-    c2 = ctx.build_instance(P.forest_3d(3, args.n))
-    s2 = single_p50(c2)
-    out["c2_forest_single"] = {"p50_ms": min(s2.values()), "by_cluster": s2}
+    # The reference's single solve on the identical instance (SURVEY.md
+    # 8(d)(i)): gmt_plan(workers=1) and (workers=every core), median of
+    # --ref-reps calls each timed in C on the monotonic clock.
+    R, threads = None, cpu_threads(args)
+    if not args.no_cpu:
+        import oracle
+        R = oracle.ref() if oracle.ref_available() else None
+
+    def ref_single(time_fn):
+        if R is None:
+            return None
+        time_fn(1, 1)  # warm-up
+        w1 = float(np.median(time_fn(1, args.ref_reps)))
+        wn = float(np.median(time_fn(threads, args.ref_reps)))
+        return {"p50_ms_workers1": w1, f"p50_ms_workers{threads}": wn, "reps": args.ref_reps,
+                "kind": "reference (oracle/_ref gmt_plan)"}
+
+    def leg(name, spec, inst, ref_fn, **extra):
+        s = single_p50(inst)
+        r = ctx.plan(inst)
+        out[name] = {"p50_ms": min(s.values()), "by_cluster": s, "n": inst.n, "status": r.status,
+                     "cost": r.cost, "iterations": r.iterations, **extra}
+        rs = ref_single(ref_fn)
+        if rs is not None:
+            out[name]["reference_single"] = rs
+            out[name]["speedup_vs_workers1"] = rs["p50_ms_workers1"] / out[name]["p50_ms"]
+
+    with open(os.path.join(ROOT, "tests", "golden", "scene_texts.json")) as f:
+        c0 = P.parse_problem(json.load(f)["rectangles_2d"]).with_n(2000)
+    ri0 = R.instance_build(c0, threads) if R else None
+    leg("rect2d_single (configs[0])", c0, ctx.build_instance(c0),
+        lambda w, k: ri0.time_plans(c0.lam, w, k))
+    c1 = P.forest_3d(3, args.n)
+    ri1 = R.instance_build(c1, threads) if R else None
+    leg("c2_forest_single (configs[1])", c1, ctx.build_instance(c1),
+        lambda w, k: ri1.time_plans(1.0, w, k))
     t0 = time.perf_counter()
-    c3 = ctx.build_instance(P.di_forest(3, args.n))
+    c2 = P.di_forest(3, args.n)
+    inst2 = ctx.build_instance(c2)
     ctx.synchronize()
-    s3 = single_p50(c3)
-    out["di6d_single (configs[2])"] = {"p50_ms": min(s3.values()), "by_cluster": s3,
-                                       "device_build_ms": (time.perf_counter() - t0) * 1e3,
-                                       "mean_out_degree": c3.num_edges / c3.n}
+    build_ms = (time.perf_counter() - t0) * 1e3
+    ri2 = None
+    if R:
+        from paper_1705_02403_b200.problem import halton_pool_size
+        pool = R.di_pool(c2.start_index, halton_pool_size([c2]), c2.di_params(), c2.radius_override, threads)
+        [ri2] = R.di_instances(pool, [c2], 1)
+    leg("di6d_single (configs[2])", c2, inst2, lambda w, k: ri2.time_plans(1.0, w, k),
+        device_build_ms=build_ms, mean_out_degree=inst2.num_edges / inst2.n)
     if not args.no_quad:
-        spec4 = P.quad_scene()
+        c3 = P.quad_scene()
         t0 = time.perf_counter()
-        c4 = ctx.build_instance(spec4)
+        inst3 = ctx.build_instance(c3)
         ctx.synchronize()
         build_ms = (time.perf_counter() - t0) * 1e3
-        s4 = single_p50(c4)
-        r4 = ctx.plan(c4)
-        out["quad12d_single (configs[3])"] = {"p50_ms": min(s4.values()), "by_cluster": s4,
-                                              "device_build_ms": build_ms, "n": c4.n, "status": r4.status,
-                                              "cost": r4.cost, "iterations": r4.iterations}
+        fn3 = None
+        if R:
+            coords, gidx, _ = inst3.download()
+            G3 = ctx.build_quad_graph(coords, c3.quad_params(), c3.radius_override, paths=True)
+            fn3 = lambda w, k: R.time_gmt_plan(c3, coords, len(gidx), G3, inst3.init_index, 1.0,  # noqa: E731
+                                               c3.radius_override, w, k)
+        leg("quad12d_single (configs[3])", c3, inst3, fn3, device_build_ms=build_ms)
     return out
 
 

@@ -364,6 +364,11 @@ class RefLib(_Lib):
                                            C.c_double, _i32p, _i64p, _i64p, _i32p, _dp]
         L.ref_instance_plan.restype = C.c_int
         L.ref_instance_plan.argtypes = [C.c_void_p, C.c_double, C.c_int32, _P(abi.PlanOut)]
+        L.ref_instance_time_plans.restype = C.c_int
+        L.ref_instance_time_plans.argtypes = [C.c_void_p, C.c_double, C.c_int32, C.c_int32, _dp]
+        L.ref_time_gmt_plan.restype = C.c_int
+        L.ref_time_gmt_plan.argtypes = [_P(abi.Scene), _dp, C.c_int32, C.c_int32, _P(abi.GraphView), C.c_int32,
+                                        C.c_double, C.c_double, C.c_int32, C.c_int32, _dp]
         L.ref_plan_many.restype = C.c_int
         L.ref_plan_many.argtypes = [_P(C.c_void_p), C.c_int32, C.c_double, C.c_int32,
                                     _P(abi.PlanSummary), _dp]
@@ -399,6 +404,17 @@ class RefLib(_Lib):
         self._check(f(C.byref(sc), abi.ptr(a, C.c_double), abi.ptr(b, C.c_double), a.shape[0],
                       abi.ptr(out, C.c_uint8)))
         return out
+
+    def time_gmt_plan(self, spec, coords, goal_count, graph, init_index, lam, radius, workers, reps):
+        """Per-call ms of `reps` gmt_plan calls on an injected graph (timed in C)."""
+        coords = abi.f64(coords)
+        ms = np.zeros(reps)
+        sc = spec.scene()
+        gv = graph.view()
+        self._check(self.lib.ref_time_gmt_plan(C.byref(sc), abi.ptr(coords, C.c_double), coords.shape[0],
+                                               goal_count, C.byref(gv), init_index, lam, radius, workers,
+                                               reps, abi.ptr(ms, C.c_double)))
+        return ms
 
     def dijkstra_oracle(self, spec, coords, goal_count, graph, init_index):
         coords = abi.f64(coords)
@@ -659,6 +675,12 @@ class RefInstance:
             self.h, abi.ptr(coords, C.c_double), abi.ptr(gidx, C.c_int32), abi.ptr(ptr, C.c_int64),
             abi.ptr(col, C.c_int32), abi.ptr(cost, C.c_double)))
         return coords.reshape(n, dim), gidx[: inf["goal_count"]], ptr, col[:ne], cost[:ne]
+
+    def time_plans(self, lam: float, workers: int, reps: int):
+        """Per-call ms of `reps` gmt_plan calls on this instance (timed in C)."""
+        ms = np.zeros(reps)
+        self.lib._check(self.lib.lib.ref_instance_time_plans(self.h, lam, workers, reps, abi.ptr(ms, C.c_double)))
+        return ms
 
     def plan(self, lam: float, workers: int = 1):
         n = self.info()["n"]

@@ -588,6 +588,49 @@ int ref_instance_plan(void* h, double lambda, int32_t workers, gmt_plan_out* out
   });
 }
 
+// Single-solve CPU baseline: `reps` timed gmt_plan calls
+// on one prebuilt instance, each on the monotonic clock like the reference's
+// own `gmtplan plan` timer (tools/gmtplan.cpp:80-90), per-call ms in ms[].
+int ref_instance_time_plans(void* h, double lambda, int32_t workers, int32_t reps, double* ms) {
+  return guard([&] {
+    auto* ri = static_cast<RefInstance*>(h);
+    GmtParams params;
+    params.lambda = lambda;
+    params.radius = ri->inst.radius;
+    params.workers = workers;
+    for (int32_t k = 0; k < reps; ++k) {
+      auto t0 = std::chrono::steady_clock::now();
+      PlanResult r = gmt_plan(ri->inst.samples, ri->inst.graph, ri->problem.obstacles,
+                              ri->problem.goal, ri->inst.init_index, params);
+      ms[k] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      (void)r;
+    }
+  });
+}
+
+// The same on an injected graph (the 12D quadrotor: the device graph with its
+// waypoint polylines handed to the unmodified gmt_plan, planner.cpp:54-60).
+int ref_time_gmt_plan(const gmt_scene* scene, const double* coords, int32_t n, int32_t goal_count,
+                      const gmt_graph_view* graph, int32_t init_index, double lambda, double radius,
+                      int32_t workers, int32_t reps, double* ms) {
+  return guard([&] {
+    SampleSet s = to_samples(coords, nullptr, n, scene->dim, goal_count);
+    NeighborGraph g = to_graph(graph);
+    ObstacleSet obs = to_obs(scene);
+    GoalRegion goal = to_goal(scene);
+    GmtParams params;
+    params.lambda = lambda;
+    params.radius = radius;
+    params.workers = workers;
+    for (int32_t k = 0; k < reps; ++k) {
+      auto t0 = std::chrono::steady_clock::now();
+      PlanResult r = gmt_plan(s, g, obs, goal, init_index, params);
+      ms[k] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      (void)r;
+    }
+  });
+}
+
 // Batched CPU baseline: one gmt_plan(workers=1) per query under
 // parallel_chunks, the pattern of simulator.cpp:212.  Returns wall seconds
 // of the whole batch in *seconds.
