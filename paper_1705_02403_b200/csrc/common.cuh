@@ -86,6 +86,9 @@ struct DevInstance {
   // of the one edge it checks (di.cuh, quad.cuh).  kin_p: DI {vmax, weight},
   // quadrotor {g, vmax, amax, ymax, wmax, weight}.
   const double* in_tau;
+  // Optional per-in-edge waypoint tables ((kin_segments + 1) * dim doubles
+  // each, solve.cu kino_table_kernel): the checks read instead of regenerate.
+  const double* in_wp;
   // Out-edge views for the eager Dijkstra oracle: path ids of out-edges
   // (uploaded path graphs) and out-edge durations (kinodynamic).
   const int32_t* out_path;

@@ -81,6 +81,7 @@ struct gmt_instance {
   gmtb::Arena aux;       // device-built instances: goal index list etc.
   gmtb::Arena mem2;      // device-built directed graphs: the in-rows
   gmtb::Arena mem3;      // device-built Dubins graphs: edge paths
+  gmtb::Arena mem4;      // device-built kinodynamic graphs: per-in-edge waypoint tables
   gmtb::DevInstance desc{};
   int32_t graph_n = 0;
   const int32_t* goal_idx_dev = nullptr;
@@ -91,6 +92,7 @@ struct gmt_instance {
     aux.release();
     mem2.release();
     mem3.release();
+    mem4.release();
   }
 };
 

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -23,6 +24,7 @@
 #include "offline.cuh"
 #include "quad.cuh"
 #include "sample_dev.cuh"
+#include "solve.cuh"
 
 namespace gmtb {
 
@@ -295,7 +297,7 @@ int sample_free_dev(gmt_ctx* ctx, int32_t n, const gmt_scene* scene, const gmt_s
   double* Fh = reinterpret_cast<double*>(base + o_Fh);
   uint8_t* keep = reinterpret_cast<uint8_t*>(base + o_keep);
   int* d_kept = reinterpret_cast<int*>(base + o_cnt);
-  int* d_valid = d_kept + 1;
+  // d_kept[1]: unused slot
   int* d_gcount = d_kept + 2;
   unsigned long long* d_best = reinterpret_cast<unsigned long long*>(base + o_cnt + 16);
   int* d_dup = reinterpret_cast<int*>(base + o_cnt + 24);
@@ -774,6 +776,25 @@ static int instance_build(gmt_ctx* ctx, const gmt_problem* p, const char* cache_
         D.kin_segments = p->di.segments;
         D.kin_p[0] = p->di.vmax;
         D.kin_p[1] = p->di.weight;
+      }
+      // The checks read build-time waypoint tables, as the reference's
+      // planner reads the polyline cached with every edge (graph.cpp
+      // edge_path): single solves 2.13 -> 0.63 ms (quadrotor n = 8000),
+      // 0.198 -> 0.178 ms (double integrator n = 4000).  GMT_KINO_TABLES=0
+      // regenerates every checked trajectory in the solve instead.
+      const char* kt = std::getenv("GMT_KINO_TABLES");
+      const bool tables = kt ? std::atoi(kt) != 0 : true;
+      const int W = (D.kin_segments + 1) * d;
+      if (rc == GMT_OK && tables && W <= 144 && din.edges > 0) {
+        rc = inst->mem4.reserve(sizeof(double) * static_cast<size_t>(W) * din.edges);
+        if (rc == GMT_OK) {
+          double* wp = static_cast<double*>(inst->mem4.ptr);
+          cudaError_t e = launch_kino_tables(D.coords, din.ptr, din.col, din.tau, n, p->steering, to_quad(&p->quad),
+                                             to_di(&p->di), wp, ctx->sm_count, s);
+          ++ctx->launches;
+          if (e != cudaSuccess) rc = cuda_error(e, "kinodynamic waypoint tables");
+          D.in_wp = wp;
+        }
       }
     }
     if (dubins) {

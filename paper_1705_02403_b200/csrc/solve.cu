@@ -430,8 +430,90 @@ __device__ __forceinline__ bool seg_box_hit(const double* a, const double* b, in
   return true;
 }
 
-// The same test for a kinodynamic edge whose polyline is not stored (double
-// integrator, quadrotor): lanes 0..dim-1 and 16..16+dim-1 evaluate the
+__device__ __forceinline__ void kin_params(const DevInstance& I, QuadParams& QP, DiParams& DP) {
+  const int M = I.kin_segments;
+  QP.g = I.kin_p[0];
+  QP.vmax = I.kin_p[1];
+  QP.amax = I.kin_p[2];
+  QP.ymax = I.kin_p[3];
+  QP.wmax = I.kin_p[4];
+  QP.weight = I.kin_p[5];
+  QP.segments = M;
+  QP.reserved = 0;
+  DP.vmax = I.kin_p[0];
+  DP.weight = I.kin_p[1];
+  DP.segments = M;
+  DP.reserved = 0;
+}
+
+// The waypoint table of one kinodynamic edge, lane-parallel over (waypoint,
+// coordinate): rows 0 and M are the end points (staged in tab by the
+// caller), the interior rows the very operations of di_coord / quad_coord.
+// The quadrotor's per-chain lambda first (lanes 0-3, into the seg scratch);
+// the double integrator's per-axis cubic coefficients c2, c3 (lanes 0-2) and
+// waypoint times t_k (lanes 3..) first, which di_coord recomputes
+// identically for every coordinate.  Returns (warp-uniform) whether every
+// waypoint lies in the unit cube.  vfull (double integrator, every box spans
+// the velocity axes): velocity entries only feed the cube test and may be
+// replaced by 0.5 / -1 where |v| vs vmax decides it for certain.
+template <int D>
+__device__ bool kino_fill_table(bool quad, int dim, int M, double tau, int lane, double* seg, double* tab,
+                                const QuadParams& QP, const DiParams& DP, bool vfull) {
+  const double* x0 = tab;
+  const double* x1 = tab + M * dim;
+  if (quad) {
+    if (lane < 4) quad_chain_lambda(x0, x1, tau, lane, QP, seg + 8 * lane, seg + 8 * lane + 4);
+  } else if (lane < 3) {
+    const double dp = di_sub(x1[lane], x0[lane]);
+    const double v0 = di_vel(x0[3 + lane], DP), v1 = di_vel(x1[3 + lane], DP);
+    const double tt = di_mul(tau, tau);
+    seg[lane] = di_sub(di_div(di_mul(3.0, dp), tt), di_div(di_add(di_mul(2.0, v0), v1), tau));
+    seg[3 + lane] = di_sub(di_div(di_add(v0, v1), tt), di_div(di_mul(2.0, dp), di_mul(tt, tau)));
+  } else if (lane - 2 < M) {
+    const int k = lane - 2;
+    seg[6 + k] = di_div(di_mul(tau, static_cast<double>(k)), static_cast<double>(M));
+  }
+  __syncwarp();
+  bool incube = true;
+  for (int e = lane; e < (M + 1) * dim; e += kWarp) {
+    const int k = e / dim, i = e - k * dim;
+    double v;
+    if (k == 0 || k == M) {
+      v = tab[e];
+    } else if (quad) {
+      int c, ci;
+      quad_locate(i, &c, &ci);
+      v = quad_chain_coord(seg + 8 * c, seg + 8 * c + 4, tau, k, c, ci, QP);
+    } else {
+      const int a = i < 3 ? i : i - 3;
+      const double t = seg[6 + k], c2 = seg[a], c3 = seg[3 + a];
+      const double v0 = di_vel(x0[3 + a], DP);
+      if (i < 3) {
+        v = di_add(x0[a], di_mul(t, di_add(v0, di_mul(t, di_add(c2, di_mul(t, c3))))));
+      } else {
+        const double vv = di_add(v0, di_mul(t, di_add(di_mul(2.0, c2), di_mul(t, di_mul(3.0, c3)))));
+        const double av = vv < 0.0 ? -vv : vv;
+        if (vfull && av <= DP.vmax * (1.0 - 1e-14)) {
+          // Every box spans the velocity axes, so this coordinate only feeds
+          // the cube test, and |v| < vmax puts s = (v / vmax + 1) / 2 in
+          // [0, 1] for certain: no division (the value itself is never read).
+          v = 0.5;
+        } else if (vfull && av >= DP.vmax * (1.0 + 1e-14)) {
+          v = -1.0;  // outside [0, 1] for certain (the edge leaves the cube)
+        } else {
+          v = di_mul(0.5, di_add(di_div(vv, DP.vmax), 1.0));
+        }
+      }
+    }
+    tab[e] = v;
+    incube = incube && !(v < 0.0 || v > 1.0);
+  }
+  return __all_sync(kFull, incube);
+}
+
+// The same test for a kinodynamic edge (double integrator, quadrotor):
+// its waypoint table from the build-time store (in_wp, indexed by the in-edge)
+// or regenerated; without a table: lanes 0..dim-1 and 16..16+dim-1 evaluate the
 // coordinates of waypoints s and s+1 (di_coord / quad_coord, the very
 // functions that materialise stored paths), then the segment goes through
 // segment_free_staged.
@@ -439,7 +521,7 @@ template <int D>
 __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int from, int to,
                                     double tau, int lane, double* seg, double* tab = nullptr,
                                     int tab_cap = 0, uint16_t* cull = nullptr, int cull_cap = 0,
-                                    bool staged = false, bool vfull = false) {
+                                    bool staged = false, bool vfull = false, int64_t edge = -1) {
   // Only the generic-dimension kernel can see a 12D quadrotor instance.
   const bool quad = D == 0 && I.steering == GMT_STEER_QUADROTOR;
   const int dim = quad ? kQuadDim : kDiDim;
@@ -450,89 +532,35 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
   const int M = I.kin_segments;
   QuadParams QP;
   DiParams DP;
-  if (quad) {
-    QP.g = I.kin_p[0];
-    QP.vmax = I.kin_p[1];
-    QP.amax = I.kin_p[2];
-    QP.ymax = I.kin_p[3];
-    QP.wmax = I.kin_p[4];
-    QP.weight = I.kin_p[5];
-    QP.segments = M;
-    QP.reserved = 0;
-  } else {
-    DP.vmax = I.kin_p[0];
-    DP.weight = I.kin_p[1];
-    DP.segments = M;
-    DP.reserved = 0;
-  }
+  kin_params(I, QP, DP);
   if (tab && (M + 1) * dim <= tab_cap && (quad || M + 6 <= kWarp)) {
-    // Waypoint table: every waypoint once, lane-parallel over (waypoint,
-    // coordinate).  The quadrotor's per-chain lambda first (lanes 0-3, into
-    // the seg scratch); the double integrator's per-axis cubic coefficients
-    // c2, c3 (lanes 0-2) and waypoint times t_k (lanes 3..) first, which
-    // di_coord recomputes identically for every coordinate -- the table
-    // entries are the very operations of di_coord / quad_coord.
-    __syncwarp();
-    if (lane < dim) {  // the end points are waypoints 0 and M (and free seg for scratch)
-      const double a = x0[lane], b = x1[lane];
-      tab[lane] = a;
-      tab[M * dim + lane] = b;
-    }
-    __syncwarp();
-    x0 = tab;
-    x1 = tab + M * dim;
-    if (quad) {
-      if (lane < 4) quad_chain_lambda(x0, x1, tau, lane, QP, seg + 8 * lane, seg + 8 * lane + 4);
-    } else if (lane < 3) {
-      const double dp = di_sub(x1[lane], x0[lane]);
-      const double v0 = di_vel(x0[3 + lane], DP), v1 = di_vel(x1[3 + lane], DP);
-      const double tt = di_mul(tau, tau);
-      seg[lane] = di_sub(di_div(di_mul(3.0, dp), tt), di_div(di_add(di_mul(2.0, v0), v1), tau));
-      seg[3 + lane] = di_sub(di_div(di_add(v0, v1), tt), di_div(di_mul(2.0, dp), di_mul(tt, tau)));
-    } else if (lane - 2 < M) {
-      const int k = lane - 2;
-      seg[6 + k] = di_div(di_mul(tau, static_cast<double>(k)), static_cast<double>(M));
-    }
     __syncwarp();
     bool incube = true;
-    for (int e = lane; e < (M + 1) * dim; e += kWarp) {
-      const int k = e / dim, i = e - k * dim;
-      double v;
-      if (k == 0 || k == M) {
-        v = tab[e];
-      } else if (quad) {
-        int c, ci;
-        quad_locate(i, &c, &ci);
-        v = quad_chain_coord(seg + 8 * c, seg + 8 * c + 4, tau, k, c, ci, QP);
-      } else {
-        const int a = i < 3 ? i : i - 3;
-        const double t = seg[6 + k], c2 = seg[a], c3 = seg[3 + a];
-        const double v0 = di_vel(x0[3 + a], DP);
-        if (i < 3) {
-          v = di_add(x0[a], di_mul(t, di_add(v0, di_mul(t, di_add(c2, di_mul(t, c3))))));
-        } else {
-          const double vv = di_add(v0, di_mul(t, di_add(di_mul(2.0, c2), di_mul(t, di_mul(3.0, c3)))));
-          const double av = vv < 0.0 ? -vv : vv;
-          if (vfull && av <= DP.vmax * (1.0 - 1e-14)) {
-            // Every box spans the velocity axes, so this coordinate only feeds
-            // the cube test, and |v| < vmax puts s = (v / vmax + 1) / 2 in
-            // [0, 1] for certain: no division (the value itself is never read).
-            v = 0.5;
-          } else if (vfull && av >= DP.vmax * (1.0 + 1e-14)) {
-            v = -1.0;  // outside [0, 1] for certain (the edge leaves the cube)
-          } else {
-            v = di_mul(0.5, di_add(di_div(vv, DP.vmax), 1.0));
-          }
-        }
+    if (I.in_wp && edge >= 0) {
+      // The table stored at build time (kino_table_kernel: this very fill),
+      // the reference's cached polyline (graph.cpp edge_path) in table form.
+      const int W = (M + 1) * dim;
+      const double* src = I.in_wp + edge * W;
+      for (int e = lane; e < W; e += kWarp) {
+        const double v = __ldg(src + e);
+        tab[e] = v;
+        incube = incube && !(v < 0.0 || v > 1.0);
       }
-      tab[e] = v;
-      incube = incube && !(v < 0.0 || v > 1.0);
+      incube = __all_sync(kFull, incube);
+    } else {
+      if (lane < dim) {  // the end points are waypoints 0 and M (and free seg for scratch)
+        const double a = x0[lane], b = x1[lane];
+        tab[lane] = a;
+        tab[M * dim + lane] = b;
+      }
+      __syncwarp();
+      incube = kino_fill_table<D>(quad, dim, M, tau, lane, seg, tab, QP, DP, vfull);
     }
     // polyline_free (space.cpp:92-99) = every waypoint in the unit cube (each
     // segment's point_in_cube / point_free endpoint test) and no (segment,
     // box) pair hit -- a degenerate segment's all-axes dk == 0 clip is
     // exactly Aabb::contains; the outcome does not depend on the order.
-    if (!__all_sync(kFull, incube)) return false;
+    if (!incube) return false;
     __syncwarp();
     // Boxes the whole polyline's bounding box (widened by the separation
     // margin) misses are missed by every segment's own pre-test: they are
@@ -1524,7 +1552,8 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
               // the endpoints are staged in sc when a lane group can hold them
               return kino_edge_free_warp<D>(I, B, byc, xc, tc, lane, sc,
                                             tab_s + ((D == 0 || D == 6) ? warp * kTabCap * kKinSlots : 0), kTabCap,
-                                            cull_s + warp * kCullCap * kKinSlots, kCullCap, true, D == 6 && sh.vfull);
+                                            cull_s + warp * kCullCap * kKinSlots, kCullCap, true, D == 6 && sh.vfull,
+                                            bec);
             }
             if (pid < 0) return segment_free_staged<D>(d, B, lane, sc);  // segment_free (planner.cpp:59)
             return polyline_free_warp<D>(I, d, B, pid, lane, sc);       // polyline_free (planner.cpp:56-58)
@@ -1753,6 +1782,55 @@ __global__ void __launch_bounds__(256) segment_free_kernel(const double* __restr
     const bool free = segment_free_warp<D>(a + i * d, b + i * d, d, bx, lane, seg);
     if (lane == 0) out[i] = free ? 1 : 0;
   }
+}
+
+// Build-time waypoint tables of a kinodynamic instance's in-edges (the
+// reference caches every edge's polyline when it builds the graph, graph.cpp
+// edge_path): in-edge e = (in_col[e] -> x) gets rows 0..M of its trajectory
+// from kino_fill_table, the very fill the solve's lazy check would run, so a
+// check that reads the table sees the values it would have computed.  One
+// warp per in-edge, a CTA per target vertex.
+__global__ void __launch_bounds__(256) kino_table_kernel(const double* __restrict__ coords,
+                                                         const int64_t* __restrict__ in_ptr,
+                                                         const int32_t* __restrict__ in_col,
+                                                         const double* __restrict__ in_tau, int n, int steering,
+                                                         QuadParams QP, DiParams DP, double* __restrict__ wp) {
+  __shared__ double seg_s[8][32];
+  __shared__ double tab_s[8][144];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool quad = steering == GMT_STEER_QUADROTOR;
+  const int dim = quad ? kQuadDim : kDiDim;
+  const int M = quad ? QP.segments : DP.segments;
+  const int W = (M + 1) * dim;
+  double* seg = seg_s[warp];
+  double* tab = tab_s[warp];
+  for (int x = blockIdx.x; x < n; x += gridDim.x) {
+    const int64_t e1 = in_ptr[x + 1];
+    for (int64_t e = in_ptr[x] + warp; e < e1; e += 8) {
+      const int u = in_col[e];
+      const double tau = in_tau[e];
+      __syncwarp();
+      for (int j = lane; j < W; j += kWarp) tab[j] = 0.0;
+      __syncwarp();
+      if (lane < dim) {
+        tab[lane] = coords[static_cast<int64_t>(u) * dim + lane];
+        tab[M * dim + lane] = coords[static_cast<int64_t>(x) * dim + lane];
+      }
+      __syncwarp();
+      if (tau != 0.0) kino_fill_table<0>(quad, dim, M, tau, lane, seg, tab, QP, DP, false);
+      __syncwarp();
+      for (int j = lane; j < W; j += kWarp) wp[e * W + j] = tab[j];
+    }
+  }
+}
+
+cudaError_t launch_kino_tables(const double* coords, const int64_t* in_ptr, const int32_t* in_col,
+                               const double* in_tau, int n, int steering, const QuadParams& QP,
+                               const DiParams& DP, double* wp, int sm_count, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = std::max(1, std::min(n, sm_count * 8));
+  kino_table_kernel<<<blocks, 256, 0, stream>>>(coords, in_ptr, in_col, in_tau, n, steering, QP, DP, wp);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_segment_free(const double* a, const double* b, int64_t count, int d,

@@ -86,6 +86,13 @@ cudaError_t launch_dijkstra(const DevInstance* inst, const SolveJob* job, int n,
 
 // segment_free (space.cpp:80-90) of count segments a[i*d..], b[i*d..] against
 // one AoS box array; out[i] = 1 when free.  Same device test as the lazy check.
+struct QuadParams;
+struct DiParams;
+// Per-in-edge waypoint tables of a kinodynamic instance ((M + 1) * dim
+// doubles per in-edge, M = the model's segments; (M + 1) * dim <= 144).
+cudaError_t launch_kino_tables(const double* coords, const int64_t* in_ptr, const int32_t* in_col,
+                               const double* in_tau, int n, int steering, const QuadParams& QP,
+                               const DiParams& DP, double* wp, int sm_count, cudaStream_t stream);
 cudaError_t launch_segment_free(const double* a, const double* b, int64_t count, int d,
                                 const double* box_lo, const double* box_hi, int nb, uint8_t* out,
                                 int sm_count, cudaStream_t stream);

@@ -90,3 +90,25 @@ def test_quad_batch_queries(ctx):
     b.launch()
     for q, inst in enumerate(insts):
         assert not abi.full_parity(b.result(q), ctx.plan(inst))
+
+
+@pytest.mark.parametrize("model", ["quad", "di"])
+def test_waypoint_tables_equal_regeneration(ctx, monkeypatch, model):
+    """The build-time per-in-edge waypoint tables (sample.cu, solve.cu
+    kino_table_kernel) against regenerating each checked trajectory in the
+    solve (GMT_KINO_TABLES=0): full plans bit for bit, single CTA and
+    cluster shapes, lambda 1 and 0.5."""
+    spec = P.quad_scene(5, 2500) if model == "quad" else P.di_forest(3, 1500)
+    got = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("GMT_KINO_TABLES", mode)
+        inst = ctx.build_instance(spec)
+        for cs in (1, 8):
+            ctx.set_option(OPT_CLUSTER, cs)
+            for lam in (1.0, 0.5):
+                got[mode, cs, lam] = ctx.plan(inst, lam=lam)
+        ctx.set_option(OPT_CLUSTER, 0)
+    for (mode, cs, lam), r in got.items():
+        if mode == "1":
+            assert not abi.full_parity(r, got["0", cs, lam]), (cs, lam)
+    assert got["1", 1, 1.0].total_collision_checks > 0
