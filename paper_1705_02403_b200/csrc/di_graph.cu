@@ -97,16 +97,31 @@ struct DubinsModel {
   static constexpr int kDim = PD + 1;
   DubinsParams P;
   double radius;
-  // within_radius's straight-line lower bound (steering.cpp:114-121),
-  // widened by 1e-12 relative: it only prunes pairs the cost test rejects.
+  // The reference's candidate set, exactly: the 3^axes grid cells around u
+  // (graph.cpp:56-101: cell = max(r, 1e-9) on the first min(dim, 3) axes,
+  // 21-bit cell keys) -- which bounds |dz| even when the cost ignores the
+  // climb -- then within_radius's straight-line prune (steering.cpp:112-118):
+  // hypot of the planar offsets (glibc's, libm_port.cuh) when the cost
+  // ignores the climb, else euclidean_distance (space.cpp:126-133).
   __device__ bool may(const double* a, const double* b) const {
-    double sq = 0.0;
-    const int m = P.planar_cost_only ? 2 : PD;
-    for (int k = 0; k < m; ++k) {
-      const double d = a[k] - b[k];
-      sq += d * d;
+    const double cell = radius > 1e-9 ? radius : 1e-9;
+    for (int k = 0; k < PD; ++k) {
+      const int ca = static_cast<int>(floor(a[k] / cell)), cb = static_cast<int>(floor(b[k] / cell));
+      const unsigned dk = static_cast<unsigned>(ca - cb) & 0x1fffffu;
+      if (dk > 1u && dk != 0x1fffffu) return false;
     }
-    return sqrt(sq) <= radius * (1.0 + 1e-12);
+    double lb;
+    if (P.planar_cost_only) {
+      lb = lmport::lm_hypot(a[0] - b[0], a[1] - b[1]);
+    } else {
+      double sq = 0.0;
+      for (int k = 0; k < PD; ++k) {
+        const double d = a[k] - b[k];
+        sq += d * d;
+      }
+      lb = sqrt(sq);
+    }
+    return !(lb > radius);
   }
   __device__ double cost_tau(const double* a, const double* b, double* t) const {
     int segs;

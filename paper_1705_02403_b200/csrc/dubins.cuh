@@ -5,19 +5,21 @@
 // algorithm of dubins.cpp:84-167 and steering.cpp:11-101 restated for one
 // thread per pose pair.
 //
-// Parity note: the word parameters go through sin, cos,
-// atan2 and acos.  The reference gets them from glibc 2.39, which is not
-// correctly rounded (measured here: 0.06-0.15 % of sin/cos/atan2/acos results
-// differ from the correctly rounded value), and no device libm reproduces
-// glibc's last bits.  Dubins costs therefore agree with the reference to a
-// few ulps rather than bit for bit; everything downstream (graph assembly,
-// the planner over the graph) is exact.
+// Parity: the word parameters and sampled poses go through
+// sin, cos, atan2 and acos, and the neighbour prune through hypot.  The
+// reference gets them from glibc 2.39, which is not correctly rounded (0.06-
+// 0.15 % of its sin / cos / atan2 / acos results differ from the correctly
+// rounded value), so CUDA's libm cannot reproduce them; libm_port.cuh
+// restates glibc's own routines operation for operation (tools/libm_port.py,
+// pinned bitwise against the host libm by tests/test_libm_port.py), which
+// makes every Dubins cost, path point and graph edge bit-identical.
 #pragma once
 
 #include <cmath>
 #include <cstdint>
 
 #include "di.cuh"  // GMT_HD
+#include "libm_port.cuh"
 
 namespace gmtb {
 
@@ -56,17 +58,17 @@ GMT_HD DubinsPath dubins_shortest(double ax, double ay, double ah, double bx, do
                                   double rho) {
   const double dx = bx - ax, dy = by - ay;
   const double d = sqrt(dx * dx + dy * dy) / rho;
-  const double theta = d > 0.0 ? atan2(dy, dx) : 0.0;
+  const double theta = d > 0.0 ? lmport::lm_atan2(dy, dx) : 0.0;
   const double alpha = dub_mod2pi(ah - theta);
   const double beta = dub_mod2pi(bh - theta);
-  const double sa = sin(alpha), ca = cos(alpha), sb = sin(beta), cb = cos(beta);
+  const double sa = lmport::lm_sin(alpha), ca = lmport::lm_cos(alpha), sb = lmport::lm_sin(beta), cb = lmport::lm_cos(beta);
   const double cab = ca * cb + sa * sb;
   double wt[6], wp[6], wq[6];
   bool ok[6] = {false, false, false, false, false, false};
   {  // LSL
     const double tmp = 2.0 + d * d - 2.0 * (cab - d * (sa - sb));
     if (tmp >= -1e-9) {
-      const double th = atan2(cb - ca, d + sa - sb);
+      const double th = lmport::lm_atan2(cb - ca, d + sa - sb);
       wt[0] = dub_snap2pi(-alpha + th);
       wp[0] = sqrt(tmp > 0.0 ? tmp : 0.0);
       wq[0] = dub_snap2pi(beta - th);
@@ -76,7 +78,7 @@ GMT_HD DubinsPath dubins_shortest(double ax, double ay, double ah, double bx, do
   {  // RSR
     const double tmp = 2.0 + d * d - 2.0 * (cab - d * (sb - sa));
     if (tmp >= -1e-9) {
-      const double th = atan2(ca - cb, d - sa + sb);
+      const double th = lmport::lm_atan2(ca - cb, d - sa + sb);
       wt[1] = dub_snap2pi(alpha - th);
       wp[1] = sqrt(tmp > 0.0 ? tmp : 0.0);
       wq[1] = dub_snap2pi(-beta + th);
@@ -87,7 +89,7 @@ GMT_HD DubinsPath dubins_shortest(double ax, double ay, double ah, double bx, do
     const double tmp = d * d - 2.0 + 2.0 * (cab - d * (sa + sb));
     if (tmp >= -1e-9) {
       const double p = sqrt(tmp > 0.0 ? tmp : 0.0);
-      const double th = atan2(ca + cb, d - sa - sb) - atan2(2.0, p);
+      const double th = lmport::lm_atan2(ca + cb, d - sa - sb) - lmport::lm_atan2(2.0, p);
       wt[2] = dub_snap2pi(alpha - th);
       wp[2] = p;
       wq[2] = dub_snap2pi(beta - th);
@@ -98,7 +100,7 @@ GMT_HD DubinsPath dubins_shortest(double ax, double ay, double ah, double bx, do
     const double tmp = -2.0 + d * d + 2.0 * (cab + d * (sa + sb));
     if (tmp >= -1e-9) {
       const double p = sqrt(tmp > 0.0 ? tmp : 0.0);
-      const double th = atan2(-ca - cb, d + sa + sb) - atan2(-2.0, p);
+      const double th = lmport::lm_atan2(-ca - cb, d + sa + sb) - lmport::lm_atan2(-2.0, p);
       wt[3] = dub_snap2pi(-alpha + th);
       wp[3] = p;
       wq[3] = dub_snap2pi(-beta + th);
@@ -108,8 +110,8 @@ GMT_HD DubinsPath dubins_shortest(double ax, double ay, double ah, double bx, do
   {  // RLR
     const double tmp = 0.125 * (6.0 - d * d + 2.0 * (cab + d * (sa - sb)));
     if (fabs(tmp) <= 1.0) {
-      const double p = kDubinsTwoPi - acos(tmp);
-      const double th = atan2(ca - cb, d - sa + sb);
+      const double p = kDubinsTwoPi - lmport::lm_acos(tmp);
+      const double th = lmport::lm_atan2(ca - cb, d - sa + sb);
       const double t = dub_snap2pi(alpha - th + 0.5 * p);
       wt[4] = t;
       wp[4] = p;
@@ -120,8 +122,8 @@ GMT_HD DubinsPath dubins_shortest(double ax, double ay, double ah, double bx, do
   {  // LRL
     const double tmp = 0.125 * (6.0 - d * d + 2.0 * (cab - d * (sa - sb)));
     if (fabs(tmp) <= 1.0) {
-      const double p = kDubinsTwoPi - acos(tmp);
-      const double th = atan2(-ca + cb, d + sa - sb);
+      const double p = kDubinsTwoPi - lmport::lm_acos(tmp);
+      const double th = lmport::lm_atan2(-ca + cb, d + sa - sb);
       const double t = dub_snap2pi(-alpha + th + 0.5 * p);
       wt[5] = t;
       wp[5] = p;
@@ -169,18 +171,18 @@ GMT_HD void dubins_sample(const DubinsPath& P, double s, double* x, double* y, d
     const double phi = ph;
     switch (dubins_seg(P.word, k)) {
       case 0:
-        px += sin(phi + v) - sin(phi);
-        py += -cos(phi + v) + cos(phi);
+        px += lmport::lm_sin(phi + v) - lmport::lm_sin(phi);
+        py += -lmport::lm_cos(phi + v) + lmport::lm_cos(phi);
         ph = phi + v;
         break;
       case 2:
-        px += -sin(phi - v) + sin(phi);
-        py += cos(phi - v) - cos(phi);
+        px += -lmport::lm_sin(phi - v) + lmport::lm_sin(phi);
+        py += lmport::lm_cos(phi - v) - lmport::lm_cos(phi);
         ph = phi - v;
         break;
       default:
-        px += v * cos(phi);
-        py += v * sin(phi);
+        px += v * lmport::lm_cos(phi);
+        py += v * lmport::lm_sin(phi);
         break;
     }
     if (rem <= 0.0) break;
