@@ -196,6 +196,17 @@ def measured_peak_hbm():
 
 
 # --------------------------------------------------------------------------
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_threads(args) -> int:
     return args.cpu_threads or os.cpu_count() or 1
 
@@ -247,6 +258,7 @@ def run_reference(args):
         "config": {"workload": "di6d_batched (configs[4])", "n": args.n, "dim": 6, "boxes": 60,
                    "radius": args.radius, "lambda": 1.0, "queries_per_step": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "cpu": cpu_model(), "nproc": os.cpu_count(),
                          "sample": f"{sample} of the workload's queries per step, gmt_plan(workers=1) per "
                                    f"query under parallel_chunks({threads}); instances built once "
                                    f"({build_s:.1f} s, untimed)"},
@@ -410,6 +422,7 @@ def run_b200(args):
                     rates, rsum, build_s = reference_di(specs[:sample], threads, 3)
                     val = statistics.median(rates)
                     cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
+                           "cpu": cpu_model(), "nproc": os.cpu_count(),
                            "sample": f"the step's first {sample} queries, median of 3 passes, "
                                      f"gmt_plan(workers=1) per query under parallel_chunks({threads}); "
                                      f"instances (reference sample_free/append_init, DI graph + polylines "
