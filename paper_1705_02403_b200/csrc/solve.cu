@@ -94,6 +94,11 @@ struct CtaShared {
   int32_t added_acc;              // rank 0: cluster-wide additions of this pass
   int32_t feasible;
   int32_t vfull;  // D = 6: every box spans [0, 1] on the three velocity axes
+  // (the 24-warp D = 6 shape) boxes staged in ascending lo_x order, and the
+  // widest staged x extent him_x - lom_x rounded up: the edge cull scans
+  // only the boxes whose lom_x lies in [pmn_x - wx, pmx_x]
+  int32_t xsorted;
+  double box_wx;
   // Loop state kept in shared memory rather than in every thread's
   // registers (the solve is register-bound): the threshold index i, the
   // pass number, the running check total (tid 0), per-warp check / commit
@@ -653,7 +658,8 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
 // waypoint table ((M + 1) * 6 <= 64); cull: its box list.
 template <int G>
 __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double tau, int gl, uint32_t gmask,
-                                  int gbase, double* seg, double* tab, uint16_t* cull, int cull_cap, bool vfull) {
+                                  int gbase, double* seg, double* tab, uint16_t* cull, int cull_cap, bool vfull,
+                                  double box_wx = -1.0) {
   constexpr int dim = kDiDim;
   static_assert(G >= 8, "a group must hold a state's coordinates and the coefficient lanes");
   constexpr uint32_t kGroupBits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
@@ -742,9 +748,35 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
   }
   Boxes sub = bx;
   int kept = 0;
-  for (int i0 = 0; i0 < bx.count && kept <= cull_cap; i0 += G) {
+  int ib = 0, ie = bx.count;
+  if (vfull && box_wx >= 0.0) {
+    // Boxes staged in ascending lom_x: only [first lom_x >= pmn_x - wx,
+    // first lom_x > pmx_x) can meet the bounding box on x (every him_x <=
+    // lom_x + wx; the 1e-9 widening absorbs the subtraction's rounding).
+    // Two rounds over the group: the chunk, then the index in it.
+    const double lo_t = (pmn[0] - box_wx) - 1e-9, hi_t = pmx[0];
+    const int chunk = (bx.count + G - 1) / G;
+    const int last = gl * chunk + chunk - 1 < bx.count ? gl * chunk + chunk - 1 : bx.count - 1;
+    const double xe = gl * chunk < bx.count ? bx.lom[last] : kInf;
+    const int c_lo = __popc((__ballot_sync(gmask, xe < lo_t) >> gbase) & kGroupBits);
+    const int c_hi = __popc((__ballot_sync(gmask, !(xe > hi_t)) >> gbase) & kGroupBits);
+    ib = c_lo * chunk;
+    ie = c_hi * chunk;
+    for (int j0 = ib; j0 < bx.count && j0 < (c_lo + 1) * chunk; j0 += G) {
+      const int j = j0 + gl;
+      const bool below = j < bx.count && j < (c_lo + 1) * chunk && bx.lom[j] < lo_t;
+      ib += __popc((__ballot_sync(gmask, below) >> gbase) & kGroupBits);
+    }
+    for (int j0 = ie; j0 < bx.count && j0 < (c_hi + 1) * chunk; j0 += G) {
+      const int j = j0 + gl;
+      const bool in = j < bx.count && j < (c_hi + 1) * chunk && !(bx.lom[j] > hi_t);
+      ie += __popc((__ballot_sync(gmask, in) >> gbase) & kGroupBits);
+    }
+    ie = ie < bx.count ? ie : bx.count;
+  }
+  for (int i0 = ib; i0 < ie && kept <= cull_cap; i0 += G) {
     const int b = i0 + gl;
-    bool meets = b < bx.count;
+    bool meets = b < ie;
     const int bc = meets ? b : 0;
     if (vfull) {  // (boxes staged: lom / him set) only the position axes can separate
 #pragma unroll
@@ -941,8 +973,28 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
     double* hi = lo + static_cast<size_t>(nb) * d;
     double* lom = hi + static_cast<size_t>(nb) * d;
     double* him = lom + static_cast<size_t>(nb) * d;
+    // The 24-warp D = 6 shape stages the boxes in ascending lo_x order (ties
+    // by index): the pair tests' outcome does not depend on the box order,
+    // and the edge cull then scans an x range (di_edge_free_half).
+    constexpr bool kXSort = D == 6 && kDynScratch;
+    constexpr int kSortMax = 256;
+    __shared__ uint8_t xrank_s[kXSort ? kSortMax : 1];
+    const bool xsort = kXSort && nb <= kSortMax;
+    if (xsort) {
+      for (int b = tid; b < nb; b += nt) {
+        const double x = I.box_lo[b * d];
+        int r = 0;
+        for (int c = 0; c < nb; ++c) {
+          const double y = I.box_lo[c * d];
+          r += (y < x || (y == x && c < b)) ? 1 : 0;
+        }
+        xrank_s[b] = static_cast<uint8_t>(r);
+      }
+      __syncthreads();
+    }
     for (int idx = tid; idx < nb * d; idx += nt) {
-      const int b = idx / d, k = idx - b * d;
+      const int b0 = idx / d, k = idx - b0 * d;
+      const int b = xsort ? xrank_s[b0] : b0;
       const double l = I.box_lo[idx], h = I.box_hi[idx];
       lo[k * nb + b] = l;
       hi[k * nb + b] = h;
@@ -950,12 +1002,24 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
       him[k * nb + b] = h + kSepMargin;
     }
     uint32_t* full = reinterpret_cast<uint32_t*>(him + static_cast<size_t>(nb) * d);
-    for (int b = tid; b < nb; b += nt) {
+    for (int b0 = tid; b0 < nb; b0 += nt) {
       uint32_t m = 0u;
       for (int k = 0; k < d; ++k)
-        if (I.box_lo[b * d + k] <= 0.0 && I.box_hi[b * d + k] >= 1.0) m |= 1u << k;
-      full[b] = m;
+        if (I.box_lo[b0 * d + k] <= 0.0 && I.box_hi[b0 * d + k] >= 1.0) m |= 1u << k;
+      full[xsort ? xrank_s[b0] : b0] = m;
     }
+    if (xsort) {
+      __syncthreads();
+      if (tid == 0) {
+        double w = 0.0;
+        for (int b = 0; b < nb; ++b) {
+          const double e = him[b] - lom[b];
+          w = e > w ? e : w;
+        }
+        sh.box_wx = w * (1.0 + 1e-12) + 1e-12;  // (rounded up: every him_x <= lom_x + box_wx)
+      }
+    }
+    if (tid == 0) sh.xsorted = xsort ? 1 : 0;
     bxl.lo = lo, bxl.hi = hi, bxl.lom = lom, bxl.him = him, bxl.bs = 1, bxl.as = nb;
     bxl.full = full;
     if constexpr (D == 6) {
@@ -969,6 +1033,7 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
     bxl.lo = I.box_lo, bxl.hi = I.box_hi, bxl.lom = nullptr, bxl.him = nullptr, bxl.bs = d, bxl.as = 1;
     bxl.full = nullptr;
     if (tid == 0) sh.vfull = 0;
+    if (tid == 0) sh.xsorted = 0;
   }
   bxl.idx = nullptr;
 
@@ -1514,7 +1579,8 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
               if (hl == 0) atomicAdd(&sh.wchecks[warp], 1);
               const bool ok = di_edge_free_half<kLanesPerRow>(
                   I, bx_s, tau_b, hl, gmask, kLanesPerRow * h, segh, tab_s + (warp * kRows + h) * kTabCap,
-                  cull_s + (warp * kRows + h) * kCullCap, kCullCap, sh.vfull);
+                  cull_s + (warp * kRows + h) * kCullCap, kCullCap, sh.vfull,
+                  (kDynScratch && sh.xsorted) ? sh.box_wx : -1.0);
               if (ok && hl == 0) {
                 atomicAdd(&sh.wadded[warp], 1);
                 cost_s[x] = bv;
