@@ -155,8 +155,8 @@ extern "C" int gmt_ctx_create(int device, gmt_ctx** out) {
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
   ctx->smem_optin = prop.sharedMemPerBlockOptin;
-  e = cudaMalloc(&ctx->counters, sizeof(int64_t) * 8);  // [0..2] traffic, [4..7] phase timing (debug)
-  if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, sizeof(int64_t) * 8);
+  e = cudaMalloc(&ctx->counters, sizeof(int64_t) * 16);  // [0..2] traffic, [4..15] phase timing (debug)
+  if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, sizeof(int64_t) * 16);
   if (e != cudaSuccess) {
     delete ctx;
     return cuda_error(e, "counters");
@@ -253,12 +253,12 @@ extern "C" int gmt_ctx_set_option(gmt_ctx* ctx, int option, int64_t value) {
 extern "C" int gmt_ctx_counters(gmt_ctx* ctx, int64_t* out, int32_t reset) {
   gmtb::AllocScope alloc_scope_(ctx);
   GMT_CUDA(cudaStreamSynchronize(ctx->stream));
-#ifdef GMT_PHASE_TIMING  // debug builds: out[4..7] = per-phase clock sums
-  GMT_CUDA(cudaMemcpy(out, ctx->counters, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost));
+#ifdef GMT_PHASE_TIMING  // debug builds: out[4..15] = per-phase clock sums
+  GMT_CUDA(cudaMemcpy(out, ctx->counters, sizeof(int64_t) * 16, cudaMemcpyDeviceToHost));
 #else
   GMT_CUDA(cudaMemcpy(out, ctx->counters, sizeof(int64_t) * 3, cudaMemcpyDeviceToHost));
 #endif
-  if (reset) GMT_CUDA(cudaMemset(ctx->counters, 0, sizeof(int64_t) * 8));
+  if (reset) GMT_CUDA(cudaMemset(ctx->counters, 0, sizeof(int64_t) * 16));
   return GMT_OK;
 }
 

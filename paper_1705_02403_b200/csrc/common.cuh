@@ -46,8 +46,21 @@ struct PoolView {
   int32_t cap;
   int32_t kc;   // rank map length (pool points scanned)
   int32_t k;    // pool graph vertices
+  const double* rec;  // per pool in-edge check records (pool_rec_len doubles each) or null
+  int32_t rec_len;
+  int32_t reserved;
 };
 constexpr uint16_t kPoolNoRank = 0xffffu;
+
+// A pool edge's check record (pool.cu pool_rec_kernel): its trajectory's
+// waypoints depend on the two pool points only, so the part of the lazy
+// check that does not involve a query's boxes is done once per pool edge:
+// [0..3) the minimum and [3..6) the maximum of the M + 1 waypoints' position
+// coordinates (rec[0] = NaN when some waypoint leaves the unit cube, which
+// makes polyline_free false whatever the boxes), then the waypoints'
+// positions (M + 1) x 3, padded to 32-byte multiples.
+constexpr int kPoolRecHead = 6;
+__host__ __device__ inline int pool_rec_len(int segments) { return (kPoolRecHead + 3 * (segments + 1) + 3) & ~3; }
 
 // Device-resident problem instance (ProblemInstance + ObstacleSet +
 // GoalRegion, problem.hpp:52-57 / space.hpp:28-41).  A POD descriptor that
@@ -99,6 +112,12 @@ struct DevInstance {
   // Non-null: the graph is a view of the shared pool (the row arrays above
   // are unused); only batched double-integrator solves see such instances.
   const PoolView* pool;
+  // Materialised pool-derived rows: the pool in-edge of each in-row entry
+  // (-1: an edge with g or init) and the pool's check records.
+  const int32_t* in_pe;
+  const double* pool_rec;
+  int32_t pool_rec_len;
+  int32_t reserved2;
 };
 
 // Scalars of one PlanResult (planner.hpp:43-51).

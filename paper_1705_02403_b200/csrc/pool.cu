@@ -68,6 +68,8 @@ struct SamplePool {
   int K = 0;         // the pool graph covers points [0, K)
   Arena out_mem, in_mem;
   DiRows out, in;
+  Arena rec_mem;     // per in-edge check records (pool_rec_kernel), empty when GMT_POOL_REC=0
+  int rec_len = 0;
   double build_ms = 0.0;      // last graph (re)build
   int last_fallbacks = 0;     // queries of the last call that took the single builder
   double stage_ms[8] = {};    // last call's stage times (GMT_POOL_TIMING=1)
@@ -78,6 +80,7 @@ void destroy_pool(SamplePool* p) {
   p->pts.release();
   p->out_mem.release();
   p->in_mem.release();
+  p->rec_mem.release();
   delete p;
 }
 
@@ -535,7 +538,49 @@ __device__ __forceinline__ void row_store(T* p, T v, bool stream) {
     *p = v;
   }
 }
+// Check records of the pool's in-edges (common.cuh pool_rec_len), a warp per
+// pool vertex x, a lane per in-edge y -> x: the waypoints are di_coord's,
+// the very values of the cached polyline the reference's planner checks
+// (graph.cpp edge_path; oracle_di_paths), and of the solve's own table.
+__global__ void __launch_bounds__(256) pool_rec_kernel(const double* __restrict__ P, int K,
+                                                       const int64_t* __restrict__ in_ptr,
+                                                       const int32_t* __restrict__ in_col,
+                                                       const double* __restrict__ in_tau, DiParams DP, int RL,
+                                                       double* __restrict__ rec) {
+  const int lane = threadIdx.x & 31;
+  const int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (x >= K) return;
+  const int M = DP.segments;
+  const int64_t e1 = in_ptr[x + 1];
+  const double* x1 = P + static_cast<int64_t>(x) * kD;
+  for (int64_t e = in_ptr[x] + lane; e < e1; e += 32) {
+    const double* x0 = P + static_cast<int64_t>(in_col[e]) * kD;
+    const double tau = in_tau[e];
+    double* r = rec + e * RL;
+    double mn[3] = {kInf, kInf, kInf}, mx[3] = {-kInf, -kInf, -kInf};
+    bool incube = true;
+    for (int k = 0; k <= M; ++k) {
+      for (int i = 0; i < kD; ++i) {
+        const double v = di_coord(x0, x1, tau, k, i, DP);
+        incube = incube && !(v < 0.0 || v > 1.0);
+        if (i < 3) {
+          r[kPoolRecHead + 3 * k + i] = v;
+          mn[i] = v < mn[i] ? v : mn[i];
+          mx[i] = mx[i] < v ? v : mx[i];
+        }
+      }
+    }
+    for (int i = 0; i < 3; ++i) {
+      r[i] = mn[i];
+      r[3 + i] = mx[i];
+    }
+    if (!incube) r[0] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: the polyline leaves the cube
+    for (int j = kPoolRecHead + 3 * (M + 1); j < RL; ++j) r[j] = 0.0;
+  }
+}
+
 template <int kRowLanes, bool kStream>
+
 __global__ void __launch_bounds__(256) pool_rows_kernel(
     const PQ* __restrict__ pq, const PQOut* __restrict__ po, int Kc, int stage_rank, const int64_t* __restrict__ pin_ptr,
     const int32_t* __restrict__ pin_col, const double* __restrict__ pin_cost, const double* __restrict__ pin_tau,
@@ -544,7 +589,8 @@ __global__ void __launch_bounds__(256) pool_rows_kernel(
     const double* __restrict__ stau, const int32_t* __restrict__ sp_code, const uint16_t* __restrict__ sp_j,
     const int64_t* __restrict__ in_start, int64_t* __restrict__ in_end,
     const int64_t* __restrict__ out_start, int64_t* __restrict__ out_end, int32_t* __restrict__ in_col,
-    double* __restrict__ in_cost, double* __restrict__ in_tau, int32_t* __restrict__ out_col) {
+    double* __restrict__ in_cost, double* __restrict__ in_tau, int32_t* __restrict__ out_col,
+    int32_t* __restrict__ in_pe) {
   extern __shared__ uint16_t rank_s[];
   const int q = blockIdx.y;
   const PQ Q = pq[q];
@@ -568,6 +614,7 @@ __global__ void __launch_bounds__(256) pool_rows_kernel(
   int32_t* icol = in_col + Q.in_off;
   double* icost = in_cost + Q.in_off;
   double* itau = in_tau + Q.in_off;
+  int32_t* ipe = in_pe ? in_pe + Q.in_off : nullptr;
   int32_t* ocol = out_col + Q.out_off;
   const int64_t lb = static_cast<int64_t>(q) * 4 * kSpecCap;
   const bool live = x <= n;
@@ -596,6 +643,7 @@ __global__ void __launch_bounds__(256) pool_rows_kernel(
       row_store(icol + is + j, scol[lb + (l + 1) * kSpecCap + j], kStream);
       row_store(icost + is + j, scost[lb + (l + 1) * kSpecCap + j], kStream);
       row_store(itau + is + j, stau[lb + (l + 1) * kSpecCap + j], kStream);
+      if (ipe) row_store(ipe + is + j, -1, kStream);
     }
     for (int j = gl; j < lo; j += kRowLanes) row_store(ocol + os + j, scol[lb + l * kSpecCap + j], kStream);
     li = lo = 0;  // (no pool rows to scan)
@@ -626,6 +674,7 @@ __global__ void __launch_bounds__(256) pool_rows_kernel(
       row_store(icol + slot, static_cast<int32_t>(ri), kStream);
       row_store(icost + slot, __ldg(pin_cost + ie0 + j), kStream);
       row_store(itau + slot, __ldg(pin_tau + ie0 + j), kStream);
+      if (ipe) row_store(ipe + slot, static_cast<int32_t>(ie0 + j), kStream);
     }
     if (ro != kNoRank) row_store(ocol + os + wo + __popc(mo & below), static_cast<int32_t>(ro), kStream);
     wi += __popc(mi);
@@ -638,6 +687,7 @@ __global__ void __launch_bounds__(256) pool_rows_kernel(
       row_store(icol + w, n - 1, kStream);
       row_store(icost + w, scost[lb + j], kStream);
       row_store(itau + w, stau[lb + j], kStream);
+      if (ipe) row_store(ipe + w, -1, kStream);
       ++w;
     }
     if (code & 4) {
@@ -645,6 +695,7 @@ __global__ void __launch_bounds__(256) pool_rows_kernel(
       row_store(icol + w, n, kStream);
       row_store(icost + w, scost[lb + 2 * kSpecCap + j], kStream);
       row_store(itau + w, stau[lb + 2 * kSpecCap + j], kStream);
+      if (ipe) row_store(ipe + w, -1, kStream);
       ++w;
     }
     row_store(in_end + Q.node_off + x, w, kStream);
@@ -667,7 +718,8 @@ __global__ void pool_desc_kernel(const PQ* __restrict__ pq, const PQOut* __restr
                                  PoolView* __restrict__ views, PoolView shared_view, const int32_t* __restrict__ sel,
                                  const uint16_t* __restrict__ rank, const int32_t* __restrict__ sp_code,
                                  const uint16_t* __restrict__ sp_j, const int32_t* __restrict__ scol,
-                                 const double* __restrict__ scost, const double* __restrict__ stau) {
+                                 const double* __restrict__ scost, const double* __restrict__ stau,
+                                 const int32_t* __restrict__ in_pe, const double* __restrict__ prec, int prec_len) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= count) return;
   const PQ Q = pq[q];
@@ -710,6 +762,11 @@ __global__ void pool_desc_kernel(const PQ* __restrict__ pq, const PQOut* __restr
     D.in_col = in_col + Q.in_off;
     D.in_cost = in_cost + Q.in_off;
     D.in_tau = in_tau + Q.in_off;
+    if (in_pe && prec) {
+      D.in_pe = in_pe + Q.in_off;
+      D.pool_rec = prec;
+      D.pool_rec_len = prec_len;
+    }
   }
   D.steering = GMT_STEER_DOUBLE_INTEGRATOR;
   D.kin_segments = P.segments;
@@ -807,10 +864,25 @@ int pool_graph(gmt_ctx* ctx, SamplePool* pool, int K) {
   K = std::min(pool->Kp, (std::max(K, pool->K + pool->K / 8) + 255) & ~255);
   pool->out_mem.release();
   pool->in_mem.release();
+  pool->rec_mem.release();
+  pool->rec_len = 0;
   pool->K = 0;
   int rc = build_di_graph_dev(ctx, static_cast<const double*>(pool->pts.ptr), K, &pool->gp, pool->radius,
                               pool->out_mem, &pool->out, pool->in_mem, &pool->in);
   if (rc) return rc;
+  const char* rec_env = std::getenv("GMT_POOL_REC");  // 0: no check records (A/B)
+  if (!(rec_env && rec_env[0] == '0') && pool->in.edges > 0) {
+    const DiParams DP = to_di(&pool->gp);
+    const int RL = pool_rec_len(DP.segments);
+    rc = pool->rec_mem.reserve(sizeof(double) * static_cast<size_t>(pool->in.edges) * RL);
+    if (rc) return rc;
+    pool_rec_kernel<<<(K + 7) / 8, 256, 0, ctx->stream>>>(static_cast<const double*>(pool->pts.ptr), K, pool->in.ptr,
+                                                        pool->in.col, pool->in.tau, DP, RL,
+                                                        static_cast<double*>(pool->rec_mem.ptr));
+    GMT_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    pool->rec_len = RL;
+  }
   GMT_CUDA(cudaStreamSynchronize(ctx->stream));
   pool->K = K;
   pool->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1045,10 +1117,12 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
         sv.cap = kSpecCap;
         sv.kc = Kc;
         sv.k = pool->K;
+        sv.rec = pool->rec_len ? static_cast<const double*>(pool->rec_mem.ptr) : nullptr;
+        sv.rec_len = pool->rec_len;
         pool_desc_kernel<<<(count + 127) / 128, 128, 0, s>>>(
             d_pq, d_po, count, pool->radius, DP, d_qc, d_blo, d_bhi, d_glo, d_ghi, nullptr, nullptr, nullptr, nullptr,
             nullptr, nullptr, nullptr, nullptr, d_desc, d_view, sv, d_sel, d_rank, d_spc, d_spj, d_scol, d_scost,
-            d_stau);
+            d_stau, nullptr, nullptr, 0);
         GMT_CUDA(cudaGetLastError());
         ++ctx->launches;
         GMT_CUDA(cudaMemcpyAsync(po.data(), d_po, sizeof(PQOut) * count, cudaMemcpyDeviceToHost, s));
@@ -1084,6 +1158,8 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       const size_t o_icost = r.take<double>(tin);
       const size_t o_itau = r.take<double>(tin);
       const size_t o_ocol = r.take<int32_t>(tout);
+      const bool recs = pool->rec_len > 0;
+      const size_t o_ipe = recs ? r.take<int32_t>(tin) : 0;
       rc = rows.reserve(r.off);
       if (rc) return rc;
       char* R = static_cast<char*>(rows.ptr);
@@ -1091,6 +1167,7 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       auto* d_icost = reinterpret_cast<double*>(R + o_icost);
       auto* d_itau = reinterpret_cast<double*>(R + o_itau);
       auto* d_ocol = reinterpret_cast<int32_t*>(R + o_ocol);
+      auto* d_ipe = recs ? reinterpret_cast<int32_t*>(R + o_ipe) : nullptr;
       if ((rc = put(d_pq, pq.data(), sizeof(PQ) * count))) return rc;
       timer.mark();
       const size_t rsm = sizeof(uint16_t) * static_cast<size_t>(Kc);
@@ -1104,12 +1181,14 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       rows_kern<<<dim3((max_n + 1 + kRowTile - 1) / kRowTile, count), 256, stage_rank ? rsm : 0, s>>>(
           d_pq, d_po, Kc, stage_rank, pool->in.ptr, pool->in.col, pool->in.cost, pool->in.tau, pool->out.ptr, pool->out.col,
           d_rank, d_sel, d_scol, d_scost, d_stau, d_spc, d_spj, d_is, d_ie, d_os, d_oe, d_icol, d_icost, d_itau,
-          d_ocol);
+          d_ocol, d_ipe);
       timer.mark();
       pool_desc_kernel<<<(count + 127) / 128, 128, 0, s>>>(d_pq, d_po, count, pool->radius, DP, d_qc, d_blo, d_bhi,
                                                            d_glo, d_ghi, d_is, d_ie, d_os, d_oe, d_icol, d_icost,
                                                            d_itau, d_ocol, d_desc, nullptr, PoolView{}, nullptr,
-                                                           nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+                                                           nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                           d_ipe, static_cast<const double*>(pool->rec_mem.ptr),
+                                                           pool->rec_len);
       GMT_CUDA(cudaGetLastError());
       timer.mark();
       ctx->launches += 2;

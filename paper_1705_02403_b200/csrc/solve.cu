@@ -656,10 +656,14 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
 // (segment, box) pair through the reference's clip) with group-masked votes.
 // seg: the group's 32 staged doubles (a = [0..6), b = [16..22)); tab: its
 // waypoint table ((M + 1) * 6 <= 64); cull: its box list.
+// rec (every box spans the velocity axes, a pool edge): the edge's check
+// record (common.cuh), which replaces the table, the cube test and the
+// bounding box; the table's positions are read only when some box survives
+// the cull.
 template <int G>
 __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double tau, int gl, uint32_t gmask,
                                   int gbase, double* seg, double* tab, uint16_t* cull, int cull_cap, bool vfull,
-                                  double box_wx = -1.0) {
+                                  double box_wx = -1.0, const double* rec = nullptr) {
   constexpr int dim = kDiDim;
   static_assert(G >= 8, "a group must hold a state's coordinates and the coefficient lanes");
   constexpr uint32_t kGroupBits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
@@ -677,6 +681,15 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     for (int b = gl; b < bx.count && !in; b += G) in = box_has<6>(seg, dim, bx, b);
     return !__any_sync(gmask, in);
   }
+  if (rec) {  // the pool edge's record: the bounding box (NaN: leaves the cube)
+    double v = 0.0;
+    if (gl < kPoolRecHead) {
+      v = __ldg(rec + gl);
+      seg[gl < 3 ? gl : 13 + gl] = v;  // min -> seg[0..3), max -> seg[16..19)
+    }
+    if (__any_sync(gmask, gl == 0 && v != v)) return false;
+    __syncwarp(gmask);
+  } else {
   if (gl < dim) {
     tab[gl] = seg[gl];
     tab[M * dim + gl] = seg[16 + gl];
@@ -740,6 +753,7 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     seg[16 + gl] = mx;
   }
   __syncwarp(gmask);
+  }  // (rec)
   double pmn[dim], pmx[dim];
 #pragma unroll
   for (int k = 0; k < dim; ++k) {
@@ -802,6 +816,13 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     sub.idx = cull;
     sub.count = kept;
   }
+  int ts = dim;  // waypoint stride in tab
+  if (rec) {
+    if (kept == 0) return true;  // no box meets the polyline's bounding box
+    for (int e = gl; e < 3 * (M + 1); e += G) tab[e] = __ldg(rec + kPoolRecHead + e);
+    __syncwarp(gmask);
+    ts = 3;
+  }
   const int nbx = sub.count;
   const int pairs = M * nbx;
   for (int p0 = 0; p0 < pairs; p0 += G) {
@@ -810,8 +831,8 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     if (p < pairs) {
       const int sg = p / nbx, bi = p - sg * nbx;
       const int box = sub.idx ? sub.idx[bi] : bi;
-      hit = vfull ? seg_box_hit<6, true>(tab + sg * dim, tab + (sg + 1) * dim, dim, bx, box)
-                  : seg_box_hit<6>(tab + sg * dim, tab + (sg + 1) * dim, dim, bx, box);
+      hit = vfull ? seg_box_hit<6, true>(tab + sg * ts, tab + (sg + 1) * ts, dim, bx, box)
+                  : seg_box_hit<6>(tab + sg * ts, tab + (sg + 1) * ts, dim, bx, box);
     }
     if (__any_sync(gmask, hit)) return false;
   }
@@ -863,6 +884,9 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 // Two CTA shapes: WIDE = 512 threads with up to 128 registers (clusters,
 // and single-CTA queries that want the registers), narrow = 256 threads,
 // 64 registers, four CTAs per SM.
+#ifndef GMT_DI_DYNAMIC
+#define GMT_DI_DYNAMIC 2  // (P5 dynamic: 24.6 -> 24.1 ms per 4096 configs[4] queries; P4 too: no gain)
+#endif
 #ifndef GMT_BATCH_MIN_BLOCKS
 #define GMT_BATCH_MIN_BLOCKS 4
 #endif
@@ -896,7 +920,12 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
   constexpr int kRows = CS == 1 ? ((D == 6 && NW == 24) ? GMT_ROWS_DI24 : GMT_ROWS_PER_WARP) : GMT_ROWS_CLUSTER;
   constexpr int kLanesPerRow = kWarp / kRows;
   constexpr int kUnroll = CS == 1 ? GMT_UNROLL_BATCH : GMT_UNROLL_CLUSTER;
-  constexpr bool kDynamic = CS > 1;  // dynamic row / candidate distribution
+  // Dynamic row / candidate distribution (a shared counter): clusters, and
+  // the batched 24-warp DI shape's candidates (GMT_DI_DYNAMIC bit 1: P4 rows,
+  // bit 2: P5 candidates), whose lazy checks vary widely in cost.
+  constexpr bool kDi24 = CS == 1 && D == 6 && NW == 24;
+  constexpr bool kDynOwn = CS > 1 || (kDi24 && (GMT_DI_DYNAMIC & 1));
+  constexpr bool kDynamic = CS > 1 || (kDi24 && (GMT_DI_DYNAMIC & 2));
   // Per-warp scratch: kRows staged segments, kinodynamic waypoint tables
   // (double integrator: D = 6; quadrotor: D = 0) and surviving-box lists --
   // batched DI solves check kRows edges per warp at once (one table / list
@@ -1139,9 +1168,12 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
   int cnt_open = 0;
 
 #ifdef GMT_PHASE_TIMING
-  __shared__ long long sh_ph[4];
+  // [0..3] the passes' phases (thread 0); [4..7] per-warp sums over the P5
+  // loop: the whole loop, inside the lazy checks (group 0), the barrier wait
+  // after the loop, the P4 loop
+  __shared__ unsigned long long sh_ph[8];
   long long ph_t = clock64();
-  if (tid == 0) sh_ph[0] = sh_ph[1] = sh_ph[2] = sh_ph[3] = 0;
+  if (tid < 8) sh_ph[tid] = 0;
 #endif
   for (;;) {
     long long i = sh.iter;  // written by tid 0 only, behind the pass barriers
@@ -1229,7 +1261,8 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
     }
 
 #ifdef GMT_PHASE_TIMING
-    if (tid == 0) { const long long t_ = clock64(); sh_ph[0] += t_ - ph_t; ph_t = t_; }
+    if (tid == 0) { const long long t_ = clock64(); sh_ph[0] += static_cast<unsigned long long>(t_ - ph_t); ph_t = t_; }
+    const long long w_p4 = clock64();
 #endif
     // Rows are processed kRows at a time per warp: lane group h (lanes
     // kLanesPerRow*h ...) streams row k + h, so kRows rows' loads are in
@@ -1277,7 +1310,7 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
         // Clusters take the next row pair from a shared counter (their few,
         // uneven rows balance better); batched CTAs stride statically.
         int kn = k + kRows * nw;
-        if constexpr (kDynamic) {
+        if constexpr (kDynOwn) {
           if (lane == 0) kn = atomicAdd(&sh.next_own, kRows);
           kn = __shfl_sync(kFull, kn, 0);
         }
@@ -1349,9 +1382,12 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
         ext = next_ext;
       }
     }
+#ifdef GMT_PHASE_TIMING
+    if (lane == 0) atomicAdd(&sh_ph[7], static_cast<unsigned long long>(clock64() - w_p4));
+#endif
     cluster_barrier<CS>();  // [1] candidate marks complete
 #ifdef GMT_PHASE_TIMING
-    if (tid == 0) { const long long t_ = clock64(); sh_ph[1] += t_ - ph_t; ph_t = t_; }
+    if (tid == 0) { const long long t_ = clock64(); sh_ph[1] += static_cast<unsigned long long>(t_ - ph_t); ph_t = t_; }
 #endif
 
     // Own candidates (words w = rank mod CS) -> list.
@@ -1371,13 +1407,20 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
     __syncthreads();
     const int ccount = sh.cand_count;
 #ifdef GMT_PHASE_TIMING
-    if (tid == 0) { const long long t_ = clock64(); sh_ph[2] += t_ - ph_t; ph_t = t_; }
+    if (tid == 0) { const long long t_ = clock64(); sh_ph[2] += static_cast<unsigned long long>(t_ - ph_t); ph_t = t_; }
 #endif
 
     // P5 + P6: connect_candidate (planner.cpp:62-90) and commit (178-189).
     // Half h scans candidate k + h's in-row and reduces its (cost, position)
     // argmin; then the whole warp lazily checks the two chosen edges in turn.
+#ifdef GMT_PHASE_TIMING
+    long long w_bar = 0;
+#endif
     {
+#ifdef GMT_PHASE_TIMING
+      const long long w_p5 = clock64();
+      unsigned long long w_chk = 0;
+#endif
       double* segh = seg + 32 * h;  // group h's segment: a = [0..15], b = [16..31]
       int k = kRows * warp;
       int x = -1;
@@ -1437,6 +1480,7 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
             if (hl == 0 && I.in_tau && nlen > 0) {
               prefetch_l2(I.in_col + n0, sizeof(int32_t) * nlen);
               prefetch_l2(I.in_cost + n0, sizeof(double) * nlen);
+              if (I.in_pe) prefetch_l2(I.in_pe + n0, sizeof(int32_t) * nlen);
             }
           }
         }
@@ -1561,6 +1605,19 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
             tau_b = __ldg(PV.stau + static_cast<int64_t>(t == 0 ? 0 : 2) * PV.cap + j);
           }
         }
+        // A pool edge's check record (batched DI over the shared pool, every
+        // box spanning the velocity axes): the edge's own pool in-edge.
+        const double* rec_b = nullptr;
+        if constexpr (D == 6 && kRows >= 2) {
+          if (bo >= 0 && sh.vfull) {
+            if (viewed) {
+              if (PV.rec && !spec_row && bo < len) rec_b = PV.rec + (e0 + bo) * PV.rec_len;
+            } else if (I.in_pe) {
+              const int32_t pe = __ldg(I.in_pe + e0 + bo);
+              if (pe >= 0) rec_b = I.pool_rec + static_cast<int64_t>(pe) * I.pool_rec_len;
+            }
+          }
+        }
         if constexpr (kLanesPerRow >= kMaxSolveDim) {
           if (bo >= 0 && hl < d) segh[hl] = __ldg(I.coords + static_cast<int64_t>(by) * d + hl);
         } else {
@@ -1577,10 +1634,16 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
             const uint32_t gmask = kGroup << (kLanesPerRow * h);
             if (bo >= 0) {
               if (hl == 0) atomicAdd(&sh.wchecks[warp], 1);
+#ifdef GMT_PHASE_TIMING
+              const long long w_c0 = clock64();
+#endif
               const bool ok = di_edge_free_half<kLanesPerRow>(
                   I, bx_s, tau_b, hl, gmask, kLanesPerRow * h, segh, tab_s + (warp * kRows + h) * kTabCap,
                   cull_s + (warp * kRows + h) * kCullCap, kCullCap, sh.vfull,
-                  (kDynScratch && sh.xsorted) ? sh.box_wx : -1.0);
+                  (kDynScratch && sh.xsorted) ? sh.box_wx : -1.0, rec_b);
+#ifdef GMT_PHASE_TIMING
+              if (lane == 0) w_chk += clock64() - w_c0;
+#endif
               if (ok && hl == 0) {
                 atomicAdd(&sh.wadded[warp], 1);
                 cost_s[x] = bv;
@@ -1654,6 +1717,13 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
         ext = next_ext;
         spec_row = next_spec;
       }
+#ifdef GMT_PHASE_TIMING
+      if (lane == 0) {
+        atomicAdd(&sh_ph[4], static_cast<unsigned long long>(clock64() - w_p5));
+        atomicAdd(&sh_ph[5], w_chk);
+      }
+      w_bar = clock64();
+#endif
     }
     if (lane == 0) {
       const int my_checks = sh.wchecks[warp], my_added = sh.wadded[warp];
@@ -1666,7 +1736,8 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
     }
     cluster_barrier<CS>();  // [2] commits visible in every replica
 #ifdef GMT_PHASE_TIMING
-    if (tid == 0) { const long long t_ = clock64(); sh_ph[3] += t_ - ph_t; ph_t = t_; }
+    if (lane == 0) atomicAdd(&sh_ph[6], static_cast<unsigned long long>(clock64() - w_bar));
+    if (tid == 0) { const long long t_ = clock64(); sh_ph[3] += static_cast<unsigned long long>(t_ - ph_t); ph_t = t_; }
 #endif
 
     if (rank == 0 && tid == 0) {  // IterationStats (planner.cpp:192-194)
@@ -1702,8 +1773,7 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
 
 #ifdef GMT_PHASE_TIMING
   if (tid == 0 && rank == 0 && R.counters)
-    for (int k = 0; k < 4; ++k)
-      atomicAdd(reinterpret_cast<unsigned long long*>(R.counters) + 4 + k, static_cast<unsigned long long>(sh_ph[k]));
+    for (int k = 0; k < 8; ++k) atomicAdd(reinterpret_cast<unsigned long long*>(R.counters) + 4 + k, sh_ph[k]);
 #endif
   if (counting) {
     long long c = cnt_open;

@@ -166,3 +166,27 @@ def test_pool_views_equal_materialised_rows(ctx, monkeypatch):
     for q in range(len(specs)):
         _same_graph(pv.graph(q), pm.graph(q))
         assert not abi.full_parity(pv.result(q), pm.result(q))
+
+
+def test_pool_check_records_equal_regeneration(ctx, monkeypatch):
+    """The pool's per-edge check records (bounding box, cube test and the
+    waypoint positions of each pool edge, built once with the pool graph)
+    replace the lazy check's table regeneration on pool edges: the same
+    results, full trees included, with GMT_POOL_REC=0 (a fresh context's pool
+    without records) as with them, through views and materialised rows."""
+    from paper_1705_02403_b200.native import Context
+    specs = _specs(96, first=500)
+    on_st, on_s, _ = ctx.plan_problems(specs)
+    on_b, _ = ctx.batch_problems(specs[:16])
+    on_b.launch()
+    monkeypatch.setenv("GMT_POOL_REC", "0")
+    off = Context(0)
+    off_st, off_s, _ = off.plan_problems(specs)
+    off_b, _ = off.batch_problems(specs[:16])
+    off_b.launch()
+    monkeypatch.delenv("GMT_POOL_REC")
+    assert (on_st == 0).all() and (off_st == 0).all()
+    key = lambda s: (s.status, bits([s.cost]), s.iterations, s.total_collision_checks)  # noqa: E731
+    assert [key(s) for s in on_s] == [key(s) for s in off_s]
+    for q in range(16):
+        assert not abi.full_parity(on_b.result(q), off_b.result(q)), q

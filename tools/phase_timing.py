@@ -14,7 +14,7 @@ b = ctx.batch(insts, 1.0)
 b.launch()
 ctx.synchronize()
 ctx.set_option(native.OPT_COUNTERS, 1)
-out = (C.c_int64 * 8)()
+out = (C.c_int64 * 16)()
 native.lib().gmt_ctx_counters(ctx.h, out, 1)
 b2 = ctx.batch(insts, 1.0)
 b2.launch()
