@@ -99,6 +99,7 @@ struct CtaShared {
   // only the boxes whose lom_x lies in [pmn_x - wx, pmx_x]
   int32_t xsorted;
   double box_wx;
+  const uint16_t* xfirst;  // x buckets of the sorted boxes (or null)
   // Loop state kept in shared memory rather than in every thread's
   // registers (the solve is register-bound): the threshold index i, the
   // pass number, the running check total (tid 0), per-warp check / commit
@@ -168,6 +169,27 @@ __device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
                : "memory");
 }
 
+
+// x buckets of the sorted boxes (the 24-warp DI shape): xfirst[b] = the
+// number of boxes whose lo_x - m lies below kXB0 + b * kXBW (b = 0: none,
+// b = kXB: all), so a check's x window [lo_t, hi_t] maps to a conservative
+// index range with two shared-memory loads (a bucket of slack either side
+// absorbs the rounding of the bucket index).
+constexpr int kXB = 256;
+constexpr double kXB0 = -1.0, kXBW = 2.5 / kXB;
+__device__ __forceinline__ int xbucket(double x) {
+  double f = (x - kXB0) * (1.0 / kXBW);
+  f = f < -4.0 ? -4.0 : (f > kXB + 4.0 ? kXB + 4.0 : f);
+  return __double2int_rd(f);
+}
+
+// One 8-byte global -> shared copy that holds no register (LDGSTS), and the
+// wait for this thread's copies.
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Closed box b contains p (Aabb::contains, space.cpp:11-16).
 template <int D>
@@ -663,7 +685,8 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
 template <int G>
 __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double tau, int gl, uint32_t gmask,
                                   int gbase, double* seg, double* tab, uint16_t* cull, int cull_cap, bool vfull,
-                                  double box_wx = -1.0, const double* rec = nullptr) {
+                                  double box_wx = -1.0, const double* rec = nullptr,
+                                  const uint16_t* xfirst = nullptr) {
   constexpr int dim = kDiDim;
   static_assert(G >= 8, "a group must hold a state's coordinates and the coefficient lanes");
   constexpr uint32_t kGroupBits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
@@ -673,7 +696,10 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
   DP.weight = I.kin_p[1];
   DP.segments = M;
   DP.reserved = 0;
-  if (tau == 0.0) {  // point_free(x0) (the degenerate edge's single state)
+  // point_free(x0) (the degenerate edge's single state).  (A record's
+  // zero-duration polyline is M copies of x0, which the record path tests
+  // the same way: cube, then Aabb::contains by the all-dk == 0 clip.)
+  if (!rec && tau == 0.0) {
     bool cube = true;
     if (gl < dim) cube = !(seg[gl] < 0.0 || seg[gl] > 1.0);
     if (!__all_sync(gmask, cube)) return false;
@@ -681,14 +707,16 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     for (int b = gl; b < bx.count && !in; b += G) in = box_has<6>(seg, dim, bx, b);
     return !__any_sync(gmask, in);
   }
-  if (rec) {  // the pool edge's record: the bounding box (NaN: leaves the cube)
-    double v = 0.0;
-    if (gl < kPoolRecHead) {
-      v = __ldg(rec + gl);
-      seg[gl < 3 ? gl : 13 + gl] = v;  // min -> seg[0..3), max -> seg[16..19)
-    }
-    if (__any_sync(gmask, gl == 0 && v != v)) return false;
+  if (rec) {
+    // The pool edge's record, all of it in flight at once: the bounding box
+    // (NaN: the polyline leaves the cube) and the waypoint positions.
+    // (asynchronous copies straight into shared memory: no registers held)
+    const int rl = kPoolRecHead + 3 * (M + 1);
+    for (int e = gl; e < rl; e += G)  // min -> seg[0..3), max -> seg[16..19), positions -> tab
+      cp_async8(e < kPoolRecHead ? seg + (e < 3 ? e : 13 + e) : tab + (e - kPoolRecHead), rec + e);
+    cp_async_wait_all();
     __syncwarp(gmask);
+    if (__any_sync(gmask, gl == 0 && seg[0] != seg[0])) return false;
   } else {
   if (gl < dim) {
     tab[gl] = seg[gl];
@@ -769,6 +797,13 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     // lom_x + wx; the 1e-9 widening absorbs the subtraction's rounding).
     // Two rounds over the group: the chunk, then the index in it.
     const double lo_t = (pmn[0] - box_wx) - 1e-9, hi_t = pmx[0];
+    if (xfirst) {
+      int bl = xbucket(lo_t) - 1, bh = xbucket(hi_t) + 2;
+      bl = bl < 0 ? 0 : (bl > kXB ? kXB : bl);
+      bh = bh < 0 ? 0 : (bh > kXB ? kXB : bh);
+      ib = xfirst[bl];
+      ie = xfirst[bh];
+    } else {
     const int chunk = (bx.count + G - 1) / G;
     const int last = gl * chunk + chunk - 1 < bx.count ? gl * chunk + chunk - 1 : bx.count - 1;
     const double xe = gl * chunk < bx.count ? bx.lom[last] : kInf;
@@ -787,6 +822,7 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
       ie += __popc((__ballot_sync(gmask, in) >> gbase) & kGroupBits);
     }
     ie = ie < bx.count ? ie : bx.count;
+    }
   }
   for (int i0 = ib; i0 < ie && kept <= cull_cap; i0 += G) {
     const int b = i0 + gl;
@@ -819,17 +855,17 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
   int ts = dim;  // waypoint stride in tab
   if (rec) {
     if (kept == 0) return true;  // no box meets the polyline's bounding box
-    for (int e = gl; e < 3 * (M + 1); e += G) tab[e] = __ldg(rec + kPoolRecHead + e);
-    __syncwarp(gmask);
     ts = 3;
   }
   const int nbx = sub.count;
   const int pairs = M * nbx;
+  const int lg_m = (M & (M - 1)) == 0 ? __ffs(M) - 1 : -1;  // (box-major pairs: no division for M = 2^k)
   for (int p0 = 0; p0 < pairs; p0 += G) {
     const int p = p0 + gl;
     bool hit = false;
     if (p < pairs) {
-      const int sg = p / nbx, bi = p - sg * nbx;
+      const int bi = lg_m >= 0 ? p >> lg_m : p / M;
+      const int sg = p - bi * M;
       const int box = sub.idx ? sub.idx[bi] : bi;
       hit = vfull ? seg_box_hit<6, true>(tab + sg * ts, tab + (sg + 1) * ts, dim, bx, box)
                   : seg_box_hit<6>(tab + sg * ts, tab + (sg + 1) * ts, dim, bx, box);
@@ -884,6 +920,15 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 // Two CTA shapes: WIDE = 512 threads with up to 128 registers (clusters,
 // and single-CTA queries that want the registers), narrow = 256 threads,
 // 64 registers, four CTAs per SM.
+#ifndef GMT_DI_XAHEAD
+#define GMT_DI_XAHEAD 1
+#endif
+#ifndef GMT_UNROLL_DI24
+#define GMT_UNROLL_DI24 GMT_UNROLL_BATCH
+#endif
+#ifndef GMT_DI_XBUCKET
+#define GMT_DI_XBUCKET 1
+#endif
 #ifndef GMT_DI_DYNAMIC
 #define GMT_DI_DYNAMIC 2  // (P5 dynamic: 24.6 -> 24.1 ms per 4096 configs[4] queries; P4 too: no gain)
 #endif
@@ -919,7 +964,7 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
   // (the 24-warp batched DI shape streams and checks four candidates per warp)
   constexpr int kRows = CS == 1 ? ((D == 6 && NW == 24) ? GMT_ROWS_DI24 : GMT_ROWS_PER_WARP) : GMT_ROWS_CLUSTER;
   constexpr int kLanesPerRow = kWarp / kRows;
-  constexpr int kUnroll = CS == 1 ? GMT_UNROLL_BATCH : GMT_UNROLL_CLUSTER;
+  constexpr int kUnroll = CS == 1 ? ((D == 6 && NW == 24) ? GMT_UNROLL_DI24 : GMT_UNROLL_BATCH) : GMT_UNROLL_CLUSTER;
   // Dynamic row / candidate distribution (a shared counter): clusters, and
   // the batched 24-warp DI shape's candidates (GMT_DI_DYNAMIC bit 1: P4 rows,
   // bit 2: P5 candidates), whose lazy checks vary widely in cost.
@@ -1008,6 +1053,10 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
     constexpr bool kXSort = D == 6 && kDynScratch;
     constexpr int kSortMax = 256;
     __shared__ uint8_t xrank_s[kXSort ? kSortMax : 1];
+    __shared__ uint16_t xfirst_s[(kXSort && GMT_DI_XBUCKET) ? kXB + 1 : 1];
+    if constexpr (kXSort && GMT_DI_XBUCKET) {
+      if (tid == 0) sh.xfirst = xfirst_s;
+    }
     const bool xsort = kXSort && nb <= kSortMax;
     if (xsort) {
       for (int b = tid; b < nb; b += nt) {
@@ -1046,6 +1095,14 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
           w = e > w ? e : w;
         }
         sh.box_wx = w * (1.0 + 1e-12) + 1e-12;  // (rounded up: every him_x <= lom_x + box_wx)
+      }
+      if constexpr (kXSort && GMT_DI_XBUCKET) {
+        for (int b = tid; b <= kXB; b += nt) {
+          const double xb = kXB0 + static_cast<double>(b) * kXBW;
+          int c = 0;
+          for (int i = 0; i < nb; ++i) c += lom[i] < xb ? 1 : 0;
+          xfirst_s[b] = static_cast<uint16_t>(b == 0 ? 0 : (b == kXB ? nb : c));
+        }
       }
     }
     if (tid == 0) sh.xsorted = xsort ? 1 : 0;
@@ -1455,6 +1512,13 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
           len = static_cast<int>(__ldg(I.in_end + x) - e0);
         }
       }
+      // (batched DI) the candidate's coordinates are loaded one iteration
+      // ahead, with the next row's offsets
+      constexpr bool kXAhead = GMT_DI_XAHEAD && D == 6 && kRows >= 2 && kLanesPerRow >= 6;
+      double xcrd = 0.0;
+      if constexpr (kXAhead) {
+        if (x >= 0 && hl < 6) xcrd = __ldg(I.coords + static_cast<int64_t>(x) * 6 + hl);
+      }
       while (k < ccount) {
         int kn = k + kRows * nw;
         if constexpr (kDynamic) {
@@ -1484,10 +1548,16 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
             }
           }
         }
+        double nxcrd = 0.0;
+        if constexpr (kXAhead) {
+          if (xn >= 0 && hl < 6) nxcrd = __ldg(I.coords + static_cast<int64_t>(xn) * 6 + hl);
+        }
         // The segment's B endpoint (the candidate) is staged while the row
         // streams in; the A endpoint (the chosen parent) after the argmin.
         __syncwarp();
-        if constexpr (kLanesPerRow >= kMaxSolveDim) {
+        if constexpr (kXAhead) {
+          if (x >= 0 && hl < 6) segh[16 + hl] = xcrd;
+        } else if constexpr (kLanesPerRow >= kMaxSolveDim) {
           if (x >= 0 && hl < d) segh[16 + hl] = __ldg(I.coords + static_cast<int64_t>(x) * d + hl);
         } else {
           for (int t = hl; x >= 0 && t < d; t += kLanesPerRow)
@@ -1592,9 +1662,26 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
         }
         // The chosen in-edge's duration (kinodynamic graphs) and both chosen
         // parents' coordinates in flight together.
+        // A pool edge's check record (batched DI over the shared pool, every
+        // box spanning the velocity axes): the edge's own pool in-edge.  The record
+        // holds everything the check reads (the duration and the end points
+        // are not loaded), so its copy starts right after the argmin.
+        const double* rec_b = nullptr;
+        if constexpr (D == 6 && kRows >= 2) {
+          if (bo >= 0 && sh.vfull) {
+            if (viewed) {
+              if (PV.rec && !spec_row && bo < len) rec_b = PV.rec + (e0 + bo) * PV.rec_len;
+            } else if (I.in_pe) {
+              // (loading it for every best update during the scan measured
+              // slower: 23.8 vs 22.0 ms, register pressure in the scan loop)
+              const int32_t pe = __ldg(I.in_pe + e0 + bo);
+              if (pe >= 0) rec_b = I.pool_rec + static_cast<int64_t>(pe) * I.pool_rec_len;
+            }
+          }
+        }
         double tau_b = 0.0;
-        if ((D == 0 || D == 6) && bo >= 0 && I.in_tau) tau_b = __ldg(I.in_tau + e0 + bo);
-        if (viewed && bo >= 0) {
+        if ((D == 0 || D == 6) && bo >= 0 && !rec_b && I.in_tau) tau_b = __ldg(I.in_tau + e0 + bo);
+        if (viewed && bo >= 0 && !rec_b) {
           if (spec_row) {
             tau_b = __ldg(PV.stau + PV.cap + bo);
           } else if (bo < len) {
@@ -1605,23 +1692,10 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
             tau_b = __ldg(PV.stau + static_cast<int64_t>(t == 0 ? 0 : 2) * PV.cap + j);
           }
         }
-        // A pool edge's check record (batched DI over the shared pool, every
-        // box spanning the velocity axes): the edge's own pool in-edge.
-        const double* rec_b = nullptr;
-        if constexpr (D == 6 && kRows >= 2) {
-          if (bo >= 0 && sh.vfull) {
-            if (viewed) {
-              if (PV.rec && !spec_row && bo < len) rec_b = PV.rec + (e0 + bo) * PV.rec_len;
-            } else if (I.in_pe) {
-              const int32_t pe = __ldg(I.in_pe + e0 + bo);
-              if (pe >= 0) rec_b = I.pool_rec + static_cast<int64_t>(pe) * I.pool_rec_len;
-            }
-          }
-        }
         if constexpr (kLanesPerRow >= kMaxSolveDim) {
           if (bo >= 0 && hl < d) segh[hl] = __ldg(I.coords + static_cast<int64_t>(by) * d + hl);
         } else {
-          for (int t = hl; bo >= 0 && t < d; t += kLanesPerRow)
+          for (int t = hl; bo >= 0 && !rec_b && t < d; t += kLanesPerRow)
             segh[t] = __ldg(I.coords + static_cast<int64_t>(by) * d + t);
         }
         __syncwarp();
@@ -1640,7 +1714,8 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
               const bool ok = di_edge_free_half<kLanesPerRow>(
                   I, bx_s, tau_b, hl, gmask, kLanesPerRow * h, segh, tab_s + (warp * kRows + h) * kTabCap,
                   cull_s + (warp * kRows + h) * kCullCap, kCullCap, sh.vfull,
-                  (kDynScratch && sh.xsorted) ? sh.box_wx : -1.0, rec_b);
+                  (kDynScratch && sh.xsorted) ? sh.box_wx : -1.0, rec_b,
+                  (kDynScratch && sh.xsorted && GMT_DI_XBUCKET) ? sh.xfirst : nullptr);
 #ifdef GMT_PHASE_TIMING
               if (lane == 0) w_chk += clock64() - w_c0;
 #endif
@@ -1655,6 +1730,7 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
             __syncwarp();
             k = kn;
             x = xn;
+            xcrd = nxcrd;
             e0 = n0;
             len = nlen;
             ext = next_ext;
@@ -1712,6 +1788,7 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
         }
         k = kn;
         x = xn;
+        xcrd = nxcrd;
         e0 = n0;
         len = nlen;
         ext = next_ext;

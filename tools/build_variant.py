@@ -13,7 +13,13 @@ name, defs = sys.argv[1], sys.argv[2:]
 obj = os.path.join(ROOT, "build", "variants", name)
 os.makedirs(obj, exist_ok=True)
 objs, procs = [], []
+# ONLY=solve.cu,...: compile just those with the defines, link the in-tree
+# build's objects (build/obj, current) for the rest
+only = [x for x in os.environ.get("ONLY", "").split(",") if x]
 for src in B.SOURCES:  # (in parallel)
+    if only and src not in only:
+        objs.append(os.path.join(B.OBJ, os.path.splitext(src)[0] + ".o"))
+        continue
     o = os.path.join(obj, os.path.splitext(src)[0] + ".o")
     procs.append(subprocess.Popen([B.NVCC, *B.FLAGS, *defs, "-c", os.path.join(B.CSRC, src), "-o", o]))
     objs.append(o)
