@@ -664,8 +664,10 @@ __global__ void __launch_bounds__(256) pool_rows_kernel(
     const int j = b0 + gl;
     const int32_t ycol = j < li ? __ldg(pin_col + ie0 + j) : -1;
     const int32_t vcol = j < lo ? __ldg(pout_col + oe0 + j) : -1;
-    const uint16_t ri = ycol >= 0 ? rk[ycol] : kNoRank;
-    const uint16_t ro = vcol >= 0 ? rk[vcol] : kNoRank;
+    // (pool points past the scan, y >= Kc, are no query's vertices: a pool
+    // graph built for larger queries is longer than a later call's rank maps)
+    const uint16_t ri = ycol >= 0 && ycol < Kc ? rk[ycol] : kNoRank;
+    const uint16_t ro = vcol >= 0 && vcol < Kc ? rk[vcol] : kNoRank;
     constexpr uint32_t kGroupMask = kRowLanes == 32 ? 0xffffffffu : ((1u << kRowLanes) - 1u);
     const uint32_t mi = (__ballot_sync(kFull, ri != kNoRank) >> gshift) & kGroupMask;
     const uint32_t mo = (__ballot_sync(kFull, ro != kNoRank) >> gshift) & kGroupMask;
@@ -1483,7 +1485,7 @@ extern "C" int gmt_batch_graph(gmt_ctx* ctx, gmt_batch* b, int32_t q, int32_t* n
       } else {
         const int p = sel[x];
         for (int64_t e = pip[p]; e < pip[p + 1]; ++e) {
-          if (rank[pic[e]] == kPoolNoRank) continue;
+          if (pic[e] >= pv.kc || rank[pic[e]] == kPoolNoRank) continue;
           icol.push_back(rank[pic[e]]);
           icost.push_back(pics[e]);
           itau.push_back(pit[e]);
@@ -1499,7 +1501,7 @@ extern "C" int gmt_batch_graph(gmt_ctx* ctx, gmt_batch* b, int32_t q, int32_t* n
           itau.push_back(stau[2 * cap + spj[2 * x + 1]]);
         }
         for (int64_t e = pop[p]; e < pop[p + 1]; ++e)
-          if (rank[poc[e]] != kPoolNoRank) ocol.push_back(rank[poc[e]]);
+          if (poc[e] < pv.kc && rank[poc[e]] != kPoolNoRank) ocol.push_back(rank[poc[e]]);
         if (pv.subst && (code[x] & 2)) ocol.push_back(g);
         if (code[x] & 8) ocol.push_back(init);
       }

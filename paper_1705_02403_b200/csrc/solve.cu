@@ -1169,8 +1169,11 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
   // Shared-pool views: pool point y -> query vertex (or -1).  (A shared-
   // memory bitmask + rank bases measured slower than this L1-cached gather:
   // 46.6 vs 41.9 ms per 4096 queries.)
+  // (The whole rank map staged in shared memory measured slower as well in
+  // the 24-warp shape: 26.6 vs 23.3 ms per 4096 queries.)
   auto pool_rank = [&](int y) -> int {
-    const uint16_t r = __ldg(PV.rank + y);
+    // (y >= kc: a pool point past this call's scan, no query's vertex)
+    const uint16_t r = y < PV.kc ? __ldg(PV.rank + y) : kPoolNoRank;
     return r == kPoolNoRank ? -1 : static_cast<int>(r);
   };
 

@@ -63,7 +63,7 @@ __host__ __device__ inline SolveLayout solve_layout(int n, int d, int nb, bool o
 #define GMT_ROWS_DI24 4  // concurrent candidates (rows, checks) per warp of the 24-warp DI shape
 #endif
 constexpr int kDiTabCap = 56;  // doubles of one DI waypoint table ((segments + 1) * 6 <= 56)
-inline size_t solve_dyn_scratch(int threads, int dim) {
+__host__ __device__ inline size_t solve_dyn_scratch(int threads, int dim) {
   if (threads != 768 || dim != 6) return 0;
   return static_cast<size_t>(24) * GMT_ROWS_DI24 * ((32 + kDiTabCap) * sizeof(double) + 64 * sizeof(uint16_t));
 }

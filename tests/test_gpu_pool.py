@@ -190,3 +190,28 @@ def test_pool_check_records_equal_regeneration(ctx, monkeypatch):
     assert [key(s) for s in on_s] == [key(s) for s in off_s]
     for q in range(16):
         assert not abi.full_parity(on_b.result(q), off_b.result(q)), q
+
+
+def test_pool_smaller_queries_after_larger():
+    """A context's pool grows to the largest query it has seen; a later call
+    with smaller queries scans fewer pool points (its rank maps are shorter
+    than the pool graph), yet pool rows still name every pool point: those
+    past the scan are no query's vertices.  Graphs and results equal the
+    single builds."""
+    from paper_1705_02403_b200.native import Context
+    c = Context(0)
+    big = _specs(8, n=4000, first=700)
+    st, _, _ = c.plan_problems(big)
+    assert (st == 0).all()
+    small = _specs(16, n=900, first=720)
+    st, summ, _ = c.plan_problems(small)
+    pb, st2 = c.batch_problems(small)
+    assert (st == 0).all() and (st2 == 0).all()
+    pb.launch()
+    for q, s in enumerate(small):
+        inst = c.build_instance(s)
+        r = c.plan(inst)
+        assert (summ[q].status, summ[q].cost, summ[q].iterations, summ[q].total_collision_checks) == \
+            (r.status, r.cost, r.iterations, r.total_collision_checks), q
+        _same_graph(pb.graph(q), c.batch([inst], 1.0).graph(0))
+        assert not abi.full_parity(pb.result(q), r), q
