@@ -191,6 +191,18 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// A pointer into the dynamic shared memory rebased on the extern array, so
+// the compiler sees its address space and loads through it are LDS (short
+// scoreboard) instead of generic LD.  (The staged boxes' pointers are read
+// back from the shared Boxes descriptor, which loses that information.)
+extern __shared__ __align__(16) unsigned char gmt_dyn_smem[];
+template <typename T>
+__device__ __forceinline__ const T* shared_view(const T* p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(gmt_dyn_smem));
+  return reinterpret_cast<const T*>(gmt_dyn_smem + static_cast<int32_t>(a - b));
+}
+
 // Closed box b contains p (Aabb::contains, space.cpp:11-16).
 template <int D>
 __device__ __forceinline__ bool box_has(const double* p, int d_rt, const Boxes& bx, int b) {
@@ -457,6 +469,49 @@ __device__ __forceinline__ bool seg_box_hit(const double* a, const double* b, in
   return true;
 }
 
+#ifndef GMT_SB_VIEWS
+#define GMT_SB_VIEWS 1
+#endif
+
+// seg_box_hit<6, true> with the staged box arrays passed in (axis stride
+// `as`, box stride 1): shared_view pointers make the bound loads LDS
+// (configs[4] rows solve 21.8 -> 21.0 ms per 4096 queries).
+// (An exact-safe variant forming the quotients with a Newton reciprocal and
+// dividing only for near ties measured no faster in rows and 16 % slower in
+// the pool-view solve -- register pressure at the 80-register cap.)
+__device__ __forceinline__ bool seg_box_hit_pos3(const double* a, const double* b, const double* blo,
+                                                 const double* bhi, const double* lom, const double* him, int as,
+                                                 int box) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double lo = lom[box + k * as], hi = him[box + k * as];
+    const double x = a[k], y = b[k];
+    if ((x < lo && y < lo) || (x > hi && y > hi)) return false;
+  }
+  double tmin = 0.0, tmax = 1.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double ak = a[k];
+    const double dk = __dsub_rn(b[k], ak);
+    const double l = blo[box + k * as], h = bhi[box + k * as];
+    if (dk == 0.0) {
+      if (ak < l || ak > h) return false;
+    } else {
+      double t0 = __ddiv_rn(__dsub_rn(l, ak), dk);
+      double t1 = __ddiv_rn(__dsub_rn(h, ak), dk);
+      if (t0 > t1) {
+        const double t = t0;
+        t0 = t1;
+        t1 = t;
+      }
+      tmin = (tmin < t0) ? t0 : tmin;
+      tmax = (t1 < tmax) ? t1 : tmax;
+      if (tmin > tmax) return false;
+    }
+  }
+  return true;
+}
+
 __device__ __forceinline__ void kin_params(const DevInstance& I, QuadParams& QP, DiParams& DP) {
   const int M = I.kin_segments;
   QP.g = I.kin_p[0];
@@ -682,7 +737,7 @@ __device__ bool kino_edge_free_warp(const DevInstance& I, const Boxes& bx, int f
 // record (common.cuh), which replaces the table, the cube test and the
 // bounding box; the table's positions are read only when some box survives
 // the cull.
-template <int G>
+template <int G, bool SB = false>
 __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double tau, int gl, uint32_t gmask,
                                   int gbase, double* seg, double* tab, uint16_t* cull, int cull_cap, bool vfull,
                                   double box_wx = -1.0, const double* rec = nullptr,
@@ -824,6 +879,25 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
     ie = ie < bx.count ? ie : bx.count;
     }
   }
+  if (SB && vfull) {
+    // The staged boxes are in this CTA's shared memory: LDS views (box
+    // stride 1, axis stride as); only the position axes can separate.
+    const double* const lom_v = shared_view(bx.lom);
+    const double* const him_v = shared_view(bx.him);
+    const int as = bx.as;
+    for (int i0 = ib; i0 < ie && kept <= cull_cap; i0 += G) {
+      const int b = i0 + gl;
+      bool meets = b < ie;
+      const int bc = meets ? b : 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) meets = meets && !(pmx[k] < lom_v[bc + k * as] || pmn[k] > him_v[bc + k * as]);
+      const uint32_t m = (__ballot_sync(gmask, meets) >> gbase) & kGroupBits;
+      const int at = kept + __popc(m & ((1u << gl) - 1u));
+      if (meets && at < cull_cap) cull[at] = static_cast<uint16_t>(b);
+      kept += __popc(m);
+    }
+    ie = ib;  // (done: the generic loop below runs no iteration)
+  }
   for (int i0 = ib; i0 < ie && kept <= cull_cap; i0 += G) {
     const int b = i0 + gl;
     bool meets = b < ie;
@@ -860,6 +934,25 @@ __device__ bool di_edge_free_half(const DevInstance& I, const Boxes& bx, double 
   const int nbx = sub.count;
   const int pairs = M * nbx;
   const int lg_m = (M & (M - 1)) == 0 ? __ffs(M) - 1 : -1;  // (box-major pairs: no division for M = 2^k)
+  if (SB && vfull) {
+    const double* const lo_v = shared_view(bx.lo);
+    const double* const hi_v = shared_view(bx.hi);
+    const double* const lom_v = shared_view(bx.lom);
+    const double* const him_v = shared_view(bx.him);
+    const int as = bx.as;
+    for (int p0 = 0; p0 < pairs; p0 += G) {
+      const int p = p0 + gl;
+      bool hit = false;
+      if (p < pairs) {
+        const int bi = lg_m >= 0 ? p >> lg_m : p / M;
+        const int sg = p - bi * M;
+        const int box = sub.idx ? sub.idx[bi] : bi;
+        hit = seg_box_hit_pos3(tab + sg * ts, tab + (sg + 1) * ts, lo_v, hi_v, lom_v, him_v, as, box);
+      }
+      if (__any_sync(gmask, hit)) return false;
+    }
+    return true;
+  }
   for (int p0 = 0; p0 < pairs; p0 += G) {
     const int p = p0 + gl;
     bool hit = false;
@@ -1170,7 +1263,9 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
   // memory bitmask + rank bases measured slower than this L1-cached gather:
   // 46.6 vs 41.9 ms per 4096 queries.)
   // (The whole rank map staged in shared memory measured slower as well in
-  // the 24-warp shape: 26.6 vs 23.3 ms per 4096 queries.)
+  // the 24-warp shape: 26.6 vs 23.3 ms per 4096 queries; so did the open set
+  // mirrored as pool-point bits, gathering ranks for open entries only: 27.9
+  // vs 27.2 ms -- the scan waits on the pool rows' loads, not on the map.)
   auto pool_rank = [&](int y) -> int {
     // (y >= kc: a pool point past this call's scan, no query's vertex)
     const uint16_t r = y < PV.kc ? __ldg(PV.rank + y) : kPoolNoRank;
@@ -1714,7 +1809,7 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
 #ifdef GMT_PHASE_TIMING
               const long long w_c0 = clock64();
 #endif
-              const bool ok = di_edge_free_half<kLanesPerRow>(
+              const bool ok = di_edge_free_half<kLanesPerRow, !GS && GMT_SB_VIEWS>(
                   I, bx_s, tau_b, hl, gmask, kLanesPerRow * h, segh, tab_s + (warp * kRows + h) * kTabCap,
                   cull_s + (warp * kRows + h) * kCullCap, kCullCap, sh.vfull,
                   (kDynScratch && sh.xsorted) ? sh.box_wx : -1.0, rec_b,

@@ -1,7 +1,7 @@
 """Top source lines by warp-stall samples from an ncu report
 (ncu --page source --print-source cuda,sass CSV).
 
-  python tools/ncu_src.py report.ncu-rep kernel_regex [top]"""
+  python tools/ncu_src.py report.ncu-rep kernel_regex|#launch_index [top]"""
 import csv
 import io
 import subprocess
@@ -9,8 +9,11 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-                      "--kernel-name", "regex:" + kern], capture_output=True, text=True).stdout
+# kern "#K" selects the report's K-th profiled launch instead of a name regex
+sel = (["--launch-skip", kern[1:], "--launch-count", "1"] if kern.startswith("#")
+       else ["--kernel-name", "regex:" + kern])
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + sel,
+                     capture_output=True, text=True).stdout
 fname, hdr, data = None, None, []
 stall_cols = []
 for r in csv.reader(io.StringIO(out)):
