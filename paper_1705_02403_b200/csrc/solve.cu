@@ -469,6 +469,9 @@ __device__ __forceinline__ bool seg_box_hit(const double* a, const double* b, in
   return true;
 }
 
+#ifndef GMT_POOL_HOIST
+#define GMT_POOL_HOIST 1
+#endif
 #ifndef GMT_SB_VIEWS
 #define GMT_SB_VIEWS 1
 #endif
@@ -1487,6 +1490,10 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
         const bool mapped = viewed && rowp == nullptr;  // pool row: entries are pool points
         const int32_t* ocol = (viewed ? (rowp ? rowp : PV.out_col + e0) : I.out_col + e0) + hl;
         const int lim = len - hl;
+#if GMT_POOL_HOIST
+        const uint16_t* const pv_rank = PV.rank;
+        const int pv_kc = PV.kc;
+#endif
         if (viewed && hl == 0 && ext) {  // the row's edges into g (n - 1) and init (n)
           if (PV.subst && (ext & 2)) atomicOr(cand_w + ((I.n - 2) >> 5), 1u << ((I.n - 2) & 31));
           if (ext & 8) atomicOr(cand_w + ((I.n - 1) >> 5), 1u << ((I.n - 1) & 31));
@@ -1497,9 +1504,18 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
           for (int u = 0; u < kUnroll; ++u)
             xs[u] = off + u * kLanesPerRow < lim ? __ldg(ocol + off + u * kLanesPerRow) : -1;
           if (mapped) {
+#if GMT_POOL_HOIST
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+              const int y = xs[u];
+              const uint16_t r = (y >= 0 && y < pv_kc) ? __ldg(pv_rank + y) : kPoolNoRank;
+              xs[u] = r == kPoolNoRank ? -1 : static_cast<int>(r);
+            }
+#else
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
               if (xs[u] >= 0) xs[u] = pool_rank(xs[u]);
+#endif
           }
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
@@ -1610,6 +1626,10 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
           len = static_cast<int>(__ldg(I.in_end + x) - e0);
         }
       }
+      // (Staging each group's next in-row into shared memory with cp.async
+      // while the current candidate is checked measured slower: 21.0 -> 24.6
+      // ms rows, 27.2 -> 35.2 ms views per 4096 configs[4] queries with 64
+      // entries per group -- the L1 carve-out it takes and the registers.)
       // (batched DI) the candidate's coordinates are loaded one iteration
       // ahead, with the next row's offsets
       constexpr bool kXAhead = GMT_DI_XAHEAD && D == 6 && kRows >= 2 && kLanesPerRow >= 6;
@@ -1674,6 +1694,10 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
         const double* rcost =
             (viewed ? (spec_row ? PV.scost + PV.cap : PV.in_cost + e0) : I.in_cost + e0) + hl;
         const int lim = len - hl;  // element u of chunk `off` exists iff off + u * kLanesPerRow < lim
+#if GMT_POOL_HOIST
+        const uint16_t* const pv_rank = PV.rank;
+        const int pv_kc = PV.kc;
+#endif
         for (int off = 0; off < lmax; off += kLanesPerRow * kUnroll) {
           int ys[kUnroll];
           double cs[kUnroll];
@@ -1684,9 +1708,20 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
             cs[u] = in ? __ldg(rcost + off + u * kLanesPerRow) : 0.0;
           }
           if (mapped) {
+#if GMT_POOL_HOIST
+            // (the map's base and length from registers: pool_rank reloads
+            // them from the shared descriptor for every element)
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+              const int y = ys[u];
+              const uint16_t r = (y >= 0 && y < pv_kc) ? __ldg(pv_rank + y) : kPoolNoRank;
+              ys[u] = r == kPoolNoRank ? -1 : static_cast<int>(r);
+            }
+#else
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
               if (ys[u] >= 0) ys[u] = pool_rank(ys[u]);
+#endif
           }
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
