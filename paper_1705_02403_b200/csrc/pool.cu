@@ -342,58 +342,50 @@ __global__ void __launch_bounds__(256) pool_init_kernel(const PQ* __restrict__ p
 // predicate and order (di_graph.cu).  Two kernels: the exact-safe prefilters
 // (few registers, many warps) compact the surviving columns in order, then
 // the capped 2BVP solve runs lane-parallel over the survivors only.
+// (One warp per special vertex testing both directions from one pass over
+// the coordinates measured slower: 2.43 -> 2.89 ms per 4096 queries -- half
+// the warps, and the two cost tests serialised.)
 __global__ void __launch_bounds__(256) pool_special_cand_kernel(const PQ* __restrict__ pq, DiParams P, double bound,
                                                                 double radius, const double* __restrict__ qcoords,
                                                                 int32_t* __restrict__ cand, PQOut* __restrict__ out) {
-  // One warp per (query, special vertex): both lists of that vertex (l =
-  // 2 * src: out-row, l + 1: in-row) from one pass over the coordinates --
-  // the position prefilter |to_k - from_k| <= bound reads the same for both
-  // directions (IEEE subtraction is sign-symmetric).
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // (query, source)
-  const int q = gw >> 1, src = gw & 1;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // (query, list)
+  const int q = gw >> 2, l = gw & 3;
   const PQ Q = pq[q];
   if (Q.skip || out[q].fallback) return;
-  if (src == 0 && !out[q].subst) return;
+  if (l < 2 && !out[q].subst) return;
   const int V = Q.n + 1;
-  const int s = src == 0 ? Q.n - 1 : Q.n;
-  const int l0 = 2 * src;
+  const int s = l < 2 ? Q.n - 1 : Q.n;
+  const bool outgoing = (l & 1) == 0;
   const double* base = qcoords + Q.node_off * kD;
   double xs[kD];
 #pragma unroll
   for (int k = 0; k < kD; ++k) xs[k] = base[static_cast<int64_t>(s) * kD + k];
-  int32_t* cl_out = cand + (static_cast<int64_t>(q) * 4 + l0) * kCandCap;
-  int32_t* cl_in = cl_out + kCandCap;
-  int len_out = 0, len_in = 0;
+  int32_t* cl = cand + (static_cast<int64_t>(q) * 4 + l) * kCandCap;
+  int len = 0;
   for (int b0 = 0; b0 < V; b0 += 32) {
     const int x = b0 + lane;
-    bool near = x < V && x != s;
-    bool may_out = false, may_in = false;
-    if (near) {
+    bool may = x < V && x != s;
+    if (may) {
       double xx[kD];
 #pragma unroll
       for (int k = 0; k < kD; ++k) xx[k] = base[static_cast<int64_t>(x) * kD + k];
+      const double* from = outgoing ? xs : xx;
+      const double* to = outgoing ? xx : xs;
       for (int k = 0; k < 3; ++k) {  // di_may_connect (di_graph.cu)
-        const double D = xx[k] - xs[k];
-        if (D > bound || -D > bound) near = false;
+        const double D = to[k] - from[k];
+        if (D > bound || -D > bound) may = false;
       }
-      if (near) {
-        may_out = !di_cost_exceeds(di_coef(xs, xx, P), radius);
-        may_in = !di_cost_exceeds(di_coef(xx, xs, P), radius);
-      }
+      if (may) may = !di_cost_exceeds(di_coef(from, to, P), radius);
     }
-    const uint32_t mo = __ballot_sync(kFull, may_out), mi = __ballot_sync(kFull, may_in);
-    const uint32_t below = (1u << lane) - 1u;
-    const int so = len_out + __popc(mo & below), si = len_in + __popc(mi & below);
-    if (may_out && so < kCandCap) cl_out[so] = x;
-    if (may_in && si < kCandCap) cl_in[si] = x;
-    len_out += __popc(mo);
-    len_in += __popc(mi);
+    const uint32_t m = __ballot_sync(kFull, may);
+    const int slot = len + __popc(m & ((1u << lane) - 1u));
+    if (may && slot < kCandCap) cl[slot] = x;
+    len += __popc(m);
   }
   if (lane == 0) {
-    out[q].spec_len[l0] = len_out;  // (candidates here; the solve kernel overwrites it)
-    out[q].spec_len[l0 + 1] = len_in;
-    if (len_out > kCandCap || len_in > kCandCap) out[q].fallback = 1;
+    out[q].spec_len[l] = len;  // (candidates here; the solve kernel overwrites it)
+    if (len > kCandCap) out[q].fallback = 1;
   }
 }
 
@@ -1113,7 +1105,7 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
       pool_init_kernel<<<count, 256, 0, s>>>(d_pq, d_init, d_qc, d_po);
       timer.mark();
       GMT_CUDA(cudaMemsetAsync(d_spc, 0, sizeof(int32_t) * node_total, s));
-      pool_special_cand_kernel<<<(2 * count + 7) / 8, 256, 0, s>>>(d_pq, DP, di_prefilter_bound(DP, pool->radius),
+      pool_special_cand_kernel<<<(4 * count + 7) / 8, 256, 0, s>>>(d_pq, DP, di_prefilter_bound(DP, pool->radius),
                                                                     pool->radius, d_qc, d_cand, d_po);
       pool_special_kernel<<<count, 128, 0, s>>>(d_pq, DP, pool->radius, d_qc, d_cand, d_scol, d_scost, d_stau, d_spc,
                                                 d_spj, d_po);
