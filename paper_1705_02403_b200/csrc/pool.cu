@@ -162,21 +162,23 @@ __global__ void __launch_bounds__(256) pool_free_kernel(const PQ* __restrict__ p
   if (Q.skip) return;
   const double* lo = box_lo + Q.box_off * kD;
   const double* hi = box_hi + Q.box_off * kD;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  double x[kD];
+  if (p < K) {
+#pragma unroll
+    for (int k = 0; k < kD; ++k) x[k] = __ldg(P + static_cast<int64_t>(p) * kD + k);
+  }
   if (Q.nb <= stage_cap) {
     for (int i = threadIdx.x; i < Q.nb * kD; i += blockDim.x) {
       bsm[i] = lo[i];
       bsm[Q.nb * kD + i] = hi[i];
     }
     __syncthreads();
-    lo = bsm;
-    hi = bsm + Q.nb * kD;
+    // (the staged copy named directly: shared-space loads, not generic)
+    if (p < K) flags[static_cast<int64_t>(q) * K + p] = free_pt(x, bsm, bsm + Q.nb * kD, Q.nb) ? 1 : 0;
+    return;
   }
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= K) return;
-  double x[kD];
-#pragma unroll
-  for (int k = 0; k < kD; ++k) x[k] = __ldg(P + static_cast<int64_t>(p) * kD + k);
-  flags[static_cast<int64_t>(q) * K + p] = free_pt(x, lo, hi, Q.nb) ? 1 : 0;
+  if (p < K) flags[static_cast<int64_t>(q) * K + p] = free_pt(x, lo, hi, Q.nb) ? 1 : 0;
 }
 
 // The first n free candidates in stream order are the query's samples
