@@ -207,11 +207,19 @@ GMT_HD double di_cost_tau(const double* x0, const double* x1, const DiParams& P,
 // search's c(tau) (|P| terms are O(10), errors O(1e-14)): a pair whose true
 // minimum is within that margin of r is left to the search.
 constexpr int kDiRejectParts = 12;
-GMT_HD bool di_cost_exceeds(const DiCoef& c, double r) {
+GMT_HD double di_reject_margin(const DiCoef& c, double r) {
   const double scale = r * r * r * r + c.a * r * r + (c.b < 0.0 ? -c.b : c.b) * r + c.c0 + 1.0;
-  const double margin = 1e-9 * scale;
+  return 1e-9 * scale;
+}
+GMT_HD double di_reject_vertex(const DiCoef& c) {
+  return c.a > 0.0 ? -c.b / (2.0 * c.a) : -1.0;  // vertex of Q (a > 0: convex)
+}
+
+// The kDiRejectParts-part test.
+GMT_HD bool di_cost_exceeds_parts(const DiCoef& c, double r) {
+  const double margin = di_reject_margin(c, r);
   const double tm = 0.75 * r;                 // argmin of tau^3 (tau - r)
-  const double tv = c.a > 0.0 ? -c.b / (2.0 * c.a) : -1.0;  // vertex of Q (a > 0: convex)
+  const double tv = di_reject_vertex(c);
   double h = r;
   for (int i = 0; i < kDiRejectParts; ++i) {
     const double l = i + 1 == kDiRejectParts ? 0.0 : r * static_cast<double>(kDiRejectParts - 1 - i) / kDiRejectParts;
@@ -229,6 +237,31 @@ GMT_HD bool di_cost_exceeds(const DiCoef& c, double r) {
     h = l;
   }
   return true;
+}
+
+// The whole interval (0, r] at once: its lower bound is below every part's
+// (a >= 0 always: sa = (v0 + v1/2)^2 + 3 v1^2 / 4), so when it clears twice
+// the margin -- far above the rounding of either evaluation -- every part
+// clears the margin and di_cost_exceeds_parts is true as well
+// (tests/cpp/test_di_reject.cpp checks that implication).
+GMT_HD bool di_cost_exceeds_whole(const DiCoef& c, double r) {
+  const double margin = di_reject_margin(c, r);
+  const double tm = 0.75 * r;
+  const double tv = di_reject_vertex(c);
+  const double g = tm * tm * tm * (tm - r);
+  const double q0 = c.c0, qr = (c.a * r + c.b) * r + c.c0;
+  double q = q0 < qr ? q0 : qr;
+  if (tv > 0.0 && tv < r) {
+    const double qv = (c.a * tv + c.b) * tv + c.c0;
+    q = qv < q ? qv : q;
+  }
+  return g + q > 2.0 * margin;
+}
+
+// Most rejected pairs are decided by the whole-interval bound; the rest
+// take the parts.  Same outcome as di_cost_exceeds_parts alone.
+GMT_HD bool di_cost_exceeds(const DiCoef& c, double r) {
+  return di_cost_exceeds_whole(c, r) || di_cost_exceeds_parts(c, r);
 }
 
 // State at time t on the optimal trajectory x0 -> x1 of duration tau

@@ -1,7 +1,9 @@
 // Host check of the double integrator's exact-safe rejection bound
 // (di_cost_exceeds, csrc/di.cuh): over random state pairs and radii, every
 // rejected pair's exact minimum cost (di_cost_tau, the same header's search)
-// exceeds r.  Prints the rejection rate.  Exit code 1 on a violation.
+// exceeds r, and the whole-interval shortcut never decides a pair the
+// 12-part bound would keep (so di_cost_exceeds == di_cost_exceeds_parts).
+// Prints the rejection rates.  Exit code 1 on a violation.
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -24,7 +26,7 @@ int main(int argc, char** argv) {
   const double radii[] = {0.4, 1.0, 1.6, 2.4, 3.5};
   long bad = 0;
   for (double r : radii) {
-    long rejected = 0, kept = 0, near = 0;
+    long rejected = 0, kept = 0, near = 0, whole = 0;
     for (long i = 0; i < pairs; ++i) {
       double x0[6], x1[6];
       const double spread = (i % 3 == 0) ? 0.15 : 1.0;  // a third of the pairs close together
@@ -36,7 +38,14 @@ int main(int argc, char** argv) {
       }
       double t;
       const double c = di_cost_tau(x0, x1, P, &t);
-      const bool rej = di_cost_exceeds(di_coef(x0, x1, P), r);
+      const DiCoef cf = di_coef(x0, x1, P);
+      const bool rej = di_cost_exceeds(cf, r);
+      const bool w = di_cost_exceeds_whole(cf, r);
+      if (w) ++whole;
+      if (rej != di_cost_exceeds_parts(cf, r) || (w && !rej)) {
+        ++bad;
+        std::printf("VIOLATION (shortcut) r=%g\n", r);
+      }
       if (rej) ++rejected;
       if (c <= r) ++kept;
       if (c > r && c < r * 1.05) ++near;
@@ -45,8 +54,8 @@ int main(int argc, char** argv) {
         std::printf("VIOLATION r=%g c=%.17g\n", r, c);
       }
     }
-    std::printf("r=%.2f pairs=%ld kept=%ld rejected=%ld (%.1f%% of the non-kept) near=%ld\n", r, pairs, kept,
-                rejected, 100.0 * rejected / (pairs - kept > 0 ? pairs - kept : 1), near);
+    std::printf("r=%.2f pairs=%ld kept=%ld rejected=%ld (%.1f%% of the non-kept; %ld by the whole interval) near=%ld\n",
+                r, pairs, kept, rejected, 100.0 * rejected / (pairs - kept > 0 ? pairs - kept : 1), whole, near);
   }
   return bad ? 1 : 0;
 }
