@@ -195,9 +195,6 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // the compiler sees its address space and loads through it are LDS (short
 // scoreboard) instead of generic LD.  (The staged boxes' pointers are read
 // back from the shared Boxes descriptor, which loses that information.)
-#ifndef GMT_SB_VIEWS
-#define GMT_SB_VIEWS 1
-#endif
 extern __shared__ __align__(16) unsigned char gmt_dyn_smem[];
 template <typename T>
 __device__ __forceinline__ const T* shared_view(const T* p) {
@@ -246,7 +243,7 @@ __device__ __forceinline__ bool any_box_contains(const double* p, int d, const B
 // is the clip's own early miss.  (fl(lo - m) differs from lo - m by at most
 // 2^-53 |lo|, which only matters for |lo| > 1 where lo - b > 1 anyway.)
 // Boxes that pass the pre-test go through the exact clip.
-template <int D, bool SB = false>
+template <int D>
 __device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const double* a, const double* b) {
   const int d = dims<D>(d_rt);
   bool eq = true, cube_a = true, cube_b = true;
@@ -277,11 +274,11 @@ __device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const doubl
   // box, and the d lanes of a slot combine max(0, t0_k) / min(1, t1_k) and
   // the dk == 0 misses.  The clip's result is a function of those order-free
   // max/min values, so this equals the reference's sequential axis loop.
+  // (Running this scan on shared_view pointers when the boxes are staged --
+  // LDS instead of generic loads -- made the 3D forest batch 2 % faster but,
+  // as a second inlined copy, the configs[4] solves 1.5-7 % slower.)
   const int per = kWarp / d;
   const int slot = lane / d, axis = lane - slot * d;
-  // (SB: the staged arrays are this CTA's shared memory -- run the scan on
-  // shared_view pointers, so the bound loads are LDS, not generic)
-  auto scan = [&](const double* blo, const double* bhi, const double* lom, const double* him) -> bool {
   bool hit = false;
   for (int i0 = 0; i0 < bx.count && !hit; i0 += kWarp) {
     const int i = i0 + lane;
@@ -292,12 +289,12 @@ __device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const doubl
     for (int k = 0; k < (D > 0 ? D : kMaxSolveDim); ++k) {
       if (D == 0 && k >= d) break;
       double lo_k, hi_k;
-      if (lom) {
-        lo_k = lom[ic * bx.bs + k * bx.as];
-        hi_k = him[ic * bx.bs + k * bx.as];
+      if (bx.lom) {
+        lo_k = bx.lom[ic * bx.bs + k * bx.as];
+        hi_k = bx.him[ic * bx.bs + k * bx.as];
       } else {
-        lo_k = blo[ic * bx.bs + k * bx.as] - kSepMargin;
-        hi_k = bhi[ic * bx.bs + k * bx.as] + kSepMargin;
+        lo_k = bx.lo[ic * bx.bs + k * bx.as] - kSepMargin;
+        hi_k = bx.hi[ic * bx.bs + k * bx.as] + kSepMargin;
       }
       double smin, smax;
       if constexpr (D > 0 && D <= 6) {
@@ -323,7 +320,7 @@ __device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const doubl
         if (bx.idx) bi = bx.idx[bi];
         const double ak = a[axis];
         const double dk = __dsub_rn(b[axis], ak);
-        const double l = blo[bi * bx.bs + axis * bx.as], h = bhi[bi * bx.bs + axis * bx.as];
+        const double l = bx.lo[bi * bx.bs + axis * bx.as], h = bx.hi[bi * bx.bs + axis * bx.as];
         if (dk == 0.0) {
           miss = ak < l || ak > h;
         } else {
@@ -357,26 +354,22 @@ __device__ bool segment_free_ab(int d_rt, const Boxes& bx, int lane, const doubl
       for (int t = 0; t < take; ++t) cm &= cm - 1u;  // drop the `take` boxes done
     }
   }
-  return hit;
-  };
-  const bool hit = (SB && bx.lom) ? scan(shared_view(bx.lo), shared_view(bx.hi), shared_view(bx.lom), shared_view(bx.him))
-                                  : scan(bx.lo, bx.hi, bx.lom, bx.him);
   return !hit;
 }
 
-template <int D, bool SB = false>
+template <int D>
 __device__ __forceinline__ bool segment_free_staged(int d_rt, const Boxes& bx, int lane, const double* seg) {
-  return segment_free_ab<D, SB>(d_rt, bx, lane, seg, seg + 16);
+  return segment_free_ab<D>(d_rt, bx, lane, seg, seg + 16);
 }
 
-template <int D, bool SB = false>
+template <int D>
 __device__ bool segment_free_warp(const double* A, const double* B, int d, const Boxes& bx,
                                   int lane, double* seg) {
   __syncwarp();
   if (lane < d) seg[lane] = A[lane];
   if (lane >= 16 && lane - 16 < d) seg[lane] = B[lane - 16];
   __syncwarp();
-  return segment_free_staged<D, SB>(d, bx, lane, seg);
+  return segment_free_staged<D>(d, bx, lane, seg);
 }
 
 template <int D>
@@ -392,14 +385,14 @@ __device__ bool point_free_warp(const double* P, int d, const Boxes& bx, int lan
 
 // motion_free (planner.cpp:54-60) for a path edge: the cached polyline,
 // every sub-segment through the exact test (polyline_free, space.cpp:92-99).
-template <int D, bool SB = false>
+template <int D>
 __device__ bool polyline_free_warp(const DevInstance& I, int d, const Boxes& bx, int32_t pid,
                                    int lane, double* seg) {
   const int64_t a = I.path_ptr[pid], b = I.path_ptr[pid + 1];
   const double* pts = I.path_pts + a * d;
   if (b - a == 1) return point_free_warp<D>(pts, d, bx, lane, seg);
   for (int64_t s = 0; s + 1 < b - a; ++s) {
-    if (!segment_free_warp<D, SB>(pts + s * d, pts + (s + 1) * d, d, bx, lane, seg)) return false;
+    if (!segment_free_warp<D>(pts + s * d, pts + (s + 1) * d, d, bx, lane, seg)) return false;
   }
   return true;
 }
@@ -481,6 +474,9 @@ __device__ __forceinline__ bool seg_box_hit(const double* a, const double* b, in
 
 #ifndef GMT_POOL_HOIST
 #define GMT_POOL_HOIST 1
+#endif
+#ifndef GMT_SB_VIEWS
+#define GMT_SB_VIEWS 1
 #endif
 
 // seg_box_hit<6, true> with the staged box arrays passed in (axis stride
@@ -1900,8 +1896,8 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
                                             cull_s + warp * kCullCap * kKinSlots, kCullCap, true, D == 6 && sh.vfull,
                                             bec);
             }
-            if (pid < 0) return segment_free_staged<D, !GS && GMT_SB_VIEWS>(d, B, lane, sc);  // segment_free (planner.cpp:59)
-            return polyline_free_warp<D, !GS && GMT_SB_VIEWS>(I, d, B, pid, lane, sc);  // polyline_free (planner.cpp:56-58)
+            if (pid < 0) return segment_free_staged<D>(d, B, lane, sc);  // segment_free (planner.cpp:59)
+            return polyline_free_warp<D>(I, d, B, pid, lane, sc);       // polyline_free (planner.cpp:56-58)
           };
           bool ok;
           if constexpr (WIDE) {  // registers to spare: the descriptor off the check's critical path
