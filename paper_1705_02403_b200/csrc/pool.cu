@@ -152,33 +152,92 @@ __global__ void pool_points_kernel(int from, int to, uint64_t start, Primes pr, 
 
 // flags[q][p] = point_free(candidate p, boxes of q); the query's boxes are
 // staged in shared memory when they fit.
+// (boxes <= kFreeSortMax: staged in ascending lo_x with the widest x
+// extent w, so a point only tests the boxes whose lo_x lies in
+// [x - w', x] (w' = w rounded up: every box containing the point is among
+// them; Aabb::contains is exact and point_free's outcome does not depend on
+// the box order).  Each block covers kFreePts points of one query.)
+constexpr int kFreeSortMax = 256;
+constexpr int kFreePts = 2048;
 __global__ void __launch_bounds__(256) pool_free_kernel(const PQ* __restrict__ pq, const double* __restrict__ P,
                                                         int K, const double* __restrict__ box_lo,
                                                         const double* __restrict__ box_hi, int stage_cap,
                                                         uint8_t* __restrict__ flags) {
   extern __shared__ double bsm[];
+  __shared__ unsigned long long wbits;
   const int q = blockIdx.y;
   const PQ Q = pq[q];
   if (Q.skip) return;
   const double* lo = box_lo + Q.box_off * kD;
   const double* hi = box_hi + Q.box_off * kD;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  double x[kD];
-  if (p < K) {
+  const int nb = Q.nb;
+  const int p0 = blockIdx.x * kFreePts;
+  if (nb <= stage_cap && nb <= kFreeSortMax) {
+    if (threadIdx.x == 0) wbits = 0ull;
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+      const double x = lo[b * kD];
+      int r = 0;
+      for (int c = 0; c < nb; ++c) {
+        const double y = lo[c * kD];
+        r += (y < x || (y == x && c < b)) ? 1 : 0;
+      }
+      for (int k = 0; k < kD; ++k) {
+        bsm[r * kD + k] = lo[b * kD + k];
+        bsm[(nb + r) * kD + k] = hi[b * kD + k];
+      }
+      const double w = hi[b * kD] - x;
+      if (w > 0.0) atomicMax(&wbits, static_cast<unsigned long long>(__double_as_longlong(w)));
+    }
+    __syncthreads();
+    const double* slo = bsm;
+    const double* shi = bsm + nb * kD;
+    const double wx = __longlong_as_double(static_cast<long long>(wbits)) * (1.0 + 1e-12) + 1e-12;
+    for (int p = p0 + threadIdx.x; p < K && p < p0 + kFreePts; p += blockDim.x) {
+      double x[kD];
 #pragma unroll
-    for (int k = 0; k < kD; ++k) x[k] = __ldg(P + static_cast<int64_t>(p) * kD + k);
+      for (int k = 0; k < kD; ++k) x[k] = __ldg(P + static_cast<int64_t>(p) * kD + k);
+      bool free = point_in_cube(x, kD);
+      if (free) {
+        // first box with lo_x >= x - wx (binary search), then every box up
+        // to lo_x > x
+        const double t = x[0] - wx;
+        int l = 0, h = nb;
+        while (l < h) {
+          const int m = (l + h) >> 1;
+          if (slo[m * kD] < t) l = m + 1; else h = m;
+        }
+        for (int b = l; b < nb && !(slo[b * kD] > x[0]); ++b)
+          if (box_contains(slo + b * kD, shi + b * kD, kD, x)) {
+            free = false;
+            break;
+          }
+      }
+      flags[static_cast<int64_t>(q) * K + p] = free ? 1 : 0;
+    }
+    return;
   }
-  if (Q.nb <= stage_cap) {
-    for (int i = threadIdx.x; i < Q.nb * kD; i += blockDim.x) {
+  if (nb <= stage_cap) {
+    for (int i = threadIdx.x; i < nb * kD; i += blockDim.x) {
       bsm[i] = lo[i];
-      bsm[Q.nb * kD + i] = hi[i];
+      bsm[nb * kD + i] = hi[i];
     }
     __syncthreads();
     // (the staged copy named directly: shared-space loads, not generic)
-    if (p < K) flags[static_cast<int64_t>(q) * K + p] = free_pt(x, bsm, bsm + Q.nb * kD, Q.nb) ? 1 : 0;
+    for (int p = p0 + threadIdx.x; p < K && p < p0 + kFreePts; p += blockDim.x) {
+      double x[kD];
+#pragma unroll
+      for (int k = 0; k < kD; ++k) x[k] = __ldg(P + static_cast<int64_t>(p) * kD + k);
+      flags[static_cast<int64_t>(q) * K + p] = free_pt(x, bsm, bsm + nb * kD, nb) ? 1 : 0;
+    }
     return;
   }
-  if (p < K) flags[static_cast<int64_t>(q) * K + p] = free_pt(x, lo, hi, Q.nb) ? 1 : 0;
+  for (int p = p0 + threadIdx.x; p < K && p < p0 + kFreePts; p += blockDim.x) {
+    double x[kD];
+#pragma unroll
+    for (int k = 0; k < kD; ++k) x[k] = __ldg(P + static_cast<int64_t>(p) * kD + k);
+    flags[static_cast<int64_t>(q) * K + p] = free_pt(x, lo, hi, nb) ? 1 : 0;
+  }
 }
 
 // The first n free candidates in stream order are the query's samples
@@ -1107,7 +1166,8 @@ int pool_derive(gmt_ctx* ctx, const gmt_problem* problems, int count, Arena& met
         GMT_CUDA(cudaFuncSetAttribute(pool_free_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(fsm)));
       timer.mark();
-      pool_free_kernel<<<dim3((Kc + 255) / 256, count), 256, fsm, s>>>(d_pq, P, Kc, d_blo, d_bhi, nb_st, d_flag);
+      pool_free_kernel<<<dim3((Kc + kFreePts - 1) / kFreePts, count), 256, fsm, s>>>(d_pq, P, Kc, d_blo, d_bhi, nb_st,
+                                                                                    d_flag);
       timer.mark();
       pool_select_kernel<<<count, 1024, 0, s>>>(d_pq, P, Kc, d_flag, d_glo, d_ghi, d_rank, d_sel, d_qc, d_po);
       GMT_CUDA(cudaGetLastError());
