@@ -413,7 +413,7 @@ def run_b200(args):
     line = None
     if rank == 0:
         cpu, parity = None, None
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:  # (the CPU baseline: rank 0 at N = 1 only)
             try:
                 import oracle
                 if oracle.ref_available():
