@@ -1019,6 +1019,9 @@ __device__ __forceinline__ void block_argmin(double& c, int32_t& v, CtaShared& s
 // Two CTA shapes: WIDE = 512 threads with up to 128 registers (clusters,
 // and single-CTA queries that want the registers), narrow = 256 threads,
 // 64 registers, four CTAs per SM.
+#ifndef GMT_ROWS_CS
+#define GMT_ROWS_CS 1
+#endif
 #ifndef GMT_DI_XAHEAD
 #define GMT_DI_XAHEAD 1
 #endif
@@ -1068,6 +1071,7 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
   // the batched 24-warp DI shape's candidates (GMT_DI_DYNAMIC bit 1: P4 rows,
   // bit 2: P5 candidates), whose lazy checks vary widely in cost.
   constexpr bool kDi24 = CS == 1 && D == 6 && NW == 24;
+  constexpr bool kRowsCs = kDi24 && GMT_ROWS_CS && !POOL;  // streaming loads of materialised rows (not compiled into the view kernel: it perturbed that one by 12 %)
   constexpr bool kDynOwn = CS > 1 || (kDi24 && (GMT_DI_DYNAMIC & 1));
   constexpr bool kDynamic = CS > 1 || (kDi24 && (GMT_DI_DYNAMIC & 2));
   // Per-warp scratch: kRows staged segments, kinodynamic waypoint tables
@@ -1505,7 +1509,9 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
           int xs[kUnroll];
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u)
-            xs[u] = off + u * kLanesPerRow < lim ? __ldg(ocol + off + u * kLanesPerRow) : -1;
+            xs[u] = off + u * kLanesPerRow < lim
+                        ? ((kRowsCs && !viewed) ? __ldcs(ocol + off + u * kLanesPerRow) : __ldg(ocol + off + u * kLanesPerRow))
+                        : -1;
           if (mapped) {
 #if GMT_POOL_HOIST
 #pragma unroll
@@ -1704,11 +1710,22 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
         for (int off = 0; off < lmax; off += kLanesPerRow * kUnroll) {
           int ys[kUnroll];
           double cs[kUnroll];
+          if (kRowsCs && !viewed) {
+            // (materialised rows are read once per launch: evict-first in
+            // L2, so the pool check records and row offsets stay resident)
 #pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
-            const bool in = off + u * kLanesPerRow < lim;
-            ys[u] = in ? __ldg(rcol + off + u * kLanesPerRow) : -1;
-            cs[u] = in ? __ldg(rcost + off + u * kLanesPerRow) : 0.0;
+            for (int u = 0; u < kUnroll; ++u) {
+              const bool in = off + u * kLanesPerRow < lim;
+              ys[u] = in ? __ldcs(rcol + off + u * kLanesPerRow) : -1;
+              cs[u] = in ? __ldcs(rcost + off + u * kLanesPerRow) : 0.0;
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+              const bool in = off + u * kLanesPerRow < lim;
+              ys[u] = in ? __ldg(rcol + off + u * kLanesPerRow) : -1;
+              cs[u] = in ? __ldg(rcost + off + u * kLanesPerRow) : 0.0;
+            }
           }
           if (mapped) {
 #if GMT_POOL_HOIST
