@@ -1666,7 +1666,8 @@ __global__ void __launch_bounds__(NW ? NW * 32 : (WIDE ? 512 : 256),
           nlen = static_cast<int>(__ldg(I.in_end + xn) - n0);
           if constexpr (D == 6 && kRows >= 2) {
             // (DI: a lazy check outlasts a row fetch -- the next rows are
-            // pulled into L2 by the TMA engine meanwhile)
+            // pulled into L2 by the TMA engine meanwhile; an evict-first
+            // cache policy on these prefetches measured 20.79 -> 20.84 ms)
             // (not in_tau: one duration per row is read, after the argmin)
             if (hl == 0 && I.in_tau && nlen > 0) {
               prefetch_l2(I.in_col + n0, sizeof(int32_t) * nlen);
