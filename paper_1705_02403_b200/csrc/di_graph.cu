@@ -61,6 +61,14 @@ struct DiModel {
   double bound;  // di_prefilter_bound
   double radius;
   __device__ bool may(const double* a, const double* b) const { return di_may_connect(a, b, bound, P, radius); }
+  // may == may_quick && may_confirm (di_cost_exceeds = whole || parts):
+  // the cheap part first, the 12-part bound only for the pairs it passes
+  __device__ bool may_quick(const double* a, const double* b) const {
+    return di_may_connect(a, b, bound) && !di_cost_exceeds_whole(di_coef(a, b, P), radius);
+  }
+  __device__ bool may_confirm(const double* a, const double* b) const {
+    return !di_cost_exceeds_parts(di_coef(a, b, P), radius);
+  }
   __device__ double cost_tau(const double* a, const double* b, double* t) const {
     return di_cost_tau(a, b, P, t);
   }
@@ -78,6 +86,8 @@ struct QuadModel {
   QuadParams P;
   double radius;
   __device__ bool may(const double* a, const double* b) const { return quad_may_connect(a, b, P, radius); }
+  __device__ bool may_quick(const double* a, const double* b) const { return may(a, b); }
+  __device__ bool may_confirm(const double*, const double*) const { return true; }
   __device__ double cost_tau(const double* a, const double* b, double* t) const {
     return quad_cost_tau(a, b, P, t);
   }
@@ -135,6 +145,8 @@ struct DubinsModel {
     return cost_tau(a, b, t);
   }
   __device__ double coord(const double*, const double*, double, int, int) const { return 0.0; }
+  __device__ bool may_quick(const double* a, const double* b) const { return may(a, b); }
+  __device__ bool may_confirm(const double*, const double*) const { return true; }
   int segments() const { return 0; }
 };
 
@@ -398,29 +410,60 @@ __global__ void __launch_bounds__(256) kino_eval_kernel(const double* __restrict
                                                         uint32_t* __restrict__ bits, int W,
                                                         int64_t* __restrict__ out_counts,
                                                         int64_t* __restrict__ in_counts) {
+  // The few columns that pass the cheap prefilter (may_quick) are queued
+  // per warp and run through the rest of the test and the capped 2BVP
+  // search 32 at a time, so no 32-column chunk waits on one lane's search.
+  // Same keep bits and counts as testing every pair in place.
   constexpr int kD = Model::kDim;
+  __shared__ int32_t queue_s[8][64];
   const int lane = threadIdx.x & 31;
+  int32_t* const queue = queue_s[(threadIdx.x >> 5) & 7];
   const int warps = (blockDim.x >> 5) * gridDim.x;
   for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
     double xr[kD];
     for (int k = 0; k < kD; ++k) xr[k] = __ldg(coords + static_cast<int64_t>(r) * kD + k);
+    uint32_t* const brow = bits + static_cast<int64_t>(r) * W;
     int64_t cnt = 0;
-    for (int w = 0; w < W; ++w) {
-      const int c = w * 32 + lane;
+    int qn = 0;
+    auto drain = [&](int take) {  // evaluate queue[0, take), keep the rest
       bool keep = false;
-      if (c < n && c != r) {
+      int c = 0;
+      if (lane < take) {
+        c = queue[lane];
         double xc[kD];
         for (int k = 0; k < kD; ++k) xc[k] = __ldg(coords + static_cast<int64_t>(c) * kD + k);
-        if (model.may(xr, xc)) {
+        if (model.may_confirm(xr, xc)) {
           double tc;
           keep = model.cost_within(xr, xc, radius, &tc) <= radius;
         }
       }
-      const uint32_t m = __ballot_sync(kFull, keep);
-      if (lane == 0) bits[static_cast<int64_t>(r) * W + w] = m;
-      if (keep) atomicAdd(reinterpret_cast<unsigned long long*>(in_counts + c), 1ull);
-      cnt += __popc(m);
+      if (keep) {
+        atomicOr(brow + (c >> 5), 1u << (c & 31));
+        atomicAdd(reinterpret_cast<unsigned long long*>(in_counts + c), 1ull);
+      }
+      cnt += __popc(__ballot_sync(kFull, keep));
+      const int rest = lane + take < qn ? queue[lane + take] : 0;
+      __syncwarp();
+      if (lane + take < qn) queue[lane] = rest;
+      qn -= take;
+      __syncwarp();
+    };
+    for (int w = 0; w < W; ++w) {
+      const int c = w * 32 + lane;
+      bool may = false;
+      if (c < n && c != r) {
+        double xc[kD];
+        for (int k = 0; k < kD; ++k) xc[k] = __ldg(coords + static_cast<int64_t>(c) * kD + k);
+        may = model.may_quick(xr, xc);
+      }
+      if (lane == 0) brow[w] = 0u;  // (before any atomicOr into this word: queued columns are >= 32 w)
+      const uint32_t m = __ballot_sync(kFull, may);
+      if (may) queue[qn + __popc(m & ((1u << lane) - 1u))] = c;
+      qn += __popc(m);
+      __syncwarp();
+      if (qn >= 32) drain(32);
     }
+    while (qn > 0) drain(qn < 32 ? qn : 32);
     if (lane == 0) out_counts[r] = cnt;
   }
 }
@@ -435,29 +478,45 @@ __global__ void __launch_bounds__(256) kino_out_fill_kernel(const double* __rest
                                                             int32_t* __restrict__ col,
                                                             double* __restrict__ cost,
                                                             double* __restrict__ tau) {
+  // The row's kept columns are queued in order and solved 32 at a time
+  // (lane i -> slot out + i), not one word's few set bits per warp step.
   constexpr int kD = Model::kDim;
+  __shared__ int32_t queue_s[8][64];
   const int lane = threadIdx.x & 31;
+  int32_t* const queue = queue_s[(threadIdx.x >> 5) & 7];
   const int warps = (blockDim.x >> 5) * gridDim.x;
   for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
     double xr[kD];
     for (int k = 0; k < kD; ++k) xr[k] = __ldg(coords + static_cast<int64_t>(r) * kD + k);
     int64_t out = row_ptr[r];
-    for (int w = 0; w < W; ++w) {
-      const uint32_t m = __ldg(bits + static_cast<int64_t>(r) * W + w);
-      if (!m) continue;
-      if ((m >> lane) & 1u) {
-        const int c = w * 32 + lane;
+    int qn = 0;
+    auto drain = [&](int take) {
+      if (lane < take) {
+        const int c = queue[lane];
         double xc[kD];
         for (int k = 0; k < kD; ++k) xc[k] = __ldg(coords + static_cast<int64_t>(c) * kD + k);
         double tc;
         const double cc = model.cost_within(xr, xc, radius, &tc);
-        const int64_t slot = out + __popc(m & ((1u << lane) - 1u));
-        col[slot] = c;
-        cost[slot] = cc;
-        tau[slot] = tc;
+        col[out + lane] = c;
+        cost[out + lane] = cc;
+        tau[out + lane] = tc;
       }
-      out += __popc(m);
+      const int rest = lane + take < qn ? queue[lane + take] : 0;
+      __syncwarp();
+      if (lane + take < qn) queue[lane] = rest;
+      out += take;
+      qn -= take;
+      __syncwarp();
+    };
+    for (int w = 0; w < W; ++w) {
+      const uint32_t m = __ldg(bits + static_cast<int64_t>(r) * W + w);
+      if (!m) continue;
+      if ((m >> lane) & 1u) queue[qn + __popc(m & ((1u << lane) - 1u))] = w * 32 + lane;
+      qn += __popc(m);
+      __syncwarp();
+      if (qn >= 32) drain(32);
     }
+    while (qn > 0) drain(qn < 32 ? qn : 32);
   }
 }
 
