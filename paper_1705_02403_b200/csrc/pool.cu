@@ -332,13 +332,21 @@ __global__ void __launch_bounds__(256) pool_subst_kernel(const PQ* __restrict__ 
       dup = 0;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < kSubstSearch; i += blockDim.x) {
-      if (i <= last) continue;
-      double c[kD];
-      candidate(i, c);
-      if (free_pt(c, lo, hi, Q.nb)) atomicMin(&best, i);
+    // the smallest free candidate index above `last`: ascending chunks of
+    // blockDim, stopping at the first chunk that holds one (usually the
+    // goal's centre, i = 0)
+    for (int base = last + 1; base < kSubstSearch; base += blockDim.x) {
+      const int i = base + static_cast<int>(threadIdx.x);
+      if (i < kSubstSearch) {
+        double c[kD];
+        candidate(i, c);
+        if (free_pt(c, lo, hi, Q.nb)) atomicMin(&best, i);
+      }
+      __syncthreads();
+      const bool done = best != 0x7fffffff;
+      __syncthreads();  // (every thread has read best before the next chunk's atomicMin)
+      if (done) break;
     }
-    __syncthreads();
     const int b = best;
     if (b == 0x7fffffff) break;
     double c[kD];
